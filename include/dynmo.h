@@ -1,0 +1,299 @@
+/*
+ * dynmo.h -- C-ABI of the B200-native DynMo per-step rebalancing hot path.
+ *
+ * DynMo (arXiv 2505.14864) rebalances a pipeline-parallel model whose
+ * per-layer work changes during training.  Each step:
+ *   1 dynmo_profile_layers   per-layer counters -> int64 cost c_i, all-gather
+ *   2 dynmo_partition_stages contiguous layers->stages min-max partition
+ *   3 dynmo_diffuse_balance  the paper's decentralised diffusion variant
+ *   4 dynmo_repack_workers   fewest workers within a throughput bound
+ *   5 dynmo_migrate_layers   move the layers whose GPU changed (NCCL P2P)
+ * Citations: P:Lnnn = PAPER.md line (SPEC:Lnnn = SPEC.md line); readings of
+ * ambiguous passages (Q1..Q20) are listed in DESIGN.md.
+ *
+ * Conventions
+ *  - Pointers prefixed d_ are DEVICE pointers, h_ are HOST pointers.  The
+ *    library never takes ownership of caller memory and never frees it.
+ *  - Calls 1-4 are asynchronous on the given cudaStream_t and never
+ *    synchronise the host; data-dependent errors are written to device
+ *    status words (int32).  Call 5 needs host boundaries (the caller copies
+ *    the <= 40 B boundary vector D2H first) and is also stream-ordered.
+ *  - Return value: host-checkable status (argument validation, CUDA/NCCL
+ *    launch errors).  0 OK, < 0 error, > 0 warning.
+ *  - int32 layer/stage indices, int64 costs and bytes.  All results are
+ *    deterministic; integer results are bit-exact with the CPU oracle.
+ *  - Thread safety: a ctx may be used from one host thread at a time.
+ */
+#ifndef DYNMO_H
+#define DYNMO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dynmo_status;
+#define DYNMO_OK 0
+#define DYNMO_E_INVALID (-1)     /* bad argument / malformed instance       */
+#define DYNMO_E_INFEASIBLE (-2)  /* no split satisfies the memory cap       */
+#define DYNMO_E_OVERFLOW (-3)    /* an int64 cost, sum or phi overflowed     */
+#define DYNMO_E_CUDA (-4)        /* CUDA runtime error (see strerror/last)   */
+#define DYNMO_E_NCCL (-5)        /* NCCL error (see dynmo_last_error)        */
+#define DYNMO_E_NOMEM (-6)       /* device allocation failed (plan create)   */
+#define DYNMO_W_NOT_CONVERGED 1  /* diffusion stopped at max_rounds          */
+#define DYNMO_W_BOUND_UNMET 2    /* repack could not meet bound / target     */
+
+typedef void *dynmo_stream; /* a cudaStream_t; NULL = legacy default stream */
+typedef struct dynmo_ctx_s *dynmo_ctx;
+typedef struct dynmo_plan_s *dynmo_plan;
+
+const char *dynmo_strerror(dynmo_status s);
+/* Last host-side error message of this thread (CUDA/NCCL string), or "". */
+const char *dynmo_last_error(void);
+/* Library version string. */
+const char *dynmo_version(void);
+
+/* ------------------------------------------------------------------ ctx --
+ * One process per GPU ("one MPI rank per GPU"; here torch.distributed
+ * ranks).  nranks == 1: no NCCL communicator is created.  nranks > 1: every
+ * rank passes the same 128-byte id obtained on rank 0 from
+ * dynmo_get_unique_id() and broadcast by the caller (e.g. through the torch
+ * process group); the ctx owns the resulting ncclComm_t.  device is the CUDA
+ * ordinal this rank drives.  ctx_create is collective over the nranks ranks. */
+dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]);
+dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
+                              const uint8_t *h_nccl_id /* 128 B, or NULL if nranks==1 */,
+                              dynmo_ctx *out);
+void dynmo_ctx_destroy(dynmo_ctx ctx);
+int32_t dynmo_ctx_nranks(dynmo_ctx ctx);
+int32_t dynmo_ctx_rank(dynmo_ctx ctx);
+
+/* ----------------------------------------------------------- profiling --
+ * Sources of per-layer workload (P:L234-239 pruning p_i, P:L266-283 freezing
+ * f_i, P:L340-353 early exit t_i, P:L376-389 MoD r_i t_i, P:L209-214 MoE
+ * tokens per expert).  A segment is a caller-owned device array that
+ * contributes to ONE layer (or, for EXIT_U8, to every local layer).  All
+ * contributions to a layer are summed, so one layer may have several
+ * segments (e.g. its four weight tensors). */
+enum {
+    DYNMO_SRC_MASK_BITS = 0,   /* uint32 words, 1 bit/param, little-endian bit
+                                  order (bit b = word b/32, bit b%32); counts
+                                  set bits among the first n_elem  -> nnz_i */
+    DYNMO_SRC_MASK_U8 = 1,     /* bool/uint8 mask, n_elem bytes; != 0 -> nnz_i */
+    DYNMO_SRC_NZ_BF16 = 2,     /* bf16 weights; (bits & 0x7FFF) != 0 -> nnz_i
+                                  (+0 and -0 are pruned, NaN counts)         */
+    DYNMO_SRC_NZ_F32 = 3,      /* f32 weights; (bits & 0x7FFFFFFF) != 0      */
+    DYNMO_SRC_TOKMASK_BITS = 4,/* per-layer token bitmask (MoD routing or an
+                                  early-exit alive mask), n_elem bits -> tok_i */
+    DYNMO_SRC_EXIT_U8 = 5,     /* per-token exit depth e[t] (token processed by
+                                  layers 0..e[t]-1), n_elem tokens; adds
+                                  #{t : e[t] > i} to tok_i of EVERY local layer
+                                  i (layer field ignored)                     */
+    DYNMO_SRC_EXPERT_I64 = 6,  /* int64 top-k expert ids [T*k] of a MoE layer;
+                                  histogram over [0, n_experts)               */
+    DYNMO_SRC_EXPERT_I32 = 7   /* int32 variant                              */
+};
+
+typedef struct dynmo_segment {
+    const void *d_ptr;   /* device pointer; alignment of its element type   */
+    int64_t n_elem;      /* bits (MASK_BITS, TOKMASK_BITS), else elements   */
+    int32_t layer;       /* global layer index in [layer_begin, +n_local)   */
+    int32_t src_kind;    /* DYNMO_SRC_*                                     */
+    int32_t n_experts;   /* EXPERT_*: E in [1, 1024]; all segments of one
+                            layer must agree.  Ignored otherwise.            */
+    int32_t top_k;       /* EXPERT_*: informational (n_elem = T*k)          */
+} dynmo_segment;
+
+/* Per-local-layer cost coefficients (readings Q1-Q6):
+ *   c_i = frozen_i ? F : tok_i * (A + B * nnz_i) + C * moe_i
+ *   moe_i = EP * max_{r<EP} sum_{e in group r} cnt_{i,e}
+ * groups = EP contiguous blocks of E/EP experts (EP <= 0 means EP = E;
+ * E % EP != 0 is INVALID).  Absent sources default to tok_i = 1, nnz_i = 0,
+ * moe_i = 0.  Checked int64 arithmetic (128-bit intermediates): a result
+ * above INT64_MAX is OVERFLOW; a negative coefficient is INVALID. */
+typedef struct dynmo_cost_coef {
+    int64_t A, B, C, F;
+    int32_t ep_ranks;
+    int32_t pad;
+} dynmo_cost_coef;
+
+/* Build the launch plan for this rank's segments (off the hot path; plain
+ * host work + two small device allocations owned by the plan).  The plan
+ * stores the segment pointers: they must stay valid while the plan is used;
+ * rebuild after migration or re-allocation.
+ *   layer_begin, n_local: the contiguous global layers this rank profiles.
+ *   n_total: length of the global cost vector.
+ *   exchange: 1 -> profile_layers all-gathers every rank's slice over the
+ *     ctx's NCCL communicator so each rank ends with the global vector
+ *     (requires nranks > 1; slices must tile [0, n_total) exactly, else the
+ *     device status is INVALID); 0 -> local only: n_total == n_local and
+ *     outputs are indexed by local layer.
+ * Errors (returned): INVALID for a null/negative argument, a layer outside
+ * the local range, an unknown src_kind, n_experts outside [1, 1024] or
+ * inconsistent within a layer, a misaligned pointer; NOMEM; CUDA. */
+dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_segs, int32_t n_segs,
+                                       int32_t layer_begin, int32_t n_local, int32_t n_total,
+                                       int32_t exchange, dynmo_plan *out);
+void dynmo_profile_plan_destroy(dynmo_plan plan);
+/* Number of work tiles the fused profiling kernel walks (diagnostics). */
+int64_t dynmo_plan_num_tiles(dynmo_plan plan);
+/* Algorithmic bytes read by one profile launch (sum of segment bytes). */
+int64_t dynmo_plan_bytes(dynmo_plan plan);
+/* Max experts over segments (0 if no MoE source). */
+int32_t dynmo_plan_max_experts(dynmo_plan plan);
+
+/* Call 1 -- profile_layers.  One fused streaming kernel over every segment
+ * (128-bit loads, warp-shuffle reductions), the cost epilogue, and (if the
+ * plan exchanges) an ncclAllGather of fixed-size per-rank slots over NVLink
+ * followed by an unpack kernel.
+ *   d_frozen   [n_local] uint8, nullable (no layer frozen)
+ *   d_coef     [n_local] dynmo_cost_coef, required
+ *   d_mem_local[n_local] int64 caller memory per layer, nullable
+ *   d_counters [n_local][4] int64 out, nullable: {nnz_i, tok_i, moe_i, c_i}
+ *              with the defaults applied (tok_i = 1 without a token source)
+ *   d_hist     [n_local][max_experts] int64 out, nullable: cnt_{i,e}
+ *   d_cost     [n_total] int64 out: global (exchange) or local cost vector
+ *   d_mem      [n_total] int64 out, nullable: gathered d_mem_local (zeros if
+ *              d_mem_local is NULL)
+ *   d_status   [1] int32 out: OK, INVALID (expert id outside [0,E), bad
+ *              coefficient, slices do not tile), OVERFLOW; the most negative
+ *              code wins.  Layers with an error get c_i = -1.
+ * Collective when the plan exchanges: every rank must call it. */
+dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t *d_frozen,
+                                  const dynmo_cost_coef *d_coef, const int64_t *d_mem_local,
+                                  int64_t *d_counters, int64_t *d_hist, int64_t *d_cost,
+                                  int64_t *d_mem, int32_t *d_status, dynmo_stream stream);
+
+/* -------------------------------------------------------------- solvers --
+ * Batched instance layout shared by calls 2-4 (one CTA per instance):
+ *   instance q owns layers [d_layer_off[q], d_layer_off[q+1]) of d_cost /
+ *   d_mem; L_q = d_layer_off[q+1] - d_layer_off[q] in [1, max_layers].
+ *   Its boundary vector b[0..n_q] (b_0 = 0, b_n = L_q, strictly increasing,
+ *   stage s = layers [b_s, b_{s+1})) is stored at d_bnd + d_bnd_off[q];
+ *   the caller sizes d_bnd_off[q+1] - d_bnd_off[q] >= n_q + 1.
+ *   d_mem nullable (no memory constraint; d_cap ignored); else d_cap[q] is
+ *   the inclusive per-stage memory cap (Alg. 2's strict "< MAX_MEM" is
+ *   cap = MAX_MEM - 1, reading Q9).
+ *   max_layers: host upper bound on every L_q, <= DYNMO_MAX_LAYERS (it picks
+ *   the kernel variant; an instance with L_q > max_layers gets INVALID).
+ * Per-instance device status d_status[q]; on an error the instance's outputs
+ * are b = -1, bottleneck = -1 (imbalance = -1.0). */
+#define DYNMO_MAX_LAYERS 1023
+
+/* Call 2 -- partition_stages ("minimize the maximum load among
+ * all workers"; P:L496, P:L720 centralised Partition, "binary search and
+ * linear probing").  B* = min over contiguous n-splits with every stage
+ * mem <= cap of the max stage cost; exact integer multi-section search over
+ * B with a warp-parallel greedy feasibility test.  Output boundaries are the
+ * lexicographically largest optimal split (reading Q7); d_imbalance (nullable)
+ * is Delta L = (L_max - L_min) / ((1/n) sum L) in fp64 (eq:imbalance,
+ * P:L193; 0 when sum is 0).  Status INVALID (n < 1, n > L, negative cost or
+ * mem), INFEASIBLE (no split meets cap), OVERFLOW (sum of costs > INT64_MAX). */
+dynmo_status dynmo_partition_stages(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                    const int64_t *d_cost, const int64_t *d_mem,
+                                    const int32_t *d_layer_off, const int32_t *d_n_stages,
+                                    const int64_t *d_cap, const int32_t *d_bnd_off,
+                                    int32_t *d_bnd, int64_t *d_bottleneck, double *d_imbalance,
+                                    int32_t *d_status, dynmo_stream stream);
+
+/* Call 3 -- diffuse_balance (P:L497 decentralised diffusion; P:L518-549
+ * Lemma 2: potential phi = sum_{u<v} |x_u - x_v|, max-neighbor pairing,
+ * "largest reductions in imbalance while satisfying memory constraints").
+ * Discrete rounds (reading Q10): every adjacent stage pair computes its best
+ * re-split j (min of (pair max, |j - b|, j) over mem-feasible j); a pair is
+ * improvable iff that lowers the pair max; each stage picks its improvable
+ * incident pair with the largest load gap (ties: lower index); mutually
+ * picked pairs apply their re-split.  Stops with OK when phi <= gamma[q] or
+ * no pair is improvable, with NOT_CONVERGED at max_rounds.  The fluid process
+ * of the proof (pairs average real loads) runs alongside from the same
+ * start: x in fp64, stop at phi_f <= gamma_f[q] (NOT_CONVERGED at max_rounds).
+ *   d_bnd_in / d_bnd_out use the d_bnd_off layout with n_q = d_n_stages[q].
+ *   d_gamma nullable (0), d_gamma_fluid nullable (0.0).
+ *   Outputs: d_rounds[q], d_phi[q] (final), d_phi0[q] (initial) nullable,
+ *   d_fluid_x (nullable) at offset d_bnd_off[q] - q (n_q doubles),
+ *   d_fluid_rounds[q] nullable, d_fluid_phi[q] nullable.
+ *   d_status[q] = worst of the discrete and fluid statuses (errors < 0 win,
+ *   then NOT_CONVERGED).  b_in must be a valid split (else INVALID); a b_in
+ *   that violates the cap is accepted and moves never exceed it. */
+dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                   const int64_t *d_cost, const int64_t *d_mem,
+                                   const int32_t *d_layer_off, const int32_t *d_n_stages,
+                                   const int64_t *d_cap, const int32_t *d_bnd_off,
+                                   const int32_t *d_bnd_in, const int64_t *d_gamma,
+                                   const double *d_gamma_fluid, int32_t max_rounds,
+                                   int32_t *d_bnd_out, int32_t *d_rounds, int64_t *d_phi,
+                                   int64_t *d_phi0, double *d_fluid_x, int32_t *d_fluid_rounds,
+                                   double *d_fluid_phi, int32_t *d_status, dynmo_stream stream);
+
+/* Call 4 -- repack_workers (P:L556-609 re-packing; "without
+ * sacrificing training throughput"; readings Q14-Q16).
+ *   mode BOUND: n' = the fewest workers k in [floor, n_cur] such that some
+ *     contiguous k-split has every stage cost <= bound[q] and mem <= cap;
+ *     boundaries = partition_stages at n' (workers 0..n'-1 stay active, in
+ *     pipeline order).  If even n_cur cannot meet the bound: BOUND_UNMET,
+ *     n' = n_cur with its optimal split.
+ *   mode ALG2: Alg. 2 first-fit merges of adjacent active
+ *     workers of the current split d_bnd_in, src ascending, if
+ *     mem[src] + mem[dst] <= cap and #active > floor (the target); fixes of
+ *     SPEC:L389 (skip and zero a deactivated src).  BOUND_UNMET if the
+ *     target is not reached.  d_bound ignored.
+ *   d_n_cur[q] plays the role of n_q for the layouts (d_bnd_off capacity
+ *   n_cur + 1; d_bnd_in only read in ALG2 mode, nullable otherwise).
+ *   Outputs d_n_new[q], d_bnd (n'+1 entries, the rest of the capacity -1),
+ *   d_bottleneck[q] = max stage cost of the output split.
+ *   INVALID if floor < 1, floor > n_cur, n_cur > L or bound < 0. */
+#define DYNMO_REPACK_BOUND 0
+#define DYNMO_REPACK_ALG2 1
+dynmo_status dynmo_repack_workers(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                  const int64_t *d_cost, const int64_t *d_mem,
+                                  const int32_t *d_layer_off, const int32_t *d_n_cur,
+                                  const int64_t *d_cap, const int32_t *d_bnd_off,
+                                  const int32_t *d_bnd_in, const int64_t *d_bound,
+                                  const int32_t *d_floor, int32_t mode, int32_t *d_n_new,
+                                  int32_t *d_bnd, int64_t *d_bottleneck, int32_t *d_status,
+                                  dynmo_stream stream);
+
+/* ------------------------------------------------------------ migration --
+ * Call 5 -- migrate_layers ("When a layer is migrated from GPU A to
+ * GPU B, the memory allocated for the layer ... is released on GPU A and
+ * allocated on GPU B"; payload at a step boundary = parameters + optimizer
+ * state, reading Q19).  COLLECTIVE: every rank calls it with identical
+ * boundary and rank arrays.  Layer i lives on rank h_rank_old[stage_old(i)]
+ * before and h_rank_new[stage_new(i)] after; every layer whose rank changes
+ * is moved with ncclSend/ncclRecv of each of its n_bufs buffers inside one
+ * NCCL group on `stream` (NVLink / NVSwitch peer transfers).
+ *   h_send[i*n_bufs + k]: on the OLD owner, the k-th buffer of layer i
+ *   (pointer + bytes); h_recv[i*n_bufs + k]: on the NEW owner, a caller-
+ *   allocated buffer of the same byte size.  Entries for layers this rank
+ *   neither sends nor receives are ignored (may be {NULL, 0}).  A needed
+ *   entry that is NULL with bytes > 0 -> INVALID before any transfer.
+ *   Sizes must agree between sender and receiver (caller metadata).
+ *   The caller frees send buffers after the stream has completed.
+ *   h_bytes_sent / h_bytes_recv (nullable): bytes this rank sends/receives.
+ * With nranks == 1 every rank entry must be 0 and nothing is transferred. */
+typedef struct dynmo_buf {
+    void *d_ptr;
+    int64_t bytes;
+} dynmo_buf;
+
+dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old,
+                                  const int32_t *h_bnd_old, const int32_t *h_rank_old,
+                                  int32_t n_new, const int32_t *h_bnd_new,
+                                  const int32_t *h_rank_new, const dynmo_buf *h_send,
+                                  const dynmo_buf *h_recv, int32_t n_bufs, int64_t *h_bytes_sent,
+                                  int64_t *h_bytes_recv, dynmo_stream stream);
+
+/* Host-only helper (no GPU, no ctx): the migration plan call 5 executes.
+ * Writes moves (layer, src_rank, dst_rank), layer ascending, for every layer
+ * whose owning rank changes, into h_moves[n_layers][3]; returns the number of
+ * moves, or DYNMO_E_INVALID (< 0) if a boundary vector is malformed. */
+int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_bnd_old,
+                             const int32_t *h_rank_old, int32_t n_new, const int32_t *h_bnd_new,
+                             const int32_t *h_rank_new, int32_t *h_moves);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNMO_H */

@@ -223,11 +223,15 @@ double oracle_phi_f64(const double *x, int32_t n) {
  * chosen greedily left to right with g.
  * On error: bnd[] = -1, *bottleneck = -1, *imbalance = -1.0.
  * ---------------------------------------------------------------------- */
+/* Prefix sums of one array.  A negative entry anywhere is INVALID, checked
+ * before the sum (so the status does not depend on where the running sum
+ * first exceeds INT64_MAX); then a sum above INT64_MAX is OVERFLOW. */
 static int build_prefix(const int64_t *v, int32_t L, int64_t *P) {
+    for (int32_t i = 0; i < L; ++i)
+        if (v[i] < 0) return O_E_INVALID;
     i128 acc = 0;
     P[0] = 0;
     for (int32_t i = 0; i < L; ++i) {
-        if (v[i] < 0) return O_E_INVALID;
         acc += v[i];
         if (acc > (i128)INT64_MAX) return O_E_OVERFLOW;
         P[i + 1] = (int64_t)acc;
@@ -470,7 +474,7 @@ int oracle_diffuse(const int64_t *cost, const int64_t *mem, int32_t L, int32_t n
     *rounds = -1; *phi_out = -1; *phi0_out = -1;
     if (L < 1 || n < 1 || n > L || max_rounds < 0 || gamma < 0 || (mem && cap < 0) ||
         !valid_bnd(bnd_in, n, L)) {
-        for (int32_t s = 0; n >= 0 && s <= n; ++s) bnd_out[s] = -1;
+        for (int32_t s = 0; n >= 1 && s <= n; ++s) bnd_out[s] = -1;
         return O_E_INVALID;
     }
     int64_t *P = malloc(sizeof(int64_t) * (L + 1));

@@ -1,0 +1,80 @@
+"""ctypes loader for libdynmo.so (the C-ABI of include/dynmo.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (nvcc,
+sm_100a).  There is no fallback: if it is missing, importing the binding
+raises, so no product call can silently run anywhere but the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdynmo.so")
+
+OK, E_INVALID, E_INFEASIBLE, E_OVERFLOW, E_CUDA, E_NCCL, E_NOMEM = 0, -1, -2, -3, -4, -5, -6
+W_NOT_CONVERGED, W_BOUND_UNMET = 1, 2
+
+SRC_MASK_BITS, SRC_MASK_U8, SRC_NZ_BF16, SRC_NZ_F32 = 0, 1, 2, 3
+SRC_TOKMASK_BITS, SRC_EXIT_U8, SRC_EXPERT_I64, SRC_EXPERT_I32 = 4, 5, 6, 7
+REPACK_BOUND, REPACK_ALG2 = 0, 1
+MAX_LAYERS = 1023
+
+
+class Segment(C.Structure):
+    _fields_ = [("d_ptr", C.c_void_p), ("n_elem", C.c_int64), ("layer", C.c_int32),
+                ("src_kind", C.c_int32), ("n_experts", C.c_int32), ("top_k", C.c_int32)]
+
+
+class Buf(C.Structure):
+    _fields_ = [("d_ptr", C.c_void_p), ("bytes", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    p, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    sigs = {
+        "dynmo_strerror": (C.c_char_p, [i32]),
+        "dynmo_last_error": (C.c_char_p, []),
+        "dynmo_version": (C.c_char_p, []),
+        "dynmo_get_unique_id": (i32, [p]),
+        "dynmo_ctx_create": (i32, [i32, i32, i32, p, C.POINTER(p)]),
+        "dynmo_ctx_destroy": (None, [p]),
+        "dynmo_ctx_nranks": (i32, [p]),
+        "dynmo_ctx_rank": (i32, [p]),
+        "dynmo_profile_plan_create": (i32, [p, p, i32, i32, i32, i32, i32, C.POINTER(p)]),
+        "dynmo_profile_plan_destroy": (None, [p]),
+        "dynmo_plan_num_tiles": (i64, [p]),
+        "dynmo_plan_bytes": (i64, [p]),
+        "dynmo_plan_max_experts": (i32, [p]),
+        "dynmo_profile_layers": (i32, [p, p, p, p, p, p, p, p, p, p, p]),
+        "dynmo_partition_stages": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, p, p]),
+        "dynmo_diffuse_balance": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, i32,
+                                        p, p, p, p, p, p, p, p, p]),
+        "dynmo_repack_workers": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, i32,
+                                       p, p, p, p, p]),
+        "dynmo_migrate_layers": (i32, [p, i32, i32, p, p, i32, p, p, p, p, i32, p, p, p]),
+        "dynmo_migration_plan": (i32, [i32, i32, p, p, i32, p, p, p]),
+    }
+    for name, (res, args) in sigs.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_unique_id",
+            "dynmo_ctx_create", "dynmo_ctx_destroy", "dynmo_ctx_nranks", "dynmo_ctx_rank",
+            "dynmo_profile_plan_create", "dynmo_profile_plan_destroy", "dynmo_plan_num_tiles",
+            "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers",
+            "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",
+            "dynmo_migrate_layers", "dynmo_migration_plan"]

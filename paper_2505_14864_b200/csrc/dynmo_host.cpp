@@ -1,0 +1,562 @@
+// dynmo_host.cpp -- host side of the C-ABI declared in include/dynmo.h:
+// argument validation, profile plans (tile decomposition), the NCCL context,
+// kernel launches and layer migration.  No device compute happens here.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dynmo_internal.h"
+
+using namespace dynmo;
+
+namespace {
+thread_local std::string g_err;
+
+dynmo_status cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return DYNMO_E_CUDA;
+}
+dynmo_status invalid(const char *what) {
+    g_err = what;
+    return DYNMO_E_INVALID;
+}
+#define CUDA_TRY(call, what)                       \
+    do {                                           \
+        cudaError_t e_ = (call);                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+}  // namespace
+
+struct dynmo_ctx_s {
+    int device = 0, nranks = 1, rank = 0;
+    ncclComm_t comm = nullptr;
+    int num_sms = 148;
+};
+
+struct dynmo_plan_s {
+    dynmo_ctx ctx = nullptr;
+    int32_t layer_begin = 0, n_local = 0, n_total = 0, exchange = 0, max_E = 0;
+    bool has_hist = false;
+    int64_t n_tiles = 0, bytes = 0;
+    int grid = 1;
+    void *dmem = nullptr;
+    ProfTile *d_tiles = nullptr;
+    LayerInfo *d_info = nullptr;
+    unsigned long long *d_acc = nullptr, *d_hist = nullptr, *d_exit = nullptr;
+    int32_t *d_ws_status = nullptr;
+    unsigned int *d_ws_done = nullptr;
+    int64_t *d_slot_send = nullptr, *d_slot_recv = nullptr;
+    int64_t slot_elems = 0;
+};
+
+extern "C" {
+
+const char *dynmo_strerror(dynmo_status s) {
+    switch (s) {
+        case DYNMO_OK: return "ok";
+        case DYNMO_E_INVALID: return "invalid argument";
+        case DYNMO_E_INFEASIBLE: return "infeasible under the memory cap";
+        case DYNMO_E_OVERFLOW: return "int64 overflow";
+        case DYNMO_E_CUDA: return "CUDA error";
+        case DYNMO_E_NCCL: return "NCCL error";
+        case DYNMO_E_NOMEM: return "out of device memory";
+        case DYNMO_W_NOT_CONVERGED: return "diffusion not converged (max_rounds)";
+        case DYNMO_W_BOUND_UNMET: return "repack bound/target unmet";
+        default: return "unknown status";
+    }
+}
+
+const char *dynmo_last_error(void) { return g_err.c_str(); }
+
+const char *dynmo_version(void) { return "dynmo-b200 0.1 (sm_100a)"; }
+
+dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]) {
+    if (!h_id_out) return invalid("null id buffer");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+        return DYNMO_E_NCCL;
+    }
+    static_assert(sizeof(id.internal) == 128, "nccl id size");
+    memcpy(h_id_out, id.internal, 128);
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
+                              const uint8_t *h_nccl_id, dynmo_ctx *out) {
+    if (!out) return invalid("null ctx out");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks || device < 0) return invalid("bad rank/device");
+    if (nranks > 1 && !h_nccl_id) return invalid("nranks > 1 needs a NCCL unique id");
+    DeviceGuard g(device);
+    CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
+    auto *c = new dynmo_ctx_s();
+    c->device = device;
+    c->nranks = nranks;
+    c->rank = rank;
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+        c->num_sms = sms;
+    if (nranks > 1) {
+        ncclUniqueId id;
+        memcpy(id.internal, h_nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            g_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            delete c;
+            return DYNMO_E_NCCL;
+        }
+    }
+    *out = c;
+    return DYNMO_OK;
+}
+
+void dynmo_ctx_destroy(dynmo_ctx ctx) {
+    if (!ctx) return;
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    delete ctx;
+}
+
+int32_t dynmo_ctx_nranks(dynmo_ctx ctx) { return ctx ? ctx->nranks : 0; }
+int32_t dynmo_ctx_rank(dynmo_ctx ctx) { return ctx ? ctx->rank : -1; }
+
+// ------------------------------------------------------------------ plans
+dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_segs, int32_t n_segs,
+                                       int32_t layer_begin, int32_t n_local, int32_t n_total,
+                                       int32_t exchange, dynmo_plan *out) {
+    if (!out) return invalid("null plan out");
+    *out = nullptr;
+    if (!ctx) return invalid("null ctx");
+    if (n_segs < 0 || (n_segs > 0 && !h_segs)) return invalid("bad segment array");
+    if (layer_begin < 0 || n_local < 0 || n_total < 0) return invalid("negative layer range");
+    if (exchange) {
+        if (ctx->nranks < 2) return invalid("exchange needs nranks > 1");
+        if ((int64_t)layer_begin + n_local > n_total) return invalid("local layers exceed n_total");
+    } else if (n_total != n_local) {
+        return invalid("without exchange n_total must equal n_local");
+    }
+    std::vector<LayerInfo> info(n_local, LayerInfo{0, 0});
+    std::vector<ProfTile> vec, sca;
+    bool any_exit = false, has_hist = false;
+    int max_E = 0;
+    int64_t bytes = 0;
+    for (int32_t i = 0; i < n_segs; ++i) {
+        const dynmo_segment &sg = h_segs[i];
+        if (sg.n_elem < 0) return invalid("negative n_elem");
+        if (sg.src_kind < DYNMO_SRC_MASK_BITS || sg.src_kind > DYNMO_SRC_EXPERT_I32)
+            return invalid("unknown src_kind");
+        const bool is_exit = sg.src_kind == DYNMO_SRC_EXIT_U8;
+        const int q = sg.layer - layer_begin;
+        if (!is_exit && (q < 0 || q >= n_local)) return invalid("segment layer outside local range");
+        int op = 0, es = 1, slot = ACC_NNZ, E = 0;
+        int64_t nb = 0, partial_bits = 0;
+        switch (sg.src_kind) {
+            case DYNMO_SRC_MASK_BITS:
+            case DYNMO_SRC_TOKMASK_BITS:
+                op = OP_POPC;
+                slot = sg.src_kind == DYNMO_SRC_MASK_BITS ? ACC_NNZ : ACC_TOK;
+                nb = sg.n_elem / 8;
+                partial_bits = sg.n_elem % 8;
+                es = 4;  // words are uint32: pointer must be 4-byte aligned
+                break;
+            case DYNMO_SRC_MASK_U8: op = OP_NZ8; nb = sg.n_elem; break;
+            case DYNMO_SRC_NZ_BF16: op = OP_NZ16; es = 2; nb = sg.n_elem * 2; break;
+            case DYNMO_SRC_NZ_F32: op = OP_NZ32; es = 4; nb = sg.n_elem * 4; break;
+            case DYNMO_SRC_EXIT_U8: op = OP_EXIT; nb = sg.n_elem; break;
+            case DYNMO_SRC_EXPERT_I64: op = OP_EXP64; es = 8; nb = sg.n_elem * 8; break;
+            case DYNMO_SRC_EXPERT_I32: op = OP_EXP32; es = 4; nb = sg.n_elem * 4; break;
+        }
+        if (sg.src_kind == DYNMO_SRC_EXPERT_I64 || sg.src_kind == DYNMO_SRC_EXPERT_I32) {
+            E = sg.n_experts;
+            if (E < 1 || E > kMaxExperts) return invalid("n_experts outside [1, 1024]");
+            if (info[q].E != 0 && info[q].E != E) return invalid("inconsistent n_experts in a layer");
+            info[q].E = E;
+            info[q].flags |= SRC_HAS_MOE;
+            max_E = std::max(max_E, E);
+            has_hist = true;
+        } else if (is_exit) {
+            any_exit = true;
+            has_hist = true;
+        } else if (slot == ACC_TOK) {
+            info[q].flags |= SRC_HAS_TOK;
+        } else {
+            info[q].flags |= SRC_HAS_NNZ;
+        }
+        if (sg.n_elem == 0) continue;
+        if (!sg.d_ptr) return invalid("null segment pointer");
+        const uintptr_t p = (uintptr_t)sg.d_ptr;
+        if (p % es) return invalid("segment pointer misaligned for its element type");
+        bytes += nb + (partial_bits ? 1 : 0);
+        const int32_t lay = is_exit ? 0 : q;
+        const uint16_t aux = (uint16_t)(E ? E : slot);
+        auto add_scalar = [&](uintptr_t a, int64_t n, uint32_t bits) {
+            if (n <= 0) return;
+            sca.push_back(ProfTile{(const void *)a, (uint32_t)n, lay, (uint16_t)(op | OP_SCALAR), aux, bits});
+        };
+        // head up to 16-byte alignment, aligned body in kTileBytes tiles, tail
+        int64_t head = (int64_t)((16 - (p & 15)) & 15);
+        if (head > nb) head = nb;
+        const int64_t body = ((nb - head) / 16) * 16;
+        const int64_t tail = nb - head - body;
+        add_scalar(p, head, 0);
+        for (int64_t o = 0; o < body; o += kTileBytes) {
+            const int64_t len = std::min<int64_t>(kTileBytes, body - o);
+            vec.push_back(ProfTile{(const void *)(p + head + o), (uint32_t)len, lay, (uint16_t)op, aux, 0});
+        }
+        add_scalar(p + head + body, tail, 0);
+        if (partial_bits) add_scalar(p + nb, 1, (uint32_t)partial_bits);
+    }
+    if (any_exit)
+        for (auto &li : info) li.flags |= SRC_HAS_TOK | SRC_HAS_EXIT;
+    auto *pl = new dynmo_plan_s();
+    pl->ctx = ctx;
+    pl->layer_begin = layer_begin;
+    pl->n_local = n_local;
+    pl->n_total = n_total;
+    pl->exchange = exchange ? 1 : 0;
+    pl->max_E = max_E;
+    pl->has_hist = has_hist;
+    pl->bytes = bytes;
+    std::vector<ProfTile> tiles;
+    tiles.reserve(vec.size() + sca.size());
+    tiles.insert(tiles.end(), vec.begin(), vec.end());
+    tiles.insert(tiles.end(), sca.begin(), sca.end());
+    pl->n_tiles = (int64_t)tiles.size();
+    // one device block: tiles | info | acc | hist | exit | status,done | slots
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sz_tiles = up(sizeof(ProfTile) * std::max<size_t>(1, tiles.size()));
+    const size_t sz_info = up(sizeof(LayerInfo) * std::max(1, n_local));
+    const size_t sz_acc = up(sizeof(unsigned long long) * ACC_N * std::max(1, n_local));
+    const size_t sz_hist = up(sizeof(unsigned long long) * (size_t)std::max(1, n_local) * std::max(1, max_E));
+    const size_t sz_exit = up(sizeof(unsigned long long) * kExitBins);
+    const size_t sz_ws = up(16);
+    pl->slot_elems = 3 + 2 * (int64_t)n_total;
+    const size_t sz_send = exchange ? up(sizeof(int64_t) * pl->slot_elems) : 0;
+    const size_t sz_recv = exchange ? up(sizeof(int64_t) * pl->slot_elems * ctx->nranks) : 0;
+    const size_t total = sz_tiles + sz_info + sz_acc + sz_hist + sz_exit + sz_ws + sz_send + sz_recv;
+    DeviceGuard g(ctx->device);
+    cudaError_t e = cudaMalloc(&pl->dmem, total);
+    if (e != cudaSuccess) {
+        delete pl;
+        g_err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+        return DYNMO_E_NOMEM;
+    }
+    char *b = (char *)pl->dmem;
+    pl->d_tiles = (ProfTile *)b; b += sz_tiles;
+    pl->d_info = (LayerInfo *)b; b += sz_info;
+    pl->d_acc = (unsigned long long *)b; b += sz_acc;
+    pl->d_hist = (unsigned long long *)b; b += sz_hist;
+    pl->d_exit = (unsigned long long *)b; b += sz_exit;
+    pl->d_ws_status = (int32_t *)b;
+    pl->d_ws_done = (unsigned int *)(b + 4); b += sz_ws;
+    if (exchange) {
+        pl->d_slot_send = (int64_t *)b; b += sz_send;
+        pl->d_slot_recv = (int64_t *)b;
+    }
+    bool ok = cudaMemset(pl->dmem, 0, total) == cudaSuccess;
+    if (ok && !tiles.empty())
+        ok = cudaMemcpy(pl->d_tiles, tiles.data(), sizeof(ProfTile) * tiles.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && n_local > 0)
+        ok = cudaMemcpy(pl->d_info, info.data(), sizeof(LayerInfo) * n_local, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) {
+        e = cudaGetLastError();
+        cudaFree(pl->dmem);
+        delete pl;
+        return cuda_fail(e, "plan upload");
+    }
+    const int warps_per_block = kProfThreads / 32;
+    const int64_t want = (pl->n_tiles + warps_per_block - 1) / warps_per_block;
+    const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(has_hist);
+    pl->grid = (int)std::max<int64_t>(1, std::min(want, cap_blocks));
+    *out = pl;
+    return DYNMO_OK;
+}
+
+void dynmo_profile_plan_destroy(dynmo_plan plan) {
+    if (!plan) return;
+    DeviceGuard g(plan->ctx->device);
+    cudaFree(plan->dmem);
+    delete plan;
+}
+
+int64_t dynmo_plan_num_tiles(dynmo_plan plan) { return plan ? plan->n_tiles : -1; }
+int64_t dynmo_plan_bytes(dynmo_plan plan) { return plan ? plan->bytes : -1; }
+int32_t dynmo_plan_max_experts(dynmo_plan plan) { return plan ? plan->max_E : -1; }
+
+// ----------------------------------------------------------- call 1 profile
+dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t *d_frozen,
+                                  const dynmo_cost_coef *d_coef, const int64_t *d_mem_local,
+                                  int64_t *d_counters, int64_t *d_hist, int64_t *d_cost,
+                                  int64_t *d_mem, int32_t *d_status, dynmo_stream stream) {
+    if (!ctx || !plan || plan->ctx != ctx) return invalid("bad ctx/plan");
+    if ((plan->n_local > 0 && !d_coef) || !d_cost || !d_status) return invalid("null required output");
+    cudaStream_t s = (cudaStream_t)stream;
+    DeviceGuard g(ctx->device);
+    ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
+                std::max(1, plan->max_E), plan->d_ws_status};
+    CUDA_TRY(launch_profile(pa, plan->has_hist, plan->grid, s), "k_profile launch");
+    EpiArgs ea{};
+    ea.layer_begin = plan->layer_begin;
+    ea.n_local = plan->n_local;
+    ea.n_total = plan->n_total;
+    ea.exchange = plan->exchange;
+    ea.max_E = std::max(1, plan->max_E);
+    ea.info = plan->d_info;
+    ea.acc = plan->d_acc;
+    ea.hist = plan->d_hist;
+    ea.exit_hist = plan->d_exit;
+    ea.frozen = d_frozen;
+    ea.coef = d_coef;
+    ea.mem_local = d_mem_local;
+    ea.counters_out = d_counters;
+    ea.hist_out = plan->max_E > 0 ? d_hist : nullptr;
+    ea.cost_out = d_cost;
+    ea.mem_out = d_mem;
+    ea.slot_send = plan->d_slot_send;
+    ea.ws_status = plan->d_ws_status;
+    ea.ws_done = plan->d_ws_done;
+    ea.status_out = d_status;
+    CUDA_TRY(launch_epilogue(ea, s), "k_epilogue launch");
+    if (plan->exchange) {
+        ncclResult_t r = ncclAllGather(plan->d_slot_send, plan->d_slot_recv, (size_t)plan->slot_elems,
+                                       ncclInt64, ctx->comm, s);
+        if (r != ncclSuccess) {
+            g_err = std::string("ncclAllGather: ") + ncclGetErrorString(r);
+            return DYNMO_E_NCCL;
+        }
+        CUDA_TRY(launch_unpack(plan->d_slot_recv, ctx->nranks, plan->n_total, d_cost, d_mem, d_status, s),
+                 "k_unpack launch");
+    }
+    return DYNMO_OK;
+}
+
+// ----------------------------------------------------------- calls 2 - 4
+static dynmo_status check_solve(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers, const void *cost,
+                                const void *layer_off, const void *n_stages, const void *bnd_off,
+                                const void *bnd_out, const void *status) {
+    if (!ctx) return invalid("null ctx");
+    if (n_inst < 1) return invalid("n_inst < 1");
+    if (max_layers < 1 || max_layers > DYNMO_MAX_LAYERS) return invalid("max_layers outside [1, 1023]");
+    if (!cost || !layer_off || !n_stages || !bnd_off || !bnd_out || !status)
+        return invalid("null required pointer");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_partition_stages(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                    const int64_t *d_cost, const int64_t *d_mem,
+                                    const int32_t *d_layer_off, const int32_t *d_n_stages,
+                                    const int64_t *d_cap, const int32_t *d_bnd_off, int32_t *d_bnd,
+                                    int64_t *d_bottleneck, double *d_imbalance, int32_t *d_status,
+                                    dynmo_stream stream) {
+    dynmo_status st = check_solve(ctx, n_inst, max_layers, d_cost, d_layer_off, d_n_stages, d_bnd_off,
+                                  d_bnd, d_status);
+    if (st) return st;
+    if (!d_bottleneck) return invalid("null bottleneck");
+    if (d_mem && !d_cap) return invalid("mem without cap");
+    SolveArgs a{};
+    a.n_inst = n_inst;
+    a.max_layers = max_layers;
+    a.cost = d_cost;
+    a.mem = d_mem;
+    a.layer_off = d_layer_off;
+    a.n_stages = d_n_stages;
+    a.cap = d_cap;
+    a.bnd_off = d_bnd_off;
+    a.bnd_out = d_bnd;
+    a.bottleneck = d_bottleneck;
+    a.imbalance = d_imbalance;
+    a.status = d_status;
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_partition(a, (cudaStream_t)stream), "k_partition launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                   const int64_t *d_cost, const int64_t *d_mem,
+                                   const int32_t *d_layer_off, const int32_t *d_n_stages,
+                                   const int64_t *d_cap, const int32_t *d_bnd_off,
+                                   const int32_t *d_bnd_in, const int64_t *d_gamma,
+                                   const double *d_gamma_fluid, int32_t max_rounds,
+                                   int32_t *d_bnd_out, int32_t *d_rounds, int64_t *d_phi,
+                                   int64_t *d_phi0, double *d_fluid_x, int32_t *d_fluid_rounds,
+                                   double *d_fluid_phi, int32_t *d_status, dynmo_stream stream) {
+    dynmo_status st = check_solve(ctx, n_inst, max_layers, d_cost, d_layer_off, d_n_stages, d_bnd_off,
+                                  d_bnd_out, d_status);
+    if (st) return st;
+    if (!d_bnd_in) return invalid("null bnd_in");
+    if (d_mem && !d_cap) return invalid("mem without cap");
+    SolveArgs a{};
+    a.n_inst = n_inst;
+    a.max_layers = max_layers;
+    a.cost = d_cost;
+    a.mem = d_mem;
+    a.layer_off = d_layer_off;
+    a.n_stages = d_n_stages;
+    a.cap = d_cap;
+    a.bnd_off = d_bnd_off;
+    a.bnd_in = d_bnd_in;
+    a.bnd_out = d_bnd_out;
+    a.status = d_status;
+    a.gamma = d_gamma;
+    a.gamma_fluid = d_gamma_fluid;
+    a.max_rounds = max_rounds;
+    a.rounds = d_rounds;
+    a.phi = d_phi;
+    a.phi0 = d_phi0;
+    a.fluid_x = d_fluid_x;
+    a.fluid_rounds = d_fluid_rounds;
+    a.fluid_phi = d_fluid_phi;
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_diffuse(a, (cudaStream_t)stream), "k_diffuse launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_repack_workers(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
+                                  const int64_t *d_cost, const int64_t *d_mem,
+                                  const int32_t *d_layer_off, const int32_t *d_n_cur,
+                                  const int64_t *d_cap, const int32_t *d_bnd_off,
+                                  const int32_t *d_bnd_in, const int64_t *d_bound,
+                                  const int32_t *d_floor, int32_t mode, int32_t *d_n_new,
+                                  int32_t *d_bnd, int64_t *d_bottleneck, int32_t *d_status,
+                                  dynmo_stream stream) {
+    dynmo_status st = check_solve(ctx, n_inst, max_layers, d_cost, d_layer_off, d_n_cur, d_bnd_off,
+                                  d_bnd, d_status);
+    if (st) return st;
+    if (mode != DYNMO_REPACK_BOUND && mode != DYNMO_REPACK_ALG2) return invalid("bad repack mode");
+    if (!d_floor || !d_n_new || !d_bottleneck) return invalid("null repack pointer");
+    if (mode == DYNMO_REPACK_BOUND && !d_bound) return invalid("BOUND mode needs d_bound");
+    if (mode == DYNMO_REPACK_ALG2 && !d_bnd_in) return invalid("ALG2 mode needs d_bnd_in");
+    if (d_mem && !d_cap) return invalid("mem without cap");
+    SolveArgs a{};
+    a.n_inst = n_inst;
+    a.max_layers = max_layers;
+    a.cost = d_cost;
+    a.mem = d_mem;
+    a.layer_off = d_layer_off;
+    a.n_stages = d_n_cur;
+    a.cap = d_cap;
+    a.bnd_off = d_bnd_off;
+    a.bnd_in = d_bnd_in;
+    a.bnd_out = d_bnd;
+    a.bottleneck = d_bottleneck;
+    a.status = d_status;
+    a.bound = d_bound;
+    a.floor_ = d_floor;
+    a.mode = mode;
+    a.n_new = d_n_new;
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_repack(a, (cudaStream_t)stream), "k_repack launch");
+    return DYNMO_OK;
+}
+
+// ------------------------------------------------------------ call 5 migrate
+static bool valid_split(int32_t L, int32_t n, const int32_t *b) {
+    if (n < 1 || !b || b[0] != 0 || b[n] != L) return false;
+    for (int32_t s = 0; s < n; ++s)
+        if (b[s + 1] <= b[s]) return false;
+    return true;
+}
+
+int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_bnd_old,
+                             const int32_t *h_rank_old, int32_t n_new, const int32_t *h_bnd_new,
+                             const int32_t *h_rank_new, int32_t *h_moves) {
+    if (n_layers < 1 || !h_rank_old || !h_rank_new || !h_moves) return DYNMO_E_INVALID;
+    if (!valid_split(n_layers, n_old, h_bnd_old) || !valid_split(n_layers, n_new, h_bnd_new))
+        return DYNMO_E_INVALID;
+    // merge walk over the two boundary vectors
+    int32_t so = 0, sn = 0, m = 0;
+    for (int32_t i = 0; i < n_layers; ++i) {
+        while (i >= h_bnd_old[so + 1]) ++so;
+        while (i >= h_bnd_new[sn + 1]) ++sn;
+        const int32_t src = h_rank_old[so], dst = h_rank_new[sn];
+        if (src != dst) {
+            h_moves[3 * m + 0] = i;
+            h_moves[3 * m + 1] = src;
+            h_moves[3 * m + 2] = dst;
+            ++m;
+        }
+    }
+    return m;
+}
+
+dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old,
+                                  const int32_t *h_bnd_old, const int32_t *h_rank_old, int32_t n_new,
+                                  const int32_t *h_bnd_new, const int32_t *h_rank_new,
+                                  const dynmo_buf *h_send, const dynmo_buf *h_recv, int32_t n_bufs,
+                                  int64_t *h_bytes_sent, int64_t *h_bytes_recv, dynmo_stream stream) {
+    if (!ctx) return invalid("null ctx");
+    if (n_bufs < 0 || (n_bufs > 0 && (!h_send || !h_recv))) return invalid("bad buffer tables");
+    for (int32_t s = 0; s < n_old; ++s)
+        if (!h_rank_old || h_rank_old[s] < 0 || h_rank_old[s] >= ctx->nranks) return invalid("bad old rank");
+    for (int32_t s = 0; s < n_new; ++s)
+        if (!h_rank_new || h_rank_new[s] < 0 || h_rank_new[s] >= ctx->nranks) return invalid("bad new rank");
+    std::vector<int32_t> moves(3 * (size_t)std::max(1, n_layers));
+    const int32_t m = dynmo_migration_plan(n_layers, n_old, h_bnd_old, h_rank_old, n_new, h_bnd_new,
+                                           h_rank_new, moves.data());
+    if (m < 0) return invalid("malformed boundary vector");
+    const int me = ctx->rank;
+    int64_t sent = 0, recvd = 0;
+    // validate every buffer this rank needs before touching NCCL
+    for (int32_t k = 0; k < m; ++k) {
+        const int32_t i = moves[3 * k], src = moves[3 * k + 1], dst = moves[3 * k + 2];
+        for (int32_t u = 0; u < n_bufs; ++u) {
+            if (src == me) {
+                const dynmo_buf &b = h_send[(int64_t)i * n_bufs + u];
+                if (b.bytes < 0 || (b.bytes > 0 && !b.d_ptr)) return invalid("missing send buffer");
+                sent += b.bytes;
+            }
+            if (dst == me) {
+                const dynmo_buf &b = h_recv[(int64_t)i * n_bufs + u];
+                if (b.bytes < 0 || (b.bytes > 0 && !b.d_ptr)) return invalid("missing recv buffer");
+                recvd += b.bytes;
+            }
+        }
+    }
+    if (h_bytes_sent) *h_bytes_sent = sent;
+    if (h_bytes_recv) *h_bytes_recv = recvd;
+    if (m == 0 || (sent == 0 && recvd == 0)) return DYNMO_OK;
+    if (ctx->nranks < 2 || !ctx->comm) return invalid("cross-rank move without a communicator");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    ncclResult_t r = ncclGroupStart();
+    for (int32_t k = 0; k < m && r == ncclSuccess; ++k) {
+        const int32_t i = moves[3 * k], src = moves[3 * k + 1], dst = moves[3 * k + 2];
+        for (int32_t u = 0; u < n_bufs && r == ncclSuccess; ++u) {
+            if (src == me) {
+                const dynmo_buf &b = h_send[(int64_t)i * n_bufs + u];
+                if (b.bytes > 0) r = ncclSend(b.d_ptr, (size_t)b.bytes, ncclUint8, dst, ctx->comm, s);
+            }
+            if (dst == me && r == ncclSuccess) {
+                const dynmo_buf &b = h_recv[(int64_t)i * n_bufs + u];
+                if (b.bytes > 0) r = ncclRecv(b.d_ptr, (size_t)b.bytes, ncclUint8, src, ctx->comm, s);
+            }
+        }
+    }
+    ncclResult_t r2 = ncclGroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess) {
+        g_err = std::string("NCCL send/recv: ") + ncclGetErrorString(r);
+        return DYNMO_E_NCCL;
+    }
+    return DYNMO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Internal declarations shared by the host library (dynmo_host.cpp) and the
+// sm_100a kernels (k_profile.cu, k_solve.cu).  Not part of the C-ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dynmo.h"
+
+namespace dynmo {
+
+// ---------------------------------------------------------------- profiling
+// A tile is a contiguous byte range of one segment processed by one warp.
+// Vector tiles are 16-byte aligned with a multiple-of-16 length; scalar tiles
+// (unaligned heads/tails, < 16 bytes, and the last partial byte of a bit
+// mask) are walked element by element.
+enum ProfOp : uint16_t {
+    OP_POPC = 0,   // count set bits                (MASK_BITS, TOKMASK_BITS)
+    OP_NZ8 = 1,    // count bytes != 0              (MASK_U8)
+    OP_NZ16 = 2,   // count (h & 0x7FFF) != 0       (NZ_BF16)
+    OP_NZ32 = 3,   // count (w & 0x7FFFFFFF) != 0   (NZ_F32)
+    OP_EXIT = 4,   // histogram of uint8 exit depths
+    OP_EXP64 = 5,  // per-layer histogram of int64 expert ids
+    OP_EXP32 = 6,  // per-layer histogram of int32 expert ids
+    OP_KINDS = 7,
+    OP_SCALAR = 0x10,  // flag: scalar tile
+};
+
+// Accumulator slots per local layer in the device workspace.
+enum { ACC_NNZ = 0, ACC_TOK = 1, ACC_N = 2 };
+
+struct ProfTile {
+    const void *ptr;   // first byte
+    uint32_t nbytes;   // bytes in the tile
+    int32_t layer;     // local layer index (ignored by OP_EXIT)
+    uint16_t op;       // ProfOp | OP_SCALAR
+    uint16_t aux;      // count ops: accumulator slot; OP_EXP*: E;
+    uint32_t bits;     // scalar OP_POPC: valid bits in the (single) last byte, 0 = all 8
+};
+static_assert(sizeof(ProfTile) == 24, "tile layout");
+
+// Static per-local-layer source flags, known at plan creation.
+enum { SRC_HAS_NNZ = 1, SRC_HAS_TOK = 2, SRC_HAS_MOE = 4, SRC_HAS_EXIT = 8 };
+struct LayerInfo {
+    int32_t flags;
+    int32_t E;   // experts of this layer (0 if no MoE source)
+};
+
+constexpr int kProfThreads = 256;
+constexpr uint32_t kTileBytes = 32u << 10;   // vector tile size
+constexpr int kExitBins = 256;
+constexpr int kColExperts = 64;              // E <= 64: per-lane columns in smem
+constexpr int kMaxExperts = 1024;
+
+struct ProfArgs {
+    const ProfTile *tiles;
+    int64_t n_tiles;
+    unsigned long long *acc;    // [n_local][ACC_N]
+    unsigned long long *hist;   // [n_local][max_E]
+    unsigned long long *exit_hist;  // [kExitBins]
+    int32_t max_E;
+    int32_t *ws_status;
+};
+
+struct EpiArgs {
+    int32_t layer_begin, n_local, n_total, exchange, max_E;
+    const LayerInfo *info;
+    unsigned long long *acc;
+    unsigned long long *hist;
+    unsigned long long *exit_hist;
+    const uint8_t *frozen;
+    const dynmo_cost_coef *coef;
+    const int64_t *mem_local;
+    int64_t *counters_out;   // [n_local][4] nullable
+    int64_t *hist_out;       // [n_local][max_E] nullable
+    int64_t *cost_out;       // local mode: [n_local]
+    int64_t *mem_out;        // local mode: [n_local] nullable
+    int64_t *slot_send;      // exchange mode: [3 + 2*n_total]
+    int32_t *ws_status;
+    unsigned int *ws_done;
+    int32_t *status_out;     // local mode final status
+};
+
+cudaError_t launch_profile(const ProfArgs &a, bool has_hist, int grid, cudaStream_t s);
+int profile_blocks_per_sm(bool has_hist);
+cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
+cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
+                          int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
+                          cudaStream_t s);
+
+// ------------------------------------------------------------------ solvers
+struct SolveArgs {
+    int32_t n_inst, max_layers;
+    const int64_t *cost, *mem;
+    const int32_t *layer_off, *n_stages;   // n_stages: n (partition/diffuse) or n_cur (repack)
+    const int64_t *cap;
+    const int32_t *bnd_off;
+    const int32_t *bnd_in;
+    int32_t *bnd_out;
+    int64_t *bottleneck;
+    double *imbalance;
+    int32_t *status;
+    // diffusion
+    const int64_t *gamma;
+    const double *gamma_fluid;
+    int32_t max_rounds;
+    int32_t *rounds;
+    int64_t *phi, *phi0;
+    double *fluid_x;
+    int32_t *fluid_rounds;
+    double *fluid_phi;
+    // repack
+    const int64_t *bound;
+    const int32_t *floor_;
+    int32_t mode;
+    int32_t *n_new;
+};
+
+cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s);
+cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s);
+cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s);
+
+}  // namespace dynmo

@@ -1,0 +1,437 @@
+// k_profile.cu -- per-layer workload profiling on sm_100a.
+//
+//  k_profile   one fused, persistent, HBM-streaming kernel over every tile of
+//              every segment: 128-bit non-allocating loads (8 in flight per
+//              lane), branch-free SWAR counting, warp __reduce_add_sync, one
+//              64-bit atomic per tile (integer sums are order independent, so
+//              the result is bit-exact and deterministic).
+//              Sources: pruning masks, token masks / exit depths
+//              (P:L340-353), MoE expert ids.
+//  k_epilogue  counters -> int64 cost c_i (a5, readings Q1-Q6) with 128-bit
+//              checked arithmetic; consumes and clears the accumulators.
+//  k_unpack    after the NCCL all-gather of fixed per-rank slots, scatters
+//              every rank's slice into the global cost / mem vectors.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dynmo_internal.h"
+
+namespace dynmo {
+namespace {
+
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// Nonzero bytes of a 32-bit word: high bit of each byte of t is set iff the
+// byte is nonzero ((b & 0x7f) + 0x7f carries into bit 7 unless b & 0x7f == 0;
+// OR-ing b restores b == 0x80).  No carry crosses a byte.
+__device__ __forceinline__ uint32_t nz8(uint32_t w) {
+    uint32_t t = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w;
+    return __popc(t & 0x80808080u);
+}
+// Nonzero bf16 halves ignoring the sign bit.
+__device__ __forceinline__ uint32_t nz16(uint32_t w) {
+    uint32_t t = (w & 0x7FFF7FFFu) + 0x7FFF7FFFu;
+    return __popc(t & 0x80008000u);
+}
+__device__ __forceinline__ uint32_t nz32(uint32_t w) { return (w & 0x7FFFFFFFu) != 0u; }
+
+template <int OPK>
+__device__ __forceinline__ uint32_t count_word(uint32_t w) {
+    if constexpr (OPK == OP_POPC) return __popc(w);
+    else if constexpr (OPK == OP_NZ8) return nz8(w);
+    else if constexpr (OPK == OP_NZ16) return nz16(w);
+    else return nz32(w);
+}
+
+template <int OPK>
+__device__ __forceinline__ uint32_t count_vec(uint4 v) {
+    return count_word<OPK>(v.x) + count_word<OPK>(v.y) + count_word<OPK>(v.z) +
+           count_word<OPK>(v.w);
+}
+
+// Vector tile: every lane streams 16-byte vectors, 8 loads in flight.  A
+// zero vector counts 0 for every count op, so out-of-range lanes load zero.
+template <int OPK>
+__device__ __forceinline__ uint32_t count_tile(const uint4 *p, uint32_t nvec, int lane) {
+    constexpr int U = 8;
+    uint32_t acc = 0;
+    for (uint32_t base = 0; base < nvec; base += 32u * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+            v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += count_vec<OPK>(v[u]);
+    }
+    return acc;
+}
+
+// Scalar tile (< 16 bytes, or one partial byte of a bit mask).
+__device__ __forceinline__ uint32_t count_scalar(const ProfTile &t, int kind, int lane) {
+    const uint8_t *b = (const uint8_t *)t.ptr;
+    uint32_t c = 0;
+    switch (kind) {
+        case OP_POPC:
+            if ((uint32_t)lane < t.nbytes) {
+                uint32_t v = b[lane];
+                if (t.bits && (uint32_t)lane == t.nbytes - 1) v &= (1u << t.bits) - 1u;
+                c = __popc(v);
+            }
+            break;
+        case OP_NZ8:
+            if ((uint32_t)lane < t.nbytes) c = b[lane] != 0;
+            break;
+        case OP_NZ16:
+            if ((uint32_t)lane < t.nbytes / 2) c = (((const uint16_t *)b)[lane] & 0x7FFFu) != 0;
+            break;
+        case OP_NZ32:
+            if ((uint32_t)lane < t.nbytes / 4) c = nz32(((const uint32_t *)b)[lane]);
+            break;
+    }
+    return c;
+}
+
+template <bool HAS_HIST>
+__global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int64_t warp = (int64_t)blockIdx.x * (kProfThreads / 32) + wib;
+    const int64_t nwarps = (int64_t)gridDim.x * (kProfThreads / 32);
+    // Per-warp scratch for histogram ops: max(kColExperts*32, kExitBins,
+    // kMaxExperts) u32 words.  Zero at entry and after every flush.
+    uint32_t *sh = nullptr;
+    constexpr int kWarpWords = kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts;
+    if constexpr (HAS_HIST) {
+        sh = smem + wib * kWarpWords;
+        for (int i = lane; i < kWarpWords; i += 32) sh[i] = 0u;
+        __syncwarp();
+    }
+    for (int64_t ti = warp; ti < a.n_tiles; ti += nwarps) {
+        const ProfTile t = a.tiles[ti];
+        const int kind = t.op & 0xF;
+        const bool scalar = (t.op & OP_SCALAR) != 0;
+        if (kind <= OP_NZ32) {
+            uint32_t c;
+            if (scalar) {
+                c = count_scalar(t, kind, lane);
+            } else {
+                const uint4 *p = (const uint4 *)t.ptr;
+                const uint32_t nvec = t.nbytes >> 4;
+                switch (kind) {
+                    case OP_POPC: c = count_tile<OP_POPC>(p, nvec, lane); break;
+                    case OP_NZ8: c = count_tile<OP_NZ8>(p, nvec, lane); break;
+                    case OP_NZ16: c = count_tile<OP_NZ16>(p, nvec, lane); break;
+                    default: c = count_tile<OP_NZ32>(p, nvec, lane); break;
+                }
+            }
+            c = __reduce_add_sync(0xFFFFFFFFu, c);
+            if (lane == 0 && c)
+                atomicAdd(&a.acc[(int64_t)t.layer * ACC_N + t.aux], (unsigned long long)c);
+            continue;
+        }
+        if constexpr (HAS_HIST) {
+            if (kind == OP_EXIT) {
+                // uint8 exit depths -> warp histogram (shared atomics), flushed per tile
+                const uint8_t *b = (const uint8_t *)t.ptr;
+                if (scalar) {
+                    if ((uint32_t)lane < t.nbytes) atomicAdd(&sh[b[lane]], 1u);
+                } else {
+                    const uint4 *p = (const uint4 *)t.ptr;
+                    const uint32_t nvec = t.nbytes >> 4;
+                    for (uint32_t i = lane; i < nvec; i += 32) {
+                        uint4 v = ld_stream(p + i);
+                        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int s = 0; s < 4; ++s) atomicAdd(&sh[(w[k] >> (8 * s)) & 0xFFu], 1u);
+                    }
+                }
+                __syncwarp();
+                for (int v = lane; v < kExitBins; v += 32) {
+                    uint32_t c = sh[v];
+                    if (c) {
+                        atomicAdd(&a.exit_hist[v], (unsigned long long)c);
+                        sh[v] = 0u;
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+            // MoE expert ids.  E <= 64: each lane owns a private column
+            // sh[e*32 + lane] (no atomics, no bank conflicts); else shared
+            // atomics on sh[e].
+            const int E = t.aux;
+            const bool cols = E <= kColExperts;
+            const int esz = kind == OP_EXP64 ? 8 : 4;
+            uint32_t bad = 0;
+            auto add = [&](uint64_t v) {
+                if (v >= (uint64_t)E) { bad = 1; return; }
+                if (cols) sh[(int)v * 32 + lane] += 1u;
+                else atomicAdd(&sh[(int)v], 1u);
+            };
+            if (scalar) {
+                const uint32_t ne = t.nbytes / esz;
+                if ((uint32_t)lane < ne) {
+                    uint64_t v = esz == 8 ? (uint64_t)((const int64_t *)t.ptr)[lane]
+                                          : (uint64_t)(int64_t)((const int32_t *)t.ptr)[lane];
+                    add(v);
+                }
+            } else {
+                const uint4 *p = (const uint4 *)t.ptr;
+                const uint32_t nvec = t.nbytes >> 4;
+                for (uint32_t base = 0; base < nvec; base += 32u * 4u) {
+                    uint4 v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+                        v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+                        if (idx >= nvec) continue;
+                        if (esz == 8) {
+                            add(((uint64_t)v[u].y << 32) | v[u].x);
+                            add(((uint64_t)v[u].w << 32) | v[u].z);
+                        } else {
+                            add((uint64_t)(int64_t)(int32_t)v[u].x);
+                            add((uint64_t)(int64_t)(int32_t)v[u].y);
+                            add((uint64_t)(int64_t)(int32_t)v[u].z);
+                            add((uint64_t)(int64_t)(int32_t)v[u].w);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            unsigned long long *dst = a.hist + (int64_t)t.layer * a.max_E;
+            for (int e = lane; e < E; e += 32) {
+                uint32_t c = 0;
+                if (cols) {
+                    for (int l = 0; l < 32; ++l) {
+                        c += sh[e * 32 + l];
+                        sh[e * 32 + l] = 0u;
+                    }
+                } else {
+                    c = sh[e];
+                    sh[e] = 0u;
+                }
+                if (c) atomicAdd(&dst[e], (unsigned long long)c);
+            }
+            __syncwarp();
+            if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
+        }
+    }
+}
+
+// -------------------------------------------------------------- epilogue
+__device__ __forceinline__ int worse(int a, int b) { return a < b ? a : b; }
+
+__global__ void k_epilogue(EpiArgs a) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    int st = DYNMO_OK;
+    if (q < a.n_local) {
+        const LayerInfo li = a.info[q];
+        const int gi = a.layer_begin + q;
+        unsigned long long nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
+        unsigned long long tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
+        a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
+        a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
+        if (li.flags & SRC_HAS_EXIT)
+            for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
+        const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
+        const dynmo_cost_coef cf = a.coef[q];
+        const bool frozen = a.frozen && a.frozen[q];
+        // moe_i = EP * max over EP groups of group token counts (reading Q5)
+        __int128 moe = 0;
+        const bool bad_coef = cf.A < 0 || cf.B < 0 || cf.C < 0 || cf.F < 0;
+        bool bad_ep = false;
+        if (li.flags & SRC_HAS_MOE) {
+            const int E = li.E;
+            const int EP = cf.ep_ranks <= 0 ? E : cf.ep_ranks;
+            unsigned long long *h = a.hist + (int64_t)q * a.max_E;
+            bad_ep = E < 1 || EP < 1 || E % EP != 0;
+            if (!bad_ep) {
+                const int g = E / EP;
+                __int128 best = 0;
+                for (int r = 0; r < EP; ++r) {
+                    __int128 s = 0;
+                    for (int e = r * g; e < (r + 1) * g; ++e) s += (__int128)h[e];
+                    if (s > best) best = s;
+                }
+                moe = (__int128)EP * best;
+            }
+            for (int e = 0; e < E; ++e) {
+                if (a.hist_out) a.hist_out[(int64_t)q * a.max_E + e] = (int64_t)h[e];
+                h[e] = 0ull;
+            }
+        }
+        const __int128 LIM = (__int128)INT64_MAX;
+        const __int128 tok = has_tok ? (__int128)tok_u : (__int128)1;
+        const __int128 nnz = (__int128)nnz_u;
+        int64_t c = -1;
+        // order of the oracle: coefficients, then frozen, then the EP groups
+        if (bad_coef) {
+            st = DYNMO_E_INVALID;
+        } else if (frozen) {
+            c = cf.F;
+        } else if (bad_ep) {
+            st = DYNMO_E_INVALID;
+        } else {
+            const __int128 inner = (__int128)cf.A + (__int128)cf.B * nnz;
+            if (inner > LIM || tok > LIM || moe > LIM) {
+                st = DYNMO_E_OVERFLOW;
+            } else {
+                __int128 v = tok * inner;
+                const __int128 cm = (__int128)cf.C * moe;
+                if (v > LIM || cm > LIM || v + cm > LIM) st = DYNMO_E_OVERFLOW;
+                else c = (int64_t)(v + cm);
+            }
+        }
+        const int64_t m = a.mem_local ? a.mem_local[q] : 0;
+        if (a.counters_out) {
+            int64_t *o = a.counters_out + (int64_t)q * 4;
+            o[0] = (int64_t)nnz_u;
+            o[1] = has_tok ? (int64_t)tok_u : 1;
+            o[2] = moe > LIM ? -1 : (int64_t)moe;
+            o[3] = c;
+        }
+        if (a.exchange) {
+            a.slot_send[3 + q] = c;
+            a.slot_send[3 + a.n_total + q] = m;
+        } else {
+            a.cost_out[q] = c;
+            if (a.mem_out) a.mem_out[q] = m;
+        }
+    }
+    // block-reduce the status, then last-block finalisation
+    __shared__ int s_st;
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) s_st = DYNMO_OK;
+    __syncthreads();
+    if (st != DYNMO_OK) atomicMin(&s_st, st);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_st != DYNMO_OK) atomicMin(a.ws_status, s_st);
+        __threadfence();
+        unsigned prev = atomicAdd(a.ws_done, 1u);
+        s_last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        for (int v = threadIdx.x; v < kExitBins; v += blockDim.x) a.exit_hist[v] = 0ull;
+        if (threadIdx.x == 0) {
+            const int fin = atomicExch(a.ws_status, 0);
+            *a.ws_done = 0u;
+            if (a.exchange) {
+                a.slot_send[0] = a.layer_begin;
+                a.slot_send[1] = a.n_local;
+                a.slot_send[2] = fin;
+            } else {
+                *a.status_out = fin;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- unpack
+// Slot of rank r at slot_recv + r*S, S = 3 + 2*n_total:
+// {layer_begin, n_local, status, cost[n_total], mem[n_total]}.
+__global__ void k_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
+                         int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+    const int64_t S = 3 + 2 * (int64_t)n_total;
+    __shared__ int s_st;
+    if (threadIdx.x == 0) {
+        int st = DYNMO_OK;
+        for (int r = 0; r < nranks; ++r) {
+            const int64_t *sl = slot_recv + r * S;
+            const int64_t b = sl[0], c = sl[1];
+            if (b < 0 || c < 0 || b + c > n_total) st = worse(st, DYNMO_E_INVALID);
+            st = worse(st, (int)sl[2]);
+        }
+        s_st = st;
+    }
+    __syncthreads();
+    int st = DYNMO_OK;
+    for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
+        int cover = 0;
+        int64_t c = -1, m = 0;
+        for (int r = 0; r < nranks; ++r) {
+            const int64_t *sl = slot_recv + r * S;
+            const int64_t b = sl[0], cnt = sl[1];
+            if (b >= 0 && cnt >= 0 && b + cnt <= n_total && i >= b && i < b + cnt) {
+                cover++;
+                c = sl[3 + (i - b)];
+                m = sl[3 + n_total + (i - b)];
+            }
+        }
+        if (cover != 1) {
+            st = DYNMO_E_INVALID;
+            c = -1;
+        }
+        cost_out[i] = c;
+        if (mem_out) mem_out[i] = m;
+    }
+    if (st != DYNMO_OK) atomicMin(&s_st, st);
+    __syncthreads();
+    if (threadIdx.x == 0) *status_out = s_st;
+}
+
+}  // namespace
+
+int profile_blocks_per_sm(bool has_hist) {
+    int nb = 0;
+    if (has_hist) {
+        size_t sm = (size_t)(kProfThreads / 32) * 4 *
+                    (kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_profile<true>, kProfThreads, sm);
+    } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_profile<false>, kProfThreads, 0);
+    }
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_profile(const ProfArgs &a, bool has_hist, int grid, cudaStream_t s) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    if (has_hist) {
+        size_t sm = (size_t)(kProfThreads / 32) * 4 *
+                    (kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_profile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm);
+            attr = true;
+        }
+        k_profile<true><<<grid, kProfThreads, sm, s>>>(a);
+    } else {
+        k_profile<false><<<grid, kProfThreads, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s) {
+    const int threads = 256;
+    const int grid = a.n_local > 0 ? (a.n_local + threads - 1) / threads : 1;
+    k_epilogue<<<grid, threads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
+                          int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
+                          cudaStream_t s) {
+    k_unpack<<<1, 1024, 0, s>>>(slot_recv, nranks, n_total, cost_out, mem_out, status_out);
+    return cudaGetLastError();
+}
+
+}  // namespace dynmo

@@ -1,0 +1,300 @@
+"""Python binding of the DynMo C-ABI (include/dynmo.h), same call names.
+
+Argument marshalling only: torch tensors -> device pointers + the current
+CUDA stream.  Every step of the hot path runs in libdynmo's sm_100a kernels
+(and NCCL for the exchange / migration).  PyTorch provides device memory,
+streams and the process group that carries the NCCL unique id.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as _L
+from ._lib import lib
+
+__all__ = [
+    "DynmoError", "Context", "ProfilePlan", "SegmentSpec", "Batch", "coef_tensor",
+    "profile_layers", "partition_stages", "diffuse_balance", "repack_workers",
+    "migrate_layers", "migration_plan",
+]
+
+
+class DynmoError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib().dynmo_strerror(status).decode()
+        detail = lib().dynmo_last_error().decode()
+        super().__init__(f"{where}: {msg} ({status}) {detail}")
+        self.status = status
+
+
+def _check(st: int, where: str) -> int:
+    if st < 0:
+        raise DynmoError(st, where)
+    return st
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("device tensor expected")
+    if not t.is_contiguous():
+        raise ValueError("contiguous tensor expected")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _i32(a, device) -> torch.Tensor:
+    return torch.as_tensor(np.asarray(a, dtype=np.int32), device=device)
+
+
+# --------------------------------------------------------------------- ctx
+class Context:
+    """One per process/GPU.  With a torch process group of world size > 1 the
+    NCCL unique id is created on rank 0 and broadcast through that group."""
+
+    def __init__(self, device: int = 0, group=None):
+        self.device = int(device)
+        rank, nranks = 0, 1
+        if group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+            import torch.distributed as dist
+            if dist.is_initialized():
+                rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        self.rank, self.nranks = rank, nranks
+        id_buf = None
+        if nranks > 1:
+            import torch.distributed as dist
+            raw = (C.c_uint8 * 128)()
+            if rank == 0:
+                _check(lib().dynmo_get_unique_id(raw), "dynmo_get_unique_id")
+            obj = [bytes(raw)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            raw = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            id_buf = raw
+        h = C.c_void_p()
+        _check(lib().dynmo_ctx_create(self.device, nranks, rank, id_buf, C.byref(h)), "dynmo_ctx_create")
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dynmo_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------- profiling
+@dataclass
+class SegmentSpec:
+    tensor: torch.Tensor        # device tensor holding the segment
+    kind: int                   # _lib.SRC_*
+    layer: int = 0              # global layer index (ignored for EXIT_U8)
+    n_elem: Optional[int] = None  # bits for *_BITS kinds; default = element count
+    n_experts: int = 0
+    top_k: int = 0
+
+
+class ProfilePlan:
+    """dynmo_profile_plan_create: tile decomposition of this rank's segments."""
+
+    def __init__(self, ctx: Context, segments: Sequence[SegmentSpec], layer_begin: int,
+                 n_local: int, n_total: Optional[int] = None, exchange: bool = False):
+        n_total = n_local if n_total is None else n_total
+        arr = (_L.Segment * max(1, len(segments)))()
+        self._keep = []  # keep the tensors alive while the plan exists
+        for i, s in enumerate(segments):
+            t = s.tensor
+            if not t.is_cuda or not t.is_contiguous():
+                raise ValueError("segments must be contiguous device tensors")
+            n = s.n_elem
+            if n is None:
+                n = t.numel() * (t.element_size() * 8 if s.kind in (_L.SRC_MASK_BITS, _L.SRC_TOKMASK_BITS) else 1)
+            arr[i] = _L.Segment(t.data_ptr(), int(n), int(s.layer), int(s.kind), int(s.n_experts), int(s.top_k))
+            self._keep.append(t)
+        h = C.c_void_p()
+        _check(lib().dynmo_profile_plan_create(ctx.handle, arr, len(segments), layer_begin, n_local,
+                                               n_total, int(bool(exchange)), C.byref(h)),
+               "dynmo_profile_plan_create")
+        self._h = h
+        self.ctx = ctx
+        self.layer_begin, self.n_local, self.n_total = layer_begin, n_local, n_total
+        self.exchange = exchange
+        self.max_experts = lib().dynmo_plan_max_experts(h)
+        self.n_tiles = lib().dynmo_plan_num_tiles(h)
+        self.bytes = lib().dynmo_plan_bytes(h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dynmo_profile_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def coef_tensor(n: int, A=0, B=0, C_=0, F=0, ep=0, device="cuda") -> torch.Tensor:
+    """dynmo_cost_coef[n] as an int64 [n, 5] tensor (A, B, C, F, ep|pad)."""
+    t = torch.zeros((n, 5), dtype=torch.int64)
+    for j, v in enumerate((A, B, C_, F)):
+        t[:, j] = torch.as_tensor(v, dtype=torch.int64)
+    t[:, 4] = torch.as_tensor(ep, dtype=torch.int64) & 0xFFFFFFFF  # int32 ep, zero pad
+    return t.to(device)
+
+
+def profile_layers(ctx: Context, plan: ProfilePlan, coef: torch.Tensor, *, frozen=None,
+                   mem_local=None, counters=None, hist=None, cost=None, mem=None, status=None,
+                   stream=None):
+    """Call 1.  Returns (cost[n_total], mem[n_total] or None, status[1])."""
+    dev = coef.device
+    if cost is None:
+        cost = torch.empty(plan.n_total, dtype=torch.int64, device=dev)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+    _check(lib().dynmo_profile_layers(ctx.handle, plan.handle, _ptr(frozen), _ptr(coef), _ptr(mem_local),
+                                      _ptr(counters), _ptr(hist), _ptr(cost), _ptr(mem), _ptr(status),
+                                      _stream(stream)), "dynmo_profile_layers")
+    return cost, mem, status
+
+
+# ------------------------------------------------------------------ solvers
+class Batch:
+    """Batched instance layout of calls 2-4 (CSR-style offsets on the device)."""
+
+    def __init__(self, layers: Sequence[int], stages: Sequence[int], device="cuda",
+                 capacity: Optional[Sequence[int]] = None):
+        layers = np.asarray(layers, np.int64)
+        stages = np.asarray(stages, np.int64)
+        cap = stages if capacity is None else np.asarray(capacity, np.int64)
+        self.n_inst = len(layers)
+        self.layers, self.stages = layers, stages
+        self.layer_off_h = np.concatenate([[0], np.cumsum(layers)]).astype(np.int32)
+        self.bnd_off_h = np.concatenate([[0], np.cumsum(cap + 1)]).astype(np.int32)
+        self.layer_off = _i32(self.layer_off_h, device)
+        self.bnd_off = _i32(self.bnd_off_h, device)
+        self.n_stages = _i32(stages, device)
+        self.max_layers = int(layers.max()) if len(layers) else 1
+        self.total_bnd = int(self.bnd_off_h[-1])
+        self.device = device
+
+    def split(self, flat: torch.Tensor):
+        """Per-instance views of a boundary-layout tensor (host numpy)."""
+        h = flat.cpu().numpy()
+        return [h[self.bnd_off_h[q]:self.bnd_off_h[q + 1]] for q in range(self.n_inst)]
+
+
+def partition_stages(ctx: Context, batch: Batch, cost: torch.Tensor, *, mem=None, cap=None,
+                     bnd=None, bottleneck=None, imbalance=None, status=None, stream=None):
+    """Call 2.  Returns (bnd, bottleneck, imbalance, status)."""
+    dev = cost.device
+    if bnd is None:
+        bnd = torch.empty(batch.total_bnd, dtype=torch.int32, device=dev)
+    if bottleneck is None:
+        bottleneck = torch.empty(batch.n_inst, dtype=torch.int64, device=dev)
+    if imbalance is None:
+        imbalance = torch.empty(batch.n_inst, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty(batch.n_inst, dtype=torch.int32, device=dev)
+    _check(lib().dynmo_partition_stages(ctx.handle, batch.n_inst, batch.max_layers, _ptr(cost), _ptr(mem),
+                                        _ptr(batch.layer_off), _ptr(batch.n_stages), _ptr(cap),
+                                        _ptr(batch.bnd_off), _ptr(bnd), _ptr(bottleneck), _ptr(imbalance),
+                                        _ptr(status), _stream(stream)), "dynmo_partition_stages")
+    return bnd, bottleneck, imbalance, status
+
+
+def diffuse_balance(ctx: Context, batch: Batch, cost: torch.Tensor, bnd_in: torch.Tensor, *,
+                    mem=None, cap=None, gamma=None, gamma_fluid=None, max_rounds: int = 256,
+                    fluid: bool = True, out: Optional[dict] = None, stream=None):
+    """Call 3.  Returns a dict of output tensors."""
+    dev = cost.device
+    o = dict(out or {})
+    o.setdefault("bnd", torch.empty(batch.total_bnd, dtype=torch.int32, device=dev))
+    o.setdefault("rounds", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
+    o.setdefault("phi", torch.empty(batch.n_inst, dtype=torch.int64, device=dev))
+    o.setdefault("phi0", torch.empty(batch.n_inst, dtype=torch.int64, device=dev))
+    o.setdefault("status", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
+    if fluid:
+        o.setdefault("fluid_x", torch.empty(max(1, batch.total_bnd - batch.n_inst), dtype=torch.float64, device=dev))
+        o.setdefault("fluid_rounds", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
+        o.setdefault("fluid_phi", torch.empty(batch.n_inst, dtype=torch.float64, device=dev))
+    _check(lib().dynmo_diffuse_balance(
+        ctx.handle, batch.n_inst, batch.max_layers, _ptr(cost), _ptr(mem), _ptr(batch.layer_off),
+        _ptr(batch.n_stages), _ptr(cap), _ptr(batch.bnd_off), _ptr(bnd_in), _ptr(gamma),
+        _ptr(gamma_fluid), int(max_rounds), _ptr(o["bnd"]), _ptr(o["rounds"]), _ptr(o["phi"]),
+        _ptr(o["phi0"]), _ptr(o.get("fluid_x")), _ptr(o.get("fluid_rounds")), _ptr(o.get("fluid_phi")),
+        _ptr(o["status"]), _stream(stream)), "dynmo_diffuse_balance")
+    return o
+
+
+def repack_workers(ctx: Context, batch: Batch, cost: torch.Tensor, *, floor: torch.Tensor,
+                   bound: Optional[torch.Tensor] = None, mode: int = _L.REPACK_BOUND, mem=None,
+                   cap=None, bnd_in=None, out: Optional[dict] = None, stream=None):
+    """Call 4.  batch.stages = n_cur.  Returns a dict of output tensors."""
+    dev = cost.device
+    o = dict(out or {})
+    o.setdefault("n_new", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
+    o.setdefault("bnd", torch.empty(batch.total_bnd, dtype=torch.int32, device=dev))
+    o.setdefault("bottleneck", torch.empty(batch.n_inst, dtype=torch.int64, device=dev))
+    o.setdefault("status", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
+    _check(lib().dynmo_repack_workers(
+        ctx.handle, batch.n_inst, batch.max_layers, _ptr(cost), _ptr(mem), _ptr(batch.layer_off),
+        _ptr(batch.n_stages), _ptr(cap), _ptr(batch.bnd_off), _ptr(bnd_in), _ptr(bound), _ptr(floor),
+        int(mode), _ptr(o["n_new"]), _ptr(o["bnd"]), _ptr(o["bottleneck"]), _ptr(o["status"]),
+        _stream(stream)), "dynmo_repack_workers")
+    return o
+
+
+# ---------------------------------------------------------------- migration
+def migration_plan(n_layers: int, bnd_old, rank_old, bnd_new, rank_new) -> np.ndarray:
+    """Host-only: moves (layer, src_rank, dst_rank) of call 5."""
+    bo, ro = np.ascontiguousarray(bnd_old, np.int32), np.ascontiguousarray(rank_old, np.int32)
+    bn, rn = np.ascontiguousarray(bnd_new, np.int32), np.ascontiguousarray(rank_new, np.int32)
+    out = np.zeros((max(1, n_layers), 3), np.int32)
+    m = lib().dynmo_migration_plan(int(n_layers), len(bo) - 1, bo.ctypes.data, ro.ctypes.data,
+                                   len(bn) - 1, bn.ctypes.data, rn.ctypes.data, out.ctypes.data)
+    if m < 0:
+        raise DynmoError(m, "dynmo_migration_plan")
+    return out[:m].copy()
+
+
+def migrate_layers(ctx: Context, n_layers: int, bnd_old, rank_old, bnd_new, rank_new,
+                   send: dict, recv: dict, n_bufs: int = 1, stream=None):
+    """Call 5 (collective).  send/recv map layer -> list of device tensors
+    (this rank's old / new layers).  Returns (bytes_sent, bytes_recv)."""
+    bo, ro = np.ascontiguousarray(bnd_old, np.int32), np.ascontiguousarray(rank_old, np.int32)
+    bn, rn = np.ascontiguousarray(bnd_new, np.int32), np.ascontiguousarray(rank_new, np.int32)
+    tab_s = (_L.Buf * max(1, n_layers * n_bufs))()
+    tab_r = (_L.Buf * max(1, n_layers * n_bufs))()
+    for tab, d in ((tab_s, send), (tab_r, recv)):
+        for layer, bufs in d.items():
+            for k, t in enumerate(bufs):
+                tab[layer * n_bufs + k] = _L.Buf(t.data_ptr(), t.numel() * t.element_size())
+    sent, rec = C.c_int64(0), C.c_int64(0)
+    _check(lib().dynmo_migrate_layers(ctx.handle, int(n_layers), len(bo) - 1, bo.ctypes.data,
+                                      ro.ctypes.data, len(bn) - 1, bn.ctypes.data, rn.ctypes.data,
+                                      tab_s, tab_r, int(n_bufs), C.byref(sent), C.byref(rec),
+                                      _stream(stream)), "dynmo_migrate_layers")
+    return sent.value, rec.value

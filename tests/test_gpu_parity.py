@@ -1,0 +1,534 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by
+element on the same seeded inputs.  Integer results bit-exact; fluid
+diffusion loads bit-equal (declared tolerance 1e-6 relative, reading Q20)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2505_14864_b200 import dynmo
+    return dynmo
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2505_14864_b200 import _lib
+    return _lib
+
+
+@pytest.fixture(scope="module")
+def ctx(D):
+    torch.cuda.set_device(0)
+    return D.Context(0)
+
+
+DEV = "cuda:0"
+
+
+def _dev(a, dtype=None):
+    a = np.ascontiguousarray(a)
+    if dtype is not None:
+        a = a.astype(dtype)
+    return torch.from_numpy(a).to(DEV)
+
+
+# ------------------------------------------------------------ a1: pruning masks
+def _mixed_segments(D, L, shape, S, milestone, offset_views=True):
+    """Masks of every layer in u8 / bits / bf16 / f32, some as unaligned views."""
+    p = synth.cfg2_keep_probs(shape, S, milestone)
+    segs, keep = [], []
+    want = np.zeros(shape.L, np.int64)
+    g = np.random.default_rng(milestone)
+    for layer in range(shape.L):
+        for t, m in enumerate(synth.cfg2_layer_masks_u8(shape, layer, p[layer], milestone)):
+            kind = (layer + t) % 4
+            flat = m.reshape(-1)
+            cut = int(g.integers(0, 7)) if offset_views else 0
+            if kind == 0:
+                base = _dev(flat)
+                v = base[cut:]
+                segs.append(D.SegmentSpec(v, L.SRC_MASK_U8, layer))
+                want[layer] += oracle.count_nz_u8(flat[cut:])
+            elif kind == 1:
+                w = synth.pack_bits(flat)
+                base = _dev(w.view(np.int32))
+                nbits = flat.size - cut  # ragged bit count
+                segs.append(D.SegmentSpec(base, L.SRC_MASK_BITS, layer, n_elem=nbits))
+                want[layer] += oracle.count_bits(w, nbits)
+            elif kind == 2:
+                bf = synth.cfg2_bf16_weights(m, layer, t).reshape(-1)
+                base = _dev(bf.view(np.int16))
+                segs.append(D.SegmentSpec(base[cut:], L.SRC_NZ_BF16, layer))
+                want[layer] += oracle.count_nz_bf16(bf[cut:])
+            else:
+                bf = synth.cfg2_bf16_weights(m, layer, t).reshape(-1)
+                f = (bf.astype(np.uint32) << 16).view(np.float32)
+                base = _dev(f)
+                segs.append(D.SegmentSpec(base[cut:], L.SRC_NZ_F32, layer))
+                want[layer] += oracle.count_nz_f32(f[cut:])
+            keep.append(base)
+    return segs, keep, want
+
+
+@pytest.mark.parametrize("S,milestone", [(0.0, 0), (0.5203125, 1), (0.9, 4)])
+def test_profile_masks_mixed_small(D, L, ctx, S, milestone):
+    shape = synth.GPTShape(L=12, h=96)
+    segs, keep, want = _mixed_segments(D, L, shape, S, milestone)
+    plan = D.ProfilePlan(ctx, segs, 0, shape.L)
+    coef = D.coef_tensor(shape.L, A=7, B=3, device=DEV)
+    counters = torch.empty((shape.L, 4), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    c = counters.cpu().numpy()
+    assert np.array_equal(c[:, 0], want)
+    want_cost = [oracle.layer_cost(nnz=int(v), A=7, B=3)[1] for v in want]
+    assert np.array_equal(cost.cpu().numpy(), want_cost)
+    # a second call (accumulators consumed and cleared) gives the same result
+    cost2, _, st2 = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert np.array_equal(cost2.cpu().numpy(), want_cost) and int(st2.item()) == 0
+
+
+def test_profile_tiny_and_empty_segments(D, L, ctx):
+    """Edge cases: empty segments, 1-element segments, bits with n_elem < 8,
+    a layer without any source (nnz = 0), a single-byte mask."""
+    segs, keep, want = [], [], np.zeros(5, np.int64)
+    t = _dev(np.array([1, 0, 3], np.uint8))
+    segs.append(D.SegmentSpec(t[:0], L.SRC_MASK_U8, 0))
+    segs.append(D.SegmentSpec(t[2:], L.SRC_MASK_U8, 0)); want[0] += 1
+    w = np.array([0b1011011], np.uint32)
+    tw = _dev(w.view(np.int32))
+    segs.append(D.SegmentSpec(tw, L.SRC_MASK_BITS, 1, n_elem=5)); want[1] += oracle.count_bits(w, 5)
+    segs.append(D.SegmentSpec(tw, L.SRC_MASK_BITS, 2, n_elem=1)); want[2] += oracle.count_bits(w, 1)
+    h = np.array([0x8000, 0x0000, 0x7F80, 0x0001, 0xFFC0], np.uint16)  # -0, +0, inf, denorm, nan
+    th = _dev(h.view(np.int16))
+    segs.append(D.SegmentSpec(th, L.SRC_NZ_BF16, 3)); want[3] += oracle.count_nz_bf16(h)
+    keep += [t, tw, th]
+    plan = D.ProfilePlan(ctx, segs, 0, 5)
+    coef = D.coef_tensor(5, A=0, B=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert np.array_equal(cost.cpu().numpy(), want)
+
+
+def test_profile_config2_full_size(D, L, ctx):
+    """BASELINE config 2 at full size (48 layers x 12 h^2, u8 masks at S=0.9),
+    in the launch configuration bench.py times; every layer vs the oracle."""
+    shape = synth.GPTShape()
+    p = synth.cfg2_keep_probs(shape, 0.9, 4)
+    segs, keep, want = [], [], np.zeros(shape.L, np.int64)
+    for layer in range(shape.L):
+        for m in synth.cfg2_layer_masks_u8(shape, layer, p[layer], 4):
+            d = _dev(m.reshape(-1))
+            segs.append(D.SegmentSpec(d, L.SRC_MASK_U8, layer))
+            keep.append(d)
+            want[layer] += oracle.count_nz_u8(m)
+    plan = D.ProfilePlan(ctx, segs, 0, shape.L)
+    assert plan.bytes == shape.L * shape.params_per_layer
+    coef = D.coef_tensor(shape.L, A=0, B=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert np.array_equal(cost.cpu().numpy(), want)
+    # partition of the full-size cost vector at 8 stages
+    b = D.Batch([shape.L], [8], device=DEV)
+    bnd, bott, imb, pst = D.partition_stages(ctx, b, cost)
+    ost, ob, oB, oimb = oracle.partition(want, 8)
+    torch.cuda.synchronize()
+    assert int(pst.item()) == ost and np.array_equal(bnd.cpu().numpy(), ob)
+    assert int(bott.item()) == oB and float(imb.item()) == oimb
+
+
+# --------------------------------------------------- a2 + a4: exit / MoD / frozen
+@pytest.mark.parametrize("F", [0, 4, 8, 12])
+def test_profile_exit_tokmask_frozen(D, L, ctx, F):
+    """Config 3 (T = 512 x 2048): exit depths (EXIT_U8) on layers 0..15 and
+    per-layer token bitmasks on layers 16..31; frozen prefix F; c = (1-f) tok."""
+    T, Lyr = 512 * 2048, 32
+    e = synth.cfg3_exit_depth(T=T, L=Lyr)
+    frozen = synth.cfg3_frozen(Lyr, F)
+    tok_exit = oracle.exit_survivors(e, 0, Lyr)
+    segs = [D.SegmentSpec(_dev(e), L.SRC_EXIT_U8, 0)]
+    keep = [segs[0].tensor]
+    # plan A: exit source for all layers
+    planA = D.ProfilePlan(ctx, segs, 0, Lyr)
+    coef = D.coef_tensor(Lyr, A=1, B=0, device=DEV)
+    cnt = torch.empty((Lyr, 4), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, planA, coef, frozen=_dev(frozen), counters=cnt)
+    torch.cuda.synchronize()
+    want = [oracle.layer_cost(frozen=bool(frozen[i]), tok=int(tok_exit[i]), A=1)[1] for i in range(Lyr)]
+    assert int(st.item()) == 0
+    assert np.array_equal(cnt[:, 1].cpu().numpy(), tok_exit)
+    assert np.array_equal(cost.cpu().numpy(), want)
+    # plan B: token bitmasks alive_i[t] = e[t] > i (the MoD / alive-mask form)
+    segsB, tok_bits = [], np.zeros(Lyr, np.int64)
+    for i in range(Lyr):
+        w = synth.pack_bits((e > i).astype(np.uint8))
+        d = _dev(w.view(np.int32))
+        keep.append(d)
+        segsB.append(D.SegmentSpec(d, L.SRC_TOKMASK_BITS, i, n_elem=T))
+        tok_bits[i] = oracle.count_bits(w, T)
+    planB = D.ProfilePlan(ctx, segsB, 0, Lyr)
+    costB, _, stB = D.profile_layers(ctx, planB, coef, frozen=_dev(frozen))
+    torch.cuda.synchronize()
+    assert np.array_equal(tok_bits, tok_exit)
+    assert np.array_equal(costB.cpu().numpy(), want) and int(stB.item()) == 0
+
+
+def test_profile_exit_local_slice(D, L, ctx):
+    """An EXIT source on a rank owning layers 10..17 yields the same slice."""
+    e = synth.cfg3_exit_depth(T=100_003, L=32)
+    d = _dev(e[3:])  # unaligned view
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(d, L.SRC_EXIT_U8, 0)], 10, 8)
+    coef = D.coef_tensor(8, A=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert np.array_equal(cost.cpu().numpy(), oracle.exit_survivors(e[3:], 10, 8))
+
+
+# -------------------------------------------------------------- a3: MoE routing
+@pytest.mark.parametrize("alpha,dtype,E,ep", [(4.0, np.int64, 8, 8), (64.0, np.int64, 8, 8),
+                                              (4.0, np.int32, 8, 2), (4.0, np.int64, 100, 4),
+                                              (4.0, np.int32, 256, 0)])
+def test_profile_moe(D, L, ctx, alpha, dtype, E, ep):
+    """Config 4: per-expert histograms of top-2 ids; c = A T + C moe_i."""
+    T, Lyr, k = 64 * 2048 if E == 8 else 20_000, 6, 2
+    segs, keep, hists = [], [], []
+    for i in range(Lyr):
+        idx = synth.cfg4_routing(i, T=T, E=E, k=k, alpha=alpha, dtype=dtype)
+        st_o, h = oracle.expert_hist(idx, E)
+        assert st_o == 0
+        hists.append(h)
+        flat = idx.reshape(-1)
+        cut = i % 2  # odd layers: unaligned start
+        if cut:
+            h2 = oracle.expert_hist(flat[1:], E)[1]
+            hists[-1] = h2
+        d = _dev(flat)
+        keep.append(d)
+        segs.append(D.SegmentSpec(d[cut:], L.SRC_EXPERT_I64 if dtype == np.int64 else L.SRC_EXPERT_I32,
+                                  i, n_experts=E, top_k=k))
+    plan = D.ProfilePlan(ctx, segs, 0, Lyr)
+    assert plan.max_experts == E
+    coef = D.coef_tensor(Lyr, A=T, C_=4, ep=ep, device=DEV)
+    hist = torch.empty((Lyr, E), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef, hist=hist)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    assert np.array_equal(hist.cpu().numpy(), np.stack(hists))
+    want = [oracle.layer_cost(cnt=hists[i], A=T, C_=4, ep=ep)[1] for i in range(Lyr)]
+    assert np.array_equal(cost.cpu().numpy(), want)
+
+
+def test_profile_moe_invalid_id(D, L, ctx):
+    idx = synth.cfg4_routing(0, T=5000, E=8, k=2)
+    idx[77, 1] = 8
+    d = _dev(idx.reshape(-1))
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(d, L.SRC_EXPERT_I64, 0, n_experts=8, top_k=2)], 0, 1)
+    coef = D.coef_tensor(1, A=1, C_=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.expert_hist(idx, 8)[0] == oracle.E_INVALID
+
+
+def test_profile_overflow_and_bad_coef(D, L, ctx):
+    m = np.ones(1000, np.uint8)
+    d = _dev(m)
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(d, L.SRC_MASK_U8, 0), D.SegmentSpec(d, L.SRC_MASK_U8, 1)], 0, 2)
+    coef = D.coef_tensor(2, A=0, B=[2 ** 62, 5], device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_OVERFLOW
+    assert list(cost.cpu().numpy()) == [-1, oracle.layer_cost(nnz=1000, B=5)[1]]
+    coef = D.coef_tensor(2, A=[-1, 0], B=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_INVALID and int(cost[0].item()) == -1
+
+
+# ---------------------------------------------------------------- a7 partition
+def _run_partition(D, ctx, insts, with_mem):
+    b = D.Batch([len(x["cost"]) for x in insts], [x["n"] for x in insts], device=DEV)
+    cost = _dev(np.concatenate([x["cost"] for x in insts]), np.int64)
+    mem = cap = None
+    if with_mem:
+        mem = _dev(np.concatenate([x["mem"] for x in insts]), np.int64)
+        cap = _dev(np.array([x["cap"] for x in insts]), np.int64)
+    bnd, bott, imb, st = D.partition_stages(ctx, b, cost, mem=mem, cap=cap)
+    torch.cuda.synchronize()
+    return b, b.split(bnd), bott.cpu().numpy(), imb.cpu().numpy(), st.cpu().numpy()
+
+
+def _check_partition(insts, res, with_mem):
+    b, bnds, bott, imb, st = res
+    for q, x in enumerate(insts):
+        ost, ob, oB, oimb = oracle.partition(x["cost"], x["n"], mem=x["mem"] if with_mem else None,
+                                             cap=x["cap"] if with_mem else 0)
+        assert st[q] == ost, (q, x)
+        assert bott[q] == oB, (q, x)
+        assert np.array_equal(bnds[q][:x["n"] + 1], ob), (q, x, bnds[q], ob)
+        assert imb[q] == oimb, (q, imb[q], oimb)
+
+
+def test_partition_config1(D, ctx):
+    """Config 1: 10,000 instances of 24 layers on 4 stages (with and without
+    the memory cap), batched one CTA per instance."""
+    insts = synth.cfg1_instances(10_000)
+    with_m = [x for x in insts if x["mem"] is not None]
+    no_m = [dict(x, mem=None) for x in insts]
+    _check_partition(with_m, _run_partition(D, ctx, with_m, True), True)
+    _check_partition(no_m, _run_partition(D, ctx, no_m, False), False)
+
+
+def _random_insts(seed, count, Lmax, nmax=8, big=False, zero_frac=0.2, with_mem=False):
+    g = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        Ly = int(g.integers(1, Lmax + 1))
+        n = int(g.integers(1, min(nmax, Ly) + 1))
+        hi = 2 ** 55 // max(Ly, 1) if big else 1000
+        cost = g.integers(0, hi, Ly)
+        cost[g.random(Ly) < zero_frac] = 0
+        x = dict(cost=cost, n=n, mem=None, cap=0)
+        if with_mem:
+            mem = g.integers(0, 100, Ly)
+            x["mem"] = mem
+            x["cap"] = int(max(1, mem.sum() // n * g.uniform(0.6, 2.0)))
+        out.append(x)
+    return out
+
+
+@pytest.mark.parametrize("Lmax,with_mem,big", [(63, False, False), (127, True, False), (255, False, True),
+                                               (1023, True, False), (1023, False, True)])
+def test_partition_random_sizes(D, ctx, Lmax, with_mem, big):
+    """Every kernel variant (L <= 63/127/255/1023), zeros, ties, large costs,
+    infeasible memory caps, n = 1 and n = L."""
+    insts = _random_insts(Lmax + with_mem, 300, Lmax, nmax=min(64, Lmax), big=big, with_mem=with_mem)
+    insts.append(dict(cost=np.arange(Lmax), n=Lmax, mem=None, cap=0) if not with_mem else
+                 dict(cost=np.arange(Lmax), n=Lmax, mem=np.ones(Lmax, np.int64), cap=1))
+    insts.append(dict(cost=np.full(Lmax, 3), n=1, mem=None, cap=0) if not with_mem else
+                 dict(cost=np.full(Lmax, 3), n=1, mem=np.ones(Lmax, np.int64), cap=Lmax))
+    _check_partition(insts, _run_partition(D, ctx, insts, with_mem), with_mem)
+
+
+def test_partition_errors(D, ctx):
+    """INVALID (n > L, n < 1, negative cost), OVERFLOW, INFEASIBLE."""
+    insts = [dict(cost=np.array([1, 2]), n=3, mem=np.array([1, 1]), cap=5),
+             dict(cost=np.array([1, 2]), n=0, mem=np.array([1, 1]), cap=5),
+             dict(cost=np.array([1, -2, 3]), n=2, mem=np.array([1, 1, 1]), cap=5),
+             dict(cost=np.array([2 ** 62, 2 ** 62]), n=1, mem=np.array([1, 1]), cap=5),
+             dict(cost=np.array([2 ** 62, 2 ** 62 - 1]), n=1, mem=np.array([1, 1]), cap=5),
+             dict(cost=np.array([1, 1, 1]), n=2, mem=np.array([3, 3, 3]), cap=5),
+             dict(cost=np.array([1, 1, 1]), n=2, mem=np.array([3, 9, 3]), cap=5),
+             dict(cost=np.array([1, 1, 1]), n=2, mem=np.array([3, -1, 3]), cap=5)]
+    b = D.Batch([len(x["cost"]) for x in insts], [x["n"] for x in insts], device=DEV,
+                capacity=[max(x["n"], 1) + 2 for x in insts])
+    cost = _dev(np.concatenate([x["cost"] for x in insts]), np.int64)
+    mem = _dev(np.concatenate([x["mem"] for x in insts]), np.int64)
+    cap = _dev(np.array([x["cap"] for x in insts]), np.int64)
+    bnd, bott, imb, st = D.partition_stages(ctx, b, cost, mem=mem, cap=cap)
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    for q, x in enumerate(insts):
+        ost, ob, oB, oimb = oracle.partition(x["cost"], x["n"], mem=x["mem"], cap=x["cap"])
+        assert st[q] == ost, (q, st[q], ost)
+        assert bott[q].item() == oB
+
+
+# ------------------------------------------------------------------ a9 repack
+def _run_repack(D, ctx, insts, mode, with_mem):
+    b = D.Batch([len(x["cost"]) for x in insts], [x["n"] for x in insts], device=DEV)
+    cost = _dev(np.concatenate([x["cost"] for x in insts]), np.int64)
+    mem = cap = None
+    if with_mem:
+        mem = _dev(np.concatenate([x["mem"] for x in insts]), np.int64)
+        cap = _dev(np.array([x["cap"] for x in insts]), np.int64)
+    floor = _dev(np.array([x["floor"] for x in insts]), np.int32)
+    bound = _dev(np.array([x.get("bound", 0) for x in insts]), np.int64)
+    bnd_in = None
+    if mode == 1:
+        flat = np.full(b.total_bnd, -7, np.int32)
+        for q, x in enumerate(insts):
+            flat[b.bnd_off_h[q]:b.bnd_off_h[q] + x["n"] + 1] = x["bnd_in"]
+        bnd_in = _dev(flat)
+    o = D.repack_workers(ctx, b, cost, floor=floor, bound=bound, mode=mode, mem=mem, cap=cap, bnd_in=bnd_in)
+    torch.cuda.synchronize()
+    return b, b.split(o["bnd"]), o["n_new"].cpu().numpy(), o["bottleneck"].cpu().numpy(), o["status"].cpu().numpy()
+
+
+def test_repack_bound_config1(D, ctx):
+    insts = synth.cfg1_instances(3000, seed_key=1)
+    for with_mem in (True, False):
+        sel = [x if with_mem else dict(x, mem=None) for x in insts if (x["mem"] is not None) == with_mem]
+        b, bnds, kn, bott, st = _run_repack(D, ctx, sel, 0, with_mem)
+        for q, x in enumerate(sel):
+            ost, ok, ob, oB = oracle.repack_bound(x["cost"], 4, x["bound"], x["floor"],
+                                                  mem=x["mem"], cap=x["cap"])
+            assert (st[q], kn[q], bott[q]) == (ost, ok, oB), (q, x)
+            assert np.array_equal(bnds[q][:5], ob)
+
+
+def test_repack_bound_random(D, ctx):
+    g = np.random.default_rng(77)
+    insts = []
+    for x in _random_insts(78, 400, 127, nmax=8, with_mem=True):
+        Ly = len(x["cost"])
+        x["floor"] = int(g.integers(1, x["n"] + 1))
+        x["bound"] = int(x["cost"].sum() * g.uniform(0.05, 1.0))
+        insts.append(x)
+    b, bnds, kn, bott, st = _run_repack(D, ctx, insts, 0, True)
+    for q, x in enumerate(insts):
+        ost, ok, ob, oB = oracle.repack_bound(x["cost"], x["n"], x["bound"], x["floor"], mem=x["mem"], cap=x["cap"])
+        assert (st[q], kn[q], bott[q]) == (ost, ok, oB), q
+        assert np.array_equal(bnds[q][:x["n"] + 1], ob)
+
+
+def test_repack_alg2(D, ctx):
+    g = np.random.default_rng(88)
+    insts = []
+    for x in _random_insts(89, 500, 127, nmax=8, with_mem=True):
+        Ly, n = len(x["cost"]), x["n"]
+        inner = np.sort(g.choice(np.arange(1, Ly), n - 1, replace=False)) if n > 1 else []
+        x["bnd_in"] = np.concatenate([[0], inner, [Ly]]).astype(np.int32)
+        x["floor"] = int(g.integers(1, n + 1))
+        x["cap"] = int(g.integers(0, 3000))
+        insts.append(x)
+    b, bnds, kn, bott, st = _run_repack(D, ctx, insts, 1, True)
+    for q, x in enumerate(insts):
+        ost, ok, ob, oB = oracle.repack_alg2(x["cost"], x["bnd_in"], x["floor"], mem=x["mem"], cap=x["cap"])
+        assert (st[q], kn[q], bott[q]) == (ost, ok, oB), q
+        assert np.array_equal(bnds[q][:x["n"] + 1], ob)
+
+
+# --------------------------------------------------------------- a8 diffusion
+def _run_diffuse(D, ctx, insts, with_mem, max_rounds):
+    b = D.Batch([len(x["cost"]) for x in insts], [x["n"] for x in insts], device=DEV)
+    cost = _dev(np.concatenate([x["cost"] for x in insts]), np.int64)
+    mem = cap = None
+    if with_mem:
+        mem = _dev(np.concatenate([x["mem"] for x in insts]), np.int64)
+        cap = _dev(np.array([x["cap"] for x in insts]), np.int64)
+    flat = np.zeros(b.total_bnd, np.int32)
+    for q, x in enumerate(insts):
+        flat[b.bnd_off_h[q]:b.bnd_off_h[q + 1]] = x["bnd_in"]
+    gamma = _dev(np.array([x.get("gamma", 0) for x in insts]), np.int64)
+    gf = _dev(np.array([x.get("gamma_f", 0.0) for x in insts]), np.float64)
+    o = D.diffuse_balance(ctx, b, cost, _dev(flat), mem=mem, cap=cap, gamma=gamma, gamma_fluid=gf,
+                          max_rounds=max_rounds)
+    torch.cuda.synchronize()
+    return b, {k: v.cpu().numpy() for k, v in o.items()}
+
+
+def _check_diffuse(D, ctx, insts, with_mem, max_rounds):
+    b, o = _run_diffuse(D, ctx, insts, with_mem, max_rounds)
+    for q, x in enumerate(insts):
+        n = x["n"]
+        dst, db, dr, dphi, dphi0 = oracle.diffuse(x["cost"], x["bnd_in"], x.get("gamma", 0), max_rounds,
+                                                  mem=x["mem"] if with_mem else None, cap=x["cap"])
+        fst, fx, fr, fphi = oracle.diffuse_fluid(x["cost"], x["bnd_in"], x.get("gamma_f", 0.0), max_rounds)
+        want_st = min(dst, fst) if (dst < 0 or fst < 0) else max(dst, fst)
+        lo = b.bnd_off_h[q]
+        assert o["status"][q] == want_st, (q, o["status"][q], dst, fst)
+        assert np.array_equal(o["bnd"][lo:lo + n + 1], db), q
+        assert (o["rounds"][q], o["phi"][q], o["phi0"][q]) == (dr, dphi, dphi0), q
+        gx = o["fluid_x"][lo - q:lo - q + n]
+        assert np.array_equal(gx, fx), (q, gx, fx)  # bit-equal (<= 1e-6 rel is the declared bar)
+        assert o["fluid_rounds"][q] == fr and o["fluid_phi"][q] == fphi
+
+
+def test_diffuse_config3(D, ctx):
+    """Config 3: exit + freezing costs on 32 layers, 8 stages, uniform start,
+    gamma = 0, max_rounds = 256, gamma_f = 1e-9 phi(0)."""
+    T, Lyr = 512 * 2048, 32
+    e = synth.cfg3_exit_depth(T=T, L=Lyr)
+    tok = oracle.exit_survivors(e, 0, Lyr)
+    insts = []
+    for F in (0, 4, 8, 12):
+        f = synth.cfg3_frozen(Lyr, F)
+        cost = np.array([oracle.layer_cost(frozen=bool(f[i]), tok=int(tok[i]), A=1)[1] for i in range(Lyr)])
+        bnd = np.arange(0, 33, 4).astype(np.int32)
+        x0 = oracle.stage_loads(cost, bnd).astype(float)
+        insts.append(dict(cost=cost, n=8, bnd_in=bnd, mem=None, cap=0, gamma=0,
+                          gamma_f=1e-9 * oracle.phi_f64(x0)))
+    _check_diffuse(D, ctx, insts, False, 256)
+
+
+@pytest.mark.parametrize("with_mem,Lmax,maxr", [(False, 63, 256), (True, 127, 256), (True, 255, 3),
+                                                (False, 1023, 64)])
+def test_diffuse_random(D, ctx, with_mem, Lmax, maxr):
+    g = np.random.default_rng(Lmax)
+    insts = []
+    for x in _random_insts(Lmax + 1000, 200, Lmax, nmax=16, with_mem=with_mem):
+        Ly, n = len(x["cost"]), x["n"]
+        inner = np.sort(g.choice(np.arange(1, Ly), n - 1, replace=False)) if n > 1 else []
+        x["bnd_in"] = np.concatenate([[0], inner, [Ly]]).astype(np.int32)
+        x["gamma"] = int(g.integers(0, 50)) if g.random() < 0.3 else 0
+        x0 = oracle.stage_loads(x["cost"], x["bnd_in"]).astype(float)
+        x["gamma_f"] = float(g.choice([0.0, 1e-9 * oracle.phi_f64(x0), 1e-3 * oracle.phi_f64(x0)]))
+        if not with_mem:
+            x["mem"], x["cap"] = None, 0
+        insts.append(x)
+    _check_diffuse(D, ctx, insts, with_mem, maxr)
+
+
+def test_diffuse_invalid(D, ctx):
+    insts = [dict(cost=np.array([1, 2, 3]), n=2, bnd_in=np.array([0, 3, 3], np.int32), mem=None, cap=0),
+             dict(cost=np.array([1, -2, 3]), n=2, bnd_in=np.array([0, 1, 3], np.int32), mem=None, cap=0),
+             dict(cost=np.array([1, 2, 3]), n=2, bnd_in=np.array([0, 1, 3], np.int32), mem=None, cap=0,
+                  gamma=-1),
+             dict(cost=np.array([1, 2, 3]), n=2, bnd_in=np.array([0, 1, 3], np.int32), mem=None, cap=0,
+                  gamma_f=-1.0)]
+    _check_diffuse(D, ctx, insts, False, 16)
+
+
+# -------------------------------------------------------- config 5 batched sweep
+def test_config5_sweep(D, L, ctx):
+    """Config 5 (sample of 256 instances): MoD token bitmasks -> tok costs ->
+    partition at n -> BOUND repack to the fewest workers, all batched."""
+    insts = [synth.cfg5_instance(i) for i in range(256)]
+    segs, keep, layer = [], [], 0
+    tok_o = []
+    for x in insts:
+        d = _dev(x.masks.view(np.int32))
+        keep.append(d)
+        for l in range(x.L):
+            segs.append(D.SegmentSpec(d[l], L.SRC_TOKMASK_BITS, layer, n_elem=4096))
+            tok_o.append(oracle.count_bits(x.masks[l], 4096))
+            layer += 1
+    plan = D.ProfilePlan(ctx, segs, 0, layer)
+    coef = D.coef_tensor(layer, A=1, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    cost_h = cost.cpu().numpy()
+    assert np.array_equal(cost_h, tok_o)
+    b = D.Batch([x.L for x in insts], [x.n for x in insts], device=DEV)
+    mem = _dev(np.concatenate([x.mem for x in insts]), np.int64)
+    cap = _dev(np.array([x.cap for x in insts]), np.int64)
+    bnd, bott, imb, pst = D.partition_stages(ctx, b, cost, mem=mem, cap=cap)
+    floor = _dev(np.ones(len(insts)), np.int32)
+    bound = _dev(np.array([x.bound for x in insts]), np.int64)
+    r = D.repack_workers(ctx, b, cost, floor=floor, bound=bound, mem=mem, cap=cap)
+    torch.cuda.synchronize()
+    bnds, rb = b.split(bnd), b.split(r["bnd"])
+    kn = r["n_new"].cpu().numpy()
+    shrunk = 0
+    for q, x in enumerate(insts):
+        c = cost_h[b.layer_off_h[q]:b.layer_off_h[q + 1]]
+        ost, ob, oB, _ = oracle.partition(c, x.n, mem=x.mem, cap=x.cap)
+        assert pst[q].item() == ost and np.array_equal(bnds[q][:x.n + 1], ob) and bott[q].item() == oB
+        rst, rk, rbb, rB = oracle.repack_bound(c, x.n, x.bound, 1, mem=x.mem, cap=x.cap)
+        assert r["status"][q].item() == rst and kn[q] == rk and np.array_equal(rb[q][:x.n + 1], rbb)
+        shrunk += rk < x.n
+    assert shrunk > 0  # MoD leaves room to release workers
