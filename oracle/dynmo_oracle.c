@@ -262,28 +262,31 @@ int oracle_partition(const int64_t *cost, const int64_t *mem, int32_t L, int32_t
         fail_partition(n, bnd, bottleneck, imbalance);
         return st;
     }
-    const int64_t INF = INT64_MAX;
-    /* f[s][j], s = 1..n, j = 0..L; stored as f[s*(L+1)+j] */
-    int64_t *f = malloc(sizeof(int64_t) * (size_t)(n + 1) * (L + 1));
-    for (int32_t s = 0; s <= n; ++s)
-        for (int32_t j = 0; j <= L; ++j) f[s * (L + 1) + j] = INF;
-    f[0] = 0; /* zero stages cover zero layers */
+    /* f[s][j] = best bottleneck of the first j layers in s stages, valid
+     * where ok[s][j] (an explicit flag: INT64_MAX itself is a legal B*). */
+    const size_t W = (size_t)(L + 1);
+    int64_t *f = malloc(sizeof(int64_t) * (size_t)(n + 1) * W);
+    unsigned char *ok = calloc((size_t)(n + 1) * W, 1);
+    ok[0] = 1; f[0] = 0; /* zero stages cover zero layers */
     for (int32_t s = 1; s <= n; ++s)
         for (int32_t j = 1; j <= L; ++j) {
-            int64_t best = INF;
+            int have = 0;
+            int64_t best = 0;
             for (int32_t k = s - 1; k < j; ++k) {
-                int64_t prev = f[(s - 1) * (L + 1) + k];
-                if (prev == INF) continue;
+                if (!ok[(s - 1) * W + k]) continue;
                 if (mem && M[j] - M[k] > cap) continue;
+                int64_t prev = f[(s - 1) * W + k];
                 int64_t seg = P[j] - P[k];
                 int64_t v = prev > seg ? prev : seg;
-                if (v < best) best = v;
+                if (!have || v < best) { best = v; have = 1; }
             }
-            f[s * (L + 1) + j] = best;
+            ok[s * W + j] = (unsigned char)have;
+            f[s * W + j] = best;
         }
-    int64_t Bs = f[n * (L + 1) + L];
-    free(f);
-    if (Bs == INF) {
+    int feasible = ok[n * W + L];
+    int64_t Bs = f[n * W + L];
+    free(f); free(ok);
+    if (!feasible) {
         free(P); free(M);
         fail_partition(n, bnd, bottleneck, imbalance);
         return O_E_INFEASIBLE;

@@ -216,6 +216,10 @@ def test_partition_lower_bound_and_invalid():
     assert oracle.partition([1, 2], 3)[0] == oracle.E_INVALID
     assert oracle.partition([1, -2], 1)[0] == oracle.E_INVALID
     assert oracle.partition([2 ** 62, 2 ** 62], 1)[0] == oracle.E_OVERFLOW
+    # a bottleneck of exactly INT64_MAX is a legal optimum (brute force agrees)
+    big = [2 ** 62, 2 ** 62 - 1]
+    assert oracle.partition(big, 1, mem=[1, 1], cap=5)[2] == 2 ** 63 - 1 == brute.partition(big, 1)[0]
+    assert oracle.partition(big, 2)[2] == 2 ** 62 == brute.partition(big, 2)[0]
 
 
 def test_partition_scale_invariance():
