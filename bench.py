@@ -1,0 +1,486 @@
+#!/usr/bin/env python
+"""Benchmark of the DynMo per-step rebalancing hot path on B200.
+
+Workload (BASELINE.json configs[1]): GPT-48 gradual global magnitude pruning
+at S = 0.9, 8 pipeline stages, stage s on GPU floor(s*G/8).  One step =
+  profile_layers   (u8 pruning masks of this GPU's layers -> int64 costs,
+                    + NCCL all-gather of the cost slots when G > 1)
+  partition_stages (centralised min-max split, memory capped)
+  diffuse_balance  (decentralised diffusion + fluid process, from the
+                    current split)
+  repack_workers   (fewest GPUs within the dense pipeline's bottleneck)
+  D2H of the new boundaries, migrate_layers (NCCL send/recv of the CSR
+  payload of every layer whose GPU changes).
+The step replays the same rebalance event (uniform split -> balanced split)
+every iteration; inputs stay resident in HBM; L2 is flushed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+Under torchrun (N > 1) one rank per GPU; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+N_STAGES = 8
+SPARSITY = 0.9
+MILESTONE = 4
+METRIC = "rebalance ms/step (profile+partition+migrate) at 1/2/4/8 B200; profile HBM GB/s"
+L2_FLUSH_BYTES = 256 << 20
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="dynmo", choices=["dynmo", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch every call eagerly instead of replaying a CUDA graph")
+    return ap.parse_args()
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def workload_config(G):
+    shape = synth.GPTShape()
+    return {
+        "workload": "config2: GPT-48 gradual global magnitude pruning, S=0.9, 8 pipeline stages, "
+                    "u8 masks, rebalance from the uniform split",
+        "layers": shape.L, "hidden": shape.h, "stages": N_STAGES,
+        "params_per_layer": shape.params_per_layer,
+        "mask_bytes_total": shape.L * shape.params_per_layer,
+        "mask_repr": "u8", "stage_to_gpu": "floor(s*G/8)",
+        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+        "parallelism": f"pp-profile{G}",
+    }
+
+
+# ------------------------------------------------------------ input set-up
+class Inputs:
+    """Host arrays of this rank's layers (seeded, synthetic)."""
+
+    def __init__(self, rank_begin, rank_count):
+        self.shape = synth.GPTShape()
+        self.p = synth.cfg2_keep_probs(self.shape, SPARSITY, MILESTONE)
+        self.payload = synth.cfg2_payload_bytes(self.shape, self.p)  # caller-side CSR bytes
+        self.begin, self.count = rank_begin, rank_count
+        self.masks = []  # (layer, np.uint8 flat)
+        for layer in range(rank_begin, rank_begin + rank_count):
+            for m in synth.cfg2_layer_masks_u8(self.shape, layer, self.p[layer], MILESTONE):
+                self.masks.append((layer, m.reshape(-1)))
+        M = int(self.payload.sum())
+        self.cap = int(1.5 * M / N_STAGES)                  # per-GPU memory budget
+        self.bound = (self.shape.L // N_STAGES) * self.shape.params_per_layer  # dense B*
+        self.gamma_fluid = 1.0                              # one weight (cost unit)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock + clock-event reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, torch_dev):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            self.N = N
+            h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
+                h = N.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(torch_dev)
+            self.h = h
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        N = self.N
+        get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            N.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
+                    "samples": 0, "note": getattr(self, "err", "no samples")}
+        rs = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": rs, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------- oracle (CPU) arm
+def oracle_step(inp, layer_subset=None):
+    """The oracle as it stands: counts, costs, partition, diffusion, repack,
+    migration plan.  Returns (seconds counting, seconds solving)."""
+    import oracle
+    from paper_2505_14864_b200.pipeline import stage_ranks, uniform_split
+    L = inp.shape.L
+    t0 = time.perf_counter()
+    nnz = np.zeros(L, np.int64)
+    for layer, m in inp.masks:
+        if layer_subset is None or layer in layer_subset:
+            nnz[layer] += oracle.count_nz_u8(m)
+    t1 = time.perf_counter()
+    cost = np.array([oracle.layer_cost(nnz=int(v), A=0, B=1)[1] for v in nnz], np.int64)
+    mem = inp.payload
+    st, b, B, imb = oracle.partition(cost, N_STAGES, mem=mem, cap=inp.cap)
+    uni = uniform_split(L, N_STAGES)
+    oracle.diffuse(cost, uni, 0, 256, mem=mem, cap=inp.cap)
+    oracle.diffuse_fluid(cost, uni, inp.gamma_fluid, 256)
+    oracle.repack_bound(cost, N_STAGES, inp.bound, 1, mem=mem, cap=inp.cap)
+    r = stage_ranks(N_STAGES, 1)
+    oracle.moves(L, uni, r, b, r)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def cpu_threads_used():
+    return 1  # the oracle is single-threaded C
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    shape = synth.GPTShape()
+    inp = Inputs(0, shape.L)
+    L = shape.L
+    # size each step so that the whole --warmup + --steps run stays ~2 minutes
+    c_full, s_full = oracle_step(inp)
+    per_step_full = c_full + s_full
+    budget = 120.0
+    m = L
+    if (args.steps + args.warmup) * per_step_full > budget:
+        m = max(1, int(L * (budget / (args.steps + args.warmup) - s_full) / max(c_full, 1e-9)))
+        m = min(L, m)
+    times = []
+    for it in range(args.warmup + args.steps):
+        sub = set(((it * m) + k) % L for k in range(m))
+        c, s = oracle_step(inp, sub if m < L else None)
+        if it >= args.warmup:
+            times.append(c * (L / m) + s)
+    ms = 1e3 * float(np.mean(times))
+    sample = (f"each step: oracle counts of {m} of {L} layers' u8 masks (rotating; count time "
+              f"scaled by {L}/{m}) + every solver on the full 48-layer cost vector"
+              if m < L else "each step: the full config-2 oracle step (all 48 layers)")
+    out = {"impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": "ms",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+           "data": "synthetic", "config": workload_config(args.gpus),
+           "cpu_baseline": {"value": round(ms, 4), "unit": "ms/step", "cores": cpu_threads_used(),
+                            "kind": "oracle", "sample": sample},
+           "e2e": {"value": round(ms, 4), "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_dynmo(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14864_b200 import _lib as LB
+    from paper_2505_14864_b200 import dynmo as D
+    from paper_2505_14864_b200.pipeline import rank_layers, stage_ranks, uniform_split
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    G = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = D.Context(local)
+    shape = synth.GPTShape()
+    L = shape.L
+    b_old = uniform_split(L, N_STAGES)
+    ranks = stage_ranks(N_STAGES, G)
+    begin, count = rank_layers(b_old, ranks, rank)
+    inp = Inputs(begin, count)
+
+    # ---- device-resident inputs
+    dmask = [torch.from_numpy(m).to(dev) for _, m in inp.masks]
+    segs = [D.SegmentSpec(t, LB.SRC_MASK_U8, layer) for t, (layer, _) in zip(dmask, inp.masks)]
+    plan = D.ProfilePlan(ctx, segs, begin, count, n_total=L, exchange=G > 1)
+    coef = D.coef_tensor(count, A=0, B=1, device=dev)
+    mem_local = torch.from_numpy(inp.payload[begin:begin + count].astype(np.int64)).to(dev)
+    cost = torch.empty(L, dtype=torch.int64, device=dev)
+    mem = torch.empty(L, dtype=torch.int64, device=dev)
+    batch = D.Batch([L], [N_STAGES], device=dev)
+    cap = torch.tensor([inp.cap], dtype=torch.int64, device=dev)
+    bnd_in = torch.from_numpy(b_old).to(dev)
+    gamma = torch.zeros(1, dtype=torch.int64, device=dev)
+    gamma_f = torch.tensor([inp.gamma_fluid], dtype=torch.float64, device=dev)
+    bound = torch.tensor([inp.bound], dtype=torch.int64, device=dev)
+    floor = torch.ones(1, dtype=torch.int32, device=dev)
+    # every int32 result the host needs lives in ONE device buffer (views), so
+    # the step's single D2H boundary is one cudaMemcpyAsync
+    nb = batch.total_bnd
+    res_d = torch.empty(nb + 4, dtype=torch.int32, device=dev)
+    res_h = torch.empty(nb + 4, dtype=torch.int32, pin_memory=True)
+    part = dict(bnd=res_d[:nb], bott=torch.empty(1, dtype=torch.int64, device=dev),
+                imb=torch.empty(1, dtype=torch.float64, device=dev), st=res_d[nb:nb + 1])
+    pst = res_d[nb + 1:nb + 2]
+    dif_out = {"status": res_d[nb + 2:nb + 3]}
+    rep_out = {"status": res_d[nb + 3:nb + 4]}
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    # ---- migration buffers (CSR payload per layer; params + optimizer state)
+    send = {layer: [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
+            for layer in range(begin, begin + count)}
+    recv = {}
+
+    side = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    comm = torch.cuda.Stream(device=dev)
+    ev_res = torch.cuda.Event(external=True)  # in-graph record node after the result D2H
+    n_host = nb + 2                            # boundaries + partition & profile status
+
+    def solve_async():
+        """profile -> partition -> D2H of the boundaries (host-critical branch);
+        diffusion and repack on two side branches, joined at the end."""
+        main = torch.cuda.current_stream()
+        D.profile_layers(ctx, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=pst)
+        for sd in side:
+            sd.wait_stream(main)
+        with torch.cuda.stream(side[0]):
+            D.diffuse_balance(ctx, batch, cost, bnd_in, mem=mem, cap=cap, gamma=gamma, gamma_fluid=gamma_f,
+                              max_rounds=256, out=dif_out)
+        with torch.cuda.stream(side[1]):
+            D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
+        D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
+                           imbalance=part["imb"], status=part["st"])
+        res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
+        ev_res.record(main)
+        for sd in side:
+            main.wait_stream(sd)
+
+    graph = None
+    migrator = None
+
+    def solve():
+        if graph is not None:
+            graph.replay()
+        else:
+            solve_async()
+        ev_res.synchronize()  # the one D2H boundary: NCCL needs host counts
+        return res_h.numpy()[:n_host].copy()
+
+    # first step: learn the new split, allocate the receive buffers
+    r0 = solve()
+    torch.cuda.synchronize()
+    b_new = r0[:N_STAGES + 1].copy()
+    if r0[nb] != 0 or r0[nb + 1] != 0:
+        raise SystemExit(f"rebalance failed: statuses {r0[nb:]}")
+    moves = D.migration_plan(L, b_old, ranks, b_new, ranks)
+    for layer, src, dst in moves:
+        if dst == rank:
+            recv[int(layer)] = [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
+    migrator = D.Migrator(ctx, L, send, recv)
+
+    def step():
+        r = solve()
+        main = torch.cuda.current_stream()
+        # the host has seen the partition, so the all-gather is complete: the
+        # NCCL send/recv runs on its own stream, overlapping the side branches
+        with torch.cuda.stream(comm):
+            sr = migrator(b_old, ranks, r[:N_STAGES + 1], ranks)
+        main.wait_stream(comm)
+        return sr
+
+    if args.graph:
+        # capture the step's device part (timing enabled so the phase events
+        # are baked into the graph as external event-record nodes)
+        ctx.set_timing(True)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=torch.cuda.Stream(device=dev)):
+            solve_async()
+        torch.cuda.synchronize()
+        ctx.timing_read()  # discard
+        ctx.set_timing(False)
+        stream = torch.cuda.current_stream()
+
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    ctx.timing_read()  # reset accumulators
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sent_recv = (0, 0)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            ev[k][0].record(stream)
+            sent_recv = step()
+            ev[k][1].record(stream)
+            ev[k][1].synchronize()  # outside the timed interval: fold the phase events
+            ctx.timing_poll()
+        torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.set_timing(False)
+    phases = ctx.timing_read()
+    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    total_ms = float(step_ms.sum())
+    prof_ms, prof_n = phases["profile"]
+    prof_avg = prof_ms / max(prof_n, 1)
+    launches = sum(phases[p][1] for p in ("profile", "epilogue", "partition", "diffuse", "repack")) + \
+        (phases["exchange"][1] if G > 1 else 0)  # k_unpack (the all-gather itself is NCCL's)
+    mig_ms = phases["migrate"][0] / max(phases["migrate"][1], 1) if phases["migrate"][1] else 0.0
+
+    # ---- e2e: host buffers, H2D of this step's masks + D2H of the result inside
+    pinned = [torch.from_numpy(m).pin_memory() for _, m in inp.masks]
+    h2d = int(sum(p.numel() for p in pinned))
+    d2h = int(res_h.numel() * 4)
+    e2e = []
+    for k in range(args.e2e_steps):
+        flush.fill_(k & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for t, p in zip(dmask, pinned):
+            t.copy_(p, non_blocking=True)
+        step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    e2e_ms = float(np.mean(e2e))
+
+    # ---- reductions over ranks (max of device time)
+    vals = torch.tensor([total_ms, prof_avg, e2e_ms, mig_ms, float(sent_recv[0]), float(sent_recv[1])],
+                        dtype=torch.float64, device=dev)
+    achieved_local = plan.bytes / (prof_avg * 1e-3) / 1e9 if prof_avg > 0 else 0.0
+    ach = torch.tensor([achieved_local], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ach, op=dist.ReduceOp.MIN)
+    total_ms, prof_avg_max, e2e_ms, mig_ms, max_sent, max_recv = vals.tolist()
+    achieved = float(ach.item())
+
+    if rank == 0:
+        peaks, peak_src = load_peaks()
+        ms = total_ms / args.steps
+        cfg = workload_config(G)
+        cost_h = cost.cpu().numpy()
+        x_old = np.add.reduceat(cost_h, b_old[:-1])
+        x_new = np.add.reduceat(cost_h, b_new[:-1])
+        dl = lambda x: float((x.max() - x.min()) / (x.sum() / len(x)))
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic_k_profile.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get("dram_bytes_per_launch_G%d" % G)
+            except Exception:
+                traffic = None
+        out = {
+            "metric": METRIC, "value": round(ms, 5), "unit": "ms", "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": cfg,
+            "roofline": {"kernel": "k_profile", "bound": "hbm", "achieved": round(achieved, 1),
+                         "peak": peaks.get("hbm_gbs"), "peak_source": peak_src, "unit": "GB/s",
+                         "frac": round(achieved / peaks.get("hbm_gbs", 1.0), 4),
+                         "traffic": traffic, "bytes_per_launch": int(plan.bytes),
+                         "avg_launch_ms": round(prof_avg, 5)},
+            "phases_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in phases.items()},
+            "step_ms": {"median": round(float(np.median(step_ms)), 5),
+                        "p95": round(float(np.percentile(step_ms, 95)), 5)},
+            "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
+                        "max_bytes_recv_per_gpu": int(max_recv), "avg_ms": round(mig_ms, 5),
+                        "nvlink_GBps": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9, 1)
+                        if mig_ms > 0 else None, "nvlink_peak_GBps": NVLINK_PEER_GBS},
+            "solution": {"b_old": b_old.tolist(), "b_new": b_new.tolist(),
+                         "bottleneck_old": int(x_old.max()), "bottleneck_new": int(part["bott"].item()),
+                         "imbalance_old": round(dl(x_old), 4), "imbalance_new": round(float(part["imb"].item()), 4),
+                         "diffusion_rounds": int(dif_out["rounds"].item()),
+                         "repack_n_new": int(rep_out["n_new"].item()),
+                         "statuses": [int(x) for x in res_d.cpu().numpy()[nb:nb + 4]]},
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": args.e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if G == 1 and not args.no_cpu_baseline:
+            c_s, s_s = [], []
+            t_end = time.perf_counter() + args.cpu_seconds
+            while time.perf_counter() < t_end or len(c_s) < 2:
+                c, s = oracle_step(inp)
+                c_s.append(c)
+                s_s.append(s)
+            ob = 1e3 * (np.mean(c_s) + np.mean(s_s))
+            out["cpu_baseline"] = {"value": round(float(ob), 3), "unit": "ms/step", "cores": cpu_threads_used(),
+                                   "kind": "oracle",
+                                   "sample": f"{len(c_s)} full config-2 oracle steps (all 48 layers' u8 masks, "
+                                             f"every solver), 1 thread; host has {os.cpu_count()} cores"}
+        print(json.dumps(out), flush=True)
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_dynmo(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

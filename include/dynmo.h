@@ -70,6 +70,30 @@ void dynmo_ctx_destroy(dynmo_ctx ctx);
 int32_t dynmo_ctx_nranks(dynmo_ctx ctx);
 int32_t dynmo_ctx_rank(dynmo_ctx ctx);
 
+/* Diagnostics: per-phase device timing.  When enabled, the library records a
+ * pair of CUDA events on the launching stream around every launch of the
+ * phase (the breakdown of the paper's overhead figure: profiling /
+ * balancing algorithm / migration).  If the stream is being captured into a
+ * CUDA graph, the pair becomes two external event-record nodes that every
+ * replay re-records: call timing_poll after each replay has completed.
+ * timing_poll adds every recorded pair to the per-phase accumulators;
+ * timing_read returns (and resets) the accumulated milliseconds and launch
+ * count of a phase.  Off by default (no events recorded). */
+enum {
+    DYNMO_PHASE_PROFILE = 0,   /* k_profile (the streaming kernel)          */
+    DYNMO_PHASE_EPILOGUE = 1,  /* k_epilogue (counters -> cost)            */
+    DYNMO_PHASE_EXCHANGE = 2,  /* ncclAllGather + k_unpack                 */
+    DYNMO_PHASE_PARTITION = 3, /* k_partition                              */
+    DYNMO_PHASE_DIFFUSE = 4,   /* k_diffuse                                */
+    DYNMO_PHASE_REPACK = 5,    /* k_repack                                 */
+    DYNMO_PHASE_MIGRATE = 6,   /* NCCL send/recv group of migrate_layers   */
+    DYNMO_NUM_PHASES = 7
+};
+dynmo_status dynmo_ctx_set_timing(dynmo_ctx ctx, int32_t enable);
+dynmo_status dynmo_ctx_timing_poll(dynmo_ctx ctx);
+dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total_ms,
+                                   int64_t *h_count);
+
 /* ----------------------------------------------------------- profiling --
  * Sources of per-layer workload (P:L234-239 pruning p_i, P:L266-283 freezing
  * f_i, P:L340-353 early exit t_i, P:L376-389 MoD r_i t_i, P:L209-214 MoE
@@ -213,10 +237,13 @@ dynmo_status dynmo_partition_stages(dynmo_ctx ctx, int32_t n_inst, int32_t max_l
  *   d_gamma nullable (0), d_gamma_fluid nullable (0.0).
  *   Outputs: d_rounds[q], d_phi[q] (final), d_phi0[q] (initial) nullable,
  *   d_fluid_x (nullable) at offset d_bnd_off[q] - q (n_q doubles),
- *   d_fluid_rounds[q] nullable, d_fluid_phi[q] nullable.
- *   d_status[q] = worst of the discrete and fluid statuses (errors < 0 win,
- *   then NOT_CONVERGED).  b_in must be a valid split (else INVALID); a b_in
- *   that violates the cap is accepted and moves never exceed it. */
+ *   d_fluid_rounds[q], d_fluid_phi[q], d_fluid_status[q] nullable.  The fluid
+ *   process runs only if d_fluid_x is given (in its own CTA, concurrently).
+ *   d_status[q]: the discrete process (OK, NOT_CONVERGED, INVALID, OVERFLOW);
+ *   d_fluid_status[q]: the fluid process (OK, NOT_CONVERGED, INVALID -- also
+ *   for gamma_fluid < 0 or NaN --, OVERFLOW).  b_in must be a valid split
+ *   (else INVALID); a b_in that violates the cap is accepted and moves never
+ *   exceed it. */
 dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_layers,
                                    const int64_t *d_cost, const int64_t *d_mem,
                                    const int32_t *d_layer_off, const int32_t *d_n_stages,
@@ -225,7 +252,8 @@ dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_la
                                    const double *d_gamma_fluid, int32_t max_rounds,
                                    int32_t *d_bnd_out, int32_t *d_rounds, int64_t *d_phi,
                                    int64_t *d_phi0, double *d_fluid_x, int32_t *d_fluid_rounds,
-                                   double *d_fluid_phi, int32_t *d_status, dynmo_stream stream);
+                                   double *d_fluid_phi, int32_t *d_fluid_status, int32_t *d_status,
+                                   dynmo_stream stream);
 
 /* Call 4 -- repack_workers (P:L556-609 re-packing; "without
  * sacrificing training throughput"; readings Q14-Q16).

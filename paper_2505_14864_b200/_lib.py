@@ -18,6 +18,7 @@ W_NOT_CONVERGED, W_BOUND_UNMET = 1, 2
 SRC_MASK_BITS, SRC_MASK_U8, SRC_NZ_BF16, SRC_NZ_F32 = 0, 1, 2, 3
 SRC_TOKMASK_BITS, SRC_EXIT_U8, SRC_EXPERT_I64, SRC_EXPERT_I32 = 4, 5, 6, 7
 REPACK_BOUND, REPACK_ALG2 = 0, 1
+PHASES = ["profile", "epilogue", "exchange", "partition", "diffuse", "repack", "migrate"]
 MAX_LAYERS = 1023
 
 
@@ -50,6 +51,9 @@ def lib():
         "dynmo_ctx_destroy": (None, [p]),
         "dynmo_ctx_nranks": (i32, [p]),
         "dynmo_ctx_rank": (i32, [p]),
+        "dynmo_ctx_set_timing": (i32, [p, i32]),
+        "dynmo_ctx_timing_read": (i32, [p, i32, p, p]),
+        "dynmo_ctx_timing_poll": (i32, [p]),
         "dynmo_profile_plan_create": (i32, [p, p, i32, i32, i32, i32, i32, C.POINTER(p)]),
         "dynmo_profile_plan_destroy": (None, [p]),
         "dynmo_plan_num_tiles": (i64, [p]),
@@ -58,7 +62,7 @@ def lib():
         "dynmo_profile_layers": (i32, [p, p, p, p, p, p, p, p, p, p, p]),
         "dynmo_partition_stages": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, p, p]),
         "dynmo_diffuse_balance": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, i32,
-                                        p, p, p, p, p, p, p, p, p]),
+                                        p, p, p, p, p, p, p, p, p, p]),
         "dynmo_repack_workers": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, i32,
                                        p, p, p, p, p]),
         "dynmo_migrate_layers": (i32, [p, i32, i32, p, p, i32, p, p, p, p, i32, p, p, p]),
@@ -74,6 +78,7 @@ def lib():
 
 EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_unique_id",
             "dynmo_ctx_create", "dynmo_ctx_destroy", "dynmo_ctx_nranks", "dynmo_ctx_rank",
+            "dynmo_ctx_set_timing", "dynmo_ctx_timing_read", "dynmo_ctx_timing_poll",
             "dynmo_profile_plan_create", "dynmo_profile_plan_destroy", "dynmo_plan_num_tiles",
             "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers",
             "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",

@@ -44,11 +44,53 @@ struct DeviceGuard {
 };
 }  // namespace
 
+struct PhaseTimer {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;     // eager launches
+    size_t used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> graph;  // baked into captured graphs
+    double acc_ms = 0.0;
+    int64_t acc_n = 0;
+};
+
 struct dynmo_ctx_s {
     int device = 0, nranks = 1, rank = 0;
     ncclComm_t comm = nullptr;
     int num_sms = 148;
+    bool timing = false;
+    PhaseTimer ph[DYNMO_NUM_PHASES];
 };
+
+namespace {
+// Records the start event of `phase` on `s`; returns the end event to record
+// after the launch (nullptr when timing is off).
+// During stream capture the pair becomes two external event-record nodes of
+// the graph (re-recorded at every replay; read them with timing_poll after
+// each replay).
+cudaEvent_t phase_begin(dynmo_ctx c, int phase, cudaStream_t s) {
+    if (!c->timing) return nullptr;
+    PhaseTimer &t = c->ph[phase];
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    const bool cap = cs == cudaStreamCaptureStatusActive;
+    std::pair<cudaEvent_t, cudaEvent_t> pr;
+    if (cap || t.used == t.ev.size()) {
+        if (cudaEventCreate(&pr.first) != cudaSuccess || cudaEventCreate(&pr.second) != cudaSuccess)
+            return nullptr;
+        if (cap) t.graph.push_back(pr);
+        else t.ev.push_back(pr);
+    }
+    if (!cap) pr = t.ev[t.used++];
+    cudaEventRecordWithFlags(pr.first, s, cap ? cudaEventRecordExternal : cudaEventRecordDefault);
+    return pr.second;
+}
+void phase_end(cudaEvent_t e, cudaStream_t s) {
+    if (!e) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    cudaEventRecordWithFlags(e, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                       : cudaEventRecordDefault);
+}
+}  // namespace
 
 struct dynmo_plan_s {
     dynmo_ctx ctx = nullptr;
@@ -132,7 +174,68 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
 void dynmo_ctx_destroy(dynmo_ctx ctx) {
     if (!ctx) return;
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (auto &t : ctx->ph) {
+        for (auto &pr : t.ev) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        for (auto &pr : t.graph) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+    }
     delete ctx;
+}
+
+dynmo_status dynmo_ctx_set_timing(dynmo_ctx ctx, int32_t enable) {
+    if (!ctx) return invalid("null ctx");
+    ctx->timing = enable != 0;
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_timing_poll(dynmo_ctx ctx) {
+    if (!ctx) return invalid("null ctx");
+    for (auto &t : ctx->ph) {
+        for (size_t i = 0; i < t.used; ++i) {
+            CUDA_TRY(cudaEventSynchronize(t.ev[i].second), "cudaEventSynchronize");
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second), "cudaEventElapsedTime");
+            t.acc_ms += ms;
+            t.acc_n++;
+        }
+        t.used = 0;
+        for (auto &pr : t.graph) {
+            CUDA_TRY(cudaEventSynchronize(pr.second), "cudaEventSynchronize");
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, pr.first, pr.second) != cudaSuccess) {
+                cudaGetLastError();  // not yet recorded by any replay
+                continue;
+            }
+            t.acc_ms += ms;
+            t.acc_n++;
+        }
+    }
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total_ms, int64_t *h_count) {
+    if (!ctx || phase < 0 || phase >= DYNMO_NUM_PHASES) return invalid("bad ctx/phase");
+    PhaseTimer &t = ctx->ph[phase];
+    if (t.used) {  // fold pending eager launches in (graph pairs need explicit polls)
+        for (size_t i = 0; i < t.used; ++i) {
+            CUDA_TRY(cudaEventSynchronize(t.ev[i].second), "cudaEventSynchronize");
+            float ms = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second), "cudaEventElapsedTime");
+            t.acc_ms += ms;
+            t.acc_n++;
+        }
+        t.used = 0;
+    }
+    if (h_total_ms) *h_total_ms = t.acc_ms;
+    if (h_count) *h_count = t.acc_n;
+    t.acc_ms = 0.0;
+    t.acc_n = 0;
+    return DYNMO_OK;
 }
 
 int32_t dynmo_ctx_nranks(dynmo_ctx ctx) { return ctx ? ctx->nranks : 0; }
@@ -312,7 +415,9 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     DeviceGuard g(ctx->device);
     ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
                 std::max(1, plan->max_E), plan->d_ws_status};
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PROFILE, s);
     CUDA_TRY(launch_profile(pa, plan->has_hist, plan->grid, s), "k_profile launch");
+    phase_end(te, s);
     EpiArgs ea{};
     ea.layer_begin = plan->layer_begin;
     ea.n_local = plan->n_local;
@@ -334,8 +439,11 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     ea.ws_status = plan->d_ws_status;
     ea.ws_done = plan->d_ws_done;
     ea.status_out = d_status;
+    te = phase_begin(ctx, DYNMO_PHASE_EPILOGUE, s);
     CUDA_TRY(launch_epilogue(ea, s), "k_epilogue launch");
+    phase_end(te, s);
     if (plan->exchange) {
+        te = phase_begin(ctx, DYNMO_PHASE_EXCHANGE, s);
         ncclResult_t r = ncclAllGather(plan->d_slot_send, plan->d_slot_recv, (size_t)plan->slot_elems,
                                        ncclInt64, ctx->comm, s);
         if (r != ncclSuccess) {
@@ -344,6 +452,7 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
         }
         CUDA_TRY(launch_unpack(plan->d_slot_recv, ctx->nranks, plan->n_total, d_cost, d_mem, d_status, s),
                  "k_unpack launch");
+        phase_end(te, s);
     }
     return DYNMO_OK;
 }
@@ -385,7 +494,9 @@ dynmo_status dynmo_partition_stages(dynmo_ctx ctx, int32_t n_inst, int32_t max_l
     a.imbalance = d_imbalance;
     a.status = d_status;
     DeviceGuard g(ctx->device);
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PARTITION, (cudaStream_t)stream);
     CUDA_TRY(launch_partition(a, (cudaStream_t)stream), "k_partition launch");
+    phase_end(te, (cudaStream_t)stream);
     return DYNMO_OK;
 }
 
@@ -397,7 +508,8 @@ dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_la
                                    const double *d_gamma_fluid, int32_t max_rounds,
                                    int32_t *d_bnd_out, int32_t *d_rounds, int64_t *d_phi,
                                    int64_t *d_phi0, double *d_fluid_x, int32_t *d_fluid_rounds,
-                                   double *d_fluid_phi, int32_t *d_status, dynmo_stream stream) {
+                                   double *d_fluid_phi, int32_t *d_fluid_status, int32_t *d_status,
+                                   dynmo_stream stream) {
     dynmo_status st = check_solve(ctx, n_inst, max_layers, d_cost, d_layer_off, d_n_stages, d_bnd_off,
                                   d_bnd_out, d_status);
     if (st) return st;
@@ -424,8 +536,11 @@ dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_la
     a.fluid_x = d_fluid_x;
     a.fluid_rounds = d_fluid_rounds;
     a.fluid_phi = d_fluid_phi;
+    a.fluid_status = d_fluid_status;
     DeviceGuard g(ctx->device);
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_DIFFUSE, (cudaStream_t)stream);
     CUDA_TRY(launch_diffuse(a, (cudaStream_t)stream), "k_diffuse launch");
+    phase_end(te, (cudaStream_t)stream);
     return DYNMO_OK;
 }
 
@@ -463,7 +578,9 @@ dynmo_status dynmo_repack_workers(dynmo_ctx ctx, int32_t n_inst, int32_t max_lay
     a.mode = mode;
     a.n_new = d_n_new;
     DeviceGuard g(ctx->device);
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_REPACK, (cudaStream_t)stream);
     CUDA_TRY(launch_repack(a, (cudaStream_t)stream), "k_repack launch");
+    phase_end(te, (cudaStream_t)stream);
     return DYNMO_OK;
 }
 
@@ -536,6 +653,7 @@ dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old
     if (ctx->nranks < 2 || !ctx->comm) return invalid("cross-rank move without a communicator");
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
     ncclResult_t r = ncclGroupStart();
     for (int32_t k = 0; k < m && r == ncclSuccess; ++k) {
         const int32_t i = moves[3 * k], src = moves[3 * k + 1], dst = moves[3 * k + 2];
@@ -551,6 +669,7 @@ dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old
         }
     }
     ncclResult_t r2 = ncclGroupEnd();
+    phase_end(te, s);
     if (r == ncclSuccess) r = r2;
     if (r != ncclSuccess) {
         g_err = std::string("NCCL send/recv: ") + ncclGetErrorString(r);

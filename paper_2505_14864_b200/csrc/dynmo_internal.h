@@ -108,6 +108,7 @@ struct SolveArgs {
     double *fluid_x;
     int32_t *fluid_rounds;
     double *fluid_phi;
+    int32_t *fluid_status;
     // repack
     const int64_t *bound;
     const int32_t *floor_;

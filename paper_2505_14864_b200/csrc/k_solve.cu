@@ -1,18 +1,22 @@
-// k_solve.cu -- batched rebalancing solvers on sm_100a, one CTA per instance
-// (SURVEY 8(a) a7-a9).
+// k_solve.cu -- batched rebalancing solvers on sm_100a.
+//
+// One instance = one CTA of ONE warp (32 threads): the solvers are latency
+// bound (dependent shared-memory lookups, tiny arithmetic), so barriers
+// between warps only add waiting; a single warp needs only __syncwarp, and a
+// batch of 4096 instances is a single wave of warps over the 148 SMs.
+// Prefix sums, boundaries and scratch live in dynamic shared memory sized
+// from max_layers.
 //
 //  k_partition  contiguous min-max partition:
-//               exact integer (W+1)-ary search over the bottleneck B, each warp
-//               testing one candidate with a warp-parallel greedy: a greedy
-//               jump from layer j is ONE __reduce_add_sync over the lanes'
-//               register-resident prefix sums (count of k with P[k] <= P[j]+B
-//               and M[k] <= M[j]+cap), so a feasibility test costs <= n jumps.
-//               Canonical lexmax boundaries (reading Q7), fp64 Delta L.
-//  k_diffuse    decentralised diffusion (reading Q10):
-//               per round every warp re-splits adjacent stage pairs (warp
-//               argmin over split points), the max-neighbor matching applies
-//               mutually chosen pairs; plus the fluid averaging process of
-//               Lemma 2's proof in fp64 (round-to-nearest, no FMA).
+//               exact integer 33-ary search over the bottleneck B: each lane
+//               tests one candidate with its own greedy (binary-search jumps
+//               in the prefix sums, memory cap folded in), a ballot picks the
+//               sub-interval.  Canonical lexmax boundaries (reading Q7),
+//               fp64 Delta L (eq:imbalance).
+//  k_diffuse    blockIdx.y = 0: discrete diffusion (P:L497, P:L518-549,
+//               reading Q10), lane = stage pair; blockIdx.y = 1: the fluid
+//               process of Lemma 2's proof, register-resident rounds on lane
+//               0 and phi of 32 rounds at a time on the 32 lanes.
 //  k_repack     fewest workers within the throughput bound (P:L13, P:L556-
 //               609): one greedy count at B = bound then the partition; or
 //               Alg. 2 first-fit (P:L562-593 with SPEC:L389 fixes).
@@ -27,25 +31,54 @@ namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr int64_t I64MAX = INT64_MAX;
+constexpr int kChunk = 32;  // fluid rounds advanced per phi evaluation pass
+constexpr int kRow = 33;    // padded history row (doubles): lanes read rows conflict-free
 
 __device__ __forceinline__ int64_t satadd(int64_t a, int64_t b) {  // a, b >= 0
     return b > I64MAX - a ? I64MAX : a + b;
 }
-__device__ __forceinline__ int worse(int a, int b) { return a < b ? a : b; }
 
-template <int Q, bool MEM>
+// Per-instance shared state (dynamic shared memory of the one-warp CTA).
 struct Inst {
-    int64_t P[Q * 32];             // P[k] = sum_{i<k} c_i, padded with I64MAX past L
-    int64_t M[MEM ? Q * 32 : 1];   // same for mem
-    int32_t b[Q * 32];             // working boundaries
-    int64_t maxc;
-    int64_t cap;
-    int32_t L, n, status;
+    int64_t *P;      // [L+1] prefix sums of cost (P[k] = sum_{i<k} c_i)
+    int64_t *M;      // [L+1] prefix sums of mem (MEM only)
+    int64_t *x;      // [L+1] stage loads (or fp64 fluid scratch)
+    int32_t *b;      // [L+1] working boundaries
+    int32_t *tgt;    // [L+1] per edge: best split, -1 if not improvable
+    int32_t *pick;   // [L+1] per stage: picked edge
+    int16_t *nxt;    // [L+1] jump table
+    int L;
+    int64_t cap, maxc;
 };
 
-// Load one instance and build the prefix sums (warp 0 scan).  Reports, per
-// array, whether a value is negative and whether the exact sum exceeds
-// INT64_MAX; each kernel combines them in the oracle's check order.
+__host__ __device__ __forceinline__ size_t base_bytes(int Lmax, bool mem) {
+    const size_t Lc = (size_t)Lmax + 1;
+    const size_t raw = 8 * Lc + (mem ? 8 * Lc : 0) + 8 * Lc + 3 * 4 * Lc + 2 * Lc;
+    return (raw + 15) & ~(size_t)15;  // the fluid history (fp64) follows
+}
+
+__host__ __device__ __forceinline__ size_t solve_smem_bytes(int Lmax, bool mem, bool fluid) {
+    return base_bytes(Lmax, mem) + (fluid ? sizeof(double) * (kChunk * kRow + kChunk) : 0);
+}
+
+__device__ Inst carve(char *sm, int Lmax, bool mem) {
+    Inst s;
+    const size_t Lc = (size_t)Lmax + 1;
+    size_t o = 0;
+    s.P = (int64_t *)(sm + o); o += 8 * Lc;
+    s.M = (int64_t *)(sm + o); o += mem ? 8 * Lc : 0;
+    s.x = (int64_t *)(sm + o); o += 8 * Lc;
+    s.b = (int32_t *)(sm + o); o += 4 * Lc;
+    s.tgt = (int32_t *)(sm + o); o += 4 * Lc;
+    s.pick = (int32_t *)(sm + o); o += 4 * Lc;
+    s.nxt = (int16_t *)(sm + o);
+    s.L = 0;
+    s.cap = 0;
+    s.maxc = 0;
+    return s;
+}
+
+// ------------------------------------------------------------ prefix sums
 struct PrefixFlags {
     bool cneg, covf, mneg, movf;
 };
@@ -56,82 +89,64 @@ __device__ bool exact_sum_overflows(const int64_t *v, int L) {
     return acc > (__int128)I64MAX;
 }
 
-template <int Q, bool MEM>
-__device__ PrefixFlags load_prefix(Inst<Q, MEM> &s, const int64_t *cost, const int64_t *mem, int L) {
-    __shared__ int s_flags;
-    const int tid = threadIdx.x;
-    for (int i = tid; i < Q * 32; i += blockDim.x) {
-        s.P[i] = (i >= 1 && i <= L) ? cost[i - 1] : 0;
-        if constexpr (MEM) s.M[i] = (i >= 1 && i <= L) ? mem[i - 1] : 0;
+// Warp-wide prefix of v[0..L) into out[0..L] (out[0] = 0), saturating at
+// INT64_MAX; blocked layout, ceil(L/32) values per lane.
+__device__ void warp_prefix(const int64_t *v, int L, int64_t *out, int lane) {
+    const int Q = (L + 31) / 32;
+    const int beg = lane * Q, end = beg + Q < L ? beg + Q : L;
+    int64_t sum = 0;
+    for (int i = beg; i < end; ++i) sum = satadd(sum, v[i]);
+    int64_t ex = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(FULL, ex, o);
+        if (lane >= o) ex = satadd(ex, t);
     }
-    __syncthreads();
+    ex = __shfl_up_sync(FULL, ex, 1);
+    if (lane == 0) {
+        ex = 0;
+        out[0] = 0;
+    }
+    for (int i = beg; i < end; ++i) {
+        ex = satadd(ex, v[i]);
+        out[i + 1] = ex;
+    }
+    __syncwarp();
+}
+
+// Negative entries (checked before the sums, like the oracle) and exact
+// overflow of each array; fills s.P (and s.M), s.maxc, s.L.
+__device__ PrefixFlags load_prefix(Inst &s, const int64_t *cost, const int64_t *mem, int L, int lane) {
+    PrefixFlags f{false, false, false, false};
     int cneg = 0, mneg = 0;
-    for (int i = tid; i < Q * 32; i += blockDim.x) {
-        cneg |= s.P[i] < 0;
-        if constexpr (MEM) mneg |= s.M[i] < 0;
+    int64_t mx = 0;
+    for (int i = lane; i < L; i += 32) {
+        const int64_t c = cost[i];
+        cneg |= c < 0;
+        mx = c > mx ? c : mx;
+        if (mem) mneg |= mem[i] < 0;
     }
-    cneg = __syncthreads_or(cneg);
-    mneg = __syncthreads_or(mneg);
-    PrefixFlags f{cneg != 0, false, mneg != 0, false};
-    if (cneg || mneg) return f;  // prefix sums are not needed on an error
-    if (tid < 32) {
-        const int lane = tid;
-        int64_t vp[Q], vm[Q];
-        int64_t sp = 0, smx = 0, mx = 0;
+    f.cneg = __any_sync(FULL, cneg);
+    f.mneg = __any_sync(FULL, mneg);
 #pragma unroll
-        for (int k = 0; k < Q; ++k) {
-            const int64_t c = s.P[lane * Q + k];
-            mx = c > mx ? c : mx;
-            sp = satadd(sp, c);
-            vp[k] = sp;
-            if constexpr (MEM) {
-                smx = satadd(smx, s.M[lane * Q + k]);
-                vm[k] = smx;
-            }
-        }
-        // exclusive scan of the lane totals (saturating)
-        int64_t ep = sp, em = smx;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t tp = __shfl_up_sync(FULL, ep, o);
-            int64_t tm = 0;
-            if constexpr (MEM) tm = __shfl_up_sync(FULL, em, o);
-            if (lane >= o) {
-                ep = satadd(ep, tp);
-                if constexpr (MEM) em = satadd(em, tm);
-            }
-        }
-        ep = __shfl_up_sync(FULL, ep, 1);
-        if constexpr (MEM) em = __shfl_up_sync(FULL, em, 1);
-        if (lane == 0) {
-            ep = 0;
-            em = 0;
-        }
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-            const int pos = lane * Q + k;
-            s.P[pos] = pos <= L ? satadd(ep, vp[k]) : I64MAX;
-            if constexpr (MEM) s.M[pos] = pos <= L ? satadd(em, vm[k]) : I64MAX;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int64_t t = __shfl_xor_sync(FULL, mx, o);
-            mx = t > mx ? t : mx;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            s.maxc = mx;
-            // a saturated prefix is I64MAX: decide overflow exactly (128-bit)
-            int fl = 0;
-            if (s.P[L] == I64MAX && exact_sum_overflows(cost, L)) fl |= 1;
-            if constexpr (MEM)
-                if (s.M[L] == I64MAX && exact_sum_overflows(mem, L)) fl |= 2;
-            s_flags = fl;
-        }
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t t = __shfl_xor_sync(FULL, mx, o);
+        mx = t > mx ? t : mx;
     }
-    __syncthreads();
-    f.covf = (s_flags & 1) != 0;
-    f.movf = (s_flags & 2) != 0;
+    s.maxc = mx;
+    s.L = L;
+    if (f.cneg || f.mneg) return f;
+    warp_prefix(cost, L, s.P, lane);
+    if (mem) warp_prefix(mem, L, s.M, lane);
+    // a saturated prefix reads INT64_MAX: decide the overflow exactly
+    int fl = 0;
+    if (lane == 0) {
+        if (s.P[L] == I64MAX && exact_sum_overflows(cost, L)) fl |= 1;
+        if (mem && s.M[L] == I64MAX && exact_sum_overflows(mem, L)) fl |= 2;
+    }
+    fl = __shfl_sync(FULL, fl, 0);
+    f.covf = (fl & 1) != 0;
+    f.movf = (fl & 2) != 0;
     return f;
 }
 
@@ -144,51 +159,46 @@ __device__ __forceinline__ int prefix_status(const PrefixFlags &f, bool use_mem)
     return DYNMO_OK;
 }
 
-// Registers: lane owns prefix positions lane*Q .. lane*Q+Q-1.
-template <int Q, bool MEM>
-struct Regs {
-    int64_t p[Q];
-    int64_t m[MEM ? Q : 1];
-};
-
-template <int Q, bool MEM>
-__device__ __forceinline__ void load_regs(Regs<Q, MEM> &r, const Inst<Q, MEM> &s, int lane) {
-#pragma unroll
-    for (int k = 0; k < Q; ++k) {
-        r.p[k] = s.P[lane * Q + k];
-        if constexpr (MEM) r.m[k] = s.M[lane * Q + k];
-    }
-}
-
-// Greedy maximal jump from j under bottleneck B (warp-uniform result):
-// the largest K with P[K]-P[j] <= B and M[K]-M[j] <= cap.  Both predicates
-// are monotone in K, so K+1 = number of positions satisfying them.
-template <int Q, bool MEM>
-__device__ __forceinline__ int warp_next(const Regs<Q, MEM> &r, const Inst<Q, MEM> &s, int j,
-                                         int64_t B) {
+// --------------------------------------------------------------- greedy
+// Largest K >= j with P[K] - P[j] <= B and M[K] - M[j] <= cap (both
+// monotone in K); K == j means layer j alone does not fit.  Stages are short
+// (about L/n layers), so first test the next kWin positions with independent
+// loads (the count of passing positions is the jump, by monotonicity); only
+// if all pass, binary-search the rest.
+constexpr int kWin = 8;
+template <bool MEM>
+__device__ __forceinline__ int bs_next(const Inst &s, int j, int64_t B) {
     const int64_t t1 = satadd(s.P[j], B);
     int64_t t2 = 0;
     if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
-    unsigned c = 0;
+    int cnt = 0;
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {
-        bool ok = r.p[k] <= t1;
-        if constexpr (MEM) ok = ok && r.m[k] <= t2;
-        c += ok;
+    for (int i = 1; i <= kWin; ++i) {
+        const int p = j + i <= s.L ? j + i : s.L;
+        bool ok = j + i <= s.L && s.P[p] <= t1;
+        if constexpr (MEM) ok = ok && s.M[p] <= t2;
+        cnt += ok;
     }
-    const int K = (int)__reduce_add_sync(FULL, c) - 1;
-    return K < s.L ? K : s.L;
+    if (cnt < kWin) return j + cnt;
+    int lo = j + kWin, hi = s.L;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        bool ok = s.P[mid] <= t1;
+        if constexpr (MEM) ok = ok && s.M[mid] <= t2;
+        if (ok) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
 }
 
-// Greedy stage count under B, stopping once it exceeds `limit`
-// (returns limit+1 for "more than limit", including an unplaceable layer).
-template <int Q, bool MEM>
-__device__ int warp_greedy_count(const Regs<Q, MEM> &r, const Inst<Q, MEM> &s, int64_t B,
-                                 int limit) {
+// Greedy maximal-prefix stage count under B, stopping once it exceeds
+// `limit` (limit + 1 also for an unplaceable layer).  Per lane.
+template <bool MEM>
+__device__ int greedy_count(const Inst &s, int64_t B, int limit) {
     int j = 0, c = 0;
     while (j < s.L) {
         if (c == limit) return limit + 1;
-        const int K = warp_next<Q, MEM>(r, s, j, B);
+        const int K = bs_next<MEM>(s, j, B);
         if (K == j) return limit + 1;
         j = K;
         ++c;
@@ -196,73 +206,92 @@ __device__ int warp_greedy_count(const Regs<Q, MEM> &r, const Inst<Q, MEM> &s, i
     return c;
 }
 
-template <int Q, bool MEM>
-__device__ __forceinline__ bool warp_feasible(const Regs<Q, MEM> &r, const Inst<Q, MEM> &s,
-                                              int64_t B, int n) {
-    return warp_greedy_count<Q, MEM>(r, s, B, n) <= n;
+// Candidate c of NC per round: lo + floor(d (c+1) / (NC+1)) in 64-bit
+// arithmetic (d = a (NC+1) + r); NC+1 is a compile-time constant.
+template <int NC1>
+__device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
+    const uint64_t qa = d / (uint64_t)NC1, qr = d % (uint64_t)NC1;
+    return lo + (int64_t)(qa * (uint64_t)(c + 1) + (qr * (uint64_t)(c + 1)) / (uint64_t)NC1);
 }
 
-// Exact min-max search over B in [lo, hi] (hi feasible), all warps.
-// Returns B* (block-uniform) or -1 if infeasible (MEM only).
-template <int Q, int W, bool MEM>
-__device__ int64_t search_bottleneck(const Regs<Q, MEM> &r, Inst<Q, MEM> &s, int n) {
-    __shared__ int64_t s_lo, s_hi;
-    __shared__ int64_t s_cand[W];
-    __shared__ int s_feas[W];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+// Exact min-max search over B in [lo, hi] (hi feasible).  Every lane of the
+// NW warps tests one candidate per round with its own greedy (NC = 32 NW
+// candidates, an (NC+1)-ary search); feasibility is monotone in B, so the
+// feasible candidates form a suffix: the first feasible one is the new hi and
+// its predecessor + 1 the new lo.  Called by all NW warps; s must be fully
+// built (warp 0) and visible (__syncthreads) before.  Returns B* (uniform),
+// or -1 if no split satisfies the memory cap.
+template <bool MEM, int NW>
+__device__ int64_t search_bottleneck(const Inst &s, int n) {
+    constexpr int NC = 32 * NW;
+    __shared__ unsigned s_m[2][NW];
+    __shared__ int s_f;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = w * 32 + lane;
     const int64_t C = s.P[s.L];
     const int64_t ceil_cn = C / n + (C % n != 0);
     int64_t lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
-    int64_t hi = satadd(ceil_cn, s.maxc);
+    int64_t hi = satadd(ceil_cn, s.maxc);  // Appendix A: always feasible on cost
     if (hi > C) hi = C;
     if (lo > hi) lo = hi;
     if constexpr (MEM) {
-        // the cost bracket may be infeasible under the memory cap
-        if (w == 0) {
-            bool f = warp_feasible<Q, MEM>(r, s, hi, n);
-            if (!f) {
-                hi = C;
-                f = warp_feasible<Q, MEM>(r, s, hi, n);
-            }
-            if (lane == 0) s_hi = f ? hi : -1;
+        // the memory cap may make the cost bracket infeasible: widen to C
+        if (threadIdx.x == 0) s_f = greedy_count<MEM>(s, hi, n) <= n;
+        if (threadIdx.x == 1) s_m[1][0] = greedy_count<MEM>(s, C, n) <= n;
+        if constexpr (NW > 1) __syncthreads();
+        else __syncwarp();
+        const int fh = s_f, fc = (int)s_m[1][0];
+        if constexpr (NW > 1) __syncthreads();
+        else __syncwarp();
+        if (!fh) {
+            if (!fc) return -1;
+            hi = C;
         }
-        __syncthreads();
-        if (s_hi < 0) return -1;
-        hi = s_hi;
     }
+    int par = 0;
     while (lo < hi) {
-        const int64_t d = hi - lo;
-        const int64_t cand =
-            lo + (int64_t)(((unsigned __int128)(uint64_t)d * (unsigned)(w + 1)) / (unsigned)(W + 1));
-        const bool f = warp_feasible<Q, MEM>(r, s, cand, n);
-        if (lane == 0) {
-            s_cand[w] = cand;
-            s_feas[w] = f;
-        }
-        __syncthreads();
-        for (int k = 0; k < W; ++k) {
-            if (s_feas[k]) {
-                if (s_cand[k] < hi) hi = s_cand[k];
-            } else {
-                if (s_cand[k] + 1 > lo) lo = s_cand[k] + 1;
+        const uint64_t d = (uint64_t)(hi - lo);
+        const int64_t cand = candidate<NC + 1>(lo, d, c);
+        const bool f = greedy_count<MEM>(s, cand, n) <= n;
+        const unsigned m = __ballot_sync(FULL, f);
+        int first;
+        if constexpr (NW == 1) {
+            first = m ? __ffs(m) - 1 : NC;
+        } else {
+            if (lane == 0) s_m[par][w] = m;
+            __syncthreads();
+            first = NC;
+#pragma unroll
+            for (int k = NW - 1; k >= 0; --k) {
+                const unsigned mk = s_m[par][k];
+                if (mk) first = k * 32 + __ffs(mk) - 1;
             }
+            par ^= 1;  // double buffer: the next round writes the other half
         }
-        __syncthreads();
+        const int64_t nhi = first < NC ? candidate<NC + 1>(lo, d, first) : hi;
+        const int64_t nlo = first > 0 ? candidate<NC + 1>(lo, d, first - 1) + 1 : lo;
+        hi = nhi;
+        lo = nlo;
     }
     return hi;
 }
 
-// Lexmax boundaries for B* (Appendix A construction), warp 0; writes s.b.
-template <int Q, bool MEM>
-__device__ void warp_construct(const Regs<Q, MEM> &r, Inst<Q, MEM> &s, int64_t Bs, int n) {
-    int j = 0;
-    if ((threadIdx.x & 31) == 0) s.b[0] = 0;
-    for (int st = 0; st < n; ++st) {
-        int K = warp_next<Q, MEM>(r, s, j, Bs);
-        const int reserve = s.L - (n - 1 - st);
-        j = K < reserve ? K : reserve;
-        if ((threadIdx.x & 31) == 0) s.b[st + 1] = j;
+// Lexmax boundaries for B* (Appendix A): jump table at B* (all lanes), then
+// b_{s+1} = min(next(b_s), L - (n-1-s)) on lane 0.  Writes s.b[0..n].
+template <bool MEM>
+__device__ void construct(Inst &s, int64_t Bs, int n, int lane) {
+    for (int j = lane; j < s.L; j += 32) s.nxt[j] = (int16_t)bs_next<MEM>(s, j, Bs);
+    __syncwarp();
+    if (lane == 0) {
+        int j = 0;
+        s.b[0] = 0;
+        for (int st = 0; st < n; ++st) {
+            const int K = s.nxt[j];
+            const int reserve = s.L - (n - 1 - st);
+            j = K < reserve ? K : reserve;
+            s.b[st + 1] = j;
+        }
     }
+    __syncwarp();
 }
 
 __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
@@ -278,52 +307,49 @@ __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
     return __ddiv_rn((double)(mx - mn), mean);
 }
 
-template <bool MEM>
-__device__ __forceinline__ const int64_t *mem_ptr(const SolveArgs &a) {
-    return MEM ? a.mem : nullptr;
-}
-
 // ------------------------------------------------------------ partition
-template <int Q, int W, bool MEM>
-__global__ void __launch_bounds__(W * 32) k_partition(SolveArgs a) {
-    __shared__ Inst<Q, MEM> s;
-    const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+template <bool MEM, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    __shared__ int s_st;
+    const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    Inst s = carve(smem, a.max_layers, MEM);
     const int off = a.layer_off[q];
     const int L = a.layer_off[q + 1] - off;
     const int n = a.n_stages[q];
     int32_t *bnd = a.bnd_out + a.bnd_off[q];
     const int64_t cap = MEM ? a.cap[q] : 0;
-    int st = DYNMO_OK;
-    if (L < 1 || L > a.max_layers || L > Q * 32 - 1 || n < 1 || n > L || (MEM && cap < 0))
-        st = DYNMO_E_INVALID;
-    if (st == DYNMO_OK)
-        st = prefix_status(load_prefix<Q, MEM>(s, a.cost + off, MEM ? a.mem + off : nullptr, L), MEM);
-    if (tid == 0) {
-        s.L = L;
-        s.n = n;
-        s.cap = cap;
+    s.cap = cap;
+    s.L = L;
+    if (w == 0) {
+        int st = DYNMO_OK;
+        if (L < 1 || L > a.max_layers || n < 1 || n > L || (MEM && cap < 0)) st = DYNMO_E_INVALID;
+        if (st == DYNMO_OK)
+            st = prefix_status(load_prefix(s, a.cost + off, MEM ? a.mem + off : nullptr, L, lane), MEM);
+        if (lane == 0) s_st = st;
+        if (lane == 0) s.x[0] = s.maxc;  // share maxc with the other warps
     }
     __syncthreads();
+    int st = s_st;
+    s.maxc = s.x[0];
     int64_t Bs = -1;
-    Regs<Q, MEM> r;
     if (st == DYNMO_OK) {
-        load_regs<Q, MEM>(r, s, lane);
-        Bs = search_bottleneck<Q, W, MEM>(r, s, n);
+        Bs = search_bottleneck<MEM, NW>(s, n);
         if (Bs < 0) st = DYNMO_E_INFEASIBLE;
     }
+    if (w != 0) return;
     if (st != DYNMO_OK) {
-        for (int k = tid; k <= n && n >= 1; k += blockDim.x) bnd[k] = -1;
-        if (tid == 0) {
+        for (int k = lane; k <= n && n >= 1; k += 32) bnd[k] = -1;
+        if (lane == 0) {
             a.bottleneck[q] = -1;
             if (a.imbalance) a.imbalance[q] = -1.0;
             a.status[q] = st;
         }
         return;
     }
-    if (tid < 32) warp_construct<Q, MEM>(r, s, Bs, n);
-    __syncthreads();
-    for (int k = tid; k <= n; k += blockDim.x) bnd[k] = s.b[k];
-    if (tid == 0) {
+    construct<MEM>(s, Bs, n, lane);
+    for (int k = lane; k <= n; k += 32) bnd[k] = s.b[k];
+    if (lane == 0) {
         a.bottleneck[q] = Bs;
         if (a.imbalance) a.imbalance[q] = imbalance_of(s.P, s.b, n);
         a.status[q] = DYNMO_OK;
@@ -331,63 +357,82 @@ __global__ void __launch_bounds__(W * 32) k_partition(SolveArgs a) {
 }
 
 // -------------------------------------------------------------- repack
-template <int Q, int W, bool MEM>
-__global__ void __launch_bounds__(W * 32) k_repack(SolveArgs a) {
-    __shared__ Inst<Q, MEM> s;
-    __shared__ int s_k;
-    const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+template <bool MEM, int NW>
+__global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    __shared__ int s_st, s_k, s_code;
+    const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    Inst s = carve(smem, a.max_layers, MEM);
     const int off = a.layer_off[q];
     const int L = a.layer_off[q + 1] - off;
     const int n_cur = a.n_stages[q];
     const int fl = a.floor_[q];
     int32_t *bnd = a.bnd_out + a.bnd_off[q];
     const int64_t cap = MEM ? a.cap[q] : 0;
+    s.cap = cap;
+    s.L = L;
     const bool alg2 = a.mode == DYNMO_REPACK_ALG2;
     const int64_t bound = alg2 ? 0 : a.bound[q];
-    int st = DYNMO_OK;
-    if (L < 1 || L > a.max_layers || L > Q * 32 - 1 || n_cur < 1 || n_cur > L || fl < 1 ||
-        fl > n_cur || (MEM && cap < 0) || (!alg2 && bound < 0))
-        st = DYNMO_E_INVALID;
-    if (st == DYNMO_OK && alg2) {
-        // b_in must be a valid split
-        const int32_t *bi = a.bnd_in + a.bnd_off[q];
-        int bad = 0;
-        for (int k = tid; k < n_cur; k += blockDim.x) bad |= bi[k + 1] <= bi[k];
-        bad |= bi[0] != 0 || bi[n_cur] != L;
-        if (__syncthreads_or(bad)) st = DYNMO_E_INVALID;
-    }
-    if (st == DYNMO_OK) {
-        const PrefixFlags f = load_prefix<Q, MEM>(s, a.cost + off, MEM ? a.mem + off : nullptr, L);
-        if (alg2)  // oracle: negatives of cost and mem first, then the cost sum
-            st = (f.cneg || f.mneg) ? DYNMO_E_INVALID : f.covf ? DYNMO_E_OVERFLOW : DYNMO_OK;
-        else
-            st = prefix_status(f, MEM);
-    }
-    if (tid == 0) {
-        s.L = L;
-        s.cap = cap;
+    const int32_t *bi = alg2 ? a.bnd_in + a.bnd_off[q] : nullptr;
+    if (w == 0) {
+        int st = DYNMO_OK;
+        if (L < 1 || L > a.max_layers || n_cur < 1 || n_cur > L || fl < 1 || fl > n_cur ||
+            (MEM && cap < 0) || (!alg2 && bound < 0))
+            st = DYNMO_E_INVALID;
+        if (st == DYNMO_OK && alg2) {
+            int bad = 0;
+            for (int k = lane; k < n_cur; k += 32) bad |= bi[k + 1] <= bi[k];
+            bad |= bi[0] != 0 || bi[n_cur] != L;
+            if (__any_sync(FULL, bad)) st = DYNMO_E_INVALID;
+        }
+        if (st == DYNMO_OK) {
+            const PrefixFlags f = load_prefix(s, a.cost + off, MEM ? a.mem + off : nullptr, L, lane);
+            if (alg2)  // oracle: negatives of cost and mem first, then the cost sum
+                st = (f.cneg || f.mneg) ? DYNMO_E_INVALID : f.covf ? DYNMO_E_OVERFLOW : DYNMO_OK;
+            else
+                st = prefix_status(f, MEM);
+        }
+        int k = n_cur, code = DYNMO_OK;
+        if (st == DYNMO_OK && !alg2) {
+            // fewest workers: greedy count at B = bound (cost and mem), reading Q15
+            int g = 0;
+            if (lane == 0) g = greedy_count<MEM>(s, bound, n_cur);
+            g = __shfl_sync(FULL, g, 0);
+            if (g <= n_cur) {
+                k = g > fl ? g : fl;
+            } else {
+                k = n_cur;
+                code = DYNMO_W_BOUND_UNMET;
+            }
+        }
+        if (lane == 0) {
+            s_st = st;
+            s_k = k;
+            s_code = code;
+            s.x[0] = s.maxc;
+        }
     }
     __syncthreads();
-    auto fail = [&](int code) {
-        for (int k = tid; k <= n_cur && n_cur >= 1; k += blockDim.x) bnd[k] = -1;
-        if (tid == 0) {
+    const int st0 = s_st;
+    s.maxc = s.x[0];
+    if (st0 != DYNMO_OK) {
+        if (w != 0) return;
+        for (int k = lane; k <= n_cur && n_cur >= 1; k += 32) bnd[k] = -1;
+        if (lane == 0) {
             a.n_new[q] = -1;
             a.bottleneck[q] = -1;
-            a.status[q] = code;
+            a.status[q] = st0;
         }
-    };
-    if (st != DYNMO_OK) {
-        fail(st);
         return;
     }
     if (alg2) {
-        // Alg. 2 with the fixes of SPEC:L364/L389, serial.
-        if (tid == 0) {
-            const int32_t *bi = a.bnd_in + a.bnd_off[q];
+        if (w != 0) return;
+        // Alg. 2 with the fixes of SPEC:L364/L389, serial on lane 0
+        int k = 0;
+        if (lane == 0) {
             const int64_t *mem = MEM ? a.mem + off : nullptr;
             __int128 mu_prev = 0;  // mem of the current chain head (src)
-            int n_active = n_cur, k = 0;
-            // mu of worker 0
+            int n_active = n_cur;
             if (mem)
                 for (int i = bi[0]; i < bi[1]; ++i) mu_prev += mem[i];
             s.b[0] = 0;
@@ -397,15 +442,14 @@ __global__ void __launch_bounds__(W * 32) k_repack(SolveArgs a) {
                     for (int i = bi[src + 1]; i < bi[src + 2]; ++i) mu_dst += mem[i];
                 const bool fits = !mem || (mu_prev + mu_dst <= (__int128)cap);
                 if (fits && n_active > fl) {
-                    n_active--;                 // src deactivated, merged into dst
+                    n_active--;  // src deactivated, its layers merged into dst
                     mu_prev = mu_prev + mu_dst;
                 } else {
-                    s.b[++k] = bi[src + 1];     // src stays active
+                    s.b[++k] = bi[src + 1];  // src stays active
                     mu_prev = mu_dst;
                 }
             }
             s.b[++k] = bi[n_cur];
-            s_k = k;
             int64_t bm = 0;
             for (int t = 0; t < k; ++t) {
                 const int64_t x = s.P[s.b[t + 1]] - s.P[s.b[t]];
@@ -415,298 +459,358 @@ __global__ void __launch_bounds__(W * 32) k_repack(SolveArgs a) {
             a.bottleneck[q] = bm;
             a.status[q] = n_active > fl ? DYNMO_W_BOUND_UNMET : DYNMO_OK;
         }
-        __syncthreads();
-        for (int t = tid; t <= n_cur; t += blockDim.x) bnd[t] = t <= s_k ? s.b[t] : -1;
+        k = __shfl_sync(FULL, k, 0);
+        __syncwarp();
+        for (int t = lane; t <= n_cur; t += 32) bnd[t] = t <= k ? s.b[t] : -1;
         return;
     }
-    Regs<Q, MEM> r;
-    load_regs<Q, MEM>(r, s, lane);
-    // fewest workers: greedy count at B = bound (cost and mem), reading Q15
-    if (tid < 32) {
-        const int g = warp_greedy_count<Q, MEM>(r, s, bound, n_cur);
-        if (lane == 0) s_k = g;
-    }
-    __syncthreads();
-    const int g = s_k;
-    int k;
-    int code = DYNMO_OK;
-    if (g <= n_cur) {
-        k = g > fl ? g : fl;
-    } else {
-        k = n_cur;
-        code = DYNMO_W_BOUND_UNMET;
-    }
-    const int64_t Bs = search_bottleneck<Q, W, MEM>(r, s, k);
+    const int k = s_k;
+    const int64_t Bs = search_bottleneck<MEM, NW>(s, k);
+    if (w != 0) return;
     if (Bs < 0) {
-        fail(DYNMO_E_INFEASIBLE);
+        for (int t = lane; t <= n_cur; t += 32) bnd[t] = -1;
+        if (lane == 0) {
+            a.n_new[q] = -1;
+            a.bottleneck[q] = -1;
+            a.status[q] = DYNMO_E_INFEASIBLE;
+        }
         return;
     }
-    if (tid < 32) warp_construct<Q, MEM>(r, s, Bs, k);
-    __syncthreads();
-    for (int t = tid; t <= n_cur; t += blockDim.x) bnd[t] = t <= k ? s.b[t] : -1;
-    if (tid == 0) {
+    construct<MEM>(s, Bs, k, lane);
+    for (int t = lane; t <= n_cur; t += 32) bnd[t] = t <= k ? s.b[t] : -1;
+    if (lane == 0) {
         a.n_new[q] = k;
         a.bottleneck[q] = Bs;
-        a.status[q] = code;
+        a.status[q] = s_code;
     }
 }
 
 // ------------------------------------------------------------- diffusion
-template <int Q, int W, bool MEM>
-__global__ void __launch_bounds__(W * 32) k_diffuse(SolveArgs a) {
-    __shared__ Inst<Q, MEM> s;
-    __shared__ int64_t sx[Q * 32];
-    __shared__ int32_t s_tgt[Q * 32];  // edge e: best split j if improvable, else -1
-    __shared__ int32_t s_pick[Q * 32];
-    __shared__ double sxf[Q * 32];
-    __shared__ int64_t s_phi, s_phi0;
-    __shared__ int s_ctl, s_rounds;
-    const int q = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int off = a.layer_off[q];
-    const int L = a.layer_off[q + 1] - off;
-    const int n = a.n_stages[q];
-    const int32_t *bi = a.bnd_in + a.bnd_off[q];
+// Discrete diffusion (reading Q10), one warp: lanes are stage pairs (edges)
+// and stages; every round: loads, phi (exact, 128-bit), the best re-split of
+// every adjacent pair, max-neighbor matching, simultaneous application.
+template <bool MEM>
+__device__ void diffuse_discrete(const SolveArgs &a, Inst &s, int q, int n, const int32_t *bi,
+                                 int st, int lane) {
     int32_t *bo = a.bnd_out + a.bnd_off[q];
-    const int64_t cap = MEM ? a.cap[q] : 0;
     const int64_t gamma = a.gamma ? a.gamma[q] : 0;
-    const double gf = a.gamma_fluid ? a.gamma_fluid[q] : 0.0;
     const int maxr = a.max_rounds;
-    const bool want_fluid = a.fluid_x != nullptr;
-    // validity shared by both processes: L, n, max_rounds, b_in
-    int common = DYNMO_OK;
-    if (L < 1 || L > a.max_layers || L > Q * 32 - 1 || n < 1 || n > L || maxr < 0)
-        common = DYNMO_E_INVALID;
-    if (common == DYNMO_OK) {
-        int bad = 0;
-        for (int k = tid; k < n; k += blockDim.x) bad |= bi[k + 1] <= bi[k];
-        bad |= bi[0] != 0 || bi[n] != L;
-        if (__syncthreads_or(bad)) common = DYNMO_E_INVALID;
-    }
-    int dst = common, fst = want_fluid ? common : DYNMO_OK;
-    if (common == DYNMO_OK) {
-        if (gamma < 0 || (MEM && cap < 0)) dst = DYNMO_E_INVALID;
-        if (want_fluid && !(gf >= 0.0)) fst = DYNMO_E_INVALID;
-        const PrefixFlags f = load_prefix<Q, MEM>(s, a.cost + off, MEM ? a.mem + off : nullptr, L);
-        const int cs = f.cneg ? DYNMO_E_INVALID : f.covf ? DYNMO_E_OVERFLOW : DYNMO_OK;
-        if (fst == DYNMO_OK && want_fluid) fst = cs;
-        if (dst == DYNMO_OK) dst = prefix_status(f, MEM);
-    }
-    if (tid == 0) {
-        s.L = L;
-        s.cap = cap;
-        s_ctl = 0;
-        s_rounds = 0;
-    }
-    __syncthreads();
-
-    // ---------------- discrete diffusion (reading Q10)
-    if (dst == DYNMO_OK) {
-        for (int k = tid; k <= n; k += blockDim.x) s.b[k] = bi[k];
-        __syncthreads();
+    const int64_t cap = s.cap;
+    int rounds = 0;
+    int64_t phi = 0, phi0 = 0;
+    if (st == DYNMO_OK) {
+        for (int k = lane; k <= n; k += 32) s.b[k] = bi[k];
+        __syncwarp();
+        int ctl = 0;  // 1 stop OK, 2 stop NOT_CONVERGED, < 0 error
         for (;;) {
-            for (int t = tid; t < n; t += blockDim.x) sx[t] = s.P[s.b[t + 1]] - s.P[s.b[t]];
-            __syncthreads();
+            for (int t = lane; t < n; t += 32) s.x[t] = s.P[s.b[t + 1]] - s.P[s.b[t]];
+            __syncwarp();
             // phi = sum_{u<v} |x_u - x_v| (reading Q12), exact in 128 bits
-            if (tid < 32) {
-                __int128 acc = 0;
-                for (int u = lane; u < n; u += 32)
-                    for (int v = u + 1; v < n; ++v) {
-                        const int64_t d = sx[u] > sx[v] ? sx[u] - sx[v] : sx[v] - sx[u];
-                        acc += d;
-                    }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const uint64_t lo = (uint64_t)acc, hi = (uint64_t)(acc >> 64);
-                    const uint64_t olo = __shfl_xor_sync(FULL, lo, o);
-                    const uint64_t ohi = __shfl_xor_sync(FULL, hi, o);
-                    acc += (__int128)(((unsigned __int128)ohi << 64) | olo);
-                }
-                if (lane == 0) {
-                    if (acc > (__int128)I64MAX) {
-                        s_ctl = DYNMO_E_OVERFLOW;
-                    } else {
-                        s_phi = (int64_t)acc;
-                        if (s_rounds == 0) s_phi0 = (int64_t)acc;
-                        s_ctl = (int64_t)acc <= gamma ? 1 : 0;
-                    }
+            __int128 acc = 0;
+            for (int u = lane; u < n; u += 32) {
+                const int64_t xu = s.x[u];
+                for (int v = u + 1; v < n; ++v) {
+                    const int64_t xv = s.x[v];
+                    acc += xu > xv ? xu - xv : xv - xu;
                 }
             }
-            __syncthreads();
-            if (s_ctl != 0) break;
-            // best re-split of every adjacent pair: min (pair max, |j - b|, j)
-            for (int e = w; e + 1 < n; e += W) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t lo = (uint64_t)acc, hi = (uint64_t)(acc >> 64);
+                const uint64_t olo = __shfl_xor_sync(FULL, lo, o);
+                const uint64_t ohi = __shfl_xor_sync(FULL, hi, o);
+                acc += (__int128)(((unsigned __int128)ohi << 64) | olo);
+            }
+            if (acc > (__int128)I64MAX) {
+                ctl = DYNMO_E_OVERFLOW;
+                break;
+            }
+            phi = (int64_t)acc;
+            if (rounds == 0) phi0 = phi;
+            if (phi <= gamma) {
+                ctl = 1;
+                break;
+            }
+            // best re-split of edge e: min of (pair max, |j - b|, j) over
+            // mem-feasible j in (b_e, b_{e+2}); lane = edge
+            int any = 0;
+            for (int e = lane; e + 1 < n; e += 32) {
                 const int lo = s.b[e], hi = s.b[e + 2], cur = s.b[e + 1];
+                const int64_t Plo = s.P[lo], Phi = s.P[hi];
                 int64_t km = I64MAX;
-                int kd = INT32_MAX, kj = INT32_MAX, found = 0;
-                for (int j = lo + 1 + lane; j < hi; j += 32) {
+                int kd = 0, kj = -1;
+                for (int j = lo + 1; j < hi; ++j) {
                     if constexpr (MEM)
                         if (s.M[j] - s.M[lo] > cap || s.M[hi] - s.M[j] > cap) continue;
-                    const int64_t l = s.P[j] - s.P[lo], rr = s.P[hi] - s.P[j];
-                    const int64_t m = l > rr ? l : rr;
+                    const int64_t l = s.P[j] - Plo, r = Phi - s.P[j];
+                    const int64_t m = l > r ? l : r;
                     const int d = j > cur ? j - cur : cur - j;
-                    if (!found || m < km || (m == km && (d < kd || (d == kd && j < kj)))) {
-                        found = 1;
+                    // j ascending, so equal (max, dist) keeps the lower j
+                    if (kj < 0 || m < km || (m == km && d < kd)) {
                         km = m;
                         kd = d;
                         kj = j;
                     }
                 }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const int64_t om = __shfl_xor_sync(FULL, km, o);
-                    const int od = __shfl_xor_sync(FULL, kd, o);
-                    const int oj = __shfl_xor_sync(FULL, kj, o);
-                    const int of = __shfl_xor_sync(FULL, found, o);
-                    const bool take = of && (!found || om < km ||
-                                             (om == km && (od < kd || (od == kd && oj < kj))));
-                    if (take) {
-                        km = om;
-                        kd = od;
-                        kj = oj;
-                        found = 1;
+                const int64_t pm = s.x[e] > s.x[e + 1] ? s.x[e] : s.x[e + 1];
+                const int t = (kj >= 0 && km < pm) ? kj : -1;
+                s.tgt[e] = t;
+                any |= t >= 0;
+            }
+            any = __any_sync(FULL, any);
+            if (!any) {
+                ctl = 1;
+                break;
+            }
+            if (rounds == maxr) {
+                ctl = 2;
+                break;
+            }
+            __syncwarp();
+            // max-neighbor matching: stage t picks its improvable
+            // incident edge with the largest gap (ties: lower edge index)
+            for (int t = lane; t < n; t += 32) {
+                int pk = -1;
+                int64_t best = -1;
+                for (int e = t - 1; e <= t; ++e) {
+                    if (e < 0 || e + 1 >= n || s.tgt[e] < 0) continue;
+                    const int64_t g = s.x[e] > s.x[e + 1] ? s.x[e] - s.x[e + 1] : s.x[e + 1] - s.x[e];
+                    if (g > best) {
+                        best = g;
+                        pk = e;
                     }
                 }
-                if (lane == 0) {
-                    const int64_t pm = sx[e] > sx[e + 1] ? sx[e] : sx[e + 1];
-                    s_tgt[e] = (found && km < pm) ? kj : -1;
-                }
+                s.pick[t] = pk;
             }
-            __syncthreads();
-            if (tid == 0) {
-                int any = 0;
-                for (int e = 0; e + 1 < n; ++e) any |= s_tgt[e] >= 0;
-                if (!any) {
-                    s_ctl = 1;
-                } else if (s_rounds == maxr) {
-                    s_ctl = 2;
-                } else {
-                    // max-neighbor matching: each stage picks its
-                    // improvable incident edge with the largest gap
-                    for (int t = 0; t < n; ++t) {
-                        int pick = -1;
-                        int64_t best = -1;
-                        for (int e = t - 1; e <= t; ++e) {
-                            if (e < 0 || e + 1 >= n || s_tgt[e] < 0) continue;
-                            const int64_t g = sx[e] > sx[e + 1] ? sx[e] - sx[e + 1] : sx[e + 1] - sx[e];
-                            if (g > best) {
-                                best = g;
-                                pick = e;
-                            }
-                        }
-                        s_pick[t] = pick;
-                    }
-                    for (int e = 0; e + 1 < n; ++e)
-                        if (s_tgt[e] >= 0 && s_pick[e] == e && s_pick[e + 1] == e) s.b[e + 1] = s_tgt[e];
-                    s_rounds++;
-                }
-            }
-            __syncthreads();
-            if (s_ctl != 0) break;
+            __syncwarp();
+            for (int e = lane; e + 1 < n; e += 32)
+                if (s.tgt[e] >= 0 && s.pick[e] == e && s.pick[e + 1] == e) s.b[e + 1] = s.tgt[e];
+            __syncwarp();
+            rounds++;
         }
-        if (s_ctl < 0) dst = s_ctl;
-        else if (s_ctl == 2) dst = DYNMO_W_NOT_CONVERGED;
+        if (ctl < 0) st = ctl;
+        else if (ctl == 2) st = DYNMO_W_NOT_CONVERGED;
     }
-    if (dst < 0) {
-        for (int k = tid; k <= n && n >= 1; k += blockDim.x) bo[k] = -1;
-        if (tid == 0) {
+    if (st < 0) {
+        for (int k = lane; k <= n && n >= 1; k += 32) bo[k] = -1;
+        if (lane == 0) {
             if (a.rounds) a.rounds[q] = -1;
             if (a.phi) a.phi[q] = -1;
             if (a.phi0) a.phi0[q] = -1;
         }
     } else {
-        for (int k = tid; k <= n; k += blockDim.x) bo[k] = s.b[k];
-        if (tid == 0) {
-            if (a.rounds) a.rounds[q] = s_rounds;
-            if (a.phi) a.phi[q] = s_phi;
-            if (a.phi0) a.phi0[q] = s_phi0;
+        for (int k = lane; k <= n; k += 32) bo[k] = s.b[k];
+        if (lane == 0) {
+            if (a.rounds) a.rounds[q] = rounds;
+            if (a.phi) a.phi[q] = phi;
+            if (a.phi0) a.phi0[q] = phi0;
         }
     }
+    if (lane == 0) a.status[q] = st;
+}
 
-    // ---------------- fluid process of Lemma 2's proof
-    if (want_fluid) {
-        double *xo = a.fluid_x + (a.bnd_off[q] - q);
-        if (fst < 0) {
-            for (int k = tid; k < n; k += blockDim.x) xo[k] = -1.0;
-            if (tid == 0) {
-                if (a.fluid_rounds) a.fluid_rounds[q] = -1;
-                if (a.fluid_phi) a.fluid_phi[q] = -1.0;
-            }
-        } else if (tid == 0) {
-            for (int t = 0; t < n; ++t) sxf[t] = (double)(s.P[bi[t + 1]] - s.P[bi[t]]);
-            int rr = 0;
-            double ph;
-            for (;;) {
-                ph = 0.0;
-                for (int u = 0; u < n; ++u)
-                    for (int v = u + 1; v < n; ++v) ph = __dadd_rn(ph, fabs(__dsub_rn(sxf[u], sxf[v])));
-                if (ph <= gf) break;
-                if (rr == maxr) {
-                    fst = DYNMO_W_NOT_CONVERGED;
-                    break;
-                }
-                for (int t = 0; t < n; ++t) {
-                    int pick = -1;
-                    double best = 0.0;
-                    for (int e = t - 1; e <= t; ++e) {
-                        if (e < 0 || e + 1 >= n) continue;
-                        const double g = fabs(__dsub_rn(sxf[e], sxf[e + 1]));
-                        if (g > best) {
-                            best = g;
-                            pick = e;
-                        }
+// Fluid process of Lemma 2's proof, exact per round, one warp
+// with lane s holding x_s (n <= 32).  A round: each stage picks its incident
+// edge with the largest gap > 0 (ties: lower edge index); mutually picked
+// pairs set both ends to (x_e + x_{e+1}) * 0.5 (neighbours via shuffles).
+// Speculative chunks of 1, 4, 16, 32, 32, ... rounds: the warp advances the
+// chunk storing every x(r), then lane k evaluates phi_f(x(base + k)) (the
+// oracle's ascending (u, v) sum); the first r with phi_f <= gamma_f, or
+// r == max_rounds, stops with x(r).
+__device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf, int maxr,
+                             double *hist, double *xo, int &rr, double &ph, int &fst, int lane) {
+    double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
+    int size = 1;
+    for (int base = 0;; base += size, size = size < kChunk / 4 ? size * 4 : kChunk) {
+        for (int k = 0; k < size; ++k) {
+            if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
+            const double xl = __shfl_up_sync(FULL, x, 1);
+            const double xr = __shfl_down_sync(FULL, x, 1);
+            int pick = -1;
+            double best = 0.0;
+            if (lane < n) {
+                if (lane >= 1) {
+                    const double g = fabs(__dsub_rn(xl, x));  // edge lane-1
+                    if (g > best) {
+                        best = g;
+                        pick = lane - 1;
                     }
-                    s_pick[t] = pick;
                 }
-                for (int e = 0; e + 1 < n; ++e)
-                    if (s_pick[e] == e && s_pick[e + 1] == e) {
-                        const double avg = __dmul_rn(__dadd_rn(sxf[e], sxf[e + 1]), 0.5);
-                        sxf[e] = avg;
-                        sxf[e + 1] = avg;
+                if (lane + 1 < n) {
+                    const double g = fabs(__dsub_rn(x, xr));  // edge lane
+                    if (g > best) {
+                        best = g;
+                        pick = lane;
                     }
-                rr++;
+                }
             }
-            for (int t = 0; t < n; ++t) xo[t] = sxf[t];
-            if (a.fluid_rounds) a.fluid_rounds[q] = rr;
-            if (a.fluid_phi) a.fluid_phi[q] = ph;
+            const int pr = __shfl_down_sync(FULL, pick, 1);
+            const int pl = __shfl_up_sync(FULL, pick, 1);
+            if (lane + 1 < n && pick == lane && pr == lane) x = __dmul_rn(__dadd_rn(x, xr), 0.5);
+            else if (lane >= 1 && lane < n && pick == lane - 1 && pl == lane - 1)
+                x = __dmul_rn(__dadd_rn(xl, x), 0.5);
         }
+        __syncwarp();
+        double acc = 0.0;
+        if (lane < size) {
+            const double *row = hist + lane * kRow;
+            for (int u = 0; u < n; ++u) {
+                const double xu = row[u];
+                for (int v = u + 1; v < n; ++v) acc = __dadd_rn(acc, fabs(__dsub_rn(xu, row[v])));
+            }
+        }
+        const bool stop = lane < size && (acc <= gf || base + lane == maxr);
+        const unsigned m = __ballot_sync(FULL, stop);
+        if (m) {
+            const int k = __ffs(m) - 1;
+            rr = base + k;
+            ph = __shfl_sync(FULL, acc, k);
+            if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
+            if (lane < n) xo[lane] = hist[k * kRow + lane];
+            return;
+        }
+        __syncwarp();
     }
-    if (tid == 0) {  // thread 0 ran the fluid loop, so its fst is final
-        a.status[q] = (dst < 0 || fst < 0) ? worse(dst, fst) : (dst > fst ? dst : fst);
+}
+
+__device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, const int32_t *bi,
+                              int fst, double *hist, int lane) {
+    const double gf = a.gamma_fluid ? a.gamma_fluid[q] : 0.0;
+    const int maxr = a.max_rounds;
+    double *xo = a.fluid_x + (a.bnd_off[q] - q);
+    if (fst < 0) {
+        for (int k = lane; k < n; k += 32) xo[k] = -1.0;
+        if (lane == 0) {
+            if (a.fluid_rounds) a.fluid_rounds[q] = -1;
+            if (a.fluid_phi) a.fluid_phi[q] = -1.0;
+            if (a.fluid_status) a.fluid_status[q] = fst;
+        }
+        return;
     }
+    int rr = 0;
+    double ph = 0.0;
+    if (n <= 32) {
+        fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+    } else if (lane == 0) {
+        // n > 32: serial on lane 0 over shared memory (s.x reused as fp64)
+        double *sxf = reinterpret_cast<double *>(s.x);
+        int32_t *pk = s.pick;
+        for (int t = 0; t < n; ++t) sxf[t] = (double)(s.P[bi[t + 1]] - s.P[bi[t]]);
+        for (;;) {
+            ph = 0.0;
+            for (int u = 0; u < n; ++u)
+                for (int v = u + 1; v < n; ++v) ph = __dadd_rn(ph, fabs(__dsub_rn(sxf[u], sxf[v])));
+            if (ph <= gf) break;
+            if (rr == maxr) {
+                fst = DYNMO_W_NOT_CONVERGED;
+                break;
+            }
+            for (int t = 0; t < n; ++t) {
+                int p = -1;
+                double best = 0.0;
+                for (int e = t - 1; e <= t; ++e) {
+                    if (e < 0 || e + 1 >= n) continue;
+                    const double g = fabs(__dsub_rn(sxf[e], sxf[e + 1]));
+                    if (g > best) {
+                        best = g;
+                        p = e;
+                    }
+                }
+                pk[t] = p;
+            }
+            for (int e = 0; e + 1 < n; ++e)
+                if (pk[e] == e && pk[e + 1] == e) {
+                    const double avg = __dmul_rn(__dadd_rn(sxf[e], sxf[e + 1]), 0.5);
+                    sxf[e] = avg;
+                    sxf[e + 1] = avg;
+                }
+            rr++;
+        }
+        for (int t = 0; t < n; ++t) xo[t] = sxf[t];
+    }
+    if (lane == 0) {
+        if (a.fluid_rounds) a.fluid_rounds[q] = rr;
+        if (a.fluid_phi) a.fluid_phi[q] = ph;
+        if (a.fluid_status) a.fluid_status[q] = fst;
+    }
+}
+
+template <bool MEM>
+__global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    const int q = blockIdx.x, lane = threadIdx.x;
+    const bool fluid = blockIdx.y == 1;
+    Inst s = carve(smem, a.max_layers, MEM && !fluid);
+    const int off = a.layer_off[q];
+    const int L = a.layer_off[q + 1] - off;
+    const int n = a.n_stages[q];
+    const int32_t *bi = a.bnd_in + a.bnd_off[q];
+    const int64_t cap = MEM ? a.cap[q] : 0;
+    s.cap = cap;
+    // validity shared by both processes: L, n, max_rounds, b_in
+    int st = DYNMO_OK;
+    if (L < 1 || L > a.max_layers || n < 1 || n > L || a.max_rounds < 0) st = DYNMO_E_INVALID;
+    if (st == DYNMO_OK) {
+        int bad = 0;
+        for (int k = lane; k < n; k += 32) bad |= bi[k + 1] <= bi[k];
+        bad |= bi[0] != 0 || bi[n] != L;
+        if (__any_sync(FULL, bad)) st = DYNMO_E_INVALID;
+    }
+    if (fluid) {
+        const double gf = a.gamma_fluid ? a.gamma_fluid[q] : 0.0;
+        if (st == DYNMO_OK && !(gf >= 0.0)) st = DYNMO_E_INVALID;
+        if (st == DYNMO_OK) {  // the fluid process reads only the costs
+            const PrefixFlags f = load_prefix(s, a.cost + off, nullptr, L, lane);
+            st = f.cneg ? DYNMO_E_INVALID : f.covf ? DYNMO_E_OVERFLOW : DYNMO_OK;
+        }
+        double *hist = reinterpret_cast<double *>(smem + base_bytes(a.max_layers, false));
+        diffuse_fluid(a, s, q, n, bi, st, hist, lane);
+        return;
+    }
+    const int64_t gamma = a.gamma ? a.gamma[q] : 0;
+    if (st == DYNMO_OK && (gamma < 0 || (MEM && cap < 0))) st = DYNMO_E_INVALID;
+    if (st == DYNMO_OK)
+        st = prefix_status(load_prefix(s, a.cost + off, MEM ? a.mem + off : nullptr, L, lane), MEM);
+    diffuse_discrete<MEM>(a, s, q, n, bi, st, lane);
 }
 
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-#define DYNMO_DISPATCH(KERNEL, a, s)                                                      \
-    do {                                                                                  \
-        const bool mem_ = (a).mem != nullptr;                                             \
-        const int ml_ = (a).max_layers;                                                   \
-        if (ml_ <= 63) {                                                                  \
-            if (mem_) KERNEL<2, 16, true><<<(a).n_inst, 512, 0, s>>>(a);                  \
-            else KERNEL<2, 16, false><<<(a).n_inst, 512, 0, s>>>(a);                      \
-        } else if (ml_ <= 127) {                                                          \
-            if (mem_) KERNEL<4, 16, true><<<(a).n_inst, 512, 0, s>>>(a);                  \
-            else KERNEL<4, 16, false><<<(a).n_inst, 512, 0, s>>>(a);                      \
-        } else if (ml_ <= 255) {                                                          \
-            if (mem_) KERNEL<8, 16, true><<<(a).n_inst, 512, 0, s>>>(a);                  \
-            else KERNEL<8, 16, false><<<(a).n_inst, 512, 0, s>>>(a);                      \
-        } else {                                                                          \
-            if (mem_) KERNEL<32, 8, true><<<(a).n_inst, 256, 0, s>>>(a);                  \
-            else KERNEL<32, 8, false><<<(a).n_inst, 256, 0, s>>>(a);                      \
-        }                                                                                 \
-    } while (0)
+// Small batches (the per-step hot path): 4 warps per instance search 128
+// candidates per round.  Large batches: 1 warp per instance (one wave).
+static bool latency_mode(const SolveArgs &a) { return a.n_inst <= 4 * 148; }
 
 cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s) {
-    DYNMO_DISPATCH(k_partition, a, s);
+    const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
+    const bool lm = latency_mode(a);
+    if (a.mem) {
+        if (lm) k_partition<true, 4><<<a.n_inst, 128, sm, s>>>(a);
+        else k_partition<true, 1><<<a.n_inst, 32, sm, s>>>(a);
+    } else {
+        if (lm) k_partition<false, 4><<<a.n_inst, 128, sm, s>>>(a);
+        else k_partition<false, 1><<<a.n_inst, 32, sm, s>>>(a);
+    }
     return cudaGetLastError();
 }
 cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s) {
-    DYNMO_DISPATCH(k_diffuse, a, s);
+    const bool fl = a.fluid_x != nullptr;
+    const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, fl);
+    const dim3 grid(a.n_inst, fl ? 2 : 1);
+    if (a.mem) k_diffuse<true><<<grid, 32, sm, s>>>(a);
+    else k_diffuse<false><<<grid, 32, sm, s>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s) {
-    DYNMO_DISPATCH(k_repack, a, s);
+    const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
+    const bool lm = latency_mode(a);
+    if (a.mem) {
+        if (lm) k_repack<true, 4><<<a.n_inst, 128, sm, s>>>(a);
+        else k_repack<true, 1><<<a.n_inst, 32, sm, s>>>(a);
+    } else {
+        if (lm) k_repack<false, 4><<<a.n_inst, 128, sm, s>>>(a);
+        else k_repack<false, 1><<<a.n_inst, 32, sm, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ from ._lib import lib
 __all__ = [
     "DynmoError", "Context", "ProfilePlan", "SegmentSpec", "Batch", "coef_tensor",
     "profile_layers", "partition_stages", "diffuse_balance", "repack_workers",
-    "migrate_layers", "migration_plan",
+    "migrate_layers", "migration_plan", "Migrator",
 ]
 
 
@@ -87,6 +87,22 @@ class Context:
     @property
     def handle(self):
         return self._h
+
+    def set_timing(self, enable: bool = True):
+        _check(lib().dynmo_ctx_set_timing(self._h, int(enable)), "dynmo_ctx_set_timing")
+
+    def timing_poll(self):
+        """Fold the phase events of the last graph replay into the accumulators."""
+        _check(lib().dynmo_ctx_timing_poll(self._h), "timing_poll")
+
+    def timing_read(self) -> dict:
+        """{phase: (total_ms, launches)} since the last read (waits on events)."""
+        out = {}
+        for i, name in enumerate(_L.PHASES):
+            ms, cnt = C.c_double(0.0), C.c_int64(0)
+            _check(lib().dynmo_ctx_timing_read(self._h, i, C.byref(ms), C.byref(cnt)), "timing_read")
+            out[name] = (ms.value, cnt.value)
+        return out
 
     def close(self):
         if getattr(self, "_h", None):
@@ -230,7 +246,7 @@ def diffuse_balance(ctx: Context, batch: Batch, cost: torch.Tensor, bnd_in: torc
                     fluid: bool = True, out: Optional[dict] = None, stream=None):
     """Call 3.  Returns a dict of output tensors."""
     dev = cost.device
-    o = dict(out or {})
+    o = out if out is not None else {}  # filled in place
     o.setdefault("bnd", torch.empty(batch.total_bnd, dtype=torch.int32, device=dev))
     o.setdefault("rounds", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
     o.setdefault("phi", torch.empty(batch.n_inst, dtype=torch.int64, device=dev))
@@ -240,12 +256,13 @@ def diffuse_balance(ctx: Context, batch: Batch, cost: torch.Tensor, bnd_in: torc
         o.setdefault("fluid_x", torch.empty(max(1, batch.total_bnd - batch.n_inst), dtype=torch.float64, device=dev))
         o.setdefault("fluid_rounds", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
         o.setdefault("fluid_phi", torch.empty(batch.n_inst, dtype=torch.float64, device=dev))
+        o.setdefault("fluid_status", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
     _check(lib().dynmo_diffuse_balance(
         ctx.handle, batch.n_inst, batch.max_layers, _ptr(cost), _ptr(mem), _ptr(batch.layer_off),
         _ptr(batch.n_stages), _ptr(cap), _ptr(batch.bnd_off), _ptr(bnd_in), _ptr(gamma),
         _ptr(gamma_fluid), int(max_rounds), _ptr(o["bnd"]), _ptr(o["rounds"]), _ptr(o["phi"]),
         _ptr(o["phi0"]), _ptr(o.get("fluid_x")), _ptr(o.get("fluid_rounds")), _ptr(o.get("fluid_phi")),
-        _ptr(o["status"]), _stream(stream)), "dynmo_diffuse_balance")
+        _ptr(o.get("fluid_status")), _ptr(o["status"]), _stream(stream)), "dynmo_diffuse_balance")
     return o
 
 
@@ -254,7 +271,7 @@ def repack_workers(ctx: Context, batch: Batch, cost: torch.Tensor, *, floor: tor
                    cap=None, bnd_in=None, out: Optional[dict] = None, stream=None):
     """Call 4.  batch.stages = n_cur.  Returns a dict of output tensors."""
     dev = cost.device
-    o = dict(out or {})
+    o = out if out is not None else {}  # filled in place
     o.setdefault("n_new", torch.empty(batch.n_inst, dtype=torch.int32, device=dev))
     o.setdefault("bnd", torch.empty(batch.total_bnd, dtype=torch.int32, device=dev))
     o.setdefault("bottleneck", torch.empty(batch.n_inst, dtype=torch.int64, device=dev))
@@ -298,3 +315,29 @@ def migrate_layers(ctx: Context, n_layers: int, bnd_old, rank_old, bnd_new, rank
                                       tab_s, tab_r, int(n_bufs), C.byref(sent), C.byref(rec),
                                       _stream(stream)), "dynmo_migrate_layers")
     return sent.value, rec.value
+
+
+class Migrator:
+    """Call 5 with the buffer tables built once (per-step cost: one C call).
+    send/recv map layer -> list of device tensors, as for migrate_layers."""
+
+    def __init__(self, ctx: Context, n_layers: int, send: dict, recv: dict, n_bufs: int = 1):
+        self.ctx, self.n_layers, self.n_bufs = ctx, int(n_layers), int(n_bufs)
+        self._tab_s = (_L.Buf * max(1, n_layers * n_bufs))()
+        self._tab_r = (_L.Buf * max(1, n_layers * n_bufs))()
+        self._keep = []
+        for tab, d in ((self._tab_s, send), (self._tab_r, recv)):
+            for layer, bufs in d.items():
+                for k, t in enumerate(bufs):
+                    tab[layer * n_bufs + k] = _L.Buf(t.data_ptr(), t.numel() * t.element_size())
+                    self._keep.append(t)
+        self._sent, self._rec = C.c_int64(0), C.c_int64(0)
+
+    def __call__(self, bnd_old, rank_old, bnd_new, rank_new, stream=None):
+        bo, ro = np.ascontiguousarray(bnd_old, np.int32), np.ascontiguousarray(rank_old, np.int32)
+        bn, rn = np.ascontiguousarray(bnd_new, np.int32), np.ascontiguousarray(rank_new, np.int32)
+        _check(lib().dynmo_migrate_layers(self.ctx.handle, self.n_layers, len(bo) - 1, bo.ctypes.data,
+                                          ro.ctypes.data, len(bn) - 1, bn.ctypes.data, rn.ctypes.data,
+                                          self._tab_s, self._tab_r, self.n_bufs, C.byref(self._sent),
+                                          C.byref(self._rec), _stream(stream)), "dynmo_migrate_layers")
+        return self._sent.value, self._rec.value

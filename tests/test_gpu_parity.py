@@ -437,9 +437,9 @@ def _check_diffuse(D, ctx, insts, with_mem, max_rounds):
         dst, db, dr, dphi, dphi0 = oracle.diffuse(x["cost"], x["bnd_in"], x.get("gamma", 0), max_rounds,
                                                   mem=x["mem"] if with_mem else None, cap=x["cap"])
         fst, fx, fr, fphi = oracle.diffuse_fluid(x["cost"], x["bnd_in"], x.get("gamma_f", 0.0), max_rounds)
-        want_st = min(dst, fst) if (dst < 0 or fst < 0) else max(dst, fst)
         lo = b.bnd_off_h[q]
-        assert o["status"][q] == want_st, (q, o["status"][q], dst, fst)
+        assert o["status"][q] == dst, (q, o["status"][q], dst)
+        assert o["fluid_status"][q] == fst, (q, o["fluid_status"][q], fst)
         assert np.array_equal(o["bnd"][lo:lo + n + 1], db), q
         assert (o["rounds"][q], o["phi"][q], o["phi0"][q]) == (dr, dphi, dphi0), q
         gx = o["fluid_x"][lo - q:lo - q + n]
