@@ -1,0 +1,106 @@
+"""Multi-GPU parity worker (run under torchrun, one rank per GPU).
+
+Each rank profiles only the layers of its own stages (stage s on GPU
+floor(s*G/n)), the library all-gathers the cost slots over NCCL, every rank
+solves the identical partition, and migrate_layers moves the payload of every
+layer whose GPU changes.  Checked against the oracle on the full model:
+  - the gathered cost vector == the single-host oracle costs (O3),
+  - identical boundaries on every rank == oracle partition,
+  - every received payload byte == the sender's deterministic pattern, and
+    the byte counts == the oracle's migration plan (O7).
+Prints "MGPU_OK <rank>" on success.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2505_14864_b200 import _lib as LB  # noqa: E402
+from paper_2505_14864_b200 import dynmo as D  # noqa: E402
+from paper_2505_14864_b200.pipeline import rank_layers, stage_ranks, uniform_split  # noqa: E402
+
+
+def pattern(layer: int, nbytes: int) -> torch.Tensor:
+    g = np.random.default_rng(1000 + layer)
+    return torch.from_numpy(g.integers(0, 256, nbytes, dtype=np.uint8))
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctx = D.Context(local)
+    assert ctx.nranks == world
+    shape = synth.GPTShape(L=24, h=128)
+    n = 8
+    b_old = uniform_split(shape.L, n)
+    ranks = stage_ranks(n, world)
+    begin, count = rank_layers(b_old, ranks, rank)
+    p = synth.cfg2_keep_probs(shape, 0.9, 4)
+    segs, keep = [], []
+    want_all = np.zeros(shape.L, np.int64)
+    for layer in range(shape.L):
+        for m in synth.cfg2_layer_masks_u8(shape, layer, p[layer], 4):
+            want_all[layer] += oracle.count_nz_u8(m)
+            if begin <= layer < begin + count:
+                t = torch.from_numpy(m.reshape(-1)).to(dev)
+                keep.append(t)
+                segs.append(D.SegmentSpec(t, LB.SRC_MASK_U8, layer))
+    want_cost = np.array([oracle.layer_cost(nnz=int(v), A=0, B=1)[1] for v in want_all])
+    payload = (synth.cfg2_payload_bytes(shape, p) // 64).astype(np.int64)  # smaller transfers
+    plan = D.ProfilePlan(ctx, segs, begin, count, n_total=shape.L, exchange=world > 1)
+    coef = D.coef_tensor(count, A=0, B=1, device=dev)
+    mem_local = torch.from_numpy(payload[begin:begin + count].copy()).to(dev)
+    mem = torch.empty(shape.L, dtype=torch.int64, device=dev)
+    cost, _, st = D.profile_layers(ctx, plan, coef, mem_local=mem_local, mem=mem)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0, st
+    assert np.array_equal(cost.cpu().numpy(), want_cost), (rank, cost.cpu().numpy(), want_cost)
+    assert np.array_equal(mem.cpu().numpy(), payload)
+    # identical partition on every rank == oracle
+    b = D.Batch([shape.L], [n], device=dev)
+    bnd, bott, _, pst = D.partition_stages(ctx, b, cost)
+    ost, ob, oB, _ = oracle.partition(want_cost, n)
+    b_new = bnd.cpu().numpy()
+    assert int(pst.item()) == 0 and np.array_equal(b_new, ob) and int(bott.item()) == oB
+    allb = [None] * world
+    dist.all_gather_object(allb, b_new.tolist())
+    assert all(x == allb[0] for x in allb)
+    # migration: senders hold the pattern, receivers get it
+    send = {l: [pattern(l, int(payload[l])).to(dev)] for l in range(begin, begin + count)}
+    moves = oracle.moves(shape.L, b_old, ranks, b_new, ranks)
+    assert np.array_equal(D.migration_plan(shape.L, b_old, ranks, b_new, ranks), moves)
+    recv = {int(l): [torch.zeros(int(payload[l]), dtype=torch.uint8, device=dev)]
+            for l, s_, d_ in moves if d_ == rank}
+    sent, got = D.migrate_layers(ctx, shape.L, b_old, ranks, b_new, ranks, send, recv)
+    torch.cuda.synchronize()
+    want_sent = int(sum(payload[l] for l, s_, d_ in moves if s_ == rank))
+    want_got = int(sum(payload[l] for l, s_, d_ in moves if d_ == rank))
+    assert (sent, got) == (want_sent, want_got), (rank, sent, got, want_sent, want_got)
+    for l, bufs in recv.items():
+        assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l)
+    # second round-trip of the same plan (steady state) still exact
+    for bufs in recv.values():
+        bufs[0].zero_()
+    D.migrate_layers(ctx, shape.L, b_old, ranks, b_new, ranks, send, recv)
+    torch.cuda.synchronize()
+    for l, bufs in recv.items():
+        assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l])))
+    dist.barrier()
+    print(f"MGPU_OK {rank} layers[{begin},{begin + count}) moves={len(moves)} sent={sent} recv={got}", flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

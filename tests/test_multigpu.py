@@ -1,0 +1,24 @@
+"""Multi-GPU parity through torchrun (real NCCL over NVLink): needs >= 2 GPUs."""
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                    reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 4])
+def test_exchange_and_migration(world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
+           os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    ok = [l for l in r.stdout.splitlines() if l.startswith("MGPU_OK")]
+    assert r.returncode == 0 and len(ok) == world, r.stdout[-3000:] + r.stderr[-3000:]
