@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--migrate", choices=["p2p", "nccl"], default="p2p",
+                    help="layer migration over NVLink peer memory (default) or NCCL send/recv")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every call eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -328,7 +330,8 @@ def run_dynmo(args):
     for layer, src, dst in moves:
         if dst == rank:
             recv[int(layer)] = [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
-    migrator = D.Migrator(ctx, L, send, recv)
+    migrator = (D.PeerMigrator(ctx, L, send, recv) if G > 1 and args.migrate == "p2p"
+                else D.Migrator(ctx, L, send, recv))
 
     def step():
         r = solve()

@@ -313,6 +313,34 @@ dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old
                                   const dynmo_buf *h_recv, int32_t n_bufs, int64_t *h_bytes_sent,
                                   int64_t *h_bytes_recv, dynmo_stream stream);
 
+/* Call 5, peer-memory variant (nranks > 1): the receivers PULL the moved
+ * layers' buffers straight from the senders' memory over NVLink with one copy
+ * kernel (128-bit loads; no NCCL in the data path).
+ * dynmo_migrate_plan_create is COLLECTIVE and off the hot path: every rank
+ * registers the buffers it may send (h_send, layers it owns now; CUDA IPC
+ * handles of their cudaMalloc allocations are exchanged over the ctx
+ * communicator and mapped by every peer) and the buffers it may receive into
+ * (h_recv), same table layout as dynmo_migrate_layers.  The buffers must stay
+ * allocated while the plan lives.  dynmo_migrate_layers_p2p is collective
+ * like call 5: on `stream` the sender marks its buffers ready (release flag in
+ * each receiver's peer window, after its prior work), each receiver waits for
+ * its senders, copies, and marks done; the sender's stream then waits for its
+ * receivers (so it may overwrite or free the send buffers afterwards).  Sizes
+ * must match between sender and receiver (INVALID).  Waits are bounded (10 s):
+ * a timeout sets a sticky error readable with dynmo_ctx_p2p_error. */
+typedef struct dynmo_mplan_s *dynmo_mplan;
+dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t n_bufs,
+                                       const dynmo_buf *h_send, const dynmo_buf *h_recv,
+                                       dynmo_mplan *out);
+void dynmo_migrate_plan_destroy(dynmo_mplan plan);
+dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
+                                      const int32_t *h_bnd_old, const int32_t *h_rank_old,
+                                      int32_t n_new, const int32_t *h_bnd_new,
+                                      const int32_t *h_rank_new, int64_t *h_bytes_sent,
+                                      int64_t *h_bytes_recv, dynmo_stream stream);
+/* Sticky device error of the peer-memory paths (0 = none); synchronous. */
+dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
+
 /* Host-only helper (no GPU, no ctx): the migration plan call 5 executes.
  * Writes moves (layer, src_rank, dst_rank), layer ascending, for every layer
  * whose owning rank changes, into h_moves[n_layers][3]; returns the number of

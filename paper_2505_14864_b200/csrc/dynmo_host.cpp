@@ -1,11 +1,13 @@
 // dynmo_host.cpp -- host side of the C-ABI declared in include/dynmo.h:
 // argument validation, profile plans (tile decomposition), the NCCL context,
 // kernel launches and layer migration.  No device compute happens here.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -58,7 +60,50 @@ struct dynmo_ctx_s {
     int num_sms = 148;
     bool timing = false;
     PhaseTimer ph[DYNMO_NUM_PHASES];
+    // peer-memory window (nranks > 1): local flags + every peer's, mapped
+    PeerWindow *d_win = nullptr;
+    std::vector<PeerWindow *> peer_win;
+    cudaStream_t aux = nullptr;  // setup collectives
+    uint64_t mig_epoch = 0;
 };
+
+namespace {
+// All-gather `n` bytes per rank over the ctx communicator (setup only:
+// synchronous, through a temporary device buffer).
+dynmo_status allgather_bytes(dynmo_ctx c, const void *mine, size_t n, std::vector<char> &all) {
+    all.assign(n * c->nranks, 0);
+    char *d = nullptr;
+    CUDA_TRY(cudaMalloc(&d, n * c->nranks), "cudaMalloc (allgather)");
+    cudaError_t e = cudaMemcpy(d + n * c->rank, mine, n, cudaMemcpyHostToDevice);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess) r = ncclAllGather(d + n * c->rank, d, n, ncclChar, c->comm, c->aux);
+    if (e == cudaSuccess && r == ncclSuccess) e = cudaStreamSynchronize(c->aux);
+    if (e == cudaSuccess && r == ncclSuccess) e = cudaMemcpy(all.data(), d, n * c->nranks, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (r != ncclSuccess) {
+        g_err = std::string("ncclAllGather (setup): ") + ncclGetErrorString(r);
+        return DYNMO_E_NCCL;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "allgather_bytes");
+    return DYNMO_OK;
+}
+
+// Base and size of the cudaMalloc allocation containing p (driver API via
+// the runtime's entry-point query; no link-time libcuda dependency).
+dynmo_status alloc_range(const void *p, CUdeviceptr *base, size_t *size) {
+    typedef CUresult (*Fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+    static Fn fn = nullptr;
+    if (!fn) {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess || !f)
+            return invalid("cuMemGetAddressRange unavailable");
+        fn = (Fn)f;
+    }
+    if (fn(base, size, (CUdeviceptr)p) != CUDA_SUCCESS) return invalid("pointer is not device memory");
+    return DYNMO_OK;
+}
+}  // namespace
 
 namespace {
 // Records the start event of `phase` on `s`; returns the end event to record
@@ -158,6 +203,10 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         c->num_sms = sms;
     if (nranks > 1) {
+        if (nranks > kMaxRanks) {
+            delete c;
+            return invalid("nranks > 16");
+        }
         ncclUniqueId id;
         memcpy(id.internal, h_nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
@@ -166,6 +215,32 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
             delete c;
             return DYNMO_E_NCCL;
         }
+        // peer window: flags every peer can write (CUDA IPC over NVLink)
+        dynmo_status st = DYNMO_OK;
+        if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "peer window");
+        cudaIpcMemHandle_t h;
+        if (!st && cudaIpcGetMemHandle(&h, c->d_win) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle");
+        std::vector<char> all;
+        if (!st) st = allgather_bytes(c, &h, sizeof(h), all);
+        c->peer_win.assign(nranks, nullptr);
+        for (int rr = 0; !st && rr < nranks; ++rr) {
+            if (rr == rank) {
+                c->peer_win[rr] = c->d_win;
+                continue;
+            }
+            cudaIpcMemHandle_t ph;
+            memcpy(&ph, all.data() + rr * sizeof(ph), sizeof(ph));
+            void *mp = nullptr;
+            if (cudaIpcOpenMemHandle(&mp, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (window)");
+            c->peer_win[rr] = (PeerWindow *)mp;
+        }
+        if (st) {
+            dynmo_ctx_destroy(c);
+            return st;
+        }
     }
     *out = c;
     return DYNMO_OK;
@@ -173,6 +248,10 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
 
 void dynmo_ctx_destroy(dynmo_ctx ctx) {
     if (!ctx) return;
+    for (int r = 0; r < (int)ctx->peer_win.size(); ++r)
+        if (r != ctx->rank && ctx->peer_win[r]) cudaIpcCloseMemHandle(ctx->peer_win[r]);
+    if (ctx->d_win) cudaFree(ctx->d_win);
+    if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     for (auto &t : ctx->ph) {
         for (auto &pr : t.ev) {
@@ -675,6 +754,204 @@ dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old
         g_err = std::string("NCCL send/recv: ") + ncclGetErrorString(r);
         return DYNMO_E_NCCL;
     }
+    return DYNMO_OK;
+}
+
+
+// ---------------------------------------------- call 5, peer-memory variant
+struct dynmo_mplan_s {
+    dynmo_ctx ctx = nullptr;
+    int32_t n_layers = 0, n_bufs = 0;
+    std::vector<dynmo_buf> recv;                        // [n_layers * n_bufs] (this rank)
+    std::map<std::pair<int, int64_t>, dynmo_buf> src;   // (rank, layer*n_bufs+k) -> readable ptr
+    std::vector<void *> opened;                         // IPC mappings to close
+};
+
+namespace {
+struct SendRec {
+    int32_t idx;      // layer * n_bufs + k
+    int32_t handle;   // index into the rank's handle list
+    uint64_t offset;  // from the allocation base
+    int64_t bytes;
+};
+}  // namespace
+
+dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t n_bufs,
+                                       const dynmo_buf *h_send, const dynmo_buf *h_recv,
+                                       dynmo_mplan *out) {
+    if (!out) return invalid("null mplan out");
+    *out = nullptr;
+    if (!ctx || n_layers < 1 || n_bufs < 1 || !h_send || !h_recv) return invalid("bad migrate plan args");
+    if (ctx->nranks < 2) return invalid("the peer-memory migration needs nranks > 1");
+    DeviceGuard g(ctx->device);
+    const int64_t nb = (int64_t)n_layers * n_bufs;
+    // this rank's send buffers -> (allocation handle, offset)
+    std::vector<CUdeviceptr> bases;
+    std::vector<cudaIpcMemHandle_t> handles;
+    std::vector<SendRec> recs;
+    for (int64_t i = 0; i < nb; ++i) {
+        const dynmo_buf &b = h_send[i];
+        if (b.bytes <= 0 || !b.d_ptr) continue;
+        CUdeviceptr base;
+        size_t size;
+        dynmo_status st = alloc_range(b.d_ptr, &base, &size);
+        if (st) return st;
+        if ((CUdeviceptr)b.d_ptr + (size_t)b.bytes > base + size) return invalid("send buffer crosses its allocation");
+        int hi = -1;
+        for (size_t k = 0; k < bases.size(); ++k)
+            if (bases[k] == base) hi = (int)k;
+        if (hi < 0) {
+            cudaIpcMemHandle_t h;
+            CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base), "cudaIpcGetMemHandle (send buffer)");
+            hi = (int)bases.size();
+            bases.push_back(base);
+            handles.push_back(h);
+        }
+        recs.push_back(SendRec{(int32_t)i, hi, (uint64_t)((CUdeviceptr)b.d_ptr - base), b.bytes});
+    }
+    // gather every rank's tables (counts, then fixed-size padded arrays)
+    int64_t cnt[2] = {(int64_t)handles.size(), (int64_t)recs.size()};
+    std::vector<char> allc;
+    dynmo_status st = allgather_bytes(ctx, cnt, sizeof(cnt), allc);
+    if (st) return st;
+    int64_t mh = 1, mr = 1;
+    for (int r = 0; r < ctx->nranks; ++r) {
+        const int64_t *c = (const int64_t *)(allc.data() + r * sizeof(cnt));
+        mh = std::max(mh, c[0]);
+        mr = std::max(mr, c[1]);
+    }
+    const size_t blk = mh * sizeof(cudaIpcMemHandle_t) + mr * sizeof(SendRec);
+    std::vector<char> mine(blk, 0), all;
+    if (!handles.empty()) memcpy(mine.data(), handles.data(), handles.size() * sizeof(cudaIpcMemHandle_t));
+    if (!recs.empty()) memcpy(mine.data() + mh * sizeof(cudaIpcMemHandle_t), recs.data(), recs.size() * sizeof(SendRec));
+    st = allgather_bytes(ctx, mine.data(), blk, all);
+    if (st) return st;
+    auto *mp = new dynmo_mplan_s();
+    mp->ctx = ctx;
+    mp->n_layers = n_layers;
+    mp->n_bufs = n_bufs;
+    mp->recv.assign(h_recv, h_recv + nb);
+    for (int r = 0; r < ctx->nranks; ++r) {
+        const int64_t *c = (const int64_t *)(allc.data() + r * sizeof(cnt));
+        const char *b = all.data() + r * blk;
+        std::vector<char *> mapped(c[0], nullptr);
+        for (int64_t k = 0; k < c[0]; ++k) {
+            if (r == ctx->rank) {
+                mapped[k] = (char *)bases[k];
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            memcpy(&h, b + k * sizeof(h), sizeof(h));
+            void *p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                dynmo_status e = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (send buffer)");
+                dynmo_migrate_plan_destroy(mp);
+                return e;
+            }
+            mp->opened.push_back(p);
+            mapped[k] = (char *)p;
+        }
+        const SendRec *rr = (const SendRec *)(b + mh * sizeof(cudaIpcMemHandle_t));
+        for (int64_t k = 0; k < c[1]; ++k)
+            mp->src[{r, rr[k].idx}] = dynmo_buf{mapped[rr[k].handle] + rr[k].offset, rr[k].bytes};
+    }
+    *out = mp;
+    return DYNMO_OK;
+}
+
+void dynmo_migrate_plan_destroy(dynmo_mplan mp) {
+    if (!mp) return;
+    DeviceGuard g(mp->ctx->device);
+    for (void *p : mp->opened) cudaIpcCloseMemHandle(p);
+    delete mp;
+}
+
+dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,
+                                      const int32_t *h_bnd_old, const int32_t *h_rank_old,
+                                      int32_t n_new, const int32_t *h_bnd_new,
+                                      const int32_t *h_rank_new, int64_t *h_bytes_sent,
+                                      int64_t *h_bytes_recv, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    for (int32_t s = 0; s < n_old; ++s)
+        if (!h_rank_old || h_rank_old[s] < 0 || h_rank_old[s] >= ctx->nranks) return invalid("bad old rank");
+    for (int32_t s = 0; s < n_new; ++s)
+        if (!h_rank_new || h_rank_new[s] < 0 || h_rank_new[s] >= ctx->nranks) return invalid("bad new rank");
+    const int L = mp->n_layers, nb = mp->n_bufs, me = ctx->rank;
+    std::vector<int32_t> moves(3 * (size_t)L);
+    const int32_t m = dynmo_migration_plan(L, n_old, h_bnd_old, h_rank_old, n_new, h_bnd_new, h_rank_new,
+                                           moves.data());
+    if (m < 0) return invalid("malformed boundary vector");
+    std::vector<int> srcs, dsts;
+    std::vector<P2PItem> items;
+    int64_t sent = 0, recvd = 0;
+    for (int32_t k = 0; k < m; ++k) {
+        const int32_t i = moves[3 * k], src = moves[3 * k + 1], dst = moves[3 * k + 2];
+        for (int32_t u = 0; u < nb; ++u) {
+            const int64_t idx = (int64_t)i * nb + u;
+            auto it = mp->src.find({src, idx});
+            const int64_t sb = it == mp->src.end() ? 0 : it->second.bytes;
+            if (src == me) sent += sb;
+            if (dst == me) {
+                const dynmo_buf &r = mp->recv[idx];
+                if (r.bytes != sb) return invalid("recv buffer size differs from the sender's");
+                if (sb > 0 && !r.d_ptr) return invalid("missing recv buffer");
+                if (sb > 0) items.push_back(P2PItem{it->second.d_ptr, r.d_ptr, (uint64_t)sb});
+                recvd += sb;
+            }
+        }
+        if (dst == me && std::find(srcs.begin(), srcs.end(), src) == srcs.end()) srcs.push_back(src);
+        if (src == me && std::find(dsts.begin(), dsts.end(), dst) == dsts.end()) dsts.push_back(dst);
+    }
+    if (h_bytes_sent) *h_bytes_sent = sent;
+    if (h_bytes_recv) *h_bytes_recv = recvd;
+    if (srcs.empty() && dsts.empty()) return DYNMO_OK;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t epoch = ++ctx->mig_epoch;
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
+    // 1. tell my receivers that my buffers are ready (stream order = after my prior work)
+    P2PSignal sig{};
+    sig.epoch = epoch;
+    for (int d : dsts) sig.remote[sig.n++] = &ctx->peer_win[d]->ready[me];
+    CUDA_TRY(launch_signal(sig, s), "k_signal launch");
+    // 2. pull every incoming buffer over NVLink, then tell the senders
+    if (!srcs.empty()) {
+        P2PPull pl{};
+        pl.n_src = (int)srcs.size();
+        for (int i = 0; i < pl.n_src; ++i) {
+            pl.src_rank[i] = srcs[i];
+            pl.done_remote[i] = &ctx->peer_win[srcs[i]]->done[me];
+        }
+        pl.ready = ctx->d_win->ready;
+        pl.epoch = epoch;
+        pl.ctr = &ctx->d_win->pull_ctr;
+        pl.err = &ctx->d_win->err;
+        size_t pos = 0;
+        do {
+            pl.n_items = (int)std::min<size_t>(kP2PMaxItems, items.size() - pos);
+            for (int i = 0; i < pl.n_items; ++i) pl.items[i] = items[pos + i];
+            pos += pl.n_items;
+            pl.signal_done = pos == items.size();
+            CUDA_TRY(launch_pull(pl, ctx->num_sms, s), "k_pull launch");
+        } while (pos < items.size());
+    }
+    // 3. my receivers have finished reading my buffers
+    P2PWait wt{};
+    wt.epoch = epoch;
+    wt.local = ctx->d_win->done;
+    wt.err = &ctx->d_win->err;
+    for (int d : dsts) wt.idx[wt.n++] = d;
+    CUDA_TRY(launch_wait(wt, s), "k_wait launch");
+    phase_end(te, s);
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err) {
+    if (!ctx || !h_err) return invalid("bad args");
+    *h_err = 0;
+    if (!ctx->d_win) return DYNMO_OK;
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(cudaMemcpy(h_err, &ctx->d_win->err, sizeof(int32_t), cudaMemcpyDeviceToHost), "read p2p error");
     return DYNMO_OK;
 }
 

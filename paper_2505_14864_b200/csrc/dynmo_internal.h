@@ -116,6 +116,56 @@ struct SolveArgs {
     int32_t *n_new;
 };
 
+// ---------------------------------------------------------------- peer P2P
+constexpr int kP2PThreads = 512;
+constexpr int kP2PMaxItems = 64;
+constexpr int kMaxRanks = 16;
+
+// Per-rank flag window, mapped by every peer (CUDA IPC).  Peers write their
+// own slot [src]; the owner reads.  Epochs only grow.
+struct PeerWindow {
+    uint64_t ready[kMaxRanks];  // sender src's buffers are ready (migration epoch)
+    uint64_t done[kMaxRanks];   // receiver dst finished pulling (migration epoch)
+    uint64_t exch[kMaxRanks];   // rank src's exchange slot is written (profile epoch)
+    uint64_t exch_epoch;        // this rank's profile-exchange epoch counter
+    unsigned int pull_ctr;      // last-block counter of k_pull
+    int32_t err;                // sticky error (timeouts)
+};
+
+struct P2PItem {
+    const void *src;
+    void *dst;
+    uint64_t bytes;
+};
+struct P2PSignal {
+    int n;
+    uint64_t epoch;
+    uint64_t *remote[kMaxRanks];
+};
+struct P2PWait {
+    int n;
+    uint64_t epoch;
+    const uint64_t *local;
+    int idx[kMaxRanks];
+    int32_t *err;
+};
+struct P2PPull {
+    int n_items;
+    P2PItem items[kP2PMaxItems];
+    int n_src;
+    int src_rank[kMaxRanks];
+    const uint64_t *ready;           // local window ready[]
+    uint64_t *done_remote[kMaxRanks];  // &peer_window[src].done[me] (written by the last block)
+    int signal_done;
+    uint64_t epoch;
+    unsigned int *ctr;
+    int32_t *err;
+};
+
+cudaError_t launch_signal(const P2PSignal &s, cudaStream_t st);
+cudaError_t launch_wait(const P2PWait &w, cudaStream_t st);
+cudaError_t launch_pull(const P2PPull &p, int grid, cudaStream_t st);
+
 cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s);
 cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s);
 cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s);

@@ -20,7 +20,7 @@ from ._lib import lib
 __all__ = [
     "DynmoError", "Context", "ProfilePlan", "SegmentSpec", "Batch", "coef_tensor",
     "profile_layers", "partition_stages", "diffuse_balance", "repack_workers",
-    "migrate_layers", "migration_plan", "Migrator",
+    "migrate_layers", "migration_plan", "Migrator", "PeerMigrator",
 ]
 
 
@@ -341,3 +341,50 @@ class Migrator:
                                           self._tab_s, self._tab_r, self.n_bufs, C.byref(self._sent),
                                           C.byref(self._rec), _stream(stream)), "dynmo_migrate_layers")
         return self._sent.value, self._rec.value
+
+
+class PeerMigrator:
+    """Call 5 over NVLink peer memory (dynmo_migrate_plan_create +
+    dynmo_migrate_layers_p2p).  Collective construction: every rank passes the
+    buffers it may send (layers it owns) and may receive into."""
+
+    def __init__(self, ctx: Context, n_layers: int, send: dict, recv: dict, n_bufs: int = 1):
+        self.ctx, self.n_layers, self.n_bufs = ctx, int(n_layers), int(n_bufs)
+        tab_s = (_L.Buf * max(1, n_layers * n_bufs))()
+        tab_r = (_L.Buf * max(1, n_layers * n_bufs))()
+        self._keep = []
+        for tab, d in ((tab_s, send), (tab_r, recv)):
+            for layer, bufs in d.items():
+                for k, t in enumerate(bufs):
+                    tab[layer * n_bufs + k] = _L.Buf(t.data_ptr(), t.numel() * t.element_size())
+                    self._keep.append(t)
+        h = C.c_void_p()
+        _check(lib().dynmo_migrate_plan_create(ctx.handle, self.n_layers, self.n_bufs, tab_s, tab_r,
+                                               C.byref(h)), "dynmo_migrate_plan_create")
+        self._h = h
+        self._sent, self._rec = C.c_int64(0), C.c_int64(0)
+
+    def __call__(self, bnd_old, rank_old, bnd_new, rank_new, stream=None):
+        bo, ro = np.ascontiguousarray(bnd_old, np.int32), np.ascontiguousarray(rank_old, np.int32)
+        bn, rn = np.ascontiguousarray(bnd_new, np.int32), np.ascontiguousarray(rank_new, np.int32)
+        _check(lib().dynmo_migrate_layers_p2p(self.ctx.handle, self._h, len(bo) - 1, bo.ctypes.data,
+                                              ro.ctypes.data, len(bn) - 1, bn.ctypes.data, rn.ctypes.data,
+                                              C.byref(self._sent), C.byref(self._rec), _stream(stream)),
+               "dynmo_migrate_layers_p2p")
+        return self._sent.value, self._rec.value
+
+    def error(self) -> int:
+        e = C.c_int32(0)
+        _check(lib().dynmo_ctx_p2p_error(self.ctx.handle, C.byref(e)), "dynmo_ctx_p2p_error")
+        return e.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dynmo_migrate_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -96,6 +96,20 @@ def main():
     torch.cuda.synchronize()
     for l, bufs in recv.items():
         assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l])))
+    # the same moves over NVLink peer memory (IPC-mapped pull kernel)
+    for bufs in recv.values():
+        bufs[0].zero_()
+    pm = D.PeerMigrator(ctx, shape.L, send, recv)
+    for rep in range(3):
+        for bufs in recv.values():
+            bufs[0].zero_()
+        s2, g2 = pm(b_old, ranks, b_new, ranks)
+        torch.cuda.synchronize()
+        assert (s2, g2) == (want_sent, want_got), (rank, s2, g2)
+        for l, bufs in recv.items():
+            assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, rep)
+    assert pm.error() == 0
+    pm.close()
     dist.barrier()
     print(f"MGPU_OK {rank} layers[{begin},{begin + count}) moves={len(moves)} sent={sent} recv={got}", flush=True)
     ctx.close()
