@@ -51,8 +51,12 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--exchange", choices=["p2p", "nccl"], default="p2p",
+                    help="cost exchange over NVLink peer memory (default) or ncclAllGather")
     ap.add_argument("--migrate", choices=["p2p", "nccl"], default="p2p",
                     help="layer migration over NVLink peer memory (default) or NCCL send/recv")
+    ap.add_argument("--serial-solvers", action="store_true",
+                    help="run partition, diffusion and repack one after another on one stream")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every call eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -255,7 +259,7 @@ def run_dynmo(args):
     # ---- device-resident inputs
     dmask = [torch.from_numpy(m).to(dev) for _, m in inp.masks]
     segs = [D.SegmentSpec(t, LB.SRC_MASK_U8, layer) for t, (layer, _) in zip(dmask, inp.masks)]
-    plan = D.ProfilePlan(ctx, segs, begin, count, n_total=L, exchange=G > 1)
+    plan = D.ProfilePlan(ctx, segs, begin, count, n_total=L, exchange=args.exchange if G > 1 else False)
     coef = D.coef_tensor(count, A=0, B=1, device=dev)
     mem_local = torch.from_numpy(inp.payload[begin:begin + count].astype(np.int64)).to(dev)
     cost = torch.empty(L, dtype=torch.int64, device=dev)
@@ -295,6 +299,15 @@ def run_dynmo(args):
         diffusion and repack on two side branches, joined at the end."""
         main = torch.cuda.current_stream()
         D.profile_layers(ctx, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=pst)
+        if args.serial_solvers:
+            D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
+                               imbalance=part["imb"], status=part["st"])
+            res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
+            ev_res.record(main)
+            D.diffuse_balance(ctx, batch, cost, bnd_in, mem=mem, cap=cap, gamma=gamma, gamma_fluid=gamma_f,
+                              max_rounds=256, out=dif_out)
+            D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
+            return
         for sd in side:
             sd.wait_stream(main)
         with torch.cuda.stream(side[0]):
@@ -366,9 +379,18 @@ def run_dynmo(args):
     ctx.timing_read()  # reset accumulators
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sent_recv = (0, 0)
+    bar = torch.zeros(1, device=dev)
+
+    def step_barrier():
+        # rebalancing runs at the training iteration barrier: align the
+        # ranks' step starts on the device, outside the timed interval
+        if G > 1:
+            dist.all_reduce(bar)
+
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
+            step_barrier()
             ev[k][0].record(stream)
             sent_recv = step()
             ev[k][1].record(stream)
@@ -395,6 +417,7 @@ def run_dynmo(args):
     e2e = []
     for k in range(args.e2e_steps):
         flush.fill_(k & 0xFF)
+        step_barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         for t, p in zip(dmask, pinned):
@@ -443,7 +466,9 @@ def run_dynmo(args):
                          "avg_launch_ms": round(prof_avg, 5)},
             "phases_ms_per_step": {k: round(v[0] / args.steps, 5) for k, v in phases.items()},
             "step_ms": {"median": round(float(np.median(step_ms)), 5),
-                        "p95": round(float(np.percentile(step_ms, 95)), 5)},
+                        "p95": round(float(np.percentile(step_ms, 95)), 5),
+                        "max": round(float(step_ms.max()), 5),
+                        "n_over_2x_median": int((step_ms > 2 * np.median(step_ms)).sum())},
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
                         "max_bytes_recv_per_gpu": int(max_recv), "avg_ms": round(mig_ms, 5),
                         "nvlink_GBps": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9, 1)

@@ -149,11 +149,18 @@ typedef struct dynmo_cost_coef {
  * rebuild after migration or re-allocation.
  *   layer_begin, n_local: the contiguous global layers this rank profiles.
  *   n_total: length of the global cost vector.
- *   exchange: 1 -> profile_layers all-gathers every rank's slice over the
- *     ctx's NCCL communicator so each rank ends with the global vector
- *     (requires nranks > 1; slices must tile [0, n_total) exactly, else the
- *     device status is INVALID); 0 -> local only: n_total == n_local and
- *     outputs are indexed by local layer.
+ *   exchange: every rank ends with the global vector (requires nranks > 1;
+ *     slices must tile [0, n_total) exactly, else the device status is
+ *     INVALID):
+ *       1 -> over NVLink peer memory: the epilogue stores this rank's slot
+ *            straight into every rank's receive area (double-buffered by a
+ *            device-side epoch, graph-safe) and releases a flag; the unpack
+ *            kernel waits (bounded, 10 s) for every rank's flag.  Plan
+ *            creation is then COLLECTIVE (CUDA IPC of the receive areas), and
+ *            every rank must make the same sequence of profile calls.
+ *       2 -> ncclAllGather of the fixed-size slots on the ctx communicator.
+ *     0 -> local only: n_total == n_local and outputs are indexed by local
+ *     layer.
  * Errors (returned): INVALID for a null/negative argument, a layer outside
  * the local range, an unknown src_kind, n_experts outside [1, 1024] or
  * inconsistent within a layer, a misaligned pointer; NOMEM; CUDA. */

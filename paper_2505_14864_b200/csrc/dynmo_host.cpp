@@ -151,6 +151,10 @@ struct dynmo_plan_s {
     unsigned int *d_ws_done = nullptr;
     int64_t *d_slot_send = nullptr, *d_slot_recv = nullptr;
     int64_t slot_elems = 0;
+    // exchange over peer memory (exchange == 1): [2][nranks][slot_elems] here,
+    // and every peer's area mapped
+    int64_t *d_p2p_slots = nullptr;
+    std::vector<int64_t *> peer_slots;
 };
 
 extern "C" {
@@ -329,6 +333,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     if (!ctx) return invalid("null ctx");
     if (n_segs < 0 || (n_segs > 0 && !h_segs)) return invalid("bad segment array");
     if (layer_begin < 0 || n_local < 0 || n_total < 0) return invalid("negative layer range");
+    if (exchange < 0 || exchange > 2) return invalid("exchange must be 0, 1 (peer memory) or 2 (NCCL)");
     if (exchange) {
         if (ctx->nranks < 2) return invalid("exchange needs nranks > 1");
         if ((int64_t)layer_begin + n_local > n_total) return invalid("local layers exceed n_total");
@@ -413,7 +418,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     pl->layer_begin = layer_begin;
     pl->n_local = n_local;
     pl->n_total = n_total;
-    pl->exchange = exchange ? 1 : 0;
+    pl->exchange = exchange;
     pl->max_E = max_E;
     pl->has_hist = has_hist;
     pl->bytes = bytes;
@@ -464,6 +469,36 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
         delete pl;
         return cuda_fail(e, "plan upload");
     }
+    if (exchange == 1) {
+        // collective: the receive slot area of every rank, mapped by every peer
+        const size_t bytes = sizeof(int64_t) * 2 * ctx->nranks * pl->slot_elems;
+        dynmo_status st = DYNMO_OK;
+        if (cudaMalloc((void **)&pl->d_p2p_slots, bytes) != cudaSuccess ||
+            cudaMemset(pl->d_p2p_slots, 0, bytes) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "p2p slots");
+        cudaIpcMemHandle_t h;
+        if (!st && cudaIpcGetMemHandle(&h, pl->d_p2p_slots) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle (slots)");
+        std::vector<char> all;
+        if (!st) st = allgather_bytes(ctx, &h, sizeof(h), all);
+        pl->peer_slots.assign(ctx->nranks, nullptr);
+        for (int r = 0; !st && r < ctx->nranks; ++r) {
+            if (r == ctx->rank) {
+                pl->peer_slots[r] = pl->d_p2p_slots;
+                continue;
+            }
+            cudaIpcMemHandle_t ph;
+            memcpy(&ph, all.data() + r * sizeof(ph), sizeof(ph));
+            void *mp = nullptr;
+            if (cudaIpcOpenMemHandle(&mp, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (slots)");
+            pl->peer_slots[r] = (int64_t *)mp;
+        }
+        if (st) {
+            dynmo_profile_plan_destroy(pl);
+            return st;
+        }
+    }
     const int warps_per_block = kProfThreads / 32;
     const int64_t want = (pl->n_tiles + warps_per_block - 1) / warps_per_block;
     const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(has_hist);
@@ -475,6 +510,9 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
 void dynmo_profile_plan_destroy(dynmo_plan plan) {
     if (!plan) return;
     DeviceGuard g(plan->ctx->device);
+    for (int r = 0; r < (int)plan->peer_slots.size(); ++r)
+        if (r != plan->ctx->rank && plan->peer_slots[r]) cudaIpcCloseMemHandle(plan->peer_slots[r]);
+    if (plan->d_p2p_slots) cudaFree(plan->d_p2p_slots);
     cudaFree(plan->dmem);
     delete plan;
 }
@@ -518,10 +556,26 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     ea.ws_status = plan->d_ws_status;
     ea.ws_done = plan->d_ws_done;
     ea.status_out = d_status;
+    if (plan->exchange == 1) {
+        ea.p2p = 1;
+        ea.rank = ctx->rank;
+        ea.nranks = ctx->nranks;
+        ea.win = ctx->d_win;
+        for (int r = 0; r < ctx->nranks; ++r) {
+            ea.peer_slots[r] = plan->peer_slots[r];
+            ea.peer_win[r] = ctx->peer_win[r];
+        }
+    }
     te = phase_begin(ctx, DYNMO_PHASE_EPILOGUE, s);
     CUDA_TRY(launch_epilogue(ea, s), "k_epilogue launch");
     phase_end(te, s);
-    if (plan->exchange) {
+    if (plan->exchange == 1) {
+        te = phase_begin(ctx, DYNMO_PHASE_EXCHANGE, s);
+        CUDA_TRY(launch_unpack_p2p(plan->d_p2p_slots, ctx->d_win, ctx->nranks, plan->n_total, d_cost, d_mem,
+                                   d_status, s),
+                 "k_unpack_p2p launch");
+        phase_end(te, s);
+    } else if (plan->exchange == 2) {
         te = phase_begin(ctx, DYNMO_PHASE_EXCHANGE, s);
         ncclResult_t r = ncclAllGather(plan->d_slot_send, plan->d_slot_recv, (size_t)plan->slot_elems,
                                        ncclInt64, ctx->comm, s);

@@ -61,8 +61,17 @@ struct ProfArgs {
     int32_t *ws_status;
 };
 
+struct PeerWindow;
+constexpr int kMaxRanksEpi = 16;
+
 struct EpiArgs {
     int32_t layer_begin, n_local, n_total, exchange, max_E;
+    // exchange over peer memory (exchange == 1): every rank's slot area is
+    // int64 [2 parity][nranks][3 + 2 n_total], mapped by every peer
+    int32_t p2p, rank, nranks;
+    int64_t *peer_slots[kMaxRanksEpi];
+    PeerWindow *win;                      // local window (exch_epoch counter)
+    PeerWindow *peer_win[kMaxRanksEpi];   // every rank's window (flags)
     const LayerInfo *info;
     unsigned long long *acc;
     unsigned long long *hist;
@@ -86,6 +95,10 @@ cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
                           cudaStream_t s);
+// peer-memory exchange: waits for every rank's flag of this epoch, then
+// unpacks the local slot area (parity of the epoch)
+cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
+                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out, cudaStream_t s);
 
 // ------------------------------------------------------------------ solvers
 struct SolveArgs {
@@ -119,7 +132,7 @@ struct SolveArgs {
 // ---------------------------------------------------------------- peer P2P
 constexpr int kP2PThreads = 512;
 constexpr int kP2PMaxItems = 64;
-constexpr int kMaxRanks = 16;
+constexpr int kMaxRanks = kMaxRanksEpi;
 
 // Per-rank flag window, mapped by every peer (CUDA IPC).  Peers write their
 // own slot [src]; the owner reads.  Epochs only grow.

@@ -236,6 +236,14 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
 
 // -------------------------------------------------------------- epilogue
 __device__ __forceinline__ int worse(int a, int b) { return a < b ? a : b; }
+__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 __global__ void k_epilogue(EpiArgs a) {
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -306,7 +314,16 @@ __global__ void k_epilogue(EpiArgs a) {
             o[2] = moe > LIM ? -1 : (int64_t)moe;
             o[3] = c;
         }
-        if (a.exchange) {
+        if (a.p2p) {
+            // straight into every rank's receive slot (NVLink stores)
+            const uint64_t epoch = a.win->exch_epoch + 1;  // incremented by the last block
+            const int64_t S = 3 + 2 * (int64_t)a.n_total;
+            const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * S;
+            for (int r = 0; r < a.nranks; ++r) {
+                a.peer_slots[r][off + 3 + q] = c;
+                a.peer_slots[r][off + 3 + a.n_total + q] = m;
+            }
+        } else if (a.exchange) {
             a.slot_send[3 + q] = c;
             a.slot_send[3 + a.n_total + q] = m;
         } else {
@@ -323,6 +340,8 @@ __global__ void k_epilogue(EpiArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s_st != DYNMO_OK) atomicMin(a.ws_status, s_st);
+        // this block's (remote) slot stores before the counter; the last
+        // block's system-scope fence + release below is cumulative over them
         __threadfence();
         unsigned prev = atomicAdd(a.ws_done, 1u);
         s_last = prev == gridDim.x - 1;
@@ -334,7 +353,19 @@ __global__ void k_epilogue(EpiArgs a) {
         if (threadIdx.x == 0) {
             const int fin = atomicExch(a.ws_status, 0);
             *a.ws_done = 0u;
-            if (a.exchange) {
+            if (a.p2p) {
+                const uint64_t epoch = a.win->exch_epoch + 1;
+                const int64_t S = 3 + 2 * (int64_t)a.n_total;
+                const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * S;
+                for (int r = 0; r < a.nranks; ++r) {
+                    a.peer_slots[r][off + 0] = a.layer_begin;
+                    a.peer_slots[r][off + 1] = a.n_local;
+                    a.peer_slots[r][off + 2] = fin;
+                }
+                __threadfence_system();
+                for (int r = 0; r < a.nranks; ++r) st_release_sys(&a.peer_win[r]->exch[a.rank], epoch);
+                a.win->exch_epoch = epoch;
+            } else if (a.exchange) {
                 a.slot_send[0] = a.layer_begin;
                 a.slot_send[1] = a.n_local;
                 a.slot_send[2] = fin;
@@ -348,8 +379,16 @@ __global__ void k_epilogue(EpiArgs a) {
 // ---------------------------------------------------------------- unpack
 // Slot of rank r at slot_recv + r*S, S = 3 + 2*n_total:
 // {layer_begin, n_local, status, cost[n_total], mem[n_total]}.
+__device__ void k_unpack_body(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
+                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out);
+
 __global__ void k_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                          int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+    k_unpack_body(slot_recv, nranks, n_total, cost_out, mem_out, status_out);
+}
+
+__device__ void k_unpack_body(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
+                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
     const int64_t S = 3 + 2 * (int64_t)n_total;
     __shared__ int s_st;
     if (threadIdx.x == 0) {
@@ -386,6 +425,42 @@ __global__ void k_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_tot
     if (st != DYNMO_OK) atomicMin(&s_st, st);
     __syncthreads();
     if (threadIdx.x == 0) *status_out = s_st;
+}
+
+// Peer-memory exchange, receive side: wait (bounded) for every rank's flag of
+// this epoch, then scatter the local slot area of the epoch's parity.
+__global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
+                             int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+    __shared__ int s_ok;
+    const uint64_t epoch = win->exch_epoch;  // advanced by this rank's epilogue
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        for (int r = 0; r < nranks; ++r) {
+            uint64_t t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            while (ld_acquire_sys(&win->exch[r]) < epoch) {
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 10ull * 1000 * 1000 * 1000) {
+                    ok = 0;
+                    win->err = DYNMO_E_NCCL;
+                    break;
+                }
+                __nanosleep(100);
+            }
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok) {
+        for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
+            cost_out[i] = -1;
+            if (mem_out) mem_out[i] = 0;
+        }
+        if (threadIdx.x == 0) *status_out = DYNMO_E_NCCL;
+        return;
+    }
+    const int64_t S = 3 + 2 * (int64_t)n_total;
+    k_unpack_body(slots + (int64_t)(epoch & 1) * nranks * S, nranks, n_total, cost_out, mem_out, status_out);
 }
 
 }  // namespace
@@ -431,6 +506,12 @@ cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_to
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
                           cudaStream_t s) {
     k_unpack<<<1, 1024, 0, s>>>(slot_recv, nranks, n_total, cost_out, mem_out, status_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
+                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out, cudaStream_t s) {
+    k_unpack_p2p<<<1, 1024, 0, s>>>(slots, win, nranks, n_total, cost_out, mem_out, status_out);
     return cudaGetLastError();
 }
 

@@ -131,7 +131,9 @@ class ProfilePlan:
     """dynmo_profile_plan_create: tile decomposition of this rank's segments."""
 
     def __init__(self, ctx: Context, segments: Sequence[SegmentSpec], layer_begin: int,
-                 n_local: int, n_total: Optional[int] = None, exchange: bool = False):
+                 n_local: int, n_total: Optional[int] = None, exchange=False):
+        """exchange: False/0 local only, True/1 or "p2p" over NVLink peer
+        memory (collective creation), 2 or "nccl" via ncclAllGather."""
         n_total = n_local if n_total is None else n_total
         arr = (_L.Segment * max(1, len(segments)))()
         self._keep = []  # keep the tensors alive while the plan exists
@@ -145,8 +147,10 @@ class ProfilePlan:
             arr[i] = _L.Segment(t.data_ptr(), int(n), int(s.layer), int(s.kind), int(s.n_experts), int(s.top_k))
             self._keep.append(t)
         h = C.c_void_p()
+        ex = {"p2p": 1, "nccl": 2}.get(exchange, exchange)
+        ex = int(ex) if not isinstance(ex, bool) else int(ex)
         _check(lib().dynmo_profile_plan_create(ctx.handle, arr, len(segments), layer_begin, n_local,
-                                               n_total, int(bool(exchange)), C.byref(h)),
+                                               n_total, ex, C.byref(h)),
                "dynmo_profile_plan_create")
         self._h = h
         self.ctx = ctx

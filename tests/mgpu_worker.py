@@ -58,15 +58,25 @@ def main():
                 segs.append(D.SegmentSpec(t, LB.SRC_MASK_U8, layer))
     want_cost = np.array([oracle.layer_cost(nnz=int(v), A=0, B=1)[1] for v in want_all])
     payload = (synth.cfg2_payload_bytes(shape, p) // 64).astype(np.int64)  # smaller transfers
-    plan = D.ProfilePlan(ctx, segs, begin, count, n_total=shape.L, exchange=world > 1)
     coef = D.coef_tensor(count, A=0, B=1, device=dev)
     mem_local = torch.from_numpy(payload[begin:begin + count].copy()).to(dev)
     mem = torch.empty(shape.L, dtype=torch.int64, device=dev)
-    cost, _, st = D.profile_layers(ctx, plan, coef, mem_local=mem_local, mem=mem)
+    for mode in ("nccl", "p2p"):
+        plan = D.ProfilePlan(ctx, segs, begin, count, n_total=shape.L, exchange=mode)
+        for rep in range(3):  # several epochs (both slot parities)
+            cost, _, st = D.profile_layers(ctx, plan, coef, mem_local=mem_local, mem=mem)
+            torch.cuda.synchronize()
+            assert int(st.item()) == 0, (mode, st)
+            assert np.array_equal(cost.cpu().numpy(), want_cost), (mode, rank, cost.cpu().numpy(), want_cost)
+            assert np.array_equal(mem.cpu().numpy(), payload)
+    # back-to-back calls without host synchronisation (fast ranks may run ahead)
+    outs = []
+    for rep in range(6):
+        c_, _, st_ = D.profile_layers(ctx, plan, coef, mem_local=mem_local)
+        outs.append((c_.clone(), st_.clone()))
     torch.cuda.synchronize()
-    assert int(st.item()) == 0, st
-    assert np.array_equal(cost.cpu().numpy(), want_cost), (rank, cost.cpu().numpy(), want_cost)
-    assert np.array_equal(mem.cpu().numpy(), payload)
+    for c_, st_ in outs:
+        assert int(st_.item()) == 0 and np.array_equal(c_.cpu().numpy(), want_cost)
     # identical partition on every rank == oracle
     b = D.Batch([shape.L], [n], device=dev)
     bnd, bott, _, pst = D.partition_stages(ctx, b, cost)
