@@ -24,7 +24,6 @@ import json
 import os
 import statistics
 import sys
-import threading
 import time
 
 import numpy as np
@@ -104,63 +103,63 @@ class Inputs:
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """Samples SM clock + clock-event reasons with NVML during the timed region."""
+    """Samples SM clock + clock-event reasons during the timed region with an
+    `nvidia-smi -lms` subprocess (no GIL contention with the timed loop)."""
 
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-               0x100: "display_clock_setting"}
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, torch_dev):
-        self.samples, self.reasons, self.ok = [], 0, False
+        import torch
+        self.dev_id = None
         try:
-            import pynvml as N
-            import torch
-            N.nvmlInit()
-            self.N = N
-            h = None
-            try:
-                uuid = str(torch.cuda.get_device_properties(torch_dev).uuid)
-                h = N.nvmlDeviceGetHandleByUUID(("GPU-" + uuid) if not uuid.startswith("GPU-") else uuid)
-            except Exception:
-                h = N.nvmlDeviceGetHandleByIndex(torch_dev)
-            self.h = h
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            self.ok = True
-        except Exception as e:  # pragma: no cover
-            self.err = repr(e)
-        self._stop = threading.Event()
-
-    def _run(self):
-        N = self.N
-        get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-            N.nvmlDeviceGetCurrentClocksThrottleReasons
-        while not self._stop.is_set():
-            try:
-                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
-                self.reasons |= int(get_r(self.h))
-            except Exception:
-                pass
-            time.sleep(0.005)
+            u = str(torch.cuda.get_device_properties(torch_dev).uuid)
+            self.dev_id = u if u.startswith("GPU-") else "GPU-" + u
+        except Exception:
+            self.dev_id = str(torch_dev)
+        self.proc, self.out = None, ""
 
     def __enter__(self):
-        if self.ok:
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
+        import subprocess
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.dev_id, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.05)
+        except Exception as e:  # pragma: no cover
+            self.err = repr(e)
         return self
 
     def __exit__(self, *a):
-        if self.ok:
-            self._stop.set()
-            self.t.join()
+        if self.proc is not None:
+            time.sleep(0.03)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
 
     def summary(self):
-        if not self.ok or not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": [],
-                    "samples": 0, "note": getattr(self, "err", "no samples")}
-        rs = [v for k, v in self.REASONS.items() if self.reasons & k and k != 0x1]
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": rs, "samples": len(self.samples)}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0,
+                    "note": getattr(self, "err", "no nvidia-smi samples")}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
 
 
 # --------------------------------------------------------- oracle (CPU) arm

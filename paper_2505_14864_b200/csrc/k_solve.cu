@@ -160,45 +160,35 @@ __device__ __forceinline__ int prefix_status(const PrefixFlags &f, bool use_mem)
 }
 
 // --------------------------------------------------------------- greedy
-// Largest K >= j with P[K] - P[j] <= B and M[K] - M[j] <= cap (both
-// monotone in K); K == j means layer j alone does not fit.  Stages are short
-// (about L/n layers), so first test the next kWin positions with independent
-// loads (the count of passing positions is the jump, by monotonicity); only
-// if all pass, binary-search the rest.
-constexpr int kWin = 8;
+// Warp-cooperative greedy jump: the largest K >= j with P[K] - P[j] <= B and
+// M[K] - M[j] <= cap (t1 = P[j] + B, t2 = M[j] + cap).  Both predicates are
+// monotone in K, so the 32-position window test below yields a ballot that
+// is a prefix of ones: its popcount is the jump length (one shared load and
+// one 64-bit compare per lane per 32 positions).  K == j: layer j does not fit.
 template <bool MEM>
-__device__ __forceinline__ int bs_next(const Inst &s, int j, int64_t B) {
-    const int64_t t1 = satadd(s.P[j], B);
-    int64_t t2 = 0;
-    if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
-    int cnt = 0;
-#pragma unroll
-    for (int i = 1; i <= kWin; ++i) {
-        const int p = j + i <= s.L ? j + i : s.L;
-        bool ok = j + i <= s.L && s.P[p] <= t1;
+__device__ __forceinline__ int warp_jump(const Inst &s, int j, int64_t t1, int64_t t2, int lane) {
+    int K = j;
+    for (;;) {
+        const int p = K + 1 + lane;
+        bool ok = p <= s.L && s.P[p] <= t1;
         if constexpr (MEM) ok = ok && s.M[p] <= t2;
-        cnt += ok;
+        const int c = __popc(__ballot_sync(FULL, ok));
+        K += c;
+        if (c < 32) return K;
     }
-    if (cnt < kWin) return j + cnt;
-    int lo = j + kWin, hi = s.L;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        bool ok = s.P[mid] <= t1;
-        if constexpr (MEM) ok = ok && s.M[mid] <= t2;
-        if (ok) lo = mid;
-        else hi = mid - 1;
-    }
-    return lo;
 }
 
-// Greedy maximal-prefix stage count under B, stopping once it exceeds
-// `limit` (limit + 1 also for an unplaceable layer).  Per lane.
+// Greedy maximal-prefix stage count under B (warp-uniform), stopping once it
+// exceeds `limit` (limit + 1 also for an unplaceable layer).
 template <bool MEM>
-__device__ int greedy_count(const Inst &s, int64_t B, int limit) {
+__device__ int warp_greedy(const Inst &s, int64_t B, int limit, int lane) {
     int j = 0, c = 0;
     while (j < s.L) {
         if (c == limit) return limit + 1;
-        const int K = bs_next<MEM>(s, j, B);
+        const int64_t t1 = satadd(s.P[j], B);
+        int64_t t2 = 0;
+        if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
+        const int K = warp_jump<MEM>(s, j, t1, t2, lane);
         if (K == j) return limit + 1;
         j = K;
         ++c;
@@ -206,27 +196,25 @@ __device__ int greedy_count(const Inst &s, int64_t B, int limit) {
     return c;
 }
 
-// Candidate c of NC per round: lo + floor(d (c+1) / (NC+1)) in 64-bit
-// arithmetic (d = a (NC+1) + r); NC+1 is a compile-time constant.
+// Candidate w of NW per round: lo + floor(d (w+1) / (NW+1)) in 64-bit
+// arithmetic (d = a (NW+1) + r); NW+1 is a compile-time constant.
 template <int NC1>
 __device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
     const uint64_t qa = d / (uint64_t)NC1, qr = d % (uint64_t)NC1;
     return lo + (int64_t)(qa * (uint64_t)(c + 1) + (qr * (uint64_t)(c + 1)) / (uint64_t)NC1);
 }
 
-// Exact min-max search over B in [lo, hi] (hi feasible).  Every lane of the
-// NW warps tests one candidate per round with its own greedy (NC = 32 NW
-// candidates, an (NC+1)-ary search); feasibility is monotone in B, so the
-// feasible candidates form a suffix: the first feasible one is the new hi and
-// its predecessor + 1 the new lo.  Called by all NW warps; s must be fully
-// built (warp 0) and visible (__syncthreads) before.  Returns B* (uniform),
-// or -1 if no split satisfies the memory cap.
+// Exact min-max search over B in [lo, hi] (hi feasible): each of the NW
+// warps tests one candidate per round with the warp-cooperative greedy, an
+// (NW+1)-ary search.  Feasibility is monotone in B, so the feasible
+// candidates form a suffix: the first feasible one is the new hi and its
+// predecessor + 1 the new lo.  Called by all NW warps after s is built and
+// visible.  Returns B* (uniform), or -1 if no split satisfies the memory cap.
 template <bool MEM, int NW>
 __device__ int64_t search_bottleneck(const Inst &s, int n) {
-    constexpr int NC = 32 * NW;
-    __shared__ unsigned s_m[2][NW];
-    __shared__ int s_f;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, c = w * 32 + lane;
+    __shared__ int s_f[2][NW];
+    __shared__ int s_pre[2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t C = s.P[s.L];
     const int64_t ceil_cn = C / n + (C % n != 0);
     int64_t lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
@@ -235,13 +223,19 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
     if (lo > hi) lo = hi;
     if constexpr (MEM) {
         // the memory cap may make the cost bracket infeasible: widen to C
-        if (threadIdx.x == 0) s_f = greedy_count<MEM>(s, hi, n) <= n;
-        if (threadIdx.x == 1) s_m[1][0] = greedy_count<MEM>(s, C, n) <= n;
-        if constexpr (NW > 1) __syncthreads();
-        else __syncwarp();
-        const int fh = s_f, fc = (int)s_m[1][0];
-        if constexpr (NW > 1) __syncthreads();
-        else __syncwarp();
+        int fh, fc;
+        if constexpr (NW > 1) {
+            if (w < 2) {
+                const int f = warp_greedy<MEM>(s, w == 0 ? hi : C, n, lane) <= n;
+                if (lane == 0) s_pre[w] = f;
+            }
+            __syncthreads();
+            fh = s_pre[0];
+            fc = s_pre[1];
+        } else {
+            fh = warp_greedy<MEM>(s, hi, n, lane) <= n;
+            fc = fh ? 1 : warp_greedy<MEM>(s, C, n, lane) <= n;
+        }
         if (!fh) {
             if (!fc) return -1;
             hi = C;
@@ -250,46 +244,42 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
     int par = 0;
     while (lo < hi) {
         const uint64_t d = (uint64_t)(hi - lo);
-        const int64_t cand = candidate<NC + 1>(lo, d, c);
-        const bool f = greedy_count<MEM>(s, cand, n) <= n;
-        const unsigned m = __ballot_sync(FULL, f);
+        const int64_t cand = candidate<NW + 1>(lo, d, w);
+        const int f = warp_greedy<MEM>(s, cand, n, lane) <= n;
         int first;
         if constexpr (NW == 1) {
-            first = m ? __ffs(m) - 1 : NC;
+            first = f ? 0 : 1;
         } else {
-            if (lane == 0) s_m[par][w] = m;
+            if (lane == 0) s_f[par][w] = f;
             __syncthreads();
-            first = NC;
+            first = NW;
 #pragma unroll
-            for (int k = NW - 1; k >= 0; --k) {
-                const unsigned mk = s_m[par][k];
-                if (mk) first = k * 32 + __ffs(mk) - 1;
-            }
+            for (int k = NW - 1; k >= 0; --k)
+                if (s_f[par][k]) first = k;
             par ^= 1;  // double buffer: the next round writes the other half
         }
-        const int64_t nhi = first < NC ? candidate<NC + 1>(lo, d, first) : hi;
-        const int64_t nlo = first > 0 ? candidate<NC + 1>(lo, d, first - 1) + 1 : lo;
+        const int64_t nhi = first < NW ? candidate<NW + 1>(lo, d, first) : hi;
+        const int64_t nlo = first > 0 ? candidate<NW + 1>(lo, d, first - 1) + 1 : lo;
         hi = nhi;
         lo = nlo;
     }
     return hi;
 }
 
-// Lexmax boundaries for B* (Appendix A): jump table at B* (all lanes), then
-// b_{s+1} = min(next(b_s), L - (n-1-s)) on lane 0.  Writes s.b[0..n].
+// Lexmax boundaries for B* (Appendix A): b_{s+1} = min(next(b_s), L - (n-1-s))
+// with warp-cooperative jumps.  One warp; writes s.b[0..n].
 template <bool MEM>
 __device__ void construct(Inst &s, int64_t Bs, int n, int lane) {
-    for (int j = lane; j < s.L; j += 32) s.nxt[j] = (int16_t)bs_next<MEM>(s, j, Bs);
-    __syncwarp();
-    if (lane == 0) {
-        int j = 0;
-        s.b[0] = 0;
-        for (int st = 0; st < n; ++st) {
-            const int K = s.nxt[j];
-            const int reserve = s.L - (n - 1 - st);
-            j = K < reserve ? K : reserve;
-            s.b[st + 1] = j;
-        }
+    int j = 0;
+    if (lane == 0) s.b[0] = 0;
+    for (int st = 0; st < n; ++st) {
+        const int64_t t1 = satadd(s.P[j], Bs);
+        int64_t t2 = 0;
+        if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
+        const int K = warp_jump<MEM>(s, j, t1, t2, lane);
+        const int reserve = s.L - (n - 1 - st);
+        j = K < reserve ? K : reserve;
+        if (lane == 0) s.b[st + 1] = j;
     }
     __syncwarp();
 }
@@ -395,9 +385,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         int k = n_cur, code = DYNMO_OK;
         if (st == DYNMO_OK && !alg2) {
             // fewest workers: greedy count at B = bound (cost and mem), reading Q15
-            int g = 0;
-            if (lane == 0) g = greedy_count<MEM>(s, bound, n_cur);
-            g = __shfl_sync(FULL, g, 0);
+            const int g = warp_greedy<MEM>(s, bound, n_cur, lane);
             if (g <= n_cur) {
                 k = g > fl ? g : fl;
             } else {
@@ -622,33 +610,26 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
     double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
     int size = 1;
     for (int base = 0;; base += size, size = size < kChunk / 4 ? size * 4 : kChunk) {
+        // branch-free round: both candidate averages are computed off the
+        // critical path; the pick is gr > gl ? s : (gl > 0 ? s-1 : -1), which
+        // is the oracle's rule (edge s-1 first, a strictly larger gap wins).
+        // (A halo-2 variant that recomputes the neighbours' picks locally
+        // instead of shuffling them measured slower: 39 vs 31 us.)
+        const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
         for (int k = 0; k < size; ++k) {
             if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
             const double xl = __shfl_up_sync(FULL, x, 1);
             const double xr = __shfl_down_sync(FULL, x, 1);
-            int pick = -1;
-            double best = 0.0;
-            if (lane < n) {
-                if (lane >= 1) {
-                    const double g = fabs(__dsub_rn(xl, x));  // edge lane-1
-                    if (g > best) {
-                        best = g;
-                        pick = lane - 1;
-                    }
-                }
-                if (lane + 1 < n) {
-                    const double g = fabs(__dsub_rn(x, xr));  // edge lane
-                    if (g > best) {
-                        best = g;
-                        pick = lane;
-                    }
-                }
-            }
+            const double gl = hasL ? fabs(__dsub_rn(xl, x)) : 0.0;  // gap of edge lane-1
+            const double gr = hasR ? fabs(__dsub_rn(x, xr)) : 0.0;  // gap of edge lane
+            const double avgL = __dmul_rn(__dadd_rn(xl, x), 0.5);
+            const double avgR = __dmul_rn(__dadd_rn(x, xr), 0.5);
+            const int pick = gr > gl ? lane : (gl > 0.0 ? lane - 1 : -1);
             const int pr = __shfl_down_sync(FULL, pick, 1);
             const int pl = __shfl_up_sync(FULL, pick, 1);
-            if (lane + 1 < n && pick == lane && pr == lane) x = __dmul_rn(__dadd_rn(x, xr), 0.5);
-            else if (lane >= 1 && lane < n && pick == lane - 1 && pl == lane - 1)
-                x = __dmul_rn(__dadd_rn(xl, x), 0.5);
+            const bool mR = hasR && pick == lane && pr == lane;
+            const bool mL = hasL && pick == lane - 1 && pl == lane - 1;
+            x = mR ? avgR : (mL ? avgL : x);
         }
         __syncwarp();
         double acc = 0.0;
@@ -777,18 +758,18 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-// Small batches (the per-step hot path): 4 warps per instance search 128
-// candidates per round.  Large batches: 1 warp per instance (one wave).
+// Small batches (the per-step hot path): 8 warps per instance, a 9-ary
+// search.  Large batches: 1 warp per instance (binary search, one wave).
 static bool latency_mode(const SolveArgs &a) { return a.n_inst <= 4 * 148; }
 
 cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s) {
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
     const bool lm = latency_mode(a);
     if (a.mem) {
-        if (lm) k_partition<true, 4><<<a.n_inst, 128, sm, s>>>(a);
+        if (lm) k_partition<true, 8><<<a.n_inst, 256, sm, s>>>(a);
         else k_partition<true, 1><<<a.n_inst, 32, sm, s>>>(a);
     } else {
-        if (lm) k_partition<false, 4><<<a.n_inst, 128, sm, s>>>(a);
+        if (lm) k_partition<false, 8><<<a.n_inst, 256, sm, s>>>(a);
         else k_partition<false, 1><<<a.n_inst, 32, sm, s>>>(a);
     }
     return cudaGetLastError();
@@ -805,10 +786,10 @@ cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s) {
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
     const bool lm = latency_mode(a);
     if (a.mem) {
-        if (lm) k_repack<true, 4><<<a.n_inst, 128, sm, s>>>(a);
+        if (lm) k_repack<true, 8><<<a.n_inst, 256, sm, s>>>(a);
         else k_repack<true, 1><<<a.n_inst, 32, sm, s>>>(a);
     } else {
-        if (lm) k_repack<false, 4><<<a.n_inst, 128, sm, s>>>(a);
+        if (lm) k_repack<false, 8><<<a.n_inst, 256, sm, s>>>(a);
         else k_repack<false, 1><<<a.n_inst, 32, sm, s>>>(a);
     }
     return cudaGetLastError();

@@ -33,7 +33,13 @@ def t(fn, iters=20, reps=20):
 
 
 res = {}
-for name, cost, n, with_mem in [("cfg2_mem", cost2, 8, True), ("cfg2_nomem", cost2, 8, False),
+import synth
+_sh = synth.GPTShape()
+_p = synth.cfg2_keep_probs(_sh, 0.9, 4)
+_pay = synth.cfg2_payload_bytes(_sh, _p)
+bench_mem = torch.as_tensor(_pay.astype(np.int64), device=dev)
+bench_cap = torch.tensor([int(1.5 * int(_pay.sum()) / 8)], dtype=torch.int64, device=dev)
+for name, cost, n, with_mem in [("cfg2_benchmem", cost2, 8, "bench"),("cfg2_mem", cost2, 8, True), ("cfg2_nomem", cost2, 8, False),
                                 ("cfg2_n1", cost2, 1, False), ("cfg2_n2", cost2, 2, False),
                                 ("small_L24_n4", np.arange(24) % 7, 4, False),
                                 ("L8_n2_tiny", np.ones(8, np.int64), 2, False),
@@ -42,7 +48,9 @@ for name, cost, n, with_mem in [("cfg2_mem", cost2, 8, True), ("cfg2_nomem", cos
     c = torch.as_tensor(np.asarray(cost, np.int64), device=dev)
     b = D.Batch([len(cost)], [n], device=dev)
     mem = cap = None
-    if with_mem:
+    if with_mem == "bench":
+        mem, cap = bench_mem, bench_cap
+    elif with_mem:
         mem = torch.ones(len(cost), dtype=torch.int64, device=dev) * 1000
         cap = torch.tensor([10 ** 9], dtype=torch.int64, device=dev)
     out = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=dev),
