@@ -9,6 +9,7 @@
 #include <cstdint>
 #include <map>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -342,6 +343,30 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     }
     std::vector<LayerInfo> info(n_local, LayerInfo{0, 0});
     std::vector<ProfTile> vec, sca;
+    // tile size: about two tiles per resident warp (small per-GPU inputs, e.g.
+    // 75 MB at 8 GPUs, must still spread over every SM), 4 KiB .. 32 KiB
+    uint32_t tile_bytes = kTileBytes;
+    {
+        int64_t total = 0;
+        bool hist = false;
+        for (int32_t i = 0; i < n_segs; ++i) {
+            const int k = h_segs[i].src_kind;
+            const int64_t ne = h_segs[i].n_elem < 0 ? 0 : h_segs[i].n_elem;
+            const int es = k == DYNMO_SRC_NZ_BF16 ? 2 : (k == DYNMO_SRC_NZ_F32 || k == DYNMO_SRC_EXPERT_I32) ? 4
+                           : k == DYNMO_SRC_EXPERT_I64 ? 8 : 1;
+            total += (k == DYNMO_SRC_MASK_BITS || k == DYNMO_SRC_TOKMASK_BITS) ? ne / 8 : ne * es;
+            hist |= k == DYNMO_SRC_EXIT_U8 || k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32;
+        }
+        const int64_t warps = (int64_t)ctx->num_sms * profile_blocks_per_sm(hist) * (kProfThreads / 32);
+        int64_t want = total / std::max<int64_t>(1, 2 * warps);
+        uint32_t t = 4096;
+        while (t < kTileBytes && (int64_t)t * 2 <= want) t *= 2;
+        tile_bytes = t;
+        if (const char *e = getenv("DYNMO_TILE_BYTES")) {  // tuning knob (multiple of 16)
+            const long v = atol(e);
+            if (v >= 16 && v % 16 == 0 && v <= (1l << 30)) tile_bytes = (uint32_t)v;
+        }
+    }
     bool any_exit = false, has_hist = false;
     int max_E = 0;
     int64_t bytes = 0;
@@ -398,14 +423,14 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
             if (n <= 0) return;
             sca.push_back(ProfTile{(const void *)a, (uint32_t)n, lay, (uint16_t)(op | OP_SCALAR), aux, bits});
         };
-        // head up to 16-byte alignment, aligned body in kTileBytes tiles, tail
+        // head up to 16-byte alignment, aligned body in tile_bytes tiles, tail
         int64_t head = (int64_t)((16 - (p & 15)) & 15);
         if (head > nb) head = nb;
         const int64_t body = ((nb - head) / 16) * 16;
         const int64_t tail = nb - head - body;
         add_scalar(p, head, 0);
-        for (int64_t o = 0; o < body; o += kTileBytes) {
-            const int64_t len = std::min<int64_t>(kTileBytes, body - o);
+        for (int64_t o = 0; o < body; o += tile_bytes) {
+            const int64_t len = std::min<int64_t>(tile_bytes, body - o);
             vec.push_back(ProfTile{(const void *)(p + head + o), (uint32_t)len, lay, (uint16_t)op, aux, 0});
         }
         add_scalar(p + head + body, tail, 0);

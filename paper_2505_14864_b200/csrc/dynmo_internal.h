@@ -46,7 +46,7 @@ struct LayerInfo {
 };
 
 constexpr int kProfThreads = 256;
-constexpr uint32_t kTileBytes = 32u << 10;   // vector tile size
+constexpr uint32_t kTileBytes = 32u << 10;   // max vector tile size (plan picks 4..32 KiB)
 constexpr int kExitBins = 256;
 constexpr int kColExperts = 64;              // E <= 64: per-lane columns in smem
 constexpr int kMaxExperts = 1024;

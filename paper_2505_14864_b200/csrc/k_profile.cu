@@ -116,8 +116,21 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
         for (int i = lane; i < kWarpWords; i += 32) sh[i] = 0u;
         __syncwarp();
     }
-    for (int64_t ti = warp; ti < a.n_tiles; ti += nwarps) {
-        const ProfTile t = a.tiles[ti];
+    // Each warp walks a CONTIGUOUS range of tiles: consecutive tiles mostly
+    // belong to the same layer, so counts accumulate in a register and one
+    // atomic is issued per (layer, slot) run instead of one per tile (thousands
+    // of same-address atomics serialise in L2 when a layer spans many tiles).
+    // The next tile descriptor is prefetched while the current one streams.
+    const int64_t per = (a.n_tiles + nwarps - 1) / nwarps;
+    const int64_t t_beg = warp * per;
+    const int64_t t_end = t_beg + per < a.n_tiles ? t_beg + per : a.n_tiles;
+    int64_t run_key = -1;
+    unsigned long long run_sum = 0;
+    ProfTile nxt;
+    if (t_beg < t_end) nxt = a.tiles[t_beg];
+    for (int64_t ti = t_beg; ti < t_end; ++ti) {
+        const ProfTile t = nxt;
+        if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
         const int kind = t.op & 0xF;
         const bool scalar = (t.op & OP_SCALAR) != 0;
         if (kind <= OP_NZ32) {
@@ -135,8 +148,13 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                 }
             }
             c = __reduce_add_sync(0xFFFFFFFFu, c);
-            if (lane == 0 && c)
-                atomicAdd(&a.acc[(int64_t)t.layer * ACC_N + t.aux], (unsigned long long)c);
+            const int64_t key = (int64_t)t.layer * ACC_N + t.aux;
+            if (key != run_key) {
+                if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
+                run_key = key;
+                run_sum = 0;
+            }
+            run_sum += c;
             continue;
         }
         if constexpr (HAS_HIST) {
@@ -232,6 +250,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
             if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
         }
     }
+    if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
 }
 
 // -------------------------------------------------------------- epilogue
