@@ -54,6 +54,9 @@ def parse():
                     help="cost exchange over NVLink peer memory (default) or ncclAllGather")
     ap.add_argument("--migrate", choices=["p2p", "nccl"], default="p2p",
                     help="layer migration over NVLink peer memory (default) or NCCL send/recv")
+    ap.add_argument("--host-migrate", action="store_true",
+                    help="host-driven migration (D2H of the boundaries, then the migrate call) "
+                         "instead of the device-driven call inside the step's graph")
     ap.add_argument("--serial-solvers", action="store_true",
                     help="run partition, diffusion and repack one after another on one stream")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
@@ -292,21 +295,18 @@ def run_dynmo(args):
     comm = torch.cuda.Stream(device=dev)
     ev_res = torch.cuda.Event(external=True)  # in-graph record node after the result D2H
     n_host = nb + 2                            # boundaries + partition & profile status
+    d_bold = torch.from_numpy(b_old.astype(np.int32)).to(dev)
+    d_ranks = torch.from_numpy(ranks.astype(np.int32)).to(dev)
+    d_bytes = torch.zeros(2, dtype=torch.int64, device=dev)
+    # device-driven migration (G > 1, peer memory): the whole step is one graph
+    dev_mig = G > 1 and args.migrate == "p2p" and not args.host_migrate
+    pmig = None
 
     def solve_async():
-        """profile -> partition -> D2H of the boundaries (host-critical branch);
+        """profile -> partition [-> device-driven migration] on the main branch,
         diffusion and repack on two side branches, joined at the end."""
         main = torch.cuda.current_stream()
         D.profile_layers(ctx, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=pst)
-        if args.serial_solvers:
-            D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
-                               imbalance=part["imb"], status=part["st"])
-            res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
-            ev_res.record(main)
-            D.diffuse_balance(ctx, batch, cost, bnd_in, mem=mem, cap=cap, gamma=gamma, gamma_fluid=gamma_f,
-                              max_rounds=256, out=dif_out)
-            D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
-            return
         for sd in side:
             sd.wait_stream(main)
         with torch.cuda.stream(side[0]):
@@ -316,6 +316,8 @@ def run_dynmo(args):
             D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
         D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
                            imbalance=part["imb"], status=part["st"])
+        if dev_mig and pmig is not None:
+            pmig.device(d_bold, d_ranks, part["bnd"], d_ranks, d_bytes[0:1], d_bytes[1:2])
         res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
         ev_res.record(main)
         for sd in side:
@@ -329,7 +331,7 @@ def run_dynmo(args):
             graph.replay()
         else:
             solve_async()
-        ev_res.synchronize()  # the one D2H boundary: NCCL needs host counts
+        ev_res.synchronize()  # result D2H (host-driven migration needs the boundaries)
         return res_h.numpy()[:n_host].copy()
 
     # first step: learn the new split, allocate the receive buffers
@@ -342,14 +344,23 @@ def run_dynmo(args):
     for layer, src, dst in moves:
         if dst == rank:
             recv[int(layer)] = [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
-    migrator = (D.PeerMigrator(ctx, L, send, recv) if G > 1 and args.migrate == "p2p"
-                else D.Migrator(ctx, L, send, recv))
+    if G > 1 and args.migrate == "p2p":
+        pmig = migrator = D.PeerMigrator(ctx, L, send, recv)
+    else:
+        migrator = D.Migrator(ctx, L, send, recv)
 
     def step():
+        if dev_mig:
+            # one graph launch: no host round trip inside the step
+            if graph is not None:
+                graph.replay()
+            else:
+                solve_async()
+            return None
         r = solve()
         main = torch.cuda.current_stream()
-        # the host has seen the partition, so the all-gather is complete: the
-        # NCCL send/recv runs on its own stream, overlapping the side branches
+        # the host has seen the partition, so the exchange is complete: the
+        # migration runs on its own stream, overlapping the side branches
         with torch.cuda.stream(comm):
             sr = migrator(b_old, ranks, r[:N_STAGES + 1], ranks)
         main.wait_stream(comm)
@@ -391,7 +402,9 @@ def run_dynmo(args):
             flush.fill_(k & 0xFF)
             step_barrier()
             ev[k][0].record(stream)
-            sent_recv = step()
+            sr = step()
+            if sr is not None:
+                sent_recv = sr
             ev[k][1].record(stream)
             ev[k][1].synchronize()  # outside the timed interval: fold the phase events
             ctx.timing_poll()
@@ -408,6 +421,8 @@ def run_dynmo(args):
     launches = sum(phases[p][1] for p in ("profile", "epilogue", "partition", "diffuse", "repack")) + \
         (phases["exchange"][1] if G > 1 else 0)  # k_unpack (the all-gather itself is NCCL's)
     mig_ms = phases["migrate"][0] / max(phases["migrate"][1], 1) if phases["migrate"][1] else 0.0
+    if dev_mig:
+        sent_recv = tuple(int(v) for v in d_bytes.cpu().tolist())
 
     # ---- e2e: host buffers, H2D of this step's masks + D2H of the result inside
     pinned = [torch.from_numpy(m).pin_memory() for _, m in inp.masks]
@@ -422,6 +437,8 @@ def run_dynmo(args):
         for t, p in zip(dmask, pinned):
             t.copy_(p, non_blocking=True)
         step()
+        if dev_mig:
+            ev_res.synchronize()  # the result has reached the host
         b.record(stream)
         torch.cuda.synchronize()
         e2e.append(a.elapsed_time(b))
@@ -442,6 +459,11 @@ def run_dynmo(args):
         peaks, peak_src = load_peaks()
         ms = total_ms / args.steps
         cfg = workload_config(G)
+        cfg["exchange"] = ("peer-memory" if args.exchange == "p2p" else "nccl-allgather") if G > 1 else "none (G=1)"
+        cfg["migration"] = ("none (G=1)" if G == 1 else "device-driven peer-memory pull, in the step graph"
+                            if dev_mig else "host-driven peer-memory pull" if args.migrate == "p2p"
+                            else "host-driven NCCL send/recv")
+        cfg["graph"] = bool(args.graph)
         cost_h = cost.cpu().numpy()
         x_old = np.add.reduceat(cost_h, b_old[:-1])
         x_new = np.add.reduceat(cost_h, b_new[:-1])

@@ -345,6 +345,20 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan plan, int32_t n
                                       int32_t n_new, const int32_t *h_bnd_new,
                                       const int32_t *h_rank_new, int64_t *h_bytes_sent,
                                       int64_t *h_bytes_recv, dynmo_stream stream);
+/* Device-driven variant: the boundaries and stage->rank maps are DEVICE
+ * arrays (e.g. straight from partition_stages / repack_workers), every kernel
+ * derives the moves itself, and the ready/done epochs are device-side, so
+ * there is no host round trip and the call can be captured in a CUDA graph
+ * together with profile + partition (the whole rebalancing step is then one
+ * graph launch).  Collective like call 5 (same call sequence on every rank).
+ * n_old / n_new: stage counts of the two maps; n_layers <= 1023.  An invalid
+ * boundary vector or a wait timeout sets the sticky peer error.
+ * d_bytes_sent / d_bytes_recv (nullable): this rank's bytes (device). */
+dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
+                                      const int32_t *d_bnd_old, const int32_t *d_rank_old,
+                                      int32_t n_new, const int32_t *d_bnd_new,
+                                      const int32_t *d_rank_new, int64_t *d_bytes_sent,
+                                      int64_t *d_bytes_recv, dynmo_stream stream);
 /* Sticky device error of the peer-memory paths (0 = none); synchronous. */
 dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
 

@@ -71,6 +71,7 @@ def lib():
         "dynmo_migrate_plan_destroy": (None, [p]),
         "dynmo_migrate_layers_p2p": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
         "dynmo_ctx_p2p_error": (i32, [p, p]),
+        "dynmo_migrate_layers_dev": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -87,4 +88,5 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers",
             "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",
             "dynmo_migrate_layers", "dynmo_migration_plan", "dynmo_migrate_plan_create",
-            "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error"]
+            "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",
+            "dynmo_migrate_layers_dev"]

@@ -844,6 +844,8 @@ struct dynmo_mplan_s {
     std::vector<dynmo_buf> recv;                        // [n_layers * n_bufs] (this rank)
     std::map<std::pair<int, int64_t>, dynmo_buf> src;   // (rank, layer*n_bufs+k) -> readable ptr
     std::vector<void *> opened;                         // IPC mappings to close
+    DevBuf *d_src_tab = nullptr;                        // [nranks][n_layers*n_bufs] (device path)
+    DevBuf *d_recv_tab = nullptr;                       // [n_layers*n_bufs]
 };
 
 namespace {
@@ -934,6 +936,19 @@ dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t 
         for (int64_t k = 0; k < c[1]; ++k)
             mp->src[{r, rr[k].idx}] = dynmo_buf{mapped[rr[k].handle] + rr[k].offset, rr[k].bytes};
     }
+    // device tables for dynmo_migrate_layers_dev
+    std::vector<DevBuf> st_h((size_t)ctx->nranks * nb, DevBuf{nullptr, 0}), rt_h(nb, DevBuf{nullptr, 0});
+    for (auto &kv : mp->src)
+        st_h[(size_t)kv.first.first * nb + kv.first.second] = DevBuf{kv.second.d_ptr, kv.second.bytes};
+    for (int64_t i = 0; i < nb; ++i) rt_h[i] = DevBuf{h_recv[i].d_ptr, h_recv[i].bytes};
+    if (cudaMalloc((void **)&mp->d_src_tab, sizeof(DevBuf) * st_h.size()) != cudaSuccess ||
+        cudaMalloc((void **)&mp->d_recv_tab, sizeof(DevBuf) * rt_h.size()) != cudaSuccess ||
+        cudaMemcpy(mp->d_src_tab, st_h.data(), sizeof(DevBuf) * st_h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(mp->d_recv_tab, rt_h.data(), sizeof(DevBuf) * rt_h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+        dynmo_status e = cuda_fail(cudaGetLastError(), "migrate plan tables");
+        dynmo_migrate_plan_destroy(mp);
+        return e;
+    }
     *out = mp;
     return DYNMO_OK;
 }
@@ -942,7 +957,43 @@ void dynmo_migrate_plan_destroy(dynmo_mplan mp) {
     if (!mp) return;
     DeviceGuard g(mp->ctx->device);
     for (void *p : mp->opened) cudaIpcCloseMemHandle(p);
+    if (mp->d_src_tab) cudaFree(mp->d_src_tab);
+    if (mp->d_recv_tab) cudaFree(mp->d_recv_tab);
     delete mp;
+}
+
+dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,
+                                      const int32_t *d_bnd_old, const int32_t *d_rank_old,
+                                      int32_t n_new, const int32_t *d_bnd_new,
+                                      const int32_t *d_rank_new, int64_t *d_bytes_sent,
+                                      int64_t *d_bytes_recv, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (!d_bnd_old || !d_rank_old || !d_bnd_new || !d_rank_new) return invalid("null boundary/rank array");
+    if (n_old < 1 || n_new < 1 || n_old > mp->n_layers || n_new > mp->n_layers) return invalid("bad stage count");
+    if (mp->n_layers > 1023) return invalid("n_layers > 1023");
+    DevMigArgs a{};
+    a.n_layers = mp->n_layers;
+    a.n_bufs = mp->n_bufs;
+    a.me = ctx->rank;
+    a.nranks = ctx->nranks;
+    a.n_old = n_old;
+    a.n_new = n_new;
+    a.bnd_old = d_bnd_old;
+    a.rank_old = d_rank_old;
+    a.bnd_new = d_bnd_new;
+    a.rank_new = d_rank_new;
+    a.src_tab = mp->d_src_tab;
+    a.recv_tab = mp->d_recv_tab;
+    a.win = ctx->d_win;
+    for (int r = 0; r < ctx->nranks; ++r) a.peer_win[r] = ctx->peer_win[r];
+    a.bytes_sent = d_bytes_sent;
+    a.bytes_recv = d_bytes_recv;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
+    CUDA_TRY(launch_mig_dev(a, ctx->num_sms, s), "migration kernels launch");
+    phase_end(te, s);
+    return DYNMO_OK;
 }
 
 dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,

@@ -143,7 +143,31 @@ struct PeerWindow {
     uint64_t exch_epoch;        // this rank's profile-exchange epoch counter
     unsigned int pull_ctr;      // last-block counter of k_pull
     int32_t err;                // sticky error (timeouts)
+    // device-driven migration (dynmo_migrate_layers_dev): own flags/epochs
+    uint64_t dready[kMaxRanksEpi];
+    uint64_t ddone[kMaxRanksEpi];
+    uint64_t mig_dev_epoch;
+    unsigned int dpull_ctr;
 };
+
+struct DevBuf {
+    void *ptr;
+    int64_t bytes;
+};
+
+// Device-driven migration: boundaries and stage->rank maps on the device;
+// every kernel derives the moves itself (no host round trip, graph-safe).
+struct DevMigArgs {
+    int32_t n_layers, n_bufs, me, nranks;
+    int32_t n_old, n_new;
+    const int32_t *bnd_old, *rank_old, *bnd_new, *rank_new;
+    const DevBuf *src_tab;   // [nranks][n_layers * n_bufs], readable from this rank
+    const DevBuf *recv_tab;  // [n_layers * n_bufs], this rank's receive buffers
+    PeerWindow *win;
+    PeerWindow *peer_win[kMaxRanksEpi];
+    int64_t *bytes_sent, *bytes_recv;  // nullable
+};
+cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, cudaStream_t s);
 
 struct P2PItem {
     const void *src;

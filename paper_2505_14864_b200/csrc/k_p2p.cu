@@ -102,7 +102,176 @@ __global__ void __launch_bounds__(kP2PThreads) k_pull(P2PPull p) {
     }
 }
 
+// ------------------------------------------------ device-driven migration
+// Stage of layer i under boundaries b[0..n] (binary search).
+__device__ __forceinline__ int stage_of(const int32_t *b, int n, int i) {
+    int lo = 0, hi = n - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (b[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ bool valid_split(const int32_t *b, int n, int L) {
+    if (n < 1 || b[0] != 0 || b[n] != L) return false;
+    for (int s = 0; s < n; ++s)
+        if (b[s + 1] <= b[s]) return false;
+    return true;
+}
+
+// Block-local view of the migration: the layers this rank receives (and
+// from whom), the set of its senders and of its receivers.
+struct MigView {
+    int n_in;
+    unsigned senders, receivers;
+    int ok;
+};
+
+__device__ void mig_view(const DevMigArgs &a, MigView &v, int16_t *in_layers, int8_t *in_src) {
+    if (threadIdx.x == 0) {
+        v.n_in = 0;
+        v.senders = v.receivers = 0u;
+        v.ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers);
+    }
+    __syncthreads();
+    if (v.ok) {
+        for (int i = threadIdx.x; i < a.n_layers; i += blockDim.x) {
+            const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
+            const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
+            if (src == dst) continue;
+            if (dst == a.me) {
+                const int k = atomicAdd(&v.n_in, 1);
+                in_layers[k] = (int16_t)i;
+                in_src[k] = (int8_t)src;
+                atomicOr(&v.senders, 1u << src);
+            }
+            if (src == a.me) atomicOr(&v.receivers, 1u << dst);
+        }
+    }
+    __syncthreads();
+}
+
+// Sender side: advance the device epoch, release ready[me] at every receiver.
+__global__ void k_mig_signal(DevMigArgs a) {
+    __shared__ unsigned s_recv;
+    __shared__ int s_ok;
+    __shared__ unsigned long long s_sent;
+    if (threadIdx.x == 0) {
+        s_recv = 0u;
+        s_sent = 0ull;
+        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers);
+    }
+    __syncthreads();
+    if (s_ok)
+        for (int i = threadIdx.x; i < a.n_layers; i += blockDim.x) {
+            const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
+            const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
+            if (src == a.me && dst != a.me) {
+                atomicOr(&s_recv, 1u << dst);
+                unsigned long long b = 0;
+                const DevBuf *row = a.src_tab + ((int64_t)a.me * a.n_layers + i) * a.n_bufs;
+                for (int k = 0; k < a.n_bufs; ++k) b += (unsigned long long)row[k].bytes;
+                atomicAdd(&s_sent, b);
+            }
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint64_t epoch = a.win->mig_dev_epoch + 1;
+        a.win->mig_dev_epoch = epoch;
+        if (!s_ok) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+        for (int r = 0; r < a.nranks; ++r)
+            if (s_recv & (1u << r)) st_release_sys(&a.peer_win[r]->dready[a.me], epoch);
+        if (a.bytes_sent) *a.bytes_sent = (int64_t)s_sent;
+    }
+}
+
+// Receiver side: every block derives the incoming set, waits for the senders,
+// copies its grid-stride share of every incoming buffer; the last block
+// releases ddone[me] at every sender.
+__global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
+    __shared__ MigView v;
+    __shared__ int16_t in_layers[1024];
+    __shared__ int8_t in_src[1024];
+    __shared__ int s_ok;
+    mig_view(a, v, in_layers, in_src);
+    const uint64_t epoch = a.win->mig_dev_epoch;
+    if (threadIdx.x == 0) {
+        int ok = v.ok;
+        for (int r = 0; ok && r < a.nranks; ++r)
+            if (v.senders & (1u << r)) ok &= wait_flag(&a.win->dready[r], epoch);
+        if (!ok) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+        s_ok = ok;
+    }
+    __syncthreads();
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    unsigned long long recvd = 0;
+    if (s_ok) {
+        for (int it = 0; it < v.n_in; ++it) {
+            const int i = in_layers[it], src = in_src[it];
+            for (int k = 0; k < a.n_bufs; ++k) {
+                const int64_t idx = (int64_t)i * a.n_bufs + k;
+                const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
+                const DevBuf rb = a.recv_tab[idx];
+                const uint64_t bytes = (uint64_t)(sb.bytes < rb.bytes ? sb.bytes : rb.bytes);
+                recvd += bytes;
+                const uint8_t *sp = (const uint8_t *)sb.ptr;
+                uint8_t *dp = (uint8_t *)rb.ptr;
+                const bool vec = (((uintptr_t)sp | (uintptr_t)dp) & 15) == 0;
+                const uint64_t nvec = vec ? bytes >> 4 : 0;
+                const uint4 *s4 = (const uint4 *)sp;
+                uint4 *d4 = (uint4 *)dp;
+                uint64_t x = gt;
+                for (; x + 3 * gs < nvec; x += 4 * gs) {
+                    const uint4 q0 = s4[x], q1 = s4[x + gs], q2 = s4[x + 2 * gs], q3 = s4[x + 3 * gs];
+                    d4[x] = q0;
+                    d4[x + gs] = q1;
+                    d4[x + 2 * gs] = q2;
+                    d4[x + 3 * gs] = q3;
+                }
+                for (; x < nvec; x += gs) d4[x] = s4[x];
+                for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
+            }
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0 && a.bytes_recv) *a.bytes_recv = (int64_t)recvd;
+        const unsigned prev = atomicAdd(&a.win->dpull_ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            a.win->dpull_ctr = 0u;
+            __threadfence_system();
+            for (int r = 0; r < a.nranks; ++r)
+                if (v.senders & (1u << r)) st_release_sys(&a.peer_win[r]->ddone[a.me], epoch);
+        }
+    }
+}
+
+// Sender side again: wait until every receiver has finished reading.
+__global__ void k_mig_wait(DevMigArgs a) {
+    __shared__ MigView v;
+    __shared__ int16_t in_layers[1024];
+    __shared__ int8_t in_src[1024];
+    mig_view(a, v, in_layers, in_src);
+    if (threadIdx.x == 0 && v.ok) {
+        const uint64_t epoch = a.win->mig_dev_epoch;
+        for (int r = 0; r < a.nranks; ++r)
+            if (v.receivers & (1u << r))
+                if (!wait_flag(&a.win->ddone[r], epoch)) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, cudaStream_t s) {
+    k_mig_signal<<<1, 256, 0, s>>>(a);
+    k_mig_pull<<<grid, kP2PThreads, 0, s>>>(a);
+    k_mig_wait<<<1, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_signal(const P2PSignal &s, cudaStream_t st) {
     if (s.n == 0) return cudaSuccess;

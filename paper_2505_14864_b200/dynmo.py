@@ -377,6 +377,15 @@ class PeerMigrator:
                "dynmo_migrate_layers_p2p")
         return self._sent.value, self._rec.value
 
+    def device(self, bnd_old: torch.Tensor, rank_old: torch.Tensor, bnd_new: torch.Tensor,
+               rank_new: torch.Tensor, bytes_sent=None, bytes_recv=None, stream=None):
+        """dynmo_migrate_layers_dev: int32 device boundaries / stage->rank maps,
+        no host round trip (capturable in a CUDA graph)."""
+        _check(lib().dynmo_migrate_layers_dev(self.ctx.handle, self._h, rank_old.numel(), _ptr(bnd_old),
+                                              _ptr(rank_old), rank_new.numel(), _ptr(bnd_new), _ptr(rank_new),
+                                              _ptr(bytes_sent), _ptr(bytes_recv), _stream(stream)),
+               "dynmo_migrate_layers_dev")
+
     def error(self) -> int:
         e = C.c_int32(0)
         _check(lib().dynmo_ctx_p2p_error(self.ctx.handle, C.byref(e)), "dynmo_ctx_p2p_error")

@@ -118,6 +118,29 @@ def main():
         assert (s2, g2) == (want_sent, want_got), (rank, s2, g2)
         for l, bufs in recv.items():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, rep)
+    # device-driven variant: boundaries straight from the partition output,
+    # captured in a CUDA graph together with the partition (several replays)
+    d_bo, d_ro = torch.from_numpy(b_old.astype(np.int32)).to(dev), torch.from_numpy(ranks.astype(np.int32)).to(dev)
+    d_rn = d_ro.clone()
+    bs, br = torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev)
+    for bufs in recv.values():
+        bufs[0].zero_()
+    pm.device(d_bo, d_ro, bnd, d_rn, bs, br)
+    torch.cuda.synchronize()
+    assert (int(bs.item()), int(br.item())) == (want_sent, want_got), (rank, bs, br)
+    for l, bufs in recv.items():
+        assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "dev")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        D.partition_stages(ctx, b, cost, bnd=bnd)
+        pm.device(d_bo, d_ro, bnd, d_rn, bs, br)
+    for rep in range(4):
+        for bufs in recv.values():
+            bufs[0].zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for l, bufs in recv.items():
+            assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "graph", rep)
     assert pm.error() == 0
     pm.close()
     dist.barrier()

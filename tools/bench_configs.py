@@ -1,0 +1,232 @@
+"""Per-config device timings of the hot path on one B200 (BASELINE configs 1, 3,
+4, 5; config 2 is bench.py's headline).  Each config's device work is captured
+once in a CUDA graph and replayed; CUDA events around each replay (L2 flushed
+between replays by a 256 MiB write outside the events).  Results are checked
+against the oracle on the same seeded inputs before timing.  Prints one JSON
+object per config and writes gpurun_out/bench_configs.json.
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2505_14864_b200 import _lib as LB  # noqa: E402
+from paper_2505_14864_b200 import dynmo as D  # noqa: E402
+
+DEV = "cuda:0"
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+flush = None
+
+
+def timed(fn, reps=20):
+    """Device ms per replay of fn captured in a CUDA graph."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts)), g
+
+
+def dev(a, dt=None):
+    a = np.ascontiguousarray(a if dt is None else np.asarray(a).astype(dt))
+    return torch.from_numpy(a).to(DEV)
+
+
+def config1(ctx):
+    insts = synth.cfg1_instances(10_000)
+    out = {}
+    for with_mem in (True, False):
+        sel = [x for x in insts if (x["mem"] is not None) == with_mem]
+        b = D.Batch([24] * len(sel), [4] * len(sel), device=DEV)
+        cost = dev(np.concatenate([x["cost"] for x in sel]), np.int64)
+        mem = dev(np.concatenate([x["mem"] for x in sel]), np.int64) if with_mem else None
+        cap = dev([x["cap"] for x in sel], np.int64) if with_mem else None
+        bound = dev([x["bound"] for x in sel], np.int64)
+        floor = dev(np.ones(len(sel)), np.int32)
+        pout = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=DEV),
+                    bottleneck=torch.empty(b.n_inst, dtype=torch.int64, device=DEV),
+                    imbalance=torch.empty(b.n_inst, dtype=torch.float64, device=DEV),
+                    status=torch.empty(b.n_inst, dtype=torch.int32, device=DEV))
+        rout = {}
+
+        def step():
+            D.partition_stages(ctx, b, cost, mem=mem, cap=cap, **pout)
+            D.repack_workers(ctx, b, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rout)
+
+        ms, _ = timed(step)
+        # parity + oracle time on the same instances (1 core)
+        bn = b.split(pout["bnd"])
+        t0 = time.perf_counter()
+        for q, x in enumerate(sel):
+            st, ob, oB, _ = oracle.partition(x["cost"], 4, mem=x["mem"], cap=x["cap"])
+            rst, rk, rb, rB = oracle.repack_bound(x["cost"], 4, x["bound"], 1, mem=x["mem"], cap=x["cap"])
+            assert np.array_equal(bn[q][:5], ob)
+        t_or = time.perf_counter() - t0
+        out["mem" if with_mem else "nomem"] = dict(instances=len(sel), device_ms=round(ms, 4),
+                                                    instances_per_s=round(len(sel) / (ms * 1e-3)),
+                                                    oracle_ms=round(t_or * 1e3, 1))
+    return out
+
+
+def config3(ctx):
+    T, L, n = 512 * 2048, 32, 8
+    e = synth.cfg3_exit_depth(T=T, L=L)
+    fr = synth.cfg3_frozen(L, 8)
+    de = dev(e)
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(de, LB.SRC_EXIT_U8, 0)], 0, L)
+    coef = D.coef_tensor(L, A=1, device=DEV)
+    frozen = dev(fr)
+    cost = torch.empty(L, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    b = D.Batch([L], [n], device=DEV)
+    bi = dev(np.arange(0, L + 1, L // n), np.int32)
+    gf = torch.tensor([1.0], dtype=torch.float64, device=DEV)
+    dout = {}
+
+    def step():
+        D.profile_layers(ctx, plan, coef, frozen=frozen, cost=cost, status=st)
+        D.diffuse_balance(ctx, b, cost, bi, gamma_fluid=gf, max_rounds=256, out=dout)
+
+    ms, _ = timed(step)
+    tok = oracle.exit_survivors(e, 0, L)
+    want = np.array([oracle.layer_cost(frozen=bool(fr[i]), tok=int(tok[i]), A=1)[1] for i in range(L)])
+    assert np.array_equal(cost.cpu().numpy(), want)
+    dst, db, dr, _, _ = oracle.diffuse(want, np.arange(0, L + 1, L // n), 0, 256)
+    assert np.array_equal(dout["bnd"].cpu().numpy(), db)
+
+    def prof_only():
+        D.profile_layers(ctx, plan, coef, frozen=frozen, cost=cost, status=st)
+
+    pms, _ = timed(prof_only)
+    return dict(tokens=T, profile_bytes=int(plan.bytes), step_device_ms=round(ms, 4),
+                profile_device_ms=round(pms, 4), diffusion_rounds=int(dout["rounds"].item()),
+                fluid_rounds=int(dout["fluid_rounds"].item()))
+
+
+def config4(ctx, alpha):
+    T, L, E, k, n = 64 * 2048, 32, 8, 2, 8
+    segs, keep, hists = [], [], []
+    for i in range(L):
+        idx = synth.cfg4_routing(i, T=T, E=E, k=k, alpha=alpha)
+        hists.append(oracle.expert_hist(idx, E)[1])
+        d = dev(idx.reshape(-1))
+        keep.append(d)
+        segs.append(D.SegmentSpec(d, LB.SRC_EXPERT_I64, i, n_experts=E, top_k=k))
+    plan = D.ProfilePlan(ctx, segs, 0, L)
+    coef = D.coef_tensor(L, A=T, C_=4, ep=8, device=DEV)
+    cost = torch.empty(L, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    b = D.Batch([L], [n], device=DEV)
+    pout = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=DEV),
+                bottleneck=torch.empty(1, dtype=torch.int64, device=DEV),
+                imbalance=torch.empty(1, dtype=torch.float64, device=DEV),
+                status=torch.empty(1, dtype=torch.int32, device=DEV))
+
+    def step():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+        D.partition_stages(ctx, b, cost, **pout)
+
+    ms, _ = timed(step)
+    want = np.array([oracle.layer_cost(cnt=hists[i], A=T, C_=4, ep=8)[1] for i in range(L)])
+    assert np.array_equal(cost.cpu().numpy(), want)
+
+    def prof_only():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+
+    pms, _ = timed(prof_only)
+    return dict(alpha=alpha, profile_bytes=int(plan.bytes), step_device_ms=round(ms, 4),
+                profile_device_ms=round(pms, 4),
+                profile_GBps=round(plan.bytes / (pms * 1e-3) / 1e9, 1),
+                imbalance=round(float(pout["imbalance"].item()), 4))
+
+
+def config5(ctx, n_inst=4096):
+    insts = [synth.cfg5_instance(i) for i in range(n_inst)]
+    masks = np.concatenate([x.masks.reshape(-1) for x in insts])
+    dm = dev(masks.view(np.int32))
+    segs, layer, off = [], 0, 0
+    for x in insts:
+        for l in range(x.L):
+            segs.append(D.SegmentSpec(dm[off:off + 128], LB.SRC_TOKMASK_BITS, layer, n_elem=4096))
+            off += 128
+            layer += 1
+    plan = D.ProfilePlan(ctx, segs, 0, layer)
+    coef = D.coef_tensor(layer, A=1, device=DEV)
+    cost = torch.empty(layer, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    b = D.Batch([x.L for x in insts], [x.n for x in insts], device=DEV)
+    mem = dev(np.concatenate([x.mem for x in insts]), np.int64)
+    cap = dev([x.cap for x in insts], np.int64)
+    bound = dev([x.bound for x in insts], np.int64)
+    floor = dev(np.ones(n_inst), np.int32)
+    pout = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=DEV),
+                bottleneck=torch.empty(n_inst, dtype=torch.int64, device=DEV),
+                imbalance=torch.empty(n_inst, dtype=torch.float64, device=DEV),
+                status=torch.empty(n_inst, dtype=torch.int32, device=DEV))
+    rout = {}
+
+    def step():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+        D.partition_stages(ctx, b, cost, mem=mem, cap=cap, **pout)
+        D.repack_workers(ctx, b, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rout)
+
+    ms, _ = timed(step, reps=10)
+
+    def prof_only():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+
+    pms, _ = timed(prof_only, reps=10)
+    # parity on a sample of instances
+    ch = cost.cpu().numpy()
+    bn, kn = b.split(pout["bnd"]), rout["n_new"].cpu().numpy()
+    for q in range(0, n_inst, 64):
+        x = insts[q]
+        c = ch[b.layer_off_h[q]:b.layer_off_h[q + 1]]
+        assert np.array_equal(c, [oracle.count_bits(x.masks[l], 4096) for l in range(x.L)])
+        ost, ob, oB, _ = oracle.partition(c, x.n, mem=x.mem, cap=x.cap)
+        assert np.array_equal(bn[q][:x.n + 1], ob)
+        assert kn[q] == oracle.repack_bound(c, x.n, x.bound, 1, mem=x.mem, cap=x.cap)[1]
+    return dict(instances=n_inst, layers=layer, profile_bytes=int(plan.bytes), step_device_ms=round(ms, 4),
+                instances_per_s=round(n_inst / (ms * 1e-3)), profile_device_ms=round(pms, 4),
+                profile_GBps=round(plan.bytes / (pms * 1e-3) / 1e9, 1),
+                mean_workers_after_repack=round(float(kn.mean()), 3),
+                mean_workers_before=round(float(np.mean([x.n for x in insts])), 3))
+
+
+def main():
+    global flush
+    torch.cuda.set_device(0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=DEV)
+    ctx = D.Context(0)
+    res = {}
+    for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
+                     ("config4_auxloss", lambda: config4(ctx, 4.0)), ("config4_sbase", lambda: config4(ctx, 64.0)),
+                     ("config5", lambda: config5(ctx))]:
+        res[name] = fn()
+        print(name, json.dumps(res[name]), flush=True)
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    json.dump(res, open(os.path.join(ROOT, "gpurun_out", "bench_configs.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
