@@ -89,6 +89,8 @@ enum {
     DYNMO_PHASE_MIGRATE = 6,   /* NCCL send/recv group of migrate_layers   */
     DYNMO_NUM_PHASES = 7
 };
+/* enable: 0 off, 1 every phase, otherwise a bitmask (bit p = phase p, e.g.
+ * 1 << DYNMO_PHASE_PROFILE only; -1 = all). */
 dynmo_status dynmo_ctx_set_timing(dynmo_ctx ctx, int32_t enable);
 dynmo_status dynmo_ctx_timing_poll(dynmo_ctx ctx);
 dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total_ms,

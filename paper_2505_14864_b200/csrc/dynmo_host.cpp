@@ -59,7 +59,7 @@ struct dynmo_ctx_s {
     int device = 0, nranks = 1, rank = 0;
     ncclComm_t comm = nullptr;
     int num_sms = 148;
-    bool timing = false;
+    int32_t timing = 0;  // bitmask of timed phases
     PhaseTimer ph[DYNMO_NUM_PHASES];
     // peer-memory window (nranks > 1): local flags + every peer's, mapped
     PeerWindow *d_win = nullptr;
@@ -113,7 +113,7 @@ namespace {
 // the graph (re-recorded at every replay; read them with timing_poll after
 // each replay).
 cudaEvent_t phase_begin(dynmo_ctx c, int phase, cudaStream_t s) {
-    if (!c->timing) return nullptr;
+    if (!(c->timing & (1 << phase))) return nullptr;
     PhaseTimer &t = c->ph[phase];
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cs);
@@ -273,7 +273,7 @@ void dynmo_ctx_destroy(dynmo_ctx ctx) {
 
 dynmo_status dynmo_ctx_set_timing(dynmo_ctx ctx, int32_t enable) {
     if (!ctx) return invalid("null ctx");
-    ctx->timing = enable != 0;
+    ctx->timing = enable == 1 ? -1 : enable;  // 1 (true) = every phase, else a bitmask
     return DYNMO_OK;
 }
 

@@ -88,8 +88,16 @@ class Context:
     def handle(self):
         return self._h
 
-    def set_timing(self, enable: bool = True):
-        _check(lib().dynmo_ctx_set_timing(self._h, int(enable)), "dynmo_ctx_set_timing")
+    def set_timing(self, enable=True, phases=None):
+        """enable all phases, or only `phases` (names from _lib.PHASES)."""
+        mask = 0
+        if phases is not None:
+            for p in phases:
+                mask |= 1 << _L.PHASES.index(p)
+            mask = mask if mask != 1 else 1 | (1 << 31)  # 1 alone means "all" in the C-ABI
+        else:
+            mask = -1 if enable else 0
+        _check(lib().dynmo_ctx_set_timing(self._h, int(mask) if enable else 0), "dynmo_ctx_set_timing")
 
     def timing_poll(self):
         """Fold the phase events of the last graph replay into the accumulators."""
