@@ -142,6 +142,8 @@ struct dynmo_plan_s {
     dynmo_ctx ctx = nullptr;
     int32_t layer_begin = 0, n_local = 0, n_total = 0, exchange = 0, max_E = 0;
     bool has_hist = false;
+    int32_t warp_words = 1;
+    int32_t ops = 1;
     int64_t n_tiles = 0, bytes = 0;
     int grid = 1;
     void *dmem = nullptr;
@@ -348,16 +350,22 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     uint32_t tile_bytes = kTileBytes;
     {
         int64_t total = 0;
-        bool hist = false;
+        bool pre_exit = false;
+        int pre_E = 0, pre_ops = 0;
         for (int32_t i = 0; i < n_segs; ++i) {
             const int k = h_segs[i].src_kind;
+            if (k == DYNMO_SRC_EXIT_U8) pre_exit = true;
+            if (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) pre_E = std::max(pre_E, (int)h_segs[i].n_experts);
+            pre_ops |= k == DYNMO_SRC_EXIT_U8 ? 2 : (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) ? 4 : 1;
             const int64_t ne = h_segs[i].n_elem < 0 ? 0 : h_segs[i].n_elem;
             const int es = k == DYNMO_SRC_NZ_BF16 ? 2 : (k == DYNMO_SRC_NZ_F32 || k == DYNMO_SRC_EXPERT_I32) ? 4
                            : k == DYNMO_SRC_EXPERT_I64 ? 8 : 1;
             total += (k == DYNMO_SRC_MASK_BITS || k == DYNMO_SRC_TOKMASK_BITS) ? ne / 8 : ne * es;
-            hist |= k == DYNMO_SRC_EXIT_U8 || k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32;
         }
-        const int64_t warps = (int64_t)ctx->num_sms * profile_blocks_per_sm(hist) * (kProfThreads / 32);
+        const int64_t warps = (int64_t)ctx->num_sms *
+                              profile_blocks_per_sm(pre_ops ? pre_ops : 1,
+                                                    profile_warp_words(pre_exit, std::min(pre_E, kMaxExperts))) *
+                              (kProfThreads / 32);
         int64_t want = total / std::max<int64_t>(1, 2 * warps);
         uint32_t t = 4096;
         while (t < kTileBytes && (int64_t)t * 2 <= want) t *= 2;
@@ -526,7 +534,14 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     }
     const int warps_per_block = kProfThreads / 32;
     const int64_t want = (pl->n_tiles + warps_per_block - 1) / warps_per_block;
-    const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(has_hist);
+    pl->warp_words = profile_warp_words(any_exit, max_E);
+    pl->ops = 0;
+    for (const ProfTile &t : tiles) {
+        const int k = t.op & 0xF;
+        pl->ops |= k <= OP_NZ32 ? 1 : k == OP_EXIT ? 2 : 4;
+    }
+    if (!pl->ops) pl->ops = 1;
+    const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(pl->ops, pl->warp_words);
     pl->grid = (int)std::max<int64_t>(1, std::min(want, cap_blocks));
     *out = pl;
     return DYNMO_OK;
@@ -556,9 +571,9 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     cudaStream_t s = (cudaStream_t)stream;
     DeviceGuard g(ctx->device);
     ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
-                std::max(1, plan->max_E), plan->d_ws_status};
+                std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words};
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PROFILE, s);
-    CUDA_TRY(launch_profile(pa, plan->has_hist, plan->grid, s), "k_profile launch");
+    CUDA_TRY(launch_profile(pa, plan->ops, plan->grid, s), "k_profile launch");
     phase_end(te, s);
     EpiArgs ea{};
     ea.layer_begin = plan->layer_begin;

@@ -59,6 +59,7 @@ struct ProfArgs {
     unsigned long long *exit_hist;  // [kExitBins]
     int32_t max_E;
     int32_t *ws_status;
+    int32_t warp_words;  // per-warp histogram scratch (u32 words)
 };
 
 struct PeerWindow;
@@ -89,8 +90,16 @@ struct EpiArgs {
     int32_t *status_out;     // local mode final status
 };
 
-cudaError_t launch_profile(const ProfArgs &a, bool has_hist, int grid, cudaStream_t s);
-int profile_blocks_per_sm(bool has_hist);
+// ops: bit 0 count ops, bit 1 exit histogram, bit 2 expert histograms
+cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s);
+int profile_blocks_per_sm(int ops, int warp_words);
+// per-warp histogram scratch words for a plan (exit bins / expert columns)
+inline int profile_warp_words(bool any_exit, int max_E) {
+    int w = any_exit ? kExitBins : 0;
+    // E <= 16 counts in registers; up to 64 in lane-private smem columns
+    const int e = max_E <= 16 ? 0 : max_E <= kColExperts ? 32 * max_E : max_E;
+    return w > e ? w : (e > 0 ? e : 1);
+}
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,

@@ -100,20 +100,36 @@ __device__ __forceinline__ uint32_t count_scalar(const ProfTile &t, int kind, in
     return c;
 }
 
-template <bool HAS_HIST>
+__device__ __forceinline__ uint32_t count_vec_rt(int kind, uint4 v) {
+    switch (kind) {
+        case OP_POPC: return count_vec<OP_POPC>(v);
+        case OP_NZ8: return count_vec<OP_NZ8>(v);
+        case OP_NZ16: return count_vec<OP_NZ16>(v);
+        default: return count_vec<OP_NZ32>(v);
+    }
+}
+
+__device__ __forceinline__ bool small_count_tile(const ProfTile &t) {
+    return (t.op & 0xF) <= OP_NZ32 && !(t.op & OP_SCALAR) && (t.nbytes >> 4) <= 32;
+}
+
+// OPS: bit 0 count ops present, bit 1 exit histogram, bit 2 expert histograms
+// (paths of absent op families are compiled out: fewer registers).
+template <int OPS>
 __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
+    constexpr bool HAS_CNT = OPS & 1, HAS_EXIT = (OPS & 2) != 0, HAS_EXP = (OPS & 4) != 0;
+    constexpr bool HAS_HIST = HAS_EXIT || HAS_EXP;
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int64_t warp = (int64_t)blockIdx.x * (kProfThreads / 32) + wib;
     const int64_t nwarps = (int64_t)gridDim.x * (kProfThreads / 32);
-    // Per-warp scratch for histogram ops: max(kColExperts*32, kExitBins,
-    // kMaxExperts) u32 words.  Zero at entry and after every flush.
+    // Per-warp histogram scratch (a.warp_words u32, sized by the plan: exit
+    // bins and/or expert columns); zero at entry and after every flush.
     uint32_t *sh = nullptr;
-    constexpr int kWarpWords = kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts;
     if constexpr (HAS_HIST) {
-        sh = smem + wib * kWarpWords;
-        for (int i = lane; i < kWarpWords; i += 32) sh[i] = 0u;
+        sh = smem + wib * a.warp_words;
+        for (int i = lane; i < a.warp_words; i += 32) sh[i] = 0u;
         __syncwarp();
     }
     // Each warp walks a CONTIGUOUS range of tiles: consecutive tiles mostly
@@ -126,14 +142,111 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
     const int64_t t_end = t_beg + per < a.n_tiles ? t_beg + per : a.n_tiles;
     int64_t run_key = -1;
     unsigned long long run_sum = 0;
+    int exit_dirty = 0;       // exit histogram pending in sh (flushed once at the end)
+    int hist_layer = -1;      // layer whose expert histogram is pending
+    int hist_E = 0;
+    uint32_t bad = 0;         // an expert id outside [0, E)
+    // E <= 16: one-hot 8-bit fields in registers (experts 0-7 in acc0, 8-15 in
+    // acc1), spilled every <= 240 entries per lane into mycnt (lane e holds
+    // the warp's count of expert e) with warp reductions
+    unsigned long long acc0 = 0, acc1 = 0;
+    uint32_t nacc = 0, mycnt = 0;
+    auto spill_regs = [&]() {
+        if (__any_sync(0xFFFFFFFFu, nacc != 0)) {
+#pragma unroll
+            for (int f = 0; f < 16; ++f) {
+                const uint32_t fv = (uint32_t)(((f < 8 ? acc0 : acc1) >> (8 * (f & 7))) & 0xFFull);
+                const uint32_t sum = __reduce_add_sync(0xFFFFFFFFu, fv);
+                if (lane == f) mycnt += sum;
+            }
+        }
+        acc0 = acc1 = 0;
+        nacc = 0;
+    };
+    auto feed = [&](int64_t key, uint32_t c) {
+        if (key != run_key) {
+            if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
+            run_key = key;
+            run_sum = 0;
+        }
+        run_sum += c;
+    };
+    auto flush_experts = [&]() {
+        if constexpr (HAS_HIST) {
+            if (hist_layer < 0) return;
+            unsigned long long *dst = a.hist + (int64_t)hist_layer * a.max_E;
+            if (hist_E <= 16) {
+                spill_regs();
+                if (lane < hist_E && mycnt) atomicAdd(&dst[lane], (unsigned long long)mycnt);
+                mycnt = 0;
+                hist_layer = -1;
+                return;
+            }
+            __syncwarp();
+            const bool cols = hist_E <= kColExperts;
+            for (int e = lane; e < hist_E; e += 32) {
+                uint32_t c = 0;
+                if (cols) {
+                    for (int l = 0; l < 32; ++l) {
+                        c += sh[e * 32 + l];
+                        sh[e * 32 + l] = 0u;
+                    }
+                } else {
+                    c = sh[e];
+                    sh[e] = 0u;
+                }
+                if (c) atomicAdd(&dst[e], (unsigned long long)c);
+            }
+            __syncwarp();
+            hist_layer = -1;
+        }
+    };
     ProfTile nxt;
     if (t_beg < t_end) nxt = a.tiles[t_beg];
     for (int64_t ti = t_beg; ti < t_end; ++ti) {
         const ProfTile t = nxt;
-        if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
         const int kind = t.op & 0xF;
         const bool scalar = (t.op & OP_SCALAR) != 0;
-        if (kind <= OP_NZ32) {
+        if (HAS_CNT && small_count_tile(t)) {
+            // Up to 8 consecutive small tiles (<= 512 B each, e.g. the
+            // 4096-token masks of config 5) per warp iteration: 4 lanes per
+            // tile, each streaming up to 8 of its tile's 16-byte vectors (all
+            // in flight together), a quad reduction, then the 8 results are
+            // fed to the run accumulator in tile order.
+            const int grp = lane >> 2, q = lane & 3;
+            const int64_t mt = ti + grp;
+            ProfTile mine = t;
+            if (grp > 0 && mt < t_end) mine = a.tiles[mt];
+            const bool ok = mt < t_end && small_count_tile(mine);
+            const unsigned okm = __ballot_sync(0xFFFFFFFFu, ok && q == 0);
+            // leading run of small tiles (group g <-> bit 4g)
+            int nb = 0;
+            while (nb < 8 && (okm >> (4 * nb)) & 1u) ++nb;
+            uint32_t c = 0;
+            if (grp < nb) {
+                const uint4 *p = (const uint4 *)mine.ptr;
+                const uint32_t nvec = mine.nbytes >> 4;
+                uint4 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t idx = (uint32_t)q + 4u * u;
+                    v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
+                }
+                const int kk = mine.op & 0xF;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) c += count_vec_rt(kk, v[u]);
+            }
+            c += __shfl_xor_sync(0xFFFFFFFFu, c, 1);
+            c += __shfl_xor_sync(0xFFFFFFFFu, c, 2);
+            const int64_t key = (int64_t)mine.layer * ACC_N + mine.aux;
+            for (int u = 0; u < nb; ++u)
+                feed(__shfl_sync(0xFFFFFFFFu, key, 4 * u), __shfl_sync(0xFFFFFFFFu, c, 4 * u));
+            ti += nb - 1;
+            if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
+            continue;
+        }
+        if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
+        if (HAS_CNT && kind <= OP_NZ32) {
             uint32_t c;
             if (scalar) {
                 c = count_scalar(t, kind, lane);
@@ -147,54 +260,118 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                     default: c = count_tile<OP_NZ32>(p, nvec, lane); break;
                 }
             }
-            c = __reduce_add_sync(0xFFFFFFFFu, c);
-            const int64_t key = (int64_t)t.layer * ACC_N + t.aux;
-            if (key != run_key) {
-                if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
-                run_key = key;
-                run_sum = 0;
-            }
-            run_sum += c;
+            feed((int64_t)t.layer * ACC_N + t.aux, __reduce_add_sync(0xFFFFFFFFu, c));
             continue;
         }
         if constexpr (HAS_HIST) {
-            if (kind == OP_EXIT) {
-                // uint8 exit depths -> warp histogram (shared atomics), flushed per tile
+            if (HAS_EXIT && kind == OP_EXIT) {
+                // uint8 exit depths -> warp histogram in sh[0..255] (shared
+                // atomics); flushed once when the warp's range is done
+                if (hist_layer >= 0) flush_experts();  // (scratch is shared)
+                exit_dirty = 1;
                 const uint8_t *b = (const uint8_t *)t.ptr;
                 if (scalar) {
                     if ((uint32_t)lane < t.nbytes) atomicAdd(&sh[b[lane]], 1u);
                 } else {
                     const uint4 *p = (const uint4 *)t.ptr;
                     const uint32_t nvec = t.nbytes >> 4;
-                    for (uint32_t i = lane; i < nvec; i += 32) {
-                        uint4 v = ld_stream(p + i);
-                        uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    for (uint32_t base = 0; base < nvec; base += 64u) {
+                        const uint32_t i0 = base + lane, i1 = base + 32 + lane;
+                        const uint4 v0 = i0 < nvec ? ld_stream(p + i0) : make_uint4(0u, 0u, 0u, 0u);
+                        const uint4 v1 = i1 < nvec ? ld_stream(p + i1) : make_uint4(0u, 0u, 0u, 0u);
+                        if (i0 < nvec) {
+                            const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
+                            for (int k = 0; k < 4; ++k)
 #pragma unroll
-                            for (int s = 0; s < 4; ++s) atomicAdd(&sh[(w[k] >> (8 * s)) & 0xFFu], 1u);
+                                for (int q = 0; q < 4; ++q) atomicAdd(&sh[(w[k] >> (8 * q)) & 0xFFu], 1u);
+                        }
+                        if (i1 < nvec) {
+                            const uint32_t w[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) atomicAdd(&sh[(w[k] >> (8 * q)) & 0xFFu], 1u);
+                        }
                     }
                 }
-                __syncwarp();
-                for (int v = lane; v < kExitBins; v += 32) {
-                    uint32_t c = sh[v];
-                    if (c) {
-                        atomicAdd(&a.exit_hist[v], (unsigned long long)c);
-                        sh[v] = 0u;
-                    }
-                }
-                __syncwarp();
                 continue;
             }
-            // MoE expert ids.  E <= 64: each lane owns a private column
-            // sh[e*32 + lane] (no atomics, no bank conflicts); else shared
-            // atomics on sh[e].
+            // MoE expert ids.  E <= 16: one-hot register counters; E <= 64:
+            // each lane owns a private column sh[e*32 + lane] (no atomics, no
+            // bank conflicts); else shared atomics on sh[e].  Flushed when the
+            // layer changes.
+            if (!HAS_EXP) continue;
             const int E = t.aux;
-            const bool cols = E <= kColExperts;
+            if (exit_dirty) {  // the scratch holds exit bins: flush them first
+                __syncwarp();
+                for (int vb = lane; vb < kExitBins; vb += 32) {
+                    const uint32_t c = sh[vb];
+                    if (c) {
+                        atomicAdd(&a.exit_hist[vb], (unsigned long long)c);
+                        sh[vb] = 0u;
+                    }
+                }
+                __syncwarp();
+                exit_dirty = 0;
+            }
+            if (hist_layer != t.layer) {
+                flush_experts();
+                hist_layer = t.layer;
+                hist_E = E;
+            }
             const int esz = kind == OP_EXP64 ? 8 : 4;
-            uint32_t bad = 0;
+            if (E <= 16) {
+                auto addr = [&](uint64_t v) {
+                    bad |= v >= (uint64_t)E;
+                    const unsigned long long one = 1ull << (8 * ((uint32_t)v & 7u));
+                    if (v < 8) acc0 += one;
+                    else if (v < (uint64_t)E) acc1 += one;
+                };
+                if (scalar) {
+                    const uint32_t ne = t.nbytes / esz;
+                    if ((uint32_t)lane < ne)
+                        addr(esz == 8 ? (uint64_t)((const int64_t *)t.ptr)[lane]
+                                      : (uint64_t)(int64_t)((const int32_t *)t.ptr)[lane]);
+                    nacc += 1;
+                } else {
+                    const uint4 *p = (const uint4 *)t.ptr;
+                    const uint32_t nvec = t.nbytes >> 4;
+                    // 4 vectors in flight per lane: the per-entry counting is the
+                    // heavier part here, so fewer registers and more resident warps
+                    for (uint32_t base = 0; base < nvec; base += 32u * 4u) {
+                        uint4 v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+                            v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+                            if (idx >= nvec) continue;
+                            if (esz == 8) {
+                                addr(((uint64_t)v[u].y << 32) | v[u].x);
+                                addr(((uint64_t)v[u].w << 32) | v[u].z);
+                            } else {
+                                addr((uint64_t)(int64_t)(int32_t)v[u].x);
+                                addr((uint64_t)(int64_t)(int32_t)v[u].y);
+                                addr((uint64_t)(int64_t)(int32_t)v[u].z);
+                                addr((uint64_t)(int64_t)(int32_t)v[u].w);
+                            }
+                        }
+                        nacc += 16;  // <= 16 entries per lane per batch
+                        if (__any_sync(0xFFFFFFFFu, nacc > 240 - 16)) spill_regs();
+                    }
+                }
+                continue;
+            }
+            const bool cols = E <= kColExperts;
             auto add = [&](uint64_t v) {
-                if (v >= (uint64_t)E) { bad = 1; return; }
+                if (v >= (uint64_t)E) {
+                    bad = 1;
+                    return;
+                }
                 if (cols) sh[(int)v * 32 + lane] += 1u;
                 else atomicAdd(&sh[(int)v], 1u);
             };
@@ -208,15 +385,15 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
             } else {
                 const uint4 *p = (const uint4 *)t.ptr;
                 const uint32_t nvec = t.nbytes >> 4;
-                for (uint32_t base = 0; base < nvec; base += 32u * 4u) {
-                    uint4 v[4];
+                for (uint32_t base = 0; base < nvec; base += 32u * 8u) {
+                    uint4 v[8];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
                         v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < 8; ++u) {
                         uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
                         if (idx >= nvec) continue;
                         if (esz == 8) {
@@ -231,26 +408,20 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                     }
                 }
             }
-            __syncwarp();
-            unsigned long long *dst = a.hist + (int64_t)t.layer * a.max_E;
-            for (int e = lane; e < E; e += 32) {
-                uint32_t c = 0;
-                if (cols) {
-                    for (int l = 0; l < 32; ++l) {
-                        c += sh[e * 32 + l];
-                        sh[e * 32 + l] = 0u;
-                    }
-                } else {
-                    c = sh[e];
-                    sh[e] = 0u;
-                }
-                if (c) atomicAdd(&dst[e], (unsigned long long)c);
-            }
-            __syncwarp();
-            if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
         }
     }
     if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
+    if constexpr (HAS_HIST) {
+        flush_experts();
+        if (exit_dirty) {
+            __syncwarp();
+            for (int vb = lane; vb < kExitBins; vb += 32) {
+                const uint32_t c = sh[vb];
+                if (c) atomicAdd(&a.exit_hist[vb], (unsigned long long)c);
+            }
+        }
+        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
+    }
 }
 
 // -------------------------------------------------------------- epilogue
@@ -484,34 +655,45 @@ __global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nran
 
 }  // namespace
 
-int profile_blocks_per_sm(bool has_hist) {
+template <int OPS>
+static int blocks_per_sm_t(int warp_words) {
     int nb = 0;
-    if (has_hist) {
-        size_t sm = (size_t)(kProfThreads / 32) * 4 *
-                    (kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_profile<true>, kProfThreads, sm);
-    } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_profile<false>, kProfThreads, 0);
-    }
+    const size_t sm = (OPS & 6) ? (size_t)(kProfThreads / 32) * 4 * warp_words : 0;
+    if (sm) cudaFuncSetAttribute(k_profile<OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_profile<OPS>, kProfThreads, sm);
     return nb > 0 ? nb : 1;
 }
 
-cudaError_t launch_profile(const ProfArgs &a, bool has_hist, int grid, cudaStream_t s) {
-    if (a.n_tiles == 0) return cudaSuccess;
-    if (has_hist) {
-        size_t sm = (size_t)(kProfThreads / 32) * 4 *
-                    (kColExperts * 32 > kMaxExperts ? kColExperts * 32 : kMaxExperts);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_profile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sm);
-            attr = true;
-        }
-        k_profile<true><<<grid, kProfThreads, sm, s>>>(a);
-    } else {
-        k_profile<false><<<grid, kProfThreads, 0, s>>>(a);
-    }
+template <int OPS>
+static cudaError_t launch_t(const ProfArgs &a, int grid, cudaStream_t s) {
+    const size_t sm = (OPS & 6) ? (size_t)(kProfThreads / 32) * 4 * a.warp_words : 0;
+    k_profile<OPS><<<grid, kProfThreads, sm, s>>>(a);
     return cudaGetLastError();
+}
+
+int profile_blocks_per_sm(int ops, int warp_words) {
+    switch (ops & 7) {
+        case 1: return blocks_per_sm_t<1>(warp_words);
+        case 2: return blocks_per_sm_t<2>(warp_words);
+        case 3: return blocks_per_sm_t<3>(warp_words);
+        case 4: return blocks_per_sm_t<4>(warp_words);
+        case 5: return blocks_per_sm_t<5>(warp_words);
+        case 6: return blocks_per_sm_t<6>(warp_words);
+        default: return blocks_per_sm_t<7>(warp_words);
+    }
+}
+
+cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    switch (ops & 7) {
+        case 1: return launch_t<1>(a, grid, s);
+        case 2: return launch_t<2>(a, grid, s);
+        case 3: return launch_t<3>(a, grid, s);
+        case 4: return launch_t<4>(a, grid, s);
+        case 5: return launch_t<5>(a, grid, s);
+        case 6: return launch_t<6>(a, grid, s);
+        default: return launch_t<7>(a, grid, s);
+    }
 }
 
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s) {
