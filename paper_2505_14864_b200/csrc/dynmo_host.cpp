@@ -351,11 +351,12 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     {
         int64_t total = 0;
         bool pre_exit = false;
-        int pre_E = 0, pre_ops = 0;
+        int pre_words = 0, pre_ops = 0;
         for (int32_t i = 0; i < n_segs; ++i) {
             const int k = h_segs[i].src_kind;
             if (k == DYNMO_SRC_EXIT_U8) pre_exit = true;
-            if (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) pre_E = std::max(pre_E, (int)h_segs[i].n_experts);
+            if (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32)
+                pre_words = std::max(pre_words, expert_words(std::min((int)h_segs[i].n_experts, kMaxExperts)));
             pre_ops |= k == DYNMO_SRC_EXIT_U8 ? 2 : (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) ? 4 : 1;
             const int64_t ne = h_segs[i].n_elem < 0 ? 0 : h_segs[i].n_elem;
             const int es = k == DYNMO_SRC_NZ_BF16 ? 2 : (k == DYNMO_SRC_NZ_F32 || k == DYNMO_SRC_EXPERT_I32) ? 4
@@ -363,8 +364,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
             total += (k == DYNMO_SRC_MASK_BITS || k == DYNMO_SRC_TOKMASK_BITS) ? ne / 8 : ne * es;
         }
         const int64_t warps = (int64_t)ctx->num_sms *
-                              profile_blocks_per_sm(pre_ops ? pre_ops : 1,
-                                                    profile_warp_words(pre_exit, std::min(pre_E, kMaxExperts))) *
+                              profile_blocks_per_sm(pre_ops ? pre_ops : 1, profile_warp_words(pre_exit, pre_words)) *
                               (kProfThreads / 32);
         int64_t want = total / std::max<int64_t>(1, 2 * warps);
         uint32_t t = 4096;
@@ -534,7 +534,9 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     }
     const int warps_per_block = kProfThreads / 32;
     const int64_t want = (pl->n_tiles + warps_per_block - 1) / warps_per_block;
-    pl->warp_words = profile_warp_words(any_exit, max_E);
+    int max_words = 0;
+    for (const LayerInfo &li : info) max_words = std::max(max_words, expert_words(li.E));
+    pl->warp_words = profile_warp_words(any_exit, max_words);
     pl->ops = 0;
     for (const ProfTile &t : tiles) {
         const int k = t.op & 0xF;

@@ -93,12 +93,14 @@ struct EpiArgs {
 // ops: bit 0 count ops, bit 1 exit histogram, bit 2 expert histograms
 cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s);
 int profile_blocks_per_sm(int ops, int warp_words);
-// per-warp histogram scratch words for a plan (exit bins / expert columns)
-inline int profile_warp_words(bool any_exit, int max_E) {
-    int w = any_exit ? kExitBins : 0;
-    // E <= 16 counts in registers; up to 64 in lane-private smem columns
-    const int e = max_E <= 16 ? 0 : max_E <= kColExperts ? 32 * max_E : max_E;
-    return w > e ? w : (e > 0 ? e : 1);
+// per-warp histogram scratch words of one expert layer: E <= 16 counts in
+// registers, E <= 64 in lane-private smem columns (32 E words), else E words
+inline int expert_words(int E) { return E <= 16 ? 0 : E <= kColExperts ? 32 * E : E; }
+// per-warp scratch of a plan: max over its exit source (256 bins) and layers
+inline int profile_warp_words(bool any_exit, int max_expert_words) {
+    const int w = any_exit ? kExitBins : 0;
+    const int m = w > max_expert_words ? w : max_expert_words;
+    return m > 0 ? m : 1;
 }
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,

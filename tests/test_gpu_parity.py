@@ -532,3 +532,48 @@ def test_config5_sweep(D, L, ctx):
         assert r["status"][q].item() == rst and kn[q] == rk and np.array_equal(rb[q][:x.n + 1], rbb)
         shrunk += rk < x.n
     assert shrunk > 0  # MoD leaves room to release workers
+
+
+def test_profile_mixed_sources_one_plan(D, L, ctx):
+    """Every source kind in ONE plan (count ops + exit histogram + experts on
+    the register (E=8), smem-column (E=40) and smem-atomic (E=300) paths),
+    unaligned views: per-layer counters and histograms vs the oracle."""
+    g = np.random.default_rng(3)
+    segs, keep = [], []
+    nnz, tok, hists = np.zeros(8, np.int64), np.zeros(8, np.int64), {}
+
+    def add(t, kind, layer, **kw):
+        keep.append(t)
+        segs.append(D.SegmentSpec(t, kind, layer, **kw))
+    u8 = (g.random(70001) < 0.3).astype(np.uint8)
+    add(_dev(u8)[3:], L.SRC_MASK_U8, 0); nnz[0] += oracle.count_nz_u8(u8[3:])
+    w = g.integers(0, 2 ** 32, 999, dtype=np.uint64).astype(np.uint32)
+    add(_dev(w.view(np.int32)), L.SRC_MASK_BITS, 1, n_elem=999 * 32 - 5); nnz[1] += oracle.count_bits(w, 999 * 32 - 5)
+    add(_dev(w.view(np.int32)), L.SRC_TOKMASK_BITS, 2, n_elem=600); tok[2] += oracle.count_bits(w, 600)
+    h16 = g.integers(0, 2 ** 16, 5003, dtype=np.uint64).astype(np.uint16)
+    add(_dev(h16.view(np.int16))[1:], L.SRC_NZ_BF16, 3); nnz[3] += oracle.count_nz_bf16(h16[1:])
+    f32 = g.normal(size=3001).astype(np.float32)
+    f32[g.random(3001) < 0.4] = 0.0
+    add(_dev(f32)[2:], L.SRC_NZ_F32, 4); nnz[4] += oracle.count_nz_f32(f32[2:])
+    e = synth.cfg3_exit_depth(T=30001, L=8)
+    add(_dev(e)[1:], L.SRC_EXIT_U8, 0)
+    tok += oracle.exit_survivors(e[1:], 0, 8)
+    for j, (E, dt) in enumerate([(8, np.int64), (40, np.int32), (300, np.int64)]):
+        idx = synth.cfg4_routing(j, T=3001, E=E, k=2, dtype=dt).reshape(-1)
+        add(_dev(idx)[1:], L.SRC_EXPERT_I64 if dt == np.int64 else L.SRC_EXPERT_I32, 5 + j, n_experts=E, top_k=2)
+        hists[5 + j] = oracle.expert_hist(idx[1:], E)[1]
+    plan = D.ProfilePlan(ctx, segs, 0, 8)
+    coef = D.coef_tensor(8, A=3, B=1, C_=2, ep=0, device=DEV)
+    counters = torch.empty((8, 4), dtype=torch.int64, device=DEV)
+    hist = torch.zeros((8, plan.max_experts), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters, hist=hist)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    c = counters.cpu().numpy()
+    assert np.array_equal(c[:, 0], nnz) and np.array_equal(c[:, 1], tok)
+    hh = hist.cpu().numpy()
+    for layer, want in hists.items():
+        assert np.array_equal(hh[layer, :len(want)], want), layer
+    want_cost = [oracle.layer_cost(tok=int(tok[i]), nnz=int(nnz[i]), cnt=hists.get(i), A=3, B=1, C_=2, ep=0)[1]
+                 for i in range(8)]
+    assert np.array_equal(cost.cpu().numpy(), want_cost)
