@@ -44,7 +44,7 @@ NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="dynmo", choices=["dynmo", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -82,9 +82,27 @@ def workload_config(G):
         "params_per_layer": shape.params_per_layer,
         "mask_bytes_total": shape.L * shape.params_per_layer,
         "mask_repr": "u8", "stage_to_gpu": "floor(s*G/8)",
-        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, then a {L2_FLUSH_BYTES >> 20} MiB "
+              "read so no dirty lines of the flush are written back inside the step)",
         "parallelism": f"pp-profile{G}",
     }
+
+
+class L2Flush:
+    """Evicts the step's data from L2 between timed steps: a write larger
+    than L2, then a read larger than L2 (the write's dirty lines are written
+    back here, outside the timed interval, instead of inside the next step)."""
+
+    def __init__(self, dev):
+        import torch
+        self.w = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(L2_FLUSH_BYTES // 8, dtype=torch.int64, device=dev)
+        self.k = 0
+
+    def __call__(self):
+        self.k += 1
+        self.w.fill_(self.k & 0xFF)
+        self.r.max()
 
 
 # ------------------------------------------------------------ input set-up
@@ -127,23 +145,43 @@ class ClockSampler:
 
     def __enter__(self):
         import subprocess
+        import threading
+        self.lines, self.t0, self.t1 = [], None, None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.dev_id, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            time.sleep(0.05)
+                 "-lms", "10"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+            def reader():  # timestamps each sample (host monotonic clock)
+                for line in self.proc.stdout:
+                    self.lines.append((time.monotonic(), line))
+            self.th = threading.Thread(target=reader, daemon=True)
+            self.th.start()
+            deadline = time.monotonic() + 10.0  # the sampler is running before the timed loop
+            while not self.lines and time.monotonic() < deadline:
+                time.sleep(0.005)
         except Exception as e:  # pragma: no cover
             self.err = repr(e)
         return self
 
+    def start(self):
+        """Marks the start of the timed region (samples before it are dropped)."""
+        self.t0 = time.monotonic()
+
+    def stop(self):
+        """Marks the end of the timed region."""
+        self.t1 = time.monotonic()
+
     def __exit__(self, *a):
         if self.proc is not None:
-            time.sleep(0.03)
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.th.join(timeout=5)
+        t0, t1 = self.t0 or 0.0, self.t1 or float("inf")
+        self.out = "".join(line for t, line in self.lines if t0 <= t <= t1 + 0.025)
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -285,7 +323,7 @@ def run_dynmo(args):
     pst = res_d[nb + 1:nb + 2]
     dif_out = {"status": res_d[nb + 2:nb + 3]}
     rep_out = {"status": res_d[nb + 3:nb + 4]}
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     stream = torch.cuda.current_stream()
 
     # ---- migration buffers (CSR payload per layer; params + optimizer state)
@@ -301,7 +339,8 @@ def run_dynmo(args):
     d_ranks = torch.from_numpy(ranks.astype(np.int32)).to(dev)
     d_bytes = torch.zeros(2, dtype=torch.int64, device=dev)
     # device-driven migration (G > 1, peer memory): the whole step is one graph
-    dev_mig = G > 1 and args.migrate == "p2p" and not args.host_migrate
+    # (also at G = 1, where nothing migrates: the step never waits on the host)
+    dev_mig = (G == 1 or args.migrate == "p2p") and not args.host_migrate
     pmig = None
 
     def solve_async():
@@ -383,7 +422,7 @@ def run_dynmo(args):
         stream = torch.cuda.current_stream()
 
     for _ in range(max(args.warmup, 3)):
-        flush.fill_(1)
+        flush()
         step()
     torch.cuda.synchronize()
     if G > 1:
@@ -402,8 +441,9 @@ def run_dynmo(args):
             dist.all_reduce(bar)
 
     with ClockSampler(local) as clk:
+        clk.start()
         for k in range(args.steps):
-            flush.fill_(k & 0xFF)
+            flush()
             step_barrier()
             ev[k][0].record(stream)
             sr = step()
@@ -413,6 +453,7 @@ def run_dynmo(args):
             ev[k][1].synchronize()  # outside the timed interval: fold the phase events
             ctx.timing_poll()
         torch.cuda.synchronize()
+        clk.stop()
     if G > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -436,7 +477,7 @@ def run_dynmo(args):
     d2h = int(res_h.numel() * 4)
     e2e = []
     for k in range(args.e2e_steps):
-        flush.fill_(k & 0xFF)
+        flush()
         step_barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -461,7 +502,7 @@ def run_dynmo(args):
         torch.cuda.synchronize()
         ctx.timing_read()
         for k in range(20):
-            flush.fill_(k & 0xFF)
+            flush()
             step_barrier()
             gdiag.replay()
             if not dev_mig:

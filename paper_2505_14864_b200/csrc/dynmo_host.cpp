@@ -573,7 +573,7 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     cudaStream_t s = (cudaStream_t)stream;
     DeviceGuard g(ctx->device);
     ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
-                std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words};
+                std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words, plan->n_local};
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PROFILE, s);
     CUDA_TRY(launch_profile(pa, plan->ops, plan->grid, s), "k_profile launch");
     phase_end(te, s);

@@ -6,6 +6,23 @@
 
 #include "dynmo.h"
 
+// Bounds-checked build (make debug -> libdynmo_dbg.so, DYNMO_DEBUG=1 loads
+// it): every scratch / shared-memory / table index is asserted; a violation
+// prints its site and traps.  Compiled out of the product library.
+#ifdef DYNMO_BOUNDS
+#include <cstdio>
+#define DYNMO_DCHECK(c)                                                                  \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("DYNMO_BOUNDS %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                               \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define DYNMO_DCHECK(c) ((void)0)
+#endif
+
 namespace dynmo {
 
 // ---------------------------------------------------------------- profiling
@@ -60,6 +77,7 @@ struct ProfArgs {
     int32_t max_E;
     int32_t *ws_status;
     int32_t warp_words;  // per-warp histogram scratch (u32 words)
+    int32_t n_local;     // layers of the plan (bounds of acc / hist rows)
 };
 
 struct PeerWindow;

@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
     };
     auto feed = [&](int64_t key, uint32_t c) {
         if (key != run_key) {
+            DYNMO_DCHECK(run_key < 0 || run_key < (int64_t)a.n_local * ACC_N);
             if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
             run_key = key;
             run_sum = 0;
@@ -174,6 +175,8 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
     auto flush_experts = [&]() {
         if constexpr (HAS_HIST) {
             if (hist_layer < 0) return;
+            DYNMO_DCHECK(hist_layer < a.n_local && hist_E <= a.max_E);
+            DYNMO_DCHECK(hist_E <= 16 || (hist_E <= kColExperts ? 32 * hist_E : hist_E) <= a.warp_words);
             unsigned long long *dst = a.hist + (int64_t)hist_layer * a.max_E;
             if (hist_E <= 16) {
                 spill_regs();
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                 // atomics); flushed once when the warp's range is done
                 if (hist_layer >= 0) flush_experts();  // (scratch is shared)
                 exit_dirty = 1;
+                DYNMO_DCHECK(kExitBins <= a.warp_words);
                 const uint8_t *b = (const uint8_t *)t.ptr;
                 if (scalar) {
                     if ((uint32_t)lane < t.nbytes) atomicAdd(&sh[b[lane]], 1u);
@@ -367,6 +371,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                 continue;
             }
             const bool cols = E <= kColExperts;
+            DYNMO_DCHECK((cols ? 32 * E : E) <= a.warp_words && E <= a.max_E && t.layer < a.n_local);
             auto add = [&](uint64_t v) {
                 if (v >= (uint64_t)E) {
                     bad = 1;
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
             }
         }
     }
+    DYNMO_DCHECK(run_key < 0 || run_key < (int64_t)a.n_local * ACC_N);
     if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
     if constexpr (HAS_HIST) {
         flush_experts();

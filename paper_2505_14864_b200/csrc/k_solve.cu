@@ -61,7 +61,14 @@ __host__ __device__ __forceinline__ size_t solve_smem_bytes(int Lmax, bool mem, 
     return base_bytes(Lmax, mem) + (fluid ? sizeof(double) * (kChunk * kRow + kChunk) : 0);
 }
 
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+
 __device__ Inst carve(char *sm, int Lmax, bool mem) {
+    DYNMO_DCHECK(base_bytes(Lmax, mem) <= dyn_smem_bytes());
     Inst s;
     const size_t Lc = (size_t)Lmax + 1;
     size_t o = 0;
@@ -83,8 +90,11 @@ struct PrefixFlags {
     bool cneg, covf, mneg, movf;
 };
 
-__device__ bool exact_sum_overflows(const int64_t *v, int L) {
+// (out of line and rolled: runs only when a prefix saturated, and the solver
+// kernels are instruction-fetch bound when cold, so their code stays small)
+__device__ __noinline__ bool exact_sum_overflows(const int64_t *v, int L) {
     __int128 acc = 0;
+#pragma unroll 1
     for (int i = 0; i < L; ++i) acc += v[i];
     return acc > (__int128)I64MAX;
 }
@@ -95,6 +105,7 @@ __device__ void warp_prefix(const int64_t *v, int L, int64_t *out, int lane) {
     const int Q = (L + 31) / 32;
     const int beg = lane * Q, end = beg + Q < L ? beg + Q : L;
     int64_t sum = 0;
+#pragma unroll 1
     for (int i = beg; i < end; ++i) sum = satadd(sum, v[i]);
     int64_t ex = sum;
 #pragma unroll
@@ -107,6 +118,7 @@ __device__ void warp_prefix(const int64_t *v, int L, int64_t *out, int lane) {
         ex = 0;
         out[0] = 0;
     }
+#pragma unroll 1
     for (int i = beg; i < end; ++i) {
         ex = satadd(ex, v[i]);
         out[i + 1] = ex;
@@ -120,6 +132,7 @@ __device__ PrefixFlags load_prefix(Inst &s, const int64_t *cost, const int64_t *
     PrefixFlags f{false, false, false, false};
     int cneg = 0, mneg = 0;
     int64_t mx = 0;
+#pragma unroll 1
     for (int i = lane; i < L; i += 32) {
         const int64_t c = cost[i];
         cneg |= c < 0;
@@ -196,6 +209,75 @@ __device__ int warp_greedy(const Inst &s, int64_t B, int limit, int lane) {
     return c;
 }
 
+// Per-lane jump table (L <= 32 Q - 1): lane owns positions j = lane + 32 r
+// and finds nx[r] = the largest K in [j, L] with P[K] <= P[j] + B (and
+// M[K] <= M[j] + cap) by binary lifting: K += step whenever K + step still
+// satisfies both (monotone) predicates, steps = powers of two <= L in
+// decreasing order.  The Q searches are independent and interleaved (ILP);
+// every lane runs the same ceil(log2(L+1)) steps.  K == j: layer j does not
+// fit.  Replaces n dependent window jumps (~335 cycles each) by one parallel
+// search (~log2 L shared loads) plus n register shuffles.
+template <bool MEM, int Q>
+__device__ __forceinline__ void lane_table(const Inst &s, int64_t B, int lane, int (&nx)[Q]) {
+    const int L = s.L;
+    DYNMO_DCHECK(L >= 1 && L <= 32 * Q - 1);
+    int64_t t1[Q], t2[Q];
+#pragma unroll
+    for (int r = 0; r < Q; ++r) {
+        const int j = lane + 32 * r;
+        nx[r] = j;
+        const int jj = j <= L ? j : L;
+        t1[r] = satadd(s.P[jj], B);
+        t2[r] = MEM ? satadd(s.M[jj], s.cap) : 0;
+    }
+    // branch-free: indices clamped to L, loads unconditional, so the Q
+    // searches interleave (their latencies overlap)
+    for (int step = 1 << (31 - __clz(L)); step > 0; step >>= 1) {
+#pragma unroll
+        for (int r = 0; r < Q; ++r) {
+            const int c = nx[r] + step;
+            const int cc = c <= L ? c : L;
+            bool ok = (c <= L) & (s.P[cc] <= t1[r]);
+            if constexpr (MEM) ok &= s.M[cc] <= t2[r];
+            nx[r] = ok ? c : nx[r];
+        }
+    }
+}
+
+// nx of position j (warp-uniform j < 32 Q): register j >> 5 of lane j & 31.
+template <int Q>
+__device__ __forceinline__ int table_at(const int (&nx)[Q], int j) {
+    int v = nx[0];
+#pragma unroll
+    for (int r = 1; r < Q; ++r)
+        if ((j >> 5) == r) v = nx[r];
+    return __shfl_sync(FULL, v, j & 31);
+}
+
+template <bool MEM, int Q>
+__device__ int table_greedy(const Inst &s, int64_t B, int limit, int lane) {
+    int nx[Q];
+    lane_table<MEM, Q>(s, B, lane, nx);
+    int j = 0, c = 0;
+    while (j < s.L) {
+        if (c == limit) return limit + 1;
+        const int K = table_at<Q>(nx, j);
+        if (K == j) return limit + 1;
+        j = K;
+        ++c;
+    }
+    return c;
+}
+
+// Greedy stage count (same contract as warp_greedy): a jump table of Q
+// registers per lane (L <= 32 Q - 1), or warp windows (Q == 0, any L).  Q is
+// chosen on the host from the batch's max_layers, so a kernel holds one path.
+template <bool MEM, int Q>
+__device__ __forceinline__ int greedy_count(const Inst &s, int64_t B, int limit, int lane) {
+    if constexpr (Q == 0) return warp_greedy<MEM>(s, B, limit, lane);
+    else return table_greedy<MEM, Q>(s, B, limit, lane);
+}
+
 // Candidate w of NW per round: lo + floor(d (w+1) / (NW+1)) in 64-bit
 // arithmetic (d = a (NW+1) + r); NW+1 is a compile-time constant.
 template <int NC1>
@@ -210,7 +292,7 @@ __device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
 // candidates form a suffix: the first feasible one is the new hi and its
 // predecessor + 1 the new lo.  Called by all NW warps after s is built and
 // visible.  Returns B* (uniform), or -1 if no split satisfies the memory cap.
-template <bool MEM, int NW>
+template <bool MEM, int NW, int Q>
 __device__ int64_t search_bottleneck(const Inst &s, int n) {
     __shared__ int s_f[2][NW];
     __shared__ int s_pre[2];
@@ -226,15 +308,15 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
         int fh, fc;
         if constexpr (NW > 1) {
             if (w < 2) {
-                const int f = warp_greedy<MEM>(s, w == 0 ? hi : C, n, lane) <= n;
+                const int f = greedy_count<MEM, Q>(s, w == 0 ? hi : C, n, lane) <= n;
                 if (lane == 0) s_pre[w] = f;
             }
             __syncthreads();
             fh = s_pre[0];
             fc = s_pre[1];
         } else {
-            fh = warp_greedy<MEM>(s, hi, n, lane) <= n;
-            fc = fh ? 1 : warp_greedy<MEM>(s, C, n, lane) <= n;
+            fh = greedy_count<MEM, Q>(s, hi, n, lane) <= n;
+            fc = fh ? 1 : greedy_count<MEM, Q>(s, C, n, lane) <= n;
         }
         if (!fh) {
             if (!fc) return -1;
@@ -245,7 +327,7 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
     while (lo < hi) {
         const uint64_t d = (uint64_t)(hi - lo);
         const int64_t cand = candidate<NW + 1>(lo, d, w);
-        const int f = warp_greedy<MEM>(s, cand, n, lane) <= n;
+        const int f = greedy_count<MEM, Q>(s, cand, n, lane) <= n;
         int first;
         if constexpr (NW == 1) {
             first = f ? 0 : 1;
@@ -268,8 +350,24 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
 
 // Lexmax boundaries for B* (Appendix A): b_{s+1} = min(next(b_s), L - (n-1-s))
 // with warp-cooperative jumps.  One warp; writes s.b[0..n].
-template <bool MEM>
+template <bool MEM, int Q>
+__device__ void table_construct(Inst &s, int64_t Bs, int n, int lane) {
+    int nx[Q];
+    lane_table<MEM, Q>(s, Bs, lane, nx);
+    int j = 0;
+    if (lane == 0) s.b[0] = 0;
+    for (int st = 0; st < n; ++st) {
+        const int K = table_at<Q>(nx, j);  // j < L here (the reserve keeps it so)
+        const int reserve = s.L - (n - 1 - st);
+        j = K < reserve ? K : reserve;
+        if (lane == 0) s.b[st + 1] = j;
+    }
+    __syncwarp();
+}
+
+template <bool MEM, int Q>
 __device__ void construct(Inst &s, int64_t Bs, int n, int lane) {
+    if constexpr (Q > 0) return table_construct<MEM, Q>(s, Bs, n, lane);
     int j = 0;
     if (lane == 0) s.b[0] = 0;
     for (int st = 0; st < n; ++st) {
@@ -286,6 +384,7 @@ __device__ void construct(Inst &s, int64_t Bs, int n, int lane) {
 
 __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
     int64_t mx = P[b[1]] - P[b[0]], mn = mx;
+#pragma unroll 1
     for (int st = 1; st < n; ++st) {
         const int64_t x = P[b[st + 1]] - P[b[st]];
         mx = x > mx ? x : mx;
@@ -298,7 +397,7 @@ __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
 }
 
 // ------------------------------------------------------------ partition
-template <bool MEM, int NW>
+template <bool MEM, int NW, int Q>
 __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st;
@@ -324,7 +423,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
     s.maxc = s.x[0];
     int64_t Bs = -1;
     if (st == DYNMO_OK) {
-        Bs = search_bottleneck<MEM, NW>(s, n);
+        Bs = search_bottleneck<MEM, NW, Q>(s, n);
         if (Bs < 0) st = DYNMO_E_INFEASIBLE;
     }
     if (w != 0) return;
@@ -337,7 +436,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
         }
         return;
     }
-    construct<MEM>(s, Bs, n, lane);
+    construct<MEM, Q>(s, Bs, n, lane);
+#pragma unroll 1
     for (int k = lane; k <= n; k += 32) bnd[k] = s.b[k];
     if (lane == 0) {
         a.bottleneck[q] = Bs;
@@ -347,7 +447,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
 }
 
 // -------------------------------------------------------------- repack
-template <bool MEM, int NW>
+template <bool MEM, int NW, int Q>
 __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st, s_k, s_code;
@@ -385,7 +485,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         int k = n_cur, code = DYNMO_OK;
         if (st == DYNMO_OK && !alg2) {
             // fewest workers: greedy count at B = bound (cost and mem), reading Q15
-            const int g = warp_greedy<MEM>(s, bound, n_cur, lane);
+            const int g = greedy_count<MEM, Q>(s, bound, n_cur, lane);
             if (g <= n_cur) {
                 k = g > fl ? g : fl;
             } else {
@@ -453,7 +553,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         return;
     }
     const int k = s_k;
-    const int64_t Bs = search_bottleneck<MEM, NW>(s, k);
+    const int64_t Bs = search_bottleneck<MEM, NW, Q>(s, k);
     if (w != 0) return;
     if (Bs < 0) {
         for (int t = lane; t <= n_cur; t += 32) bnd[t] = -1;
@@ -464,7 +564,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         }
         return;
     }
-    construct<MEM>(s, Bs, k, lane);
+    construct<MEM, Q>(s, Bs, k, lane);
     for (int t = lane; t <= n_cur; t += 32) bnd[t] = t <= k ? s.b[t] : -1;
     if (lane == 0) {
         a.n_new[q] = k;
@@ -605,6 +705,33 @@ __device__ void diffuse_discrete(const SolveArgs &a, Inst &s, int q, int n, cons
 // chunk storing every x(r), then lane k evaluates phi_f(x(base + k)) (the
 // oracle's ascending (u, v) sum); the first r with phi_f <= gamma_f, or
 // r == max_rounds, stops with x(r).
+// phi_f of one history row: sum over u < v of |x_u - x_v| in ascending
+// (u, v) order (reading Q20).  n <= 8: the row in registers, all 28 pairs
+// unrolled (absent pairs add nothing), so only the dependent adds remain on
+// the critical path; the nested runtime-bound loop spent ~10x that in
+// branches and reloads.  Larger n: the plain loop.
+__device__ __forceinline__ double phi_row(const double *row, int n) {
+    double acc = 0.0;
+    if (n <= 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = u < n ? row[u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = u + 1; v < 8; ++v)
+                if (v < n) acc = __dadd_rn(acc, fabs(__dsub_rn(x[u], x[v])));
+        return acc;
+    }
+#pragma unroll 1
+    for (int u = 0; u < n; ++u) {
+        const double xu = row[u];
+#pragma unroll 1
+        for (int v = u + 1; v < n; ++v) acc = __dadd_rn(acc, fabs(__dsub_rn(xu, row[v])));
+    }
+    return acc;
+}
+
 __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf, int maxr,
                              double *hist, double *xo, int &rr, double &ph, int &fst, int lane) {
     double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
@@ -632,14 +759,7 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
             x = mR ? avgR : (mL ? avgL : x);
         }
         __syncwarp();
-        double acc = 0.0;
-        if (lane < size) {
-            const double *row = hist + lane * kRow;
-            for (int u = 0; u < n; ++u) {
-                const double xu = row[u];
-                for (int v = u + 1; v < n; ++v) acc = __dadd_rn(acc, fabs(__dsub_rn(xu, row[v])));
-            }
-        }
+        const double acc = lane < size ? phi_row(hist + lane * kRow, n) : 0.0;
         const bool stop = lane < size && (acc <= gf || base + lane == maxr);
         const unsigned m = __ballot_sync(FULL, stop);
         if (m) {
@@ -722,6 +842,7 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
     const int q = blockIdx.x, lane = threadIdx.x;
     const bool fluid = blockIdx.y == 1;
     Inst s = carve(smem, a.max_layers, MEM && !fluid);
+    DYNMO_DCHECK(!fluid || solve_smem_bytes(a.max_layers, false, true) <= dyn_smem_bytes());
     const int off = a.layer_off[q];
     const int L = a.layer_off[q + 1] - off;
     const int n = a.n_stages[q];
@@ -762,18 +883,46 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
 // search.  Large batches: 1 warp per instance (binary search, one wave).
 static bool latency_mode(const SolveArgs &a) { return a.n_inst <= 4 * 148; }
 
-cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s) {
+// jump-table width for the batch: registers per lane (L <= 32 Q - 1), 0 = windows
+static int table_q(int max_layers) {
+    return max_layers < 32 ? 1 : max_layers < 64 ? 2 : max_layers < 128 ? 4 : max_layers < 256 ? 8 : 0;
+}
+
+template <template <bool, int, int> class K>
+static cudaError_t launch_solver(const SolveArgs &a, cudaStream_t s) {
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
-    const bool lm = latency_mode(a);
-    if (a.mem) {
-        if (lm) k_partition<true, 8><<<a.n_inst, 256, sm, s>>>(a);
-        else k_partition<true, 1><<<a.n_inst, 32, sm, s>>>(a);
-    } else {
-        if (lm) k_partition<false, 8><<<a.n_inst, 256, sm, s>>>(a);
-        else k_partition<false, 1><<<a.n_inst, 32, sm, s>>>(a);
+    const bool lm = latency_mode(a), mem = a.mem != nullptr;
+    const dim3 grid(a.n_inst), block(lm ? 256 : 32);
+#define DYNMO_SOLVER_Q(M, NW)                                                   \
+    switch (table_q(a.max_layers)) {                                            \
+        case 1: K<M, NW, 1>::launch(grid, block, sm, s, a); break;            \
+        case 2: K<M, NW, 2>::launch(grid, block, sm, s, a); break;            \
+        case 4: K<M, NW, 4>::launch(grid, block, sm, s, a); break;            \
+        case 8: K<M, NW, 8>::launch(grid, block, sm, s, a); break;            \
+        default: K<M, NW, 0>::launch(grid, block, sm, s, a); break;           \
     }
+    if (mem && lm) { DYNMO_SOLVER_Q(true, 8) }
+    else if (mem) { DYNMO_SOLVER_Q(true, 1) }
+    else if (lm) { DYNMO_SOLVER_Q(false, 8) }
+    else { DYNMO_SOLVER_Q(false, 1) }
+#undef DYNMO_SOLVER_Q
     return cudaGetLastError();
 }
+
+template <bool M, int NW, int Q>
+struct PartitionK {
+    static void launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
+        k_partition<M, NW, Q><<<g, b, sm, s>>>(a);
+    }
+};
+template <bool M, int NW, int Q>
+struct RepackK {
+    static void launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
+        k_repack<M, NW, Q><<<g, b, sm, s>>>(a);
+    }
+};
+
+cudaError_t launch_partition(const SolveArgs &a, cudaStream_t s) { return launch_solver<PartitionK>(a, s); }
 cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s) {
     const bool fl = a.fluid_x != nullptr;
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, fl);
@@ -782,17 +931,6 @@ cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s) {
     else k_diffuse<false><<<grid, 32, sm, s>>>(a);
     return cudaGetLastError();
 }
-cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s) {
-    const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
-    const bool lm = latency_mode(a);
-    if (a.mem) {
-        if (lm) k_repack<true, 8><<<a.n_inst, 256, sm, s>>>(a);
-        else k_repack<true, 1><<<a.n_inst, 32, sm, s>>>(a);
-    } else {
-        if (lm) k_repack<false, 8><<<a.n_inst, 256, sm, s>>>(a);
-        else k_repack<false, 1><<<a.n_inst, 32, sm, s>>>(a);
-    }
-    return cudaGetLastError();
-}
+cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s) { return launch_solver<RepackK>(a, s); }
 
 }  // namespace dynmo

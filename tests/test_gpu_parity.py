@@ -322,6 +322,32 @@ def test_partition_random_sizes(D, ctx, Lmax, with_mem, big):
     _check_partition(insts, _run_partition(D, ctx, insts, with_mem), with_mem)
 
 
+@pytest.mark.parametrize("count", [48, 700])  # 8-warp latency mode / 1-warp throughput mode (> 592)
+def test_partition_repack_threshold_sizes(D, ctx, count):
+    """L on both sides of every jump-table width (31/32, 63/64, 127/128,
+    255/256: Q = 1, 2, 4, 8 registers, then warp windows), with and without
+    the memory cap: partition and BOUND repack vs the oracle."""
+    g = np.random.default_rng(4242 + count)
+    sizes = [31, 32, 63, 64, 127, 128, 255, 256]
+    insts = []
+    for i in range(count):
+        Ly = sizes[i % len(sizes)]
+        n = int(g.integers(1, min(16, Ly) + 1))
+        cost = g.integers(0, 1000, Ly)
+        cost[g.random(Ly) < 0.2] = 0
+        mem = g.integers(0, 100, Ly)
+        insts.append(dict(cost=cost, n=n, mem=mem, cap=int(max(1, mem.sum() // n * g.uniform(0.6, 2.0))),
+                          bound=int(cost.sum() // n * g.uniform(0.8, 3.0)), floor=1))
+    for with_mem in (False, True):
+        _check_partition(insts, _run_partition(D, ctx, insts, with_mem), with_mem)
+        b, bnds, kn, bott, st = _run_repack(D, ctx, insts, 0, with_mem)
+        for q, x in enumerate(insts):
+            ost, ok, ob, oB = oracle.repack_bound(x["cost"], x["n"], x["bound"], 1,
+                                                  mem=x["mem"] if with_mem else None, cap=x["cap"] if with_mem else 0)
+            assert (st[q], kn[q], bott[q]) == (ost, ok, oB), (q, with_mem)
+            assert np.array_equal(bnds[q][:x["n"] + 1], ob), (q, with_mem)
+
+
 def test_partition_errors(D, ctx):
     """INVALID (n > L, n < 1, negative cost), OVERFLOW, INFEASIBLE."""
     insts = [dict(cost=np.array([1, 2]), n=3, mem=np.array([1, 1]), cap=5),
