@@ -68,6 +68,16 @@ struct dynmo_ctx_s {
     uint64_t mig_epoch = 0;
 };
 
+namespace dynmo {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("DYNMO_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+}  // namespace dynmo
+
 namespace {
 // All-gather `n` bytes per rank over the ctx communicator (setup only:
 // synchronous, through a temporary device buffer).

@@ -62,6 +62,39 @@ struct LayerInfo {
     int32_t E;   // experts of this layer (0 if no MoE source)
 };
 
+// ------------------------------------------------ programmatic dependent launch
+// Kernels that follow another kernel of the path on a stream are launched
+// with programmatic stream serialization: they may be scheduled while the
+// predecessor still runs (hiding launch latency) and execute pdl_wait()
+// before touching ANY memory, so the ordering seen by the data is that of a
+// normal launch (griddepcontrol.wait returns once the predecessor grid has
+// completed and its writes are visible; it is a no-op without the attribute).
+// pdl_trigger() lets the successor be scheduled early.  DYNMO_PDL=0 disables.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args... args) {
+    if (!pdl_enabled()) {
+        k<<<grid, block, smem, s>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 constexpr int kProfThreads = 256;
 constexpr uint32_t kTileBytes = 32u << 10;   // max vector tile size (plan picks 4..32 KiB)
 constexpr int kExitBins = 256;

@@ -155,6 +155,8 @@ __device__ void mig_view(const DevMigArgs &a, MigView &v, int16_t *in_layers, in
 
 // Sender side: advance the device epoch, release ready[me] at every receiver.
 __global__ void k_mig_signal(DevMigArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ unsigned s_recv;
     __shared__ int s_ok;
     __shared__ unsigned long long s_sent;
@@ -191,6 +193,8 @@ __global__ void k_mig_signal(DevMigArgs a) {
 // copies its grid-stride share of every incoming buffer; the last block
 // releases ddone[me] at every sender.
 __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ MigView v;
     __shared__ int16_t in_layers[1024];
     __shared__ int8_t in_src[1024];
@@ -252,6 +256,8 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
 
 // Sender side again: wait until every receiver has finished reading.
 __global__ void k_mig_wait(DevMigArgs a) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ MigView v;
     __shared__ int16_t in_layers[1024];
     __shared__ int8_t in_src[1024];
@@ -267,10 +273,10 @@ __global__ void k_mig_wait(DevMigArgs a) {
 }  // namespace
 
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, cudaStream_t s) {
-    k_mig_signal<<<1, 256, 0, s>>>(a);
-    k_mig_pull<<<grid, kP2PThreads, 0, s>>>(a);
-    k_mig_wait<<<1, 256, 0, s>>>(a);
-    return cudaGetLastError();
+    cudaError_t e = launch_pdl(k_mig_signal, 1, 256, 0, s, a);
+    if (e == cudaSuccess) e = launch_pdl(k_mig_pull, grid, kP2PThreads, 0, s, a);
+    if (e == cudaSuccess) e = launch_pdl(k_mig_wait, 1, 256, 0, s, a);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_signal(const P2PSignal &s, cudaStream_t st) {

@@ -117,6 +117,7 @@ __device__ __forceinline__ bool small_count_tile(const ProfTile &t) {
 // (paths of absent op families are compiled out: fewer registers).
 template <int OPS>
 __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
+    pdl_trigger();  // the epilogue may be scheduled now (it waits for this grid)
     constexpr bool HAS_CNT = OPS & 1, HAS_EXIT = (OPS & 2) != 0, HAS_EXP = (OPS & 4) != 0;
     constexpr bool HAS_HIST = HAS_EXIT || HAS_EXP;
     extern __shared__ uint32_t smem[];
@@ -442,6 +443,8 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
 }
 
 __global__ void k_epilogue(EpiArgs a) {
+    pdl_wait();
+    pdl_trigger();
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     int st = DYNMO_OK;
     if (q < a.n_local) {
@@ -580,6 +583,8 @@ __device__ void k_unpack_body(const int64_t *slot_recv, int32_t nranks, int32_t 
 
 __global__ void k_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                          int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+    pdl_wait();
+    pdl_trigger();
     k_unpack_body(slot_recv, nranks, n_total, cost_out, mem_out, status_out);
 }
 
@@ -627,6 +632,8 @@ __device__ void k_unpack_body(const int64_t *slot_recv, int32_t nranks, int32_t 
 // this epoch, then scatter the local slot area of the epoch's parity.
 __global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+    pdl_wait();
+    pdl_trigger();
     __shared__ int s_ok;
     const uint64_t epoch = win->exch_epoch;  // advanced by this rank's epilogue
     if (threadIdx.x == 0) {
@@ -705,21 +712,18 @@ cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s)
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s) {
     const int threads = 256;
     const int grid = a.n_local > 0 ? (a.n_local + threads - 1) / threads : 1;
-    k_epilogue<<<grid, threads, 0, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k_epilogue, grid, threads, 0, s, a);
 }
 
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
                           cudaStream_t s) {
-    k_unpack<<<1, 1024, 0, s>>>(slot_recv, nranks, n_total, cost_out, mem_out, status_out);
-    return cudaGetLastError();
+    return launch_pdl(k_unpack, 1, 1024, 0, s, slot_recv, nranks, n_total, cost_out, mem_out, status_out);
 }
 
 cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
                               int64_t *cost_out, int64_t *mem_out, int32_t *status_out, cudaStream_t s) {
-    k_unpack_p2p<<<1, 1024, 0, s>>>(slots, win, nranks, n_total, cost_out, mem_out, status_out);
-    return cudaGetLastError();
+    return launch_pdl(k_unpack_p2p, 1, 1024, 0, s, slots, win, nranks, n_total, cost_out, mem_out, status_out);
 }
 
 }  // namespace dynmo

@@ -399,6 +399,8 @@ __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
 // ------------------------------------------------------------ partition
 template <bool MEM, int NW, int Q>
 __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st;
     const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -449,6 +451,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
 // -------------------------------------------------------------- repack
 template <bool MEM, int NW, int Q>
 __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st, s_k, s_code;
     const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -737,21 +741,26 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
     double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
     int size = 1;
     for (int base = 0;; base += size, size = size < kChunk / 4 ? size * 4 : kChunk) {
-        // branch-free round: both candidate averages are computed off the
-        // critical path; the pick is gr > gl ? s : (gl > 0 ? s-1 : -1), which
-        // is the oracle's rule (edge s-1 first, a strictly larger gap wins).
-        // (A halo-2 variant that recomputes the neighbours' picks locally
-        // instead of shuffling them measured slower: 39 vs 31 us.)
+        // Branch-free round: both candidate averages are computed off the
+        // critical path; stage s picks its right edge iff gr > gl, else its
+        // left edge iff gl > 0 (a missing edge has gap 0: the oracle's rule);
+        // gaps are compared through |.| operand modifiers with the edge masks
+        // folded into predicates.  Two shuffle phases (x, then the picks).
+        // (A halo-2 variant deciding both edges locally from x at distance
+        // 1 and 2 -- one phase of 8 shuffles -- measured slower, 24.2 vs
+        // 22.8 us on config 2: the shuffle pipe, not latency, bounds it.)
         const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
         for (int k = 0; k < size; ++k) {
             if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
             const double xl = __shfl_up_sync(FULL, x, 1);
             const double xr = __shfl_down_sync(FULL, x, 1);
-            const double gl = hasL ? fabs(__dsub_rn(xl, x)) : 0.0;  // gap of edge lane-1
-            const double gr = hasR ? fabs(__dsub_rn(x, xr)) : 0.0;  // gap of edge lane
+            const double dl = __dsub_rn(xl, x), dr = __dsub_rn(x, xr);
             const double avgL = __dmul_rn(__dadd_rn(xl, x), 0.5);
             const double avgR = __dmul_rn(__dadd_rn(x, xr), 0.5);
-            const int pick = gr > gl ? lane : (gl > 0.0 ? lane - 1 : -1);
+            const bool cRL = fabs(dr) > fabs(dl), cR0 = fabs(dr) > 0.0, cL0 = fabs(dl) > 0.0;
+            const bool pR = hasR & ((hasL & cRL) | (!hasL & cR0));  // bitwise: no branches
+            const bool pL = hasL & cL0;
+            const int pick = pR ? lane : (pL ? lane - 1 : -1);
             const int pr = __shfl_down_sync(FULL, pick, 1);
             const int pl = __shfl_up_sync(FULL, pick, 1);
             const bool mR = hasR && pick == lane && pr == lane;
@@ -838,6 +847,8 @@ __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, c
 
 template <bool MEM>
 __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
+    pdl_wait();
+    pdl_trigger();
     extern __shared__ __align__(16) char smem[];
     const int q = blockIdx.x, lane = threadIdx.x;
     const bool fluid = blockIdx.y == 1;
@@ -893,32 +904,33 @@ static cudaError_t launch_solver(const SolveArgs &a, cudaStream_t s) {
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
     const bool lm = latency_mode(a), mem = a.mem != nullptr;
     const dim3 grid(a.n_inst), block(lm ? 256 : 32);
+    cudaError_t e = cudaSuccess;
 #define DYNMO_SOLVER_Q(M, NW)                                                   \
     switch (table_q(a.max_layers)) {                                            \
-        case 1: K<M, NW, 1>::launch(grid, block, sm, s, a); break;            \
-        case 2: K<M, NW, 2>::launch(grid, block, sm, s, a); break;            \
-        case 4: K<M, NW, 4>::launch(grid, block, sm, s, a); break;            \
-        case 8: K<M, NW, 8>::launch(grid, block, sm, s, a); break;            \
-        default: K<M, NW, 0>::launch(grid, block, sm, s, a); break;           \
+        case 1: e = K<M, NW, 1>::launch(grid, block, sm, s, a); break;        \
+        case 2: e = K<M, NW, 2>::launch(grid, block, sm, s, a); break;        \
+        case 4: e = K<M, NW, 4>::launch(grid, block, sm, s, a); break;        \
+        case 8: e = K<M, NW, 8>::launch(grid, block, sm, s, a); break;        \
+        default: e = K<M, NW, 0>::launch(grid, block, sm, s, a); break;       \
     }
     if (mem && lm) { DYNMO_SOLVER_Q(true, 8) }
     else if (mem) { DYNMO_SOLVER_Q(true, 1) }
     else if (lm) { DYNMO_SOLVER_Q(false, 8) }
     else { DYNMO_SOLVER_Q(false, 1) }
 #undef DYNMO_SOLVER_Q
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <bool M, int NW, int Q>
 struct PartitionK {
-    static void launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
-        k_partition<M, NW, Q><<<g, b, sm, s>>>(a);
+    static cudaError_t launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
+        return launch_pdl(k_partition<M, NW, Q>, g, b, sm, s, a);
     }
 };
 template <bool M, int NW, int Q>
 struct RepackK {
-    static void launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
-        k_repack<M, NW, Q><<<g, b, sm, s>>>(a);
+    static cudaError_t launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
+        return launch_pdl(k_repack<M, NW, Q>, g, b, sm, s, a);
     }
 };
 
@@ -927,9 +939,9 @@ cudaError_t launch_diffuse(const SolveArgs &a, cudaStream_t s) {
     const bool fl = a.fluid_x != nullptr;
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, fl);
     const dim3 grid(a.n_inst, fl ? 2 : 1);
-    if (a.mem) k_diffuse<true><<<grid, 32, sm, s>>>(a);
-    else k_diffuse<false><<<grid, 32, sm, s>>>(a);
-    return cudaGetLastError();
+    const cudaError_t e = a.mem ? launch_pdl(k_diffuse<true>, grid, 32, sm, s, a)
+                                : launch_pdl(k_diffuse<false>, grid, 32, sm, s, a);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 cudaError_t launch_repack(const SolveArgs &a, cudaStream_t s) { return launch_solver<RepackK>(a, s); }
 
