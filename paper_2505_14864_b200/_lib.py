@@ -11,7 +11,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # DYNMO_DEBUG=1 loads the bounds-checked build (csrc: make debug) instead
-LIB_PATH = os.path.join(_HERE, "libdynmo_dbg.so" if os.environ.get("DYNMO_DEBUG") == "1" else "libdynmo.so")
+# (DYNMO_LIB=<path> loads another build of the same ABI, for A/B measurements)
+LIB_PATH = os.environ.get("DYNMO_LIB") or os.path.join(
+    _HERE, "libdynmo_dbg.so" if os.environ.get("DYNMO_DEBUG") == "1" else "libdynmo.so")
 
 OK, E_INVALID, E_INFEASIBLE, E_OVERFLOW, E_CUDA, E_NCCL, E_NOMEM = 0, -1, -2, -3, -4, -5, -6
 W_NOT_CONVERGED, W_BOUND_UNMET = 1, 2

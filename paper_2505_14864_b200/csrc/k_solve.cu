@@ -894,8 +894,14 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
 // search.  Large batches: 1 warp per instance (binary search, one wave).
 static bool latency_mode(const SolveArgs &a) { return a.n_inst <= 4 * 148; }
 
-// jump-table width for the batch: registers per lane (L <= 32 Q - 1), 0 = windows
-static int table_q(int max_layers) {
+// Jump-table width for the batch: registers per lane (L <= 32 Q - 1), or 0
+// = warp windows.  Tables shorten the dependent chain of ONE instance (the
+// latency mode); in the throughput mode (thousands of one-warp CTAs) total
+// work and occupancy decide, and a table of Q >= 4 costs 4-8x the shared
+// loads of n window jumps and ~150 registers (config 5: 38 -> 163 us), so
+// there only Q <= 2 is used.
+static int table_q(int max_layers, bool latency) {
+    if (!latency && max_layers >= 64) return 0;
     return max_layers < 32 ? 1 : max_layers < 64 ? 2 : max_layers < 128 ? 4 : max_layers < 256 ? 8 : 0;
 }
 
@@ -906,7 +912,7 @@ static cudaError_t launch_solver(const SolveArgs &a, cudaStream_t s) {
     const dim3 grid(a.n_inst), block(lm ? 256 : 32);
     cudaError_t e = cudaSuccess;
 #define DYNMO_SOLVER_Q(M, NW)                                                   \
-    switch (table_q(a.max_layers)) {                                            \
+    switch (table_q(a.max_layers, lm)) {                                        \
         case 1: e = K<M, NW, 1>::launch(grid, block, sm, s, a); break;        \
         case 2: e = K<M, NW, 2>::launch(grid, block, sm, s, a); break;        \
         case 4: e = K<M, NW, 4>::launch(grid, block, sm, s, a); break;        \

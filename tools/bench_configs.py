@@ -1,7 +1,7 @@
 """Per-config device timings of the hot path on one B200 (BASELINE configs 1, 3,
 4, 5; config 2 is bench.py's headline).  Each config's device work is captured
 once in a CUDA graph and replayed; CUDA events around each replay (L2 flushed
-between replays by a 256 MiB write outside the events).  Results are checked
+between replays outside the events, as in bench.py).  Results are checked
 against the oracle on the same seeded inputs before timing.  Prints one JSON
 object per config and writes gpurun_out/bench_configs.json.
 """
@@ -18,6 +18,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import bench  # noqa: E402
 import oracle  # noqa: E402
 import synth  # noqa: E402
 from paper_2505_14864_b200 import _lib as LB  # noqa: E402
@@ -29,7 +30,8 @@ flush = None
 
 
 def timed(fn, reps=20):
-    """Device ms per replay of fn captured in a CUDA graph."""
+    """Device ms per replay of fn captured in a CUDA graph (L2 flushed
+    before each replay as in bench.py: a write and a read larger than L2)."""
     fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -37,7 +39,7 @@ def timed(fn, reps=20):
         fn()
     ts = []
     for _ in range(reps):
-        flush.fill_(1)
+        flush()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         g.replay()
@@ -216,7 +218,7 @@ def config5(ctx, n_inst=4096):
 def main():
     global flush
     torch.cuda.set_device(0)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=DEV)
+    flush = bench.L2Flush(DEV)
     ctx = D.Context(0)
     res = {}
     for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
