@@ -99,7 +99,8 @@ dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total
 /* ----------------------------------------------------------- profiling --
  * Sources of per-layer workload (P:L234-239 pruning p_i, P:L266-283 freezing
  * f_i, P:L340-353 early exit t_i, P:L376-389 MoD r_i t_i, P:L209-214 MoE
- * tokens per expert).  A segment is a caller-owned device array that
+ * tokens per expert; P:L632 + P:L720 + P:L743 execution time, the "by Time"
+ * balancers).  A segment is a caller-owned device array that
  * contributes to ONE layer (or, for EXIT_U8, to every local layer).  All
  * contributions to a layer are summed, so one layer may have several
  * segments (e.g. its four weight tensors). */
@@ -119,7 +120,14 @@ enum {
                                   i (layer field ignored)                     */
     DYNMO_SRC_EXPERT_I64 = 6,  /* int64 top-k expert ids [T*k] of a MoE layer;
                                   histogram over [0, n_experts)               */
-    DYNMO_SRC_EXPERT_I32 = 7   /* int32 variant                              */
+    DYNMO_SRC_EXPERT_I32 = 7,  /* int32 variant                              */
+    DYNMO_SRC_TIME_NS = 8      /* int64 (begin, end) timestamp pairs in ns,
+                                  n_elem int64 values (even; 8-byte aligned);
+                                  adds sum(end - begin) to time_i.  end < begin
+                                  is INVALID.  Stamps from dynmo_timestamp (or
+                                  any monotonic ns clock); a layer's boundary
+                                  stamps s[i], s[i+1] can be the overlapping
+                                  segment {&s[i], 2}.                         */
 };
 
 typedef struct dynmo_segment {
@@ -132,15 +140,16 @@ typedef struct dynmo_segment {
     int32_t top_k;       /* EXPERT_*: informational (n_elem = T*k)          */
 } dynmo_segment;
 
-/* Per-local-layer cost coefficients (readings Q1-Q6):
- *   c_i = frozen_i ? F : tok_i * (A + B * nnz_i) + C * moe_i
+/* Per-local-layer cost coefficients (readings Q1-Q6, Q21):
+ *   c_i = frozen_i ? F : tok_i * (A + B * nnz_i) + C * moe_i + D * time_i
+ * ("by Param" balancing: B = 1; "by Time": D = 1, A = B = C = 0)
  *   moe_i = EP * max_{r<EP} sum_{e in group r} cnt_{i,e}
  * groups = EP contiguous blocks of E/EP experts (EP <= 0 means EP = E;
  * E % EP != 0 is INVALID).  Absent sources default to tok_i = 1, nnz_i = 0,
- * moe_i = 0.  Checked int64 arithmetic (128-bit intermediates): a result
- * above INT64_MAX is OVERFLOW; a negative coefficient is INVALID. */
+ * moe_i = 0, time_i = 0.  Checked int64 arithmetic (128-bit intermediates):
+ * a result above INT64_MAX is OVERFLOW; a negative coefficient is INVALID. */
 typedef struct dynmo_cost_coef {
-    int64_t A, B, C, F;
+    int64_t A, B, C, F, D;
     int32_t ep_ranks;
     int32_t pad;
 } dynmo_cost_coef;
@@ -184,20 +193,30 @@ int32_t dynmo_plan_max_experts(dynmo_plan plan);
  *   d_frozen   [n_local] uint8, nullable (no layer frozen)
  *   d_coef     [n_local] dynmo_cost_coef, required
  *   d_mem_local[n_local] int64 caller memory per layer, nullable
- *   d_counters [n_local][4] int64 out, nullable: {nnz_i, tok_i, moe_i, c_i}
- *              with the defaults applied (tok_i = 1 without a token source)
+ *   d_counters [n_local][5] int64 out, nullable: {nnz_i, tok_i, moe_i, c_i,
+ *              time_i} with the defaults applied (tok_i = 1 without a token
+ *              source)
  *   d_hist     [n_local][max_experts] int64 out, nullable: cnt_{i,e}
  *   d_cost     [n_total] int64 out: global (exchange) or local cost vector
  *   d_mem      [n_total] int64 out, nullable: gathered d_mem_local (zeros if
  *              d_mem_local is NULL)
- *   d_status   [1] int32 out: OK, INVALID (expert id outside [0,E), bad
- *              coefficient, slices do not tile), OVERFLOW; the most negative
+ *   d_status   [1] int32 out: OK, INVALID (expert id outside [0,E), a time
+ *              pair with end < begin, bad coefficient, slices do not tile),
+ *              OVERFLOW; the most negative
  *              code wins.  Layers with an error get c_i = -1.
  * Collective when the plan exchanges: every rank must call it. */
 dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t *d_frozen,
                                   const dynmo_cost_coef *d_coef, const int64_t *d_mem_local,
                                   int64_t *d_counters, int64_t *d_hist, int64_t *d_cost,
                                   int64_t *d_mem, int32_t *d_status, dynmo_stream stream);
+
+/* Device timestamp for the "by Time" source (the profiling
+ * iteration's layer execution times): enqueues on `stream` a one-thread
+ * kernel that stores %globaltimer (ns, monotonic, GPU-wide) into *d_slot when
+ * the work enqueued before it on the stream has completed -- call it at layer
+ * boundaries of the profiling iteration, no host synchronisation.  Capturable
+ * in a CUDA graph.  d_slot: int64 device pointer, caller-owned. */
+dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream);
 
 /* -------------------------------------------------------------- solvers --
  * Batched instance layout shared by calls 2-4 (one CTA per instance):

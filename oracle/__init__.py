@@ -54,7 +54,8 @@ def lib():
             "oracle_expert_hist_i64": (C.c_int, [p, i64, i32, p]),
             "oracle_expert_hist_i32": (C.c_int, [p, i64, i32, p]),
             "oracle_layer_cost": (C.c_int, [C.c_int, C.c_int, i64, i64, C.c_int, p, i32,
-                                            i64, i64, i64, i64, i32, p]),
+                                            i64, i64, i64, i64, i32, i64, i64, p]),
+            "oracle_time_ns": (C.c_int, [p, i64, p]),
             "oracle_stage_loads": (None, [p, i32, p, p]),
             "oracle_imbalance": (dbl, [p, i32]),
             "oracle_phi": (C.c_int, [p, i32, p]),
@@ -121,14 +122,22 @@ def expert_hist(idx: np.ndarray, E: int) -> tuple[int, np.ndarray]:
 
 
 # ------------------------------------------------------------------ O2 cost
-def layer_cost(*, frozen=False, tok=None, nnz=0, cnt=None, A=0, B=0, C_=0, F=0, ep=0):
+def time_ns(v: np.ndarray) -> tuple[int, int]:
+    """(status, sum of end - begin) over (begin, end) int64 pairs."""
+    a = _c(v, np.int64)
+    out = np.zeros(1, np.int64)
+    st = lib().oracle_time_ns(_ptr(a), a.size, _ptr(out))
+    return int(st), int(out[0])
+
+
+def layer_cost(*, frozen=False, tok=None, nnz=0, cnt=None, A=0, B=0, C_=0, F=0, ep=0, D=0, time=0):
     cost = np.zeros(1, np.int64)
     c = _c(cnt, np.int64) if cnt is not None else np.zeros(1, np.int64)
     E = 0 if cnt is None else len(cnt)
     st = lib().oracle_layer_cost(int(bool(frozen)), int(tok is not None),
                                  int(tok if tok is not None else 0), int(nnz),
                                  int(cnt is not None), _ptr(c), E, int(A), int(B), int(C_),
-                                 int(F), int(ep), _ptr(cost))
+                                 int(F), int(ep), int(D), int(time), _ptr(cost))
     return int(st), int(cost[0])
 
 

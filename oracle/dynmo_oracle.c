@@ -114,22 +114,42 @@ int oracle_expert_hist_i32(const int32_t *idx, int64_t n, int32_t E, int64_t *cn
 }
 
 /* ------------------------------------------------------------------------
- * O2 cost of one layer (readings Q1-Q6):
- *   c = frozen ? F : tok*(A + B*nnz) + C*moe,
+ * O1' execution time of a layer from its timestamp pairs ("by Time"
+ * balancers, P:L632 profiling iteration timers, "decoder layer
+ * execution times"; reading Q21): time = sum over pairs of
+ * (end - begin), pairs stored (begin, end) consecutively, n values (even).
+ * A pair with end < begin is INVALID (skipped); an odd n is INVALID.
+ * ---------------------------------------------------------------------- */
+int oracle_time_ns(const int64_t *v, int64_t n, int64_t *time) {
+    int st = (n % 2) ? O_E_INVALID : O_OK;
+    i128 acc = 0;
+    for (int64_t j = 0; j + 1 < n; j += 2) {
+        if (v[j + 1] < v[j]) { st = O_E_INVALID; continue; }
+        acc += (i128)v[j + 1] - (i128)v[j];
+    }
+    *time = acc > (i128)INT64_MAX ? -1 : (int64_t)acc;
+    if (acc > (i128)INT64_MAX) st = O_E_OVERFLOW;
+    return st;
+}
+
+/* ------------------------------------------------------------------------
+ * O2 cost of one layer (readings Q1-Q6, Q21):
+ *   c = frozen ? F : tok*(A + B*nnz) + C*moe + D*time,
  *   moe = EP * max_{r<EP} sum_{e in group r} cnt[e]   (groups of E/EP
  *   consecutive experts; EP<=0 means EP=E), defaults tok=1 (no token
  *   source), nnz=0, moe=0 (no expert source).
  * Freezing P:L278-282 (F=0 is the paper's "contributing no computational
- * load"), pruning P:L238 (A=0,B=1), early exit P:L344 / MoD P:L380 (B=0).
+ * load"), pruning P:L238 (A=0,B=1), early exit P:L344 / MoD P:L380 (B=0),
+ * by Time P:L720/P:L743 (D=1, A=B=C=0; time = 0 without a time source).
  * Checked arithmetic in 128 bits; negative coefficients INVALID; a result
  * above INT64_MAX is OVERFLOW.  On error *cost = -1.
  * ---------------------------------------------------------------------- */
 int oracle_layer_cost(int frozen, int has_tok, int64_t tok, int64_t nnz,
                       int has_moe, const int64_t *cnt, int32_t E,
                       int64_t A, int64_t B, int64_t C, int64_t F, int32_t ep,
-                      int64_t *cost) {
+                      int64_t D, int64_t time, int64_t *cost) {
     *cost = -1;
-    if (A < 0 || B < 0 || C < 0 || F < 0 || tok < 0 || nnz < 0) return O_E_INVALID;
+    if (A < 0 || B < 0 || C < 0 || F < 0 || D < 0 || tok < 0 || nnz < 0 || time < 0) return O_E_INVALID;
     if (frozen) { *cost = F; return O_OK; }
     i128 moe = 0;
     if (has_moe) {
@@ -155,6 +175,10 @@ int oracle_layer_cost(int frozen, int has_tok, int64_t tok, int64_t nnz,
     i128 cm = (i128)C * moe;
     if (cm > LIM) return O_E_OVERFLOW;
     c += cm;
+    if (c > LIM) return O_E_OVERFLOW;
+    i128 ct = (i128)D * (i128)time;
+    if (ct > LIM) return O_E_OVERFLOW;
+    c += ct;
     if (c > LIM) return O_E_OVERFLOW;
     *cost = (int64_t)c;
     return O_OK;

@@ -120,6 +120,35 @@ def test_cost_overflow_and_invalid():
 
 
 # -------------------------------------------------------------- ΔL and φ
+def test_time_ns_pins():
+    """O1' (P:L632/P:L720 execution-time profiling, reading Q21): boundary
+    stamps telescope -- sum over layers of (s[i+1] - s[i]) = s[L] - s[0];
+    random pairs vs Python integers; end < begin and an odd count INVALID;
+    a sum above INT64_MAX is OVERFLOW; the by-Time cost is the time itself."""
+    g = np.random.default_rng(21)
+    for _ in range(50):
+        L = int(g.integers(1, 40))
+        s_ = np.cumsum(g.integers(0, 10 ** 9, L + 1)).astype(np.int64)
+        per = [oracle.time_ns(s_[i:i + 2]) for i in range(L)]
+        assert all(st == 0 for st, _ in per)
+        assert sum(t for _, t in per) == int(s_[-1] - s_[0])
+        pairs = g.integers(0, 2 ** 40, (int(g.integers(1, 30)), 2)).astype(np.int64)
+        pairs.sort(axis=1)
+        assert oracle.time_ns(pairs.reshape(-1)) == (0, sum(int(e) - int(b) for b, e in pairs))
+    assert oracle.time_ns(np.array([5, 4], np.int64))[0] == oracle.E_INVALID
+    assert oracle.time_ns(np.array([1, 2, 3], np.int64))[0] == oracle.E_INVALID
+    assert oracle.time_ns(np.array([0, 2 ** 62, 0, 2 ** 62, 0, 2 ** 62], np.int64))[0] == oracle.E_OVERFLOW
+    assert oracle.time_ns(np.zeros(0, np.int64)) == (0, 0)
+    # cost: D * time added last, checked; by Time = the time itself
+    assert oracle.layer_cost(D=1, time=123456789) == (0, 123456789)
+    assert oracle.layer_cost(tok=3, A=2, nnz=5, B=1, D=4, time=10) == (0, 3 * (2 + 5) + 40)
+    assert oracle.layer_cost(frozen=True, F=7, D=1, time=99) == (0, 7)
+    assert oracle.layer_cost(D=-1, time=1)[0] == oracle.E_INVALID
+    assert oracle.layer_cost(D=2, time=2 ** 62)[0] == oracle.E_OVERFLOW
+    assert oracle.layer_cost(D=1, time=2 ** 63 - 1) == (0, 2 ** 63 - 1)
+    assert oracle.layer_cost(A=1, D=1, time=2 ** 63 - 1)[0] == oracle.E_OVERFLOW
+
+
 def test_imbalance_and_phi_spec_examples():
     """Pin: SPEC.md:L89-91 (eq:imbalance) and SPEC.md:L301-303 (phi)."""
     for ex in GOLD["imbalance"]:
