@@ -19,7 +19,7 @@ OK, E_INVALID, E_INFEASIBLE, E_OVERFLOW, E_CUDA, E_NCCL, E_NOMEM = 0, -1, -2, -3
 W_NOT_CONVERGED, W_BOUND_UNMET = 1, 2
 
 SRC_MASK_BITS, SRC_MASK_U8, SRC_NZ_BF16, SRC_NZ_F32 = 0, 1, 2, 3
-SRC_TOKMASK_BITS, SRC_EXIT_U8, SRC_EXPERT_I64, SRC_EXPERT_I32 = 4, 5, 6, 7
+SRC_TOKMASK_BITS, SRC_EXIT_U8, SRC_EXPERT_I64, SRC_EXPERT_I32, SRC_TIME_NS = 4, 5, 6, 7, 8
 REPACK_BOUND, REPACK_ALG2 = 0, 1
 PHASES = ["profile", "epilogue", "exchange", "partition", "diffuse", "repack", "migrate"]
 MAX_LAYERS = 1023
@@ -63,6 +63,7 @@ def lib():
         "dynmo_plan_bytes": (i64, [p]),
         "dynmo_plan_max_experts": (i32, [p]),
         "dynmo_profile_layers": (i32, [p, p, p, p, p, p, p, p, p, p, p]),
+        "dynmo_timestamp": (i32, [p, p, p]),
         "dynmo_partition_stages": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, p, p]),
         "dynmo_diffuse_balance": (i32, [p, i32, i32, p, p, p, p, p, p, p, p, p, i32,
                                         p, p, p, p, p, p, p, p, p, p]),
@@ -88,7 +89,7 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_ctx_create", "dynmo_ctx_destroy", "dynmo_ctx_nranks", "dynmo_ctx_rank",
             "dynmo_ctx_set_timing", "dynmo_ctx_timing_read", "dynmo_ctx_timing_poll",
             "dynmo_profile_plan_create", "dynmo_profile_plan_destroy", "dynmo_plan_num_tiles",
-            "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers",
+            "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers", "dynmo_timestamp",
             "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",
             "dynmo_migrate_layers", "dynmo_migration_plan", "dynmo_migrate_plan_create",
             "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",

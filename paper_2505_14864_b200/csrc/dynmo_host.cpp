@@ -367,7 +367,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
             if (k == DYNMO_SRC_EXIT_U8) pre_exit = true;
             if (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32)
                 pre_words = std::max(pre_words, expert_words(std::min((int)h_segs[i].n_experts, kMaxExperts)));
-            pre_ops |= k == DYNMO_SRC_EXIT_U8 ? 2 : (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) ? 4 : 1;
+            pre_ops |= k == DYNMO_SRC_EXIT_U8 ? 2 : (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) ? 4 : 1;  // TIME: count family
             const int64_t ne = h_segs[i].n_elem < 0 ? 0 : h_segs[i].n_elem;
             const int es = k == DYNMO_SRC_NZ_BF16 ? 2 : (k == DYNMO_SRC_NZ_F32 || k == DYNMO_SRC_EXPERT_I32) ? 4
                            : k == DYNMO_SRC_EXPERT_I64 ? 8 : 1;
@@ -391,8 +391,10 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     for (int32_t i = 0; i < n_segs; ++i) {
         const dynmo_segment &sg = h_segs[i];
         if (sg.n_elem < 0) return invalid("negative n_elem");
-        if (sg.src_kind < DYNMO_SRC_MASK_BITS || sg.src_kind > DYNMO_SRC_EXPERT_I32)
+        if (sg.src_kind < DYNMO_SRC_MASK_BITS || sg.src_kind > DYNMO_SRC_TIME_NS)
             return invalid("unknown src_kind");
+        if (sg.src_kind == DYNMO_SRC_TIME_NS && sg.n_elem % 2)
+            return invalid("TIME_NS segment with an odd number of stamps");
         const bool is_exit = sg.src_kind == DYNMO_SRC_EXIT_U8;
         const int q = sg.layer - layer_begin;
         if (!is_exit && (q < 0 || q >= n_local)) return invalid("segment layer outside local range");
@@ -413,6 +415,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
             case DYNMO_SRC_EXIT_U8: op = OP_EXIT; nb = sg.n_elem; break;
             case DYNMO_SRC_EXPERT_I64: op = OP_EXP64; es = 8; nb = sg.n_elem * 8; break;
             case DYNMO_SRC_EXPERT_I32: op = OP_EXP32; es = 4; nb = sg.n_elem * 4; break;
+            case DYNMO_SRC_TIME_NS: op = OP_TIME; es = 8; nb = sg.n_elem * 8; slot = ACC_TIME; break;
         }
         if (sg.src_kind == DYNMO_SRC_EXPERT_I64 || sg.src_kind == DYNMO_SRC_EXPERT_I32) {
             E = sg.n_experts;
@@ -427,6 +430,8 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
             has_hist = true;
         } else if (slot == ACC_TOK) {
             info[q].flags |= SRC_HAS_TOK;
+        } else if (slot == ACC_TIME) {
+            info[q].flags |= SRC_HAS_TIME;
         } else {
             info[q].flags |= SRC_HAS_NNZ;
         }
@@ -437,6 +442,13 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
         bytes += nb + (partial_bits ? 1 : 0);
         const int32_t lay = is_exit ? 0 : q;
         const uint16_t aux = (uint16_t)(E ? E : slot);
+        if (op == OP_TIME) {  // pairs only need 8-byte alignment: tiles of <= 1024 pairs
+            for (int64_t o = 0; o < nb; o += 16 * 1024) {
+                const int64_t len = std::min<int64_t>(16 * 1024, nb - o);
+                sca.push_back(ProfTile{(const void *)(p + o), (uint32_t)len, lay, (uint16_t)OP_TIME, aux, 0});
+            }
+            continue;
+        }
         auto add_scalar = [&](uintptr_t a, int64_t n, uint32_t bits) {
             if (n <= 0) return;
             sca.push_back(ProfTile{(const void *)a, (uint32_t)n, lay, (uint16_t)(op | OP_SCALAR), aux, bits});
@@ -550,7 +562,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     pl->ops = 0;
     for (const ProfTile &t : tiles) {
         const int k = t.op & 0xF;
-        pl->ops |= k <= OP_NZ32 ? 1 : k == OP_EXIT ? 2 : 4;
+        pl->ops |= (k <= OP_NZ32 || k == OP_TIME) ? 1 : k == OP_EXIT ? 2 : 4;
     }
     if (!pl->ops) pl->ops = 1;
     const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(pl->ops, pl->warp_words);
@@ -651,6 +663,13 @@ static dynmo_status check_solve(dynmo_ctx ctx, int32_t n_inst, int32_t max_layer
     if (max_layers < 1 || max_layers > DYNMO_MAX_LAYERS) return invalid("max_layers outside [1, 1023]");
     if (!cost || !layer_off || !n_stages || !bnd_off || !bnd_out || !status)
         return invalid("null required pointer");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream) {
+    if (!ctx || !d_slot) return invalid("null ctx/slot");
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_stamp(d_slot, (cudaStream_t)stream), "k_stamp launch");
     return DYNMO_OK;
 }
 

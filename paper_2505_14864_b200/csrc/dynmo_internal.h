@@ -38,12 +38,13 @@ enum ProfOp : uint16_t {
     OP_EXIT = 4,   // histogram of uint8 exit depths
     OP_EXP64 = 5,  // per-layer histogram of int64 expert ids
     OP_EXP32 = 6,  // per-layer histogram of int32 expert ids
-    OP_KINDS = 7,
+    OP_TIME = 7,   // sum of (end - begin) over int64 timestamp pairs (TIME_NS)
+    OP_KINDS = 8,
     OP_SCALAR = 0x10,  // flag: scalar tile
 };
 
 // Accumulator slots per local layer in the device workspace.
-enum { ACC_NNZ = 0, ACC_TOK = 1, ACC_N = 2 };
+enum { ACC_NNZ = 0, ACC_TOK = 1, ACC_TIME = 2, ACC_N = 3 };
 
 struct ProfTile {
     const void *ptr;   // first byte
@@ -56,7 +57,7 @@ struct ProfTile {
 static_assert(sizeof(ProfTile) == 24, "tile layout");
 
 // Static per-local-layer source flags, known at plan creation.
-enum { SRC_HAS_NNZ = 1, SRC_HAS_TOK = 2, SRC_HAS_MOE = 4, SRC_HAS_EXIT = 8 };
+enum { SRC_HAS_NNZ = 1, SRC_HAS_TOK = 2, SRC_HAS_MOE = 4, SRC_HAS_EXIT = 8, SRC_HAS_TIME = 16 };
 struct LayerInfo {
     int32_t flags;
     int32_t E;   // experts of this layer (0 if no MoE source)
@@ -154,6 +155,7 @@ inline int profile_warp_words(bool any_exit, int max_expert_words) {
     return m > 0 ? m : 1;
 }
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
+cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
                           cudaStream_t s);

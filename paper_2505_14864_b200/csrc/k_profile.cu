@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
         acc0 = acc1 = 0;
         nacc = 0;
     };
-    auto feed = [&](int64_t key, uint32_t c) {
+    auto feed = [&](int64_t key, unsigned long long c) {
         if (key != run_key) {
             DYNMO_DCHECK(run_key < 0 || run_key < (int64_t)a.n_local * ACC_N);
             if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
@@ -250,6 +250,22 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
             continue;
         }
         if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
+        if (HAS_CNT && kind == OP_TIME) {
+            // (begin, end) int64 ns pairs (8-byte aligned): lane-strided
+            // pairs, end - begin summed in 64 bits; end < begin is INVALID
+            const int64_t *v = (const int64_t *)t.ptr;
+            const uint32_t np = t.nbytes >> 4;
+            unsigned long long s = 0;
+            for (uint32_t i = lane; i < np; i += 32) {
+                const int64_t b = v[2 * i], e = v[2 * i + 1];
+                if (e < b) bad = 1;
+                else s += (unsigned long long)(e - b);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
+            feed((int64_t)t.layer * ACC_N + t.aux, s);
+            continue;
+        }
         if (HAS_CNT && kind <= OP_NZ32) {
             uint32_t c;
             if (scalar) {
@@ -427,8 +443,9 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                 if (c) atomicAdd(&a.exit_hist[vb], (unsigned long long)c);
             }
         }
-        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
     }
+    // an expert id outside [0, E) or a time pair with end < begin
+    if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
 }
 
 // -------------------------------------------------------------- epilogue
@@ -452,8 +469,10 @@ __global__ void k_epilogue(EpiArgs a) {
         const int gi = a.layer_begin + q;
         unsigned long long nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
         unsigned long long tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
+        const unsigned long long time_u = a.acc[(int64_t)q * ACC_N + ACC_TIME];
         a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
         a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
+        a.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
         if (li.flags & SRC_HAS_EXIT)
             for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
         const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
@@ -461,7 +480,7 @@ __global__ void k_epilogue(EpiArgs a) {
         const bool frozen = a.frozen && a.frozen[q];
         // moe_i = EP * max over EP groups of group token counts (reading Q5)
         __int128 moe = 0;
-        const bool bad_coef = cf.A < 0 || cf.B < 0 || cf.C < 0 || cf.F < 0;
+        const bool bad_coef = cf.A < 0 || cf.B < 0 || cf.C < 0 || cf.F < 0 || cf.D < 0;
         bool bad_ep = false;
         if (li.flags & SRC_HAS_MOE) {
             const int E = li.E;
@@ -501,17 +520,21 @@ __global__ void k_epilogue(EpiArgs a) {
             } else {
                 __int128 v = tok * inner;
                 const __int128 cm = (__int128)cf.C * moe;
-                if (v > LIM || cm > LIM || v + cm > LIM) st = DYNMO_E_OVERFLOW;
-                else c = (int64_t)(v + cm);
+                const __int128 tm = (__int128)time_u;
+                const __int128 ct = tm > LIM ? LIM + 1 : (__int128)cf.D * tm;
+                if (tm > LIM || v > LIM || cm > LIM || v + cm > LIM || ct > LIM || v + cm + ct > LIM)
+                    st = DYNMO_E_OVERFLOW;
+                else c = (int64_t)(v + cm + ct);
             }
         }
         const int64_t m = a.mem_local ? a.mem_local[q] : 0;
         if (a.counters_out) {
-            int64_t *o = a.counters_out + (int64_t)q * 4;
+            int64_t *o = a.counters_out + (int64_t)q * 5;
             o[0] = (int64_t)nnz_u;
             o[1] = has_tok ? (int64_t)tok_u : 1;
             o[2] = moe > LIM ? -1 : (int64_t)moe;
             o[3] = c;
+            o[4] = time_u > (unsigned long long)INT64_MAX ? -1 : (int64_t)time_u;
         }
         if (a.p2p) {
             // straight into every rank's receive slot (NVLink stores)
@@ -713,6 +736,19 @@ cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s) {
     const int threads = 256;
     const int grid = a.n_local > 0 ? (a.n_local + threads - 1) / threads : 1;
     return launch_pdl(k_epilogue, grid, threads, 0, s, a);
+}
+
+// %globaltimer (ns) into *p once the preceding work of the stream is done
+// (a normal launch, NOT programmatic: it must not start early)
+__global__ void k_stamp(int64_t *p) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *p = (int64_t)t;
+}
+
+cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s) {
+    k_stamp<<<1, 1, 0, s>>>(d_slot);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,

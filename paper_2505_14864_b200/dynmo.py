@@ -184,13 +184,22 @@ class ProfilePlan:
             pass
 
 
-def coef_tensor(n: int, A=0, B=0, C_=0, F=0, ep=0, device="cuda") -> torch.Tensor:
-    """dynmo_cost_coef[n] as an int64 [n, 5] tensor (A, B, C, F, ep|pad)."""
-    t = torch.zeros((n, 5), dtype=torch.int64)
-    for j, v in enumerate((A, B, C_, F)):
+def coef_tensor(n: int, A=0, B=0, C_=0, F=0, ep=0, D=0, device="cuda") -> torch.Tensor:
+    """dynmo_cost_coef[n] as an int64 [n, 6] tensor (A, B, C, F, D, ep|pad):
+    c_i = frozen ? F : tok (A + B nnz) + C moe + D time."""
+    t = torch.zeros((n, 6), dtype=torch.int64)
+    for j, v in enumerate((A, B, C_, F, D)):
         t[:, j] = torch.as_tensor(v, dtype=torch.int64)
-    t[:, 4] = torch.as_tensor(ep, dtype=torch.int64) & 0xFFFFFFFF  # int32 ep, zero pad
+    t[:, 5] = torch.as_tensor(ep, dtype=torch.int64) & 0xFFFFFFFF  # int32 ep, zero pad
     return t.to(device)
+
+
+def timestamp(ctx: Context, slot: torch.Tensor, stream=None):
+    """dynmo_timestamp: %globaltimer (ns) into the int64 device scalar `slot`
+    (e.g. stamps[i]) once the work queued before it on the stream is done."""
+    if slot.dtype != torch.int64 or not slot.is_cuda:
+        raise ValueError("slot must be an int64 device tensor element")
+    _check(lib().dynmo_timestamp(ctx.handle, _ptr(slot), _stream(stream)), "dynmo_timestamp")
 
 
 def profile_layers(ctx: Context, plan: ProfilePlan, coef: torch.Tensor, *, frozen=None,

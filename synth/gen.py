@@ -227,3 +227,25 @@ def cfg5_instance(i: int, T: int = 4096, h: int = 1024) -> SweepInstance:
     # split of ceil(L/n) layers per stage, each layer processing all T tokens
     bound = -(-L // n) * T
     return SweepInstance(L=L, n=n, masks=masks, mem=mem, cap=cap, bound=bound)
+
+
+# ----------------------------------------------------------------------------
+# "By Time" profiling input: per-layer timestamps of a profiling iteration.
+def time_stamps(base_ns: np.ndarray, microbatches: int = 4, jitter: float = 0.05, gap_ns: int = 2000,
+                t0: int = 1_760_000_000_000_000_000, seed_key: int = 0) -> np.ndarray:
+    """Boundary stamps int64 [M, L+1] of M micro-batch forward passes through
+    L layers (a monotonic ns clock like %globaltimer): layer i of micro-batch
+    m runs from s[m, i] to s[m, i+1], lasting base_ns[i] * LogNormal(0, jitter)
+    (rounded to ns); passes are separated by gap_ns.  base_ns is the caller's
+    per-layer model of the execution time (e.g. proportional to kept params)."""
+    base_ns = np.asarray(base_ns, np.float64)
+    L = len(base_ns)
+    g = rng(6, seed_key, L, microbatches)
+    dur = np.maximum(1, np.rint(base_ns[None, :] * np.exp(g.normal(0.0, jitter, (microbatches, L))))).astype(np.int64)
+    out = np.empty((microbatches, L + 1), np.int64)
+    t = int(t0)
+    for m in range(microbatches):
+        out[m, 0] = t
+        out[m, 1:] = t + np.cumsum(dur[m])
+        t = int(out[m, -1]) + gap_ns
+    return out

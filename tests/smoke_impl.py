@@ -41,7 +41,7 @@ def run_smoke() -> None:
             keep.append(d)
     plan = D.ProfilePlan(ctx, segs, 0, shape.L)
     coef = D.coef_tensor(shape.L, A=0, B=1, device=dev)
-    counters = torch.empty((shape.L, 4), dtype=torch.int64, device=dev)
+    counters = torch.empty((shape.L, 5), dtype=torch.int64, device=dev)
     cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters)
     torch.cuda.synchronize()
     assert int(st.item()) == 0

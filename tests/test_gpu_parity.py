@@ -85,7 +85,7 @@ def test_profile_masks_mixed_small(D, L, ctx, S, milestone):
     segs, keep, want = _mixed_segments(D, L, shape, S, milestone)
     plan = D.ProfilePlan(ctx, segs, 0, shape.L)
     coef = D.coef_tensor(shape.L, A=7, B=3, device=DEV)
-    counters = torch.empty((shape.L, 4), dtype=torch.int64, device=DEV)
+    counters = torch.empty((shape.L, 5), dtype=torch.int64, device=DEV)
     cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters)
     torch.cuda.synchronize()
     assert int(st.item()) == 0
@@ -164,7 +164,7 @@ def test_profile_exit_tokmask_frozen(D, L, ctx, F):
     # plan A: exit source for all layers
     planA = D.ProfilePlan(ctx, segs, 0, Lyr)
     coef = D.coef_tensor(Lyr, A=1, B=0, device=DEV)
-    cnt = torch.empty((Lyr, 4), dtype=torch.int64, device=DEV)
+    cnt = torch.empty((Lyr, 5), dtype=torch.int64, device=DEV)
     cost, _, st = D.profile_layers(ctx, planA, coef, frozen=_dev(frozen), counters=cnt)
     torch.cuda.synchronize()
     want = [oracle.layer_cost(frozen=bool(frozen[i]), tok=int(tok_exit[i]), A=1)[1] for i in range(Lyr)]
@@ -590,7 +590,7 @@ def test_profile_mixed_sources_one_plan(D, L, ctx):
         hists[5 + j] = oracle.expert_hist(idx[1:], E)[1]
     plan = D.ProfilePlan(ctx, segs, 0, 8)
     coef = D.coef_tensor(8, A=3, B=1, C_=2, ep=0, device=DEV)
-    counters = torch.empty((8, 4), dtype=torch.int64, device=DEV)
+    counters = torch.empty((8, 5), dtype=torch.int64, device=DEV)
     hist = torch.zeros((8, plan.max_experts), dtype=torch.int64, device=DEV)
     cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters, hist=hist)
     torch.cuda.synchronize()
@@ -603,3 +603,94 @@ def test_profile_mixed_sources_one_plan(D, L, ctx):
     want_cost = [oracle.layer_cost(tok=int(tok[i]), nnz=int(nnz[i]), cnt=hists.get(i), A=3, B=1, C_=2, ep=0)[1]
                  for i in range(8)]
     assert np.array_equal(cost.cpu().numpy(), want_cost)
+
+
+# ------------------------------------------------- NEXT-1: "by Time" source
+def test_profile_time_source(D, L, ctx):
+    """TIME_NS (P:L632/P:L720/P:L743, reading Q21): per layer and micro-batch
+    the overlapping boundary segment {&s[m, i], 2} (8-byte aligned only),
+    long contiguous pair arrays on two layers (several 1024-pair tiles, a
+    ragged last one), and a u8 mask source on every layer: time_i and
+    c_i = B nnz_i + D time_i vs the oracle; then by-Time costs (D = 1) and
+    their partition vs the oracle's."""
+    g = np.random.default_rng(61)
+    Lyr, M = 24, 4
+    s = synth.time_stamps(g.uniform(0.5, 2.0, Lyr) * 1e6, M)
+    ds = _dev(s.reshape(-1))
+    segs, want_t, keep = [], np.zeros(Lyr, np.int64), [ds]
+    for m in range(M):
+        for i in range(Lyr):
+            off = m * (Lyr + 1) + i
+            segs.append(D.SegmentSpec(ds[off:off + 2], L.SRC_TIME_NS, i))
+            want_t[i] += oracle.time_ns(s[m, i:i + 2])[1]
+    for i, npairs in ((3, 2500), (10, 1025)):
+        b = g.integers(0, 2 ** 40, npairs)
+        pr = np.stack([b, b + g.integers(0, 10 ** 6, npairs)], 1).astype(np.int64).reshape(-1)
+        t = _dev(pr)
+        keep.append(t)
+        segs.append(D.SegmentSpec(t, L.SRC_TIME_NS, i))
+        want_t[i] += oracle.time_ns(pr)[1]
+    masks = [(g.random(5000 + 7 * i) < 0.4).astype(np.uint8) for i in range(Lyr)]
+    nnz = np.array([oracle.count_nz_u8(m_) for m_ in masks])
+    mt = [_dev(m_) for m_ in masks]
+    segs += [D.SegmentSpec(t, L.SRC_MASK_U8, i) for i, t in enumerate(mt)]
+    plan = D.ProfilePlan(ctx, segs, 0, Lyr)
+    counters = torch.empty((Lyr, 5), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, D.coef_tensor(Lyr, B=3, D=1, device=DEV), counters=counters)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    c = counters.cpu().numpy()
+    assert np.array_equal(c[:, 4], want_t) and np.array_equal(c[:, 0], nnz)
+    want_cost = [oracle.layer_cost(nnz=int(nnz[i]), B=3, D=1, time=int(want_t[i]))[1] for i in range(Lyr)]
+    assert np.array_equal(cost.cpu().numpy(), want_cost)
+    costT, _, st = D.profile_layers(ctx, plan, D.coef_tensor(Lyr, D=1, device=DEV))
+    b = D.Batch([Lyr], [4], device=DEV)
+    bnd, bott, _, pst = D.partition_stages(ctx, b, costT)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and int(pst.item()) == 0
+    assert np.array_equal(costT.cpu().numpy(), want_t)
+    ost, ob, oB, _ = oracle.partition(want_t, 4)
+    assert np.array_equal(bnd.cpu().numpy()[:5], ob) and int(bott.item()) == oB
+
+
+def test_profile_time_invalid(D, L, ctx):
+    """A pair with end < begin is INVALID (device status), an odd stamp count
+    is rejected at plan creation (host)."""
+    pr = np.array([10, 20, 30, 25, 40, 41], np.int64)
+    assert oracle.time_ns(pr)[0] == oracle.E_INVALID
+    t = _dev(pr)
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, L.SRC_TIME_NS, 0)], 0, 1)
+    cost, _, st = D.profile_layers(ctx, plan, D.coef_tensor(1, D=1, device=DEV))
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_INVALID
+    with pytest.raises(D.DynmoError):
+        D.ProfilePlan(ctx, [D.SegmentSpec(t[:3], L.SRC_TIME_NS, 0)], 0, 1)
+
+
+def test_timestamp_kernel(D, ctx):
+    """dynmo_timestamp: stamps taken when the preceding stream work is done
+    (monotonic ns; durations proportional to the work between stamps) and
+    re-taken at every CUDA-graph replay."""
+    st = torch.zeros(3, dtype=torch.int64, device=DEV)
+    torch.cuda._sleep(1000)  # load the sleep kernel (lazy loading would idle the stream)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(50_000_000)  # keep the device busy while the host enqueues the rest
+    D.timestamp(ctx, st[0])
+    torch.cuda._sleep(2_000_000)
+    D.timestamp(ctx, st[1])
+    torch.cuda._sleep(8_000_000)
+    D.timestamp(ctx, st[2])
+    torch.cuda.synchronize()
+    s = st.cpu().numpy()
+    d1, d2 = int(s[1] - s[0]), int(s[2] - s[1])
+    assert 0 < d1 < d2 and 2.5 < d2 / d1 < 6.0, (d1, d2)
+    one = torch.zeros(1, dtype=torch.int64, device=DEV)
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr):
+        D.timestamp(ctx, one[0])
+    seen = []
+    for _ in range(3):
+        gr.replay()
+        torch.cuda.synchronize()
+        seen.append(int(one.item()))
+    assert seen[0] > int(s[2]) and seen[0] < seen[1] < seen[2]

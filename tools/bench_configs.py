@@ -215,6 +215,42 @@ def config5(ctx, n_inst=4096):
                 mean_workers_before=round(float(np.mean([x.n for x in insts])), 3))
 
 
+def config_bytime(ctx):
+    """NEXT-1 "by Time": config 2's 48 layers / 8 stages with per-layer
+    execution times from the profiling iteration (4 micro-batches of
+    boundary stamps, "four micro-batches per GPU"; base time of a
+    layer proportional to its kept parameters), D = 1: profile + partition."""
+    shape = synth.GPTShape()
+    L, n, M = shape.L, 8, 4
+    p = synth.cfg2_keep_probs(shape, 0.9, 4)
+    sizes = np.array([3, 1, 4, 4], np.float64) * shape.h * shape.h  # QKV, proj, fc1, fc2
+    kept = p @ sizes  # expected kept params per layer (p: keep probability per tensor)
+    s = synth.time_stamps(kept * 0.05, M)
+    ds = dev(s.reshape(-1))
+    segs = [D.SegmentSpec(ds[m * (L + 1) + i:m * (L + 1) + i + 2], LB.SRC_TIME_NS, i) for m in range(M) for i in range(L)]
+    plan = D.ProfilePlan(ctx, segs, 0, L)
+    coef = D.coef_tensor(L, D=1, device=DEV)
+    cost = torch.empty(L, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    b = D.Batch([L], [n], device=DEV)
+    out = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=DEV),
+               bottleneck=torch.empty(1, dtype=torch.int64, device=DEV),
+               imbalance=torch.empty(1, dtype=torch.float64, device=DEV),
+               status=torch.empty(1, dtype=torch.int32, device=DEV))
+
+    def step():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+        D.partition_stages(ctx, b, cost, **out)
+
+    ms, _ = timed(step)
+    want = np.array([sum(oracle.time_ns(s[m, i:i + 2])[1] for m in range(M)) for i in range(L)])
+    assert np.array_equal(cost.cpu().numpy(), want)
+    ost, ob, oB, _ = oracle.partition(want, n)
+    assert np.array_equal(out["bnd"].cpu().numpy()[:n + 1], ob)
+    return dict(layers=L, microbatches=M, segments=len(segs), step_device_ms=round(ms, 4),
+                b_new=[int(x) for x in ob], imbalance=round(float(out["imbalance"].item()), 4))
+
+
 def main():
     global flush
     torch.cuda.set_device(0)
@@ -223,7 +259,7 @@ def main():
     res = {}
     for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
                      ("config4_auxloss", lambda: config4(ctx, 4.0)), ("config4_sbase", lambda: config4(ctx, 64.0)),
-                     ("config5", lambda: config5(ctx))]:
+                     ("config5", lambda: config5(ctx)), ("bytime_cfg2", lambda: config_bytime(ctx))]:
         res[name] = fn()
         print(name, json.dumps(res[name]), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)

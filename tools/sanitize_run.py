@@ -30,7 +30,7 @@ for lay, (E, dt) in enumerate([(8, np.int64), (40, np.int32), (300, np.int64)]):
     add(idx[1:], LB.SRC_EXPERT_I64 if dt == np.int64 else LB.SRC_EXPERT_I32, 5 + lay, n_experts=E, top_k=2)
 plan = D.ProfilePlan(ctx, segs, 0, 8)
 coef = D.coef_tensor(8, A=3, B=1, C_=2, ep=0, device=dev)
-counters = torch.empty((8, 4), dtype=torch.int64, device=dev)
+counters = torch.empty((8, 5), dtype=torch.int64, device=dev)
 hist = torch.empty((8, plan.max_experts), dtype=torch.int64, device=dev)
 cost, _, st = D.profile_layers(ctx, plan, coef, counters=counters, hist=hist,
                                frozen=torch.tensor([0, 1, 0, 0, 0, 0, 0, 0], dtype=torch.uint8, device=dev))
