@@ -66,6 +66,7 @@ def lib():
             "oracle_diffuse": (C.c_int, [p, p, i32, i32, i64, p, i64, i32, p, p, p, p]),
             "oracle_diffuse_fluid": (C.c_int, [p, i32, i32, p, dbl, i32, p, p, p]),
             "oracle_moves": (i32, [i32, i32, p, p, i32, p, p, p]),
+            "oracle_global_prune": (C.c_int, [p, i64, i64, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -243,3 +244,26 @@ def moves(L, bnd_old, rank_old, bnd_new, rank_new) -> np.ndarray:
     if m < 0:
         raise ValueError("boundaries do not cover every layer")
     return out[:m].copy()
+
+
+# ------------------------------------------------------ O8 global pruning
+def global_prune(shards, k: int):
+    """Alg. 1: keep the k largest |w| over the concatenation of the shards
+    (list of float arrays, bf16 given as uint16 bit patterns via
+    bf16_to_f64).  Returns (status, [mask per shard])."""
+    w = np.concatenate([np.asarray(x, np.float64).reshape(-1) for x in shards]) if shards else np.zeros(0)
+    w = np.ascontiguousarray(w, np.float64)
+    mask = np.zeros(max(1, w.size), np.uint8)
+    st = lib().oracle_global_prune(_ptr(w), w.size, int(k), _ptr(mask))
+    out, o = [], 0
+    for x in shards:
+        n = np.asarray(x).size
+        out.append(mask[o:o + n].copy())
+        o += n
+    return int(st), out
+
+
+def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> exact float64 values."""
+    b = np.asarray(bits, np.uint16).astype(np.uint32) << 16
+    return b.view(np.float32).astype(np.float64)

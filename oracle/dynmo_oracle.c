@@ -663,3 +663,49 @@ int32_t oracle_moves(int32_t L, int32_t n_old, const int32_t *bnd_old, const int
     }
     return m;
 }
+
+/* ------------------------------------------------------------------------
+ * O8 global magnitude pruning (Algorithm 1):
+ * over the concatenation of every rank's parameters (rank order, then the
+ * rank's segments in order) keep exactly k parameters with the largest
+ * magnitude |w| (Alg. 1 lines 2-3 "k <- num_params (1 - sparsity)",
+ * "topk(abs(params), k)"; line 6 the global top-k); equal magnitudes are
+ * broken by global position ascending (SPEC: "(shard id, local index)
+ * ascending").  mask[j] = 1 keep, 0 prune.  Magnitudes are compared as
+ * doubles (f32 and bf16 convert exactly).  A NaN is never kept and makes
+ * the status INVALID; k < 0 or k > #non-NaN is INVALID (then nothing is
+ * written).  The paper's gather to rank 0 / scatter of indices is data
+ * movement; the kept SET is what this function defines.
+ * Plain O(N log N) sort of positions by (|w| desc, position asc).
+ * ---------------------------------------------------------------------- */
+static const double *g_mag;
+static int cmp_mag_desc(const void *a, const void *b) {
+    int64_t i = *(const int64_t *)a, j = *(const int64_t *)b;
+    if (g_mag[i] > g_mag[j]) return -1;
+    if (g_mag[i] < g_mag[j]) return 1;
+    return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+int oracle_global_prune(const double *w, int64_t n, int64_t k, uint8_t *mask) {
+    int st = O_OK;
+    double *mag = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int64_t *pos = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t m = 0;
+    for (int64_t j = 0; j < n; ++j) {
+        mag[j] = fabs(w[j]);
+        if (isnan(w[j])) st = O_E_INVALID;
+        else pos[m++] = j;
+    }
+    if (k < 0 || k > m) {
+        free(mag);
+        free(pos);
+        return O_E_INVALID;
+    }
+    g_mag = mag;
+    qsort(pos, (size_t)m, sizeof(int64_t), cmp_mag_desc);
+    for (int64_t j = 0; j < n; ++j) mask[j] = 0;
+    for (int64_t r = 0; r < k; ++r) mask[pos[r]] = 1;
+    free(mag);
+    free(pos);
+    return st;
+}

@@ -513,3 +513,46 @@ def test_sparsity_schedule_milestones():
     """Pin: Eq. 3 milestones 52/79/90% (reading Q17)."""
     for ex in GOLD["sparsity_schedule"]:
         assert synth.sparsity_at(ex["t"]) == pytest.approx(ex["S"], abs=1e-12), ex["cite"]
+
+
+# ------------------------------------------------------ O8 global pruning
+def test_global_prune_spec_examples():
+    """Alg. 1: SPEC S:L181-183 worked examples; k from line 2."""
+    for ex in GOLD["global_prune"]:
+        n = sum(len(x) for x in ex["shards"])
+        assert int(math.floor(n * (1 - ex["sparsity"]))) == ex["k"], ex["cite"]
+        st, masks = oracle.global_prune([np.array(x, np.float64) for x in ex["shards"]], ex["k"])
+        assert st == 0
+        assert [list(np.flatnonzero(m)) for m in masks] == ex["keep"], ex["cite"]
+
+
+def test_global_prune_vs_lexsort_and_separation():
+    """Kept set = first k of an independent ranking (np.lexsort by |w| desc,
+    position asc) on tie-heavy data; exactly k kept; every kept magnitude >=
+    every pruned one; f32 and bf16 shards mixed; NaN never kept -> INVALID."""
+    g = np.random.default_rng(8)
+    for _ in range(60):
+        shards = []
+        for _ in range(int(g.integers(1, 5))):
+            n = int(g.integers(0, 300))
+            if g.random() < 0.5:
+                shards.append((g.integers(-8, 9, n) * 0.25).astype(np.float32).astype(np.float64))  # ties, +-0
+            else:
+                bits = g.integers(0, 2 ** 16, n).astype(np.uint16)
+                bits[(bits & 0x7F80) == 0x7F80] = 0  # no inf/NaN here
+                shards.append(oracle.bf16_to_f64(bits))
+        w = np.concatenate(shards) if shards else np.zeros(0)
+        k = int(g.integers(0, w.size + 1))
+        st, masks = oracle.global_prune(shards, k)
+        m = np.concatenate(masks) if masks else np.zeros(0, np.uint8)
+        assert st == 0 and int(m.sum()) == k
+        order = np.lexsort((np.arange(w.size), -np.abs(w)))
+        want = np.zeros(w.size, np.uint8)
+        want[order[:k]] = 1
+        assert np.array_equal(m, want)
+        if 0 < k < w.size:
+            assert np.abs(w[m == 1]).min() >= np.abs(w[m == 0]).max()
+    st, masks = oracle.global_prune([np.array([1.0, np.nan, -3.0])], 1)
+    assert st == oracle.E_INVALID and list(masks[0]) == [0, 0, 1]
+    assert oracle.global_prune([np.array([1.0, 2.0])], 3)[0] == oracle.E_INVALID
+    assert list(oracle.bf16_to_f64(np.array([0x3F80, 0xBF80, 0x8000, 0x4049], np.uint16))) == [1.0, -1.0, -0.0, 3.140625]
