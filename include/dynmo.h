@@ -391,6 +391,47 @@ int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_b
                              const int32_t *h_rank_old, int32_t n_new, const int32_t *h_bnd_new,
                              const int32_t *h_rank_new, int32_t *h_moves);
 
+/* ---------------------------------------- global magnitude pruning (NEXT-2)
+ * Algorithm 1: every rank holds a portion of the model; keep
+ * exactly k parameters of largest magnitude |w| over ALL ranks (line 2:
+ * k = num_params (1 - sparsity), computed by the caller; lines 3-8: local
+ * top-k, gather, global top-k, scatter); equal magnitudes are kept in the
+ * global order (rank, then segment order, then element index; SPEC
+ * S:L175-184).  Same kept set as the paper's gather/scatter, found by an
+ * exact distributed radix select on magnitude keys: 2 (all bf16) or 3
+ * HBM-streaming histogram passes over this rank's weights with an NCCL
+ * all-reduce of 2049 counters per pass, then one mask-writing pass. */
+enum { DYNMO_W_F32 = 0, DYNMO_W_BF16 = 1 };
+
+typedef struct dynmo_prune_segment {
+    const void *d_w;   /* weights, 16-byte aligned, caller-owned           */
+    uint8_t *d_mask;   /* out: 1 keep / 0 prune per weight (n bytes)       */
+    int64_t n;         /* weights in the segment (>= 0)                    */
+    int32_t dtype;     /* DYNMO_W_F32 | DYNMO_W_BF16                       */
+    int32_t pad;
+} dynmo_prune_segment;
+
+typedef struct dynmo_pplan_s *dynmo_pplan;
+
+/* Plan of this rank's weight segments (in order; off the hot path: tile
+ * table + workspace on the device).  Pointers must stay valid while the plan
+ * is used.  INVALID: unknown dtype, negative n, a misaligned pointer. */
+dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h_segs, int32_t n_segs,
+                                     dynmo_pplan *out);
+void dynmo_prune_plan_destroy(dynmo_pplan plan);
+
+/* Collective (every rank, same k): writes every segment's mask.
+ *   k       global number of weights to keep; k < 0 is INVALID (host).
+ *   d_info  [5] int64 out, nullable: {tau key (bits of the k-th largest |w|
+ *           as f32; -1 if nothing is kept), global non-NaN count, global
+ *           count above tau, ties kept on this rank, ties on this rank}.
+ *   d_status [1] int32 out: OK; INVALID if k > global non-NaN count (all
+ *           masks 0) or a NaN weight exists (NaN is never kept).
+ * Asynchronous on `stream`, no host synchronisation; capturable in a CUDA
+ * graph (NCCL calls included). */
+dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int64_t *d_info,
+                                int32_t *d_status, dynmo_stream stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,14 @@ class Buf(C.Structure):
     _fields_ = [("d_ptr", C.c_void_p), ("bytes", C.c_int64)]
 
 
+W_F32, W_BF16 = 0, 1
+
+
+class PruneSegment(C.Structure):
+    _fields_ = [("d_w", C.c_void_p), ("d_mask", C.c_void_p), ("n", C.c_int64), ("dtype", C.c_int32),
+                ("pad", C.c_int32)]
+
+
 _lib = None
 
 
@@ -71,6 +79,9 @@ def lib():
                                        p, p, p, p, p]),
         "dynmo_migrate_layers": (i32, [p, i32, i32, p, p, i32, p, p, p, p, i32, p, p, p]),
         "dynmo_migration_plan": (i32, [i32, i32, p, p, i32, p, p, p]),
+        "dynmo_prune_plan_create": (i32, [p, p, i32, p]),
+        "dynmo_prune_plan_destroy": (None, [p]),
+        "dynmo_global_prune": (i32, [p, p, i64, p, p, p]),
         "dynmo_migrate_plan_create": (i32, [p, i32, i32, p, p, C.POINTER(p)]),
         "dynmo_migrate_plan_destroy": (None, [p]),
         "dynmo_migrate_layers_p2p": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
@@ -92,5 +103,6 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers", "dynmo_timestamp",
             "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",
             "dynmo_migrate_layers", "dynmo_migration_plan", "dynmo_migrate_plan_create",
+            "dynmo_prune_plan_create", "dynmo_prune_plan_destroy", "dynmo_global_prune",
             "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",
             "dynmo_migrate_layers_dev"]

@@ -585,6 +585,122 @@ int64_t dynmo_plan_num_tiles(dynmo_plan plan) { return plan ? plan->n_tiles : -1
 int64_t dynmo_plan_bytes(dynmo_plan plan) { return plan ? plan->bytes : -1; }
 int32_t dynmo_plan_max_experts(dynmo_plan plan) { return plan ? plan->max_E : -1; }
 
+// ------------------------------------------------ global pruning (NEXT-2)
+struct dynmo_pplan_s {
+    dynmo_ctx ctx = nullptr;
+    void *dmem = nullptr;
+    PruneArgs args{};
+    int grid = 1;
+};
+
+dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h_segs, int32_t n_segs,
+                                     dynmo_pplan *out) {
+    if (!out) return invalid("null plan out");
+    *out = nullptr;
+    if (!ctx) return invalid("null ctx");
+    if (n_segs < 0 || (n_segs > 0 && !h_segs)) return invalid("bad segment list");
+    std::vector<PruneTile> tiles;
+    bool any_f32 = false;
+    for (int32_t i = 0; i < n_segs; ++i) {
+        const dynmo_prune_segment &sg = h_segs[i];
+        if (sg.n < 0) return invalid("negative segment length");
+        if (sg.dtype != DYNMO_W_F32 && sg.dtype != DYNMO_W_BF16) return invalid("unknown weight dtype");
+        if (sg.n == 0) continue;
+        if (!sg.d_w || !sg.d_mask) return invalid("null segment pointer");
+        if ((uintptr_t)sg.d_w % 16) return invalid("weights must be 16-byte aligned");
+        any_f32 |= sg.dtype == DYNMO_W_F32;
+        const int64_t esz = sg.dtype == DYNMO_W_F32 ? 4 : 2;
+        for (int64_t o = 0; o < sg.n; o += kPruneTileElems) {
+            const int64_t len = std::min<int64_t>(kPruneTileElems, sg.n - o);
+            tiles.push_back(PruneTile{(const char *)sg.d_w + o * esz, sg.d_mask + o, (uint32_t)len, sg.dtype});
+        }
+    }
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t nt = std::max<size_t>(1, tiles.size());
+    const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 2049);
+    const size_t sz_sel = up(sizeof(PruneSel)), sz_tie = up(sizeof(long long) * std::max(1, ctx->nranks));
+    const size_t sz_tt = up(sizeof(uint32_t) * nt), sz_to = up(sizeof(unsigned long long) * nt);
+    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to;
+    DeviceGuard g(ctx->device);
+    auto *pl = new dynmo_pplan_s();
+    pl->ctx = ctx;
+    cudaError_t e = cudaMalloc(&pl->dmem, total);
+    if (e != cudaSuccess) {
+        delete pl;
+        g_err = std::string("cudaMalloc: ") + cudaGetErrorString(e);
+        return DYNMO_E_NOMEM;
+    }
+    char *b = (char *)pl->dmem;
+    PruneArgs &a = pl->args;
+    a.tiles = (const PruneTile *)b; b += sz_tiles;
+    a.hist_local = (unsigned long long *)b; b += sz_hist;
+    a.hist_global = (unsigned long long *)b; b += sz_hist;
+    a.sel = (PruneSel *)b; b += sz_sel;
+    a.tie_all = (const long long *)b; b += sz_tie;
+    a.tile_ties = (uint32_t *)b; b += sz_tt;
+    a.tile_off = (unsigned long long *)b;
+    a.n_tiles = (int64_t)tiles.size();
+    a.rank = ctx->rank;
+    a.nranks = ctx->nranks;
+    a.last_pass = any_f32 ? 2 : 1;  // bf16 keys have 16 zero low bits: 2 digits suffice
+    bool ok = cudaMemset(pl->dmem, 0, total) == cudaSuccess;
+    if (ok && !tiles.empty())
+        ok = cudaMemcpy((void *)a.tiles, tiles.data(), sizeof(PruneTile) * tiles.size(), cudaMemcpyHostToDevice) ==
+             cudaSuccess;
+    if (!ok) {
+        e = cudaGetLastError();
+        cudaFree(pl->dmem);
+        delete pl;
+        return cuda_fail(e, "prune plan upload");
+    }
+    // persistent grid: 4 blocks of 256 threads (32 KB shared) per SM
+    pl->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 4, a.n_tiles));
+    *out = pl;
+    return DYNMO_OK;
+}
+
+void dynmo_prune_plan_destroy(dynmo_pplan plan) {
+    if (!plan) return;
+    DeviceGuard g(plan->ctx->device);
+    cudaFree(plan->dmem);
+    delete plan;
+}
+
+dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int64_t *d_info,
+                                int32_t *d_status, dynmo_stream stream) {
+    if (!ctx || !plan || plan->ctx != ctx) return invalid("bad ctx/plan");
+    if (k < 0) return invalid("k < 0");
+    const cudaStream_t s = (cudaStream_t)stream;
+    DeviceGuard g(ctx->device);
+    const PruneArgs &a = plan->args;
+    const bool multi = ctx->nranks > 1;
+    CUDA_TRY(launch_prune_begin(a.sel, (long long)k, s), "k_prune_begin");
+    for (int pass = 0; pass <= a.last_pass; ++pass) {
+        CUDA_TRY(launch_prune(a, pass, plan->grid, s), "k_prune_hist");
+        if (multi) {
+            const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, 2049, ncclUint64, ncclSum, ctx->comm, s);
+            if (r != ncclSuccess) {
+                g_err = std::string("ncclAllReduce (prune): ") + ncclGetErrorString(r);
+                return DYNMO_E_NCCL;
+            }
+        }
+        CUDA_TRY(launch_prune(a, 10 + pass, 1, s), "k_prune_select");
+    }
+    if (multi) {
+        const ncclResult_t r = ncclAllGather(&a.sel->tie_local, (void *)a.tie_all, 1, ncclInt64, ctx->comm, s);
+        if (r != ncclSuccess) {
+            g_err = std::string("ncclAllGather (prune): ") + ncclGetErrorString(r);
+            return DYNMO_E_NCCL;
+        }
+    }
+    CUDA_TRY(launch_prune(a, 20, 1, s), "k_prune_ties");
+    CUDA_TRY(launch_prune(a, 21, plan->grid, s), "k_prune_tiecount");
+    CUDA_TRY(launch_prune(a, 22, 1, s), "k_prune_tiescan");
+    CUDA_TRY(launch_prune(a, 23, plan->grid, s), "k_prune_mask");
+    CUDA_TRY(launch_prune_info(a, (long long *)d_info, d_status, s), "k_prune_info");
+    return DYNMO_OK;
+}
+
 // ----------------------------------------------------------- call 1 profile
 dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t *d_frozen,
                                   const dynmo_cost_coef *d_coef, const int64_t *d_mem_local,

@@ -154,6 +154,37 @@ inline int profile_warp_words(bool any_exit, int max_expert_words) {
     const int m = w > max_expert_words ? w : max_expert_words;
     return m > 0 ? m : 1;
 }
+// ------------------------------------------------- global pruning (Alg. 1)
+struct PruneTile {
+    const void *w;    // 16-byte aligned first element
+    uint8_t *mask;    // its mask bytes
+    uint32_t n;       // elements (<= kPruneTileElems)
+    int32_t dtype;    // DYNMO_W_F32 | DYNMO_W_BF16
+};
+static_assert(sizeof(PruneTile) == 24, "prune tile layout");
+constexpr uint32_t kPruneTileElems = 8192;
+
+struct PruneSel {  // device-side selection state of one call
+    long long k, k_rem, above, tie_local, keep_ties, n_global;
+    uint32_t prefix, tau;
+    int32_t partial, status, done, pad;
+};
+
+struct PruneArgs {
+    const PruneTile *tiles;
+    int64_t n_tiles;
+    unsigned long long *hist_local;   // [2049] (bin 2048: NaN count)
+    unsigned long long *hist_global;  // [2049] all-reduced (nranks > 1)
+    PruneSel *sel;
+    const long long *tie_all;         // [nranks] all-gathered tie counts
+    uint32_t *tile_ties;              // [n_tiles]
+    unsigned long long *tile_off;     // [n_tiles]
+    int32_t rank, nranks, last_pass;
+};
+cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s);
+cudaError_t launch_prune_begin(PruneSel *sel, long long k, cudaStream_t s);
+cudaError_t launch_prune_info(const PruneArgs &a, long long *d_info, int32_t *d_status, cudaStream_t s);
+
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,

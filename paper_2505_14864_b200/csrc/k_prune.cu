@@ -1,0 +1,423 @@
+// Global magnitude pruning, Algorithm 1 -- NEXT-2 of SURVEY
+// 8(f).  Alg. 1 keeps the k largest |w| over every rank's parameters (local
+// top-k, gather to rank 0, global top-k, scatter of indices).  Here the SAME
+// kept set is found without moving any weights: an exact distributed radix
+// select on magnitude keys.
+//   key(w) = bits(|w|) for f32; bits(|bf16|) << 16 for bf16 (the f32 key of
+//   the same value), so segments of both types share one ordered key space
+//   (monotone in |w| for non-NaN values; +0 and -0 both key 0).
+//   pass 0: histogram of key >> 20      (2048 bins)  -> all-reduce -> bin
+//   pass 1: histogram of key >> 10 & 1023 among keys with that prefix
+//   pass 2: histogram of key & 1023 among keys with the 21-bit prefix
+//           (skipped when every segment is bf16: its low 16 key bits are 0)
+// Each pass streams the rank's weights (HBM-bound); only the histograms cross
+// GPUs (NCCL all-reduce, 16 KB).  The threshold tau is the k-th largest key;
+// keys > tau are kept, and of the keys == tau the first `need` in the global
+// order (rank, then segment order, then index -- SPEC S:L184) are kept:
+// per-rank tie counts are all-gathered, and only the rank whose share of the
+// ties is partial ranks its ties (per-tile counts, an exclusive scan, and an
+// in-tile block scan in element order).
+#include "dynmo_internal.h"
+
+namespace dynmo {
+namespace {
+
+constexpr int kPruneThreads = 256;
+constexpr int kBins0 = 2048;  // pass 0 digit: key bits 30..20 (11 bits)
+constexpr int kBins1 = 1024;  // pass 1/2 digits: 10 bits
+constexpr uint32_t kNanKey = 0x7F800000u;  // key > this: NaN
+
+__device__ __forceinline__ uint4 ld_nc(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t key_f32(uint32_t b) { return b & 0x7FFFFFFFu; }
+__device__ __forceinline__ uint32_t key_bf16(uint32_t h) { return (h & 0x7FFFu) << 16; }
+
+// Applies f(key) to every element of tile t in element order per thread
+// chunk: 16-byte vectors (8 bf16 / 4 f32) then a scalar tail.
+template <typename F>
+__device__ __forceinline__ void for_keys(const PruneTile &t, F &&f) {
+    if (t.dtype == DYNMO_W_BF16) {
+        const uint4 *v = (const uint4 *)t.w;
+        const uint32_t nv = t.n >> 3;
+        for (uint32_t i = threadIdx.x; i < nv; i += kPruneThreads) {
+            const uint4 x = ld_nc(v + i);
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                f(key_bf16(w[q] & 0xFFFFu));
+                f(key_bf16(w[q] >> 16));
+            }
+        }
+        const uint16_t *s = (const uint16_t *)t.w;
+        for (uint32_t i = (nv << 3) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_bf16(s[i]));
+    } else {
+        const uint4 *v = (const uint4 *)t.w;
+        const uint32_t nv = t.n >> 2;
+        for (uint32_t i = threadIdx.x; i < nv; i += kPruneThreads) {
+            const uint4 x = ld_nc(v + i);
+            f(key_f32(x.x));
+            f(key_f32(x.y));
+            f(key_f32(x.z));
+            f(key_f32(x.w));
+        }
+        const uint32_t *s = (const uint32_t *)t.w;
+        for (uint32_t i = (nv << 2) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_f32(s[i]));
+    }
+}
+
+// Shared sub-histograms, one per warp pair (less same-address contention;
+// 4 x 2048 x 4 B = 32 KB fits the static limit), flushed as ONE global atomic
+// per nonzero bin per block.  hist[NB] counts NaN keys (pass 0).
+template <int PASS>
+__global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NB = PASS == 0 ? kBins0 : kBins1;
+    constexpr int W = kPruneThreads / 64;
+    __shared__ uint32_t sh[W][NB];
+    __shared__ uint32_t s_nan;
+    for (int i = threadIdx.x; i < W * NB; i += kPruneThreads) (&sh[0][0])[i] = 0u;
+    if (threadIdx.x == 0) s_nan = 0u;
+    __syncthreads();
+    const PruneSel *sel = a.sel;
+    if (sel->done) return;  // k = 0, invalid k, or tau already found
+    const uint32_t prefix = sel->prefix;
+    uint32_t *my = sh[threadIdx.x >> 6];
+    uint32_t nan = 0;
+    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+        const PruneTile t = a.tiles[ti];
+        for_keys(t, [&](uint32_t k) {
+            if constexpr (PASS == 0) {
+                if (k > kNanKey) ++nan;
+                else atomicAdd(&my[k >> 20], 1u);
+            } else if constexpr (PASS == 1) {
+                if (k <= kNanKey && (k >> 20) == prefix) atomicAdd(&my[(k >> 10) & 1023u], 1u);
+            } else {
+                if (k <= kNanKey && (k >> 10) == prefix) atomicAdd(&my[k & 1023u], 1u);
+            }
+        });
+    }
+    if constexpr (PASS == 0)
+        if (nan) atomicAdd(&s_nan, nan);
+    __syncthreads();
+    for (int b = threadIdx.x; b < NB; b += kPruneThreads) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) c += sh[w][b];
+        if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
+    }
+    if (PASS == 0 && threadIdx.x == 0 && s_nan) atomicAdd(&a.hist_local[kBins0], (unsigned long long)s_nan);
+}
+
+// One block: locate the bin of the k_rem-th largest key in the (global)
+// histogram by a suffix scan, narrow the prefix, and clear both histograms.
+template <int PASS>
+__global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NB = PASS == 0 ? kBins0 : kBins1;
+    constexpr int PER = NB / 1024;  // bins per thread (2 or 1)
+    __shared__ unsigned long long s_part[1024];
+    __shared__ int s_bin;
+    PruneSel *sel = a.sel;
+    const unsigned long long *h = a.nranks > 1 ? a.hist_global : a.hist_local;
+    const int tid = threadIdx.x;
+    const bool done0 = sel->done != 0;
+    if (PASS == 0 && tid == 0) {
+        // NaN count and the global number of non-NaN keys; validate k
+        const unsigned long long nan = h[kBins0];
+        if (nan) sel->status = DYNMO_E_INVALID;
+    }
+    // thread tid owns bins [tid*PER, tid*PER+PER): its partial sum, then a
+    // suffix scan over threads (bins from the top down)
+    unsigned long long mine = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) mine += h[tid * PER + j];
+    s_part[tid] = mine;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix sums: s_part[t] = sum_{u >= t}
+        const unsigned long long add = tid + o < 1024 ? s_part[tid + o] : 0ull;
+        __syncthreads();
+        s_part[tid] += add;
+        __syncthreads();
+    }
+    if (tid == 0) s_bin = -1;
+    __syncthreads();
+    const unsigned long long total = s_part[0];
+    if (PASS == 0 && tid == 0) {
+        sel->n_global = (long long)total;
+        if (!done0 && (sel->k > (long long)total)) {
+            sel->status = DYNMO_E_INVALID;
+            sel->done = 1;
+        }
+    }
+    __syncthreads();
+    const long long krem = sel->k_rem;
+    if (!done0 && !sel->done && krem > 0) {
+        // the bin b with suffix(b) >= krem > suffix(b + 1)
+        const unsigned long long above_thread = tid + 1 < 1024 ? s_part[tid + 1] : 0ull;
+        if (above_thread < (unsigned long long)krem && s_part[tid] >= (unsigned long long)krem) {
+            unsigned long long acc = above_thread;
+            int b = tid * PER + PER - 1;
+            for (int j = PER - 1; j >= 0; --j) {
+                const unsigned long long c = h[tid * PER + j];
+                if (acc + c >= (unsigned long long)krem) {
+                    b = tid * PER + j;
+                    break;
+                }
+                acc += c;
+            }
+            s_bin = b;
+            sel->k_rem = krem - (long long)acc;
+            sel->above += (long long)acc;
+            sel->prefix = PASS == 0 ? (uint32_t)b : ((sel->prefix << 10) | (uint32_t)b);
+            // this rank's keys in the chosen bin (the ties, after the last pass)
+            sel->tie_local = (long long)a.hist_local[b];
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && !done0 && !sel->done && krem == 0) sel->done = 2;  // k = 0: nothing kept
+    for (int b = tid; b < NB + (PASS == 0 ? 1 : 0); b += 1024) {
+        a.hist_local[b] = 0ull;
+        if (a.nranks > 1) a.hist_global[b] = 0ull;
+    }
+}
+
+// After the last pass: tau, and this rank's share of the ties (global order
+// = rank order): tie_all[] holds every rank's tie count (all-gathered).
+__global__ void k_prune_ties(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    PruneSel *sel = a.sel;
+    if (threadIdx.x != 0) return;
+    if (sel->done) {  // k = 0 or invalid: nothing kept
+        sel->keep_ties = 0;
+        sel->partial = 0;
+        sel->tau = 0xFFFFFFFFu;
+        return;
+    }
+    sel->tau = a.last_pass == 1 ? (sel->prefix << 10) : sel->prefix;
+    long long before = 0;
+    for (int r = 0; r < a.rank; ++r) before += a.nranks > 1 ? a.tie_all[r] : 0;
+    const long long need = sel->k_rem;  // ties to keep globally (>= 1)
+    long long mine = need - before;
+    mine = mine < 0 ? 0 : (mine > sel->tie_local ? sel->tie_local : mine);
+    sel->keep_ties = mine;
+    sel->partial = mine > 0 && mine < sel->tie_local;
+}
+
+// Ties per tile (only for a partial share): keys == tau.
+__global__ void __launch_bounds__(kPruneThreads) k_prune_tiecount(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const PruneSel *sel = a.sel;
+    if (!sel->partial) return;
+    const uint32_t tau = sel->tau;
+    __shared__ uint32_t s_c;
+    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+        if (threadIdx.x == 0) s_c = 0u;
+        __syncthreads();
+        uint32_t c = 0;
+        for_keys(a.tiles[ti], [&](uint32_t k) { c += k == tau; });
+        c = __reduce_add_sync(0xFFFFFFFFu, c);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
+        __syncthreads();
+        if (threadIdx.x == 0) a.tile_ties[ti] = s_c;
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of the per-tile tie counts (one block; only if partial).
+__global__ void __launch_bounds__(1024) k_prune_tiescan(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    if (!a.sel->partial) return;
+    __shared__ unsigned long long s[1024];
+    __shared__ unsigned long long s_carry;
+    if (threadIdx.x == 0) s_carry = 0ull;
+    __syncthreads();
+    for (int64_t base = 0; base < a.n_tiles; base += 1024) {
+        const int64_t i = base + threadIdx.x;
+        const unsigned long long v = i < a.n_tiles ? a.tile_ties[i] : 0u;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            const unsigned long long add = threadIdx.x >= o ? s[threadIdx.x - o] : 0ull;
+            __syncthreads();
+            s[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (i < a.n_tiles) a.tile_off[i] = s_carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry += s[1023];
+        __syncthreads();
+    }
+}
+
+// Masks: keep key > tau; keys == tau kept when all of this rank's ties are
+// (non-partial share) or, for a partial share, when their rank in element
+// order (tile offset + in-tile block scan over thread-contiguous chunks) is
+// below keep_ties.  16 elements per thread per step, 16-byte mask stores.
+__global__ void __launch_bounds__(kPruneThreads) k_prune_mask(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    const PruneSel *sel = a.sel;
+    const uint32_t tau = sel->tau;
+    const bool all_ties = sel->keep_ties > 0 && !sel->partial;
+    const bool partial = sel->partial != 0;
+    const long long keep_ties = sel->keep_ties;
+    __shared__ uint32_t s_warp[kPruneThreads / 32];
+    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+        const PruneTile t = a.tiles[ti];
+        unsigned long long run = partial ? a.tile_off[ti] : 0ull;  // ties before this chunk
+        const uint32_t nchunk = (t.n + 16 * kPruneThreads - 1) / (16 * kPruneThreads);
+        for (uint32_t ch = 0; ch < nchunk; ++ch) {
+            const uint32_t e0 = ch * 16 * kPruneThreads + threadIdx.x * 16;  // 16 elements per thread
+            uint32_t keys[16];
+            const uint32_t ne = e0 < t.n ? (t.n - e0 < 16 ? t.n - e0 : 16) : 0;
+            if (t.dtype == DYNMO_W_BF16) {
+                const uint16_t *s = (const uint16_t *)t.w + e0;
+                if (ne == 16) {
+                    const uint4 x0 = ld_nc((const uint4 *)s), x1 = ld_nc((const uint4 *)s + 1);
+                    const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        keys[2 * q] = key_bf16(w[q] & 0xFFFFu);
+                        keys[2 * q + 1] = key_bf16(w[q] >> 16);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) keys[q] = q < (int)ne ? key_bf16(s[q]) : 0xFFFFFFFFu;
+                }
+            } else {
+                const uint32_t *s = (const uint32_t *)t.w + e0;
+                if (ne == 16) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 x = ld_nc((const uint4 *)s + q);
+                        keys[4 * q] = key_f32(x.x);
+                        keys[4 * q + 1] = key_f32(x.y);
+                        keys[4 * q + 2] = key_f32(x.z);
+                        keys[4 * q + 3] = key_f32(x.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) keys[q] = q < (int)ne ? key_f32(s[q]) : 0xFFFFFFFFu;
+                }
+            }
+            // rank of this thread's first tie among the chunk's ties (block
+            // scan, every thread takes part: the barriers are uniform)
+            uint32_t before = 0;
+            const unsigned long long base = run;
+            if (partial) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) c += keys[q] == tau;
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if ((threadIdx.x & 31) >= o) incl += y;
+                }
+                if ((threadIdx.x & 31) == 31) s_warp[threadIdx.x >> 5] = incl;
+                __syncthreads();
+                uint32_t wbefore = 0, tot = 0;
+#pragma unroll
+                for (int w = 0; w < kPruneThreads / 32; ++w) {
+                    wbefore += w < (int)(threadIdx.x >> 5) ? s_warp[w] : 0u;
+                    tot += s_warp[w];
+                }
+                __syncthreads();  // s_warp is rewritten by the next chunk
+                before = wbefore + incl - c;
+                run += tot;  // uniform across the block
+            }
+            if (ne > 0) {
+                uint32_t m[4] = {0u, 0u, 0u, 0u};
+                uint32_t seen = 0;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const uint32_t k = keys[q];
+                    bool keep = k > tau && k <= kNanKey;
+                    if (k == tau && q < (int)ne) {
+                        keep = partial ? (base + before + seen < (unsigned long long)keep_ties) : all_ties;
+                        ++seen;
+                    }
+                    m[q >> 2] |= (keep ? 1u : 0u) << (8 * (q & 3));
+                }
+                uint8_t *mk = t.mask + e0;
+                if (ne == 16 && (((uintptr_t)mk) & 15u) == 0) {
+                    *(uint4 *)mk = make_uint4(m[0], m[1], m[2], m[3]);
+                } else {
+                    for (uint32_t q = 0; q < ne; ++q) mk[q] = (uint8_t)((m[q >> 2] >> (8 * (q & 3))) & 1u);
+                }
+            }
+        }
+    }
+}
+
+// This rank's kept count and the info vector (one thread).
+__global__ void k_prune_info(PruneArgs a, long long *d_info, int32_t *d_status) {
+    pdl_wait();
+    pdl_trigger();
+    PruneSel *sel = a.sel;
+    if (threadIdx.x != 0) return;
+    const bool none = sel->done != 0;
+    if (d_info) {
+        d_info[0] = none ? -1 : (long long)sel->tau;
+        d_info[1] = sel->n_global;
+        d_info[2] = none ? 0 : sel->above;
+        d_info[3] = none ? 0 : sel->keep_ties;
+        d_info[4] = none ? 0 : sel->tie_local;
+    }
+    if (d_status) *d_status = sel->status;
+}
+
+}  // namespace
+
+// Reset the selection state for a call (k is the global keep count).
+__global__ void k_prune_begin(PruneSel *sel, long long k) {
+    pdl_wait();
+    pdl_trigger();
+    sel->k = k;
+    sel->k_rem = k;
+    sel->above = 0;
+    sel->prefix = 0u;
+    sel->tau = 0xFFFFFFFFu;
+    sel->tie_local = 0;
+    sel->keep_ties = 0;
+    sel->partial = 0;
+    sel->status = DYNMO_OK;
+    sel->n_global = 0;
+    sel->done = 0;
+}
+
+cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s) {
+    switch (pass_kind) {
+        case 0: return launch_pdl(k_prune_hist<0>, grid, kPruneThreads, 0, s, a);
+        case 1: return launch_pdl(k_prune_hist<1>, grid, kPruneThreads, 0, s, a);
+        case 2: return launch_pdl(k_prune_hist<2>, grid, kPruneThreads, 0, s, a);
+        case 10: return launch_pdl(k_prune_select<0>, 1, 1024, 0, s, a);
+        case 11: return launch_pdl(k_prune_select<1>, 1, 1024, 0, s, a);
+        case 12: return launch_pdl(k_prune_select<2>, 1, 1024, 0, s, a);
+        case 20: return launch_pdl(k_prune_ties, 1, 32, 0, s, a);
+        case 21: return launch_pdl(k_prune_tiecount, grid, kPruneThreads, 0, s, a);
+        case 22: return launch_pdl(k_prune_tiescan, 1, 1024, 0, s, a);
+        case 23: return launch_pdl(k_prune_mask, grid, kPruneThreads, 0, s, a);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_prune_begin(PruneSel *sel, long long k, cudaStream_t s) {
+    return launch_pdl(k_prune_begin, 1, 1, 0, s, sel, k);
+}
+
+cudaError_t launch_prune_info(const PruneArgs &a, long long *d_info, int32_t *d_status, cudaStream_t s) {
+    return launch_pdl(k_prune_info, 1, 32, 0, s, a, d_info, d_status);
+}
+
+}  // namespace dynmo

@@ -418,3 +418,49 @@ class PeerMigrator:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------- global pruning (NEXT-2)
+class PrunePlan:
+    """dynmo_prune_plan_create over this rank's (weights, mask) pairs, in the
+    global order of Alg. 1 (rank order, then this list's order)."""
+
+    def __init__(self, ctx: Context, pairs: Sequence[tuple]):
+        arr = (_L.PruneSegment * max(1, len(pairs)))()
+        self._keep = []
+        for i, (w, m) in enumerate(pairs):
+            if not (w.is_cuda and m.is_cuda and w.is_contiguous() and m.is_contiguous()):
+                raise ValueError("weights and masks must be contiguous device tensors")
+            if w.dtype not in (torch.float32, torch.bfloat16) or m.dtype != torch.uint8 or m.numel() != w.numel():
+                raise ValueError("weights f32/bf16, masks uint8 of the same length")
+            dt = _L.W_F32 if w.dtype == torch.float32 else _L.W_BF16
+            arr[i] = _L.PruneSegment(w.data_ptr(), m.data_ptr(), w.numel(), dt, 0)
+            self._keep += [w, m]
+        h = C.c_void_p()
+        _check(lib().dynmo_prune_plan_create(ctx.handle, arr, len(pairs), C.byref(h)), "dynmo_prune_plan_create")
+        self.handle = h
+        self.ctx = ctx
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().dynmo_prune_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def global_prune(ctx: Context, plan: PrunePlan, k: int, info=None, status=None, stream=None):
+    """Alg. 1 (collective): masks of the k globally largest |w|.  Returns
+    (info[5] int64, status[1] int32) device tensors."""
+    dev = torch.device("cuda", ctx.device)
+    if info is None:
+        info = torch.empty(5, dtype=torch.int64, device=dev)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+    _check(lib().dynmo_global_prune(ctx.handle, plan.handle, int(k), _ptr(info), _ptr(status), _stream(stream)),
+           "dynmo_global_prune")
+    return info, status

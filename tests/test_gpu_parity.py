@@ -694,3 +694,106 @@ def test_timestamp_kernel(D, ctx):
         torch.cuda.synchronize()
         seen.append(int(one.item()))
     assert seen[0] > int(s[2]) and seen[0] < seen[1] < seen[2]
+
+
+# --------------------------------------- NEXT-2: Alg. 1 global pruning
+def _prune_shards(g, sizes, quant):
+    """Mixed f32 / bf16 shards; `quant` > 0 quantises magnitudes (many ties)."""
+    shards, vals = [], []
+    for j, n in enumerate(sizes):
+        x = g.normal(0.0, 1.0, n)
+        if quant:
+            x = np.round(x * quant) / quant
+        if j % 2 == 0:
+            w = x.astype(np.float32)
+            shards.append(torch.from_numpy(w).to(DEV))
+            vals.append(w.astype(np.float64))
+        else:
+            t = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+            bits = t.view(torch.int16).numpy().view(np.uint16)
+            shards.append(t.to(DEV))
+            vals.append(oracle.bf16_to_f64(bits))
+    return shards, vals
+
+
+@pytest.mark.parametrize("quant", [0, 4])
+def test_global_prune_parity(D, ctx, quant):
+    """Alg. 1: masks == the oracle's for k in {0, 1, N/10,
+    N/2, N-1, N} and random k, mixed f32/bf16, ragged segments spanning
+    several 8192-element tiles, heavy ties (quant=4) so that a partial tie
+    share falls inside a tile."""
+    g = np.random.default_rng(100 + quant)
+    sizes = [20001, 7, 8192, 30000, 0, 16385]
+    shards, vals = _prune_shards(g, sizes, quant)
+    masks = [torch.zeros(max(1, s.numel()), dtype=torch.uint8, device=DEV)[:s.numel()] for s in shards]
+    plan = D.PrunePlan(ctx, list(zip(shards, masks)))
+    N = sum(sizes)
+    for k in [0, 1, N // 10, N // 2, N - 1, N] + [int(x) for x in g.integers(0, N + 1, 4)]:
+        info, st = D.global_prune(ctx, plan, k)
+        torch.cuda.synchronize()
+        ost, omask = oracle.global_prune(vals, k)
+        assert int(st.item()) == ost == 0, (k, int(st.item()))
+        for m, om in zip(masks, omask):
+            assert np.array_equal(m.cpu().numpy(), om), (k, quant)
+        inf = info.cpu().numpy()
+        assert inf[1] == N and inf[2] + inf[3] == k
+    plan.close()
+
+
+def test_global_prune_errors_and_nan(D, ctx):
+    """k > N: INVALID, all masks 0; a NaN is never kept and sets INVALID
+    (the selection runs over the other weights, like the oracle)."""
+    w = torch.tensor([1.0, float("nan"), -3.0, 0.5], device=DEV)
+    m = torch.full((4,), 7, dtype=torch.uint8, device=DEV)
+    plan = D.PrunePlan(ctx, [(w, m)])
+    info, st = D.global_prune(ctx, plan, 2)
+    torch.cuda.synchronize()
+    ost, om = oracle.global_prune([w.cpu().numpy().astype(np.float64)], 2)
+    assert int(st.item()) == ost == oracle.E_INVALID and np.array_equal(m.cpu().numpy(), om[0])
+    info, st = D.global_prune(ctx, plan, 4)  # 3 non-NaN weights
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_INVALID and int(m.sum().item()) == 0
+    with pytest.raises(D.DynmoError):
+        D.global_prune(ctx, plan, -1)
+    plan.close()
+
+
+def test_global_prune_config2_full_size(D, ctx):
+    """Config 2 at full size (48 layers x 12,582,912 bf16 weights = 604 M,
+    sigma_l per layer as in synth.cfg2; drawn on the GPU, seeded), S = 0.9:
+    properties the oracle fixes at any size -- exactly k kept, every kept
+    |w| >= every pruned |w|, and the kept ties (|w| = tau) are a prefix of the
+    ties in global order (layer, then index)."""
+    shape = synth.GPTShape()
+    gen = torch.Generator(device=DEV).manual_seed(2505)
+    sig = torch.from_numpy(np.exp(np.random.default_rng(3).normal(0, 0.35, shape.L))).float()
+    ws = [(torch.randn(shape.params_per_layer, generator=gen, device=DEV) * float(sig[l])).to(torch.bfloat16)
+          for l in range(shape.L)]
+    ms = [torch.empty(shape.params_per_layer, dtype=torch.uint8, device=DEV) for _ in range(shape.L)]
+    plan = D.PrunePlan(ctx, list(zip(ws, ms)))
+    N = shape.L * shape.params_per_layer
+    k = int(N * (1 - 0.9))
+    info, st = D.global_prune(ctx, plan, k)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    inf = info.cpu().numpy()
+    tau = int(inf[0])
+    kept = sum(int(m.sum(dtype=torch.int64).item()) for m in ms)
+    assert kept == k and inf[2] + inf[3] == k
+    kmin = min(float(w.float().abs()[m.bool()].min().item()) for w, m in zip(ws, ms) if int(m.sum().item()) > 0)
+    pmax = max(float(w.float().abs()[~m.bool()].max().item()) for w, m in zip(ws, ms) if int((m == 0).sum().item()) > 0)
+    assert kmin >= pmax
+    tau_val = float(np.array([tau], np.uint32).view(np.float32)[0])
+    assert kmin == tau_val
+    seen_pruned_tie = False
+    for w, m in zip(ws, ms):
+        tie = w.float().abs() == tau_val
+        kt = (m.bool() & tie).nonzero().flatten()
+        pt = (~m.bool() & tie).nonzero().flatten()
+        if seen_pruned_tie:
+            assert kt.numel() == 0
+        if pt.numel():
+            if kt.numel():
+                assert int(kt.max().item()) < int(pt.min().item())
+            seen_pruned_tie = True
+    plan.close()
