@@ -66,6 +66,9 @@ dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]);
 dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
                               const uint8_t *h_nccl_id /* 128 B, or NULL if nranks==1 */,
                               dynmo_ctx *out);
+/* Collective when nranks > 1.  CUDA graphs that captured collective calls of
+ * this ctx (NCCL exchange, dynmo_global_prune) must be destroyed first: the
+ * communicator cannot be torn down while a graph still holds its work. */
 void dynmo_ctx_destroy(dynmo_ctx ctx);
 int32_t dynmo_ctx_nranks(dynmo_ctx ctx);
 int32_t dynmo_ctx_rank(dynmo_ctx ctx);

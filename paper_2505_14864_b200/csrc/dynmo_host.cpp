@@ -590,7 +590,7 @@ struct dynmo_pplan_s {
     dynmo_ctx ctx = nullptr;
     void *dmem = nullptr;
     PruneArgs args{};
-    int grid = 1;
+    int grid[24] = {};  // per launch kind: persistent grid (SMs x resident blocks), capped by the tiles
 };
 
 dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h_segs, int32_t n_segs,
@@ -619,7 +619,8 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     const size_t nt = std::max<size_t>(1, tiles.size());
     const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 2049);
     const size_t sz_sel = up(sizeof(PruneSel)), sz_tie = up(sizeof(long long) * std::max(1, ctx->nranks));
-    const size_t sz_tt = up(sizeof(uint32_t) * nt), sz_to = up(sizeof(unsigned long long) * nt);
+    // tie counts / offsets per (tile, warp range of the mask pass)
+    const size_t sz_tt = up(sizeof(uint32_t) * nt * 8), sz_to = up(sizeof(unsigned long long) * nt * 8);
     const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to;
     DeviceGuard g(ctx->device);
     auto *pl = new dynmo_pplan_s();
@@ -653,8 +654,10 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
         delete pl;
         return cuda_fail(e, "prune plan upload");
     }
-    // persistent grid: 4 blocks of 256 threads (32 KB shared) per SM
-    pl->grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)ctx->num_sms * 4, a.n_tiles));
+    // persistent grids: every SM filled to its occupancy for each streaming kernel
+    for (int kind : {0, 1, 2, 21, 23})
+        pl->grid[kind] = (int)std::max<int64_t>(
+            1, std::min<int64_t>((int64_t)ctx->num_sms * prune_blocks_per_sm(kind), a.n_tiles));
     *out = pl;
     return DYNMO_OK;
 }
@@ -676,7 +679,7 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
     const bool multi = ctx->nranks > 1;
     CUDA_TRY(launch_prune_begin(a.sel, (long long)k, s), "k_prune_begin");
     for (int pass = 0; pass <= a.last_pass; ++pass) {
-        CUDA_TRY(launch_prune(a, pass, plan->grid, s), "k_prune_hist");
+        CUDA_TRY(launch_prune(a, pass, plan->grid[pass], s), "k_prune_hist");
         if (multi) {
             const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, 2049, ncclUint64, ncclSum, ctx->comm, s);
             if (r != ncclSuccess) {
@@ -694,9 +697,9 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
         }
     }
     CUDA_TRY(launch_prune(a, 20, 1, s), "k_prune_ties");
-    CUDA_TRY(launch_prune(a, 21, plan->grid, s), "k_prune_tiecount");
+    CUDA_TRY(launch_prune(a, 21, plan->grid[21], s), "k_prune_tiecount");
     CUDA_TRY(launch_prune(a, 22, 1, s), "k_prune_tiescan");
-    CUDA_TRY(launch_prune(a, 23, plan->grid, s), "k_prune_mask");
+    CUDA_TRY(launch_prune(a, 23, plan->grid[23], s), "k_prune_mask");
     CUDA_TRY(launch_prune_info(a, (long long *)d_info, d_status, s), "k_prune_info");
     return DYNMO_OK;
 }

@@ -162,7 +162,7 @@ struct PruneTile {
     int32_t dtype;    // DYNMO_W_F32 | DYNMO_W_BF16
 };
 static_assert(sizeof(PruneTile) == 24, "prune tile layout");
-constexpr uint32_t kPruneTileElems = 8192;
+constexpr uint32_t kPruneTileElems = 32768;
 
 struct PruneSel {  // device-side selection state of one call
     long long k, k_rem, above, tie_local, keep_ties, n_global;
@@ -182,6 +182,7 @@ struct PruneArgs {
     int32_t rank, nranks, last_pass;
 };
 cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s);
+int prune_blocks_per_sm(int kind);
 cudaError_t launch_prune_begin(PruneSel *sel, long long k, cudaStream_t s);
 cudaError_t launch_prune_info(const PruneArgs &a, long long *d_info, int32_t *d_status, cudaStream_t s);
 

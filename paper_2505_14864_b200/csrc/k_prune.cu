@@ -26,6 +26,8 @@ constexpr int kPruneThreads = 256;
 constexpr int kBins0 = 2048;  // pass 0 digit: key bits 30..20 (11 bits)
 constexpr int kBins1 = 1024;  // pass 1/2 digits: 10 bits
 constexpr uint32_t kNanKey = 0x7F800000u;  // key > this: NaN
+constexpr int kPruneWarps = kPruneThreads / 32;  // tie-offset entries per tile
+constexpr int kU = 8;  // 16-byte loads in flight per thread in the streaming passes
 
 __device__ __forceinline__ uint4 ld_nc(const uint4 *p) {
     uint4 v;
@@ -37,34 +39,40 @@ __device__ __forceinline__ uint4 ld_nc(const uint4 *p) {
 __device__ __forceinline__ uint32_t key_f32(uint32_t b) { return b & 0x7FFFFFFFu; }
 __device__ __forceinline__ uint32_t key_bf16(uint32_t h) { return (h & 0x7FFFu) << 16; }
 
-// Applies f(key) to every element of tile t in element order per thread
-// chunk: 16-byte vectors (8 bf16 / 4 f32) then a scalar tail.
+// Applies f(key) to every element of tile t (any order): 16-byte vectors
+// (8 bf16 / 4 f32 keys), kU loads in flight per thread, then a scalar tail.
 template <typename F>
 __device__ __forceinline__ void for_keys(const PruneTile &t, F &&f) {
-    if (t.dtype == DYNMO_W_BF16) {
-        const uint4 *v = (const uint4 *)t.w;
-        const uint32_t nv = t.n >> 3;
-        for (uint32_t i = threadIdx.x; i < nv; i += kPruneThreads) {
-            const uint4 x = ld_nc(v + i);
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+    const uint4 *v = (const uint4 *)t.w;
+    const bool bf = t.dtype == DYNMO_W_BF16;
+    const uint32_t nv = bf ? t.n >> 3 : t.n >> 2;
+    for (uint32_t b = threadIdx.x; b < nv; b += kU * kPruneThreads) {
+        uint4 x[kU];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                f(key_bf16(w[q] & 0xFFFFu));
-                f(key_bf16(w[q] >> 16));
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t i = b + u * kPruneThreads;
+            x[u] = i < nv ? ld_nc(v + i) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if (b + u * kPruneThreads >= nv) break;
+            const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+            if (bf) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    f(key_bf16(w[q] & 0xFFFFu));
+                    f(key_bf16(w[q] >> 16));
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) f(key_f32(w[q]));
             }
         }
+    }
+    if (bf) {
         const uint16_t *s = (const uint16_t *)t.w;
         for (uint32_t i = (nv << 3) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_bf16(s[i]));
     } else {
-        const uint4 *v = (const uint4 *)t.w;
-        const uint32_t nv = t.n >> 2;
-        for (uint32_t i = threadIdx.x; i < nv; i += kPruneThreads) {
-            const uint4 x = ld_nc(v + i);
-            f(key_f32(x.x));
-            f(key_f32(x.y));
-            f(key_f32(x.z));
-            f(key_f32(x.w));
-        }
         const uint32_t *s = (const uint32_t *)t.w;
         for (uint32_t i = (nv << 2) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_f32(s[i]));
     }
@@ -89,8 +97,11 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
     const uint32_t prefix = sel->prefix;
     uint32_t *my = sh[threadIdx.x >> 6];
     uint32_t nan = 0;
+    PruneTile nxt;
+    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
     for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
-        const PruneTile t = a.tiles[ti];
+        const PruneTile t = nxt;
+        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];  // prefetch the next descriptor
         for_keys(t, [&](uint32_t k) {
             if constexpr (PASS == 0) {
                 if (k > kNanKey) ++nan;
@@ -211,55 +222,184 @@ __global__ void k_prune_ties(PruneArgs a) {
     sel->partial = mine > 0 && mine < sel->tie_local;
 }
 
-// Ties per tile (only for a partial share): keys == tau.
+// Ties (keys == tau) per (tile, warp range), only for a partial share.
+// Full tiles: warp w counts its contiguous vectors [w VW, (w+1) VW) -- the
+// ranges the mask pass gives each warp; a ragged tile puts its whole count
+// in entry 0 (the mask pass ranks it with block scans from the tile start).
 __global__ void __launch_bounds__(kPruneThreads) k_prune_tiecount(PruneArgs a) {
     pdl_wait();
     pdl_trigger();
     const PruneSel *sel = a.sel;
     if (!sel->partial) return;
     const uint32_t tau = sel->tau;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __shared__ uint32_t s_c;
+    PruneTile nxt;
+    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
     for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
-        if (threadIdx.x == 0) s_c = 0u;
-        __syncthreads();
-        uint32_t c = 0;
-        for_keys(a.tiles[ti], [&](uint32_t k) { c += k == tau; });
-        c = __reduce_add_sync(0xFFFFFFFFu, c);
-        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
-        __syncthreads();
-        if (threadIdx.x == 0) a.tile_ties[ti] = s_c;
-        __syncthreads();
+        const PruneTile t = nxt;
+        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];
+        if (t.n == kPruneTileElems) {
+            const bool bf = t.dtype == DYNMO_W_BF16;
+            const int VW = (int)kPruneTileElems / (bf ? 8 : 4) / kPruneWarps;
+            const uint4 *v = (const uint4 *)t.w + w * VW;
+            uint32_t c = 0;
+            for (int b = lane; b < VW; b += kU * 32) {
+                uint4 x[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) x[u] = b + 32 * u < VW ? ld_nc(v + b + 32 * u) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if (b + 32 * u >= VW) break;
+                    const uint32_t q[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (bf) c += (key_bf16(q[e] & 0xFFFFu) == tau) + (key_bf16(q[e] >> 16) == tau);
+                        else c += key_f32(q[e]) == tau;
+                    }
+                }
+            }
+            c = __reduce_add_sync(0xFFFFFFFFu, c);
+            if (lane == 0) a.tile_ties[ti * kPruneWarps + w] = c;
+        } else {
+            if (threadIdx.x == 0) s_c = 0u;
+            __syncthreads();
+            uint32_t c = 0;
+            for_keys(t, [&](uint32_t k) { c += k == tau; });
+            c = __reduce_add_sync(0xFFFFFFFFu, c);
+            if (lane == 0 && c) atomicAdd(&s_c, c);
+            __syncthreads();
+            if (threadIdx.x < kPruneWarps) a.tile_ties[ti * kPruneWarps + threadIdx.x] = threadIdx.x == 0 ? s_c : 0u;
+            __syncthreads();
+        }
     }
 }
 
-// Exclusive scan of the per-tile tie counts (one block; only if partial).
+// Exclusive scan of the per-tile tie totals (sum of the tile's warp-range
+// counts; one block of 32 warps, only if partial): each warp owns a
+// contiguous range of tiles read coalesced in chunks of 32 (4 chunks of
+// loads in flight): warp totals, a scan over the 32 warps, then per chunk a
+// warp scan plus the running offset.
 __global__ void __launch_bounds__(1024) k_prune_tiescan(PruneArgs a) {
     pdl_wait();
     pdl_trigger();
     if (!a.sel->partial) return;
-    __shared__ unsigned long long s[1024];
-    __shared__ unsigned long long s_carry;
-    if (threadIdx.x == 0) s_carry = 0ull;
+    __shared__ unsigned long long s_w[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t n = a.n_tiles;
+    const int64_t per = (n + 31) / 32;
+    const int64_t b0 = w * per, e0 = b0 + per < n ? b0 + per : n;
+    auto total = [&](int64_t i) -> unsigned long long {  // tile i's ties (8 warp ranges, 32 B)
+        if (i >= e0) return 0ull;
+        const uint4 *p = (const uint4 *)(a.tile_ties + i * kPruneWarps);
+        const uint4 x = p[0], y = p[1];
+        return (unsigned long long)x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w;
+    };
+    unsigned long long tot = 0;
+    for (int64_t c = b0; c < e0; c += 4 * 32) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = total(c + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tot += v[u];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, o);
+    if (lane == 0) s_w[w] = tot;
     __syncthreads();
-    for (int64_t base = 0; base < a.n_tiles; base += 1024) {
-        const int64_t i = base + threadIdx.x;
-        const unsigned long long v = i < a.n_tiles ? a.tile_ties[i] : 0u;
-        s[threadIdx.x] = v;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            const unsigned long long add = threadIdx.x >= o ? s[threadIdx.x - o] : 0ull;
-            __syncthreads();
-            s[threadIdx.x] += add;
-            __syncthreads();
+    unsigned long long run = 0;
+    for (int u = 0; u < w; ++u) run += s_w[u];
+    for (int64_t c = b0; c < e0; c += 4 * 32) {
+        unsigned long long v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = total(c + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            unsigned long long incl = v[u];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int64_t i = c + u * 32 + lane;
+            if (i < e0) a.tile_off[i] = run + incl - v[u];
+            run += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        if (i < a.n_tiles) a.tile_off[i] = s_carry + s[threadIdx.x] - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) s_carry += s[1023];
-        __syncthreads();
     }
 }
 
-// Masks: keep key > tau; keys == tau kept when all of this rank's ties are
+// Full tile (kPruneTileElems elements, 16-byte aligned): warp w owns the
+// contiguous vectors [w VW, (w+1) VW) and walks them in groups of 4 x 32
+// (lane L loads vector g*128 + u*32 + L: 4 coalesced 16-byte loads in
+// flight).  A tie's rank in element order = the warp range's offset (from
+// the tie-count scan) + ties earlier in the range (u-major, lane-minor warp
+// scans, a running count) + its position in the vector.  No block barrier.
+// Masks stored per vector (8 or 4 bytes, coalesced).
+template <bool BF>
+__device__ __forceinline__ void mask_full_tile(const PruneTile &t, uint32_t tau, bool partial, bool all_ties,
+                                               long long keep_ties, unsigned long long wbase) {
+    constexpr int EV = BF ? 8 : 4;
+    constexpr int VW = (int)kPruneTileElems / EV / kPruneWarps;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint4 *v = (const uint4 *)t.w + w * VW;
+    const bool al = ((uintptr_t)t.mask & (EV - 1)) == 0;
+    unsigned long long run = wbase;
+    for (int g = 0; g < VW; g += kU * 32) {
+        uint4 x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) x[u] = ld_nc(v + g + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t q[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+            uint32_t keys[EV];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                if (BF) {
+                    keys[2 * e] = key_bf16(q[e] & 0xFFFFu);
+                    keys[2 * e + 1] = key_bf16(q[e] >> 16);
+                } else {
+                    keys[e] = key_f32(q[e]);
+                }
+            }
+            unsigned long long before = 0;
+            if (partial) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int e = 0; e < EV; ++e) c += keys[e] == tau;
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                before = run + incl - c;
+                run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+            }
+            uint32_t m[2] = {0u, 0u}, seen = 0;
+#pragma unroll
+            for (int e = 0; e < EV; ++e) {
+                const uint32_t k = keys[e];
+                bool keep = k > tau && k <= kNanKey;
+                if (k == tau) {
+                    keep = partial ? (before + seen < (unsigned long long)keep_ties) : all_ties;
+                    ++seen;
+                }
+                m[e >> 2] |= (keep ? 1u : 0u) << (8 * (e & 3));
+            }
+            uint8_t *mk = t.mask + (int64_t)(w * VW + g + u * 32 + lane) * EV;
+            if (al) {
+                if (BF) *(uint2 *)mk = make_uint2(m[0], m[1]);
+                else *(uint32_t *)mk = m[0];
+            } else {
+#pragma unroll
+                for (int e = 0; e < EV; ++e) mk[e] = (uint8_t)((m[e >> 2] >> (8 * (e & 3))) & 1u);
+            }
+        }
+    }
+}
+
+// Masks (ragged last tile of a segment: thread-contiguous chunks of 16):
+// keep key > tau; keys == tau kept when all of this rank's ties are
 // (non-partial share) or, for a partial share, when their rank in element
 // order (tile offset + in-tile block scan over thread-contiguous chunks) is
 // below keep_ties.  16 elements per thread per step, 16-byte mask stores.
@@ -272,8 +412,21 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_mask(PruneArgs a) {
     const bool partial = sel->partial != 0;
     const long long keep_ties = sel->keep_ties;
     __shared__ uint32_t s_warp[kPruneThreads / 32];
+    PruneTile nxt;
+    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
     for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
-        const PruneTile t = a.tiles[ti];
+        const PruneTile t = nxt;
+        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];
+        if (t.n == kPruneTileElems) {  // the common case: coalesced fast path, no barriers
+            unsigned long long wb = 0;
+            if (partial) {  // tile offset + the earlier warp ranges of this tile
+                wb = a.tile_off[ti];
+                for (int u = 0; u < (int)(threadIdx.x >> 5); ++u) wb += a.tile_ties[ti * kPruneWarps + u];
+            }
+            if (t.dtype == DYNMO_W_BF16) mask_full_tile<true>(t, tau, partial, all_ties, keep_ties, wb);
+            else mask_full_tile<false>(t, tau, partial, all_ties, keep_ties, wb);
+            continue;
+        }
         unsigned long long run = partial ? a.tile_off[ti] : 0ull;  // ties before this chunk
         const uint32_t nchunk = (t.n + 16 * kPruneThreads - 1) / (16 * kPruneThreads);
         for (uint32_t ch = 0; ch < nchunk; ++ch) {
@@ -394,6 +547,19 @@ __global__ void k_prune_begin(PruneSel *sel, long long k) {
     sel->status = DYNMO_OK;
     sel->n_global = 0;
     sel->done = 0;
+}
+
+// Resident blocks per SM of the streaming kernels (grid = SMs x this).
+int prune_blocks_per_sm(int kind) {
+    int nb = 1;
+    switch (kind) {
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<0>, kPruneThreads, 0); break;
+        case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<1>, kPruneThreads, 0); break;
+        case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<2>, kPruneThreads, 0); break;
+        case 21: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_tiecount, kPruneThreads, 0); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_mask, kPruneThreads, 0); break;
+    }
+    return nb > 0 ? nb : 1;
 }
 
 cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s) {

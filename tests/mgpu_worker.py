@@ -143,6 +143,39 @@ def main():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "graph", rep)
     assert pm.error() == 0
     pm.close()
+    # Alg. 1 global pruning across ranks (NCCL all-reduce of the histograms,
+    # all-gather of the tie counts): every rank's masks == the oracle's on the
+    # concatenation of all ranks' shards in rank order; quantised magnitudes
+    # so ties straddle the rank boundary
+    shards_all, vals_all = [], []
+    for r in range(world):
+        gr = np.random.default_rng(700 + r)
+        sz = [9000 + 1000 * r, 17]
+        sh_r = []
+        for j, n_ in enumerate(sz):
+            x = np.round(gr.normal(0, 1, n_) * 4) / 4
+            if j == 0:
+                w = x.astype(np.float32)
+                sh_r.append((w, w.astype(np.float64), torch.float32))
+            else:
+                tb = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+                sh_r.append((tb, oracle.bf16_to_f64(tb.view(torch.int16).numpy().view(np.uint16)), torch.bfloat16))
+        shards_all.append(sh_r)
+        vals_all += [v for _, v, _ in sh_r]
+    mine = shards_all[rank]
+    wt = [torch.as_tensor(w).to(dev) for w, _, _ in mine]
+    mk = [torch.zeros(t.numel(), dtype=torch.uint8, device=dev) for t in wt]
+    pplan = D.PrunePlan(ctx, list(zip(wt, mk)))
+    Ntot = sum(v.size for v in vals_all)
+    first = sum(len(shards_all[r]) for r in range(rank))
+    for kk in (0, 1, Ntot // 3, Ntot // 2 + 7, Ntot):
+        info, pst2 = D.global_prune(ctx, pplan, kk)
+        torch.cuda.synchronize()
+        ost2, om = oracle.global_prune(vals_all, kk)
+        assert int(pst2.item()) == ost2 == 0
+        for j, m in enumerate(mk):
+            assert np.array_equal(m.cpu().numpy(), om[first + j]), (rank, kk, j)
+    pplan.close()
     dist.barrier()
     print(f"MGPU_OK {rank} layers[{begin},{begin + count}) moves={len(moves)} sent={sent} recv={got}", flush=True)
     ctx.close()

@@ -720,10 +720,10 @@ def _prune_shards(g, sizes, quant):
 def test_global_prune_parity(D, ctx, quant):
     """Alg. 1: masks == the oracle's for k in {0, 1, N/10,
     N/2, N-1, N} and random k, mixed f32/bf16, ragged segments spanning
-    several 8192-element tiles, heavy ties (quant=4) so that a partial tie
+    several 32768-element tiles, heavy ties (quant=4) so that a partial tie
     share falls inside a tile."""
     g = np.random.default_rng(100 + quant)
-    sizes = [20001, 7, 8192, 30000, 0, 16385]
+    sizes = [70001, 7, 32768, 100000, 0, 33000, 32767]  # full 32768-element tiles and ragged ones
     shards, vals = _prune_shards(g, sizes, quant)
     masks = [torch.zeros(max(1, s.numel()), dtype=torch.uint8, device=DEV)[:s.numel()] for s in shards]
     plan = D.PrunePlan(ctx, list(zip(shards, masks)))
