@@ -709,3 +709,67 @@ int oracle_global_prune(const double *w, int64_t n, int64_t k, uint8_t *mask) {
     free(pos);
     return st;
 }
+
+/* ------------------------------------------------------------------------
+ * O9 migration-minimising stage -> rank map (NEXT-3; P:L636 a migrated
+ * layer is released on GPU A and allocated on GPU B, P:L600 re-packing to
+ * fewer GPUs; reading Q23): layer i is on rank owner(i) = rank_old[stage_old(i)]
+ * before; the new split has n_new stages, each placed on a distinct rank of
+ * `allowed` (bit mask over G <= 16 ranks).  kept(pi) = sum of bytes[i] over
+ * layers whose new stage s has pi[s] == owner(i).  Returns the pi with the
+ * largest kept bytes, the lexicographically smallest such vector, defined by
+ *   f(used) = 0 if |used| = n_new, else max over g in allowed \ used of
+ *             w[|used|][g] + f(used + g)      (w[s][g] = bytes of new stage s on g)
+ * and the greedy lexicographic walk of f.  INFEASIBLE if n_new > |allowed|,
+ * INVALID on malformed splits or G outside [1, 16].
+ * ---------------------------------------------------------------------- */
+int oracle_map_stages(int32_t L, int32_t n_old, const int32_t *bnd_old, const int32_t *rank_old,
+                      int32_t n_new, const int32_t *bnd_new, const int64_t *bytes, int32_t G,
+                      uint32_t allowed, int32_t *rank_new, int64_t *kept) {
+    *kept = -1;
+    if (G < 1 || G > 16 || n_new < 1 || n_old < 1 || L < 1) return O_E_INVALID;
+    if (bnd_old[0] != 0 || bnd_old[n_old] != L || bnd_new[0] != 0 || bnd_new[n_new] != L) return O_E_INVALID;
+    for (int32_t s = 0; s < n_old; ++s)
+        if (bnd_old[s + 1] <= bnd_old[s] || rank_old[s] < 0 || rank_old[s] >= G) return O_E_INVALID;
+    for (int32_t s = 0; s < n_new; ++s)
+        if (bnd_new[s + 1] <= bnd_new[s]) return O_E_INVALID;
+    for (int32_t i = 0; i < L; ++i)
+        if (bytes[i] < 0) return O_E_INVALID;
+    allowed &= (G == 32 ? 0xFFFFFFFFu : ((1u << G) - 1u));
+    if (n_new > __builtin_popcount(allowed)) return O_E_INFEASIBLE;
+    int64_t w[32][16];
+    memset(w, 0, sizeof(w));
+    for (int32_t s = 0; s < n_new; ++s)
+        for (int32_t i = bnd_new[s]; i < bnd_new[s + 1]; ++i) {
+            int32_t so = 0;
+            while (!(bnd_old[so] <= i && i < bnd_old[so + 1])) ++so;
+            w[s][rank_old[so]] += bytes[i];
+        }
+    const uint32_t NS = 1u << G;
+    int64_t *f = (int64_t *)malloc(sizeof(int64_t) * NS);
+    for (int32_t k = G; k >= 0; --k)
+        for (uint32_t u = 0; u < NS; ++u) {
+            if (__builtin_popcount(u) != k || (u & ~allowed)) continue;
+            if (k >= n_new) { f[u] = 0; continue; }
+            int64_t best = -1;
+            for (int32_t g = 0; g < G; ++g) {
+                if (!((allowed >> g) & 1u) || ((u >> g) & 1u)) continue;
+                int64_t v = w[k][g] + f[u | (1u << g)];
+                if (v > best) best = v;
+            }
+            f[u] = best;
+        }
+    uint32_t used = 0;
+    for (int32_t s = 0; s < n_new; ++s)
+        for (int32_t g = 0; g < G; ++g) {
+            if (!((allowed >> g) & 1u) || ((used >> g) & 1u)) continue;
+            if (w[s][g] + f[used | (1u << g)] == f[used]) {
+                rank_new[s] = g;
+                used |= 1u << g;
+                break;
+            }
+        }
+    *kept = f[0];
+    free(f);
+    return O_OK;
+}

@@ -556,3 +556,39 @@ def test_global_prune_vs_lexsort_and_separation():
     assert st == oracle.E_INVALID and list(masks[0]) == [0, 0, 1]
     assert oracle.global_prune([np.array([1.0, 2.0])], 3)[0] == oracle.E_INVALID
     assert list(oracle.bf16_to_f64(np.array([0x3F80, 0xBF80, 0x8000, 0x4049], np.uint16))) == [1.0, -1.0, -0.0, 3.140625]
+
+
+# ----------------------------------------- O9 stage -> rank map (NEXT-3)
+def test_map_stages_vs_bruteforce():
+    """Reading Q23: the map keeping the most bytes in place, the
+    lexicographically smallest among optima == brute force over every
+    injective map (itertools.permutations enumerates them in lexicographic
+    order); small byte alphabet so optima tie often; allowed-rank masks;
+    INFEASIBLE when n_new > |allowed|; INVALID on a malformed split."""
+    import itertools
+    g = np.random.default_rng(23)
+    for _ in range(400):
+        G = int(g.integers(1, 7))
+        L = int(g.integers(2, 13))
+        n_old = int(g.integers(1, min(L, 6) + 1))
+        bo = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_old - 1, replace=False)), [L]]).astype(np.int32)
+        ro = g.integers(0, G, n_old).astype(np.int32)
+        allowed = int(g.integers(1, 1 << G))
+        n_new = int(g.integers(1, min(L, 6) + 1))
+        bn = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_new - 1, replace=False)), [L]]).astype(np.int32)
+        nb = g.integers(0, 4, L).astype(np.int64)
+        st, rn, kept = oracle.map_stages(L, bo, ro, bn, nb, G, allowed)
+        ranks = [r for r in range(G) if (allowed >> r) & 1]
+        if n_new > len(ranks):
+            assert st == oracle.E_INFEASIBLE
+            continue
+        owner = np.repeat(ro, np.diff(bo))
+        best, best_pi = -1, None
+        for pi in itertools.permutations(ranks, n_new):
+            k = sum(int(nb[i]) for s in range(n_new) for i in range(bn[s], bn[s + 1]) if owner[i] == pi[s])
+            if k > best:
+                best, best_pi = k, pi
+        assert st == 0 and kept == best and tuple(rn) == best_pi, (G, allowed, list(rn), best_pi)
+    assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2, 0b01)[0] == oracle.E_INFEASIBLE
+    assert oracle.map_stages(4, [0, 2, 5], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2)[0] == oracle.E_INVALID
+    assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 17)[0] == oracle.E_INVALID
