@@ -70,6 +70,13 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
  * this ctx (NCCL exchange, dynmo_global_prune) must be destroyed first: the
  * communicator cannot be torn down while a graph still holds its work. */
 void dynmo_ctx_destroy(dynmo_ctx ctx);
+/* Releasing GPUs after re-packing ("splitting the communicator
+ * via ncclCommSplit()"): collective over ctx's ranks.  Ranks passing the
+ * same color >= 0 get a new ctx over their group (ranks ordered by key, then
+ * by old rank), with its own communicator and peer windows; color < 0 (a
+ * released GPU) returns *out = NULL.  The old ctx stays valid (destroy it
+ * separately).  E_NCCL on a communicator error. */
+dynmo_status dynmo_ctx_split(dynmo_ctx ctx, int32_t color, int32_t key, dynmo_ctx *out);
 int32_t dynmo_ctx_nranks(dynmo_ctx ctx);
 int32_t dynmo_ctx_rank(dynmo_ctx ctx);
 
@@ -393,6 +400,25 @@ dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
 int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_bnd_old,
                              const int32_t *h_rank_old, int32_t n_new, const int32_t *h_bnd_new,
                              const int32_t *h_rank_new, int32_t *h_moves);
+
+/* Migration-minimising stage -> rank map (NEXT-3; reading Q23): layer i
+ * lives on rank_old[stage_old(i)]; place the n_new stages of the new split on
+ * DISTINCT ranks of `allowed` (bit r = rank r may host a stage, ranks < G <=
+ * 16) so that the bytes of layers that stay on their rank are maximal (each
+ * byte kept is a byte not migrated); among optimal maps the
+ * lexicographically smallest rank vector.  Exact (DP over subsets of ranks,
+ * one CTA, ctx workspace), asynchronous, capturable; feeds d_rank_new of
+ * dynmo_migrate_layers_dev directly.
+ *   d_bnd_old[n_old+1], d_rank_old[n_old], d_bnd_new[n_new+1] int32 device
+ *   d_bytes[n_layers] int64 device (e.g. the mem vector of profile_layers)
+ *   out: d_rank_new[n_new] int32 (-1 on error), d_kept[1] int64 (bytes kept,
+ *        -1 on error), d_status[1] int32: OK, INVALID (malformed split, rank
+ *        outside [0, G), negative bytes), INFEASIBLE (n_new > |allowed|).
+ * Host INVALID: n_layers outside [1, 1023], G outside [1, 16], null pointers. */
+dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, const int32_t *d_bnd_old,
+                              const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                              const int64_t *d_bytes, int32_t G, uint32_t allowed, int32_t *d_rank_new,
+                              int64_t *d_kept, int32_t *d_status, dynmo_stream stream);
 
 /* ---------------------------------------- global magnitude pruning (NEXT-2)
  * Algorithm 1: every rank holds a portion of the model; keep

@@ -66,6 +66,7 @@ struct dynmo_ctx_s {
     std::vector<PeerWindow *> peer_win;
     cudaStream_t aux = nullptr;  // setup collectives
     uint64_t mig_epoch = 0;
+    long long *d_map_work = nullptr;  // [1 << kMaxMapRanks] DP table of dynmo_map_stages
 };
 
 namespace dynmo {
@@ -204,6 +205,35 @@ dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]) {
     return DYNMO_OK;
 }
 
+// Peer window of a multi-rank ctx: a page of flags every peer can write,
+// CUDA-IPC mapped by every rank (handles all-gathered over the ctx comm).
+static dynmo_status setup_peer_window(dynmo_ctx c) {
+    const int nranks = c->nranks, rank = c->rank;
+    // peer window: flags every peer can write (CUDA IPC over NVLink)
+    dynmo_status st = DYNMO_OK;
+    if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
+        st = cuda_fail(cudaGetLastError(), "peer window");
+    cudaIpcMemHandle_t h;
+    if (!st && cudaIpcGetMemHandle(&h, c->d_win) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle");
+    std::vector<char> all;
+    if (!st) st = allgather_bytes(c, &h, sizeof(h), all);
+    c->peer_win.assign(nranks, nullptr);
+    for (int rr = 0; !st && rr < nranks; ++rr) {
+        if (rr == rank) {
+            c->peer_win[rr] = c->d_win;
+            continue;
+        }
+        cudaIpcMemHandle_t ph;
+        memcpy(&ph, all.data() + rr * sizeof(ph), sizeof(ph));
+        void *mp = nullptr;
+        if (cudaIpcOpenMemHandle(&mp, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (window)");
+        c->peer_win[rr] = (PeerWindow *)mp;
+    }
+    return st;
+}
+
 dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
                               const uint8_t *h_nccl_id, dynmo_ctx *out) {
     if (!out) return invalid("null ctx out");
@@ -219,6 +249,10 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         c->num_sms = sms;
+    if (cudaMalloc((void **)&c->d_map_work, sizeof(long long) << kMaxMapRanks) != cudaSuccess) {
+        delete c;
+        return cuda_fail(cudaGetLastError(), "ctx workspace");
+    }
     if (nranks > 1) {
         if (nranks > kMaxRanks) {
             delete c;
@@ -232,28 +266,54 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
             delete c;
             return DYNMO_E_NCCL;
         }
-        // peer window: flags every peer can write (CUDA IPC over NVLink)
-        dynmo_status st = DYNMO_OK;
-        if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
-            st = cuda_fail(cudaGetLastError(), "peer window");
-        cudaIpcMemHandle_t h;
-        if (!st && cudaIpcGetMemHandle(&h, c->d_win) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle");
-        std::vector<char> all;
-        if (!st) st = allgather_bytes(c, &h, sizeof(h), all);
-        c->peer_win.assign(nranks, nullptr);
-        for (int rr = 0; !st && rr < nranks; ++rr) {
-            if (rr == rank) {
-                c->peer_win[rr] = c->d_win;
-                continue;
-            }
-            cudaIpcMemHandle_t ph;
-            memcpy(&ph, all.data() + rr * sizeof(ph), sizeof(ph));
-            void *mp = nullptr;
-            if (cudaIpcOpenMemHandle(&mp, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
-                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (window)");
-            c->peer_win[rr] = (PeerWindow *)mp;
+        const dynmo_status st = setup_peer_window(c);
+        if (st) {
+            dynmo_ctx_destroy(c);
+            return st;
         }
+    }
+    *out = c;
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_split(dynmo_ctx ctx, int32_t color, int32_t key, dynmo_ctx *out) {
+    if (!ctx || !out) return invalid("null ctx/out");
+    *out = nullptr;
+    DeviceGuard g(ctx->device);
+    auto *c = new dynmo_ctx_s();
+    c->device = ctx->device;
+    c->num_sms = ctx->num_sms;
+    if (cudaMalloc((void **)&c->d_map_work, sizeof(long long) << kMaxMapRanks) != cudaSuccess) {
+        delete c;
+        return cuda_fail(cudaGetLastError(), "ctx workspace");
+    }
+    if (ctx->nranks == 1) {  // nothing to split: a fresh single-rank ctx (or none)
+        if (color < 0) {
+            dynmo_ctx_destroy(c);
+            return DYNMO_OK;
+        }
+        *out = c;
+        return DYNMO_OK;
+    }
+    ncclComm_t nc = nullptr;
+    ncclResult_t r = ncclCommSplit(ctx->comm, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &nc, nullptr);
+    if (r != ncclSuccess) {
+        g_err = std::string("ncclCommSplit: ") + ncclGetErrorString(r);
+        dynmo_ctx_destroy(c);
+        return DYNMO_E_NCCL;
+    }
+    if (color < 0 || !nc) {  // this rank is released (no communicator)
+        dynmo_ctx_destroy(c);
+        return DYNMO_OK;
+    }
+    int n = 1, rk = 0;
+    ncclCommCount(nc, &n);
+    ncclCommUserRank(nc, &rk);
+    c->comm = nc;
+    c->nranks = n;
+    c->rank = rk;
+    if (n > 1) {
+        const dynmo_status st = setup_peer_window(c);
         if (st) {
             dynmo_ctx_destroy(c);
             return st;
@@ -268,6 +328,7 @@ void dynmo_ctx_destroy(dynmo_ctx ctx) {
     for (int r = 0; r < (int)ctx->peer_win.size(); ++r)
         if (r != ctx->rank && ctx->peer_win[r]) cudaIpcCloseMemHandle(ctx->peer_win[r]);
     if (ctx->d_win) cudaFree(ctx->d_win);
+    if (ctx->d_map_work) cudaFree(ctx->d_map_work);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     for (auto &t : ctx->ph) {
@@ -789,6 +850,23 @@ dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream
     if (!ctx || !d_slot) return invalid("null ctx/slot");
     DeviceGuard g(ctx->device);
     CUDA_TRY(launch_stamp(d_slot, (cudaStream_t)stream), "k_stamp launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, const int32_t *d_bnd_old,
+                              const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                              const int64_t *d_bytes, int32_t G, uint32_t allowed, int32_t *d_rank_new,
+                              int64_t *d_kept, int32_t *d_status, dynmo_stream stream) {
+    if (!ctx) return invalid("null ctx");
+    if (n_layers < 1 || n_layers > 1023 || n_old < 1 || n_old > n_layers || n_new < 1 || n_new > n_layers)
+        return invalid("n_layers in [1, 1023], stage counts in [1, n_layers]");
+    if (G < 1 || G > kMaxMapRanks) return invalid("G outside [1, 16]");
+    if (!d_bnd_old || !d_rank_old || !d_bnd_new || !d_bytes || !d_rank_new || !d_kept || !d_status)
+        return invalid("null pointer");
+    DeviceGuard g(ctx->device);
+    MapArgs a{n_layers, n_old, n_new, G, allowed, d_bnd_old, d_rank_old, d_bnd_new, d_bytes,
+              d_rank_new, d_kept, d_status, ctx->d_map_work};
+    CUDA_TRY(launch_map_stages(a, (cudaStream_t)stream), "k_map_stages launch");
     return DYNMO_OK;
 }
 

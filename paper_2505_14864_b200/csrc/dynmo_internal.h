@@ -186,6 +186,20 @@ int prune_blocks_per_sm(int kind);
 cudaError_t launch_prune_begin(PruneSel *sel, long long k, cudaStream_t s);
 cudaError_t launch_prune_info(const PruneArgs &a, long long *d_info, int32_t *d_status, cudaStream_t s);
 
+// --------------------------------------- stage -> rank map (NEXT-3, Q23)
+constexpr int kMaxMapRanks = 16;
+struct MapArgs {
+    int32_t L, n_old, n_new, G;
+    uint32_t allowed;
+    const int32_t *bnd_old, *rank_old, *bnd_new;
+    const int64_t *bytes;
+    int32_t *rank_new;
+    int64_t *kept;
+    int32_t *status;
+    long long *work;  // [1 << G]
+};
+cudaError_t launch_map_stages(const MapArgs &a, cudaStream_t s);
+
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,

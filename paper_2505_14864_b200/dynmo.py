@@ -88,6 +88,24 @@ class Context:
     def handle(self):
         return self._h
 
+    @classmethod
+    def _wrap(cls, h, device: int):
+        obj = cls.__new__(cls)
+        obj.device = device
+        obj._h = h
+        obj.nranks = int(lib().dynmo_ctx_nranks(h))
+        obj.rank = int(lib().dynmo_ctx_rank(h))
+        return obj
+
+    def split(self, active: bool, key: Optional[int] = None) -> Optional["Context"]:
+        """Release GPUs after re-packing: collective; active
+        ranks get a Context over the active group (ordered by key, default
+        the old rank), released ranks get None."""
+        h = C.c_void_p()
+        _check(lib().dynmo_ctx_split(self._h, 0 if active else -1, self.rank if key is None else int(key),
+                                     C.byref(h)), "dynmo_ctx_split")
+        return Context._wrap(h, self.device) if h.value else None
+
     def set_timing(self, enable=True, phases=None):
         """enable all phases, or only `phases` (names from _lib.PHASES)."""
         mask = 0
@@ -464,3 +482,24 @@ def global_prune(ctx: Context, plan: PrunePlan, k: int, info=None, status=None, 
     _check(lib().dynmo_global_prune(ctx.handle, plan.handle, int(k), _ptr(info), _ptr(status), _stream(stream)),
            "dynmo_global_prune")
     return info, status
+
+
+# ----------------------------------------- stage -> rank map (NEXT-3)
+def map_stages(ctx: Context, n_layers: int, bnd_old: torch.Tensor, rank_old: torch.Tensor, bnd_new: torch.Tensor,
+               nbytes: torch.Tensor, G: int, allowed: Optional[int] = None, rank_new=None, kept=None, status=None,
+               stream=None):
+    """dynmo_map_stages: migration-minimising distinct ranks for the new
+    stages.  Returns (rank_new[n_new], kept[1], status[1]) device tensors."""
+    dev = bnd_new.device
+    n_new = bnd_new.numel() - 1
+    if rank_new is None:
+        rank_new = torch.empty(n_new, dtype=torch.int32, device=dev)
+    if kept is None:
+        kept = torch.empty(1, dtype=torch.int64, device=dev)
+    if status is None:
+        status = torch.empty(1, dtype=torch.int32, device=dev)
+    allowed = (1 << G) - 1 if allowed is None else int(allowed)
+    _check(lib().dynmo_map_stages(ctx.handle, int(n_layers), bnd_old.numel() - 1, _ptr(bnd_old), _ptr(rank_old),
+                                  n_new, _ptr(bnd_new), _ptr(nbytes), int(G), allowed & 0xFFFFFFFF,
+                                  _ptr(rank_new), _ptr(kept), _ptr(status), _stream(stream)), "dynmo_map_stages")
+    return rank_new, kept, status

@@ -176,6 +176,48 @@ def main():
         for j, m in enumerate(mk):
             assert np.array_equal(m.cpu().numpy(), om[first + j]), (rank, kk, j)
     pplan.close()
+    # Releasing GPUs after re-packing: split the ctx -- even
+    # ranks stay active, odd ranks are released (None) -- then the smaller
+    # group profiles, partitions and maps its stages onto its own ranks
+    sub = ctx.split(active=(rank % 2 == 0))
+    if rank % 2:
+        assert sub is None
+    else:
+        assert sub.nranks == (world + 1) // 2 and sub.rank == rank // 2
+        Gs = sub.nranks
+        n2 = 4
+        b2 = uniform_split(shape.L, n2)
+        r2 = np.array([s_ * Gs // n2 for s_ in range(n2)], np.int32)
+        beg2, cnt2 = rank_layers(b2, r2, sub.rank)
+        segs2 = []
+        for layer in range(beg2, beg2 + cnt2):
+            for m in synth.cfg2_layer_masks_u8(shape, layer, p[layer], 4):
+                t = torch.from_numpy(m.reshape(-1)).to(dev)
+                keep.append(t)
+                segs2.append(D.SegmentSpec(t, LB.SRC_MASK_U8, layer))
+        plan2 = D.ProfilePlan(sub, segs2, beg2, cnt2, n_total=shape.L, exchange="p2p" if Gs > 1 else False)
+        mem2 = torch.empty(shape.L, dtype=torch.int64, device=dev)
+        cost2, _, st2 = D.profile_layers(sub, plan2, D.coef_tensor(cnt2, A=0, B=1, device=dev),
+                                         mem_local=torch.from_numpy(payload[beg2:beg2 + cnt2].copy()).to(dev), mem=mem2)
+        b2t = D.Batch([shape.L], [n2], device=dev)
+        bnd2, _, _, pst2 = D.partition_stages(sub, b2t, cost2)
+        torch.cuda.synchronize()
+        assert int(st2.item()) == 0 and int(pst2.item()) == 0
+        assert np.array_equal(cost2.cpu().numpy(), want_cost)
+        ost2, ob2, _, _ = oracle.partition(want_cost, n2)
+        assert np.array_equal(bnd2.cpu().numpy()[:n2 + 1], ob2)
+        # one stage per active GPU after the re-pack: where to put them
+        if Gs > 1:
+            bn2_h = np.array([0, int(ob2[n2 // 2]), shape.L], np.int32)  # 2 workers after the re-pack
+            bn2 = torch.from_numpy(bn2_h).to(dev)
+            rn2, kept2, mst = D.map_stages(sub, shape.L, torch.from_numpy(b2.astype(np.int32)).to(dev),
+                                           torch.from_numpy(r2).to(dev), bn2, mem2, Gs)
+            torch.cuda.synchronize()
+            ost3, orn3, okept3 = oracle.map_stages(shape.L, b2, r2, bn2_h, payload, Gs)
+            assert int(mst.item()) == ost3 == 0 and np.array_equal(rn2.cpu().numpy(), orn3)
+            assert int(kept2.item()) == okept3
+        plan2.close()
+        sub.close()
     dist.barrier()
     print(f"MGPU_OK {rank} layers[{begin},{begin + count}) moves={len(moves)} sent={sent} recv={got}", flush=True)
     ctx.close()

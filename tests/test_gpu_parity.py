@@ -797,3 +797,38 @@ def test_global_prune_config2_full_size(D, ctx):
                 assert int(kt.max().item()) < int(pt.min().item())
             seen_pruned_tie = True
     plan.close()
+
+
+# ------------------------------ NEXT-3: migration-minimising stage -> rank map
+def test_map_stages_parity(D, ctx):
+    """dynmo_map_stages == the oracle (reading Q23): rank vector, kept bytes
+    and status on random instances, G up to 16 ranks, up to 1023 layers,
+    random allowed masks (INFEASIBLE ones included), tie-heavy bytes."""
+    g = np.random.default_rng(230)
+    for it in range(150):
+        G = int(g.integers(1, 17))
+        L = int(g.integers(2, 1024 if it % 10 == 0 else 120))
+        n_old = int(g.integers(1, min(L, 16) + 1))
+        bo = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_old - 1, replace=False)), [L]]).astype(np.int32)
+        ro = g.integers(0, G, n_old).astype(np.int32)
+        allowed = int(g.integers(1, 1 << G))
+        n_new = int(g.integers(1, min(L, 16) + 1))
+        bn = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_new - 1, replace=False)), [L]]).astype(np.int32)
+        nb = (g.integers(0, 5, L) * (1 << int(g.integers(0, 30)))).astype(np.int64)
+        rn, kept, st = D.map_stages(ctx, L, _dev(bo), _dev(ro), _dev(bn), _dev(nb), G, allowed)
+        torch.cuda.synchronize()
+        ost, orn, okept = oracle.map_stages(L, bo, ro, bn, nb, G, allowed)
+        assert int(st.item()) == ost, (it, int(st.item()), ost)
+        if ost == 0:
+            assert np.array_equal(rn.cpu().numpy(), orn) and int(kept.item()) == okept, it
+    # malformed split and negative bytes: INVALID
+    bo, ro, bn = np.array([0, 2, 4], np.int32), np.array([0, 1], np.int32), np.array([0, 3, 3], np.int32)
+    rn, kept, st = D.map_stages(ctx, 4, _dev(bo), _dev(ro), _dev(bn), _dev(np.ones(4, np.int64)), 2)
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_INVALID
+    rn, kept, st = D.map_stages(ctx, 4, _dev(bo), _dev(ro), _dev(np.array([0, 4], np.int32)),
+                                _dev(np.array([1, -1, 1, 1], np.int64)), 2)
+    torch.cuda.synchronize()
+    assert int(st.item()) == oracle.E_INVALID
+    with pytest.raises(D.DynmoError):
+        D.map_stages(ctx, 4, _dev(bo), _dev(ro), _dev(bn), _dev(np.ones(4, np.int64)), 17)
