@@ -251,6 +251,35 @@ def config_bytime(ctx):
                 b_new=[int(x) for x in ob], imbalance=round(float(out["imbalance"].item()), 4))
 
 
+def map_stages_cfg(ctx):
+    """NEXT-3 stage -> rank map latency: config 2's 48 layers / CSR payloads,
+    old split 8 stages on 8 ranks, new split = the partition of the costs
+    (G = 8), and a 16-rank / 16-stage worst case (2^16 DP states)."""
+    shape = synth.GPTShape()
+    p = synth.cfg2_keep_probs(shape, 0.9, 4)
+    pay = synth.cfg2_payload_bytes(shape, p).astype(np.int64)
+    cost = np.load(os.path.join(os.path.dirname(__file__), "cfg2_cost.npy")).astype(np.int64)
+    out = {}
+    for G, n in ((8, 8), (16, 16)):
+        bo = np.array([round(s * shape.L / n) for s in range(n + 1)], np.int32)
+        ro = np.arange(n, dtype=np.int32) % G
+        st, bn, _, _ = oracle.partition(cost, n)
+        bn = np.asarray(bn, np.int32)
+        args = (shape.L, dev(bo), dev(ro), dev(bn), dev(pay), G)
+        res = {}
+
+        def step():
+            res["r"] = D.map_stages(ctx, *args)
+
+        ms, _ = timed(step)
+        rn, kept, mst = res["r"]
+        ost, orn, okept = oracle.map_stages(shape.L, bo, ro, bn, pay, G)
+        assert int(mst.item()) == ost == 0 and np.array_equal(rn.cpu().numpy(), orn)
+        out[f"G{G}_n{n}"] = dict(device_ms=round(ms, 4), kept_fraction=round(okept / float(pay.sum()), 4),
+                                 ranks=[int(x) for x in orn])
+    return out
+
+
 def main():
     global flush
     torch.cuda.set_device(0)
@@ -259,7 +288,8 @@ def main():
     res = {}
     for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
                      ("config4_auxloss", lambda: config4(ctx, 4.0)), ("config4_sbase", lambda: config4(ctx, 64.0)),
-                     ("config5", lambda: config5(ctx)), ("bytime_cfg2", lambda: config_bytime(ctx))]:
+                     ("config5", lambda: config5(ctx)), ("bytime_cfg2", lambda: config_bytime(ctx)),
+                     ("map_stages", lambda: map_stages_cfg(ctx))]:
         res[name] = fn()
         print(name, json.dumps(res[name]), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
