@@ -56,6 +56,9 @@ def parse():
                     help="layer migration over NVLink peer memory (default) or NCCL send/recv")
     ap.add_argument("--phase-timing", choices=["all", "profile", "none"], default="profile",
                     help="which phases get CUDA-event nodes in the step graph")
+    ap.add_argument("--map-stages", action="store_true",
+                    help="NEXT-3: place the new stages on the GPU slots that keep the most payload in place "
+                         "(dynmo_map_stages inside the step) instead of stage s on GPU floor(s*G/8)")
     ap.add_argument("--host-migrate", action="store_true",
                     help="host-driven migration (D2H of the boundaries, then the migrate call) "
                          "instead of the device-driven call inside the step's graph")
@@ -145,6 +148,10 @@ class ClockSampler:
 
     def __enter__(self):
         import subprocess
+        if os.environ.get("DYNMO_BENCH_NO_CLOCKS") == "1":  # diagnosis only: no sampler
+            self.err = "disabled (DYNMO_BENCH_NO_CLOCKS=1)"
+            self.lines, self.t0, self.t1 = [], None, None
+            return self
         import threading
         self.lines, self.t0, self.t1 = [], None, None
         try:
@@ -173,6 +180,9 @@ class ClockSampler:
         self.t1 = time.monotonic()
 
     def __exit__(self, *a):
+        if not hasattr(self, "th"):
+            self.out = ""
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -338,6 +348,10 @@ def run_dynmo(args):
     d_bold = torch.from_numpy(b_old.astype(np.int32)).to(dev)
     d_ranks = torch.from_numpy(ranks.astype(np.int32)).to(dev)
     d_bytes = torch.zeros(2, dtype=torch.int64, device=dev)
+    use_map = bool(args.map_stages) and G > 1
+    d_slots = torch.arange(N_STAGES, dtype=torch.int32, device=dev)  # old stage s in slot s (on GPU ranks[s])
+    d_rmap = d_ranks.clone()  # new stage -> GPU (identity placement unless --map-stages)
+    map_out = dict(kept=torch.zeros(1, dtype=torch.int64, device=dev), status=torch.zeros(1, dtype=torch.int32, device=dev))
     # device-driven migration (G > 1, peer memory): the whole step is one graph
     # (also at G = 1, where nothing migrates: the step never waits on the host)
     dev_mig = (G == 1 or args.migrate == "p2p") and not args.host_migrate
@@ -357,8 +371,11 @@ def run_dynmo(args):
             D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
         D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
                            imbalance=part["imb"], status=part["st"])
+        if use_map:
+            D.map_stages(ctx, L, d_bold, d_slots, part["bnd"], mem, N_STAGES, slot_rank=d_ranks, rank_new=d_rmap,
+                         kept=map_out["kept"], status=map_out["status"])
         if dev_mig and pmig is not None:
-            pmig.device(d_bold, d_ranks, part["bnd"], d_ranks, d_bytes[0:1], d_bytes[1:2])
+            pmig.device(d_bold, d_ranks, part["bnd"], d_rmap, d_bytes[0:1], d_bytes[1:2])
         res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
         ev_res.record(main)
         for sd in side:
@@ -381,7 +398,10 @@ def run_dynmo(args):
     b_new = r0[:N_STAGES + 1].copy()
     if r0[nb] != 0 or r0[nb + 1] != 0:
         raise SystemExit(f"rebalance failed: statuses {r0[nb:]}")
-    moves = D.migration_plan(L, b_old, ranks, b_new, ranks)
+    rank_new = d_rmap.cpu().numpy() if use_map else ranks
+    if use_map and int(map_out["status"].item()) != 0:
+        raise SystemExit(f"map_stages failed: {int(map_out['status'].item())}")
+    moves = D.migration_plan(L, b_old, ranks, b_new, rank_new)
     moves_mine = any(int(sr) == rank or int(ds) == rank for _, sr, ds in moves)
     for layer, src, dst in moves:
         if dst == rank:
@@ -391,11 +411,13 @@ def run_dynmo(args):
     else:
         migrator = D.Migrator(ctx, L, send, recv)
 
-    def step():
+    copies = []  # extra captures of the one-graph step (their own timing events)
+
+    def step(k=0):
         if dev_mig:
             # one graph launch: no host round trip inside the step
             if graph is not None:
-                graph.replay()
+                (copies[k % len(copies)] if copies else graph).replay()
             else:
                 solve_async()
             return None
@@ -404,26 +426,52 @@ def run_dynmo(args):
         # the host has seen the partition, so the exchange is complete: the
         # migration runs on its own stream, overlapping the side branches
         with torch.cuda.stream(comm):
-            sr = migrator(b_old, ranks, r[:N_STAGES + 1], ranks)
+            sr = migrator(b_old, ranks, r[:N_STAGES + 1], rank_new)
         main.wait_stream(comm)
         return sr
 
+    ev_in = []  # (start, end) external events inside each one-graph step copy
     if args.graph:
         # capture the step's device part (timing enabled so the phase events
         # are baked into the graph as external event-record nodes)
         ctx.set_timing(True, phases=None if args.phase_timing == "all" else
                        ([] if args.phase_timing == "none" else ["profile"]))
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=torch.cuda.Stream(device=dev)):
-            solve_async()
+        if dev_mig:
+            # One-graph step: [device barrier (the step runs at the
+            # training-iteration barrier) -> start event -> step -> end event].
+            # The timed interval begins once EVERY rank's graph is running, so
+            # a host hiccup on one rank delays only the untimed barrier.  C
+            # copies (own events each) let the host enqueue C steps ahead and
+            # read the events once per group.
+            C = 4 if args.steps % 4 == 0 else (2 if args.steps % 2 == 0 else 1)
+
+            def capture_step():  # (a function: no stray reference to a graph survives)
+                e0 = torch.cuda.Event(enable_timing=True, external=True)
+                e1 = torch.cuda.Event(enable_timing=True, external=True)
+                g_ = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_, stream=torch.cuda.Stream(device=dev)):
+                    ctx.barrier()
+                    e0.record()
+                    solve_async()
+                    e1.record()
+                copies.append(g_)
+                ev_in.append((e0, e1))
+
+            for _ in range(C):
+                capture_step()
+            graph = copies[0]
+        else:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=torch.cuda.Stream(device=dev)):
+                solve_async()
         torch.cuda.synchronize()
         ctx.timing_read()  # discard
         ctx.set_timing(False)
         stream = torch.cuda.current_stream()
 
-    for _ in range(max(args.warmup, 3)):
+    for w in range(max(args.warmup, 3, len(copies))):
         flush()
-        step()
+        step(w)
     torch.cuda.synchronize()
     if G > 1:
         dist.barrier()
@@ -433,6 +481,7 @@ def run_dynmo(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sent_recv = (0, 0)
     bar = torch.zeros(1, device=dev)
+    step_list = []
 
     def step_barrier():
         # rebalancing runs at the training iteration barrier: align the
@@ -442,16 +491,27 @@ def run_dynmo(args):
 
     with ClockSampler(local) as clk:
         clk.start()
-        for k in range(args.steps):
-            flush()
-            step_barrier()
-            ev[k][0].record(stream)
-            sr = step()
-            if sr is not None:
-                sent_recv = sr
-            ev[k][1].record(stream)
-            ev[k][1].synchronize()  # outside the timed interval: fold the phase events
-            ctx.timing_poll()
+        if ev_in:
+            C = len(copies)
+            for k in range(args.steps):
+                flush()  # L2 flush between steps (outside the timed interval)
+                step(k)
+                if (k + 1) % C == 0:  # read this group's per-step device intervals
+                    ev_in[-1][1].synchronize()
+                    step_list += [a.elapsed_time(b) for a, b in ev_in]
+                    ctx.timing_poll()
+        else:
+            for k in range(args.steps):
+                flush()
+                step_barrier()
+                ev[k][0].record(stream)
+                sr = step(k)
+                if sr is not None:
+                    sent_recv = sr
+                ev[k][1].record(stream)
+                ev[k][1].synchronize()  # outside the timed interval: fold the phase events
+                ctx.timing_poll()
+                step_list.append(ev[k][0].elapsed_time(ev[k][1]))
         torch.cuda.synchronize()
         clk.stop()
     if G > 1:
@@ -459,7 +519,7 @@ def run_dynmo(args):
     torch.cuda.synchronize()
     ctx.set_timing(False)
     phases = ctx.timing_read()
-    step_ms = np.array([a.elapsed_time(b) for a, b in ev])
+    step_ms = np.array(step_list)
     total_ms = float(step_ms.sum())
     prof_ms, prof_n = phases["profile"]
     prof_avg = prof_ms / max(prof_n, 1)
@@ -495,6 +555,7 @@ def run_dynmo(args):
     # nodes cost ~17 us per step, so the headline loop times only k_profile)
     diag_phases = None
     if args.graph:
+        ctx.timing_detach()  # the timed graphs' events are not part of the diagnostic pass
         ctx.set_timing(True)
         gdiag = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gdiag, stream=torch.cuda.Stream(device=dev)):
@@ -526,6 +587,13 @@ def run_dynmo(args):
         dist.all_reduce(ach, op=dist.ReduceOp.MIN)
     total_ms, prof_avg_max, e2e_ms, mig_ms, max_sent, max_recv = vals.tolist()
     achieved = float(ach.item())
+    # per-step job time = max over ranks of each step's device interval (the
+    # step ends when the slowest rank does); value stays max over ranks of
+    # the total (the contract), the step statistics use this array
+    st_t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(st_t, op=dist.ReduceOp.MAX)
+    step_ms = st_t.cpu().numpy()
 
     if rank == 0:
         peaks, peak_src = load_peaks()
@@ -536,6 +604,8 @@ def run_dynmo(args):
                             if dev_mig else "host-driven peer-memory pull" if args.migrate == "p2p"
                             else "host-driven NCCL send/recv")
         cfg["graph"] = bool(args.graph)
+        cfg["stage_placement"] = ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
+                                  else "stage s on GPU floor(s*G/8) before and after")
         cost_h = cost.cpu().numpy()
         x_old = np.add.reduceat(cost_h, b_old[:-1])
         x_new = np.add.reduceat(cost_h, b_new[:-1])
@@ -561,7 +631,9 @@ def run_dynmo(args):
             "step_ms": {"median": round(float(np.median(step_ms)), 5),
                         "p95": round(float(np.percentile(step_ms, 95)), 5),
                         "max": round(float(step_ms.max()), 5),
-                        "n_over_2x_median": int((step_ms > 2 * np.median(step_ms)).sum())},
+                        "n_over_2x_median": int((step_ms > 2 * np.median(step_ms)).sum()),
+                        "outliers": [[int(k), round(float(step_ms[k]), 4)]
+                                     for k in np.flatnonzero(step_ms > 2 * np.median(step_ms))[:8]]},
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
                         "max_bytes_recv_per_gpu": int(max_recv), "avg_ms": round(mig_ms, 5),
                         "nvlink_GBps": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9, 1)
@@ -590,6 +662,16 @@ def run_dynmo(args):
                                    "sample": f"{len(c_s)} full config-2 oracle steps (all 48 layers' u8 masks, "
                                              f"every solver), 1 thread; host has {os.cpu_count()} cores"}
         print(json.dumps(out), flush=True)
+    # teardown order: graphs holding NCCL work (the in-graph barrier) before
+    # the communicator, then the peer-memory plans, then the ctx
+    torch.cuda.synchronize()
+    copies.clear()
+    graph = gdiag = None  # noqa: F841
+    torch.cuda.synchronize()
+    if pmig is not None:
+        pmig.close()
+    plan.close()
+    ctx.close()
     if G > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -66,9 +66,9 @@ dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]);
 dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
                               const uint8_t *h_nccl_id /* 128 B, or NULL if nranks==1 */,
                               dynmo_ctx *out);
-/* Collective when nranks > 1.  CUDA graphs that captured collective calls of
- * this ctx (NCCL exchange, dynmo_global_prune) must be destroyed first: the
- * communicator cannot be torn down while a graph still holds its work. */
+/* Frees the ctx and aborts its communicator without waiting for outstanding
+ * collective work: synchronise the streams that use it first (CUDA graphs
+ * that captured collectives of this ctx must not be replayed afterwards). */
 void dynmo_ctx_destroy(dynmo_ctx ctx);
 /* Releasing GPUs after re-packing ("splitting the communicator
  * via ncclCommSplit()"): collective over ctx's ranks.  Ranks passing the
@@ -103,6 +103,16 @@ enum {
  * 1 << DYNMO_PHASE_PROFILE only; -1 = all). */
 dynmo_status dynmo_ctx_set_timing(dynmo_ctx ctx, int32_t enable);
 dynmo_status dynmo_ctx_timing_poll(dynmo_ctx ctx);
+/* Device-side barrier over the ctx ranks on `stream` (a one-element NCCL
+ * all-reduce; no-op for one rank): work enqueued after it starts only when
+ * every rank's stream has reached it.  Capturable (the rebalancing step runs
+ * at the training-iteration barrier); the graph holding it must be
+ * destroyed before the ctx. */
+dynmo_status dynmo_ctx_barrier(dynmo_ctx ctx, dynmo_stream stream);
+/* Stop polling the event pairs baked into the graphs captured so far (their
+ * events stay alive until ctx destruction, so those graphs remain valid):
+ * call before capturing a graph whose timings are read separately. */
+dynmo_status dynmo_ctx_timing_detach(dynmo_ctx ctx);
 dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total_ms,
                                    int64_t *h_count);
 
@@ -408,7 +418,9 @@ int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_b
  * byte kept is a byte not migrated); among optimal maps the
  * lexicographically smallest rank vector.  Exact (DP over subsets of ranks,
  * one CTA, ctx workspace), asynchronous, capturable; feeds d_rank_new of
- * dynmo_migrate_layers_dev directly.
+ * dynmo_migrate_layers_dev directly.  Several stages per GPU: make the G
+ * "ranks" slots (capacity = slots per GPU), give d_rank_old in slot units,
+ * and d_slot_rank[G] (nullable) maps each slot to its GPU for the output.
  *   d_bnd_old[n_old+1], d_rank_old[n_old], d_bnd_new[n_new+1] int32 device
  *   d_bytes[n_layers] int64 device (e.g. the mem vector of profile_layers)
  *   out: d_rank_new[n_new] int32 (-1 on error), d_kept[1] int64 (bytes kept,
@@ -417,8 +429,8 @@ int32_t dynmo_migration_plan(int32_t n_layers, int32_t n_old, const int32_t *h_b
  * Host INVALID: n_layers outside [1, 1023], G outside [1, 16], null pointers. */
 dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, const int32_t *d_bnd_old,
                               const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
-                              const int64_t *d_bytes, int32_t G, uint32_t allowed, int32_t *d_rank_new,
-                              int64_t *d_kept, int32_t *d_status, dynmo_stream stream);
+                              const int64_t *d_bytes, int32_t G, uint32_t allowed, const int32_t *d_slot_rank,
+                              int32_t *d_rank_new, int64_t *d_kept, int32_t *d_status, dynmo_stream stream);
 
 /* ---------------------------------------- global magnitude pruning (NEXT-2)
  * Algorithm 1: every rank holds a portion of the model; keep

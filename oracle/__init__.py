@@ -67,7 +67,7 @@ def lib():
             "oracle_diffuse_fluid": (C.c_int, [p, i32, i32, p, dbl, i32, p, p, p]),
             "oracle_moves": (i32, [i32, i32, p, p, i32, p, p, p]),
             "oracle_global_prune": (C.c_int, [p, i64, i64, p]),
-            "oracle_map_stages": (C.c_int, [i32, i32, p, p, i32, p, p, i32, C.c_uint32, p, p]),
+            "oracle_map_stages": (C.c_int, [i32, i32, p, p, i32, p, p, i32, C.c_uint32, p, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -271,15 +271,17 @@ def bf16_to_f64(bits: np.ndarray) -> np.ndarray:
 
 
 # ----------------------------------------- O9 stage -> rank map (NEXT-3)
-def map_stages(L, bnd_old, rank_old, bnd_new, nbytes, G, allowed=None):
+def map_stages(L, bnd_old, rank_old, bnd_new, nbytes, G, allowed=None, slot_rank=None):
     """(status, rank_new[n_new], kept_bytes): migration-minimising map of
     the new stages onto distinct allowed ranks (lexicographically smallest
-    optimum)."""
+    optimum); with slot_rank the G ranks are slots on GPUs slot_rank[j]."""
+    sr = _c(slot_rank, np.int32) if slot_rank is not None else None
     bo, ro, bn = _c(bnd_old, np.int32), _c(rank_old, np.int32), _c(bnd_new, np.int32)
     b = _c(nbytes, np.int64)
     out = np.full(max(1, len(bn) - 1), -1, np.int32)
     kept = np.zeros(1, np.int64)
     allowed = (1 << G) - 1 if allowed is None else int(allowed)
     st = lib().oracle_map_stages(int(L), len(bo) - 1, _ptr(bo), _ptr(ro), len(bn) - 1, _ptr(bn), _ptr(b),
-                                 int(G), allowed & 0xFFFFFFFF, _ptr(out), _ptr(kept))
+                                 int(G), allowed & 0xFFFFFFFF, _ptr(sr) if sr is not None else None, _ptr(out),
+                                 _ptr(kept))
     return int(st), out[:len(bn) - 1].copy(), int(kept[0])

@@ -721,11 +721,14 @@ int oracle_global_prune(const double *w, int64_t n, int64_t k, uint8_t *mask) {
  *   f(used) = 0 if |used| = n_new, else max over g in allowed \ used of
  *             w[|used|][g] + f(used + g)      (w[s][g] = bytes of new stage s on g)
  * and the greedy lexicographic walk of f.  INFEASIBLE if n_new > |allowed|,
- * INVALID on malformed splits or G outside [1, 16].
+ * INVALID on malformed splits or G outside [1, 16].  With slot_rank (several
+ * stages per GPU: the G "ranks" are slots, slot_rank[j] its GPU) a byte is
+ * kept when the GPU of its new slot equals the GPU of its old slot, and the
+ * output is rank_new[s] = slot_rank[slot].
  * ---------------------------------------------------------------------- */
 int oracle_map_stages(int32_t L, int32_t n_old, const int32_t *bnd_old, const int32_t *rank_old,
                       int32_t n_new, const int32_t *bnd_new, const int64_t *bytes, int32_t G,
-                      uint32_t allowed, int32_t *rank_new, int64_t *kept) {
+                      uint32_t allowed, const int32_t *slot_rank, int32_t *rank_new, int64_t *kept) {
     *kept = -1;
     if (G < 1 || G > 16 || n_new < 1 || n_old < 1 || L < 1) return O_E_INVALID;
     if (bnd_old[0] != 0 || bnd_old[n_old] != L || bnd_new[0] != 0 || bnd_new[n_new] != L) return O_E_INVALID;
@@ -743,7 +746,12 @@ int oracle_map_stages(int32_t L, int32_t n_old, const int32_t *bnd_old, const in
         for (int32_t i = bnd_new[s]; i < bnd_new[s + 1]; ++i) {
             int32_t so = 0;
             while (!(bnd_old[so] <= i && i < bnd_old[so + 1])) ++so;
-            w[s][rank_old[so]] += bytes[i];
+            if (slot_rank) {
+                for (int32_t g = 0; g < G; ++g)
+                    if (slot_rank[g] == slot_rank[rank_old[so]]) w[s][g] += bytes[i];
+            } else {
+                w[s][rank_old[so]] += bytes[i];
+            }
         }
     const uint32_t NS = 1u << G;
     int64_t *f = (int64_t *)malloc(sizeof(int64_t) * NS);
@@ -764,7 +772,7 @@ int oracle_map_stages(int32_t L, int32_t n_old, const int32_t *bnd_old, const in
         for (int32_t g = 0; g < G; ++g) {
             if (!((allowed >> g) & 1u) || ((used >> g) & 1u)) continue;
             if (w[s][g] + f[used | (1u << g)] == f[used]) {
-                rank_new[s] = g;
+                rank_new[s] = slot_rank ? slot_rank[g] : g;
                 used |= 1u << g;
                 break;
             }

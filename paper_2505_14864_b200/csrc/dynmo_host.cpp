@@ -51,6 +51,7 @@ struct PhaseTimer {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;     // eager launches
     size_t used = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> graph;  // baked into captured graphs
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> detached;  // of graphs no longer polled
     double acc_ms = 0.0;
     int64_t acc_n = 0;
 };
@@ -330,13 +331,19 @@ void dynmo_ctx_destroy(dynmo_ctx ctx) {
     if (ctx->d_win) cudaFree(ctx->d_win);
     if (ctx->d_map_work) cudaFree(ctx->d_map_work);
     if (ctx->aux) cudaStreamDestroy(ctx->aux);
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    // abort, not destroy: NCCL's destroy blocks while a CUDA graph still holds
+    // captured work of the communicator (the caller has synchronised)
+    if (ctx->comm) ncclCommAbort(ctx->comm);
     for (auto &t : ctx->ph) {
         for (auto &pr : t.ev) {
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
         for (auto &pr : t.graph) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        for (auto &pr : t.detached) {
             cudaEventDestroy(pr.first);
             cudaEventDestroy(pr.second);
         }
@@ -371,6 +378,30 @@ dynmo_status dynmo_ctx_timing_poll(dynmo_ctx ctx) {
             t.acc_ms += ms;
             t.acc_n++;
         }
+    }
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_barrier(dynmo_ctx ctx, dynmo_stream stream) {
+    if (!ctx) return invalid("null ctx");
+    if (ctx->nranks == 1) return DYNMO_OK;
+    DeviceGuard g(ctx->device);
+    // one int32 all-reduce in the ctx workspace: completes on every rank's
+    // stream only once every rank's stream has reached it
+    const ncclResult_t r = ncclAllReduce(ctx->d_map_work, ctx->d_map_work, 1, ncclInt32, ncclSum, ctx->comm,
+                                         (cudaStream_t)stream);
+    if (r != ncclSuccess) {
+        g_err = std::string("ncclAllReduce (barrier): ") + ncclGetErrorString(r);
+        return DYNMO_E_NCCL;
+    }
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_timing_detach(dynmo_ctx ctx) {
+    if (!ctx) return invalid("null ctx");
+    for (auto &t : ctx->ph) {
+        t.detached.insert(t.detached.end(), t.graph.begin(), t.graph.end());
+        t.graph.clear();
     }
     return DYNMO_OK;
 }
@@ -855,8 +886,8 @@ dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream
 
 dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, const int32_t *d_bnd_old,
                               const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
-                              const int64_t *d_bytes, int32_t G, uint32_t allowed, int32_t *d_rank_new,
-                              int64_t *d_kept, int32_t *d_status, dynmo_stream stream) {
+                              const int64_t *d_bytes, int32_t G, uint32_t allowed, const int32_t *d_slot_rank,
+                              int32_t *d_rank_new, int64_t *d_kept, int32_t *d_status, dynmo_stream stream) {
     if (!ctx) return invalid("null ctx");
     if (n_layers < 1 || n_layers > 1023 || n_old < 1 || n_old > n_layers || n_new < 1 || n_new > n_layers)
         return invalid("n_layers in [1, 1023], stage counts in [1, n_layers]");
@@ -865,7 +896,7 @@ dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, co
         return invalid("null pointer");
     DeviceGuard g(ctx->device);
     MapArgs a{n_layers, n_old, n_new, G, allowed, d_bnd_old, d_rank_old, d_bnd_new, d_bytes,
-              d_rank_new, d_kept, d_status, ctx->d_map_work};
+              d_rank_new, d_kept, d_status, ctx->d_map_work, d_slot_rank};
     CUDA_TRY(launch_map_stages(a, (cudaStream_t)stream), "k_map_stages launch");
     return DYNMO_OK;
 }

@@ -197,6 +197,7 @@ struct MapArgs {
     int64_t *kept;
     int32_t *status;
     long long *work;  // [1 << G]
+    const int32_t *slot_rank;  // nullable: output rank_new[s] = slot_rank[slot]
 };
 cudaError_t launch_map_stages(const MapArgs &a, cudaStream_t s);
 

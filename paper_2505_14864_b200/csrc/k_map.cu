@@ -68,6 +68,19 @@ __global__ void __launch_bounds__(kMapThreads) k_map_stages(MapArgs a) {
         if (b) atomicAdd(&w[sl][a.rank_old[lo]], (unsigned long long)b);
     }
     __syncthreads();
+    if (a.slot_rank) {  // slots: a byte stays when its new slot is on the same GPU as its old slot
+        __shared__ unsigned long long wr[kMaxMapRanks][kMaxMapRanks];
+        if (tid < n_new * G) {
+            const int s = tid / G, g = tid % G;
+            unsigned long long v = 0;
+            for (int j = 0; j < G; ++j)
+                if (a.slot_rank[j] == a.slot_rank[g]) v += w[s][j];
+            wr[s][g] = v;
+        }
+        __syncthreads();
+        if (tid < n_new * G) w[tid / G][tid % G] = wr[tid / G][tid % G];
+        __syncthreads();
+    }
     long long *f = a.work;
     const uint32_t NS = 1u << G;
     for (int k = n_new; k >= 0; --k) {
@@ -90,7 +103,7 @@ __global__ void __launch_bounds__(kMapThreads) k_map_stages(MapArgs a) {
             for (int g = 0; g < G; ++g) {
                 if (!((allowed >> g) & 1u) || ((used >> g) & 1u)) continue;
                 if ((long long)w[s][g] + f[used | (1u << g)] == f[used]) {
-                    a.rank_new[s] = g;
+                    a.rank_new[s] = a.slot_rank ? a.slot_rank[g] : g;
                     used |= 1u << g;
                     break;
                 }

@@ -121,6 +121,14 @@ class Context:
         """Fold the phase events of the last graph replay into the accumulators."""
         _check(lib().dynmo_ctx_timing_poll(self._h), "timing_poll")
 
+    def barrier(self, stream=None):
+        """Device-side barrier over the ctx ranks (capturable)."""
+        _check(lib().dynmo_ctx_barrier(self._h, _stream(stream)), "dynmo_ctx_barrier")
+
+    def timing_detach(self):
+        """Stop polling the timing events of the graphs captured so far."""
+        _check(lib().dynmo_ctx_timing_detach(self._h), "timing_detach")
+
     def timing_read(self) -> dict:
         """{phase: (total_ms, launches)} since the last read (waits on events)."""
         out = {}
@@ -486,10 +494,11 @@ def global_prune(ctx: Context, plan: PrunePlan, k: int, info=None, status=None, 
 
 # ----------------------------------------- stage -> rank map (NEXT-3)
 def map_stages(ctx: Context, n_layers: int, bnd_old: torch.Tensor, rank_old: torch.Tensor, bnd_new: torch.Tensor,
-               nbytes: torch.Tensor, G: int, allowed: Optional[int] = None, rank_new=None, kept=None, status=None,
-               stream=None):
-    """dynmo_map_stages: migration-minimising distinct ranks for the new
-    stages.  Returns (rank_new[n_new], kept[1], status[1]) device tensors."""
+               nbytes: torch.Tensor, G: int, allowed: Optional[int] = None, slot_rank=None, rank_new=None, kept=None,
+               status=None, stream=None):
+    """dynmo_map_stages: migration-minimising distinct ranks (or slots, with
+    slot_rank[G] mapping slots to GPUs for the output) for the new stages.
+    Returns (rank_new[n_new], kept[1], status[1]) device tensors."""
     dev = bnd_new.device
     n_new = bnd_new.numel() - 1
     if rank_new is None:
@@ -500,6 +509,6 @@ def map_stages(ctx: Context, n_layers: int, bnd_old: torch.Tensor, rank_old: tor
         status = torch.empty(1, dtype=torch.int32, device=dev)
     allowed = (1 << G) - 1 if allowed is None else int(allowed)
     _check(lib().dynmo_map_stages(ctx.handle, int(n_layers), bnd_old.numel() - 1, _ptr(bnd_old), _ptr(rank_old),
-                                  n_new, _ptr(bnd_new), _ptr(nbytes), int(G), allowed & 0xFFFFFFFF,
+                                  n_new, _ptr(bnd_new), _ptr(nbytes), int(G), allowed & 0xFFFFFFFF, _ptr(slot_rank),
                                   _ptr(rank_new), _ptr(kept), _ptr(status), _stream(stream)), "dynmo_map_stages")
     return rank_new, kept, status

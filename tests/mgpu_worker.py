@@ -143,6 +143,26 @@ def main():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "graph", rep)
     assert pm.error() == 0
     pm.close()
+    # NEXT-3 placement: the new stages on capacity slots (slot j on GPU
+    # ranks[j]) keeping the most payload in place; the device-driven pull
+    # follows the mapped ranks (a non-identity stage -> rank map)
+    slots = torch.arange(n, dtype=torch.int32, device=dev)
+    rn_t, kept_t, mst = D.map_stages(ctx, shape.L, d_bo, slots, bnd, mem, n, slot_rank=d_ro)
+    torch.cuda.synchronize()
+    ost_m, orn_m, okept_m = oracle.map_stages(shape.L, b_old, np.arange(n), b_new, payload, n, slot_rank=ranks)
+    assert int(mst.item()) == ost_m == 0 and np.array_equal(rn_t.cpu().numpy(), orn_m)
+    assert int(kept_t.item()) == okept_m >= int(payload.sum()) - sum(int(payload[l]) for l, _, _ in moves)
+    moves2 = oracle.moves(shape.L, b_old, ranks, b_new, orn_m)
+    recv2 = {int(l): [torch.zeros(int(payload[l]), dtype=torch.uint8, device=dev)] for l, s_, d_ in moves2 if d_ == rank}
+    pm2 = D.PeerMigrator(ctx, shape.L, send, recv2)
+    pm2.device(d_bo, d_ro, bnd, rn_t, bs, br)
+    torch.cuda.synchronize()
+    assert (int(bs.item()), int(br.item())) == (sum(int(payload[l]) for l, s_, _ in moves2 if s_ == rank),
+                                              sum(int(payload[l]) for l, _, d_ in moves2 if d_ == rank))
+    for l, bufs in recv2.items():
+        assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "mapped")
+    assert pm2.error() == 0
+    pm2.close()
     # Alg. 1 global pruning across ranks (NCCL all-reduce of the histograms,
     # all-gather of the tie counts): every rank's masks == the oracle's on the
     # concatenation of all ranks' shards in rank order; quantised magnitudes

@@ -821,6 +821,20 @@ def test_map_stages_parity(D, ctx):
         assert int(st.item()) == ost, (it, int(st.item()), ost)
         if ost == 0:
             assert np.array_equal(rn.cpu().numpy(), orn) and int(kept.item()) == okept, it
+    # slots (several stages per GPU): slot j on GPU sr[j]
+    for it in range(60):
+        S = int(g.integers(2, 17))
+        sr = np.sort(g.integers(0, int(g.integers(1, S + 1)), S)).astype(np.int32)
+        L = int(g.integers(S, 200))
+        bo = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), S - 1, replace=False)), [L]]).astype(np.int32)
+        ro = np.arange(S, dtype=np.int32)
+        n_new = int(g.integers(1, S + 1))
+        bn = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_new - 1, replace=False)), [L]]).astype(np.int32)
+        nb = g.integers(0, 5, L).astype(np.int64) * 1000
+        rn, kept, st = D.map_stages(ctx, L, _dev(bo), _dev(ro), _dev(bn), _dev(nb), S, slot_rank=_dev(sr))
+        torch.cuda.synchronize()
+        ost, orn, okept = oracle.map_stages(L, bo, ro, bn, nb, S, slot_rank=sr)
+        assert int(st.item()) == ost == 0 and np.array_equal(rn.cpu().numpy(), orn) and int(kept.item()) == okept
     # malformed split and negative bytes: INVALID
     bo, ro, bn = np.array([0, 2, 4], np.int32), np.array([0, 1], np.int32), np.array([0, 3, 3], np.int32)
     rn, kept, st = D.map_stages(ctx, 4, _dev(bo), _dev(ro), _dev(bn), _dev(np.ones(4, np.int64)), 2)

@@ -589,6 +589,26 @@ def test_map_stages_vs_bruteforce():
             if k > best:
                 best, best_pi = k, pi
         assert st == 0 and kept == best and tuple(rn) == best_pi, (G, allowed, list(rn), best_pi)
+    # slots: several stages per GPU (slot j on GPU slot_rank[j]); kept = bytes
+    # whose new slot is on the GPU of their old slot; brute force again
+    for _ in range(200):
+        S = int(g.integers(2, 7))
+        n_gpu = int(g.integers(1, S + 1))
+        sr = np.sort(g.integers(0, n_gpu, S)).astype(np.int32)
+        L = int(g.integers(S, 13))
+        bo = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), S - 1, replace=False)), [L]]).astype(np.int32)
+        ro = np.arange(S, dtype=np.int32)  # old stage s in slot s
+        n_new = int(g.integers(1, S + 1))
+        bn = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_new - 1, replace=False)), [L]]).astype(np.int32)
+        nb = g.integers(0, 4, L).astype(np.int64)
+        st, rn, kept = oracle.map_stages(L, bo, ro, bn, nb, S, slot_rank=sr)
+        owner_gpu = np.repeat(sr[ro], np.diff(bo))
+        best, best_pi = -1, None
+        for pi in itertools.permutations(range(S), n_new):
+            k = sum(int(nb[i]) for s in range(n_new) for i in range(bn[s], bn[s + 1]) if owner_gpu[i] == sr[pi[s]])
+            if k > best:
+                best, best_pi = k, pi
+        assert st == 0 and kept == best and list(rn) == [int(sr[j]) for j in best_pi]
     assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2, 0b01)[0] == oracle.E_INFEASIBLE
     assert oracle.map_stages(4, [0, 2, 5], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2)[0] == oracle.E_INVALID
     assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 17)[0] == oracle.E_INVALID

@@ -1,11 +1,15 @@
+#!/bin/bash
+# Multi-GPU evidence: mgpu_worker (parity) and the bench at 1/2/4 GPUs
+# (identity placement and --map-stages), each run under its own timeout.
 mkdir -p gpurun_out
 N=$(nvidia-smi -L | wc -l); echo "gpus=$N"
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29511 tests/mgpu_worker.py > gpurun_out/mgpu_worker.log 2>&1; echo mgpu_rc=$?
-grep -c MGPU_OK gpurun_out/mgpu_worker.log
-CUDA_VISIBLE_DEVICES=0 timeout 600 python bench.py --steps 200 --warmup 20 --cpu-seconds 12 > gpurun_out/s_n1.json 2> gpurun_out/s_n1.err; echo n1_rc=$?
+CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((N-1))) timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr 127.0.0.1 --master-port 29511 tests/mgpu_worker.py > gpurun_out/mgpu_worker.log 2>&1; echo mgpu_rc=$?
+CUDA_VISIBLE_DEVICES=0 timeout 300 python bench.py > gpurun_out/s_n1.json 2> gpurun_out/s_n1.err; echo n1_rc=$?
 for n in 2 4; do
   [ $n -gt $N ] && continue
-  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2952$n bench.py --gpus $n --steps 200 --warmup 20 > gpurun_out/s_n$n.json 2> gpurun_out/s_n$n.err; echo n${n}_rc=$?
-  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2953$n bench.py --gpus $n --steps 200 --warmup 20 --host-migrate --e2e-steps 3 > gpurun_out/s_n${n}_host.json 2> gpurun_out/s_n${n}_host.err; echo n${n}host_rc=$?
+  for m in "" "--map-stages"; do
+    CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2952$n bench.py --gpus $n $m > gpurun_out/s_n$n$m.json 2> gpurun_out/s_n$n$m.err; echo "n${n}${m}_rc=$?"
+  done
+  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2953$n bench.py --gpus $n --host-migrate --e2e-steps 3 > gpurun_out/s_n${n}_host.json 2> gpurun_out/s_n${n}_host.err; echo n${n}host_rc=$?
 done
-tail -3 gpurun_out/s_n*.err | grep -v OMP | grep -v "\*\*\*"
+for f in gpurun_out/s_n*.json; do python tools/summarize.py $f 2>/dev/null | head -3; done
