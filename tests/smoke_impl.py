@@ -1,7 +1,9 @@
 """One small rebalancing step on cuda:0 through the C-ABI, checked against the
 oracle (used by __graft_entry__.smoke()): pruning masks in three
 representations -> profile_layers -> partition_stages -> diffuse_balance ->
-repack_workers, all compared bit-exactly with oracle/."""
+repack_workers, plus the by-Time source with a device timestamp, global
+pruning (Alg. 1) and the stage -> rank map, all compared bit-exactly with
+oracle/."""
 from __future__ import annotations
 
 import numpy as np
@@ -73,4 +75,43 @@ def run_smoke() -> None:
     torch.cuda.synchronize()
     assert int(r["status"].item()) == rst and int(r["n_new"].item()) == rk
     assert np.array_equal(r["bnd"].cpu().numpy(), rb) and int(r["bottleneck"].item()) == rB
-    print(f"smoke OK: nnz={want_nnz.sum()} B*={oB} b={list(ob)} diffusion rounds={dr} repack n'={rk}")
+
+    # NEXT-1 "by Time": stamps -> time costs (D = 1) == oracle; the stamp kernel runs
+    stamps = synth.time_stamps(np.linspace(1e5, 3e5, shape.L), 2)
+    ds = torch.from_numpy(stamps.reshape(-1)).to(dev)
+    tsegs = [D.SegmentSpec(ds[m * (shape.L + 1) + i:m * (shape.L + 1) + i + 2], L.SRC_TIME_NS, i)
+             for m in range(2) for i in range(shape.L)]
+    tplan = D.ProfilePlan(ctx, tsegs, 0, shape.L)
+    tcost, _, tst = D.profile_layers(ctx, tplan, D.coef_tensor(shape.L, D=1, device=dev))
+    slot = torch.zeros(1, dtype=torch.int64, device=dev)
+    D.timestamp(ctx, slot[0])
+    torch.cuda.synchronize()
+    want_t = [sum(oracle.time_ns(stamps[m, i:i + 2])[1] for m in range(2)) for i in range(shape.L)]
+    assert int(tst.item()) == 0 and np.array_equal(tcost.cpu().numpy(), want_t) and int(slot.item()) > 0
+
+    # NEXT-2 global magnitude pruning (Alg. 1): masks == oracle
+    g = np.random.default_rng(5)
+    wf = g.normal(0, 1, 40000).astype(np.float32)
+    wb = torch.from_numpy(g.normal(0, 2, 33333).astype(np.float32)).to(torch.bfloat16)
+    shards = [torch.from_numpy(wf).to(dev), wb.to(dev)]
+    masks = [torch.empty(x.numel(), dtype=torch.uint8, device=dev) for x in shards]
+    pplan = D.PrunePlan(ctx, list(zip(shards, masks)))
+    k = int(0.1 * (wf.size + wb.numel()))
+    pinfo, pst2 = D.global_prune(ctx, pplan, k)
+    torch.cuda.synchronize()
+    vals = [wf.astype(np.float64), oracle.bf16_to_f64(wb.view(torch.int16).numpy().view(np.uint16))]
+    ost2, om = oracle.global_prune(vals, k)
+    assert int(pst2.item()) == ost2 == 0
+    assert all(np.array_equal(m.cpu().numpy(), o_) for m, o_ in zip(masks, om)), "prune mask mismatch"
+    pplan.close()
+
+    # NEXT-3 migration-minimising stage -> rank map == oracle
+    nb = np.arange(1, shape.L + 1, dtype=np.int64) * 1000
+    rn, kept, mst = D.map_stages(ctx, shape.L, torch.from_numpy(uni).to(dev),
+                                 torch.arange(n, dtype=torch.int32, device=dev), bnd,
+                                 torch.from_numpy(nb).to(dev), n)
+    torch.cuda.synchronize()
+    ost3, orn, okept = oracle.map_stages(shape.L, uni, np.arange(n), ob, nb, n)
+    assert int(mst.item()) == ost3 == 0 and np.array_equal(rn.cpu().numpy(), orn) and int(kept.item()) == okept
+    print(f"smoke OK: nnz={want_nnz.sum()} B*={oB} b={[int(x) for x in ob]} diffusion rounds={dr} "
+          f"repack n'={rk} prune k={k} stage map={[int(x) for x in orn]}")
