@@ -525,7 +525,8 @@ def run_dynmo(args):
     prof_avg = prof_ms / max(prof_n, 1)
     # our kernel nodes per step: k_profile, k_epilogue, [k_unpack(_p2p)], k_partition,
     # k_diffuse, k_repack, [k_mig_signal, k_mig_pull, k_mig_wait | k_signal, k_pull, k_wait]
-    per_step = 5 + (1 if G > 1 else 0) + (3 if (G > 1 and args.migrate == "p2p" and moves_mine) else 0)
+    per_step = (5 + (1 if G > 1 else 0) + (3 if (G > 1 and args.migrate == "p2p" and moves_mine) else 0)
+                + (1 if use_map else 0))  # + k_map_stages
     launches = per_step * args.steps
     mig_ms = phases["migrate"][0] / max(phases["migrate"][1], 1) if phases["migrate"][1] else 0.0
     if dev_mig:
