@@ -7,9 +7,15 @@
  *   2 dynmo_partition_stages contiguous layers->stages min-max partition
  *   3 dynmo_diffuse_balance  the paper's decentralised diffusion variant
  *   4 dynmo_repack_workers   fewest workers within a throughput bound
- *   5 dynmo_migrate_layers   move the layers whose GPU changed (NCCL P2P)
+ *   5 dynmo_migrate_layers   move the layers whose GPU changed (NCCL P2P),
+ *     or _p2p / _dev: receiver pull over NVLink peer memory (host- or
+ *     device-driven; the latter keeps the whole step one graph launch)
+ * Beyond the per-step path:
+ *     DYNMO_SRC_TIME_NS + dynmo_timestamp   "by Time" profiling (NEXT-1)
+ *     dynmo_global_prune                    Alg. 1 global pruning (NEXT-2)
+ *     dynmo_ctx_split, dynmo_map_stages     release GPUs / placement (NEXT-3)
  * Citations: P:Lnnn = PAPER.md line (SPEC:Lnnn = SPEC.md line); readings of
- * ambiguous passages (Q1..Q20) are listed in DESIGN.md.
+ * ambiguous passages (Q1..Q23) are listed in DESIGN.md.
  *
  * Conventions
  *  - Pointers prefixed d_ are DEVICE pointers, h_ are HOST pointers.  The
