@@ -249,3 +249,25 @@ def time_stamps(base_ns: np.ndarray, microbatches: int = 4, jitter: float = 0.05
         out[m, 1:] = t + np.cumsum(dur[m])
         t = int(out[m, -1]) + gap_ns
     return out
+
+
+# ----------------------------------------------------------------------------
+# Dynamic sparse (hash-based) flash attention block masks.
+def sparse_attention_blocks(layer: int, T: int = 2048, block: int = 64, heads: int = 16, batch: int = 2,
+                            seed_key: int = 0) -> np.ndarray:
+    """Bit-packed (little-endian uint32) block masks [batch, heads, nb, nb],
+    nb = T / block, of a hash-based sparse causal attention: query block i
+    and key block j (j <= i) are computed iff their hash buckets match or
+    j == i; the bucket count per layer is drawn from {2, 4, 8, 16}, so the
+    sparsity s_i varies across layers ('varying sparsification across
+    layers')."""
+    nb = T // block
+    g = rng(7, seed_key, layer)
+    buckets = int(g.choice([2, 4, 8, 16]))
+    qh = g.integers(0, buckets, (batch, heads, nb))
+    kh = g.integers(0, buckets, (batch, heads, nb))
+    i = np.arange(nb)[:, None]
+    j = np.arange(nb)[None, :]
+    causal = j <= i
+    m = ((qh[:, :, :, None] == kh[:, :, None, :]) | (i == j)) & causal
+    return pack_bits(m.reshape(-1).astype(np.uint8))

@@ -846,3 +846,32 @@ def test_map_stages_parity(D, ctx):
     assert int(st.item()) == oracle.E_INVALID
     with pytest.raises(D.DynmoError):
         D.map_stages(ctx, 4, _dev(bo), _dev(ro), _dev(bn), _dev(np.ones(4, np.int64)), 17)
+
+
+# ------------------------------- NEXT-4: sparse-attention block masks (a1 source)
+def test_sparse_attention_block_masks(D, L, ctx):
+    """Dynamic sparse flash attention: layer cost s_i c_i =
+    (computed attention blocks) x (cost per block) -- a bit-mask source: the
+    per-layer block counts and B * count costs vs the oracle, then the
+    partition of those costs."""
+    Lyr, n, per_block = 32, 8, 64 * 64 * 64 * 2
+    segs, keep, want = [], [], np.zeros(Lyr, np.int64)
+    for l in range(Lyr):
+        w = synth.sparse_attention_blocks(l)
+        nbits = 2 * 16 * 32 * 32
+        want[l] = oracle.count_bits(w, nbits)
+        t = _dev(w.view(np.int32))
+        keep.append(t)
+        segs.append(D.SegmentSpec(t, L.SRC_MASK_BITS, l, n_elem=nbits))
+    plan = D.ProfilePlan(ctx, segs, 0, Lyr)
+    counters = torch.empty((Lyr, 5), dtype=torch.int64, device=DEV)
+    cost, _, st = D.profile_layers(ctx, plan, D.coef_tensor(Lyr, B=per_block, device=DEV), counters=counters)
+    b = D.Batch([Lyr], [n], device=DEV)
+    bnd, bott, _, pst = D.partition_stages(ctx, b, cost)
+    torch.cuda.synchronize()
+    want_cost = np.array([oracle.layer_cost(nnz=int(v), B=per_block)[1] for v in want])
+    assert int(st.item()) == 0 and np.array_equal(counters[:, 0].cpu().numpy(), want)
+    assert np.array_equal(cost.cpu().numpy(), want_cost)
+    ost, ob, oB, _ = oracle.partition(want_cost, n)
+    assert int(pst.item()) == ost == 0 and np.array_equal(bnd.cpu().numpy()[:n + 1], ob)
+    assert len(set(want.tolist())) > 4  # sparsity really varies across layers

@@ -280,6 +280,39 @@ def map_stages_cfg(ctx):
     return out
 
 
+def sparse_attention(ctx):
+    """NEXT-4: dynamic sparse flash attention, 32 layers / 8
+    stages, hash-based causal block masks (T = 2048, 64-token blocks, 16
+    heads, 2 micro-batches) as bit-mask sources: profile + partition."""
+    Lyr, n, per_block = 32, 8, 64 * 64 * 64 * 2
+    nbits = 2 * 16 * 32 * 32
+    ws = [synth.sparse_attention_blocks(l) for l in range(Lyr)]
+    ts = [dev(w.view(np.int32)) for w in ws]
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, LB.SRC_MASK_BITS, l, n_elem=nbits) for l, t in enumerate(ts)], 0, Lyr)
+    coef = D.coef_tensor(Lyr, B=per_block, device=DEV)
+    cost = torch.empty(Lyr, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    b = D.Batch([Lyr], [n], device=DEV)
+    out = dict(bnd=torch.empty(b.total_bnd, dtype=torch.int32, device=DEV),
+               bottleneck=torch.empty(1, dtype=torch.int64, device=DEV),
+               imbalance=torch.empty(1, dtype=torch.float64, device=DEV),
+               status=torch.empty(1, dtype=torch.int32, device=DEV))
+
+    def step():
+        D.profile_layers(ctx, plan, coef, cost=cost, status=st)
+        D.partition_stages(ctx, b, cost, **out)
+
+    ms, _ = timed(step)
+    want = np.array([oracle.layer_cost(nnz=oracle.count_bits(w, nbits), B=per_block)[1] for w in ws])
+    assert np.array_equal(cost.cpu().numpy(), want)
+    ost, ob, oB, _ = oracle.partition(want, n)
+    assert np.array_equal(out["bnd"].cpu().numpy()[:n + 1], ob)
+    x_old = np.add.reduceat(want, np.arange(0, Lyr, Lyr // n))
+    return dict(layers=Lyr, step_device_ms=round(ms, 4), b_new=[int(x) for x in ob],
+                imbalance_uniform=round(float(oracle.imbalance(x_old)), 4),
+                imbalance_new=round(float(out["imbalance"].item()), 4))
+
+
 def main():
     global flush
     torch.cuda.set_device(0)
@@ -289,7 +322,8 @@ def main():
     for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
                      ("config4_auxloss", lambda: config4(ctx, 4.0)), ("config4_sbase", lambda: config4(ctx, 64.0)),
                      ("config5", lambda: config5(ctx)), ("bytime_cfg2", lambda: config_bytime(ctx)),
-                     ("map_stages", lambda: map_stages_cfg(ctx))]:
+                     ("map_stages", lambda: map_stages_cfg(ctx)),
+                     ("sparse_attention", lambda: sparse_attention(ctx))]:
         res[name] = fn()
         print(name, json.dumps(res[name]), flush=True)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
