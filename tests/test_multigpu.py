@@ -1,5 +1,6 @@
 """Multi-GPU parity through torchrun (real NCCL over NVLink): needs >= 2 GPUs."""
 import os
+import re
 import subprocess
 import sys
 
@@ -20,5 +21,6 @@ def test_exchange_and_migration(world):
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    ok = [l for l in r.stdout.splitlines() if l.startswith("MGPU_OK")]
-    assert r.returncode == 0 and len(ok) == world, r.stdout[-3000:] + r.stderr[-3000:]
+    # ranks print concurrently, so lines can interleave: collect the rank ids
+    ok = {int(x) for x in re.findall(r"MGPU_OK (\d+)", r.stdout)}
+    assert r.returncode == 0 and ok == set(range(world)), r.stdout[-3000:] + r.stderr[-3000:]
