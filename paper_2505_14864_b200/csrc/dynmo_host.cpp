@@ -241,6 +241,7 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
     *out = nullptr;
     if (nranks < 1 || rank < 0 || rank >= nranks || device < 0) return invalid("bad rank/device");
     if (nranks > 1 && !h_nccl_id) return invalid("nranks > 1 needs a NCCL unique id");
+    if (nranks > kMaxRanks) return invalid("nranks > 16");
     DeviceGuard g(device);
     CUDA_TRY(cudaSetDevice(device), "cudaSetDevice");
     auto *c = new dynmo_ctx_s();
@@ -255,16 +256,13 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
         return cuda_fail(cudaGetLastError(), "ctx workspace");
     }
     if (nranks > 1) {
-        if (nranks > kMaxRanks) {
-            delete c;
-            return invalid("nranks > 16");
-        }
         ncclUniqueId id;
         memcpy(id.internal, h_nccl_id, 128);
         ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
         if (r != ncclSuccess) {
             g_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
-            delete c;
+            c->comm = nullptr;
+            dynmo_ctx_destroy(c);  // frees the workspace
             return DYNMO_E_NCCL;
         }
         const dynmo_status st = setup_peer_window(c);
