@@ -875,3 +875,39 @@ def test_sparse_attention_block_masks(D, L, ctx):
     ost, ob, oB, _ = oracle.partition(want_cost, n)
     assert int(pst.item()) == ost == 0 and np.array_equal(bnd.cpu().numpy()[:n + 1], ob)
     assert len(set(want.tolist())) > 4  # sparsity really varies across layers
+
+
+def test_ctx_barrier_timing_detach_and_split_single(D, L, ctx):
+    """dynmo_ctx_barrier is a no-op for one rank and capturable; timing_detach
+    stops polling earlier graphs' events (their graphs stay valid); a split
+    of a one-rank ctx gives a usable ctx (color >= 0) or None (color < 0)."""
+    x = torch.zeros(1, device=DEV)
+    g = torch.cuda.CUDAGraph()
+    ctx.set_timing(True, phases=["profile"])
+    seg = D.SegmentSpec(_dev(np.ones(4096, np.uint8)), L.SRC_MASK_U8, 0)
+    plan = D.ProfilePlan(ctx, [seg], 0, 1)
+    coef = D.coef_tensor(1, B=1, device=DEV)
+    D.profile_layers(ctx, plan, coef)  # warm
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g):
+        ctx.barrier()
+        D.profile_layers(ctx, plan, coef)
+        x.add_(1)
+    g.replay()
+    torch.cuda.synchronize()
+    ctx.timing_poll()
+    n1 = ctx.timing_read()["profile"][1]
+    ctx.timing_detach()
+    g.replay()
+    torch.cuda.synchronize()
+    ctx.timing_poll()
+    assert n1 >= 1 and ctx.timing_read()["profile"][1] == 0 and float(x.item()) == 2.0
+    ctx.set_timing(False)
+    sub = ctx.split(active=True)
+    assert sub is not None and sub.nranks == 1 and sub.rank == 0
+    cost, _, st = D.profile_layers(sub, D.ProfilePlan(sub, [seg], 0, 1), coef)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0 and int(cost[0].item()) == 4096
+    sub.close()
+    assert ctx.split(active=False) is None
+    del g

@@ -3,6 +3,7 @@
 // (ld.global.nc.L1::no_allocate.L2::256B.v4), several grid shapes / loads in
 // flight.  nvcc -O3 -gencode arch=compute_100a,code=sm_100a hbm_read.cu -o hbm_read
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
@@ -73,8 +74,8 @@ __global__ void rd_tiles(const uint4 *__restrict__ p, size_t n, unsigned *out) {
     if (acc == 0xFFFFFFFFu) *out = acc;
 }
 
-int main() {
-    const size_t bytes = 603979776ull, n = bytes / 16;
+int main(int argc, char **argv) {
+    const size_t bytes = argc > 1 ? (size_t)atoll(argv[1]) : 603979776ull, n = bytes / 16;
     uint4 *p; unsigned *o; char *fl;
     cudaMalloc(&p, bytes); cudaMalloc(&o, 4); cudaMalloc(&fl, 256u << 20);
     cudaMemset(p, 0x5a, bytes);
