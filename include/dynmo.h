@@ -445,9 +445,10 @@ dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, co
  * top-k, gather, global top-k, scatter); equal magnitudes are kept in the
  * global order (rank, then segment order, then element index; SPEC
  * S:L175-184).  Same kept set as the paper's gather/scatter, found by an
- * exact distributed radix select on magnitude keys: 2 (all bf16) or 3
- * HBM-streaming histogram passes over this rank's weights with an NCCL
- * all-reduce of 2049 counters per pass, then one mask-writing pass. */
+ * exact distributed radix select on magnitude keys: 1 (all bf16: the 15-bit
+ * first digit is the whole magnitude) or 3 HBM-streaming histogram passes
+ * over this rank's weights with an NCCL all-reduce of the counters per pass
+ * (32769 after the first), then one mask-writing pass. */
 enum { DYNMO_W_F32 = 0, DYNMO_W_BF16 = 1 };
 
 typedef struct dynmo_prune_segment {

@@ -707,7 +707,7 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     }
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t nt = std::max<size_t>(1, tiles.size());
-    const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 2049);
+    const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 32769);
     const size_t sz_sel = up(sizeof(PruneSel)), sz_tie = up(sizeof(long long) * std::max(1, ctx->nranks));
     // tie counts / offsets per (tile, warp range of the mask pass)
     const size_t sz_tt = up(sizeof(uint32_t) * nt * 8), sz_to = up(sizeof(unsigned long long) * nt * 8);
@@ -733,7 +733,7 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     a.n_tiles = (int64_t)tiles.size();
     a.rank = ctx->rank;
     a.nranks = ctx->nranks;
-    a.last_pass = any_f32 ? 2 : 1;  // bf16 keys have 16 zero low bits: 2 digits suffice
+    a.last_pass = any_f32 ? 2 : 0;  // bf16 keys have 16 zero low bits: the 15-bit first digit is exact
     bool ok = cudaMemset(pl->dmem, 0, total) == cudaSuccess;
     if (ok && !tiles.empty())
         ok = cudaMemcpy((void *)a.tiles, tiles.data(), sizeof(PruneTile) * tiles.size(), cudaMemcpyHostToDevice) ==
@@ -771,7 +771,7 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
     for (int pass = 0; pass <= a.last_pass; ++pass) {
         CUDA_TRY(launch_prune(a, pass, plan->grid[pass], s), "k_prune_hist");
         if (multi) {
-            const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, 2049, ncclUint64, ncclSum, ctx->comm, s);
+            const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, 32769, ncclUint64, ncclSum, ctx->comm, s);
             if (r != ncclSuccess) {
                 g_err = std::string("ncclAllReduce (prune): ") + ncclGetErrorString(r);
                 return DYNMO_E_NCCL;

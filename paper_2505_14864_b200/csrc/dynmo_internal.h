@@ -173,8 +173,8 @@ struct PruneSel {  // device-side selection state of one call
 struct PruneArgs {
     const PruneTile *tiles;
     int64_t n_tiles;
-    unsigned long long *hist_local;   // [2049] (bin 2048: NaN count)
-    unsigned long long *hist_global;  // [2049] all-reduced (nranks > 1)
+    unsigned long long *hist_local;   // [32769] (bin 32768: NaN count)
+    unsigned long long *hist_global;  // [32769] all-reduced (nranks > 1)
     PruneSel *sel;
     const long long *tie_all;         // [nranks] all-gathered tie counts
     uint32_t *tile_ties;              // [n_tiles]

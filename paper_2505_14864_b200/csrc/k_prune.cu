@@ -6,12 +6,12 @@
 //   key(w) = bits(|w|) for f32; bits(|bf16|) << 16 for bf16 (the f32 key of
 //   the same value), so segments of both types share one ordered key space
 //   (monotone in |w| for non-NaN values; +0 and -0 both key 0).
-//   pass 0: histogram of key >> 20      (2048 bins)  -> all-reduce -> bin
-//   pass 1: histogram of key >> 10 & 1023 among keys with that prefix
-//   pass 2: histogram of key & 1023 among keys with the 21-bit prefix
-//           (skipped when every segment is bf16: its low 16 key bits are 0)
+//   pass 0: histogram of key >> 16      (32768 bins) -> all-reduce -> bin
+//           (for bf16 the whole 15-bit magnitude: an all-bf16 plan is done)
+//   pass 1: histogram of key >> 6 & 1023 among keys with that prefix
+//   pass 2: histogram of key & 63 among keys with the 25-bit prefix
 // Each pass streams the rank's weights (HBM-bound); only the histograms cross
-// GPUs (NCCL all-reduce, 16 KB).  The threshold tau is the k-th largest key;
+// GPUs (NCCL all-reduce, 256 KB).  The threshold tau is the k-th largest key;
 // keys > tau are kept, and of the keys == tau the first `need` in the global
 // order (rank, then segment order, then index -- SPEC S:L184) are kept:
 // per-rank tie counts are all-gathered, and only the rank whose share of the
@@ -23,8 +23,9 @@ namespace dynmo {
 namespace {
 
 constexpr int kPruneThreads = 256;
-constexpr int kBins0 = 2048;  // pass 0 digit: key bits 30..20 (11 bits)
-constexpr int kBins1 = 1024;  // pass 1/2 digits: 10 bits
+constexpr int kBins0 = 32768;  // pass 0 digit: key bits 30..16 (15 bits = a bf16 magnitude)
+constexpr int kBins1 = 1024;   // pass 1 digit: key bits 15..6; pass 2: bits 5..0 (64 of the bins)
+constexpr int kHist0Threads = 1024;  // pass 0: one 128 KB shared histogram per block, one block per SM
 constexpr uint32_t kNanKey = 0x7F800000u;  // key > this: NaN
 constexpr int kPruneWarps = kPruneThreads / 32;  // tie-offset entries per tile
 constexpr int kU = 8;  // 16-byte loads in flight per thread in the streaming passes
@@ -46,16 +47,17 @@ __device__ __forceinline__ void for_keys(const PruneTile &t, F &&f) {
     const uint4 *v = (const uint4 *)t.w;
     const bool bf = t.dtype == DYNMO_W_BF16;
     const uint32_t nv = bf ? t.n >> 3 : t.n >> 2;
-    for (uint32_t b = threadIdx.x; b < nv; b += kU * kPruneThreads) {
+    const uint32_t T = blockDim.x;
+    for (uint32_t b = threadIdx.x; b < nv; b += kU * T) {
         uint4 x[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            const uint32_t i = b + u * kPruneThreads;
+            const uint32_t i = b + u * T;
             x[u] = i < nv ? ld_nc(v + i) : make_uint4(0u, 0u, 0u, 0u);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            if (b + u * kPruneThreads >= nv) break;
+            if (b + u * T >= nv) break;
             const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
             if (bf) {
 #pragma unroll
@@ -71,31 +73,26 @@ __device__ __forceinline__ void for_keys(const PruneTile &t, F &&f) {
     }
     if (bf) {
         const uint16_t *s = (const uint16_t *)t.w;
-        for (uint32_t i = (nv << 3) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_bf16(s[i]));
+        for (uint32_t i = (nv << 3) + threadIdx.x; i < t.n; i += T) f(key_bf16(s[i]));
     } else {
         const uint32_t *s = (const uint32_t *)t.w;
-        for (uint32_t i = (nv << 2) + threadIdx.x; i < t.n; i += kPruneThreads) f(key_f32(s[i]));
+        for (uint32_t i = (nv << 2) + threadIdx.x; i < t.n; i += T) f(key_f32(s[i]));
     }
 }
 
-// Shared sub-histograms, one per warp pair (less same-address contention;
-// 4 x 2048 x 4 B = 32 KB fits the static limit), flushed as ONE global atomic
-// per nonzero bin per block.  hist[NB] counts NaN keys (pass 0).
-template <int PASS>
-__global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
+// Pass 0: the 15-bit digit key >> 16 (for bf16 the whole magnitude, so an
+// all-bf16 plan needs this one pass only): one 128 KB shared histogram per
+// 1024-thread block, one block per SM, flushed as one global atomic per
+// nonzero bin per block.  hist[kBins0] counts NaN keys.
+__global__ void __launch_bounds__(kHist0Threads) k_prune_hist0(PruneArgs a) {
     pdl_wait();
     pdl_trigger();
-    constexpr int NB = PASS == 0 ? kBins0 : kBins1;
-    constexpr int W = kPruneThreads / 64;
-    __shared__ uint32_t sh[W][NB];
+    extern __shared__ uint32_t sh0[];  // [kBins0]
     __shared__ uint32_t s_nan;
-    for (int i = threadIdx.x; i < W * NB; i += kPruneThreads) (&sh[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < kBins0; i += kHist0Threads) sh0[i] = 0u;
     if (threadIdx.x == 0) s_nan = 0u;
     __syncthreads();
-    const PruneSel *sel = a.sel;
-    if (sel->done) return;  // k = 0, invalid k, or tau already found
-    const uint32_t prefix = sel->prefix;
-    uint32_t *my = sh[threadIdx.x >> 6];
+    if (a.sel->done) return;  // k = 0 or invalid k
     uint32_t nan = 0;
     PruneTile nxt;
     if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
@@ -103,18 +100,48 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
         const PruneTile t = nxt;
         if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];  // prefetch the next descriptor
         for_keys(t, [&](uint32_t k) {
-            if constexpr (PASS == 0) {
-                if (k > kNanKey) ++nan;
-                else atomicAdd(&my[k >> 20], 1u);
-            } else if constexpr (PASS == 1) {
-                if (k <= kNanKey && (k >> 20) == prefix) atomicAdd(&my[(k >> 10) & 1023u], 1u);
+            if (k > kNanKey) ++nan;
+            else atomicAdd(&sh0[k >> 16], 1u);
+        });
+    }
+    if (nan) atomicAdd(&s_nan, nan);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins0; b += kHist0Threads) {
+        const uint32_t c = sh0[b];
+        if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
+    }
+    if (threadIdx.x == 0 && s_nan) atomicAdd(&a.hist_local[kBins0], (unsigned long long)s_nan);
+}
+
+// Passes 1 / 2 (f32 keys only): among the keys carrying the selected prefix
+// (rare), histogram of key bits 15..6 / 5..0; shared sub-histograms, one
+// per warp pair.
+template <int PASS>
+__global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NB = kBins1;
+    constexpr int W = kPruneThreads / 64;
+    __shared__ uint32_t sh[W][NB];
+    for (int i = threadIdx.x; i < W * NB; i += kPruneThreads) (&sh[0][0])[i] = 0u;
+    __syncthreads();
+    const PruneSel *sel = a.sel;
+    if (sel->done) return;  // k = 0, invalid k, or tau already found
+    const uint32_t prefix = sel->prefix;
+    uint32_t *my = sh[threadIdx.x >> 6];
+    PruneTile nxt;
+    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
+    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+        const PruneTile t = nxt;
+        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];
+        for_keys(t, [&](uint32_t k) {
+            if constexpr (PASS == 1) {
+                if (k <= kNanKey && (k >> 16) == prefix) atomicAdd(&my[(k >> 6) & 1023u], 1u);
             } else {
-                if (k <= kNanKey && (k >> 10) == prefix) atomicAdd(&my[k & 1023u], 1u);
+                if (k <= kNanKey && (k >> 6) == prefix) atomicAdd(&my[k & 63u], 1u);
             }
         });
     }
-    if constexpr (PASS == 0)
-        if (nan) atomicAdd(&s_nan, nan);
     __syncthreads();
     for (int b = threadIdx.x; b < NB; b += kPruneThreads) {
         uint32_t c = 0;
@@ -122,7 +149,6 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
         for (int w = 0; w < W; ++w) c += sh[w][b];
         if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
     }
-    if (PASS == 0 && threadIdx.x == 0 && s_nan) atomicAdd(&a.hist_local[kBins0], (unsigned long long)s_nan);
 }
 
 // One block: locate the bin of the k_rem-th largest key in the (global)
@@ -175,18 +201,28 @@ __global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
         if (above_thread < (unsigned long long)krem && s_part[tid] >= (unsigned long long)krem) {
             unsigned long long acc = above_thread;
             int b = tid * PER + PER - 1;
-            for (int j = PER - 1; j >= 0; --j) {
-                const unsigned long long c = h[tid * PER + j];
-                if (acc + c >= (unsigned long long)krem) {
-                    b = tid * PER + j;
-                    break;
+            bool found = false;
+            // this thread's bins from the top, 8 independent loads at a time
+            for (int j0 = PER - 1; j0 >= 0 && !found; j0 -= 8) {
+                unsigned long long c[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) c[q] = j0 - q >= 0 ? h[tid * PER + j0 - q] : 0ull;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (found || j0 - q < 0) continue;
+                    if (acc + c[q] >= (unsigned long long)krem) {
+                        b = tid * PER + j0 - q;
+                        found = true;
+                    } else {
+                        acc += c[q];
+                    }
                 }
-                acc += c;
             }
             s_bin = b;
             sel->k_rem = krem - (long long)acc;
             sel->above += (long long)acc;
-            sel->prefix = PASS == 0 ? (uint32_t)b : ((sel->prefix << 10) | (uint32_t)b);
+            sel->prefix = PASS == 0 ? (uint32_t)b
+                        : PASS == 1 ? ((sel->prefix << 10) | (uint32_t)b) : ((sel->prefix << 6) | (uint32_t)b);
             // this rank's keys in the chosen bin (the ties, after the last pass)
             sel->tie_local = (long long)a.hist_local[b];
         }
@@ -212,7 +248,8 @@ __global__ void k_prune_ties(PruneArgs a) {
         sel->tau = 0xFFFFFFFFu;
         return;
     }
-    sel->tau = a.last_pass == 1 ? (sel->prefix << 10) : sel->prefix;
+    // tau from the digits: 15 bits (bf16-only plans) or 15 + 10 + 6 = 31 bits
+    sel->tau = a.last_pass == 0 ? (sel->prefix << 16) : sel->prefix;
     long long before = 0;
     for (int r = 0; r < a.rank; ++r) before += a.nranks > 1 ? a.tie_all[r] : 0;
     const long long need = sel->k_rem;  // ties to keep globally (>= 1)
@@ -553,7 +590,10 @@ __global__ void k_prune_begin(PruneSel *sel, long long k) {
 int prune_blocks_per_sm(int kind) {
     int nb = 1;
     switch (kind) {
-        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<0>, kPruneThreads, 0); break;
+        case 0:
+            cudaFuncSetAttribute(k_prune_hist0, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins0 * 4);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist0, kHist0Threads, kBins0 * 4);
+            break;
         case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<1>, kPruneThreads, 0); break;
         case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<2>, kPruneThreads, 0); break;
         case 21: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_tiecount, kPruneThreads, 0); break;
@@ -564,7 +604,7 @@ int prune_blocks_per_sm(int kind) {
 
 cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s) {
     switch (pass_kind) {
-        case 0: return launch_pdl(k_prune_hist<0>, grid, kPruneThreads, 0, s, a);
+        case 0: return launch_pdl(k_prune_hist0, grid, kHist0Threads, (size_t)kBins0 * 4, s, a);
         case 1: return launch_pdl(k_prune_hist<1>, grid, kPruneThreads, 0, s, a);
         case 2: return launch_pdl(k_prune_hist<2>, grid, kPruneThreads, 0, s, a);
         case 10: return launch_pdl(k_prune_select<0>, 1, 1024, 0, s, a);
