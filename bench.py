@@ -274,9 +274,9 @@ def run_reference(args):
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
            "data": "synthetic", "config": workload_config(args.gpus),
-           "cpu_baseline": {"value": round(ms, 4), "unit": "ms/step", "cores": cpu_threads_used(),
+           "cpu_baseline": {"value": round(ms, 4), "unit": "ms", "cores": cpu_threads_used(),
                             "kind": "oracle", "sample": sample},
-           "e2e": {"value": round(ms, 4), "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "e2e": {"value": round(ms, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
 
