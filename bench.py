@@ -658,7 +658,7 @@ def run_dynmo(args):
                 c_s.append(c)
                 s_s.append(s)
             ob = 1e3 * (np.mean(c_s) + np.mean(s_s))
-            out["cpu_baseline"] = {"value": round(float(ob), 3), "unit": "ms/step", "cores": cpu_threads_used(),
+            out["cpu_baseline"] = {"value": round(float(ob), 3), "unit": "ms", "cores": cpu_threads_used(),
                                    "kind": "oracle",
                                    "sample": f"{len(c_s)} full config-2 oracle steps (all 48 layers' u8 masks, "
                                              f"every solver), 1 thread; host has {os.cpu_count()} cores"}
