@@ -4,9 +4,9 @@ over G ranks by pipeline stage (8 stages, stage s on GPU floor(s*G/8)), S = 0.9
 (k = 10 % of all weights).  One call = dynmo_global_prune over this rank's
 layers (histogram passes + NCCL all-reduces + mask pass), captured in a CUDA
 graph, timed with CUDA events; max over ranks.  Algorithmic HBM bytes per
-rank and call: (passes + 1) x weight bytes (reads) + 1 B per weight (mask
-writes) [+ one more read of the weights when a rank holds a partial share of
-the threshold ties].
+rank and call: (1 histogram pass + 1 mask pass) x weight bytes (reads) + 1 B
+per weight (mask writes) [+ one more read of the weights when a rank holds a
+partial share of the threshold ties].
 
 python tools/bench_prune.py  |  torchrun --nproc-per-node G ... tools/bench_prune.py
 """
@@ -92,7 +92,7 @@ def main():
     kept_local = sum(int(m.sum(dtype=torch.int64).item()) for m in ms)
     partial = 0 < inf[3] < inf[4]
     wbytes = count * P * 2
-    passes = 2  # all bf16
+    passes = 1  # all bf16: the 15-bit first digit is the whole magnitude
     alg_bytes = (passes + 1 + (1 if partial else 0)) * wbytes + count * P
     v = torch.tensor([float(np.median(ts)), float(alg_bytes), float(kept_local)], dtype=torch.float64, device=dev)
     if G > 1:

@@ -13,3 +13,10 @@ for n in 2 4; do
   CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2953$n bench.py --gpus $n --host-migrate --e2e-steps 3 > gpurun_out/s_n${n}_host.json 2> gpurun_out/s_n${n}_host.err; echo n${n}host_rc=$?
 done
 for f in gpurun_out/s_n*.json; do python tools/summarize.py $f 2>/dev/null | head -3; done
+# Alg. 1 global pruning at 1..N GPUs
+CUDA_VISIBLE_DEVICES=0 timeout 200 python tools/bench_prune.py > gpurun_out/prune_n1.json 2>/dev/null; echo prune1_rc=$?
+for n in 2 4; do
+  [ $n -gt $N ] && continue
+  CUDA_VISIBLE_DEVICES=$(seq -s, 0 $((n-1))) timeout 200 python -m torch.distributed.run --nnodes=1 --nproc-per-node=$n --master-addr 127.0.0.1 --master-port 2954$n tools/bench_prune.py 2>/dev/null | grep "{" > gpurun_out/prune_n$n.json; echo prune${n}_rc=$?
+done
+cat gpurun_out/prune_n*.json
