@@ -163,6 +163,39 @@ def main():
         assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "mapped")
     assert pm2.error() == 0
     pm2.close()
+    # several buffers per layer (a CSR payload is values, indices and
+    # optimizer state): 3 buffers of different sizes and dtypes per layer,
+    # through NCCL send/recv, the host-driven and the device-driven pull
+    def bufs_of(l):
+        nb_ = int(payload[l])
+        return [pattern(l, nb_), pattern(l + 100, nb_ // 3 + 1).view(torch.uint8),
+                torch.from_numpy(np.arange(nb_ // 7 + 1, dtype=np.int32) * (l + 1))]
+    send3 = {l: [t.to(dev) for t in bufs_of(l)] for l in range(begin, begin + count)}
+    recv3 = {int(l): [torch.zeros_like(t, device=dev) for t in bufs_of(int(l))] for l, s_, d_ in moves if d_ == rank}
+    want3_s = sum(sum(t.numel() * t.element_size() for t in bufs_of(int(l))) for l, s_, d_ in moves if s_ == rank)
+    want3_r = sum(sum(t.numel() * t.element_size() for t in bufs_of(int(l))) for l, s_, d_ in moves if d_ == rank)
+    for mode in ("nccl", "p2p", "dev"):
+        for bufs in recv3.values():
+            for t in bufs:
+                t.zero_()
+        if mode == "nccl":
+            s3, r3 = D.migrate_layers(ctx, shape.L, b_old, ranks, b_new, ranks, send3, recv3, n_bufs=3)
+        else:
+            pm3 = D.PeerMigrator(ctx, shape.L, send3, recv3, n_bufs=3)
+            if mode == "p2p":
+                s3, r3 = pm3(b_old, ranks, b_new, ranks)
+            else:
+                pm3.device(d_bo, d_ro, bnd, d_ro, bs, br)
+        torch.cuda.synchronize()
+        if mode == "dev":
+            s3, r3 = int(bs.item()), int(br.item())
+            assert pm3.error() == 0
+        if mode != "nccl":
+            pm3.close()
+        assert (s3, r3) == (want3_s, want3_r), (rank, mode, s3, r3, want3_s, want3_r)
+        for l, bufs in recv3.items():
+            for t, w in zip(bufs, bufs_of(l)):
+                assert torch.equal(t.cpu(), w), (rank, mode, l)
     # Alg. 1 global pruning across ranks (NCCL all-reduce of the histograms,
     # all-gather of the tie counts): every rank's masks == the oracle's on the
     # concatenation of all ranks' shards in rank order; quantised magnitudes
