@@ -638,7 +638,12 @@ def run_dynmo(args):
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
                         "max_bytes_recv_per_gpu": int(max_recv), "avg_ms": round(mig_ms, 5),
                         "nvlink_GBps": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9, 1)
-                        if mig_ms > 0 else None, "nvlink_peak_GBps": NVLINK_PEER_GBS},
+                        if mig_ms > 0 else None, "nvlink_peak_GBps": NVLINK_PEER_GBS,
+                        "nvlink_nominal_GBps": 900.0,
+                        "frac_of_nominal": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9 / 900.0, 3)
+                        if mig_ms > 0 else None,
+                        "path": ("NCCL send/recv" if args.migrate == "nccl" else "NVLink peer-memory pull")
+                        if G > 1 else None},
             "solution": {"b_old": b_old.tolist(), "b_new": b_new.tolist(),
                          "bottleneck_old": int(x_old.max()), "bottleneck_new": int(part["bott"].item()),
                          "imbalance_old": round(dl(x_old), 4), "imbalance_new": round(float(part["imb"].item()), 4),
