@@ -162,6 +162,32 @@ def config4(ctx, alpha):
                 imbalance=round(float(pout["imbalance"].item()), 4))
 
 
+def _oracle_cfg5_chunk(idx):
+    """Oracle work of config-5 instances idx (token counts, partition,
+    BOUND repack) -- run in worker processes for the all-cores timing."""
+    import oracle as o
+    import synth as sy
+    for q in idx:
+        x = sy.cfg5_instance(q)
+        c = np.array([o.count_bits(x.masks[l], 4096) for l in range(x.L)])
+        o.partition(c, x.n, mem=x.mem, cap=x.cap)
+        o.repack_bound(c, x.n, x.bound, 1, mem=x.mem, cap=x.cap)
+    return len(idx)
+
+
+def host_info():
+    import platform
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return dict(cpu_count=os.cpu_count(), affinity=len(os.sched_getaffinity(0)), cpu_model=model or platform.processor())
+
+
 def config5(ctx, n_inst=4096):
     insts = [synth.cfg5_instance(i) for i in range(n_inst)]
     masks = np.concatenate([x.masks.reshape(-1) for x in insts])
@@ -208,7 +234,21 @@ def config5(ctx, n_inst=4096):
         ost, ob, oB, _ = oracle.partition(c, x.n, mem=x.mem, cap=x.cap)
         assert np.array_equal(bn[q][:x.n + 1], ob)
         assert kn[q] == oracle.repack_bound(c, x.n, x.bound, 1, mem=x.mem, cap=x.cap)[1]
+    # the oracle on config 5: one core (a 256-instance sample, scaled) and all
+    # host cores (a process pool over all 4096 instances), SURVEY 8(d)
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    _oracle_cfg5_chunk(range(256))
+    one_core_ms = (time.perf_counter() - t0) * 1e3 * n_inst / 256
+    ncores = len(os.sched_getaffinity(0))
+    chunks = [list(range(i, n_inst, ncores * 4)) for i in range(ncores * 4)]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(ncores) as pool:
+        assert sum(pool.map(_oracle_cfg5_chunk, chunks)) == n_inst
+    all_cores_ms = (time.perf_counter() - t0) * 1e3
     return dict(instances=n_inst, layers=layer, profile_bytes=int(plan.bytes), step_device_ms=round(ms, 4),
+                oracle_ms_1core_est=round(one_core_ms, 1), oracle_ms_all_cores=round(all_cores_ms, 1),
+                oracle_cores=ncores,
                 instances_per_s=round(n_inst / (ms * 1e-3)), profile_device_ms=round(pms, 4),
                 profile_GBps=round(plan.bytes / (pms * 1e-3) / 1e9, 1),
                 mean_workers_after_repack=round(float(kn.mean()), 3),
@@ -318,7 +358,7 @@ def main():
     torch.cuda.set_device(0)
     flush = bench.L2Flush(DEV)
     ctx = D.Context(0)
-    res = {}
+    res = {"host": host_info()}
     for name, fn in [("config1", lambda: config1(ctx)), ("config3", lambda: config3(ctx)),
                      ("config4_auxloss", lambda: config4(ctx, 4.0)), ("config4_sbase", lambda: config4(ctx, 64.0)),
                      ("config5", lambda: config5(ctx)), ("bytime_cfg2", lambda: config_bytime(ctx)),
