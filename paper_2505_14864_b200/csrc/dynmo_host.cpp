@@ -616,7 +616,7 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     }
     if (exchange == 1) {
         // collective: the receive slot area of every rank, mapped by every peer
-        const size_t bytes = sizeof(int64_t) * 2 * ctx->nranks * pl->slot_elems;
+        const size_t bytes = sizeof(int64_t) * 2 * ctx->nranks * pl->slot_elems * 2;  // LL: 2 words per value
         dynmo_status st = DYNMO_OK;
         if (cudaMalloc((void **)&pl->d_p2p_slots, bytes) != cudaSuccess ||
             cudaMemset(pl->d_p2p_slots, 0, bytes) != cudaSuccess)
@@ -844,7 +844,7 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     phase_end(te, s);
     if (plan->exchange == 1) {
         te = phase_begin(ctx, DYNMO_PHASE_EXCHANGE, s);
-        CUDA_TRY(launch_unpack_p2p(plan->d_p2p_slots, ctx->d_win, ctx->nranks, plan->n_total, d_cost, d_mem,
+        CUDA_TRY(launch_unpack_p2p(plan->d_p2p_slots, ctx->d_win, ctx->nranks, plan->n_total, plan->d_slot_recv, d_cost, d_mem,
                                    d_status, s),
                  "k_unpack_p2p launch");
         phase_end(te, s);

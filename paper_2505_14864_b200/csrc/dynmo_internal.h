@@ -120,7 +120,10 @@ constexpr int kMaxRanksEpi = 16;
 struct EpiArgs {
     int32_t layer_begin, n_local, n_total, exchange, max_E;
     // exchange over peer memory (exchange == 1): every rank's slot area is
-    // int64 [2 parity][nranks][3 + 2 n_total], mapped by every peer
+    // LL words uint64 [2 parity][nranks][2 (3 + 2 n_total)]: every int64 of
+    // the slot {layer_begin, n_local, status, cost[n_total], mem[n_total]} as
+    // two 8-byte words {32 data bits, 32-bit epoch} (flag in the data: no
+    // fence or flag release needed), mapped by every peer
     int32_t p2p, rank, nranks;
     int64_t *peer_slots[kMaxRanksEpi];
     PeerWindow *win;                      // local window (exch_epoch counter)
@@ -209,7 +212,8 @@ cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_to
 // peer-memory exchange: waits for every rank's flag of this epoch, then
 // unpacks the local slot area (parity of the epoch)
 cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
-                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out, cudaStream_t s);
+                              int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
+                              cudaStream_t s);
 
 // ------------------------------------------------------------------ solvers
 struct SolveArgs {

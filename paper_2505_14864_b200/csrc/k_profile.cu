@@ -450,13 +450,36 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
 
 // -------------------------------------------------------------- epilogue
 __device__ __forceinline__ int worse(int a, int b) { return a < b ? a : b; }
-__device__ __forceinline__ void st_release_sys(uint64_t *p, uint64_t v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// LL ("flag in the data") words of the peer-memory exchange: an int64 as two
+// 8-byte words {32 data bits, low 32 bits of the call epoch}.  An aligned
+// 8-byte store is single-copy atomic, so a word read with the current epoch
+// holds this call's data -- no fence or separate flag release is needed.
+__device__ __forceinline__ void st_relaxed_sys(uint64_t *p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t *p) {
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t *p) {
     uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void ll_store(int64_t *p, int64_t v, uint64_t epoch) {
+    const uint64_t e = (uint64_t)(uint32_t)epoch << 32;
+    st_relaxed_sys((uint64_t *)p, e | (uint32_t)(uint64_t)v);
+    st_relaxed_sys((uint64_t *)p + 1, e | (uint32_t)((uint64_t)v >> 32));
+}
+// Spins until both words carry `epoch` (false after 10 s from t0).
+__device__ __forceinline__ bool ll_poll(const uint64_t *p, uint64_t epoch, uint64_t t0, int64_t &v) {
+    const uint32_t e = (uint32_t)epoch;
+    for (;;) {
+        const uint64_t w0 = ld_relaxed_sys(p), w1 = ld_relaxed_sys(p + 1);
+        if ((uint32_t)(w0 >> 32) == e && (uint32_t)(w1 >> 32) == e) {
+            v = (int64_t)(((uint64_t)(uint32_t)w1 << 32) | (uint32_t)w0);
+            return true;
+        }
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > 10ull * 1000 * 1000 * 1000) return false;
+    }
 }
 
 __global__ void k_epilogue(EpiArgs a) {
@@ -537,13 +560,14 @@ __global__ void k_epilogue(EpiArgs a) {
             o[4] = time_u > (unsigned long long)INT64_MAX ? -1 : (int64_t)time_u;
         }
         if (a.p2p) {
-            // straight into every rank's receive slot (NVLink stores)
-            const uint64_t epoch = a.win->exch_epoch + 1;  // incremented by the last block
+            // straight into every rank's receive slot as LL words (NVLink
+            // stores; each word carries the epoch, no fence or flag needed)
+            const uint64_t epoch = a.win->exch_epoch + 1;  // advanced by the last block
             const int64_t S = 3 + 2 * (int64_t)a.n_total;
-            const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * S;
+            const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * 2 * S;
             for (int r = 0; r < a.nranks; ++r) {
-                a.peer_slots[r][off + 3 + q] = c;
-                a.peer_slots[r][off + 3 + a.n_total + q] = m;
+                ll_store(a.peer_slots[r] + off + 2 * (3 + q), c, epoch);
+                ll_store(a.peer_slots[r] + off + 2 * (3 + a.n_total + q), m, epoch);
             }
         } else if (a.exchange) {
             a.slot_send[3 + q] = c;
@@ -578,14 +602,12 @@ __global__ void k_epilogue(EpiArgs a) {
             if (a.p2p) {
                 const uint64_t epoch = a.win->exch_epoch + 1;
                 const int64_t S = 3 + 2 * (int64_t)a.n_total;
-                const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * S;
+                const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * 2 * S;
                 for (int r = 0; r < a.nranks; ++r) {
-                    a.peer_slots[r][off + 0] = a.layer_begin;
-                    a.peer_slots[r][off + 1] = a.n_local;
-                    a.peer_slots[r][off + 2] = fin;
+                    ll_store(a.peer_slots[r] + off + 0, a.layer_begin, epoch);
+                    ll_store(a.peer_slots[r] + off + 2, a.n_local, epoch);
+                    ll_store(a.peer_slots[r] + off + 4, fin, epoch);
                 }
-                __threadfence_system();
-                for (int r = 0; r < a.nranks; ++r) st_release_sys(&a.peer_win[r]->exch[a.rank], epoch);
                 a.win->exch_epoch = epoch;
             } else if (a.exchange) {
                 a.slot_send[0] = a.layer_begin;
@@ -653,29 +675,51 @@ __device__ void k_unpack_body(const int64_t *slot_recv, int32_t nranks, int32_t 
 
 // Peer-memory exchange, receive side: wait (bounded) for every rank's flag of
 // this epoch, then scatter the local slot area of the epoch's parity.
+// Receiver side of the LL exchange: for every sender rank, poll its three
+// header words, then the words of its [layer_begin, +n_local) slice, until
+// each carries this call's epoch (bounded: 10 s), decoding into `decoded`
+// ([nranks][S] plain int64 slots) for the shared validation / scatter.
 __global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
-                             int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
+                             int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
     pdl_wait();
     pdl_trigger();
     __shared__ int s_ok;
+    __shared__ int64_t s_hdr[3];
     const uint64_t epoch = win->exch_epoch;  // advanced by this rank's epilogue
-    if (threadIdx.x == 0) {
-        int ok = 1;
-        for (int r = 0; r < nranks; ++r) {
-            uint64_t t0, t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            while (ld_acquire_sys(&win->exch[r]) < epoch) {
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                if (t - t0 > 10ull * 1000 * 1000 * 1000) {
-                    ok = 0;
-                    win->err = DYNMO_E_NCCL;
-                    break;
-                }
-                __nanosleep(100);
-            }
+    const int64_t S = 3 + 2 * (int64_t)n_total;
+    const uint64_t *ll = (const uint64_t *)slots + (int64_t)(epoch & 1) * nranks * 2 * S;
+    uint64_t t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    if (threadIdx.x == 0) s_ok = 1;
+    __syncthreads();
+    for (int r = 0; r < nranks; ++r) {
+        const uint64_t *src = ll + (int64_t)r * 2 * S;
+        int64_t *dst = decoded + (int64_t)r * S;
+        if (threadIdx.x < 3) {  // header: layer_begin, n_local, status
+            int64_t v;
+            if (!ll_poll(src + 2 * threadIdx.x, epoch, t0, v)) atomicExch(&s_ok, 0);
+            s_hdr[threadIdx.x] = v;
+            dst[threadIdx.x] = v;
         }
-        s_ok = ok;
+        __syncthreads();
+        if (!s_ok) break;
+        const int64_t lb = s_hdr[0], n = s_hdr[1];
+        const bool sane = lb >= 0 && n >= 0 && lb + n <= n_total;  // else the shared check flags it
+        for (int64_t i = threadIdx.x; sane && i < n; i += blockDim.x) {
+            int64_t c, m;
+            bool ok = ll_poll(src + 2 * (3 + i), epoch, t0, c);
+            ok = ok && ll_poll(src + 2 * (3 + n_total + i), epoch, t0, m);
+            if (!ok) {
+                atomicExch(&s_ok, 0);
+                break;
+            }
+            dst[3 + i] = c;
+            dst[3 + n_total + i] = m;
+        }
+        __syncthreads();
+        if (!s_ok) break;
     }
+    if (!s_ok && threadIdx.x == 0) win->err = DYNMO_E_NCCL;
     __syncthreads();
     if (!s_ok) {
         for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
@@ -685,8 +729,8 @@ __global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nran
         if (threadIdx.x == 0) *status_out = DYNMO_E_NCCL;
         return;
     }
-    const int64_t S = 3 + 2 * (int64_t)n_total;
-    k_unpack_body(slots + (int64_t)(epoch & 1) * nranks * S, nranks, n_total, cost_out, mem_out, status_out);
+    __syncthreads();
+    k_unpack_body(decoded, nranks, n_total, cost_out, mem_out, status_out);
 }
 
 }  // namespace
@@ -758,8 +802,10 @@ cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_to
 }
 
 cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
-                              int64_t *cost_out, int64_t *mem_out, int32_t *status_out, cudaStream_t s) {
-    return launch_pdl(k_unpack_p2p, 1, 1024, 0, s, slots, win, nranks, n_total, cost_out, mem_out, status_out);
+                              int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
+                              cudaStream_t s) {
+    return launch_pdl(k_unpack_p2p, 1, 1024, 0, s, slots, win, nranks, n_total, decoded, cost_out, mem_out,
+                      status_out);
 }
 
 }  // namespace dynmo
