@@ -748,7 +748,10 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
         // folded into predicates.  Two shuffle phases (x, then the picks).
         // (A halo-2 variant deciding both edges locally from x at distance
         // 1 and 2 -- one phase of 8 shuffles -- measured slower, 24.2 vs
-        // 22.8 us on config 2: the shuffle pipe, not latency, bounds it.)
+        // 22.8 us on config 2: the shuffle pipe, not latency, bounds it.  So
+        // did all n <= 8 loads replicated in every lane, a fully unrolled
+        // shuffle-free round: 39 vs 21 us at L = 127, n = 8 -- issue-bound
+        // on the fp64 pipe.)
         const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
         for (int k = 0; k < size; ++k) {
             if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
