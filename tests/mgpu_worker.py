@@ -163,6 +163,23 @@ def main():
         assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "mapped")
     assert pm2.error() == 0
     pm2.close()
+    # ranks without layers (more GPUs than layers): 2 layers over `world`
+    # ranks, ranks >= 2 hold empty slices; the peer-memory and NCCL exchanges
+    # still give every rank the full cost vector
+    tiny = [np.full(1000 + 17 * l, 1, np.uint8) for l in range(2)]
+    lb0, cnt0 = (rank, 1) if rank < 2 else (2, 0)
+    segs0 = []
+    for l in range(lb0, lb0 + cnt0):
+        t0_ = torch.from_numpy(tiny[l]).to(dev)
+        keep.append(t0_)
+        segs0.append(D.SegmentSpec(t0_, LB.SRC_MASK_U8, l))
+    for mode0 in ("p2p", "nccl"):
+        plan0 = D.ProfilePlan(ctx, segs0, lb0, cnt0, n_total=2, exchange=mode0)
+        for rep0 in range(2):
+            c0, _, st0 = D.profile_layers(ctx, plan0, D.coef_tensor(max(cnt0, 1), B=1, device=dev))
+            torch.cuda.synchronize()
+            assert int(st0.item()) == 0 and c0.cpu().tolist() == [1000, 1017], (rank, mode0, c0.cpu().tolist())
+        plan0.close()
     # several buffers per layer (a CSR payload is values, indices and
     # optimizer state): 3 buffers of different sizes and dtypes per layer,
     # through NCCL send/recv, the host-driven and the device-driven pull

@@ -1,5 +1,6 @@
 """Summaries of gpurun outputs: bench JSON line and ncu launch lists."""
 import collections
+import signal
 import csv
 import json
 import sys
@@ -28,6 +29,7 @@ def bench(path):
 
 
 if __name__ == "__main__":
+    signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under | head
     for p in sys.argv[1:]:
         print("==", p)
         (launches if p.endswith(".csv") else bench)(p)
