@@ -22,8 +22,10 @@
  *    library never takes ownership of caller memory and never frees it.
  *  - Calls 1-4 are asynchronous on the given cudaStream_t and never
  *    synchronise the host; data-dependent errors are written to device
- *    status words (int32).  Call 5 needs host boundaries (the caller copies
- *    the <= 40 B boundary vector D2H first) and is also stream-ordered.
+ *    status words (int32).  Call 5 (NCCL, or dynmo_migrate_layers_p2p) takes
+ *    host boundaries (the caller copies the <= 40 B boundary vector D2H
+ *    first); dynmo_migrate_layers_dev reads them from device memory, so the
+ *    whole step can be one CUDA graph launch.  All calls are stream-ordered.
  *  - Return value: host-checkable status (argument validation, CUDA/NCCL
  *    launch errors).  0 OK, < 0 error, > 0 warning.
  *  - int32 layer/stage indices, int64 costs and bytes.  All results are
