@@ -367,19 +367,31 @@ __global__ void __launch_bounds__(1024) k_prune_tiescan(PruneArgs a) {
 
 // Full tile (kPruneTileElems elements, 16-byte aligned): warp w owns the
 // contiguous vectors [w VW, (w+1) VW) and walks them in groups of 4 x 32
-// (lane L loads vector g*128 + u*32 + L: 4 coalesced 16-byte loads in
+// (lane L loads vector g*256 + u*32 + L: kU coalesced 16-byte loads in
 // flight).  A tie's rank in element order = the warp range's offset (from
 // the tie-count scan) + ties earlier in the range (u-major, lane-minor warp
-// scans, a running count) + its position in the vector.  No block barrier.
-// Masks stored per vector (8 or 4 bytes, coalesced).
-template <bool BF>
-__device__ __forceinline__ void mask_full_tile(const PruneTile &t, uint32_t tau, bool partial, bool all_ties,
-                                               long long keep_ties, unsigned long long wbase) {
-    constexpr int EV = BF ? 8 : 4;
-    constexpr int VW = (int)kPruneTileElems / EV / kPruneWarps;
+// scans -- skipped when no lane of the warp holds a tie -- and a running
+// count) + its position in the vector.  No block barrier.  Masks stored per
+// vector (8 or 4 bytes, coalesced).
+//
+// bf16 full tile, two magnitudes per 32-bit word: m = w & 0x7FFF7FFF holds
+// two 15-bit fields, and for a field value x <= 0x7FFF and t <= 0x7FFF,
+// x > t  <=>  bit 15 of x + (0x7FFF - t), with no carry out of the field.
+// For a bf16 key (m << 16): key > tau <=> m > tau >> 16; key == tau <=>
+// m == tau >> 16 and tau's low half is 0; NaN <=> m > 0x7F80.  The flags
+// sit in bits 15 / 31; one byte permute per word pair gathers the four
+// flag bytes in element order.  Same ranks and masks as the general path.
+__device__ __forceinline__ void mask_full_tile_bf16(const PruneTile &t, uint32_t tau, bool partial, bool all_ties,
+                                                    long long keep_ties, unsigned long long wbase) {
+    constexpr int VW = (int)kPruneTileElems / 8 / kPruneWarps;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint4 *v = (const uint4 *)t.w + w * VW;
-    const bool al = ((uintptr_t)t.mask & (EV - 1)) == 0;
+    const bool al = ((uintptr_t)t.mask & 7u) == 0;
+    const uint32_t t16 = tau >> 16;
+    const uint32_t cg = t16 >= 0x7FFFu ? 0u : 0x7FFFu - t16;                  // > t16
+    const uint32_t ce = (t16 > 0x7FFFu || (tau & 0xFFFFu)) ? 0u : 0x8000u - t16;  // >= t16 (ties possible)
+    const uint32_t CG = cg | cg << 16, CE = ce | ce << 16, CN = 0x007F007Fu;   // CN: > 0x7F80 (NaN)
+    const bool tie_flags = partial || all_ties;
     unsigned long long run = wbase;
     for (int g = 0; g < VW; g += kU * 32) {
         uint4 x[kU];
@@ -388,21 +400,80 @@ __device__ __forceinline__ void mask_full_tile(const PruneTile &t, uint32_t tau,
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const uint32_t q[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
-            uint32_t keys[EV];
+            uint32_t kp[4], eq[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                if (BF) {
-                    keys[2 * e] = key_bf16(q[e] & 0xFFFFu);
-                    keys[2 * e + 1] = key_bf16(q[e] >> 16);
-                } else {
-                    keys[e] = key_f32(q[e]);
+                const uint32_t m = q[e] & 0x7FFF7FFFu;
+                const uint32_t gt = m + CG, nan = m + CN;
+                kp[e] = gt & ~nan & 0x80008000u;
+                eq[e] = tie_flags ? (m + CE) & ~gt & 0x80008000u : 0u;
+            }
+            uint32_t m0 = (__byte_perm(kp[0], kp[1], 0x7531) >> 7) & 0x01010101u;
+            uint32_t m1 = (__byte_perm(kp[2], kp[3], 0x7531) >> 7) & 0x01010101u;
+            const uint32_t e0 = (__byte_perm(eq[0], eq[1], 0x7531) >> 7) & 0x01010101u;
+            const uint32_t e1 = (__byte_perm(eq[2], eq[3], 0x7531) >> 7) & 0x01010101u;
+            if (!partial) {
+                m0 |= e0;  // all of this rank's ties kept (e0/e1 are 0 when none are)
+                m1 |= e1;
+            } else {
+                const uint32_t c = __popc(e0) + __popc(e1);
+                if (__any_sync(0xFFFFFFFFu, c != 0)) {  // most warp vectors hold no tie
+                    uint32_t incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    unsigned long long r = run + incl - c;  // rank of this lane's first tie
+                    run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+                    if (c) {
+                        uint32_t f0 = e0, f1 = e1;  // ties in element order: bytes of m0, then m1
+                        while (f0) {
+                            const uint32_t b = f0 & (0u - f0);
+                            if (r++ < (unsigned long long)keep_ties) m0 |= b;
+                            f0 ^= b;
+                        }
+                        while (f1) {
+                            const uint32_t b = f1 & (0u - f1);
+                            if (r++ < (unsigned long long)keep_ties) m1 |= b;
+                            f1 ^= b;
+                        }
+                    }
                 }
             }
-            unsigned long long before = 0;
-            if (partial) {
-                uint32_t c = 0;
+            uint8_t *mk = t.mask + (int64_t)(w * VW + g + u * 32 + lane) * 8;
+            if (al) {
+                *(uint2 *)mk = make_uint2(m0, m1);
+            } else {
 #pragma unroll
-                for (int e = 0; e < EV; ++e) c += keys[e] == tau;
+                for (int e = 0; e < 8; ++e) mk[e] = (uint8_t)(((e < 4 ? m0 : m1) >> (8 * (e & 3))) & 1u);
+            }
+        }
+    }
+}
+
+// f32 full tile: 4 keys per vector, compared directly.
+__device__ __forceinline__ void mask_full_tile_f32(const PruneTile &t, uint32_t tau, bool partial, bool all_ties,
+                                                   long long keep_ties, unsigned long long wbase) {
+    constexpr int VW = (int)kPruneTileElems / 4 / kPruneWarps;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint4 *v = (const uint4 *)t.w + w * VW;
+    const bool al = ((uintptr_t)t.mask & 3u) == 0;
+    unsigned long long run = wbase;
+    for (int g = 0; g < VW; g += kU * 32) {
+        uint4 x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) x[u] = ld_nc(v + g + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const uint32_t keys[4] = {key_f32(x[u].x), key_f32(x[u].y), key_f32(x[u].z), key_f32(x[u].w)};
+            unsigned long long before = 0;
+            uint32_t c = 0;
+            if (partial) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) c += keys[e] == tau;
+            }
+            if (__any_sync(0xFFFFFFFFu, c != 0)) {  // most warp vectors hold no tie: skip the scan
                 uint32_t incl = c;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -412,24 +483,23 @@ __device__ __forceinline__ void mask_full_tile(const PruneTile &t, uint32_t tau,
                 before = run + incl - c;
                 run += __shfl_sync(0xFFFFFFFFu, incl, 31);
             }
-            uint32_t m[2] = {0u, 0u}, seen = 0;
+            uint32_t m = 0u, seen = 0;
 #pragma unroll
-            for (int e = 0; e < EV; ++e) {
+            for (int e = 0; e < 4; ++e) {
                 const uint32_t k = keys[e];
                 bool keep = k > tau && k <= kNanKey;
                 if (k == tau) {
                     keep = partial ? (before + seen < (unsigned long long)keep_ties) : all_ties;
                     ++seen;
                 }
-                m[e >> 2] |= (keep ? 1u : 0u) << (8 * (e & 3));
+                m |= (keep ? 1u : 0u) << (8 * e);
             }
-            uint8_t *mk = t.mask + (int64_t)(w * VW + g + u * 32 + lane) * EV;
+            uint8_t *mk = t.mask + (int64_t)(w * VW + g + u * 32 + lane) * 4;
             if (al) {
-                if (BF) *(uint2 *)mk = make_uint2(m[0], m[1]);
-                else *(uint32_t *)mk = m[0];
+                *(uint32_t *)mk = m;
             } else {
 #pragma unroll
-                for (int e = 0; e < EV; ++e) mk[e] = (uint8_t)((m[e >> 2] >> (8 * (e & 3))) & 1u);
+                for (int e = 0; e < 4; ++e) mk[e] = (uint8_t)((m >> (8 * e)) & 1u);
             }
         }
     }
@@ -460,8 +530,8 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_mask(PruneArgs a) {
                 wb = a.tile_off[ti];
                 for (int u = 0; u < (int)(threadIdx.x >> 5); ++u) wb += a.tile_ties[ti * kPruneWarps + u];
             }
-            if (t.dtype == DYNMO_W_BF16) mask_full_tile<true>(t, tau, partial, all_ties, keep_ties, wb);
-            else mask_full_tile<false>(t, tau, partial, all_ties, keep_ties, wb);
+            if (t.dtype == DYNMO_W_BF16) mask_full_tile_bf16(t, tau, partial, all_ties, keep_ties, wb);
+            else mask_full_tile_f32(t, tau, partial, all_ties, keep_ties, wb);
             continue;
         }
         unsigned long long run = partial ? a.tile_off[ti] : 0ull;  // ties before this chunk

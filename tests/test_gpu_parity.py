@@ -740,6 +740,42 @@ def test_global_prune_parity(D, ctx, quant):
     plan.close()
 
 
+def test_global_prune_bf16_unaligned_masks_specials(D, ctx):
+    """The packed bf16 mask path (two 15-bit magnitudes per word): all-bf16
+    plan, masks at odd byte offsets (the unaligned store branch), +-inf
+    (kept above every finite value, not NaN), +-0, subnormals and the
+    largest finite value, and thresholds that fall on inf, on the largest
+    finite value, inside the quantised bulk and on zero (a partial share of
+    the ties in each case) -- masks == the oracle's."""
+    g = np.random.default_rng(7)
+    sizes = [3 * 32768 + 5, 65536, 32768, 40000]
+    specials = np.array([0x7F80, 0xFF80, 0x0000, 0x8000, 0x0001, 0x8003, 0x7F7F, 0xFF7F], np.uint16)
+    shards, vals = [], []
+    for n in sizes:
+        x = np.round(g.normal(0.0, 1.0, n) * 4) / 4
+        bits = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        pos = g.choice(n, 64, replace=False)
+        bits[pos] = specials[np.arange(64) % len(specials)]
+        shards.append(torch.from_numpy(bits.view(np.int16).copy()).view(torch.bfloat16).to(DEV))
+        vals.append(oracle.bf16_to_f64(bits))
+    buf = torch.zeros(sum(sizes) + 64, dtype=torch.uint8, device=DEV)
+    masks, off = [], 1
+    for n in sizes:
+        masks.append(buf[off:off + n])
+        off += n + 2  # odd offsets throughout
+    plan = D.PrunePlan(ctx, list(zip(shards, masks)))
+    N = sum(sizes)
+    n_inf = 4 * 16  # 16 infs (+-) per shard, as many largest-finite values
+    for k in [1, n_inf - 3, n_inf + 5, N // 3, N - 10, N]:
+        info, st = D.global_prune(ctx, plan, k)
+        torch.cuda.synchronize()
+        ost, omask = oracle.global_prune(vals, k)
+        assert int(st.item()) == ost == 0, (k, int(st.item()))
+        for m, om in zip(masks, omask):
+            assert np.array_equal(m.cpu().numpy(), om), k
+    plan.close()
+
+
 def test_global_prune_errors_and_nan(D, ctx):
     """k > N: INVALID, all masks 0; a NaN is never kept and sets INVALID
     (the selection runs over the other weights, like the oracle)."""
