@@ -472,9 +472,13 @@ void dynmo_prune_plan_destroy(dynmo_pplan plan);
 
 /* Collective (every rank, same k): writes every segment's mask.
  *   k       global number of weights to keep; k < 0 is INVALID (host).
- *   d_info  [5] int64 out, nullable: {tau key (bits of the k-th largest |w|
+ *   d_info  [6] int64 out, nullable: {tau key (bits of the k-th largest |w|
  *           as f32; -1 if nothing is kept), global non-NaN count, global
- *           count above tau, ties kept on this rank, ties on this rank}.
+ *           count above tau, ties kept on this rank, ties on this rank,
+ *           flags: bit 0 = the first digit's bin window (estimated from a
+ *           1/16 tile sample) missed and the full first-digit histogram
+ *           ran; bit 1 = the tie counts came from the windowed pass (no
+ *           tie-count pass over the weights)}.
  *   d_status [1] int32 out: OK; INVALID if k > global non-NaN count (all
  *           masks 0) or a NaN weight exists (NaN is never kept).
  * Asynchronous on `stream`, no host synchronisation; capturable in a CUDA

@@ -680,7 +680,7 @@ struct dynmo_pplan_s {
     dynmo_ctx ctx = nullptr;
     void *dmem = nullptr;
     PruneArgs args{};
-    int grid[24] = {};  // per launch kind: persistent grid (SMs x resident blocks), capped by the tiles
+    int grid[40] = {};  // per launch kind: persistent grid (SMs x resident blocks), capped by the tiles
 };
 
 dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h_segs, int32_t n_segs,
@@ -707,11 +707,13 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     }
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t nt = std::max<size_t>(1, tiles.size());
-    const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 32769);
+    const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 32770);
     const size_t sz_sel = up(sizeof(PruneSel)), sz_tie = up(sizeof(long long) * std::max(1, ctx->nranks));
     // tie counts / offsets per (tile, warp range of the mask pass)
     const size_t sz_tt = up(sizeof(uint32_t) * nt * 8), sz_to = up(sizeof(unsigned long long) * nt * 8);
-    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to;
+    // per-(tile, warp range) window-bin counts (bf16-only plans: ties on the first digit)
+    const size_t sz_tw = any_f32 ? 0 : up(sizeof(uint16_t) * nt * 8 * kWinCnt);
+    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to + sz_tw;
     DeviceGuard g(ctx->device);
     auto *pl = new dynmo_pplan_s();
     pl->ctx = ctx;
@@ -729,8 +731,10 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     a.sel = (PruneSel *)b; b += sz_sel;
     a.tie_all = (const long long *)b; b += sz_tie;
     a.tile_ties = (uint32_t *)b; b += sz_tt;
-    a.tile_off = (unsigned long long *)b;
+    a.tile_off = (unsigned long long *)b; b += sz_to;
+    a.tile_win = sz_tw ? (uint16_t *)b : nullptr;
     a.n_tiles = (int64_t)tiles.size();
+    for (const PruneTile &t : tiles) a.n_elems += t.n;
     a.rank = ctx->rank;
     a.nranks = ctx->nranks;
     a.last_pass = any_f32 ? 2 : 0;  // bf16 keys have 16 zero low bits: the 15-bit first digit is exact
@@ -745,9 +749,12 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
         return cuda_fail(e, "prune plan upload");
     }
     // persistent grids: every SM filled to its occupancy for each streaming kernel
-    for (int kind : {0, 1, 2, 21, 23})
+    for (int kind : {0, 1, 2, 21, 23, 32})
         pl->grid[kind] = (int)std::max<int64_t>(
             1, std::min<int64_t>((int64_t)ctx->num_sms * prune_blocks_per_sm(kind), a.n_tiles));
+    pl->grid[30] = (int)std::max<int64_t>(  // the sample pass: every kPruneSampleStride-th tile
+        1, std::min<int64_t>((int64_t)ctx->num_sms * prune_blocks_per_sm(30),
+                             (a.n_tiles + kPruneSampleStride - 1) / kPruneSampleStride));
     *out = pl;
     return DYNMO_OK;
 }
@@ -768,15 +775,32 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
     const PruneArgs &a = plan->args;
     const bool multi = ctx->nranks > 1;
     CUDA_TRY(launch_prune_begin(a.sel, (long long)k, s), "k_prune_begin");
-    for (int pass = 0; pass <= a.last_pass; ++pass) {
-        CUDA_TRY(launch_prune(a, pass, plan->grid[pass], s), "k_prune_hist");
-        if (multi) {
-            const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, 32769, ncclUint64, ncclSum, ctx->comm, s);
-            if (r != ncclSuccess) {
-                g_err = std::string("ncclAllReduce (prune): ") + ncclGetErrorString(r);
-                return DYNMO_E_NCCL;
-            }
+    auto all_reduce = [&](int count) -> dynmo_status {
+        if (!multi) return DYNMO_OK;
+        const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, count, ncclUint64, ncclSum, ctx->comm, s);
+        if (r != ncclSuccess) {
+            g_err = std::string("ncclAllReduce (prune): ") + ncclGetErrorString(r);
+            return DYNMO_E_NCCL;
         }
+        return DYNMO_OK;
+    };
+    dynmo_status st;
+    // pass 0: sample histogram -> bin window -> windowed full pass -> select;
+    // on a miss (the k-th key outside the window) the full histogram and a
+    // second select run (both launched unconditionally: graph-capturable;
+    // they return at once without a miss)
+    CUDA_TRY(launch_prune(a, 30, plan->grid[30], s), "k_prune_hist0 (sample)");
+    if ((st = all_reduce(32770)) != DYNMO_OK) return st;
+    CUDA_TRY(launch_prune(a, 31, 1, s), "k_prune_window");
+    CUDA_TRY(launch_prune(a, 0, plan->grid[0], s), "k_prune_hist0w");
+    if ((st = all_reduce(32769)) != DYNMO_OK) return st;
+    CUDA_TRY(launch_prune(a, 10, 1, s), "k_prune_select");
+    CUDA_TRY(launch_prune(a, 32, plan->grid[32], s), "k_prune_hist0 (on a miss)");
+    if ((st = all_reduce(32769)) != DYNMO_OK) return st;
+    CUDA_TRY(launch_prune(a, 13, 1, s), "k_prune_select (on a miss)");
+    for (int pass = 1; pass <= a.last_pass; ++pass) {
+        CUDA_TRY(launch_prune(a, pass, plan->grid[pass], s), "k_prune_hist");
+        if ((st = all_reduce(32769)) != DYNMO_OK) return st;
         CUDA_TRY(launch_prune(a, 10 + pass, 1, s), "k_prune_select");
     }
     if (multi) {

@@ -166,22 +166,31 @@ struct PruneTile {
 };
 static_assert(sizeof(PruneTile) == 24, "prune tile layout");
 constexpr uint32_t kPruneTileElems = 32768;
+constexpr int64_t kPruneSampleStride = 16;
+constexpr int kWinCnt = 16;  // windows up to 16 bins also record per-(tile, warp range) bin counts  // pass-0 sample: every 16th tile (1/16 of the weights)
 
 struct PruneSel {  // device-side selection state of one call
     long long k, k_rem, above, tie_local, keep_ties, n_global;
     uint32_t prefix, tau;
     int32_t partial, status, done, pad;
+    uint32_t win_lo, win_hi;  // pass-0 bin window estimated from the sample histogram
+    int32_t miss;             // the k-th key fell outside the window: full pass-0 histogram
+    int32_t missed;           // a miss happened in this call (d_info[5])
+    int32_t wincnt;           // tile_win holds the per-(tile, warp range) counts of tau's bin
+    uint32_t tau_d;           // tau's bin - win_lo
 };
 
 struct PruneArgs {
     const PruneTile *tiles;
     int64_t n_tiles;
-    unsigned long long *hist_local;   // [32769] (bin 32768: NaN count)
-    unsigned long long *hist_global;  // [32769] all-reduced (nranks > 1)
+    unsigned long long *hist_local;   // [32770] (bin 32768: NaN count; 32769: elements, sample pass)
+    unsigned long long *hist_global;  // [32770] all-reduced (nranks > 1)
     PruneSel *sel;
     const long long *tie_all;         // [nranks] all-gathered tie counts
     uint32_t *tile_ties;              // [n_tiles]
     unsigned long long *tile_off;     // [n_tiles]
+    uint16_t *tile_win;               // [n_tiles][8][kWinCnt] window-bin counts (bf16-only plans), else null
+    long long n_elems;                // this rank's weights
     int32_t rank, nranks, last_pass;
 };
 cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s);

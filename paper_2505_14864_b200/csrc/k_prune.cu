@@ -26,6 +26,7 @@ constexpr int kPruneThreads = 256;
 constexpr int kBins0 = 32768;  // pass 0 digit: key bits 30..16 (15 bits = a bf16 magnitude)
 constexpr int kBins1 = 1024;   // pass 1 digit: key bits 15..6; pass 2: bits 5..0 (64 of the bins)
 constexpr int kHist0Threads = 1024;  // pass 0: one 128 KB shared histogram per block, one block per SM
+constexpr uint32_t kWinMax = 4096;   // widest pass-0 window (bins) of the windowed pass: 16 KB shared
 constexpr uint32_t kNanKey = 0x7F800000u;  // key > this: NaN
 constexpr int kPruneWarps = kPruneThreads / 32;  // tie-offset entries per tile
 constexpr int kU = 8;  // 16-byte loads in flight per thread in the streaming passes
@@ -80,25 +81,30 @@ __device__ __forceinline__ void for_keys(const PruneTile &t, F &&f) {
     }
 }
 
-// Pass 0: the 15-bit digit key >> 16 (for bf16 the whole magnitude, so an
-// all-bf16 plan needs this one pass only): one 128 KB shared histogram per
-// 1024-thread block, one block per SM, flushed as one global atomic per
-// nonzero bin per block.  hist[kBins0] counts NaN keys.
+// Pass 0 histogram of the 15-bit digit key >> 16 (for bf16 the whole
+// magnitude, so an all-bf16 plan needs pass 0 only): one 128 KB shared
+// histogram per 1024-thread block, one block per SM, flushed as one global
+// atomic per nonzero bin per block; hist[kBins0] counts NaN keys.
+//   MODE 0 (sample): every kPruneSampleStride-th tile, plus this rank's
+//     element count in hist[kBins0 + 1] -- the input of k_prune_window;
+//   MODE 1 (miss): every tile, only when the windowed pass missed.
+template <int MODE>
 __global__ void __launch_bounds__(kHist0Threads) k_prune_hist0(PruneArgs a) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ uint32_t sh0[];  // [kBins0]
     __shared__ uint32_t s_nan;
+    if (a.sel->done || (MODE == 1 && !a.sel->miss)) return;  // k = 0 / invalid k; no miss
     for (int i = threadIdx.x; i < kBins0; i += kHist0Threads) sh0[i] = 0u;
     if (threadIdx.x == 0) s_nan = 0u;
     __syncthreads();
-    if (a.sel->done) return;  // k = 0 or invalid k
+    constexpr int64_t S = MODE == 0 ? kPruneSampleStride : 1;
     uint32_t nan = 0;
     PruneTile nxt;
-    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
-    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+    if (blockIdx.x * S < a.n_tiles) nxt = a.tiles[blockIdx.x * S];
+    for (int64_t ti = blockIdx.x * S; ti < a.n_tiles; ti += gridDim.x * S) {
         const PruneTile t = nxt;
-        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];  // prefetch the next descriptor
+        if (ti + gridDim.x * S < a.n_tiles) nxt = a.tiles[ti + gridDim.x * S];  // prefetch the next descriptor
         for_keys(t, [&](uint32_t k) {
             if (k > kNanKey) ++nan;
             else atomicAdd(&sh0[k >> 16], 1u);
@@ -111,6 +117,163 @@ __global__ void __launch_bounds__(kHist0Threads) k_prune_hist0(PruneArgs a) {
         if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
     }
     if (threadIdx.x == 0 && s_nan) atomicAdd(&a.hist_local[kBins0], (unsigned long long)s_nan);
+    if (MODE == 0 && blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(&a.hist_local[kBins0 + 1], (unsigned long long)a.n_elems);
+}
+
+// Windowed pass 0 over every tile: keys whose digit lies in the window
+// [lo, hi] (estimated from the sample, k_prune_window) go to the shared
+// histogram; the others are only counted (registers), and the counts land
+// in bins hi + 1 (all keys above the window) and lo - 1 (all below), so the
+// histogram stays exact in total and k_prune_select<0> either finds the
+// k-th key's bin inside the window or reports a miss.  bf16 vectors are
+// classified two magnitudes per word with the field arithmetic of the mask
+// pass (x > t <=> bit 15 of x + 0x7FFF - t); in-window keys are rare
+// (≈ 1 % on config 2), so almost every key costs a few ALU operations
+// instead of a shared atomic.
+__global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint32_t shw[kWinMax];  // bins [lo, hi], hi - lo < kWinMax
+    __shared__ unsigned long long s_cnt[3];  // NaN, below, in the window
+    const PruneSel *sel = a.sel;
+    if (sel->done) return;
+    const uint32_t lo = sel->win_lo, hi = sel->win_hi;
+    uint32_t *sh0 = shw - lo;  // indexed by the digit
+    for (uint32_t i = lo + threadIdx.x; i <= hi; i += kPruneThreads) sh0[i] = 0u;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
+    __syncthreads();
+    constexpr uint32_t H = 0x80008000u;
+    const uint32_t ch = 0x7FFFu - hi, cl = 0x8000u - lo;  // m > hi; m >= lo  (hi, lo <= 0x7FFF)
+    const uint32_t CH = ch | ch << 16, CL = cl | cl << 16, CN = 0x007F007Fu;
+    // per thread: keys below the window and NaN keys; the in-window keys
+    // are summed from the shared bins at the end, and the keys above the
+    // window = the block's keys - the rest (nothing counted on the hot path)
+    unsigned long long below = 0, nan = 0, seen = 0;
+    // count mode (bf16-only plan, window <= kWinCnt bins): also the count of
+    // each window bin per (tile, warp range of the mask pass) -> tile_win,
+    // from which the tie counts of tau's bin are gathered (no tie-count pass)
+    const bool cnt = a.tile_win != nullptr && hi - lo + 1 <= (uint32_t)kWinCnt;
+    __shared__ uint32_t s_wc[kPruneWarps][kWinCnt];  // per warp (full tiles) / [0] per block (ragged)
+    if (threadIdx.x < kPruneWarps * kWinCnt) (&s_wc[0][0])[threadIdx.x] = 0u;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // the in-window counters, indexed by the digit: in count mode this warp's
+    // row of s_wc (its totals, kept by lanes < kWinCnt in wtot, give the
+    // window bins), else the block's window histogram
+    uint32_t *const wbin = cnt ? &s_wc[w][0] - lo : sh0;
+    uint32_t *const rbin = cnt ? &s_wc[0][0] - lo : sh0;  // ragged tiles: row 0
+    unsigned long long wtot = 0;
+    auto scalar = [&](uint32_t k) {
+        if (k > kNanKey) {
+            ++nan;
+        } else {
+            const uint32_t p = k >> 16;
+            if (p < lo) ++below;
+            else if (p <= hi) atomicAdd(&rbin[p], 1u);
+        }
+    };
+    PruneTile nxt;
+    if (blockIdx.x < a.n_tiles) nxt = a.tiles[blockIdx.x];
+    for (int64_t ti = blockIdx.x; ti < a.n_tiles; ti += gridDim.x) {
+        const PruneTile t = nxt;
+        if (ti + gridDim.x < a.n_tiles) nxt = a.tiles[ti + gridDim.x];
+        seen += t.n;  // every thread: the block's keys
+        if (t.dtype != DYNMO_W_BF16 || t.n != kPruneTileElems) {  // f32 or ragged: per key
+            if (cnt) __syncthreads();  // every warp's full-tile counts flushed (row 0 is reused here)
+            for_keys(t, scalar);
+            if (cnt) {  // a ragged tile's counts all go to warp range 0 (as in k_prune_tiecount)
+                __syncthreads();
+                if (threadIdx.x < kPruneWarps * kWinCnt)
+                    a.tile_win[ti * kPruneWarps * kWinCnt + threadIdx.x] =
+                        threadIdx.x < kWinCnt ? (uint16_t)s_wc[0][threadIdx.x] : (uint16_t)0;
+                __syncthreads();
+                if (threadIdx.x < kWinCnt) {  // warp 0, lane d: row 0's totals
+                    wtot += s_wc[0][threadIdx.x];
+                    s_wc[0][threadIdx.x] = 0u;
+                }
+                __syncthreads();
+            }
+            continue;
+        }
+        // bf16 full tile: warp w owns vectors [w VW, (w+1) VW) (the mask pass's ranges)
+        constexpr int VW = (int)kPruneTileElems / 8 / kPruneWarps;
+        const uint4 *v = (const uint4 *)t.w + w * VW;
+        uint32_t pb = 0;    // two 16-bit counters of below-window keys (<= 64 per field per tile)
+        uint32_t nacc = 0;  // bit 15 / 31 set: a NaN somewhere in this thread's vectors
+        for (int g = 0; g < VW; g += kU * 32) {
+            uint4 x[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) x[u] = ld_nc(v + g + u * 32 + lane);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const uint32_t q[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const uint32_t m = q[e] & 0x7FFF7FFFu;
+                    const uint32_t ge = m + CL, ah = m + CH;
+                    nacc |= m + CN;
+                    pb += (~ge & H) >> 15;
+                    const uint32_t in = ge & ~ah & H;  // lo <= m <= hi (NaN bins dropped at the flush)
+                    if (in & 0x8000u) atomicAdd(&wbin[m & 0x7FFFu], 1u);  // (a predicated red.shared
+                    if (in >> 16) atomicAdd(&wbin[m >> 16], 1u);        //  measured slower)
+                }
+            }
+        }
+        below += (pb & 0xFFFFu) + (pb >> 16);
+        if (nacc & H) {  // rare: count this thread's NaN keys of the tile
+            for (int g = lane; g < VW; g += 32) {
+                const uint4 x = ld_nc(v + g);
+                const uint32_t q[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) nan += __popc(((q[e] & 0x7FFF7FFFu) + CN) & H);
+            }
+        }
+        if (cnt) {  // this warp range's window-bin counts (NaN bins included, never tau's)
+            __syncwarp();
+            if (lane < kWinCnt) {
+                const uint32_t c = s_wc[w][lane];
+                a.tile_win[(ti * kPruneWarps + w) * kWinCnt + lane] = (uint16_t)c;
+                wtot += c;
+                s_wc[w][lane] = 0u;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (cnt) {  // the window bins from the per-warp totals (into sh0, unused in count mode)
+        for (uint32_t b = lo + threadIdx.x; b <= hi; b += kPruneThreads) sh0[b] = 0u;
+        __syncthreads();
+        if (lane < kWinCnt && lo + lane <= hi && wtot) atomicAdd(&sh0[lo + lane], (uint32_t)wtot);
+        __syncthreads();
+    }
+    // flush the window (bins above 0x7F80 hold NaN keys of the packed path,
+    // already counted) and sum the in-window keys
+    unsigned long long inw = 0;
+    const uint32_t top = hi < (kNanKey >> 16) ? hi : (kNanKey >> 16);
+    for (uint32_t b = lo + threadIdx.x; b <= top; b += kPruneThreads) {
+        const uint32_t c = sh0[b];
+        if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
+        inw += c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nan += __shfl_xor_sync(0xFFFFFFFFu, nan, o);
+        below += __shfl_xor_sync(0xFFFFFFFFu, below, o);
+        inw += __shfl_xor_sync(0xFFFFFFFFu, inw, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nan) atomicAdd(&s_cnt[0], nan);
+        if (below) atomicAdd(&s_cnt[1], below);
+        if (inw) atomicAdd(&s_cnt[2], inw);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long above = seen - s_cnt[0] - s_cnt[1] - s_cnt[2];
+        if (s_cnt[0]) atomicAdd(&a.hist_local[kBins0], s_cnt[0]);
+        if (above) atomicAdd(&a.hist_local[hi + 1], above);      // above > 0 => hi < 0x7FFF
+        if (s_cnt[1]) atomicAdd(&a.hist_local[lo - 1], s_cnt[1]);  // below > 0 => lo > 0
+    }
 }
 
 // Passes 1 / 2 (f32 keys only): among the keys carrying the selected prefix
@@ -151,42 +314,155 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist(PruneArgs a) {
     }
 }
 
-// One block: locate the bin of the k_rem-th largest key in the (global)
-// histogram by a suffix scan, narrow the prefix, and clear both histograms.
-template <int PASS>
-__global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    constexpr int NB = PASS == 0 ? kBins0 : kBins1;
-    constexpr int PER = NB / 1024;  // bins per thread (2 or 1)
-    __shared__ unsigned long long s_part[1024];
-    __shared__ int s_bin;
-    PruneSel *sel = a.sel;
-    const unsigned long long *h = a.nranks > 1 ? a.hist_global : a.hist_local;
+// Block-wide (1024 threads) suffix sums over an NB-bin histogram whose
+// nonzero bins lie in [rlo, rhi]: thread t owns bins [t PER, t PER + PER)
+// (loaded only where they meet [rlo, rhi]); s_part[t] = the keys in the
+// bins of threads >= t.  Returns the total.
+template <int NB>
+__device__ unsigned long long suffix_scan(const unsigned long long *h, unsigned long long *s_part, int rlo = 0,
+                                          int rhi = NB - 1) {
+    constexpr int PER = NB / 1024;  // bins per thread (32 or 1)
     const int tid = threadIdx.x;
-    const bool done0 = sel->done != 0;
-    if (PASS == 0 && tid == 0) {
-        // NaN count and the global number of non-NaN keys; validate k
-        const unsigned long long nan = h[kBins0];
-        if (nan) sel->status = DYNMO_E_INVALID;
-    }
-    // thread tid owns bins [tid*PER, tid*PER+PER): its partial sum, then a
-    // suffix scan over threads (bins from the top down)
     unsigned long long mine = 0;
+    if (tid * PER + PER - 1 >= rlo && tid * PER <= rhi) {
+        const uint4 *hv = (const uint4 *)(h + tid * PER);  // 16-byte loads (PER is 1 or even)
+        if constexpr (PER >= 2) {
 #pragma unroll
-    for (int j = 0; j < PER; ++j) mine += h[tid * PER + j];
+            for (int j = 0; j < PER / 2; ++j) {
+                const uint4 x = hv[j];
+                mine += ((unsigned long long)x.y << 32 | x.x) + ((unsigned long long)x.w << 32 | x.z);
+            }
+        } else {
+            mine = h[tid];
+        }
+    }
     s_part[tid] = mine;
     __syncthreads();
-    for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix sums: s_part[t] = sum_{u >= t}
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive suffix sums
         const unsigned long long add = tid + o < 1024 ? s_part[tid + o] : 0ull;
         __syncthreads();
         s_part[tid] += add;
         __syncthreads();
     }
-    if (tid == 0) s_bin = -1;
+    return s_part[0];
+}
+
+// Block-wide, after suffix_scan: the bin b with suffix(b) >= r > suffix(b+1)
+// (the bin of the r-th largest key, 1 <= r <= total) and suffix(b + 1), for
+// every thread.
+template <int NB>
+__device__ void find_bin(const unsigned long long *h, const unsigned long long *s_part, unsigned long long r,
+                         int *bin, unsigned long long *above) {
+    constexpr int PER = NB / 1024;
+    __shared__ int s_bin;
+    __shared__ unsigned long long s_above;
+    const int tid = threadIdx.x;
+    const unsigned long long above_thread = tid + 1 < 1024 ? s_part[tid + 1] : 0ull;
+    if (above_thread < r && s_part[tid] >= r) {
+        unsigned long long acc = above_thread;
+        int b = tid * PER + PER - 1;
+        bool found = false;
+        // this thread's bins from the top, 8 independent loads at a time
+        for (int j0 = PER - 1; j0 >= 0 && !found; j0 -= 8) {
+            unsigned long long c[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) c[q] = j0 - q >= 0 ? h[tid * PER + j0 - q] : 0ull;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (found || j0 - q < 0) continue;
+                if (acc + c[q] >= r) {
+                    b = tid * PER + j0 - q;
+                    found = true;
+                } else {
+                    acc += c[q];
+                }
+            }
+        }
+        s_bin = b;
+        s_above = acc;
+    }
     __syncthreads();
-    const unsigned long long total = s_part[0];
-    if (PASS == 0 && tid == 0) {
+    *bin = s_bin;
+    *above = s_above;
+    __syncthreads();  // s_bin / s_above are reused by the next call
+}
+
+// Pass-0 bin window from the sample histogram (one block): the sample holds
+// S of the N keys (every rank), so the k_rem-th largest key is expected near
+// sample rank r = k_rem S / N; the window spans the bins of sample ranks
+// r -+ (4 sqrt(r) + r / 32 + 16) (binomial 4-sigma plus 3 % for the
+// tile-granular sample).  Any window is exact -- a wrong estimate only costs
+// the full pass (a miss).  Clears the histograms.
+__global__ void __launch_bounds__(1024) k_prune_window(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ unsigned long long s_part[1024];
+    PruneSel *sel = a.sel;
+    const unsigned long long *h = a.nranks > 1 ? a.hist_global : a.hist_local;
+    const unsigned long long S = suffix_scan<kBins0>(h, s_part);  // non-NaN sampled keys
+    const unsigned long long S_all = S + h[kBins0], N = h[kBins0 + 1];
+    uint32_t lo = 0, hi = kBins0 - 1;
+    if (!sel->done && S > 0 && N > 0) {
+        const double r = (double)sel->k_rem * (double)S_all / (double)N;
+        const double d = 4.0 * sqrt(r) + r / 32.0 + 16.0;
+        const double rh = r - d, rl = ceil(r + d);
+        int b;
+        unsigned long long acc;
+        if (rh >= 1.0) {
+            find_bin<kBins0>(h, s_part, (unsigned long long)rh, &b, &acc);
+            hi = (uint32_t)b;
+        }
+        if (rl <= (double)S) {
+            find_bin<kBins0>(h, s_part, (unsigned long long)rl, &b, &acc);
+            lo = (uint32_t)b;
+        }
+        if (hi - lo + 1 > kWinMax) {  // too wide for the shared window: kWinMax bins around the estimate
+            const double rc = r < 1.0 ? 1.0 : (r > (double)S ? (double)S : r);
+            find_bin<kBins0>(h, s_part, (unsigned long long)rc, &b, &acc);
+            const uint32_t c = (uint32_t)b;
+            uint32_t l2 = c >= lo + kWinMax / 2 ? c - kWinMax / 2 : lo;
+            if (l2 + kWinMax - 1 > hi) l2 = hi - (kWinMax - 1);
+            lo = l2;
+            hi = l2 + kWinMax - 1;
+        }
+    } else {  // no sample (k = 0, invalid, or no keys): a window the miss path will not need
+        lo = 0;
+        hi = kWinMax - 1;
+    }
+    if (threadIdx.x == 0) {
+        sel->win_lo = lo;
+        sel->win_hi = hi;
+        sel->miss = 0;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins0 + 2; b += 1024) {
+        a.hist_local[b] = 0ull;
+        if (a.nranks > 1) a.hist_global[b] = 0ull;
+    }
+}
+
+// One block: locate the bin of the k_rem-th largest key in the (global)
+// histogram by a suffix scan, narrow the prefix, and clear both histograms.
+// Pass 0, MODE 0 (after the windowed pass): a bin outside the window (the
+// counts of all keys above / below it) means a miss -- the state is left
+// for MODE 1, which runs after the full histogram and only on a miss.
+template <int PASS, int MODE>
+__global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    constexpr int NB = PASS == 0 ? kBins0 : kBins1;
+    __shared__ unsigned long long s_part[1024];
+    PruneSel *sel = a.sel;
+    if (MODE == 1 && !sel->miss) return;  // nothing was histogrammed
+    const unsigned long long *h = a.nranks > 1 ? a.hist_global : a.hist_local;
+    const int tid = threadIdx.x;
+    const bool done0 = sel->done != 0;
+    if (PASS == 0 && tid == 0 && h[kBins0]) sel->status = DYNMO_E_INVALID;  // NaN keys
+    // after the windowed pass only bins lo - 1 .. hi + 1 can be nonzero
+    const int rlo = PASS == 0 && MODE == 0 ? (int)sel->win_lo - 1 : 0;
+    const int rhi = PASS == 0 && MODE == 0 ? (int)sel->win_hi + 1 : NB - 1;
+    const unsigned long long total = suffix_scan<NB>(h, s_part, rlo, rhi);
+    if (PASS == 0 && tid == 0) {  // the global number of non-NaN keys; validate k
         sel->n_global = (long long)total;
         if (!done0 && (sel->k > (long long)total)) {
             sel->status = DYNMO_E_INVALID;
@@ -196,42 +472,39 @@ __global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
     __syncthreads();
     const long long krem = sel->k_rem;
     if (!done0 && !sel->done && krem > 0) {
-        // the bin b with suffix(b) >= krem > suffix(b + 1)
-        const unsigned long long above_thread = tid + 1 < 1024 ? s_part[tid + 1] : 0ull;
-        if (above_thread < (unsigned long long)krem && s_part[tid] >= (unsigned long long)krem) {
-            unsigned long long acc = above_thread;
-            int b = tid * PER + PER - 1;
-            bool found = false;
-            // this thread's bins from the top, 8 independent loads at a time
-            for (int j0 = PER - 1; j0 >= 0 && !found; j0 -= 8) {
-                unsigned long long c[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) c[q] = j0 - q >= 0 ? h[tid * PER + j0 - q] : 0ull;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (found || j0 - q < 0) continue;
-                    if (acc + c[q] >= (unsigned long long)krem) {
-                        b = tid * PER + j0 - q;
-                        found = true;
-                    } else {
-                        acc += c[q];
-                    }
+        int b;
+        unsigned long long acc;
+        find_bin<NB>(h, s_part, (unsigned long long)krem, &b, &acc);
+        if (tid == 0) {
+            if (PASS == 0 && MODE == 0 && (b == (int)sel->win_hi + 1 || b == (int)sel->win_lo - 1)) {
+                sel->miss = 1;
+            } else {
+                sel->k_rem = krem - (long long)acc;
+                sel->above += (long long)acc;
+                sel->prefix = PASS == 0 ? (uint32_t)b
+                            : PASS == 1 ? ((sel->prefix << 10) | (uint32_t)b) : ((sel->prefix << 6) | (uint32_t)b);
+                // this rank's keys in the chosen bin (the ties, after the last pass)
+                sel->tie_local = (long long)a.hist_local[b];
+                if (PASS == 0) {
+                    sel->missed = MODE;  // reported in d_info[5]
+                    sel->wincnt = MODE == 0 && a.tile_win != nullptr &&
+                                  sel->win_hi - sel->win_lo + 1 <= (uint32_t)kWinCnt;
+                    sel->tau_d = (uint32_t)b - sel->win_lo;
                 }
+                sel->miss = 0;
             }
-            s_bin = b;
-            sel->k_rem = krem - (long long)acc;
-            sel->above += (long long)acc;
-            sel->prefix = PASS == 0 ? (uint32_t)b
-                        : PASS == 1 ? ((sel->prefix << 10) | (uint32_t)b) : ((sel->prefix << 6) | (uint32_t)b);
-            // this rank's keys in the chosen bin (the ties, after the last pass)
-            sel->tie_local = (long long)a.hist_local[b];
         }
     }
     __syncthreads();
     if (tid == 0 && !done0 && !sel->done && krem == 0) sel->done = 2;  // k = 0: nothing kept
-    for (int b = tid; b < NB + (PASS == 0 ? 1 : 0); b += 1024) {
+    const int c0 = rlo < 0 ? 0 : rlo, c1 = rhi > NB - 1 ? NB - 1 : rhi;
+    for (int b = c0 + tid; b <= c1; b += 1024) {
         a.hist_local[b] = 0ull;
         if (a.nranks > 1) a.hist_global[b] = 0ull;
+    }
+    if (PASS == 0 && tid == 0) {  // the NaN count
+        a.hist_local[kBins0] = 0ull;
+        if (a.nranks > 1) a.hist_global[kBins0] = 0ull;
     }
 }
 
@@ -268,6 +541,13 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_tiecount(PruneArgs a) {
     pdl_trigger();
     const PruneSel *sel = a.sel;
     if (!sel->partial) return;
+    if (sel->wincnt) {  // counted by the windowed pass: gather tau's bin column
+        const uint32_t d = sel->tau_d;
+        const int64_t n = a.n_tiles * kPruneWarps;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            a.tile_ties[i] = a.tile_win[i * kWinCnt + d];
+        return;
+    }
     const uint32_t tau = sel->tau;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __shared__ uint32_t s_c;
@@ -633,6 +913,7 @@ __global__ void k_prune_info(PruneArgs a, long long *d_info, int32_t *d_status) 
         d_info[2] = none ? 0 : sel->above;
         d_info[3] = none ? 0 : sel->keep_ties;
         d_info[4] = none ? 0 : sel->tie_local;
+        d_info[5] = sel->missed | (sel->partial && sel->wincnt ? 2 : 0);  // flags
     }
     if (d_status) *d_status = sel->status;
 }
@@ -654,15 +935,23 @@ __global__ void k_prune_begin(PruneSel *sel, long long k) {
     sel->status = DYNMO_OK;
     sel->n_global = 0;
     sel->done = 0;
+    sel->win_lo = 0u;
+    sel->win_hi = 0x7FFFu;
+    sel->miss = 0;
+    sel->missed = 0;
+    sel->wincnt = 0;
 }
 
 // Resident blocks per SM of the streaming kernels (grid = SMs x this).
 int prune_blocks_per_sm(int kind) {
     int nb = 1;
     switch (kind) {
-        case 0:
-            cudaFuncSetAttribute(k_prune_hist0, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins0 * 4);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist0, kHist0Threads, kBins0 * 4);
+        case 0: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist0w, kPruneThreads, 0); break;
+        case 30:
+        case 32:  // the full-width histogram passes (sample, miss): 128 KB of shared memory
+            cudaFuncSetAttribute(k_prune_hist0<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins0 * 4);
+            cudaFuncSetAttribute(k_prune_hist0<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBins0 * 4);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist0<1>, kHist0Threads, kBins0 * 4);
             break;
         case 1: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<1>, kPruneThreads, 0); break;
         case 2: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_prune_hist<2>, kPruneThreads, 0); break;
@@ -674,12 +963,16 @@ int prune_blocks_per_sm(int kind) {
 
 cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream_t s) {
     switch (pass_kind) {
-        case 0: return launch_pdl(k_prune_hist0, grid, kHist0Threads, (size_t)kBins0 * 4, s, a);
+        case 0: return launch_pdl(k_prune_hist0w, grid, kPruneThreads, 0, s, a);
+        case 30: return launch_pdl(k_prune_hist0<0>, grid, kHist0Threads, (size_t)kBins0 * 4, s, a);
+        case 31: return launch_pdl(k_prune_window, 1, 1024, 0, s, a);
+        case 32: return launch_pdl(k_prune_hist0<1>, grid, kHist0Threads, (size_t)kBins0 * 4, s, a);
         case 1: return launch_pdl(k_prune_hist<1>, grid, kPruneThreads, 0, s, a);
         case 2: return launch_pdl(k_prune_hist<2>, grid, kPruneThreads, 0, s, a);
-        case 10: return launch_pdl(k_prune_select<0>, 1, 1024, 0, s, a);
-        case 11: return launch_pdl(k_prune_select<1>, 1, 1024, 0, s, a);
-        case 12: return launch_pdl(k_prune_select<2>, 1, 1024, 0, s, a);
+        case 10: return launch_pdl(k_prune_select<0, 0>, 1, 1024, 0, s, a);
+        case 11: return launch_pdl(k_prune_select<1, 0>, 1, 1024, 0, s, a);
+        case 12: return launch_pdl(k_prune_select<2, 0>, 1, 1024, 0, s, a);
+        case 13: return launch_pdl(k_prune_select<0, 1>, 1, 1024, 0, s, a);
         case 20: return launch_pdl(k_prune_ties, 1, 32, 0, s, a);
         case 21: return launch_pdl(k_prune_tiecount, grid, kPruneThreads, 0, s, a);
         case 22: return launch_pdl(k_prune_tiescan, 1, 1024, 0, s, a);

@@ -481,10 +481,10 @@ class PrunePlan:
 
 def global_prune(ctx: Context, plan: PrunePlan, k: int, info=None, status=None, stream=None):
     """Alg. 1 (collective): masks of the k globally largest |w|.  Returns
-    (info[5] int64, status[1] int32) device tensors."""
+    (info[6] int64, status[1] int32) device tensors."""
     dev = torch.device("cuda", ctx.device)
     if info is None:
-        info = torch.empty(5, dtype=torch.int64, device=dev)
+        info = torch.empty(6, dtype=torch.int64, device=dev)
     if status is None:
         status = torch.empty(1, dtype=torch.int32, device=dev)
     _check(lib().dynmo_global_prune(ctx.handle, plan.handle, int(k), _ptr(info), _ptr(status), _stream(stream)),

@@ -776,6 +776,76 @@ def test_global_prune_bf16_unaligned_masks_specials(D, ctx):
     plan.close()
 
 
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_global_prune_window_hit_and_miss(D, ctx, dtype):
+    """The first digit's bin window comes from a sample of every 16th tile.
+    (a) Homogeneous weights (20 x 32768 + ragged): the window holds the k-th
+    key (info[5] = 0).  (b) Adversarial: the sampled tiles (0 and 16) hold
+    N(0, 100) weights, the rest N(0, 0.01), so the estimate is far off; the
+    full histogram and the second select run (info[5] = 1).  Masks == the
+    oracle's in both, f32 plans continuing with passes 1 and 2."""
+    T = 32768
+    n = 20 * T + 1234
+    g = np.random.default_rng(11)
+    for adversarial, ks in [(False, [n // 10, n // 2]), (True, [n // 3, 2 * T + 1000])]:
+        x = g.normal(0.0, 1.0, n)
+        if adversarial:
+            x *= 0.01
+            for t in (0, 16):
+                x[t * T:(t + 1) * T] = g.normal(0.0, 100.0, T)
+        if dtype == "f32":
+            w = x.astype(np.float32)
+            shard, val = torch.from_numpy(w).to(DEV), w.astype(np.float64)
+        else:
+            t16 = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+            shard = t16.to(DEV)
+            val = oracle.bf16_to_f64(t16.view(torch.int16).numpy().view(np.uint16))
+        mask = torch.zeros(n, dtype=torch.uint8, device=DEV)
+        plan = D.PrunePlan(ctx, [(shard, mask)])
+        for k in ks:
+            info, st = D.global_prune(ctx, plan, k)
+            torch.cuda.synchronize()
+            ost, omask = oracle.global_prune([val], k)
+            assert int(st.item()) == ost == 0
+            assert np.array_equal(mask.cpu().numpy(), omask[0]), (adversarial, k)
+            assert (int(info[5].item()) & 1) == int(adversarial), (adversarial, k)
+            if dtype == "bf16" and not adversarial and k == n // 10:
+                # a window of ~10 bins and a partial tie share: the tie counts
+                # come from the windowed pass (flag bit 1)
+                assert int(info[5].item()) == 2
+        plan.close()
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_global_prune_wide_window_clamped(D, ctx, dtype):
+    """Magnitudes log-uniform over 2^-120 .. 2^0 (≈ 15000 first-digit bins)
+    and small k: the estimated window is wider than the 4096 bins of the
+    windowed pass and is clamped around the estimate (k = 1 still hits);
+    k near N takes lo = 0.  Masks == the oracle's."""
+    T = 32768
+    n = 3 * T + 77
+    g = np.random.default_rng(12)
+    x = np.exp2(g.uniform(-120.0, 0.0, n)) * np.where(g.random(n) < 0.5, -1.0, 1.0)
+    if dtype == "f32":
+        w = x.astype(np.float32)
+        shard, val = torch.from_numpy(w).to(DEV), w.astype(np.float64)
+    else:
+        t16 = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+        shard = t16.to(DEV)
+        val = oracle.bf16_to_f64(t16.view(torch.int16).numpy().view(np.uint16))
+    mask = torch.zeros(n, dtype=torch.uint8, device=DEV)
+    plan = D.PrunePlan(ctx, [(shard, mask)])
+    for k in [1, 100, 5000, n - 50, n]:
+        info, st = D.global_prune(ctx, plan, k)
+        torch.cuda.synchronize()
+        ost, omask = oracle.global_prune([val], k)
+        assert int(st.item()) == ost == 0
+        assert np.array_equal(mask.cpu().numpy(), omask[0]), k
+        if k == 1:
+            assert (int(info[5].item()) & 1) == 0
+    plan.close()
+
+
 def test_global_prune_errors_and_nan(D, ctx):
     """k > N: INVALID, all masks 0; a NaN is never kept and sets INVALID
     (the selection runs over the other weights, like the oracle)."""
@@ -816,6 +886,7 @@ def test_global_prune_config2_full_size(D, ctx):
     tau = int(inf[0])
     kept = sum(int(m.sum(dtype=torch.int64).item()) for m in ms)
     assert kept == k and inf[2] + inf[3] == k
+    assert inf[5] == 2  # window hit, tie counts from the windowed pass (the bench's path)
     kmin = min(float(w.float().abs()[m.bool()].min().item()) for w, m in zip(ws, ms) if int(m.sum().item()) > 0)
     pmax = max(float(w.float().abs()[~m.bool()].max().item()) for w, m in zip(ws, ms) if int((m == 0).sum().item()) > 0)
     assert kmin >= pmax

@@ -6,7 +6,9 @@ layers (histogram passes + NCCL all-reduces + mask pass), captured in a CUDA
 graph, timed with CUDA events; max over ranks.  Algorithmic HBM bytes per
 rank and call: (1 histogram pass + 1 mask pass) x weight bytes (reads) + 1 B
 per weight (mask writes) [+ one more read of the weights when a rank holds a
-partial share of the threshold ties].
+partial share of the threshold ties that the windowed pass did not count
+(d_info[5] bit 1 clear), + one when the bin window missed (bit 0)].  The
+1/16 tile sample is not counted (overhead of this design, not of Alg. 1).
 
 python tools/bench_prune.py  |  torchrun --nproc-per-node G ... tools/bench_prune.py
 """
@@ -55,7 +57,7 @@ def main():
     ms = [torch.empty(P, dtype=torch.uint8, device=dev) for _ in ws]
     plan = D.PrunePlan(ctx, list(zip(ws, ms)))
     k = int(L * P * (1 - 0.9))
-    info = torch.empty(5, dtype=torch.int64, device=dev)
+    info = torch.empty(6, dtype=torch.int64, device=dev)
     st = torch.empty(1, dtype=torch.int32, device=dev)
     mark("eager call")
     D.global_prune(ctx, plan, k, info=info, status=st)
@@ -91,9 +93,11 @@ def main():
     mark("info read")
     kept_local = sum(int(m.sum(dtype=torch.int64).item()) for m in ms)
     partial = 0 < inf[3] < inf[4]
+    flags = int(inf[5])
     wbytes = count * P * 2
     passes = 1  # all bf16: the 15-bit first digit is the whole magnitude
-    alg_bytes = (passes + 1 + (1 if partial else 0)) * wbytes + count * P
+    extra = (1 if partial and not flags & 2 else 0) + (1 if flags & 1 else 0)
+    alg_bytes = (passes + 1 + extra) * wbytes + count * P
     v = torch.tensor([float(np.median(ts)), float(alg_bytes), float(kept_local)], dtype=torch.float64, device=dev)
     if G > 1:
         mx = v.clone()
@@ -107,7 +111,7 @@ def main():
         print(json.dumps({
             "workload": "Alg. 1 global magnitude pruning, config-2 weights: 48 x 12.58 M bf16 (604 M), S = 0.9",
             "n_gpus": G, "ms_per_call": round(ms_, 4), "k": k, "kept_total": int(tot[2]),
-            "status": int(st.item()), "tau_key": int(inf[0]),
+            "status": int(st.item()), "tau_key": int(inf[0]), "flags": flags,
             "max_rank_alg_bytes": int(mx[1]),
             "hbm_GBps_max_rank": round(float(mx[1]) / (ms_ * 1e-3) / 1e9, 1),
         }), flush=True)
