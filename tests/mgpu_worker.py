@@ -246,6 +246,31 @@ def main():
         for j, m in enumerate(mk):
             assert np.array_equal(m.cpu().numpy(), om[first + j]), (rank, kk, j)
     pplan.close()
+    # the same over all-bf16 shards of several 32768-element tiles per rank
+    # (N(0, 1) weights: ties of the threshold bin on every rank): the bin
+    # window holds the k-th key and, on the rank with the partial tie share,
+    # the tie counts come from the windowed pass (d_info[5] bit 1)
+    shards_all, vals_all = [], []
+    for r in range(world):
+        gr = np.random.default_rng(900 + r)
+        x = gr.normal(0, 1, 3 * 32768 + 500 * (r + 1))
+        tb = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+        shards_all.append(tb)
+        vals_all.append(oracle.bf16_to_f64(tb.view(torch.int16).numpy().view(np.uint16)))
+    wt = shards_all[rank].to(dev)
+    mk = torch.zeros(wt.numel(), dtype=torch.uint8, device=dev)
+    pplan = D.PrunePlan(ctx, [(wt, mk)])
+    Ntot = sum(v.size for v in vals_all)
+    for kk in (Ntot // 10, Ntot // 5):
+        info, pst2 = D.global_prune(ctx, pplan, kk)
+        torch.cuda.synchronize()
+        ost2, om = oracle.global_prune(vals_all, kk)
+        assert int(pst2.item()) == ost2 == 0
+        assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk)
+        flags = torch.tensor([int(info[5].item())], device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX)
+        assert int(flags.item()) == 2, (rank, kk, int(flags.item()))  # hit; counted ties on the partial rank
+    pplan.close()
     # Releasing GPUs after re-packing: split the ctx -- even
     # ranks stay active, odd ranks are released (None) -- then the smaller
     # group profiles, partitions and maps its stages onto its own ranks
