@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
     const PruneSel *sel = a.sel;
     if (sel->done) return;
     const uint32_t lo = sel->win_lo, hi = sel->win_hi;
+    DYNMO_DCHECK(lo <= hi && hi - lo < kWinMax && hi < (uint32_t)kBins0);
     uint32_t *sh0 = shw - lo;  // indexed by the digit
     for (uint32_t i = lo + threadIdx.x; i <= hi; i += kPruneThreads) sh0[i] = 0u;
     if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
@@ -269,6 +270,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        DYNMO_DCHECK(seen >= s_cnt[0] + s_cnt[1] + s_cnt[2]);
         const unsigned long long above = seen - s_cnt[0] - s_cnt[1] - s_cnt[2];
         if (s_cnt[0]) atomicAdd(&a.hist_local[kBins0], s_cnt[0]);
         if (above) atomicAdd(&a.hist_local[hi + 1], above);      // above > 0 => hi < 0x7FFF
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(1024) k_prune_window(PruneArgs a) {
         lo = 0;
         hi = kWinMax - 1;
     }
+    DYNMO_DCHECK(lo <= hi && hi - lo < kWinMax && hi < (uint32_t)kBins0);
     if (threadIdx.x == 0) {
         sel->win_lo = lo;
         sel->win_hi = hi;
@@ -543,6 +546,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_tiecount(PruneArgs a) {
     if (!sel->partial) return;
     if (sel->wincnt) {  // counted by the windowed pass: gather tau's bin column
         const uint32_t d = sel->tau_d;
+        DYNMO_DCHECK(d < (uint32_t)kWinCnt && a.tile_win != nullptr);
         const int64_t n = a.n_tiles * kPruneWarps;
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
             a.tile_ties[i] = a.tile_win[i * kWinCnt + d];
