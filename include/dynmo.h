@@ -408,6 +408,15 @@ dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan plan, int32_t n
                                       int32_t n_new, const int32_t *d_bnd_new,
                                       const int32_t *d_rank_new, int64_t *d_bytes_sent,
                                       int64_t *d_bytes_recv, dynmo_stream stream);
+/* SM budget of dynmo_migrate_layers_dev's pull kernel: at most max_ctas
+ * CTAs of 512 threads (0 = one per SM, the default; clamped to the SM
+ * count).  For a migration overlapped with backward compute on another
+ * stream ("moving layers while the gradients calculation take
+ * place"): each CTA keeps 64 KB of NVLink loads in flight, so
+ * a small budget still fills the link while the other SMs compute.  Host
+ * setting, takes effect at the next call (and at graph capture).  INVALID if
+ * max_ctas < 0. */
+dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
 /* Sticky device error of the peer-memory paths (0 = none); synchronous. */
 dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
 

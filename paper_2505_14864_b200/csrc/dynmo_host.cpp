@@ -1142,6 +1142,7 @@ struct dynmo_mplan_s {
     std::vector<void *> opened;                         // IPC mappings to close
     DevBuf *d_src_tab = nullptr;                        // [nranks][n_layers*n_bufs] (device path)
     DevBuf *d_recv_tab = nullptr;                       // [n_layers*n_bufs]
+    int32_t max_ctas = 0;                               // device-driven pull: SM budget (0 = every SM)
 };
 
 namespace {
@@ -1287,8 +1288,16 @@ dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
-    CUDA_TRY(launch_mig_dev(a, ctx->num_sms, s), "migration kernels launch");
+    const bool budget = mp->max_ctas > 0 && mp->max_ctas < ctx->num_sms;
+    CUDA_TRY(launch_mig_dev(a, budget ? mp->max_ctas : ctx->num_sms, budget, s), "migration kernels launch");
     phase_end(te, s);
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas) {
+    if (!plan) return invalid("null plan");
+    if (max_ctas < 0) return invalid("max_ctas < 0");
+    plan->max_ctas = max_ctas;
     return DYNMO_OK;
 }
 

@@ -291,7 +291,7 @@ struct DevMigArgs {
     PeerWindow *peer_win[kMaxRanksEpi];
     int64_t *bytes_sent, *bytes_recv;  // nullable
 };
-cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
 
 struct P2PItem {
     const void *src;

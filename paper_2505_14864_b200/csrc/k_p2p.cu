@@ -192,6 +192,11 @@ __global__ void k_mig_signal(DevMigArgs a) {
 // Receiver side: every block derives the incoming set, waits for the senders,
 // copies its grid-stride share of every incoming buffer; the last block
 // releases ddone[me] at every sender.
+// U = 16-byte NVLink loads in flight per thread: 4 with one CTA per SM (the
+// full-GPU migration: finer tail), 16 under an SM budget (the migration
+// overlapped with compute: 128 KB per CTA, so 16-32 CTAs cover the peer
+// latency; bench_overlap.py)
+template <int U>
 __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -228,12 +233,12 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
                 const uint4 *s4 = (const uint4 *)sp;
                 uint4 *d4 = (uint4 *)dp;
                 uint64_t x = gt;
-                for (; x + 3 * gs < nvec; x += 4 * gs) {
-                    const uint4 q0 = s4[x], q1 = s4[x + gs], q2 = s4[x + 2 * gs], q3 = s4[x + 3 * gs];
-                    d4[x] = q0;
-                    d4[x + gs] = q1;
-                    d4[x + 2 * gs] = q2;
-                    d4[x + 3 * gs] = q3;
+                for (; x + (U - 1) * gs < nvec; x += U * gs) {
+                    uint4 q[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
                 }
                 for (; x < nvec; x += gs) d4[x] = s4[x];
                 for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
@@ -272,9 +277,11 @@ __global__ void k_mig_wait(DevMigArgs a) {
 
 }  // namespace
 
-cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, cudaStream_t s) {
+cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s) {
     cudaError_t e = launch_pdl(k_mig_signal, 1, 256, 0, s, a);
-    if (e == cudaSuccess) e = launch_pdl(k_mig_pull, grid, kP2PThreads, 0, s, a);
+    if (e == cudaSuccess)
+        e = budget ? launch_pdl(k_mig_pull<16>, grid, kP2PThreads, 0, s, a)
+                   : launch_pdl(k_mig_pull<4>, grid, kP2PThreads, 0, s, a);
     if (e == cudaSuccess) e = launch_pdl(k_mig_wait, 1, 256, 0, s, a);
     return e != cudaSuccess ? e : cudaGetLastError();
 }

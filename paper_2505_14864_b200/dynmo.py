@@ -429,6 +429,11 @@ class PeerMigrator:
                                               _ptr(bytes_sent), _ptr(bytes_recv), _stream(stream)),
                "dynmo_migrate_layers_dev")
 
+    def set_ctas(self, max_ctas: int):
+        """dynmo_migrate_plan_set_ctas: SM budget of the device-driven pull
+        (0 = every SM), for a migration overlapped with compute."""
+        _check(lib().dynmo_migrate_plan_set_ctas(self._h, int(max_ctas)), "dynmo_migrate_plan_set_ctas")
+
     def error(self) -> int:
         e = C.c_int32(0)
         _check(lib().dynmo_ctx_p2p_error(self.ctx.handle, C.byref(e)), "dynmo_ctx_p2p_error")

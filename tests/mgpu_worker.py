@@ -141,6 +141,24 @@ def main():
         torch.cuda.synchronize()
         for l, bufs in recv.items():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "graph", rep)
+    # NEXT-3 overlap: the pull under a 2-CTA SM budget on a side stream while
+    # the main stream runs a GEMM (the backward stand-in): byte-exact
+    pm.set_ctas(2)
+    side = torch.cuda.Stream(device=dev)
+    for bufs in recv.values():
+        bufs[0].zero_()
+    A = torch.randn(2048, 2048, device=dev, dtype=torch.bfloat16)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        pm.device(d_bo, d_ro, bnd, d_rn, bs, br)
+    for _ in range(8):
+        A = (A @ A).clamp_(-1, 1)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    assert (int(bs.item()), int(br.item())) == (want_sent, want_got), (rank, "budget")
+    for l, bufs in recv.items():
+        assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "budget")
+    pm.set_ctas(0)
     assert pm.error() == 0
     pm.close()
     # NEXT-3 placement: the new stages on capacity slots (slot j on GPU
