@@ -485,7 +485,7 @@ void dynmo_prune_plan_destroy(dynmo_pplan plan);
  *           as f32; -1 if nothing is kept), global non-NaN count, global
  *           count above tau, ties kept on this rank, ties on this rank,
  *           flags: bit 0 = the first digit's bin window (estimated from a
- *           1/16 tile sample) missed and the full first-digit histogram
+ *           1/32 tile sample) missed and the full first-digit histogram
  *           ran; bit 1 = the tie counts came from the windowed pass (no
  *           tie-count pass over the weights)}.
  *   d_status [1] int32 out: OK; INVALID if k > global non-NaN count (all

@@ -166,8 +166,8 @@ struct PruneTile {
 };
 static_assert(sizeof(PruneTile) == 24, "prune tile layout");
 constexpr uint32_t kPruneTileElems = 32768;
-constexpr int64_t kPruneSampleStride = 16;
-constexpr int kWinCnt = 16;  // windows up to 16 bins also record per-(tile, warp range) bin counts  // pass-0 sample: every 16th tile (1/16 of the weights)
+constexpr int64_t kPruneSampleStride = 32;  // pass-0 sample: every 32nd tile
+constexpr int kWinCnt = 16;  // windows up to 16 bins also record per-(tile, warp range) bin counts
 
 struct PruneSel {  // device-side selection state of one call
     long long k, k_rem, above, tie_local, keep_ties, n_global;

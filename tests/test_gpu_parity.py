@@ -778,9 +778,9 @@ def test_global_prune_bf16_unaligned_masks_specials(D, ctx):
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 def test_global_prune_window_hit_and_miss(D, ctx, dtype):
-    """The first digit's bin window comes from a sample of every 16th tile.
+    """The first digit's bin window comes from a sample of every 32nd tile.
     (a) Homogeneous weights (20 x 32768 + ragged): the window holds the k-th
-    key (info[5] = 0).  (b) Adversarial: the sampled tiles (0 and 16) hold
+    key (info[5] = 0).  (b) Adversarial: tiles 0 (the sample) and 16 hold
     N(0, 100) weights, the rest N(0, 0.01), so the estimate is far off; the
     full histogram and the second select run (info[5] = 1).  Masks == the
     oracle's in both, f32 plans continuing with passes 1 and 2."""

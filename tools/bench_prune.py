@@ -8,7 +8,7 @@ rank and call: (1 histogram pass + 1 mask pass) x weight bytes (reads) + 1 B
 per weight (mask writes) [+ one more read of the weights when a rank holds a
 partial share of the threshold ties that the windowed pass did not count
 (d_info[5] bit 1 clear), + one when the bin window missed (bit 0)].  The
-1/16 tile sample is not counted (overhead of this design, not of Alg. 1).
+1/32 tile sample is not counted (overhead of this design, not of Alg. 1).
 
 python tools/bench_prune.py  |  torchrun --nproc-per-node G ... tools/bench_prune.py
 """
