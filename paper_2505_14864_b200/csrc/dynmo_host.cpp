@@ -713,7 +713,8 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     const size_t sz_tt = up(sizeof(uint32_t) * nt * 8), sz_to = up(sizeof(unsigned long long) * nt * 8);
     // per-(tile, warp range) window-bin counts (bf16-only plans: ties on the first digit)
     const size_t sz_tw = any_f32 ? 0 : up(sizeof(uint16_t) * nt * 8 * kWinCnt);
-    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to + sz_tw;
+    const size_t sz_tot = up(sizeof(uint32_t) * nt);
+    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to + sz_tw + sz_tot;
     DeviceGuard g(ctx->device);
     auto *pl = new dynmo_pplan_s();
     pl->ctx = ctx;
@@ -733,6 +734,8 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     a.tile_ties = (uint32_t *)b; b += sz_tt;
     a.tile_off = (unsigned long long *)b; b += sz_to;
     a.tile_win = sz_tw ? (uint16_t *)b : nullptr;
+    b += sz_tw;
+    a.tile_tot = (uint32_t *)b;
     a.n_tiles = (int64_t)tiles.size();
     for (const PruneTile &t : tiles) a.n_elems += t.n;
     a.rank = ctx->rank;

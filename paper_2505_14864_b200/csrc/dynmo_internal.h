@@ -190,6 +190,7 @@ struct PruneArgs {
     uint32_t *tile_ties;              // [n_tiles]
     unsigned long long *tile_off;     // [n_tiles]
     uint16_t *tile_win;               // [n_tiles][8][kWinCnt] window-bin counts (bf16-only plans), else null
+    uint32_t *tile_tot;               // [n_tiles] tau's ties per tile (from tile_win)
     long long n_elems;                // this rank's weights
     int32_t rank, nranks, last_pass;
 };

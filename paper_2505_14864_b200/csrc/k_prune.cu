@@ -329,10 +329,15 @@ __device__ unsigned long long suffix_scan(const unsigned long long *h, unsigned 
     if (tid * PER + PER - 1 >= rlo && tid * PER <= rhi) {
         const uint4 *hv = (const uint4 *)(h + tid * PER);  // 16-byte loads (PER is 1 or even)
         if constexpr (PER >= 2) {
+            constexpr int NV = PER / 2, B = NV < 8 ? NV : 8;  // batches of 8 independent loads
 #pragma unroll
-            for (int j = 0; j < PER / 2; ++j) {
-                const uint4 x = hv[j];
-                mine += ((unsigned long long)x.y << 32 | x.x) + ((unsigned long long)x.w << 32 | x.z);
+            for (int j0 = 0; j0 < NV; j0 += B) {
+                uint4 x[B];
+#pragma unroll
+                for (int j = 0; j < B; ++j) x[j] = ld_nc(hv + j0 + j);
+#pragma unroll
+                for (int j = 0; j < B; ++j)
+                    mine += ((unsigned long long)x[j].y << 32 | x[j].x) + ((unsigned long long)x[j].w << 32 | x[j].z);
             }
         } else {
             mine = h[tid];
@@ -351,42 +356,44 @@ __device__ unsigned long long suffix_scan(const unsigned long long *h, unsigned 
 
 // Block-wide, after suffix_scan: the bin b with suffix(b) >= r > suffix(b+1)
 // (the bin of the r-th largest key, 1 <= r <= total) and suffix(b + 1), for
-// every thread.
+// every thread.  The thread whose range holds it is found from s_part; then
+// warp 0 loads that range (one bin per lane, one round of loads) and finds
+// the bin by a suffix sum over the lanes and a ballot.
 template <int NB>
 __device__ void find_bin(const unsigned long long *h, const unsigned long long *s_part, unsigned long long r,
                          int *bin, unsigned long long *above) {
     constexpr int PER = NB / 1024;
-    __shared__ int s_bin;
+    static_assert(PER <= 32, "one bin per lane");
+    __shared__ int s_owner, s_bin;
     __shared__ unsigned long long s_above;
     const int tid = threadIdx.x;
     const unsigned long long above_thread = tid + 1 < 1024 ? s_part[tid + 1] : 0ull;
-    if (above_thread < r && s_part[tid] >= r) {
-        unsigned long long acc = above_thread;
-        int b = tid * PER + PER - 1;
-        bool found = false;
-        // this thread's bins from the top, 8 independent loads at a time
-        for (int j0 = PER - 1; j0 >= 0 && !found; j0 -= 8) {
-            unsigned long long c[8];
+    if (tid == 0) s_owner = 0;  // (r outside [1, total] is a caller bug: stay in bounds)
+    __syncthreads();
+    if (above_thread < r && s_part[tid] >= r) s_owner = tid;
+    __syncthreads();
+    if (tid < 32) {
+        const int o = s_owner, lane = tid;
+        const unsigned long long base = o + 1 < 1024 ? s_part[o + 1] : 0ull;
+        const unsigned long long c = lane < PER ? h[o * PER + lane] : 0ull;
+        unsigned long long suf = c;  // sum of the owner's bins >= lane
 #pragma unroll
-            for (int q = 0; q < 8; ++q) c[q] = j0 - q >= 0 ? h[tid * PER + j0 - q] : 0ull;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (found || j0 - q < 0) continue;
-                if (acc + c[q] >= r) {
-                    b = tid * PER + j0 - q;
-                    found = true;
-                } else {
-                    acc += c[q];
-                }
-            }
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long y = __shfl_down_sync(0xFFFFFFFFu, suf, d);
+            if (lane + d < 32) suf += y;
         }
-        s_bin = b;
-        s_above = acc;
+        const unsigned hit = __ballot_sync(0xFFFFFFFFu, lane < PER && base + suf >= r);
+        const int b = hit ? 31 - __clz(hit) : 0;  // the highest such bin: suffix(b) >= r > suffix(b + 1)
+        const unsigned long long sb1 = __shfl_sync(0xFFFFFFFFu, suf, (b + 1) & 31);
+        if (lane == 0) {
+            s_bin = o * PER + b;
+            s_above = base + (b + 1 < PER ? sb1 : 0ull);
+        }
     }
     __syncthreads();
     *bin = s_bin;
     *above = s_above;
-    __syncthreads();  // s_bin / s_above are reused by the next call
+    __syncthreads();  // s_owner / s_bin / s_above are reused by the next call
 }
 
 // Pass-0 bin window from the sample histogram (one block): the sample holds
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(1024) k_prune_window(PruneArgs a) {
         const double rh = r - d, rl = ceil(r + d);
         int b;
         unsigned long long acc;
-        if (rh >= 1.0) {
+        if (rh >= 1.0 && rh <= (double)S) {
             find_bin<kBins0>(h, s_part, (unsigned long long)rh, &b, &acc);
             hi = (uint32_t)b;
         }
@@ -544,12 +551,22 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_tiecount(PruneArgs a) {
     pdl_trigger();
     const PruneSel *sel = a.sel;
     if (!sel->partial) return;
-    if (sel->wincnt) {  // counted by the windowed pass: gather tau's bin column
+    if (sel->wincnt) {  // counted by the windowed pass: gather tau's bin column, and tile totals
         const uint32_t d = sel->tau_d;
         DYNMO_DCHECK(d < (uint32_t)kWinCnt && a.tile_win != nullptr);
-        const int64_t n = a.n_tiles * kPruneWarps;
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-            a.tile_ties[i] = a.tile_win[i * kWinCnt + d];
+        for (int64_t ti = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ti < a.n_tiles;
+             ti += (int64_t)gridDim.x * blockDim.x) {
+            uint32_t c[kPruneWarps], tot = 0;
+#pragma unroll
+            for (int w = 0; w < kPruneWarps; ++w) {
+                c[w] = a.tile_win[(ti * kPruneWarps + w) * kWinCnt + d];
+                tot += c[w];
+            }
+            uint4 *tt = (uint4 *)(a.tile_ties + ti * kPruneWarps);
+            tt[0] = make_uint4(c[0], c[1], c[2], c[3]);
+            tt[1] = make_uint4(c[4], c[5], c[6], c[7]);
+            a.tile_tot[ti] = tot;
+        }
         return;
     }
     const uint32_t tau = sel->tau;
@@ -610,8 +627,10 @@ __global__ void __launch_bounds__(1024) k_prune_tiescan(PruneArgs a) {
     const int64_t n = a.n_tiles;
     const int64_t per = (n + 31) / 32;
     const int64_t b0 = w * per, e0 = b0 + per < n ? b0 + per : n;
+    const bool tot_ready = a.sel->wincnt != 0;  // the gather wrote per-tile totals
     auto total = [&](int64_t i) -> unsigned long long {  // tile i's ties (8 warp ranges, 32 B)
         if (i >= e0) return 0ull;
+        if (tot_ready) return a.tile_tot[i];
         const uint4 *p = (const uint4 *)(a.tile_ties + i * kPruneWarps);
         const uint4 x = p[0], y = p[1];
         return (unsigned long long)x.x + x.y + x.z + x.w + y.x + y.y + y.z + y.w;
