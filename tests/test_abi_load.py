@@ -43,6 +43,8 @@ def test_host_argument_validation_without_gpu():
     assert L.dynmo_ctx_create(0, 2, 0, None, ctypes.byref(out)) == _lib.E_INVALID  # no NCCL id
     assert L.dynmo_ctx_create(0, 1, 1, None, ctypes.byref(out)) == _lib.E_INVALID  # rank >= nranks
     assert L.dynmo_partition_stages(None, 1, 8, *([None] * 11)) == _lib.E_INVALID
+    assert L.dynmo_migrate_plan_set_ctas(None, 16) == _lib.E_INVALID  # null plan
+    assert L.dynmo_global_prune(None, None, 1, None, None, None) == _lib.E_INVALID  # null ctx / plan
 
 
 def test_migration_plan_vs_oracle():
