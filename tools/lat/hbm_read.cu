@@ -29,6 +29,34 @@ __global__ void rd(const uint4 *__restrict__ p, size_t n, unsigned *out) {
     if (acc == 0xFFFFFFFFu) *out = acc;
 }
 
+// 256-bit loads (ld.global...v8.b32, LDG.256 on sm_100): U loads of 32 B per thread
+struct u8x32 { unsigned a[8]; };
+__device__ __forceinline__ u8x32 ld_stream256(const uint4 *p) {
+    u8x32 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.a[0]), "=r"(v.a[1]), "=r"(v.a[2]), "=r"(v.a[3]), "=r"(v.a[4]), "=r"(v.a[5]),
+                   "=r"(v.a[6]), "=r"(v.a[7]) : "l"(p));
+    return v;
+}
+template <int U>
+__global__ void rd256(const uint4 *__restrict__ p, size_t n, unsigned *out) {
+    const size_t n2 = n / 2;  // 32-byte elements
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    unsigned acc = 0;
+    for (; i + (U - 1) * stride < n2; i += U * stride) {
+        u8x32 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ld_stream256(p + 2 * (i + u * stride));
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            acc += __popc(v[u].a[0] ^ v[u].a[1]) + __popc(v[u].a[2] ^ v[u].a[3]) + __popc(v[u].a[4] ^ v[u].a[5]) +
+                   __popc(v[u].a[6] ^ v[u].a[7]);
+    }
+    for (; i < n2; i += stride) acc += ld_stream256(p + 2 * i).a[0];
+    if (acc == 0xFFFFFFFFu) *out = acc;
+}
+
 // contiguous chunk per warp (k_profile's layout): each warp streams its own range
 template <int U>
 __global__ void rd_chunk(const uint4 *__restrict__ p, size_t n, unsigned *out) {
@@ -96,6 +124,9 @@ int main(int argc, char **argv) {
     };
     for (int bps : {4}) {
         run("grid-U8", rd<8>, sms * bps, 256);
+        run("g256-U4", rd256<4>, sms * bps, 256);
+        run("g256-U8", rd256<8>, sms * bps, 256);
+        run("g256-U4x2", rd256<4>, sms * bps * 2, 256);
         run("chunk-U8", rd_chunk<8>, sms * bps, 256);
         run("tiles-C1", rd_tiles<1>, sms * bps, 256);
         run("tiles-C2", rd_tiles<2>, sms * bps, 256);
