@@ -209,15 +209,21 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
                 const uint32_t q[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+                uint32_t m[4], in[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const uint32_t m = q[e] & 0x7FFF7FFFu;
-                    const uint32_t ge = m + CL, ah = m + CH;
-                    nacc |= m + CN;
+                    m[e] = q[e] & 0x7FFF7FFFu;
+                    const uint32_t ge = m[e] + CL, ah = m[e] + CH;
+                    nacc |= m[e] + CN;
                     pb += (~ge & H) >> 15;
-                    const uint32_t in = ge & ~ah & H;  // lo <= m <= hi (NaN bins dropped at the flush)
-                    if (in & 0x8000u) atomicAdd(&wbin[m & 0x7FFFu], 1u);  // (a predicated red.shared
-                    if (in >> 16) atomicAdd(&wbin[m >> 16], 1u);        //  measured slower)
+                    in[e] = ge & ~ah & H;  // lo <= m <= hi (NaN bins dropped at the flush)
+                }
+                if (in[0] | in[1] | in[2] | in[3]) {  // one branch per vector (in-window keys are rare)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        if (in[e] & 0x8000u) atomicAdd(&wbin[m[e] & 0x7FFFu], 1u);  // (a predicated
+                        if (in[e] >> 16) atomicAdd(&wbin[m[e] >> 16], 1u);        //  red.shared was slower)
+                    }
                 }
             }
         }
