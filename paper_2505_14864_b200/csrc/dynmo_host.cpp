@@ -714,7 +714,8 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     // per-(tile, warp range) window-bin counts (bf16-only plans: ties on the first digit)
     const size_t sz_tw = any_f32 ? 0 : up(sizeof(uint16_t) * nt * 8 * kWinCnt);
     const size_t sz_tot = up(sizeof(uint32_t) * nt);
-    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to + sz_tw + sz_tot;
+    const size_t sz_cw = up(sizeof(unsigned long long) * kPruneCw);
+    const size_t total = sz_tiles + 2 * sz_hist + sz_sel + sz_tie + sz_tt + sz_to + sz_tw + sz_tot + 2 * sz_cw;
     DeviceGuard g(ctx->device);
     auto *pl = new dynmo_pplan_s();
     pl->ctx = ctx;
@@ -735,7 +736,9 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     a.tile_off = (unsigned long long *)b; b += sz_to;
     a.tile_win = sz_tw ? (uint16_t *)b : nullptr;
     b += sz_tw;
-    a.tile_tot = (uint32_t *)b;
+    a.tile_tot = (uint32_t *)b; b += sz_tot;
+    a.cw_local = (unsigned long long *)b; b += sz_cw;
+    a.cw_global = (unsigned long long *)b;
     a.n_tiles = (int64_t)tiles.size();
     for (const PruneTile &t : tiles) a.n_elems += t.n;
     a.rank = ctx->rank;
@@ -778,9 +781,10 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
     const PruneArgs &a = plan->args;
     const bool multi = ctx->nranks > 1;
     CUDA_TRY(launch_prune_begin(a.sel, (long long)k, s), "k_prune_begin");
-    auto all_reduce = [&](int count) -> dynmo_status {
+    auto all_reduce = [&](int count, bool compact = false) -> dynmo_status {
         if (!multi) return DYNMO_OK;
-        const ncclResult_t r = ncclAllReduce(a.hist_local, a.hist_global, count, ncclUint64, ncclSum, ctx->comm, s);
+        const ncclResult_t r = compact ? ncclAllReduce(a.cw_local, a.cw_global, count, ncclUint64, ncclSum, ctx->comm, s)
+                                       : ncclAllReduce(a.hist_local, a.hist_global, count, ncclUint64, ncclSum, ctx->comm, s);
         if (r != ncclSuccess) {
             g_err = std::string("ncclAllReduce (prune): ") + ncclGetErrorString(r);
             return DYNMO_E_NCCL;
@@ -796,8 +800,8 @@ dynmo_status dynmo_global_prune(dynmo_ctx ctx, dynmo_pplan plan, int64_t k, int6
     if ((st = all_reduce(32770)) != DYNMO_OK) return st;
     CUDA_TRY(launch_prune(a, 31, 1, s), "k_prune_window");
     CUDA_TRY(launch_prune(a, 0, plan->grid[0], s), "k_prune_hist0w");
-    if ((st = all_reduce(32769)) != DYNMO_OK) return st;
-    CUDA_TRY(launch_prune(a, 10, 1, s), "k_prune_select");
+    if ((st = all_reduce(kPruneCw, true)) != DYNMO_OK) return st;  // the compact window histogram
+    CUDA_TRY(launch_prune(a, 10, 1, s), "k_prune_select_win");
     CUDA_TRY(launch_prune(a, 32, plan->grid[32], s), "k_prune_hist0 (on a miss)");
     if ((st = all_reduce(32769)) != DYNMO_OK) return st;
     CUDA_TRY(launch_prune(a, 13, 1, s), "k_prune_select (on a miss)");

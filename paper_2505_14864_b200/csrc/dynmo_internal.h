@@ -167,7 +167,8 @@ struct PruneTile {
 static_assert(sizeof(PruneTile) == 24, "prune tile layout");
 constexpr uint32_t kPruneTileElems = 32768;
 constexpr int64_t kPruneSampleStride = 32;  // pass-0 sample: every 32nd tile
-constexpr int kWinCnt = 16;  // windows up to 16 bins also record per-(tile, warp range) bin counts
+constexpr int kWinCnt = 16;
+constexpr int kPruneCw = 4097;  // counters of the windowed pass's compact histogram (4096 bins + NaN)  // windows up to 16 bins also record per-(tile, warp range) bin counts
 
 struct PruneSel {  // device-side selection state of one call
     long long k, k_rem, above, tie_local, keep_ties, n_global;
@@ -191,6 +192,8 @@ struct PruneArgs {
     unsigned long long *tile_off;     // [n_tiles]
     uint16_t *tile_win;               // [n_tiles][8][kWinCnt] window-bin counts (bf16-only plans), else null
     uint32_t *tile_tot;               // [n_tiles] tau's ties per tile (from tile_win)
+    unsigned long long *cw_local;     // [4097] the windowed pass's compact histogram (k_prune.cu kCw)
+    unsigned long long *cw_global;    // [4097] all-reduced (nranks > 1)
     long long n_elems;                // this rank's weights
     int32_t rank, nranks, last_pass;
 };

@@ -26,7 +26,13 @@ constexpr int kPruneThreads = 256;
 constexpr int kBins0 = 32768;  // pass 0 digit: key bits 30..16 (15 bits = a bf16 magnitude)
 constexpr int kBins1 = 1024;   // pass 1 digit: key bits 15..6; pass 2: bits 5..0 (64 of the bins)
 constexpr int kHist0Threads = 1024;  // pass 0: one 128 KB shared histogram per block, one block per SM
-constexpr uint32_t kWinMax = 4096;   // widest pass-0 window (bins) of the windowed pass: 16 KB shared
+constexpr uint32_t kWinMax = 4094;   // widest pass-0 window (bins) of the windowed pass: 16 KB shared
+// The windowed pass's histogram in compact form (the only counters its
+// all-reduce carries): bin 0 = keys below the window, 1 .. W = digits lo .. hi,
+// W + 1 = keys above the window (W <= kWinMax, so W + 2 <= kCw); NaN count last.
+constexpr int kCw = 4096;
+constexpr int kCwNan = kCw;  // cw[kCwNan]; arrays of kCw + 1 = kPruneCw counters
+static_assert(kCw + 1 == kPruneCw, "compact histogram size");
 constexpr uint32_t kNanKey = 0x7F800000u;  // key > this: NaN
 constexpr int kPruneWarps = kPruneThreads / 32;  // tie-offset entries per tile
 constexpr int kU = 8;  // 16-byte loads in flight per thread in the streaming passes
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
     const uint32_t top = hi < (kNanKey >> 16) ? hi : (kNanKey >> 16);
     for (uint32_t b = lo + threadIdx.x; b <= top; b += kPruneThreads) {
         const uint32_t c = sh0[b];
-        if (c) atomicAdd(&a.hist_local[b], (unsigned long long)c);
+        if (c) atomicAdd(&a.cw_local[1 + (b - lo)], (unsigned long long)c);
         inw += c;
     }
 #pragma unroll
@@ -278,9 +284,9 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
     if (threadIdx.x == 0) {
         DYNMO_DCHECK(seen >= s_cnt[0] + s_cnt[1] + s_cnt[2]);
         const unsigned long long above = seen - s_cnt[0] - s_cnt[1] - s_cnt[2];
-        if (s_cnt[0]) atomicAdd(&a.hist_local[kBins0], s_cnt[0]);
-        if (above) atomicAdd(&a.hist_local[hi + 1], above);      // above > 0 => hi < 0x7FFF
-        if (s_cnt[1]) atomicAdd(&a.hist_local[lo - 1], s_cnt[1]);  // below > 0 => lo > 0
+        if (s_cnt[0]) atomicAdd(&a.cw_local[kCwNan], s_cnt[0]);
+        if (above) atomicAdd(&a.cw_local[hi - lo + 2], above);
+        if (s_cnt[1]) atomicAdd(&a.cw_local[0], s_cnt[1]);
     }
 }
 
@@ -457,11 +463,66 @@ __global__ void __launch_bounds__(1024) k_prune_window(PruneArgs a) {
     }
 }
 
+// Pass 0 after the windowed pass (one block): the bin of the k_rem-th
+// largest key in the compact histogram; a compact bin outside the window
+// (all keys below / above it) is a miss, left for the full histogram and
+// k_prune_select<0, 1>.  Clears the compact counters.
+__global__ void __launch_bounds__(1024) k_prune_select_win(PruneArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ unsigned long long s_part[1024];
+    PruneSel *sel = a.sel;
+    const unsigned long long *h = a.nranks > 1 ? a.cw_global : a.cw_local;
+    const uint32_t lo = sel->win_lo, W = sel->win_hi - lo + 1;
+    DYNMO_DCHECK(W >= 1 && W <= kWinMax);
+    const int tid = threadIdx.x;
+    const bool done0 = sel->done != 0;
+    if (tid == 0 && h[kCwNan]) sel->status = DYNMO_E_INVALID;  // NaN keys
+    const unsigned long long total = suffix_scan<kCw>(h, s_part, 0, (int)W + 1);
+    if (tid == 0) {  // the global number of non-NaN keys; validate k
+        sel->n_global = (long long)total;
+        if (!done0 && (sel->k > (long long)total)) {
+            sel->status = DYNMO_E_INVALID;
+            sel->done = 1;
+        }
+    }
+    __syncthreads();
+    const long long krem = sel->k_rem;
+    if (!done0 && !sel->done && krem > 0) {
+        int c;
+        unsigned long long acc;
+        find_bin<kCw>(h, s_part, (unsigned long long)krem, &c, &acc);
+        if (tid == 0) {
+            if (c == 0 || c == (int)W + 1) {
+                sel->miss = 1;
+            } else {
+                sel->k_rem = krem - (long long)acc;
+                sel->above += (long long)acc;
+                sel->prefix = lo + (uint32_t)c - 1;
+                sel->tie_local = (long long)a.cw_local[c];  // this rank's keys in the chosen bin
+                sel->missed = 0;
+                sel->wincnt = a.tile_win != nullptr && W <= (uint32_t)kWinCnt;
+                sel->tau_d = (uint32_t)c - 1;
+                sel->miss = 0;
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && !done0 && !sel->done && krem == 0) sel->done = 2;  // k = 0: nothing kept
+    for (int i = tid; i < (int)W + 2; i += 1024) {
+        a.cw_local[i] = 0ull;
+        if (a.nranks > 1) a.cw_global[i] = 0ull;
+    }
+    if (tid == 0) {
+        a.cw_local[kCwNan] = 0ull;
+        if (a.nranks > 1) a.cw_global[kCwNan] = 0ull;
+    }
+}
+
 // One block: locate the bin of the k_rem-th largest key in the (global)
 // histogram by a suffix scan, narrow the prefix, and clear both histograms.
-// Pass 0, MODE 0 (after the windowed pass): a bin outside the window (the
-// counts of all keys above / below it) means a miss -- the state is left
-// for MODE 1, which runs after the full histogram and only on a miss.
+// Passes 1 / 2 (f32 keys); pass 0 with MODE 1 runs after the full
+// first-digit histogram, only when the windowed pass missed.
 template <int PASS, int MODE>
 __global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
     pdl_wait();
@@ -474,10 +535,7 @@ __global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
     const int tid = threadIdx.x;
     const bool done0 = sel->done != 0;
     if (PASS == 0 && tid == 0 && h[kBins0]) sel->status = DYNMO_E_INVALID;  // NaN keys
-    // after the windowed pass only bins lo - 1 .. hi + 1 can be nonzero
-    const int rlo = PASS == 0 && MODE == 0 ? (int)sel->win_lo - 1 : 0;
-    const int rhi = PASS == 0 && MODE == 0 ? (int)sel->win_hi + 1 : NB - 1;
-    const unsigned long long total = suffix_scan<NB>(h, s_part, rlo, rhi);
+    const unsigned long long total = suffix_scan<NB>(h, s_part);
     if (PASS == 0 && tid == 0) {  // the global number of non-NaN keys; validate k
         sel->n_global = (long long)total;
         if (!done0 && (sel->k > (long long)total)) {
@@ -492,35 +550,24 @@ __global__ void __launch_bounds__(1024) k_prune_select(PruneArgs a) {
         unsigned long long acc;
         find_bin<NB>(h, s_part, (unsigned long long)krem, &b, &acc);
         if (tid == 0) {
-            if (PASS == 0 && MODE == 0 && (b == (int)sel->win_hi + 1 || b == (int)sel->win_lo - 1)) {
-                sel->miss = 1;
-            } else {
-                sel->k_rem = krem - (long long)acc;
-                sel->above += (long long)acc;
-                sel->prefix = PASS == 0 ? (uint32_t)b
-                            : PASS == 1 ? ((sel->prefix << 10) | (uint32_t)b) : ((sel->prefix << 6) | (uint32_t)b);
-                // this rank's keys in the chosen bin (the ties, after the last pass)
-                sel->tie_local = (long long)a.hist_local[b];
-                if (PASS == 0) {
-                    sel->missed = MODE;  // reported in d_info[5]
-                    sel->wincnt = MODE == 0 && a.tile_win != nullptr &&
-                                  sel->win_hi - sel->win_lo + 1 <= (uint32_t)kWinCnt;
-                    sel->tau_d = (uint32_t)b - sel->win_lo;
-                }
-                sel->miss = 0;
+            sel->k_rem = krem - (long long)acc;
+            sel->above += (long long)acc;
+            sel->prefix = PASS == 0 ? (uint32_t)b
+                        : PASS == 1 ? ((sel->prefix << 10) | (uint32_t)b) : ((sel->prefix << 6) | (uint32_t)b);
+            // this rank's keys in the chosen bin (the ties, after the last pass)
+            sel->tie_local = (long long)a.hist_local[b];
+            if (PASS == 0) {  // after a miss: reported in d_info[5]; ties counted by k_prune_tiecount
+                sel->missed = 1;
+                sel->wincnt = 0;
             }
+            sel->miss = 0;
         }
     }
     __syncthreads();
     if (tid == 0 && !done0 && !sel->done && krem == 0) sel->done = 2;  // k = 0: nothing kept
-    const int c0 = rlo < 0 ? 0 : rlo, c1 = rhi > NB - 1 ? NB - 1 : rhi;
-    for (int b = c0 + tid; b <= c1; b += 1024) {
+    for (int b = tid; b < NB + (PASS == 0 ? 1 : 0); b += 1024) {
         a.hist_local[b] = 0ull;
         if (a.nranks > 1) a.hist_global[b] = 0ull;
-    }
-    if (PASS == 0 && tid == 0) {  // the NaN count
-        a.hist_local[kBins0] = 0ull;
-        if (a.nranks > 1) a.hist_global[kBins0] = 0ull;
     }
 }
 
@@ -998,7 +1045,7 @@ cudaError_t launch_prune(const PruneArgs &a, int pass_kind, int grid, cudaStream
         case 32: return launch_pdl(k_prune_hist0<1>, grid, kHist0Threads, (size_t)kBins0 * 4, s, a);
         case 1: return launch_pdl(k_prune_hist<1>, grid, kPruneThreads, 0, s, a);
         case 2: return launch_pdl(k_prune_hist<2>, grid, kPruneThreads, 0, s, a);
-        case 10: return launch_pdl(k_prune_select<0, 0>, 1, 1024, 0, s, a);
+        case 10: return launch_pdl(k_prune_select_win, 1, 1024, 0, s, a);
         case 11: return launch_pdl(k_prune_select<1, 0>, 1, 1024, 0, s, a);
         case 12: return launch_pdl(k_prune_select<2, 0>, 1, 1024, 0, s, a);
         case 13: return launch_pdl(k_prune_select<0, 1>, 1, 1024, 0, s, a);
