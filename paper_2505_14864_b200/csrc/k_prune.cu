@@ -6,17 +6,24 @@
 //   key(w) = bits(|w|) for f32; bits(|bf16|) << 16 for bf16 (the f32 key of
 //   the same value), so segments of both types share one ordered key space
 //   (monotone in |w| for non-NaN values; +0 and -0 both key 0).
-//   pass 0: histogram of key >> 16      (32768 bins) -> all-reduce -> bin
-//           (for bf16 the whole 15-bit magnitude: an all-bf16 plan is done)
+//   pass 0: the digit key >> 16 (32768 bins; for bf16 the whole 15-bit
+//           magnitude: an all-bf16 plan is done after it), in three steps:
+//           a histogram of every 32nd tile -> all-reduce -> a bin window
+//           [lo, hi] around the estimated k-th key -> one pass over every
+//           key that histograms the window (and counts the keys below /
+//           above it: exact totals) -> all-reduce -> bin.  A window that
+//           misses the k-th key runs the full histogram (same launches,
+//           graph-capturable; they return at once on a hit).
 //   pass 1: histogram of key >> 6 & 1023 among keys with that prefix
 //   pass 2: histogram of key & 63 among keys with the 25-bit prefix
 // Each pass streams the rank's weights (HBM-bound); only the histograms cross
-// GPUs (NCCL all-reduce, 256 KB).  The threshold tau is the k-th largest key;
+// GPUs (NCCL all-reduce).  The threshold tau is the k-th largest key;
 // keys > tau are kept, and of the keys == tau the first `need` in the global
 // order (rank, then segment order, then index -- SPEC S:L184) are kept:
 // per-rank tie counts are all-gathered, and only the rank whose share of the
-// ties is partial ranks its ties (per-tile counts, an exclusive scan, and an
-// in-tile block scan in element order).
+// ties is partial ranks its ties (per-(tile, warp range) counts -- recorded by
+// the windowed pass for bf16 plans, else a counting pass -- an exclusive
+// scan, and in-range warp scans in element order).
 #include "dynmo_internal.h"
 
 namespace dynmo {
