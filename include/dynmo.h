@@ -474,7 +474,10 @@ typedef struct dynmo_pplan_s *dynmo_pplan;
 
 /* Plan of this rank's weight segments (in order; off the hot path: tile
  * table + workspace on the device).  Pointers must stay valid while the plan
- * is used.  INVALID: unknown dtype, negative n, a misaligned pointer. */
+ * is used.  COLLECTIVE when the ctx has more than one rank (every rank calls
+ * it, synchronous): the ranks agree on the passes (an f32 segment on any rank
+ * adds the f32 passes on all).  INVALID: unknown dtype, negative n, a
+ * misaligned pointer -- on any rank, returned by every rank. */
 dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h_segs, int32_t n_segs,
                                      dynmo_pplan *out);
 void dynmo_prune_plan_destroy(dynmo_pplan plan);

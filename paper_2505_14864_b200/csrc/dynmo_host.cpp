@@ -688,16 +688,17 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     if (!out) return invalid("null plan out");
     *out = nullptr;
     if (!ctx) return invalid("null ctx");
-    if (n_segs < 0 || (n_segs > 0 && !h_segs)) return invalid("bad segment list");
     std::vector<PruneTile> tiles;
     bool any_f32 = false;
-    for (int32_t i = 0; i < n_segs; ++i) {
+    const char *bad = nullptr;  // validated before the collective: every rank takes part in it
+    if (n_segs < 0 || (n_segs > 0 && !h_segs)) bad = "bad segment list";
+    for (int32_t i = 0; !bad && i < n_segs; ++i) {
         const dynmo_prune_segment &sg = h_segs[i];
-        if (sg.n < 0) return invalid("negative segment length");
-        if (sg.dtype != DYNMO_W_F32 && sg.dtype != DYNMO_W_BF16) return invalid("unknown weight dtype");
+        if (sg.n < 0) { bad = "negative segment length"; break; }
+        if (sg.dtype != DYNMO_W_F32 && sg.dtype != DYNMO_W_BF16) { bad = "unknown weight dtype"; break; }
         if (sg.n == 0) continue;
-        if (!sg.d_w || !sg.d_mask) return invalid("null segment pointer");
-        if ((uintptr_t)sg.d_w % 16) return invalid("weights must be 16-byte aligned");
+        if (!sg.d_w || !sg.d_mask) { bad = "null segment pointer"; break; }
+        if ((uintptr_t)sg.d_w % 16) { bad = "weights must be 16-byte aligned"; break; }
         any_f32 |= sg.dtype == DYNMO_W_F32;
         const int64_t esz = sg.dtype == DYNMO_W_F32 ? 4 : 2;
         for (int64_t o = 0; o < sg.n; o += kPruneTileElems) {
@@ -705,6 +706,23 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
             tiles.push_back(PruneTile{(const char *)sg.d_w + o * esz, sg.d_mask + o, (uint32_t)len, sg.dtype});
         }
     }
+    // every rank must run the same passes (one NCCL all-reduce per pass): an
+    // f32 segment on any rank adds passes 1 and 2 everywhere; an invalid
+    // argument on any rank fails the call on every rank
+    bool global_f32 = any_f32;
+    if (ctx->nranks > 1) {
+        const char mine = (char)((any_f32 ? 1 : 0) | (bad ? 2 : 0));
+        std::vector<char> all;
+        const dynmo_status st = allgather_bytes(ctx, &mine, 1, all);
+        if (st != DYNMO_OK) return st;
+        bool any_bad = false;
+        for (char c : all) {
+            global_f32 |= (c & 1) != 0;
+            any_bad |= (c & 2) != 0;
+        }
+        if (any_bad && !bad) bad = "invalid segments on another rank";
+    }
+    if (bad) return invalid(bad);
     auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
     const size_t nt = std::max<size_t>(1, tiles.size());
     const size_t sz_tiles = up(sizeof(PruneTile) * nt), sz_hist = up(sizeof(unsigned long long) * 32770);
@@ -743,7 +761,7 @@ dynmo_status dynmo_prune_plan_create(dynmo_ctx ctx, const dynmo_prune_segment *h
     for (const PruneTile &t : tiles) a.n_elems += t.n;
     a.rank = ctx->rank;
     a.nranks = ctx->nranks;
-    a.last_pass = any_f32 ? 2 : 0;  // bf16 keys have 16 zero low bits: the 15-bit first digit is exact
+    a.last_pass = global_f32 ? 2 : 0;  // bf16 keys have 16 zero low bits: the 15-bit first digit is exact
     bool ok = cudaMemset(pl->dmem, 0, total) == cudaSuccess;
     if (ok && !tiles.empty())
         ok = cudaMemcpy((void *)a.tiles, tiles.data(), sizeof(PruneTile) * tiles.size(), cudaMemcpyHostToDevice) ==

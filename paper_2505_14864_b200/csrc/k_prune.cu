@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(kPruneThreads) k_prune_hist0w(PruneArgs a) {
     // count mode (bf16-only plan, window <= kWinCnt bins): also the count of
     // each window bin per (tile, warp range of the mask pass) -> tile_win,
     // from which the tie counts of tau's bin are gathered (no tie-count pass)
-    const bool cnt = a.tile_win != nullptr && hi - lo + 1 <= (uint32_t)kWinCnt;
+    const bool cnt = a.tile_win != nullptr && a.last_pass == 0 && hi - lo + 1 <= (uint32_t)kWinCnt;
     __shared__ uint32_t s_wc[kPruneWarps][kWinCnt];  // per warp (full tiles) / [0] per block (ragged)
     if (threadIdx.x < kPruneWarps * kWinCnt) (&s_wc[0][0])[threadIdx.x] = 0u;
     __syncthreads();
@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(1024) k_prune_select_win(PruneArgs a) {
                 sel->prefix = lo + (uint32_t)c - 1;
                 sel->tie_local = (long long)a.cw_local[c];  // this rank's keys in the chosen bin
                 sel->missed = 0;
-                sel->wincnt = a.tile_win != nullptr && W <= (uint32_t)kWinCnt;
+                sel->wincnt = a.tile_win != nullptr && a.last_pass == 0 && W <= (uint32_t)kWinCnt;
                 sel->tau_d = (uint32_t)c - 1;
                 sel->miss = 0;
             }

@@ -289,6 +289,31 @@ def main():
         dist.all_reduce(flags, op=dist.ReduceOp.MAX)
         assert int(flags.item()) == 2, (rank, kk, int(flags.item()))  # hit; counted ties on the partial rank
     pplan.close()
+    # different dtype sets per rank (rank 0 bf16 only, the others f32): the
+    # collective plan creation makes every rank run the f32 passes
+    shards_all, vals_all = [], []
+    for r in range(world):
+        gr = np.random.default_rng(950 + r)
+        x = np.round(gr.normal(0, 1, 40000 + 300 * r) * 64) / 64  # ties across ranks
+        if r == 0:
+            tb = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+            shards_all.append(tb)
+            vals_all.append(oracle.bf16_to_f64(tb.view(torch.int16).numpy().view(np.uint16)))
+        else:
+            w = x.astype(np.float32)
+            shards_all.append(torch.from_numpy(w))
+            vals_all.append(w.astype(np.float64))
+    wt = shards_all[rank].to(dev)
+    mk = torch.zeros(wt.numel(), dtype=torch.uint8, device=dev)
+    pplan = D.PrunePlan(ctx, [(wt, mk)])
+    Ntot = sum(v.size for v in vals_all)
+    for kk in (Ntot // 7, Ntot // 2 + 3):
+        info, pst2 = D.global_prune(ctx, pplan, kk)
+        torch.cuda.synchronize()
+        ost2, om = oracle.global_prune(vals_all, kk)
+        assert int(pst2.item()) == ost2 == 0
+        assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "mixed dtype sets")
+    pplan.close()
     # Releasing GPUs after re-packing: split the ctx -- even
     # ranks stay active, odd ranks are released (None) -- then the smaller
     # group profiles, partitions and maps its stages onto its own ranks
