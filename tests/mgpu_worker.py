@@ -314,6 +314,30 @@ def main():
         assert int(pst2.item()) == ost2 == 0
         assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "mixed dtype sets")
     pplan.close()
+    # a rank without weights (the last one): empty plan, still in every collective
+    shards_all, vals_all = [], []
+    for r in range(world):
+        gr = np.random.default_rng(970 + r)
+        n_r = 0 if r == world - 1 else 2 * 32768 + 77 * r
+        tb = torch.from_numpy(gr.normal(0, 1, n_r).astype(np.float32)).to(torch.bfloat16)
+        shards_all.append(tb)
+        vals_all.append(oracle.bf16_to_f64(tb.view(torch.int16).numpy().view(np.uint16)))
+    if rank == world - 1:
+        pplan = D.PrunePlan(ctx, [])
+    else:
+        wt = shards_all[rank].to(dev)
+        mk = torch.zeros(wt.numel(), dtype=torch.uint8, device=dev)
+        pplan = D.PrunePlan(ctx, [(wt, mk)])
+    Ntot = sum(v.size for v in vals_all)
+    for kk in (Ntot // 10, Ntot):
+        info, pst2 = D.global_prune(ctx, pplan, kk)
+        torch.cuda.synchronize()
+        ost2, om = oracle.global_prune(vals_all, kk)
+        assert int(pst2.item()) == ost2 == 0
+        assert int(info[1].item()) == Ntot
+        if rank != world - 1:
+            assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "empty rank")
+    pplan.close()
     # Releasing GPUs after re-packing: split the ctx -- even
     # ranks stay active, odd ranks are released (None) -- then the smaller
     # group profiles, partitions and maps its stages onto its own ranks
