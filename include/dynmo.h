@@ -65,7 +65,9 @@ const char *dynmo_version(void);
 
 /* ------------------------------------------------------------------ ctx --
  * One process per GPU ("one MPI rank per GPU"; here torch.distributed
- * ranks).  nranks == 1: no NCCL communicator is created.  nranks > 1: every
+ * ranks).  nranks == 1: no NCCL communicator is created up front (a
+ * one-rank communicator is created by the first plan that asks for the NCCL
+ * exchange), and the peer window is local.  nranks > 1: every
  * rank passes the same 128-byte id obtained on rank 0 from
  * dynmo_get_unique_id() and broadcast by the caller (e.g. through the torch
  * process group); the ctx owns the resulting ncclComm_t.  device is the CUDA
@@ -188,15 +190,19 @@ typedef struct dynmo_cost_coef {
  * rebuild after migration or re-allocation.
  *   layer_begin, n_local: the contiguous global layers this rank profiles.
  *   n_total: length of the global cost vector.
- *   exchange: every rank ends with the global vector (requires nranks > 1;
- *     slices must tile [0, n_total) exactly, else the device status is
- *     INVALID):
+ *   exchange: every rank ends with the global vector (slices must tile
+ *     [0, n_total) exactly, else the device status is INVALID; on a
+ *     single-rank ctx the exchange runs against the rank itself, so the same
+ *     code path -- LL slot encode/decode, slot validation, unpack -- runs on
+ *     one GPU):
  *       1 -> over NVLink peer memory: the epilogue stores this rank's slot
  *            straight into every rank's receive area (double-buffered by a
  *            device-side epoch, graph-safe) and releases a flag; the unpack
  *            kernel waits (bounded, 10 s) for every rank's flag.  Plan
- *            creation is then COLLECTIVE (CUDA IPC of the receive areas), and
- *            every rank must make the same sequence of profile calls.
+ *            creation is then COLLECTIVE (CUDA IPC of the receive areas; a
+ *            failure on any rank -- validation, allocation, mapping -- fails
+ *            the call on every rank, none is left waiting), and every rank
+ *            must make the same sequence of profile calls.
  *       2 -> ncclAllGather of the fixed-size slots on the ctx communicator.
  *     0 -> local only: n_total == n_local and outputs are indexed by local
  *     layer.
@@ -377,13 +383,18 @@ dynmo_status dynmo_migrate_layers(dynmo_ctx ctx, int32_t n_layers, int32_t n_old
  * handles of their cudaMalloc allocations are exchanged over the ctx
  * communicator and mapped by every peer) and the buffers it may receive into
  * (h_recv), same table layout as dynmo_migrate_layers.  The buffers must stay
- * allocated while the plan lives.  dynmo_migrate_layers_p2p is collective
+ * allocated while the plan lives.  A failure on any rank during plan creation
+ * fails it on every rank (no rank is left in a setup collective).
+ * dynmo_migrate_layers_p2p is collective
  * like call 5: on `stream` the sender marks its buffers ready (release flag in
  * each receiver's peer window, after its prior work), each receiver waits for
  * its senders, copies, and marks done; the sender's stream then waits for its
  * receivers (so it may overwrite or free the send buffers afterwards).  Sizes
- * must match between sender and receiver (INVALID).  Waits are bounded (10 s):
- * a timeout sets a sticky error readable with dynmo_ctx_p2p_error. */
+ * must match between sender and receiver (INVALID).  The ready/done flags
+ * carry one epoch per directed rank pair, advanced only in calls where that
+ * pair moves data, so ranks that sit a call out stay in step.  Waits are
+ * bounded (10 s): a timeout sets a sticky error readable with
+ * dynmo_ctx_p2p_error. */
 typedef struct dynmo_mplan_s *dynmo_mplan;
 dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t n_bufs,
                                        const dynmo_buf *h_send, const dynmo_buf *h_recv,
@@ -401,7 +412,10 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan plan, int32_t n
  * together with profile + partition (the whole rebalancing step is then one
  * graph launch).  Collective like call 5 (same call sequence on every rank).
  * n_old / n_new: stage counts of the two maps; n_layers <= 1023.  An invalid
- * boundary vector or a wait timeout sets the sticky peer error.
+ * boundary vector, a stage -> rank entry outside [0, nranks) (e.g. the -1 of
+ * a failed dynmo_map_stages) or a send/receive size mismatch sets the sticky
+ * peer error to INVALID and moves nothing (for a size mismatch: that buffer);
+ * a wait timeout sets it to NCCL.
  * d_bytes_sent / d_bytes_recv (nullable): this rank's bytes (device). */
 dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
                                       const int32_t *d_bnd_old, const int32_t *d_rank_old,

@@ -66,7 +66,8 @@ struct dynmo_ctx_s {
     PeerWindow *d_win = nullptr;
     std::vector<PeerWindow *> peer_win;
     cudaStream_t aux = nullptr;  // setup collectives
-    uint64_t mig_epoch = 0;
+    // host-driven peer migration: epochs per directed rank pair (P2PSignal)
+    uint64_t send_epoch[kMaxRanks] = {}, recv_epoch[kMaxRanks] = {};
     long long *d_map_work = nullptr;  // [1 << kMaxMapRanks] DP table of dynmo_map_stages
 };
 
@@ -235,6 +236,32 @@ static dynmo_status setup_peer_window(dynmo_ctx c) {
     return st;
 }
 
+// Single-rank ctx: the window is local (peer_win[0] = d_win), so the
+// peer-memory exchange runs against itself; no NCCL communicator until a
+// plan asks for the NCCL exchange (ensure_comm).
+static dynmo_status setup_single_window(dynmo_ctx c) {
+    if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
+        return cuda_fail(cudaGetLastError(), "peer window (single rank)");
+    c->peer_win.assign(1, c->d_win);
+    return DYNMO_OK;
+}
+
+// A one-rank NCCL communicator (legal in NCCL) for the NCCL exchange of a
+// single-rank ctx: the all-gather then degenerates to a local copy.
+static dynmo_status ensure_comm(dynmo_ctx c) {
+    if (c->comm) return DYNMO_OK;
+    if (c->nranks != 1) return invalid("multi-rank ctx without a communicator");
+    int dev = c->device;
+    const ncclResult_t r = ncclCommInitAll(&c->comm, 1, &dev);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        g_err = std::string("ncclCommInitAll (single rank): ") + ncclGetErrorString(r);
+        return DYNMO_E_NCCL;
+    }
+    return DYNMO_OK;
+}
+
 dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
                               const uint8_t *h_nccl_id, dynmo_ctx *out) {
     if (!out) return invalid("null ctx out");
@@ -270,6 +297,12 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
             dynmo_ctx_destroy(c);
             return st;
         }
+    } else {
+        const dynmo_status st = setup_single_window(c);
+        if (st) {
+            dynmo_ctx_destroy(c);
+            return st;
+        }
     }
     *out = c;
     return DYNMO_OK;
@@ -291,6 +324,11 @@ dynmo_status dynmo_ctx_split(dynmo_ctx ctx, int32_t color, int32_t key, dynmo_ct
             dynmo_ctx_destroy(c);
             return DYNMO_OK;
         }
+        const dynmo_status st = setup_single_window(c);
+        if (st) {
+            dynmo_ctx_destroy(c);
+            return st;
+        }
         *out = c;
         return DYNMO_OK;
     }
@@ -311,12 +349,10 @@ dynmo_status dynmo_ctx_split(dynmo_ctx ctx, int32_t color, int32_t key, dynmo_ct
     c->comm = nc;
     c->nranks = n;
     c->rank = rk;
-    if (n > 1) {
-        const dynmo_status st = setup_peer_window(c);
-        if (st) {
-            dynmo_ctx_destroy(c);
-            return st;
-        }
+    const dynmo_status st = n > 1 ? setup_peer_window(c) : setup_single_window(c);
+    if (st) {
+        dynmo_ctx_destroy(c);
+        return st;
     }
     *out = c;
     return DYNMO_OK;
@@ -384,10 +420,10 @@ dynmo_status dynmo_ctx_barrier(dynmo_ctx ctx, dynmo_stream stream) {
     if (!ctx) return invalid("null ctx");
     if (ctx->nranks == 1) return DYNMO_OK;
     DeviceGuard g(ctx->device);
-    // one int32 all-reduce in the ctx workspace: completes on every rank's
-    // stream only once every rank's stream has reached it
-    const ncclResult_t r = ncclAllReduce(ctx->d_map_work, ctx->d_map_work, 1, ncclInt32, ncclSum, ctx->comm,
-                                         (cudaStream_t)stream);
+    // one int32 all-reduce on the window's own barrier word: completes on
+    // every rank's stream only once every rank's stream has reached it
+    const ncclResult_t r = ncclAllReduce(&ctx->d_win->barrier, &ctx->d_win->barrier, 1, ncclInt32, ncclSum,
+                                         ctx->comm, (cudaStream_t)stream);
     if (r != ncclSuccess) {
         g_err = std::string("ncclAllReduce (barrier): ") + ncclGetErrorString(r);
         return DYNMO_E_NCCL;
@@ -428,17 +464,15 @@ int32_t dynmo_ctx_nranks(dynmo_ctx ctx) { return ctx ? ctx->nranks : 0; }
 int32_t dynmo_ctx_rank(dynmo_ctx ctx) { return ctx ? ctx->rank : -1; }
 
 // ------------------------------------------------------------------ plans
-dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_segs, int32_t n_segs,
+// The rank-local part of dynmo_profile_plan_create: validation, the tile
+// decomposition and the device workspace (no collective).
+static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_segs, int32_t n_segs,
                                        int32_t layer_begin, int32_t n_local, int32_t n_total,
                                        int32_t exchange, dynmo_plan *out) {
-    if (!out) return invalid("null plan out");
-    *out = nullptr;
-    if (!ctx) return invalid("null ctx");
     if (n_segs < 0 || (n_segs > 0 && !h_segs)) return invalid("bad segment array");
     if (layer_begin < 0 || n_local < 0 || n_total < 0) return invalid("negative layer range");
     if (exchange < 0 || exchange > 2) return invalid("exchange must be 0, 1 (peer memory) or 2 (NCCL)");
     if (exchange) {
-        if (ctx->nranks < 2) return invalid("exchange needs nranks > 1");
         if ((int64_t)layer_begin + n_local > n_total) return invalid("local layers exceed n_total");
     } else if (n_total != n_local) {
         return invalid("without exchange n_total must equal n_local");
@@ -614,36 +648,6 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
         delete pl;
         return cuda_fail(e, "plan upload");
     }
-    if (exchange == 1) {
-        // collective: the receive slot area of every rank, mapped by every peer
-        const size_t bytes = sizeof(int64_t) * 2 * ctx->nranks * pl->slot_elems * 2;  // LL: 2 words per value
-        dynmo_status st = DYNMO_OK;
-        if (cudaMalloc((void **)&pl->d_p2p_slots, bytes) != cudaSuccess ||
-            cudaMemset(pl->d_p2p_slots, 0, bytes) != cudaSuccess)
-            st = cuda_fail(cudaGetLastError(), "p2p slots");
-        cudaIpcMemHandle_t h;
-        if (!st && cudaIpcGetMemHandle(&h, pl->d_p2p_slots) != cudaSuccess)
-            st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle (slots)");
-        std::vector<char> all;
-        if (!st) st = allgather_bytes(ctx, &h, sizeof(h), all);
-        pl->peer_slots.assign(ctx->nranks, nullptr);
-        for (int r = 0; !st && r < ctx->nranks; ++r) {
-            if (r == ctx->rank) {
-                pl->peer_slots[r] = pl->d_p2p_slots;
-                continue;
-            }
-            cudaIpcMemHandle_t ph;
-            memcpy(&ph, all.data() + r * sizeof(ph), sizeof(ph));
-            void *mp = nullptr;
-            if (cudaIpcOpenMemHandle(&mp, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
-                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (slots)");
-            pl->peer_slots[r] = (int64_t *)mp;
-        }
-        if (st) {
-            dynmo_profile_plan_destroy(pl);
-            return st;
-        }
-    }
     const int warps_per_block = kProfThreads / 32;
     const int64_t want = (pl->n_tiles + warps_per_block - 1) / warps_per_block;
     int max_words = 0;
@@ -657,6 +661,86 @@ dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_seg
     if (!pl->ops) pl->ops = 1;
     const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(pl->ops, pl->warp_words);
     pl->grid = (int)std::max<int64_t>(1, std::min(want, cap_blocks));
+    *out = pl;
+    return DYNMO_OK;
+}
+
+// All ranks agree on a setup step: every rank contributes its status and
+// every rank gets the worst one (a failure on any rank fails the call on
+// every rank, so no rank is left waiting in a later collective).
+static dynmo_status agree(dynmo_ctx ctx, dynmo_status mine, const char *what) {
+    if (ctx->nranks < 2) return mine;
+    const int32_t v = (int32_t)mine;
+    std::vector<char> all;
+    const dynmo_status st = allgather_bytes(ctx, &v, sizeof(v), all);
+    if (st) return st;
+    int32_t worst = DYNMO_OK;
+    for (int r = 0; r < ctx->nranks; ++r) {
+        int32_t x;
+        memcpy(&x, all.data() + r * sizeof(x), sizeof(x));
+        if (x < worst) worst = x;
+    }
+    if (mine == DYNMO_OK && worst != DYNMO_OK) g_err = std::string(what) + " failed on another rank";
+    return mine != DYNMO_OK ? mine : (dynmo_status)worst;
+}
+
+dynmo_status dynmo_profile_plan_create(dynmo_ctx ctx, const dynmo_segment *h_segs, int32_t n_segs,
+                                       int32_t layer_begin, int32_t n_local, int32_t n_total,
+                                       int32_t exchange, dynmo_plan *out) {
+    if (!out) return invalid("null plan out");
+    *out = nullptr;
+    if (!ctx) return invalid("null ctx");
+    dynmo_plan pl = nullptr;
+    dynmo_status st = profile_plan_local(ctx, h_segs, n_segs, layer_begin, n_local, n_total, exchange, &pl);
+    if (exchange == 2 && !st && ctx->nranks == 1) st = ensure_comm(ctx);
+    if (exchange != 1) {
+        if (st && pl) dynmo_profile_plan_destroy(pl);
+        if (!st) *out = pl;
+        return st;
+    }
+    // exchange == 1 is collective: the receive slot area of every rank,
+    // mapped by every peer.  Every rank takes part in both agreement steps
+    // even after a local failure.
+    DeviceGuard g(ctx->device);
+    const size_t bytes = pl ? sizeof(int64_t) * 2 * ctx->nranks * pl->slot_elems * 2 : 0;  // LL: 2 words per value
+    if (!st && (cudaMalloc((void **)&pl->d_p2p_slots, bytes) != cudaSuccess ||
+                cudaMemset(pl->d_p2p_slots, 0, bytes) != cudaSuccess))
+        st = cuda_fail(cudaGetLastError(), "p2p slots");
+    if (ctx->nranks == 1) {  // the slot area of the only rank is local
+        if (!st) pl->peer_slots.assign(1, pl->d_p2p_slots);
+    } else {
+        struct {
+            int32_t st;
+            cudaIpcMemHandle_t h;
+        } mine{}, other{};
+        if (!st && cudaIpcGetMemHandle(&mine.h, pl->d_p2p_slots) != cudaSuccess)
+            st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle (slots)");
+        mine.st = st;
+        std::vector<char> all;
+        const dynmo_status ag = allgather_bytes(ctx, &mine, sizeof(mine), all);
+        if (!st) st = ag;
+        for (int r = 0; !st && r < ctx->nranks; ++r) {
+            memcpy(&other, all.data() + r * sizeof(other), sizeof(other));
+            if (other.st) st = invalid("profile plan creation failed on another rank");
+        }
+        if (!st) pl->peer_slots.assign(ctx->nranks, nullptr);
+        for (int r = 0; !st && r < ctx->nranks; ++r) {
+            if (r == ctx->rank) {
+                pl->peer_slots[r] = pl->d_p2p_slots;
+                continue;
+            }
+            memcpy(&other, all.data() + r * sizeof(other), sizeof(other));
+            void *mp = nullptr;
+            if (cudaIpcOpenMemHandle(&mp, other.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (slots)");
+            pl->peer_slots[r] = (int64_t *)mp;
+        }
+        if (ag == DYNMO_OK) st = agree(ctx, st, "profile plan (peer mapping)");
+    }
+    if (st) {
+        if (pl) dynmo_profile_plan_destroy(pl);
+        return st;
+    }
     *out = pl;
     return DYNMO_OK;
 }
@@ -1184,42 +1268,53 @@ dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t 
                                        dynmo_mplan *out) {
     if (!out) return invalid("null mplan out");
     *out = nullptr;
-    if (!ctx || n_layers < 1 || n_bufs < 1 || !h_send || !h_recv) return invalid("bad migrate plan args");
-    if (ctx->nranks < 2) return invalid("the peer-memory migration needs nranks > 1");
+    if (!ctx || ctx->nranks < 2) return invalid(!ctx ? "null ctx" : "the peer-memory migration needs nranks > 1");
+    // collective: a local failure is recorded and every rank still takes
+    // part in the first all-gather, which carries the status
+    dynmo_status st = DYNMO_OK;
+    if (n_layers < 1 || n_bufs < 1 || !h_send || !h_recv) st = invalid("bad migrate plan args");
     DeviceGuard g(ctx->device);
-    const int64_t nb = (int64_t)n_layers * n_bufs;
+    const int64_t nb = st ? 0 : (int64_t)n_layers * n_bufs;
     // this rank's send buffers -> (allocation handle, offset)
     std::vector<CUdeviceptr> bases;
     std::vector<cudaIpcMemHandle_t> handles;
     std::vector<SendRec> recs;
-    for (int64_t i = 0; i < nb; ++i) {
+    for (int64_t i = 0; !st && i < nb; ++i) {
         const dynmo_buf &b = h_send[i];
         if (b.bytes <= 0 || !b.d_ptr) continue;
         CUdeviceptr base;
         size_t size;
-        dynmo_status st = alloc_range(b.d_ptr, &base, &size);
-        if (st) return st;
-        if ((CUdeviceptr)b.d_ptr + (size_t)b.bytes > base + size) return invalid("send buffer crosses its allocation");
+        st = alloc_range(b.d_ptr, &base, &size);
+        if (st) break;
+        if ((CUdeviceptr)b.d_ptr + (size_t)b.bytes > base + size) {
+            st = invalid("send buffer crosses its allocation");
+            break;
+        }
         int hi = -1;
         for (size_t k = 0; k < bases.size(); ++k)
             if (bases[k] == base) hi = (int)k;
         if (hi < 0) {
             cudaIpcMemHandle_t h;
-            CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)base), "cudaIpcGetMemHandle (send buffer)");
+            if (cudaIpcGetMemHandle(&h, (void *)base) != cudaSuccess) {
+                st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle (send buffer)");
+                break;
+            }
             hi = (int)bases.size();
             bases.push_back(base);
             handles.push_back(h);
         }
         recs.push_back(SendRec{(int32_t)i, hi, (uint64_t)((CUdeviceptr)b.d_ptr - base), b.bytes});
     }
-    // gather every rank's tables (counts, then fixed-size padded arrays)
-    int64_t cnt[2] = {(int64_t)handles.size(), (int64_t)recs.size()};
+    // gather every rank's tables (counts + status, then fixed-size padded arrays)
+    int64_t cnt[3] = {(int64_t)handles.size(), (int64_t)recs.size(), (int64_t)st};
     std::vector<char> allc;
-    dynmo_status st = allgather_bytes(ctx, cnt, sizeof(cnt), allc);
+    const dynmo_status ag = allgather_bytes(ctx, cnt, sizeof(cnt), allc);
     if (st) return st;
+    if (ag) return ag;
     int64_t mh = 1, mr = 1;
     for (int r = 0; r < ctx->nranks; ++r) {
         const int64_t *c = (const int64_t *)(allc.data() + r * sizeof(cnt));
+        if (c[2] != DYNMO_OK) return invalid("migrate plan creation failed on another rank");
         mh = std::max(mh, c[0]);
         mr = std::max(mr, c[1]);
     }
@@ -1247,13 +1342,13 @@ dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t 
             memcpy(&h, b + k * sizeof(h), sizeof(h));
             void *p = nullptr;
             if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-                dynmo_status e = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (send buffer)");
-                dynmo_migrate_plan_destroy(mp);
-                return e;
+                st = cuda_fail(cudaGetLastError(), "cudaIpcOpenMemHandle (send buffer)");
+                break;
             }
             mp->opened.push_back(p);
             mapped[k] = (char *)p;
         }
+        if (st) break;
         const SendRec *rr = (const SendRec *)(b + mh * sizeof(cudaIpcMemHandle_t));
         for (int64_t k = 0; k < c[1]; ++k)
             mp->src[{r, rr[k].idx}] = dynmo_buf{mapped[rr[k].handle] + rr[k].offset, rr[k].bytes};
@@ -1263,13 +1358,17 @@ dynmo_status dynmo_migrate_plan_create(dynmo_ctx ctx, int32_t n_layers, int32_t 
     for (auto &kv : mp->src)
         st_h[(size_t)kv.first.first * nb + kv.first.second] = DevBuf{kv.second.d_ptr, kv.second.bytes};
     for (int64_t i = 0; i < nb; ++i) rt_h[i] = DevBuf{h_recv[i].d_ptr, h_recv[i].bytes};
-    if (cudaMalloc((void **)&mp->d_src_tab, sizeof(DevBuf) * st_h.size()) != cudaSuccess ||
-        cudaMalloc((void **)&mp->d_recv_tab, sizeof(DevBuf) * rt_h.size()) != cudaSuccess ||
-        cudaMemcpy(mp->d_src_tab, st_h.data(), sizeof(DevBuf) * st_h.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(mp->d_recv_tab, rt_h.data(), sizeof(DevBuf) * rt_h.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-        dynmo_status e = cuda_fail(cudaGetLastError(), "migrate plan tables");
+    if (!st && (cudaMalloc((void **)&mp->d_src_tab, sizeof(DevBuf) * st_h.size()) != cudaSuccess ||
+                cudaMalloc((void **)&mp->d_recv_tab, sizeof(DevBuf) * rt_h.size()) != cudaSuccess ||
+                cudaMemcpy(mp->d_src_tab, st_h.data(), sizeof(DevBuf) * st_h.size(), cudaMemcpyHostToDevice) !=
+                    cudaSuccess ||
+                cudaMemcpy(mp->d_recv_tab, rt_h.data(), sizeof(DevBuf) * rt_h.size(), cudaMemcpyHostToDevice) !=
+                    cudaSuccess))
+        st = cuda_fail(cudaGetLastError(), "migrate plan tables");
+    st = agree(ctx, st, "migrate plan (peer mapping)");
+    if (st) {
         dynmo_migrate_plan_destroy(mp);
-        return e;
+        return st;
     }
     *out = mp;
     return DYNMO_OK;
@@ -1367,12 +1466,19 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     if (srcs.empty() && dsts.empty()) return DYNMO_OK;
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
-    const uint64_t epoch = ++ctx->mig_epoch;
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
+    // epochs per directed pair: both ends count the calls in which the pair
+    // moves data (identical move sets on every rank), so they agree whatever
+    // the other ranks do (one ctx-wide epoch drifted between
+    // ranks that skip calls)
+    for (int d : dsts) ++ctx->send_epoch[d];
+    for (int r : srcs) ++ctx->recv_epoch[r];
     // 1. tell my receivers that my buffers are ready (stream order = after my prior work)
     P2PSignal sig{};
-    sig.epoch = epoch;
-    for (int d : dsts) sig.remote[sig.n++] = &ctx->peer_win[d]->ready[me];
+    for (int d : dsts) {
+        sig.epoch[sig.n] = ctx->send_epoch[d];
+        sig.remote[sig.n++] = &ctx->peer_win[d]->ready[me];
+    }
     CUDA_TRY(launch_signal(sig, s), "k_signal launch");
     // 2. pull every incoming buffer over NVLink, then tell the senders
     if (!srcs.empty()) {
@@ -1381,9 +1487,9 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
         for (int i = 0; i < pl.n_src; ++i) {
             pl.src_rank[i] = srcs[i];
             pl.done_remote[i] = &ctx->peer_win[srcs[i]]->done[me];
+            pl.epoch[i] = ctx->recv_epoch[srcs[i]];
         }
         pl.ready = ctx->d_win->ready;
-        pl.epoch = epoch;
         pl.ctr = &ctx->d_win->pull_ctr;
         pl.err = &ctx->d_win->err;
         size_t pos = 0;
@@ -1397,10 +1503,12 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     }
     // 3. my receivers have finished reading my buffers
     P2PWait wt{};
-    wt.epoch = epoch;
     wt.local = ctx->d_win->done;
     wt.err = &ctx->d_win->err;
-    for (int d : dsts) wt.idx[wt.n++] = d;
+    for (int d : dsts) {
+        wt.epoch[wt.n] = ctx->send_epoch[d];
+        wt.idx[wt.n++] = d;
+    }
     CUDA_TRY(launch_wait(wt, s), "k_wait launch");
     phase_end(te, s);
     return DYNMO_OK;

@@ -276,6 +276,7 @@ struct PeerWindow {
     uint64_t ddone[kMaxRanksEpi];
     uint64_t mig_dev_epoch;
     unsigned int dpull_ctr;
+    int32_t barrier;            // dynmo_ctx_barrier's all-reduce word (local use only)
 };
 
 struct DevBuf {
@@ -302,14 +303,18 @@ struct P2PItem {
     void *dst;
     uint64_t bytes;
 };
+// Host-driven migration epochs are kept per directed rank pair (sender ->
+// receiver): both sides derive the same move set, so both count the calls in
+// which the pair exchanges data and agree on the epoch, whichever other
+// ranks take part in a call.
 struct P2PSignal {
     int n;
-    uint64_t epoch;
+    uint64_t epoch[kMaxRanks];       // per receiver: ++send_epoch[dst]
     uint64_t *remote[kMaxRanks];
 };
 struct P2PWait {
     int n;
-    uint64_t epoch;
+    uint64_t epoch[kMaxRanks];       // per receiver: send_epoch[dst]
     const uint64_t *local;
     int idx[kMaxRanks];
     int32_t *err;
@@ -322,7 +327,7 @@ struct P2PPull {
     const uint64_t *ready;           // local window ready[]
     uint64_t *done_remote[kMaxRanks];  // &peer_window[src].done[me] (written by the last block)
     int signal_done;
-    uint64_t epoch;
+    uint64_t epoch[kMaxRanks];       // per sender: ++recv_epoch[src]
     unsigned int *ctr;
     int32_t *err;
 };

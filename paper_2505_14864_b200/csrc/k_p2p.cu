@@ -47,20 +47,20 @@ __device__ bool wait_flag(const uint64_t *flag, uint64_t epoch) {
 
 __global__ void k_signal(P2PSignal s) {
     if (threadIdx.x == 0 && blockIdx.x == 0)
-        for (int i = 0; i < s.n; ++i) st_release_sys(s.remote[i], s.epoch);
+        for (int i = 0; i < s.n; ++i) st_release_sys(s.remote[i], s.epoch[i]);
 }
 
 __global__ void k_wait(P2PWait w) {
     if (threadIdx.x == 0 && blockIdx.x == 0)
         for (int i = 0; i < w.n; ++i)
-            if (!wait_flag(w.local + w.idx[i], w.epoch)) atomicExch(w.err, (int)DYNMO_E_NCCL);
+            if (!wait_flag(w.local + w.idx[i], w.epoch[i])) atomicExch(w.err, (int)DYNMO_E_NCCL);
 }
 
 __global__ void __launch_bounds__(kP2PThreads) k_pull(P2PPull p) {
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
         int ok = 1;
-        for (int i = 0; i < p.n_src; ++i) ok &= wait_flag(p.ready + p.src_rank[i], p.epoch);
+        for (int i = 0; i < p.n_src; ++i) ok &= wait_flag(p.ready + p.src_rank[i], p.epoch[i]);
         s_ok = ok;
         if (!ok) atomicExch(p.err, (int)DYNMO_E_NCCL);
     }
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_pull(P2PPull p) {
             *p.ctr = 0u;
             __threadfence_system();
             if (p.signal_done)
-                for (int i = 0; i < p.n_src; ++i) st_release_sys(p.done_remote[i], p.epoch);
+                for (int i = 0; i < p.n_src; ++i) st_release_sys(p.done_remote[i], p.epoch[i]);
         }
     }
 }
@@ -122,18 +122,28 @@ __device__ bool valid_split(const int32_t *b, int n, int L) {
 }
 
 // Block-local view of the migration: the layers this rank receives (and
-// from whom), the set of its senders and of its receivers.
+// from whom), the set of its senders and of its receivers.  ok = 0 when a
+// split is malformed or a stage -> rank entry lies outside [0, nranks) (e.g.
+// the -1 k_map_stages writes on failure): then nothing moves anywhere and
+// every rank reports DYNMO_E_INVALID in its window's error word.
 struct MigView {
     int n_in;
     unsigned senders, receivers;
     int ok;
 };
 
+__device__ __forceinline__ bool ranks_ok(const int32_t *rk, int n, int nranks) {
+    for (int s = 0; s < n; ++s)
+        if (rk[s] < 0 || rk[s] >= nranks) return false;
+    return true;
+}
+
 __device__ void mig_view(const DevMigArgs &a, MigView &v, int16_t *in_layers, int8_t *in_src) {
     if (threadIdx.x == 0) {
         v.n_in = 0;
         v.senders = v.receivers = 0u;
-        v.ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers);
+        v.ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
+               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
     }
     __syncthreads();
     if (v.ok) {
@@ -163,7 +173,8 @@ __global__ void k_mig_signal(DevMigArgs a) {
     if (threadIdx.x == 0) {
         s_recv = 0u;
         s_sent = 0ull;
-        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers);
+        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
+               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
     }
     __syncthreads();
     if (s_ok)
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
         int ok = v.ok;
         for (int r = 0; ok && r < a.nranks; ++r)
             if (v.senders & (1u << r)) ok &= wait_flag(&a.win->dready[r], epoch);
-        if (!ok) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+        if (!ok) atomicExch(&a.win->err, v.ok ? (int)DYNMO_E_NCCL : (int)DYNMO_E_INVALID);
         s_ok = ok;
     }
     __syncthreads();
@@ -224,7 +235,13 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_pull(DevMigArgs a) {
                 const int64_t idx = (int64_t)i * a.n_bufs + k;
                 const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
                 const DevBuf rb = a.recv_tab[idx];
-                const uint64_t bytes = (uint64_t)(sb.bytes < rb.bytes ? sb.bytes : rb.bytes);
+                if (sb.bytes != rb.bytes || (sb.bytes > 0 && (!sb.ptr || !rb.ptr))) {
+                    // the receive buffer does not match the sender's: reported,
+                    // never silently truncated
+                    if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+                    continue;
+                }
+                const uint64_t bytes = (uint64_t)sb.bytes;
                 recvd += bytes;
                 const uint8_t *sp = (const uint8_t *)sb.ptr;
                 uint8_t *dp = (uint8_t *)rb.ptr;

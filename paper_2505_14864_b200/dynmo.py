@@ -138,6 +138,12 @@ class Context:
             out[name] = (ms.value, cnt.value)
         return out
 
+    def p2p_error(self) -> int:
+        """Sticky device error word of the peer-memory paths (0 = none)."""
+        e = C.c_int32(0)
+        _check(lib().dynmo_ctx_p2p_error(self._h, C.byref(e)), "dynmo_ctx_p2p_error")
+        return int(e.value)
+
     def close(self):
         if getattr(self, "_h", None):
             lib().dynmo_ctx_destroy(self._h)

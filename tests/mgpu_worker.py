@@ -338,6 +338,72 @@ def main():
         if rank != world - 1:
             assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "empty rank")
     pplan.close()
+    # the host-driven pull with a CHANGING set of ranks
+    # that move data between calls (some ranks sit calls out).  Epochs are
+    # per directed rank pair, so every call is exact whatever the history.
+    recv_all = {l: [torch.zeros(int(payload[l]), dtype=torch.uint8, device=dev)]
+                for l in range(shape.L) if not (begin <= l < begin + count)}
+    pmx = D.PeerMigrator(ctx, shape.L, send, recv_all)
+    seq = []
+    for r_src, r_dst in [(0, 1), (world - 1, 0), (1, world - 1), (0, 1), (world - 1, 0), (1, 0)]:
+        if r_src == r_dst:
+            continue
+        rn_x = ranks.copy()
+        s_src = [s_ for s_ in range(n) if ranks[s_] == r_src]
+        rn_x[s_src[-1]] = r_dst  # the last stage of r_src moves to r_dst
+        seq.append(rn_x)
+    for it, rn_x in enumerate(seq * 2):
+        mv = oracle.moves(shape.L, b_old, ranks, b_old, rn_x)
+        for l, s_, d_ in mv:
+            if d_ == rank:
+                recv_all[int(l)][0].zero_()
+        sx, gx = pmx(b_old, ranks, b_old, rn_x)
+        torch.cuda.synchronize()
+        assert sx == sum(int(payload[l]) for l, s_, _ in mv if s_ == rank), (rank, it, "changing sets")
+        assert gx == sum(int(payload[l]) for l, _, d_ in mv if d_ == rank), (rank, it, "changing sets")
+        for l, s_, d_ in mv:
+            if d_ == rank:
+                assert torch.equal(recv_all[int(l)][0].cpu(), pattern(int(l), int(payload[l]))), (rank, it, int(l))
+    assert pmx.error() == 0
+    pmx.close()
+    # a plan-creation failure on ONE rank fails the
+    # collective plan creation on EVERY rank instead of leaving the others in
+    # the setup all-gather
+    bad_segs = segs if rank != 0 else segs + [D.SegmentSpec(keep[0], LB.SRC_MASK_U8, shape.L + 5)]
+    try:
+        D.ProfilePlan(ctx, bad_segs, begin, count, n_total=shape.L, exchange="p2p")
+        raised = False
+    except RuntimeError:
+        raised = True
+    assert raised, (rank, "profile plan agreement")
+    bad_send = dict(send)
+    if rank == 0:
+        bad_send[begin] = [torch.zeros(16, dtype=torch.uint8)]  # host memory: not IPC-mappable
+    try:
+        D.PeerMigrator(ctx, shape.L, bad_send, recv_all)
+        raised = False
+    except (RuntimeError, ValueError):
+        raised = True
+    assert raised, (rank, "migrate plan agreement")
+    # a plan after the failed ones still works (no rank is out of step)
+    plan_ok = D.ProfilePlan(ctx, segs, begin, count, n_total=shape.L, exchange="p2p")
+    c_ok, _, st_ok = D.profile_layers(ctx, plan_ok, coef)
+    torch.cuda.synchronize()
+    assert int(st_ok.item()) == 0 and np.array_equal(c_ok.cpu().numpy(), want_cost)
+    plan_ok.close()
+    # a stage -> rank entry outside [0, nranks) (the -1 a
+    # failed map_stages writes) moves nothing and reports INVALID on every
+    # rank -- no out-of-bounds table read, no hang.  Last: the error is sticky.
+    pmb = D.PeerMigrator(ctx, shape.L, send, recv_all)
+    for t in recv_all.values():
+        t[0].fill_(7)
+    rn_bad = d_ro.clone()
+    rn_bad[n - 1] = -1
+    pmb.device(d_bo, d_ro, bnd, rn_bad, bs, br)
+    torch.cuda.synchronize()
+    assert pmb.error() == LB.E_INVALID, (rank, pmb.error())
+    assert all(bool((t[0] == 7).all()) for t in recv_all.values()), rank
+    pmb.close()
     # Releasing GPUs after re-packing: split the ctx -- even
     # ranks stay active, odd ranks are released (None) -- then the smaller
     # group profiles, partitions and maps its stages onto its own ranks

@@ -1018,3 +1018,112 @@ def test_ctx_barrier_timing_detach_and_split_single(D, L, ctx):
     sub.close()
     assert ctx.split(active=False) is None
     del g
+
+
+# ------------------------------- round 2: hand traces, large n, 1-rank exchange
+import json as _json
+import os as _os
+
+_GOLD = _json.load(open(_os.path.join(_os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def test_diffuse_hand_traces_gpu(D, ctx):
+    """The hand-worked traces of DESIGN.md 2a (tests/golden) on the GPU,
+    stopped after every round (max_rounds = r) and run to the end: the kernel
+    reproduces each hand-derived split / phi and, for F1/F2, the fluid loads
+    after every round (dyadic, so exact)."""
+    for ex in _GOLD["diffusion_traces"]:
+        n = len(ex["bnd_in"]) - 1
+        mem = ex.get("mem")
+        wm = mem is not None
+        rows = [r for r in ex["rounds"] if r["bnd_after"] is not None]
+        for r in range(len(rows) + 2):
+            x = dict(cost=np.array(ex["cost"]), n=n, bnd_in=np.array(ex["bnd_in"], np.int32),
+                     mem=np.array(mem) if wm else None, cap=ex.get("cap", 0), gamma=ex["gamma"])
+            b, o = _run_diffuse(D, ctx, [x], wm, r)
+            want_b = ex["bnd_in"] if r == 0 else (rows[r - 1]["bnd_after"] if r <= len(rows) else ex["bnd_out"])
+            assert list(o["bnd"][:n + 1]) == list(want_b), (ex["name"], r)
+            assert o["rounds"][0] == min(r, ex["n_rounds"]) and o["phi0"][0] == ex["phi0"], (ex["name"], r)
+            assert o["status"][0] == (0 if r >= ex["n_rounds"] else 1), (ex["name"], r)
+        assert o["phi"][0] == ex["phi"]
+    for ex in _GOLD["fluid_traces"]:
+        n = len(ex["bnd_in"]) - 1
+        for r, xr in enumerate(ex["x_after"]):
+            x = dict(cost=np.array(ex["cost"]), n=n, bnd_in=np.array(ex["bnd_in"], np.int32), mem=None, cap=0,
+                     gamma_f=ex["gamma_f"])
+            b, o = _run_diffuse(D, ctx, [x], False, r)
+            assert list(o["fluid_x"][:n]) == xr and o["fluid_rounds"][0] == r, (ex["name"], r)
+            assert o["fluid_phi"][0] == ex["phi_after"][r]
+
+
+@pytest.mark.parametrize("n,Lmax,with_mem", [(33, 200, False), (64, 600, True), (200, 1023, False),
+                                             (200, 1023, True)])
+def test_diffuse_large_n(D, ctx, n, Lmax, with_mem):
+    """Diffusion with n > 32 stages: the lane-strided
+    discrete loops and the serial fluid path of k_diffuse, L up to 1023,
+    against the oracle element by element (fluid loads bit-equal)."""
+    g = np.random.default_rng(n * 7 + Lmax)
+    insts = []
+    for q in range(12):
+        Ly = int(g.integers(n, Lmax + 1)) if q else Lmax
+        cost = g.integers(0, 1000, Ly)
+        cost[g.random(Ly) < 0.1] = 0
+        inner = np.sort(g.choice(np.arange(1, Ly), n - 1, replace=False))
+        bnd = np.concatenate([[0], inner, [Ly]]).astype(np.int32)
+        x0 = oracle.stage_loads(cost, bnd).astype(float)
+        x = dict(cost=cost, n=n, bnd_in=bnd, gamma=0, gamma_f=float(g.choice([1e-9, 1e-3])) * oracle.phi_f64(x0),
+                 mem=None, cap=0)
+        if with_mem:
+            x["mem"] = g.integers(0, 50, Ly)
+            x["cap"] = int(max(x["mem"].max(), x["mem"].sum() * 2 // n))
+        insts.append(x)
+    _check_diffuse(D, ctx, insts, with_mem, 4096)
+
+
+@pytest.mark.parametrize("exchange", [1, 2])
+def test_profile_exchange_single_rank(D, L, ctx, exchange):
+    """Exchange modes on a one-rank ctx: the peer-memory
+    LL slots (encode with the call epoch, poll/decode, double buffering by
+    epoch parity) and the NCCL all-gather (a one-rank communicator) + unpack
+    run against the oracle on one GPU, over several calls and CUDA-graph
+    replays; a slice that does not tile [0, n_total) gives INVALID."""
+    T, Lyr = 300_007, 24
+    e = synth.cfg3_exit_depth(T=T, L=Lyr)
+    tok = oracle.exit_survivors(e, 0, Lyr)
+    seg = [D.SegmentSpec(_dev(e), L.SRC_EXIT_U8, 0)]
+    c1 = D.Context(0)
+    plan = D.ProfilePlan(c1, seg, 0, Lyr, Lyr, exchange=exchange)
+    memv = np.arange(Lyr, dtype=np.int64) * 1000 + 7
+    coef = D.coef_tensor(Lyr, A=3, device=DEV)
+    want = [oracle.layer_cost(tok=int(tok[i]), A=3)[1] for i in range(Lyr)]
+    cost = torch.empty(Lyr, dtype=torch.int64, device=DEV)
+    mem = torch.empty(Lyr, dtype=torch.int64, device=DEV)
+    st = torch.empty(1, dtype=torch.int32, device=DEV)
+    mem_local = _dev(memv)
+    for _ in range(3):
+        cost.fill_(-5); mem.fill_(-5)
+        D.profile_layers(c1, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=st)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        assert np.array_equal(cost.cpu().numpy(), want) and np.array_equal(mem.cpu().numpy(), memv)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    gph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s), torch.cuda.graph(gph, stream=s):
+        D.profile_layers(c1, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=st, stream=s)
+    for _ in range(5):
+        cost.fill_(-5)
+        gph.replay()
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0 and np.array_equal(cost.cpu().numpy(), want)
+    assert c1.p2p_error() == 0
+    # a slice that does not cover [0, n_total): layers 20..23 have no owner
+    plan2 = D.ProfilePlan(c1, seg, 0, 20, Lyr, exchange=exchange)
+    coef2 = D.coef_tensor(20, A=3, device=DEV)
+    cost2, _, st2 = D.profile_layers(c1, plan2, coef2)
+    torch.cuda.synchronize()
+    assert int(st2.item()) == L.E_INVALID
+    c2 = cost2.cpu().numpy()
+    assert np.array_equal(c2[:20], want[:20]) and np.all(c2[20:] == -1)
+    del gph, plan, plan2
+    c1.close()

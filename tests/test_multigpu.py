@@ -21,6 +21,11 @@ def test_exchange_and_migration(world):
            "--master-addr", "127.0.0.1", "--master-port", str(29500 + world),
            os.path.join(ROOT, "tests", "mgpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    log_dir = os.environ.get("DYNMO_MGPU_LOG_DIR")  # keep the raw pass log (evidence)
+    if log_dir:
+        os.makedirs(log_dir, exist_ok=True)
+        with open(os.path.join(log_dir, f"mgpu_worker_w{world}.log"), "w") as f:
+            f.write(f"$ {' '.join(cmd)}\nrc={r.returncode}\n--- stdout\n{r.stdout}\n--- stderr\n{r.stderr}\n")
     # ranks print concurrently, so lines can interleave: collect the rank ids
     ok = {int(x) for x in re.findall(r"MGPU_OK (\d+)", r.stdout)}
     assert r.returncode == 0 and ok == set(range(world)), r.stdout[-3000:] + r.stderr[-3000:]

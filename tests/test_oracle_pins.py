@@ -612,3 +612,102 @@ def test_map_stages_vs_bruteforce():
     assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2, 0b01)[0] == oracle.E_INFEASIBLE
     assert oracle.map_stages(4, [0, 2, 5], [0, 1], [0, 3, 4], [1, 1, 1, 1], 2)[0] == oracle.E_INVALID
     assert oracle.map_stages(4, [0, 2, 4], [0, 1], [0, 3, 4], [1, 1, 1, 1], 17)[0] == oracle.E_INVALID
+
+
+# ------------------------------------- O6 / O6' hand-worked traces (DESIGN 2a)
+def _edge_keys_by_enumeration(cost, b, mem=None, cap=0):
+    """Each edge's minimum of (pair max, |j - b|, j) by listing every j --
+    used only to check the hand-written golden rows themselves."""
+    P = np.concatenate([[0], np.cumsum(cost)])
+    M = np.concatenate([[0], np.cumsum(mem)]) if mem is not None else None
+    out = []
+    for e in range(len(b) - 2):
+        lo, cur, hi = b[e], b[e + 1], b[e + 2]
+        keys = [(max(P[j] - P[lo], P[hi] - P[j]), abs(j - cur), j) for j in range(lo + 1, hi)
+                if M is None or (M[j] - M[lo] <= cap and M[hi] - M[j] <= cap)]
+        out.append(min(keys) if keys else None)
+    return out
+
+
+@pytest.mark.parametrize("ex", GOLD["diffusion_traces"], ids=lambda e: e["name"][:2])
+def test_diffusion_hand_traces(ex):
+    """Pin: hand-worked discrete-diffusion traces, n = 3-5
+    (DESIGN.md 2a): equal-gap tie -> lower edge (D1, D5), largest gap beats a
+    smaller improvable gap (D2), non-mutual picks (D1, D2, D5), the secondary
+    key |j - b| on both sides of b (D3, D4), two matched edges in one round
+    (D5), a memory cap excluding the cost-optimal re-split (D6).  The oracle
+    is stopped after every round (max_rounds = r) and its split compared with
+    the hand trace."""
+    cost, mem, cap = ex["cost"], ex.get("mem"), ex.get("cap", 0)
+    b = list(ex["bnd_in"])
+    for r, row in enumerate(ex["rounds"]):
+        x = oracle.stage_loads(cost, b)
+        assert list(x) == row["x"], (ex["name"], r)
+        assert oracle.phi(x) == (0, row["phi"]), (ex["name"], r)
+        if row["edges"] is not None:  # the golden row itself, by enumeration
+            keys = _edge_keys_by_enumeration(cost, b, mem, cap)
+            for e, (k, ge) in enumerate(zip(keys, row["edges"])):
+                assert (k[2], k[0]) == (ge["best_j"], ge["best_max"]), (ex["name"], r, e)
+                assert (k[0] < max(x[e], x[e + 1])) == ge["improvable"], (ex["name"], r, e)
+        st, bo, rr, ph, ph0 = oracle.diffuse(cost, ex["bnd_in"], ex["gamma"], r, mem=mem, cap=cap)
+        assert list(bo) == b and rr == r and ph == row["phi"] and ph0 == ex["phi0"], (ex["name"], r)
+        if row["bnd_after"] is None:
+            assert st == oracle.OK
+            break
+        assert st == oracle.W_NOT_CONVERGED
+        b = row["bnd_after"]
+    st, bo, rr, ph, ph0 = oracle.diffuse(cost, ex["bnd_in"], ex["gamma"], 64, mem=mem, cap=cap)
+    assert st == oracle.OK and list(bo) == ex["bnd_out"] and rr == ex["n_rounds"]
+    assert ph == ex["phi"] and ph0 == ex["phi0"]
+
+
+@pytest.mark.parametrize("ex", GOLD["fluid_traces"], ids=lambda e: e["name"][:2])
+def test_fluid_hand_traces(ex):
+    """Pin: hand-worked fluid traces (n = 3 and 4): x and phi_f
+    after every round (all values dyadic, so exact), stop at phi_f <= gamma_f."""
+    for r, (xr, pr) in enumerate(zip(ex["x_after"], ex["phi_after"])):
+        st, x, rr, ph = oracle.diffuse_fluid(ex["cost"], ex["bnd_in"], ex["gamma_f"], r)
+        assert list(x) == xr and ph == pr and rr == r, (ex["name"], r)
+        assert st == (oracle.OK if r == ex["n_rounds"] else oracle.W_NOT_CONVERGED)
+    st, x, rr, ph = oracle.diffuse_fluid(ex["cost"], ex["bnd_in"], ex["gamma_f"], 1000)
+    assert st == oracle.OK and rr == ex["n_rounds"] and list(x) == ex["x_after"][-1]
+
+
+def test_map_stages_vs_assignment_solver():
+    """Pin (independent of the subset DP): the kept bytes of
+    the O9 map equal the optimum of the rectangular assignment problem
+    w[s][g] (scipy's linear_sum_assignment, a Jonker-Volgenant solver) up to
+    G = 16; the returned map is injective, uses allowed ranks only and attains
+    that optimum; for G <= 8 brute force over every injective map in
+    lexicographic order pins the tie-break."""
+    import itertools
+    from scipy.optimize import linear_sum_assignment
+    g = np.random.default_rng(1606)
+    for it in range(300):
+        G = int(g.integers(1, 17))
+        L = int(g.integers(max(2, G), 64))
+        n_old = int(g.integers(1, min(L, G) + 1))
+        bo = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_old - 1, replace=False)), [L]]).astype(np.int32)
+        ro = g.choice(G, n_old, replace=False).astype(np.int32)
+        allowed = (1 << G) - 1 if it % 3 else int(g.integers(1, 1 << G))
+        ranks = [r for r in range(G) if (allowed >> r) & 1]
+        n_new = int(g.integers(1, min(L, len(ranks)) + 1))
+        bn = np.concatenate([[0], np.sort(g.choice(np.arange(1, L), n_new - 1, replace=False)), [L]]).astype(np.int32)
+        nb = g.integers(0, 5 if it % 2 else 1 << 20, L).astype(np.int64)
+        st, rn, kept = oracle.map_stages(L, bo, ro, bn, nb, G, allowed)
+        assert st == 0
+        owner = np.repeat(ro, np.diff(bo))
+        new_stage = np.repeat(np.arange(n_new), np.diff(bn))
+        w = np.zeros((n_new, G), np.int64)
+        np.add.at(w, (new_stage, owner), nb)
+        wa = w[:, ranks]
+        rows, cols = linear_sum_assignment(wa, maximize=True)
+        assert kept == int(wa[rows, cols].sum()), (G, n_new)
+        rn = [int(v) for v in rn]
+        assert len(set(rn)) == n_new and all((allowed >> r) & 1 for r in rn)
+        assert int(sum(w[s, rn[s]] for s in range(n_new))) == kept
+        if G <= 8:
+            best = max(sum(int(w[s, pi[s]]) for s in range(n_new)) for pi in itertools.permutations(ranks, n_new))
+            first = next(pi for pi in itertools.permutations(ranks, n_new)
+                         if sum(int(w[s, pi[s]]) for s in range(n_new)) == best)
+            assert tuple(rn) == first
