@@ -492,6 +492,7 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
             if (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32)
                 pre_words = std::max(pre_words, expert_words(std::min((int)h_segs[i].n_experts, kMaxExperts)));
             pre_ops |= k == DYNMO_SRC_EXIT_U8 ? 2 : (k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) ? 4 : 1;  // TIME: count family
+            if ((k == DYNMO_SRC_EXPERT_I64 || k == DYNMO_SRC_EXPERT_I32) && h_segs[i].n_experts > 16) pre_ops |= 8;
             const int64_t ne = h_segs[i].n_elem < 0 ? 0 : h_segs[i].n_elem;
             const int es = k == DYNMO_SRC_NZ_BF16 ? 2 : (k == DYNMO_SRC_NZ_F32 || k == DYNMO_SRC_EXPERT_I32) ? 4
                            : k == DYNMO_SRC_EXPERT_I64 ? 8 : 1;
@@ -507,6 +508,46 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
         if (const char *e = getenv("DYNMO_TILE_BYTES")) {  // tuning knob (multiple of 16)
             const long v = atol(e);
             if (v >= 16 && v % 16 == 0 && v <= (1l << 30)) tile_bytes = (uint32_t)v;
+        }
+    }
+    // Strided runs: consecutive bit-mask segments of one kind, back to back in
+    // memory, one per consecutive local layer, all of one 16-byte-multiple
+    // size in [512 B, 4 KiB] (config 5: 4096-bit token masks).  run[i] > 0:
+    // a run of run[i] segments starts at i; -1: a member (tiles emitted by
+    // the run's first segment).
+    std::vector<int32_t> run(std::max(0, n_segs), 0);
+    {
+        auto seg_bytes = [](const dynmo_segment &g) -> int64_t {  // bit-mask kinds only
+            switch (g.src_kind) {
+                case DYNMO_SRC_MASK_BITS:
+                case DYNMO_SRC_TOKMASK_BITS: return g.n_elem % 8 ? -1 : g.n_elem / 8;
+                default: return -1;
+            }
+        };
+        auto start_ok = [&](const dynmo_segment &g) {
+            const int64_t nb = seg_bytes(g);
+            const int q = g.layer - layer_begin;
+            return g.n_elem > 0 && g.d_ptr && nb > 0 && nb % 16 == 0 && nb / 16 >= kStridedMinVec &&
+                   nb / 16 <= kStridedMaxVec && ((uintptr_t)g.d_ptr & 15) == 0 && q >= 0 && q < n_local;
+        };
+        const char *e = getenv("DYNMO_STRIDED");  // 0: never merge (A/B knob)
+        for (int32_t i = 0; i < n_segs && !(e && e[0] == '0');) {
+            const dynmo_segment &a0 = h_segs[i];
+            if (!start_ok(a0)) {
+                ++i;
+                continue;
+            }
+            const int64_t nb = seg_bytes(a0);
+            int32_t j = i + 1;
+            while (j < n_segs && h_segs[j].src_kind == a0.src_kind && h_segs[j].n_elem == a0.n_elem &&
+                   (uintptr_t)h_segs[j].d_ptr == (uintptr_t)h_segs[j - 1].d_ptr + (uintptr_t)nb &&
+                   h_segs[j].layer == h_segs[j - 1].layer + 1 && h_segs[j].layer - layer_begin < n_local)
+                ++j;
+            if (j - i >= kStridedMinRun) {
+                run[i] = j - i;
+                for (int32_t m = i + 1; m < j; ++m) run[m] = -1;
+            }
+            i = j;
         }
     }
     bool any_exit = false, has_hist = false;
@@ -566,6 +607,18 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
         bytes += nb + (partial_bits ? 1 : 0);
         const int32_t lay = is_exit ? 0 : q;
         const uint16_t aux = (uint16_t)(E ? E : slot);
+        if (run[i] != 0) {  // member of a strided run: whole layers per tile
+            if (run[i] > 0) {
+                const uint32_t S = (uint32_t)(nb / 16);
+                const int32_t per = (int32_t)std::max<uint32_t>(1u, tile_bytes / (S * 16u));
+                for (int32_t l0 = 0; l0 < run[i]; l0 += per) {
+                    const int32_t k = std::min(per, run[i] - l0);
+                    vec.push_back(ProfTile{(const void *)(p + (uintptr_t)l0 * S * 16u), k * S * 16u, lay + l0,
+                                           (uint16_t)(op | OP_STRIDED), aux, S});
+                }
+            }
+            continue;
+        }
         if (op == OP_TIME) {  // pairs only need 8-byte alignment: tiles of <= 1024 pairs
             for (int64_t o = 0; o < nb; o += 16 * 1024) {
                 const int64_t len = std::min<int64_t>(16 * 1024, nb - o);
@@ -657,6 +710,7 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
     for (const ProfTile &t : tiles) {
         const int k = t.op & 0xF;
         pl->ops |= (k <= OP_NZ32 || k == OP_TIME) ? 1 : k == OP_EXIT ? 2 : 4;
+        if ((k == OP_EXP64 || k == OP_EXP32) && t.aux > 16) pl->ops |= 8;  // smem expert histograms
     }
     if (!pl->ops) pl->ops = 1;
     const int64_t cap_blocks = (int64_t)ctx->num_sms * profile_blocks_per_sm(pl->ops, pl->warp_words);

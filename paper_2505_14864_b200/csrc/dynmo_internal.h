@@ -41,7 +41,15 @@ enum ProfOp : uint16_t {
     OP_TIME = 7,   // sum of (end - begin) over int64 timestamp pairs (TIME_NS)
     OP_KINDS = 8,
     OP_SCALAR = 0x10,  // flag: scalar tile
+    OP_STRIDED = 0x20, // flag: strided count tile -- whole layers of `bits` 16-byte vectors each,
+                       // back to back (layer = tile.layer + vector / bits), see kStrided*
 };
+// Strided tiles: runs of bit-mask segments of one kind that are contiguous
+// in memory, one per consecutive layer, all of the same 16-byte-multiple
+// size (e.g. config 5's 4096-bit MoD token masks, 512 B per layer) become
+// one descriptor per tile instead of one per layer.
+constexpr uint32_t kStridedMinVec = 32, kStridedMaxVec = 256;  // layer sizes 512 B .. 4 KiB
+constexpr int kStridedMinRun = 8;                              // layers per run worth merging
 
 // Accumulator slots per local layer in the device workspace.
 enum { ACC_NNZ = 0, ACC_TOK = 1, ACC_TIME = 2, ACC_N = 3 };
@@ -50,9 +58,10 @@ struct ProfTile {
     const void *ptr;   // first byte
     uint32_t nbytes;   // bytes in the tile
     int32_t layer;     // local layer index (ignored by OP_EXIT)
-    uint16_t op;       // ProfOp | OP_SCALAR
+    uint16_t op;       // ProfOp | OP_SCALAR | OP_STRIDED
     uint16_t aux;      // count ops: accumulator slot; OP_EXP*: E;
-    uint32_t bits;     // scalar OP_POPC: valid bits in the (single) last byte, 0 = all 8
+    uint32_t bits;     // scalar OP_POPC: valid bits in the (single) last byte, 0 = all 8;
+                       // OP_STRIDED: 16-byte vectors per layer
 };
 static_assert(sizeof(ProfTile) == 24, "tile layout");
 

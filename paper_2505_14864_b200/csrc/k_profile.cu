@@ -109,16 +109,157 @@ __device__ __forceinline__ uint32_t count_vec_rt(int kind, uint4 v) {
     }
 }
 
-__device__ __forceinline__ bool small_count_tile(const ProfTile &t) {
-    return (t.op & 0xF) <= OP_NZ32 && !(t.op & OP_SCALAR) && (t.nbytes >> 4) <= 32;
+// ---------------------------------------------- MoE ids, E <= 16 (a3)
+// One-hot counting in 8-bit fields of 64-bit registers: expert x adds
+// 1 << 8x to acc0 (x < 8) or 1 << 8(x-8) to acc1 (8 <= x < 16).  The shift
+// amount is clamped to 64 first (min(x, 8) * 8), and shl.b64 by 64 is 0, so
+// ids outside [0, 8) / [8, 16) add nothing and no branch is taken.
+__device__ __forceinline__ unsigned long long onehot8(uint32_t x) {
+    unsigned long long r;
+    const uint32_t sh = (x < 8u ? x : 8u) << 3;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(1ull), "r"(sh));
+    return r;
 }
 
-// OPS: bit 0 count ops present, bit 1 exit histogram, bit 2 expert histograms
-// (paths of absent op families are compiled out: fewer registers).
+// Validation of the ids without per-entry compares on 64 bits: a valid id
+// has a zero high word (int64) and a low word < E; OR of the high words and
+// the max of the low words (unsigned: a negative int32 id is >= 2^31) over
+// the tile decide it once per tile.
+template <int ESZ, bool E16>
+struct ExpertLane {
+    unsigned long long acc0 = 0, acc1 = 0;
+    uint32_t hi = 0, mx = 0;
+    __device__ __forceinline__ void id(uint32_t x) {
+        mx = x > mx ? x : mx;
+        acc0 += onehot8(x);
+        if constexpr (E16) acc1 += onehot8(x - 8u);  // x < 8 wraps to >= 2^32-8: adds 0
+    }
+    __device__ __forceinline__ void vec(const uint4 &v) {
+        if constexpr (ESZ == 8) {
+            hi |= v.y | v.w;
+            id(v.x);
+            id(v.z);
+        } else {
+            id(v.x);
+            id(v.y);
+            id(v.z);
+            id(v.w);
+        }
+    }
+};
+
+__device__ __forceinline__ bool small_count_tile(const ProfTile &t) {
+    return (t.op & 0xF) <= OP_NZ32 && !(t.op & (OP_SCALAR | OP_STRIDED)) && (t.nbytes >> 4) <= 32;
+}
+
+// Strided tile (bit masks: MASK_BITS / TOKMASK_BITS): k whole layers of S >= 32 vectors each (one per warp lane
+// and chunk).  Each warp iteration covers 8 layers: one 16-byte load per
+// lane per layer (8 loads in flight, each load instruction reading 512
+// contiguous bytes of one layer), chunks of 32 vectors accumulated for
+// S > 32, then one warp reduction per layer and lane u adds layer g0 + u's
+// count with one 64-bit atomic (distinct layers: no same-address contention,
+// and no per-layer descriptor to fetch).
+__device__ __forceinline__ void count_strided(const ProfTile &t, int lane, unsigned long long *acc) {
+    const uint32_t S = t.bits;
+    const uint32_t k = t.nbytes / (S * 16u);
+    const uint4 *p = (const uint4 *)t.ptr;
+    for (uint32_t g0 = 0; g0 < k; g0 += 8u) {
+        uint32_t c[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) c[u] = 0u;
+        for (uint32_t x = (uint32_t)lane; x < S; x += 32u) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = g0 + u < k ? ld_stream(p + (size_t)(g0 + u) * S + x) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) c[u] += count_vec<OP_POPC>(v[u]);
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t r = __reduce_add_sync(0xFFFFFFFFu, c[u]);
+            mine = lane == u ? r : mine;
+        }
+        if (lane < 8 && g0 + lane < k && mine)
+            atomicAdd(&acc[(int64_t)(t.layer + (int32_t)(g0 + lane)) * ACC_N + t.aux], (unsigned long long)mine);
+    }
+}
+
+// One tile of E <= 16 expert ids: 8 x 16-byte loads in flight per lane (as
+// the count ops), full batches without bounds predicates, the ragged last
+// batch predicated; fields spilled to the warp counters before they can
+// reach 256 (nacc is warp-uniform: every lane adds the batch maximum).
+template <int ESZ, bool E16, typename Spill>
+__device__ __forceinline__ void expert_small(const ProfTile &t, bool scalar, int lane, uint32_t E,
+                                             unsigned long long &acc0, unsigned long long &acc1,
+                                             uint32_t &nacc, uint32_t &bad, Spill &spill) {
+    ExpertLane<ESZ, E16> el;
+    el.acc0 = acc0;
+    el.acc1 = acc1;
+    constexpr int U = 8;
+    constexpr uint32_t PER = U * (16 / ESZ);  // ids per lane per batch
+    if (scalar) {
+        if (nacc > 254u) {
+            acc0 = el.acc0;
+            acc1 = el.acc1;
+            spill();
+            el.acc0 = el.acc1 = 0;
+        }
+        const uint32_t ne = t.nbytes / ESZ;
+        if ((uint32_t)lane < ne) {
+            if constexpr (ESZ == 8) {
+                const uint2 w = ((const uint2 *)t.ptr)[lane];
+                el.hi |= w.y;
+                el.id(w.x);
+            } else {
+                el.id(((const uint32_t *)t.ptr)[lane]);
+            }
+        }
+        nacc += 1;
+    } else {
+        const uint4 *p = (const uint4 *)t.ptr;
+        const uint32_t nvec = t.nbytes >> 4;
+        const uint32_t nfull = nvec / (32u * U) * (32u * U);
+        for (uint32_t base = 0; base < nvec; base += 32u * U) {
+            if (nacc > 255u - PER) {
+                acc0 = el.acc0;
+                acc1 = el.acc1;
+                spill();
+                el.acc0 = el.acc1 = 0;
+            }
+            uint4 v[U];
+            if (base < nfull) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) v[u] = ld_stream(p + base + (uint32_t)u * 32u + (uint32_t)lane);
+#pragma unroll
+                for (int u = 0; u < U; ++u) el.vec(v[u]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
+                    v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (base + (uint32_t)u * 32u + (uint32_t)lane < nvec) el.vec(v[u]);
+            }
+            nacc += PER;
+        }
+    }
+    acc0 = el.acc0;
+    acc1 = el.acc1;
+    bad |= (el.hi != 0u) | (el.mx >= E);
+}
+
+// OPS: bit 0 count ops present, bit 1 exit histogram, bit 2 expert histograms,
+// bit 3 expert layers with E > 16 (paths of absent op families are compiled
+// out: fewer registers, more resident warps).
 template <int OPS>
-__global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
+__global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OPS & 8) ? 2 : 3) k_profile(ProfArgs a) {
     pdl_trigger();  // the epilogue may be scheduled now (it waits for this grid)
     constexpr bool HAS_CNT = OPS & 1, HAS_EXIT = (OPS & 2) != 0, HAS_EXP = (OPS & 4) != 0;
+    constexpr bool HAS_BIGE = (OPS & 8) != 0;  // some expert layer has E > 16 (smem histograms)
     constexpr bool HAS_HIST = HAS_EXIT || HAS_EXP;
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -211,6 +352,12 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
         const ProfTile t = nxt;
         const int kind = t.op & 0xF;
         const bool scalar = (t.op & OP_SCALAR) != 0;
+        if (HAS_CNT && (t.op & OP_STRIDED)) {
+            if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
+            DYNMO_DCHECK(t.layer + (int64_t)(t.nbytes / (t.bits * 16u)) <= a.n_local);
+            count_strided(t, lane, a.acc);
+            continue;
+        }
         if (HAS_CNT && small_count_tile(t)) {
             // Up to 8 consecutive small tiles (<= 512 B each, e.g. the
             // 4096-token masks of config 5) per warp iteration: 4 lanes per
@@ -341,52 +488,18 @@ __global__ void __launch_bounds__(kProfThreads) k_profile(ProfArgs a) {
                 hist_layer = t.layer;
                 hist_E = E;
             }
-            const int esz = kind == OP_EXP64 ? 8 : 4;
             if (E <= 16) {
-                auto addr = [&](uint64_t v) {
-                    bad |= v >= (uint64_t)E;
-                    const unsigned long long one = 1ull << (8 * ((uint32_t)v & 7u));
-                    if (v < 8) acc0 += one;
-                    else if (v < (uint64_t)E) acc1 += one;
-                };
-                if (scalar) {
-                    const uint32_t ne = t.nbytes / esz;
-                    if ((uint32_t)lane < ne)
-                        addr(esz == 8 ? (uint64_t)((const int64_t *)t.ptr)[lane]
-                                      : (uint64_t)(int64_t)((const int32_t *)t.ptr)[lane]);
-                    nacc += 1;
+                if (kind == OP_EXP64) {
+                    if (E <= 8) expert_small<8, false>(t, scalar, lane, (uint32_t)E, acc0, acc1, nacc, bad, spill_regs);
+                    else expert_small<8, true>(t, scalar, lane, (uint32_t)E, acc0, acc1, nacc, bad, spill_regs);
                 } else {
-                    const uint4 *p = (const uint4 *)t.ptr;
-                    const uint32_t nvec = t.nbytes >> 4;
-                    // 4 vectors in flight per lane: the per-entry counting is the
-                    // heavier part here, so fewer registers and more resident warps
-                    for (uint32_t base = 0; base < nvec; base += 32u * 4u) {
-                        uint4 v[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
-                            v[u] = idx < nvec ? ld_stream(p + idx) : make_uint4(0u, 0u, 0u, 0u);
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const uint32_t idx = base + (uint32_t)u * 32u + (uint32_t)lane;
-                            if (idx >= nvec) continue;
-                            if (esz == 8) {
-                                addr(((uint64_t)v[u].y << 32) | v[u].x);
-                                addr(((uint64_t)v[u].w << 32) | v[u].z);
-                            } else {
-                                addr((uint64_t)(int64_t)(int32_t)v[u].x);
-                                addr((uint64_t)(int64_t)(int32_t)v[u].y);
-                                addr((uint64_t)(int64_t)(int32_t)v[u].z);
-                                addr((uint64_t)(int64_t)(int32_t)v[u].w);
-                            }
-                        }
-                        nacc += 16;  // <= 16 entries per lane per batch
-                        if (__any_sync(0xFFFFFFFFu, nacc > 240 - 16)) spill_regs();
-                    }
+                    if (E <= 8) expert_small<4, false>(t, scalar, lane, (uint32_t)E, acc0, acc1, nacc, bad, spill_regs);
+                    else expert_small<4, true>(t, scalar, lane, (uint32_t)E, acc0, acc1, nacc, bad, spill_regs);
                 }
                 continue;
             }
+            if constexpr (!HAS_BIGE) continue;
+            const int esz = kind == OP_EXP64 ? 8 : 4;
             const bool cols = E <= kColExperts;
             DYNMO_DCHECK((cols ? 32 * E : E) <= a.warp_words && E <= a.max_E && t.layer < a.n_local);
             auto add = [&](uint64_t v) {
@@ -751,28 +864,37 @@ static cudaError_t launch_t(const ProfArgs &a, int grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+// ops: bit 3 (E > 16) only ever comes with bit 2
 int profile_blocks_per_sm(int ops, int warp_words) {
-    switch (ops & 7) {
+    switch (ops & 15) {
         case 1: return blocks_per_sm_t<1>(warp_words);
         case 2: return blocks_per_sm_t<2>(warp_words);
         case 3: return blocks_per_sm_t<3>(warp_words);
         case 4: return blocks_per_sm_t<4>(warp_words);
         case 5: return blocks_per_sm_t<5>(warp_words);
         case 6: return blocks_per_sm_t<6>(warp_words);
-        default: return blocks_per_sm_t<7>(warp_words);
+        case 7: return blocks_per_sm_t<7>(warp_words);
+        case 12: return blocks_per_sm_t<12>(warp_words);
+        case 13: return blocks_per_sm_t<13>(warp_words);
+        case 14: return blocks_per_sm_t<14>(warp_words);
+        default: return blocks_per_sm_t<15>(warp_words);
     }
 }
 
 cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s) {
     if (a.n_tiles == 0) return cudaSuccess;
-    switch (ops & 7) {
+    switch (ops & 15) {
         case 1: return launch_t<1>(a, grid, s);
         case 2: return launch_t<2>(a, grid, s);
         case 3: return launch_t<3>(a, grid, s);
         case 4: return launch_t<4>(a, grid, s);
         case 5: return launch_t<5>(a, grid, s);
         case 6: return launch_t<6>(a, grid, s);
-        default: return launch_t<7>(a, grid, s);
+        case 7: return launch_t<7>(a, grid, s);
+        case 12: return launch_t<12>(a, grid, s);
+        case 13: return launch_t<13>(a, grid, s);
+        case 14: return launch_t<14>(a, grid, s);
+        default: return launch_t<15>(a, grid, s);
     }
 }
 

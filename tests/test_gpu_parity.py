@@ -1127,3 +1127,41 @@ def test_profile_exchange_single_rank(D, L, ctx, exchange):
     assert np.array_equal(c2[:20], want[:20]) and np.all(c2[20:] == -1)
     del gph, plan, plan2
     c1.close()
+
+
+@pytest.mark.parametrize("T_bits", [4096, 8192, 32768])
+def test_profile_strided_bitmask_runs(D, L, ctx, T_bits):
+    """Runs of bit-mask segments back to back in memory (one per consecutive
+    layer, equal sizes) become strided tiles (one descriptor per tile of
+    whole layers): run lengths that are not multiples of 8, a run broken by
+    a gap, by a different size and by a non-consecutive layer, S = 32 / 64 /
+    256 vectors per layer, MASK_BITS and TOKMASK_BITS; per-layer counts vs
+    the oracle."""
+    g = np.random.default_rng(T_bits)
+    W = T_bits // 32
+    nl = 61
+    words = g.integers(0, 2 ** 32, (nl + 3) * W, dtype=np.uint64).astype(np.uint32)
+    words[:W * 5] &= 0x01010101  # sparse rows too
+    d = _dev(words.view(np.int32))
+    segs, want = [], np.zeros(nl + 2, np.int64)
+    off = 0
+    for layer in range(nl):
+        if layer == 23:
+            off += W  # a gap: the run breaks here
+        kind = L.SRC_MASK_BITS if layer < 40 else L.SRC_TOKMASK_BITS  # kind change breaks the run
+        nb = T_bits if layer != 50 else T_bits - 128  # a shorter segment breaks the run
+        segs.append(D.SegmentSpec(d[off:off + nb // 32], kind, layer, n_elem=nb))
+        want[layer] = oracle.count_bits(words[off:off + nb // 32], nb)
+        off += W
+    # a second source on an earlier layer (not consecutive): its own tiles
+    segs.append(D.SegmentSpec(d[off:off + W], L.SRC_MASK_BITS, 3, n_elem=T_bits))
+    want[3] += oracle.count_bits(words[off:off + W], T_bits)
+    plan = D.ProfilePlan(ctx, segs, 0, nl + 2)
+    coef = D.coef_tensor(nl + 2, A=0, B=1, device=DEV)
+    for rep in range(2):
+        cost, _, st = D.profile_layers(ctx, plan, coef)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        assert np.array_equal(cost.cpu().numpy(), want), rep
+    if T_bits <= 32768:  # runs merged: far fewer tiles than segments
+        assert plan.n_tiles < len(segs) // 2, plan.n_tiles
