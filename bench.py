@@ -1,20 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the DynMo per-step rebalancing hot path on B200.
 
-Workload (BASELINE.json configs[1]): GPT-48 gradual global magnitude pruning
-at S = 0.9, 8 pipeline stages, stage s on GPU floor(s*G/8).  One step =
-  profile_layers   (u8 pruning masks of this GPU's layers -> int64 costs,
-                    + NCCL all-gather of the cost slots when G > 1)
+Default workload (BASELINE.json configs[1]): GPT-48 gradual global magnitude
+pruning at S = 0.9, 8 pipeline stages, stage s on GPU floor(s*G/8).  One step =
+  profile_layers   (this GPU's layers' sources -> int64 costs, + the exchange
+                    of the cost slots over NVLink peer memory when G > 1)
   partition_stages (centralised min-max split, memory capped)
   diffuse_balance  (decentralised diffusion + fluid process, from the
                     current split)
   repack_workers   (fewest GPUs within the dense pipeline's bottleneck)
-  D2H of the new boundaries, migrate_layers (NCCL send/recv of the CSR
-  payload of every layer whose GPU changes).
+  migrate_layers   (the payload of every layer whose GPU changes, pulled over
+                    NVLink peer memory; device-driven, in the step's graph)
 The step replays the same rebalance event (uniform split -> balanced split)
 every iteration; inputs stay resident in HBM; L2 is flushed between steps.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+--config selects the other BASELINE workloads with the same JSON schema:
+  3  GPT-32 freezing + early exit (per-layer token bitmasks, 512 x 2048
+     tokens, frozen prefix), dense-layer payload (bf16 + fp32 optimizer state)
+  4  Mixtral-8x7B-shaped MoE routing (int64 top-2 ids, E = 8, EP = 8) with
+     popularity drifting by depth, 2.90 GB bf16 payload per migrated layer
+  5  batched sweep: 4096 instances (48-128 layers, 2-8 stages, MoD token
+     bitmasks) -> partition + repack to the fewest workers; instances are
+     sharded 4096/G per GPU, no exchange, no migration
+
+  python bench.py [--config {2,3,4,5}] [--gpus N --steps K --warmup W] [--impl reference]
 Under torchrun (N > 1) one rank per GPU; rank 0 prints one JSON line.
 """
 from __future__ import annotations
@@ -33,16 +42,15 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-N_STAGES = 8
-SPARSITY = 0.9
-MILESTONE = 4
 METRIC = "rebalance ms/step (profile+partition+migrate) at 1/2/4/8 B200; profile HBM GB/s"
 L2_FLUSH_BYTES = 256 << 20
 NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="BASELINE.json workload (configs[1..4]); 2 = the headline")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
@@ -58,15 +66,16 @@ def parse():
                     help="which phases get CUDA-event nodes in the step graph")
     ap.add_argument("--map-stages", action="store_true",
                     help="NEXT-3: place the new stages on the GPU slots that keep the most payload in place "
-                         "(dynmo_map_stages inside the step) instead of stage s on GPU floor(s*G/8)")
+                         "(dynmo_map_stages inside the step) instead of stage s on GPU floor(s*G/n)")
     ap.add_argument("--host-migrate", action="store_true",
                     help="host-driven migration (D2H of the boundaries, then the migrate call) "
                          "instead of the device-driven call inside the step's graph")
-    ap.add_argument("--serial-solvers", action="store_true",
-                    help="run partition, diffusion and repack one after another on one stream")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every call eagerly instead of replaying a CUDA graph")
-    return ap.parse_args()
+    ap.add_argument("--cfg4-routing", choices=["drift", "aux", "sbase"], default="drift",
+                    help="config 4 popularity: Dirichlet alpha drifting 64 -> 0.3 with depth (default), "
+                         "alpha = 4 (aux-loss) or 64 (S-BASE) on every layer")
+    return ap.parse_args(argv)
 
 
 def load_peaks():
@@ -76,19 +85,22 @@ def load_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def workload_config(G):
-    shape = synth.GPTShape()
-    return {
-        "workload": "config2: GPT-48 gradual global magnitude pruning, S=0.9, 8 pipeline stages, "
-                    "u8 masks, rebalance from the uniform split",
-        "layers": shape.L, "hidden": shape.h, "stages": N_STAGES,
-        "params_per_layer": shape.params_per_layer,
-        "mask_bytes_total": shape.L * shape.params_per_layer,
-        "mask_repr": "u8", "stage_to_gpu": "floor(s*G/8)",
-        "l2": f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, then a {L2_FLUSH_BYTES >> 20} MiB "
-              "read so no dirty lines of the flush are written back inside the step)",
-        "parallelism": f"pp-profile{G}",
-    }
+def uniform_split(L, n):
+    """Megatron-style even split b_s = floor(s L / n) (bookkeeping, inline so
+    the oracle arm does not import the product package)."""
+    return np.array([(s * L) // n for s in range(n + 1)], np.int32)
+
+
+def stage_ranks(n, G):
+    """Stage s on GPU floor(s G / n)."""
+    return np.array([(s * G) // n for s in range(n)], np.int32)
+
+
+def rank_layers(bnd, ranks, rank):
+    mine = [s for s in range(len(bnd) - 1) if ranks[s] == rank]
+    if not mine:
+        return int(bnd[0]), 0
+    return int(bnd[mine[0]]), int(bnd[mine[-1] + 1] - bnd[mine[0]])
 
 
 class L2Flush:
@@ -108,23 +120,162 @@ class L2Flush:
         self.r.max()
 
 
-# ------------------------------------------------------------ input set-up
-class Inputs:
-    """Host arrays of this rank's layers (seeded, synthetic)."""
+L2_NOTE = (f"flushed between steps ({L2_FLUSH_BYTES >> 20} MiB write, then a {L2_FLUSH_BYTES >> 20} MiB "
+           "read so no dirty lines of the flush are written back inside the step)")
 
-    def __init__(self, rank_begin, rank_count):
+
+# --------------------------------------------------------------- workloads
+# A workload holds the host side of one BASELINE config for the layers of one
+# rank: seeded synthetic sources (synth/), the cost coefficients, the
+# per-layer payload (migration bytes = the solver's memory), the cap, the
+# repack bound.  Sources are (kind, layer, np array, n_elem, n_experts).
+SRC_MASK_U8, SRC_TOKMASK_BITS, SRC_EXPERT_I64 = 1, 4, 6  # include/dynmo.h dynmo_src_kind
+
+
+class Cfg2:
+    """GPT-48 gradual global magnitude pruning."""
+    key, L, n = 2, 48, 8
+    SPARSITY, MILESTONE = 0.9, 4
+
+    def __init__(self, args=None):
         self.shape = synth.GPTShape()
-        self.p = synth.cfg2_keep_probs(self.shape, SPARSITY, MILESTONE)
+        self.p = synth.cfg2_keep_probs(self.shape, self.SPARSITY, self.MILESTONE)
         self.payload = synth.cfg2_payload_bytes(self.shape, self.p)  # caller-side CSR bytes
-        self.begin, self.count = rank_begin, rank_count
-        self.masks = []  # (layer, np.uint8 flat)
-        for layer in range(rank_begin, rank_begin + rank_count):
-            for m in synth.cfg2_layer_masks_u8(self.shape, layer, self.p[layer], MILESTONE):
-                self.masks.append((layer, m.reshape(-1)))
-        M = int(self.payload.sum())
-        self.cap = int(1.5 * M / N_STAGES)                  # per-GPU memory budget
-        self.bound = (self.shape.L // N_STAGES) * self.shape.params_per_layer  # dense B*
-        self.gamma_fluid = 1.0                              # one weight (cost unit)
+        self.cap = int(1.5 * int(self.payload.sum()) / self.n)      # per-GPU memory budget
+        self.bound = (self.L // self.n) * self.shape.params_per_layer  # dense B*
+        self.gamma_fluid = 1.0
+        self.coef = dict(A=0, B=1)
+        self.frozen = None
+
+    def config(self, G):
+        return {"workload": "config2: GPT-48 gradual global magnitude pruning, S=0.9, 8 pipeline stages, "
+                            "u8 masks (the exact global top-k of the synthetic bf16 weights), rebalance from "
+                            "the uniform split",
+                "layers": self.L, "hidden": self.shape.h, "stages": self.n,
+                "params_per_layer": self.shape.params_per_layer,
+                "mask_bytes_total": self.L * self.shape.params_per_layer, "mask_repr": "u8",
+                "stage_to_gpu": "floor(s*G/8)", "l2": L2_NOTE, "parallelism": f"pp-profile{G}"}
+
+    def sources(self, begin, count):
+        for layer in range(begin, begin + count):
+            for m in synth.cfg2_layer_masks_u8(self.shape, layer, self.p[layer], self.MILESTONE):
+                yield (SRC_MASK_U8, layer, m.reshape(-1), None, 0)
+
+    def oracle_cost(self, src_list, layer_subset=None):
+        import oracle
+        nnz = np.zeros(self.L, np.int64)
+        for kind, layer, a, ne, E in src_list:
+            if layer_subset is None or layer in layer_subset:
+                nnz[layer] += oracle.count_nz_u8(a)
+        return np.array([oracle.layer_cost(nnz=int(v), **self.coef)[1] for v in nnz], np.int64)
+
+
+class Cfg3:
+    """GPT-32 layer freezing + early exit."""
+    key, L, n = 3, 32, 8
+    T, F, H = 512 * 2048, 8, 1024
+
+    def __init__(self, args=None):
+        self.e = synth.cfg3_exit_depth(T=self.T, L=self.L)
+        self.f = synth.cfg3_frozen(self.L, self.F)
+        P = 12 * self.H * self.H
+        # payload (reading Q19): bf16 weights, + fp32 master / m / v unless frozen
+        self.payload = np.array([P * (2 if self.f[i] else 14) for i in range(self.L)], np.int64)
+        self.cap = int(1.5 * int(self.payload.sum()) / self.n)
+        self.bound = (self.L // self.n) * self.T  # dense bottleneck: every token through L/n layers
+        self.gamma_fluid = 1.0
+        self.coef = dict(A=1, B=0)
+        self.frozen = self.f
+
+    def config(self, G):
+        return {"workload": f"config3: GPT-32 layer freezing (layers < {self.F} frozen) + early exit "
+                            "(no exit before layer 8, then 8%/layer), 512x2048 tokens, per-layer token "
+                            "bitmasks, 8 stages, rebalance from the uniform split",
+                "layers": self.L, "stages": self.n, "tokens": self.T, "frozen_prefix": self.F,
+                "mask_bytes_total": self.L * self.T // 8, "mask_repr": "token bitmasks (uint32)",
+                "stage_to_gpu": "floor(s*G/8)", "l2": L2_NOTE, "parallelism": f"pp-profile{G}"}
+
+    def sources(self, begin, count):
+        for layer in range(begin, begin + count):
+            yield (SRC_TOKMASK_BITS, layer, synth.pack_bits((self.e > layer).astype(np.uint8)), self.T, 0)
+
+    def oracle_cost(self, src_list, layer_subset=None):
+        import oracle
+        tok = np.zeros(self.L, np.int64)
+        for kind, layer, a, ne, E in src_list:
+            if layer_subset is None or layer in layer_subset:
+                tok[layer] += oracle.count_bits(a, ne)
+        return np.array([oracle.layer_cost(frozen=bool(self.f[i]), tok=int(tok[i]), **self.coef)[1]
+                         for i in range(self.L)], np.int64)
+
+
+class Cfg4:
+    """Mixtral-8x7B-shaped MoE routing."""
+    key, L, n = 4, 32, 8
+    T, E, K, EP = 64 * 2048, 8, 2, 8
+
+    def __init__(self, args=None):
+        self.routing = getattr(args, "cfg4_routing", "drift") if args is not None else "drift"
+        self.payload = np.full(self.L, synth.MIXTRAL_LAYER_PARAMS * 2, np.int64)  # bf16 layer
+        self.cap = int(1.5 * int(self.payload.sum()) / self.n)
+        self.coef = dict(A=self.T, C_=4, ep=self.EP)
+        balanced = self.T + 4 * self.T * self.K  # c = T + 4 moe with moe = T k when balanced
+        self.bound = (self.L // self.n) * balanced
+        self.gamma_fluid = 1.0
+        self.frozen = None
+
+    def config(self, G):
+        desc = {"drift": "Dirichlet alpha drifting 64 -> 0.3 with depth", "aux": "Dirichlet alpha 4 (aux-loss)",
+                "sbase": "Dirichlet alpha 64 (S-BASE)"}[self.routing]
+        return {"workload": f"config4: Mixtral-8x7B-shaped MoE routing, 32 layers, E=8, top-2, 64x2048 tokens, "
+                            f"EP=8, {desc}; 2.90 GB bf16 payload per migrated layer, rebalance from the "
+                            "uniform split",
+                "layers": self.L, "stages": self.n, "tokens": self.T, "experts": self.E, "top_k": self.K,
+                "routing": self.routing, "id_bytes_total": self.L * self.T * self.K * 8,
+                "payload_bytes_per_layer": int(self.payload[0]),
+                "stage_to_gpu": "floor(s*G/8)", "l2": L2_NOTE, "parallelism": f"pp-profile{G}"}
+
+    def ids(self, layer):
+        if self.routing == "drift":
+            return synth.cfg4_routing_drift(layer, self.L, T=self.T, E=self.E, k=self.K)
+        return synth.cfg4_routing(layer, T=self.T, E=self.E, k=self.K, alpha=4.0 if self.routing == "aux" else 64.0)
+
+    def sources(self, begin, count):
+        for layer in range(begin, begin + count):
+            yield (SRC_EXPERT_I64, layer, self.ids(layer).reshape(-1), None, self.E)
+
+    def oracle_cost(self, src_list, layer_subset=None):
+        import oracle
+        cost = np.zeros(self.L, np.int64)
+        for kind, layer, a, ne, E in src_list:
+            if layer_subset is None or layer in layer_subset:
+                st, h = oracle.expert_hist(a, E)
+                cost[layer] = oracle.layer_cost(cnt=h, **self.coef)[1]
+        return cost
+
+
+class Cfg5:
+    """Batched sweep: 4096 independent instances."""
+    key, N_INST, T = 5, 4096, 4096
+
+    def __init__(self, args=None):
+        self.insts = None
+
+    def config(self, G):
+        return {"workload": "config5: batched rebalance sweep, 4096 instances of 48-128 layers x 2-8 stages, "
+                            "MoD token bitmasks (T=4096, every other layer routed at 12.5% x U(0.5,1.5)), "
+                            "memory-capped partition + BOUND repack to the fewest workers",
+                "instances": self.N_INST, "instances_per_gpu": self.N_INST // G, "tokens": self.T,
+                "mask_repr": "token bitmasks (uint32), back to back per instance",
+                "sharding": "instances [r*4096/G, (r+1)*4096/G) on rank r, no exchange, no migration",
+                "l2": L2_NOTE, "parallelism": f"dp{G}"}
+
+    def shard(self, rank, G):
+        q0, q1 = rank * self.N_INST // G, (rank + 1) * self.N_INST // G
+        return [synth.cfg5_instance(i) for i in range(q0, q1)]
+
+
+WORKLOADS = {2: Cfg2, 3: Cfg3, 4: Cfg4, 5: Cfg5}
 
 
 # ------------------------------------------------------------------ clocks

@@ -990,8 +990,13 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     if ((plan->n_local > 0 && !d_coef) || !d_cost || !d_status) return invalid("null required output");
     cudaStream_t s = (cudaStream_t)stream;
     DeviceGuard g(ctx->device);
+    static const int64_t l2_max = [] {  // DYNMO_L2_PREFETCH_MAX=<bytes> (0: off), A/B knob
+        const char *e = getenv("DYNMO_L2_PREFETCH_MAX");
+        return e ? (int64_t)atoll(e) : kL2PrefetchMaxBytes;
+    }();
     ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
-                std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words, plan->n_local};
+                std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words, plan->n_local,
+                plan->bytes <= l2_max ? 1 : 0};
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PROFILE, s);
     CUDA_TRY(launch_profile(pa, plan->ops, plan->grid, s), "k_profile launch");
     phase_end(te, s);

@@ -121,7 +121,13 @@ struct ProfArgs {
     int32_t *ws_status;
     int32_t warp_words;  // per-warp histogram scratch (u32 words)
     int32_t n_local;     // layers of the plan (bounds of acc / hist rows)
+    int32_t l2_prefetch; // 1: each warp bulk-prefetches its whole tile range into L2 at entry
 };
+// Plans whose bytes fit comfortably in the 126 MB L2 issue one L2 bulk
+// prefetch per tile at kernel entry (all of a warp's range at once), so the
+// HBM queues fill at once instead of one register batch per warp at a time
+// (small per-GPU shares are latency / ramp bound).
+constexpr int64_t kL2PrefetchMaxBytes = 96ll << 20;
 
 struct PeerWindow;
 constexpr int kMaxRanksEpi = 16;

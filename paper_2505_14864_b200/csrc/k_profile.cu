@@ -282,6 +282,16 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
     const int64_t per = (a.n_tiles + nwarps - 1) / nwarps;
     const int64_t t_beg = warp * per;
     const int64_t t_end = t_beg + per < a.n_tiles ? t_beg + per : a.n_tiles;
+    if (a.l2_prefetch) {
+        // the warp's tiles are read once, soon: one fire-and-forget L2 bulk
+        // prefetch per vector tile (lane j: tile t_beg + j, then + 32 ...)
+        for (int64_t ti = t_beg + lane; ti < t_end; ti += 32) {
+            const ProfTile d = a.tiles[ti];
+            if (!(d.op & OP_SCALAR) && (d.op & 0xF) != OP_TIME && d.nbytes >= 16u)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.ptr), "r"(d.nbytes & ~15u)
+                             : "memory");
+        }
+    }
     int64_t run_key = -1;
     unsigned long long run_sum = 0;
     int exit_dirty = 0;       // exit histogram pending in sh (flushed once at the end)

@@ -136,6 +136,26 @@ def cfg2_payload_bytes(shape: GPTShape, p: np.ndarray) -> np.ndarray:
     return nnz * 18 + rowptr
 
 
+CFG2_TAU_BF16 = 0x3C00  # bf16 bit pattern of the global magnitude threshold (2^-7)
+
+
+def cfg2_topk_weights_bf16(mask_u8: np.ndarray, layer: int, t: int, milestone: int = 4) -> np.ndarray:
+    """bf16 weights whose GLOBAL top-k by magnitude (Alg. 1) is
+    exactly the given masks, k = the masks' kept count: every kept weight has
+    a magnitude bit pattern in [TAU, TAU + 1024) and every pruned one in
+    [0, TAU) (positive bf16 patterns are ordered like their values), so no
+    pruned magnitude reaches any kept one and there is no tie across the
+    threshold.  Random signs.  With cfg2_layer_masks_u8's Bernoulli draws
+    under the erfc threshold of cfg2_keep_probs this makes the config-2
+    masks the exact global top-k of these weights (no selection is done
+    here: the order holds by construction)."""
+    g = rng(2, 3, milestone, layer, t)
+    kept = g.integers(CFG2_TAU_BF16, CFG2_TAU_BF16 + 1024, mask_u8.shape, dtype=np.uint16)
+    pruned = g.integers(0, CFG2_TAU_BF16, mask_u8.shape, dtype=np.uint16)
+    sign = (g.integers(0, 2, mask_u8.shape, dtype=np.uint16) << 15).astype(np.uint16)
+    return (np.where(mask_u8 != 0, kept, pruned) | sign).astype(np.uint16)
+
+
 def cfg2_bf16_weights(mask_u8: np.ndarray, layer: int, t: int) -> np.ndarray:
     """bf16 bit patterns of masked weights: pruned -> +0 or -0 (random sign),
     kept -> nonzero normal draws (small tests only)."""
@@ -189,6 +209,29 @@ def cfg4_routing(layer: int, T: int = 64 * 2048, E: int = 8, k: int = 2, alpha: 
     alpha=64 'S-BASE' (near balanced).  Gumbel-top-k sampling."""
     g = rng(4, seed_key, layer, int(alpha))
     pi = g.dirichlet(np.full(E, alpha))
+    gumb = -np.log(-np.log(g.random((T, E))))
+    score = np.log(pi)[None, :] + gumb
+    idx = np.argpartition(-score, k - 1, axis=1)[:, :k]
+    return np.ascontiguousarray(idx.astype(dtype))
+
+
+def cfg4_alpha_drift(layer: int, L: int = 32, a0: float = 64.0, a1: float = 0.3) -> float:
+    """Routing popularity that drifts with depth: the
+    Dirichlet concentration falls geometrically from a0 (S-BASE-like, near
+    balanced) at layer 0 to a1 (strongly skewed) at layer L-1, so deep MoE
+    layers carry more load imbalance -- the expert-parallel max group sets
+    the layer time (reading Q5) -- and the balanced split moves layers."""
+    return float(a0 * (a1 / a0) ** (layer / max(1, L - 1)))
+
+
+def cfg4_routing_drift(layer: int, L: int = 32, T: int = 64 * 2048, E: int = 8, k: int = 2,
+                       dtype=np.int64, seed_key: int = 0) -> np.ndarray:
+    """Top-k ids [T, k] of layer `layer` under cfg4_alpha_drift (Gumbel-top-k,
+    distinct experts per token)."""
+    alpha = cfg4_alpha_drift(layer, L)
+    g = rng(4, 1000 + seed_key, layer)
+    pi = g.dirichlet(np.full(E, alpha))
+    pi = np.maximum(pi, 1e-12)
     gumb = -np.log(-np.log(g.random((T, E))))
     score = np.log(pi)[None, :] + gumb
     idx = np.argpartition(-score, k - 1, axis=1)[:, :k]

@@ -1158,10 +1158,16 @@ def test_profile_strided_bitmask_runs(D, L, ctx, T_bits):
     want[3] += oracle.count_bits(words[off:off + W], T_bits)
     plan = D.ProfilePlan(ctx, segs, 0, nl + 2)
     coef = D.coef_tensor(nl + 2, A=0, B=1, device=DEV)
+    cnt = torch.empty((nl + 2, 5), dtype=torch.int64, device=DEV)
+    tokl = np.arange(nl + 2) >= 40  # TOKMASK layers count tokens, the others nonzeros
     for rep in range(2):
-        cost, _, st = D.profile_layers(ctx, plan, coef)
+        cnt.fill_(-7)
+        cost, _, st = D.profile_layers(ctx, plan, coef, counters=cnt)
         torch.cuda.synchronize()
         assert int(st.item()) == 0
-        assert np.array_equal(cost.cpu().numpy(), want), rep
+        c = cnt.cpu().numpy()
+        got = np.where(tokl, c[:, 1], c[:, 0])
+        got[nl:] = c[nl:, 0]  # layers without a source: nnz = 0
+        assert np.array_equal(got, want), (rep, np.flatnonzero(got != want))
     if T_bits <= 8192:  # runs merged: several layers per tile
         assert plan.n_tiles < len(segs) // 2, plan.n_tiles
