@@ -72,6 +72,8 @@ def parse(argv=None):
                          "instead of the device-driven call inside the step's graph")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every call eagerly instead of replaying a CUDA graph")
+    ap.add_argument("--ref-budget", type=float, default=120.0,
+                    help="--impl reference: seconds of oracle work for the whole --warmup + --steps run")
     ap.add_argument("--cfg4-routing", choices=["drift", "aux", "sbase"], default="drift",
                     help="config 4 popularity: Dirichlet alpha drifting 64 -> 0.3 with depth (default), "
                          "alpha = 4 (aux-loss) or 64 (S-BASE) on every layer")
@@ -367,64 +369,112 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- oracle (CPU) arm
-def oracle_step(inp, layer_subset=None):
-    """The oracle as it stands: counts, costs, partition, diffusion, repack,
-    migration plan.  Returns (seconds counting, seconds solving)."""
+def oracle_solvers(wl, cost):
+    """Every solver of the step on the oracle (as it stands)."""
     import oracle
-    from paper_2505_14864_b200.pipeline import stage_ranks, uniform_split
-    L = inp.shape.L
+    b_old = uniform_split(wl.L, wl.n)
+    mem = wl.payload
+    st, b, B, imb = oracle.partition(cost, wl.n, mem=mem, cap=wl.cap)
+    oracle.diffuse(cost, b_old, 0, 256, mem=mem, cap=wl.cap)
+    oracle.diffuse_fluid(cost, b_old, wl.gamma_fluid, 256)
+    oracle.repack_bound(cost, wl.n, wl.bound, 1, mem=mem, cap=wl.cap)
+    r = stage_ranks(wl.n, 1)
+    oracle.moves(wl.L, b_old, r, b, r)
+    return b
+
+
+def oracle_step(wl, srcs, layer_subset=None):
+    """The oracle as it stands: counts, costs, every solver, the migration
+    plan.  Returns (seconds counting, seconds solving)."""
     t0 = time.perf_counter()
-    nnz = np.zeros(L, np.int64)
-    for layer, m in inp.masks:
-        if layer_subset is None or layer in layer_subset:
-            nnz[layer] += oracle.count_nz_u8(m)
+    cost = wl.oracle_cost(srcs, layer_subset)
     t1 = time.perf_counter()
-    cost = np.array([oracle.layer_cost(nnz=int(v), A=0, B=1)[1] for v in nnz], np.int64)
-    mem = inp.payload
-    st, b, B, imb = oracle.partition(cost, N_STAGES, mem=mem, cap=inp.cap)
-    uni = uniform_split(L, N_STAGES)
-    oracle.diffuse(cost, uni, 0, 256, mem=mem, cap=inp.cap)
-    oracle.diffuse_fluid(cost, uni, inp.gamma_fluid, 256)
-    oracle.repack_bound(cost, N_STAGES, inp.bound, 1, mem=mem, cap=inp.cap)
-    r = stage_ranks(N_STAGES, 1)
-    oracle.moves(L, uni, r, b, r)
+    oracle_solvers(wl, cost)
     t2 = time.perf_counter()
     return t1 - t0, t2 - t1
+
+
+def oracle_batch_step(insts):
+    """Config 5 on the oracle: token counts, costs, memory-capped partition
+    and BOUND repack of every instance.  Returns seconds."""
+    import oracle
+    t0 = time.perf_counter()
+    for x in insts:
+        tok = [oracle.count_bits(x.masks[l], x.masks.shape[1] * 32) for l in range(x.L)]
+        cost = np.array([oracle.layer_cost(tok=int(v), A=1)[1] for v in tok], np.int64)
+        oracle.partition(cost, x.n, mem=x.mem, cap=x.cap)
+        oracle.repack_bound(cost, x.n, x.bound, 1, mem=x.mem, cap=x.cap)
+    return time.perf_counter() - t0
 
 
 def cpu_threads_used():
     return 1  # the oracle is single-threaded C
 
 
+def cpu_baseline(wl, args, srcs=None):
+    """The oracle timed on this host for about args.cpu_seconds (bounded
+    sample of the same workload, scaled to one whole step)."""
+    if wl.key == 5:
+        insts = wl.shard(0, 1)[:64]
+        ts = []
+        t_end = time.perf_counter() + args.cpu_seconds
+        while time.perf_counter() < t_end or not ts:
+            ts.append(oracle_batch_step(insts) * wl.N_INST / len(insts))
+        return {"value": round(1e3 * float(np.mean(ts)), 3), "unit": "ms", "cores": cpu_threads_used(),
+                "kind": "oracle", "sample": f"{len(ts)} passes over 64 of the 4096 instances (counts, costs, "
+                                            f"partition, repack), scaled x64 to the whole batch; 1 thread; "
+                                            f"host has {os.cpu_count()} cores"}
+    c_s, s_s = [], []
+    t_end = time.perf_counter() + args.cpu_seconds
+    while time.perf_counter() < t_end or len(c_s) < 2:
+        c, s_ = oracle_step(wl, srcs)
+        c_s.append(c)
+        s_s.append(s_)
+    ob = 1e3 * (np.mean(c_s) + np.mean(s_s))
+    return {"value": round(float(ob), 3), "unit": "ms", "cores": cpu_threads_used(), "kind": "oracle",
+            "sample": f"{len(c_s)} full config-{wl.key} oracle steps (all {wl.L} layers' sources, every solver), "
+                      f"1 thread; host has {os.cpu_count()} cores"}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    shape = synth.GPTShape()
-    inp = Inputs(0, shape.L)
-    L = shape.L
-    # size each step so that the whole --warmup + --steps run stays ~2 minutes
-    c_full, s_full = oracle_step(inp)
-    per_step_full = c_full + s_full
-    budget = 120.0
-    m = L
-    if (args.steps + args.warmup) * per_step_full > budget:
-        m = max(1, int(L * (budget / (args.steps + args.warmup) - s_full) / max(c_full, 1e-9)))
-        m = min(L, m)
+    wl = WORKLOADS[args.config](args)
+    budget = args.ref_budget  # seconds for the whole --warmup + --steps run
+    nsteps = args.steps + args.warmup
     times = []
-    for it in range(args.warmup + args.steps):
-        sub = set(((it * m) + k) % L for k in range(m))
-        c, s = oracle_step(inp, sub if m < L else None)
-        if it >= args.warmup:
-            times.append(c * (L / m) + s)
+    if wl.key == 5:
+        insts = wl.shard(0, 1)
+        t1 = oracle_batch_step(insts[:16]) / 16
+        m = int(max(1, min(len(insts), budget / nsteps / max(t1, 1e-9))))
+        for it in range(nsteps):
+            sub = [insts[(it * m + k) % len(insts)] for k in range(m)]
+            t = oracle_batch_step(sub) * len(insts) / m
+            if it >= args.warmup:
+                times.append(t)
+        sample = (f"each step: the oracle on {m} of the 4096 instances (rotating), scaled x{4096 / m:.1f} "
+                  "to the whole batch")
+    else:
+        srcs = list(wl.sources(0, wl.L))
+        L = wl.L
+        c_full, s_full = oracle_step(wl, srcs)
+        m = L
+        if nsteps * (c_full + s_full) > budget:
+            m = max(1, min(L, int(L * (budget / nsteps - s_full) / max(c_full, 1e-9))))
+        for it in range(nsteps):
+            sub = set(((it * m) + k) % L for k in range(m))
+            c, s_ = oracle_step(wl, srcs, sub if m < L else None)
+            if it >= args.warmup:
+                times.append(c * (L / m) + s_)
+        sample = (f"each step: oracle counts of {m} of {L} layers' sources (rotating; count time scaled by "
+                  f"{L}/{m}) + every solver on the full {L}-layer cost vector"
+                  if m < L else f"each step: the full config-{wl.key} oracle step (all {L} layers)")
     ms = 1e3 * float(np.mean(times))
-    sample = (f"each step: oracle counts of {m} of {L} layers' u8 masks (rotating; count time "
-              f"scaled by {L}/{m}) + every solver on the full 48-layer cost vector"
-              if m < L else "each step: the full config-2 oracle step (all 48 layers)")
     out = {"impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": "ms",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
-           "data": "synthetic", "config": workload_config(args.gpus),
+           "higher_is_better": False, "scaling": "weak" if wl.key == 5 else "strong", "vs_baseline": None,
+           "dtype": "int64", "data": "synthetic", "config": wl.config(args.gpus),
            "cpu_baseline": {"value": round(ms, 4), "unit": "ms", "cores": cpu_threads_used(),
                             "kind": "oracle", "sample": sample},
            "e2e": {"value": round(ms, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -433,46 +483,148 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU arm
-def run_dynmo(args):
+class StepTimer:
+    """One-graph steps: [device barrier (the step runs at the
+    training-iteration barrier) -> start event -> step -> end event], C graph
+    copies with their own events replayed back to back; the host reads the
+    events once per group.  The timed interval begins once EVERY rank's graph
+    is running, so a host hiccup on one rank delays only the untimed barrier."""
+
+    def __init__(self, ctx, dev, steps):
+        self.ctx, self.dev = ctx, dev
+        self.C = 4 if steps % 4 == 0 else (2 if steps % 2 == 0 else 1)
+        self.copies, self.ev = [], []
+
+    def capture(self, body):
+        import torch
+        for _ in range(self.C):
+            e0 = torch.cuda.Event(enable_timing=True, external=True)
+            e1 = torch.cuda.Event(enable_timing=True, external=True)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=torch.cuda.Stream(device=self.dev)):
+                self.ctx.barrier()
+                e0.record()
+                body()
+                e1.record()
+            self.copies.append(g)
+            self.ev.append((e0, e1))
+
+    def replay(self, k):
+        self.copies[k % len(self.copies)].replay()
+
+    def run(self, steps, flush, after_group=None):
+        out = []
+        for k in range(steps):
+            flush()  # L2 flush between steps (outside the timed interval)
+            self.replay(k)
+            if (k + 1) % self.C == 0:  # read this group's per-step device intervals
+                self.ev[-1][1].synchronize()
+                out += [a.elapsed_time(b) for a, b in self.ev]
+                if after_group:
+                    after_group()
+        return out
+
+
+def dist_setup(args):
     import torch
     import torch.distributed as dist
-
-    from paper_2505_14864_b200 import _lib as LB
-    from paper_2505_14864_b200 import dynmo as D
-    from paper_2505_14864_b200.pipeline import rank_layers, stage_ranks, uniform_split
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    G = world
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if G > 1:
+    if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+    return world, rank, local, dev
+
+
+def reduce_max(vals, dev, G, op="max"):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.MIN)
+    return t.tolist()
+
+
+def gather_list(v, dev, G):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device=dev)
+    if G == 1:
+        return [float(v)]
+    out = [torch.zeros_like(t) for _ in range(G)]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]
+
+
+def step_stats(step_ms):
+    med = float(np.median(step_ms))
+    return {"median": round(med, 5), "p95": round(float(np.percentile(step_ms, 95)), 5),
+            "max": round(float(step_ms.max()), 5), "n_over_2x_median": int((step_ms > 2 * med).sum()),
+            "outliers": [[int(k), round(float(step_ms[k]), 4)] for k in np.flatnonzero(step_ms > 2 * med)[:8]]}
+
+
+def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G):
+    peaks, peak_src = load_peaks()
+    achieved = plan_bytes / (prof_avg_ms * 1e-3) / 1e9 if prof_avg_ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_k_profile.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_launch_G%d" % G)
+        except Exception:
+            traffic = None
+    return {"kernel": "k_profile", "bound": "hbm", "achieved": round(achieved, 1),
+            "peak": peaks.get("hbm_gbs"), "peak_source": peak_src, "unit": "GB/s",
+            "frac": round(achieved / peaks.get("hbm_gbs", 1.0), 4), "traffic": traffic,
+            "bytes_per_launch": int(plan_bytes), "avg_launch_ms": round(prof_avg_ms, 5),
+            "per_rank_frac": [round(x / peaks.get("hbm_gbs", 1.0), 4) for x in per_rank_frac]}
+
+
+def make_segments(D, srcs, dev):
+    import torch
+    dts, segs = [], []
+    for kind, layer, a, ne, E in srcs:
+        arr = a.view(np.int32) if a.dtype == np.uint32 else a
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+        dts.append((t, arr))
+        segs.append(D.SegmentSpec(t, kind, layer, n_elem=ne, n_experts=E))
+    return dts, segs
+
+
+def run_pipeline(args, wl):
+    """Configs 2-4: the pipeline's rebalance step (stage s on GPU floor(s G / n))."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14864_b200 import dynmo as D
+
+    G, rank, local, dev = dist_setup(args)
     ctx = D.Context(local)
-    shape = synth.GPTShape()
-    L = shape.L
-    b_old = uniform_split(L, N_STAGES)
-    ranks = stage_ranks(N_STAGES, G)
+    L, n = wl.L, wl.n
+    b_old = uniform_split(L, n)
+    ranks = stage_ranks(n, G)
     begin, count = rank_layers(b_old, ranks, rank)
-    inp = Inputs(begin, count)
+    srcs = list(wl.sources(begin, count))
 
     # ---- device-resident inputs
-    dmask = [torch.from_numpy(m).to(dev) for _, m in inp.masks]
-    segs = [D.SegmentSpec(t, LB.SRC_MASK_U8, layer) for t, (layer, _) in zip(dmask, inp.masks)]
+    dsrc, segs = make_segments(D, srcs, dev)
     plan = D.ProfilePlan(ctx, segs, begin, count, n_total=L, exchange=args.exchange if G > 1 else False)
-    coef = D.coef_tensor(count, A=0, B=1, device=dev)
-    mem_local = torch.from_numpy(inp.payload[begin:begin + count].astype(np.int64)).to(dev)
+    coef = D.coef_tensor(count, device=dev, **wl.coef)
+    frozen = (torch.from_numpy(np.ascontiguousarray(wl.frozen[begin:begin + count])).to(dev)
+              if wl.frozen is not None else None)
+    mem_local = torch.from_numpy(wl.payload[begin:begin + count].astype(np.int64)).to(dev)
     cost = torch.empty(L, dtype=torch.int64, device=dev)
     mem = torch.empty(L, dtype=torch.int64, device=dev)
-    batch = D.Batch([L], [N_STAGES], device=dev)
-    cap = torch.tensor([inp.cap], dtype=torch.int64, device=dev)
+    batch = D.Batch([L], [n], device=dev)
+    cap = torch.tensor([wl.cap], dtype=torch.int64, device=dev)
     bnd_in = torch.from_numpy(b_old).to(dev)
     gamma = torch.zeros(1, dtype=torch.int64, device=dev)
-    gamma_f = torch.tensor([inp.gamma_fluid], dtype=torch.float64, device=dev)
-    bound = torch.tensor([inp.bound], dtype=torch.int64, device=dev)
+    gamma_f = torch.tensor([wl.gamma_fluid], dtype=torch.float64, device=dev)
+    bound = torch.tensor([wl.bound], dtype=torch.int64, device=dev)
     floor = torch.ones(1, dtype=torch.int32, device=dev)
     # every int32 result the host needs lives in ONE device buffer (views), so
     # the step's single D2H boundary is one cudaMemcpyAsync
@@ -485,11 +637,10 @@ def run_dynmo(args):
     dif_out = {"status": res_d[nb + 2:nb + 3]}
     rep_out = {"status": res_d[nb + 3:nb + 4]}
     flush = L2Flush(dev)
-    stream = torch.cuda.current_stream()
 
-    # ---- migration buffers (CSR payload per layer; params + optimizer state)
-    send = {layer: [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
-            for layer in range(begin, begin + count)}
+    # ---- migration buffers (payload per layer; nothing migrates at G = 1)
+    send = ({layer: [torch.empty(int(wl.payload[layer]), dtype=torch.uint8, device=dev)]
+             for layer in range(begin, begin + count)} if G > 1 else {})
     recv = {}
 
     side = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
@@ -500,9 +651,10 @@ def run_dynmo(args):
     d_ranks = torch.from_numpy(ranks.astype(np.int32)).to(dev)
     d_bytes = torch.zeros(2, dtype=torch.int64, device=dev)
     use_map = bool(args.map_stages) and G > 1
-    d_slots = torch.arange(N_STAGES, dtype=torch.int32, device=dev)  # old stage s in slot s (on GPU ranks[s])
+    d_slots = torch.arange(n, dtype=torch.int32, device=dev)  # old stage s in slot s (on GPU ranks[s])
     d_rmap = d_ranks.clone()  # new stage -> GPU (identity placement unless --map-stages)
-    map_out = dict(kept=torch.zeros(1, dtype=torch.int64, device=dev), status=torch.zeros(1, dtype=torch.int32, device=dev))
+    map_out = dict(kept=torch.zeros(1, dtype=torch.int64, device=dev),
+                   status=torch.zeros(1, dtype=torch.int32, device=dev))
     # device-driven migration (G > 1, peer memory): the whole step is one graph
     # (also at G = 1, where nothing migrates: the step never waits on the host)
     dev_mig = (G == 1 or args.migrate == "p2p") and not args.host_migrate
@@ -512,41 +664,35 @@ def run_dynmo(args):
         """profile -> partition [-> device-driven migration] on the main branch,
         diffusion and repack on two side branches, joined at the end."""
         main = torch.cuda.current_stream()
-        D.profile_layers(ctx, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=pst)
+        with torch.cuda.nvtx.range("dynmo.profile"):
+            D.profile_layers(ctx, plan, coef, frozen=frozen, mem_local=mem_local, cost=cost, mem=mem, status=pst)
         for sd in side:
             sd.wait_stream(main)
-        with torch.cuda.stream(side[0]):
+        with torch.cuda.stream(side[0]), torch.cuda.nvtx.range("dynmo.diffuse"):
             D.diffuse_balance(ctx, batch, cost, bnd_in, mem=mem, cap=cap, gamma=gamma, gamma_fluid=gamma_f,
                               max_rounds=256, out=dif_out)
-        with torch.cuda.stream(side[1]):
+        with torch.cuda.stream(side[1]), torch.cuda.nvtx.range("dynmo.repack"):
             D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
-        D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
-                           imbalance=part["imb"], status=part["st"])
+        with torch.cuda.nvtx.range("dynmo.partition"):
+            D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
+                               imbalance=part["imb"], status=part["st"])
         if use_map:
-            D.map_stages(ctx, L, d_bold, d_slots, part["bnd"], mem, N_STAGES, slot_rank=d_ranks, rank_new=d_rmap,
+            D.map_stages(ctx, L, d_bold, d_slots, part["bnd"], mem, n, slot_rank=d_ranks, rank_new=d_rmap,
                          kept=map_out["kept"], status=map_out["status"])
         if dev_mig and pmig is not None:
-            pmig.device(d_bold, d_ranks, part["bnd"], d_rmap, d_bytes[0:1], d_bytes[1:2])
+            with torch.cuda.nvtx.range("dynmo.migrate"):
+                pmig.device(d_bold, d_ranks, part["bnd"], d_rmap, d_bytes[0:1], d_bytes[1:2])
         res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
         ev_res.record(main)
         for sd in side:
             main.wait_stream(sd)
 
-    graph = None
-    migrator = None
-
-    def solve():
-        if graph is not None:
-            graph.replay()
-        else:
-            solve_async()
-        ev_res.synchronize()  # result D2H (host-driven migration needs the boundaries)
-        return res_h.numpy()[:n_host].copy()
-
-    # first step: learn the new split, allocate the receive buffers
-    r0 = solve()
+    # first step (eager): learn the new split, allocate the receive buffers
+    solve_async()
+    ev_res.synchronize()
     torch.cuda.synchronize()
-    b_new = r0[:N_STAGES + 1].copy()
+    r0 = res_h.numpy()[:n_host].copy()
+    b_new = r0[:n + 1].copy()
     if r0[nb] != 0 or r0[nb + 1] != 0:
         raise SystemExit(f"rebalance failed: statuses {r0[nb:]}")
     rank_new = d_rmap.cpu().numpy() if use_map else ranks
@@ -554,63 +700,44 @@ def run_dynmo(args):
         raise SystemExit(f"map_stages failed: {int(map_out['status'].item())}")
     moves = D.migration_plan(L, b_old, ranks, b_new, rank_new)
     moves_mine = any(int(sr) == rank or int(ds) == rank for _, sr, ds in moves)
-    for layer, src, dst in moves:
-        if dst == rank:
-            recv[int(layer)] = [torch.empty(int(inp.payload[layer]), dtype=torch.uint8, device=dev)]
-    if G > 1 and args.migrate == "p2p":
-        pmig = migrator = D.PeerMigrator(ctx, L, send, recv)
-    else:
-        migrator = D.Migrator(ctx, L, send, recv)
+    if G > 1:
+        for layer, src, dst in moves:
+            if dst == rank:
+                recv[int(layer)] = [torch.empty(int(wl.payload[layer]), dtype=torch.uint8, device=dev)]
+        if args.migrate == "p2p":
+            pmig = migrator = D.PeerMigrator(ctx, L, send, recv)
+        else:
+            migrator = D.Migrator(ctx, L, send, recv)
 
-    copies = []  # extra captures of the one-graph step (their own timing events)
+    timer = StepTimer(ctx, dev, args.steps)
+    graph = None
 
     def step(k=0):
+        """One step; host-driven migration: D2H of the boundaries, then the call."""
         if dev_mig:
-            # one graph launch: no host round trip inside the step
-            if graph is not None:
-                (copies[k % len(copies)] if copies else graph).replay()
+            if timer.copies:
+                timer.replay(k)
             else:
                 solve_async()
             return None
-        r = solve()
+        if graph is not None:
+            graph.replay()
+        else:
+            solve_async()
+        ev_res.synchronize()
+        r = res_h.numpy()[:n_host].copy()
         main = torch.cuda.current_stream()
-        # the host has seen the partition, so the exchange is complete: the
-        # migration runs on its own stream, overlapping the side branches
-        with torch.cuda.stream(comm):
-            sr = migrator(b_old, ranks, r[:N_STAGES + 1], rank_new)
+        with torch.cuda.stream(comm):  # overlaps the side branches
+            sr = migrator(b_old, ranks, r[:n + 1], rank_new) if G > 1 else (0, 0)
         main.wait_stream(comm)
         return sr
 
-    ev_in = []  # (start, end) external events inside each one-graph step copy
     if args.graph:
-        # capture the step's device part (timing enabled so the phase events
-        # are baked into the graph as external event-record nodes)
+        # capture (phase events baked into the graph as external event-record nodes)
         ctx.set_timing(True, phases=None if args.phase_timing == "all" else
                        ([] if args.phase_timing == "none" else ["profile"]))
         if dev_mig:
-            # One-graph step: [device barrier (the step runs at the
-            # training-iteration barrier) -> start event -> step -> end event].
-            # The timed interval begins once EVERY rank's graph is running, so
-            # a host hiccup on one rank delays only the untimed barrier.  C
-            # copies (own events each) let the host enqueue C steps ahead and
-            # read the events once per group.
-            C = 4 if args.steps % 4 == 0 else (2 if args.steps % 2 == 0 else 1)
-
-            def capture_step():  # (a function: no stray reference to a graph survives)
-                e0 = torch.cuda.Event(enable_timing=True, external=True)
-                e1 = torch.cuda.Event(enable_timing=True, external=True)
-                g_ = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g_, stream=torch.cuda.Stream(device=dev)):
-                    ctx.barrier()
-                    e0.record()
-                    solve_async()
-                    e1.record()
-                copies.append(g_)
-                ev_in.append((e0, e1))
-
-            for _ in range(C):
-                capture_step()
-            graph = copies[0]
+            timer.capture(solve_async)
         else:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=torch.cuda.Stream(device=dev)):
@@ -618,9 +745,9 @@ def run_dynmo(args):
         torch.cuda.synchronize()
         ctx.timing_read()  # discard
         ctx.set_timing(False)
-        stream = torch.cuda.current_stream()
+    stream = torch.cuda.current_stream()
 
-    for w in range(max(args.warmup, 3, len(copies))):
+    for w in range(max(args.warmup, 3, len(timer.copies))):
         flush()
         step(w)
     torch.cuda.synchronize()
@@ -629,10 +756,7 @@ def run_dynmo(args):
     torch.cuda.synchronize()
     ctx.set_timing(True)
     ctx.timing_read()  # reset accumulators
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sent_recv = (0, 0)
     bar = torch.zeros(1, device=dev)
-    step_list = []
 
     def step_barrier():
         # rebalancing runs at the training iteration barrier: align the
@@ -640,29 +764,25 @@ def run_dynmo(args):
         if G > 1:
             dist.all_reduce(bar)
 
+    sent_recv = (0, 0)
     with ClockSampler(local) as clk:
         clk.start()
-        if ev_in:
-            C = len(copies)
-            for k in range(args.steps):
-                flush()  # L2 flush between steps (outside the timed interval)
-                step(k)
-                if (k + 1) % C == 0:  # read this group's per-step device intervals
-                    ev_in[-1][1].synchronize()
-                    step_list += [a.elapsed_time(b) for a, b in ev_in]
-                    ctx.timing_poll()
+        if timer.copies:
+            step_list = timer.run(args.steps, flush, ctx.timing_poll)
         else:
+            step_list = []
             for k in range(args.steps):
                 flush()
                 step_barrier()
-                ev[k][0].record(stream)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
                 sr = step(k)
                 if sr is not None:
                     sent_recv = sr
-                ev[k][1].record(stream)
-                ev[k][1].synchronize()  # outside the timed interval: fold the phase events
+                b.record(stream)
+                b.synchronize()  # outside the timed interval: fold the phase events
                 ctx.timing_poll()
-                step_list.append(ev[k][0].elapsed_time(ev[k][1]))
+                step_list.append(a.elapsed_time(b))
         torch.cuda.synchronize()
         clk.stop()
     if G > 1:
@@ -683,9 +803,9 @@ def run_dynmo(args):
     if dev_mig:
         sent_recv = tuple(int(v) for v in d_bytes.cpu().tolist())
 
-    # ---- e2e: host buffers, H2D of this step's masks + D2H of the result inside
-    pinned = [torch.from_numpy(m).pin_memory() for _, m in inp.masks]
-    h2d = int(sum(p.numel() for p in pinned))
+    # ---- e2e: host buffers, H2D of this step's sources + D2H of the result inside
+    pinned = [torch.from_numpy(np.ascontiguousarray(arr)).pin_memory() for _, arr in dsrc]
+    h2d = int(sum(p.numel() * p.element_size() for p in pinned))
     d2h = int(res_h.numel() * 4)
     e2e = []
     for k in range(args.e2e_steps):
@@ -693,7 +813,7 @@ def run_dynmo(args):
         step_barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for t, p in zip(dmask, pinned):
+        for (t, _), p in zip(dsrc, pinned):
             t.copy_(p, non_blocking=True)
         step()
         if dev_mig:
@@ -725,67 +845,46 @@ def run_dynmo(args):
         diag = ctx.timing_read()
         ctx.set_timing(False)
         diag_phases = {k: round(v[0] / max(v[1], 1), 5) if v[1] else 0.0 for k, v in diag.items()}
-
+        del gdiag
     if diag_phases and diag_phases.get("migrate"):
         mig_ms = diag_phases["migrate"]
 
     # ---- reductions over ranks (max of device time)
-    vals = torch.tensor([total_ms, prof_avg, e2e_ms, mig_ms, float(sent_recv[0]), float(sent_recv[1])],
-                        dtype=torch.float64, device=dev)
     achieved_local = plan.bytes / (prof_avg * 1e-3) / 1e9 if prof_avg > 0 else 0.0
-    ach = torch.tensor([achieved_local], dtype=torch.float64, device=dev)
-    if G > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ach, op=dist.ReduceOp.MIN)
-    total_ms, prof_avg_max, e2e_ms, mig_ms, max_sent, max_recv = vals.tolist()
-    achieved = float(ach.item())
-    # per-step job time = max over ranks of each step's device interval (the
-    # step ends when the slowest rank does); value stays max over ranks of
-    # the total (the contract), the step statistics use this array
+    total_ms, prof_avg_max, e2e_ms, mig_ms, max_sent, max_recv = reduce_max(
+        [total_ms, prof_avg, e2e_ms, mig_ms, float(sent_recv[0]), float(sent_recv[1])], dev, G)
+    per_rank_gbs = gather_list(achieved_local, dev, G)
+    prof_at_min = gather_list(prof_avg, dev, G)
+    bytes_all = gather_list(plan.bytes, dev, G)
+    # per-step job time = max over ranks of each step's device interval
     st_t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
     if G > 1:
         dist.all_reduce(st_t, op=dist.ReduceOp.MAX)
     step_ms = st_t.cpu().numpy()
 
     if rank == 0:
-        peaks, peak_src = load_peaks()
         ms = total_ms / args.steps
-        cfg = workload_config(G)
-        cfg["exchange"] = ("peer-memory" if args.exchange == "p2p" else "nccl-allgather") if G > 1 else "none (G=1)"
-        cfg["migration"] = ("none (G=1)" if G == 1 else "device-driven peer-memory pull, in the step graph"
-                            if dev_mig else "host-driven peer-memory pull" if args.migrate == "p2p"
-                            else "host-driven NCCL send/recv")
-        cfg["graph"] = bool(args.graph)
-        cfg["stage_placement"] = ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
-                                  else "stage s on GPU floor(s*G/8) before and after")
+        worst = int(np.argmin(per_rank_gbs))  # the roofline line reports the slowest rank's kernel
         cost_h = cost.cpu().numpy()
         x_old = np.add.reduceat(cost_h, b_old[:-1])
         x_new = np.add.reduceat(cost_h, b_new[:-1])
         dl = lambda x: float((x.max() - x.min()) / (x.sum() / len(x)))
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic_k_profile.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get("dram_bytes_per_launch_G%d" % G)
-            except Exception:
-                traffic = None
         out = {
             "metric": METRIC, "value": round(ms, 5), "unit": "ms", "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": cfg,
-            "roofline": {"kernel": "k_profile", "bound": "hbm", "achieved": round(achieved, 1),
-                         "peak": peaks.get("hbm_gbs"), "peak_source": peak_src, "unit": "GB/s",
-                         "frac": round(achieved / peaks.get("hbm_gbs", 1.0), 4),
-                         "traffic": traffic, "bytes_per_launch": int(plan.bytes),
-                         "avg_launch_ms": round(prof_avg, 5)},
+            "config": wl.config(G),
+            "setup": {
+                "exchange": ("peer-memory" if args.exchange == "p2p" else "nccl-allgather") if G > 1 else "none (G=1)",
+                "migration": ("none (G=1)" if G == 1 else "device-driven peer-memory pull, in the step graph"
+                              if dev_mig else "host-driven peer-memory pull" if args.migrate == "p2p"
+                              else "host-driven NCCL send/recv"),
+                "graph": bool(args.graph),
+                "stage_placement": ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
+                                    else f"stage s on GPU floor(s*G/{n}) before and after")},
+            "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G),
             "phases_ms_per_launch_diagnostic": diag_phases,
-            "step_ms": {"median": round(float(np.median(step_ms)), 5),
-                        "p95": round(float(np.percentile(step_ms, 95)), 5),
-                        "max": round(float(step_ms.max()), 5),
-                        "n_over_2x_median": int((step_ms > 2 * np.median(step_ms)).sum()),
-                        "outliers": [[int(k), round(float(step_ms[k]), 4)]
-                                     for k in np.flatnonzero(step_ms > 2 * np.median(step_ms))[:8]]},
+            "step_ms": step_stats(step_ms),
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
                         "max_bytes_recv_per_gpu": int(max_recv), "avg_ms": round(mig_ms, 5),
                         "nvlink_GBps": round(max(max_sent, max_recv) / (mig_ms * 1e-3) / 1e9, 1)
@@ -807,23 +906,13 @@ def run_dynmo(args):
             "clocks": clk.summary(),
         }
         if G == 1 and not args.no_cpu_baseline:
-            c_s, s_s = [], []
-            t_end = time.perf_counter() + args.cpu_seconds
-            while time.perf_counter() < t_end or len(c_s) < 2:
-                c, s = oracle_step(inp)
-                c_s.append(c)
-                s_s.append(s)
-            ob = 1e3 * (np.mean(c_s) + np.mean(s_s))
-            out["cpu_baseline"] = {"value": round(float(ob), 3), "unit": "ms", "cores": cpu_threads_used(),
-                                   "kind": "oracle",
-                                   "sample": f"{len(c_s)} full config-2 oracle steps (all 48 layers' u8 masks, "
-                                             f"every solver), 1 thread; host has {os.cpu_count()} cores"}
+            out["cpu_baseline"] = cpu_baseline(wl, args, srcs)
         print(json.dumps(out), flush=True)
     # teardown order: graphs holding NCCL work (the in-graph barrier) before
     # the communicator, then the peer-memory plans, then the ctx
     torch.cuda.synchronize()
-    copies.clear()
-    graph = gdiag = None  # noqa: F841
+    timer.copies.clear()
+    graph = None  # noqa: F841
     torch.cuda.synchronize()
     if pmig is not None:
         pmig.close()
@@ -833,6 +922,161 @@ def run_dynmo(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def run_batch(args, wl):
+    """Config 5: 4096 independent instances sharded 4096/G per GPU (weak
+    scaling per GPU: no exchange, no migration); one step = profile of the
+    MoD token masks -> memory-capped partition and BOUND repack of every
+    instance -> D2H of the per-instance results."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14864_b200 import _lib as LB
+    from paper_2505_14864_b200 import dynmo as D
+
+    G, rank, local, dev = dist_setup(args)
+    ctx = D.Context(local)
+    insts = wl.shard(rank, G)
+    words = np.concatenate([x.masks.reshape(-1) for x in insts]).view(np.int32)
+    dwords = torch.from_numpy(words).to(dev)
+    segs, off, nl = [], 0, 0
+    W = insts[0].masks.shape[1]
+    for x in insts:
+        for l in range(x.L):
+            segs.append(D.SegmentSpec(dwords[off:off + W], LB.SRC_TOKMASK_BITS, nl, n_elem=W * 32))
+            off += W
+            nl += 1
+    plan = D.ProfilePlan(ctx, segs, 0, nl)
+    coef = D.coef_tensor(nl, A=1, device=dev)
+    cost = torch.empty(nl, dtype=torch.int64, device=dev)
+    batch = D.Batch([x.L for x in insts], [x.n for x in insts], device=dev)
+    mem = torch.from_numpy(np.concatenate([x.mem for x in insts]).astype(np.int64)).to(dev)
+    cap = torch.from_numpy(np.array([x.cap for x in insts], np.int64)).to(dev)
+    bound = torch.from_numpy(np.array([x.bound for x in insts], np.int64)).to(dev)
+    floor = torch.ones(len(insts), dtype=torch.int32, device=dev)
+    q = len(insts)
+    # per-instance results the host reads: partition status, repack n_new and
+    # status, + the profile status (one D2H)
+    res_d = torch.empty(3 * q + 1, dtype=torch.int32, device=dev)
+    res_h = torch.empty(3 * q + 1, dtype=torch.int32, pin_memory=True)
+    part = dict(bnd=torch.empty(batch.total_bnd, dtype=torch.int32, device=dev),
+                bott=torch.empty(q, dtype=torch.int64, device=dev), st=res_d[:q])
+    rep_out = {"n_new": res_d[q:2 * q], "status": res_d[2 * q:3 * q]}
+    pst = res_d[3 * q:3 * q + 1]
+    flush = L2Flush(dev)
+    side = torch.cuda.Stream(device=dev)
+    ev_res = torch.cuda.Event(external=True)
+
+    def solve_async():
+        main = torch.cuda.current_stream()
+        with torch.cuda.nvtx.range("dynmo.profile"):
+            D.profile_layers(ctx, plan, coef, cost=cost, status=pst)
+        side.wait_stream(main)
+        with torch.cuda.stream(side), torch.cuda.nvtx.range("dynmo.repack"):
+            D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep_out)
+        with torch.cuda.nvtx.range("dynmo.partition"):
+            D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
+                               status=part["st"])
+        main.wait_stream(side)
+        res_h.copy_(res_d, non_blocking=True)
+        ev_res.record(main)
+
+    solve_async()
+    torch.cuda.synchronize()
+    r0 = res_h.numpy().copy()
+    if np.any(r0[:q] != 0) or np.any(r0[2 * q:3 * q] < 0) or r0[3 * q] != 0:
+        raise SystemExit("config 5 rebalance failed")
+    timer = StepTimer(ctx, dev, args.steps)
+    ctx.set_timing(True, phases=["profile"])
+    timer.capture(solve_async)
+    torch.cuda.synchronize()
+    ctx.timing_read()
+    ctx.set_timing(False)
+    for w in range(max(args.warmup, 3, timer.C)):
+        flush()
+        timer.replay(w)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    ctx.set_timing(True)
+    ctx.timing_read()
+    with ClockSampler(local) as clk:
+        clk.start()
+        step_list = timer.run(args.steps, flush, ctx.timing_poll)
+        torch.cuda.synchronize()
+        clk.stop()
+    if G > 1:
+        dist.barrier()
+    ctx.set_timing(False)
+    prof_ms, prof_n = ctx.timing_read()["profile"]
+    prof_avg = prof_ms / max(prof_n, 1)
+    step_ms = np.array(step_list)
+    total_ms = float(step_ms.sum())
+    # e2e: H2D of the rank's token masks from pinned memory + the result D2H
+    pinned = torch.from_numpy(words).pin_memory()
+    e2e = []
+    bar = torch.zeros(1, device=dev)
+    stream = torch.cuda.current_stream()
+    for k in range(args.e2e_steps):
+        flush()
+        if G > 1:
+            dist.all_reduce(bar)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dwords.copy_(pinned, non_blocking=True)
+        timer.replay(k)
+        ev_res.synchronize()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e.append(a.elapsed_time(b))
+    e2e_ms = float(np.mean(e2e))
+    achieved_local = plan.bytes / (prof_avg * 1e-3) / 1e9 if prof_avg > 0 else 0.0
+    total_ms, e2e_ms = reduce_max([total_ms, e2e_ms], dev, G)
+    per_rank_gbs = gather_list(achieved_local, dev, G)
+    prof_all = gather_list(prof_avg, dev, G)
+    bytes_all = gather_list(plan.bytes, dev, G)
+    n_new_sum = gather_list(float(r0[q:2 * q].sum()), dev, G)
+    n_cur_sum = gather_list(float(sum(x.n for x in insts)), dev, G)
+    st_t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(st_t, op=dist.ReduceOp.MAX)
+    step_ms = st_t.cpu().numpy()
+    if rank == 0:
+        ms = total_ms / args.steps
+        worst = int(np.argmin(per_rank_gbs))
+        out = {
+            "metric": METRIC, "value": round(ms, 5), "unit": "ms", "n_gpus": G, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": wl.config(G),
+            "setup": {"graph": True, "exchange": "none (independent instances)", "migration": "none"},
+            "instances_per_s": round(wl.N_INST / (ms * 1e-3), 1),
+            "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G),
+            "step_ms": step_stats(step_ms),
+            "solution": {"workers_before": int(sum(n_cur_sum)), "workers_after_repack": int(sum(n_new_sum))},
+            "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(words.nbytes),
+                    "d2h_bytes_per_step": int(res_h.numel() * 4), "steps": args.e2e_steps},
+            "gpu_launches": 4 * args.steps,  # k_profile, k_epilogue, k_partition, k_repack
+            "clocks": clk.summary(),
+        }
+        if G == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(wl, args)
+        print(json.dumps(out), flush=True)
+    torch.cuda.synchronize()
+    timer.copies.clear()
+    torch.cuda.synchronize()
+    plan.close()
+    ctx.close()
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_dynmo(args):
+    wl = WORKLOADS[args.config](args)
+    return run_batch(args, wl) if wl.key == 5 else run_pipeline(args, wl)
 
 
 def main():

@@ -1171,3 +1171,44 @@ def test_profile_strided_bitmask_runs(D, L, ctx, T_bits):
         assert np.array_equal(got, want), (rep, np.flatnonzero(got != want))
     if T_bits <= 8192:  # runs merged: several layers per tile
         assert plan.n_tiles < len(segs) // 2, plan.n_tiles
+
+
+def test_global_prune_reproduces_cfg2_masks(D, ctx):
+    """The config-2 masks are the exact global top-k of synth's bf16 weights
+    (by construction): the GPU's Alg. 1 (dynmo_global_prune) with k = the
+    masks' kept count reproduces every mask byte (GPT-12 at h = 256, 9.4 M
+    weights, several 32768-element tiles per tensor)."""
+    shape = synth.GPTShape(L=12, h=256)
+    p = synth.cfg2_keep_probs(shape, 0.9, 4)
+    pairs, masks = [], []
+    for layer in range(shape.L):
+        for t, m in enumerate(synth.cfg2_layer_masks_u8(shape, layer, p[layer], 4)):
+            w = synth.cfg2_topk_weights_bf16(m, layer, t).reshape(-1)
+            wt = _dev(w.view(np.int16)).view(torch.bfloat16)
+            pairs.append((wt, torch.zeros(w.size, dtype=torch.uint8, device=DEV)))
+            masks.append(m.reshape(-1))
+    k = int(sum(int(m.sum()) for m in masks))
+    pplan = D.PrunePlan(ctx, pairs)
+    info, st = D.global_prune(ctx, pplan, k)
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    for (_, mk), m in zip(pairs, masks):
+        assert np.array_equal(mk.cpu().numpy(), m)
+    pplan.close()
+
+
+@pytest.mark.parametrize("cfg", [3, 4, 5])
+def test_bench_configs_gpu_arm(cfg):
+    """bench.py --config 3/4/5 on one GPU: the GPU arm runs every step in
+    its graph and prints the contract's JSON line (roofline, e2e, clocks)."""
+    import json as js
+    import subprocess
+    import sys
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "bench.py", "--config", str(cfg), "--steps", "8", "--warmup", "3",
+                        "--e2e-steps", "2", "--no-cpu-baseline"], cwd=root, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = js.loads(r.stdout.strip().splitlines()[-1])
+    assert d["value"] > 0 and d["roofline"]["frac"] > 0 and d["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0

@@ -10,8 +10,8 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 
 torch.cuda.set_device(0)
-inp = bench.Inputs(0, 48)
-pinned = [torch.from_numpy(m).pin_memory() for _, m in inp.masks]
+srcs = list(bench.Cfg2().sources(0, 48))
+pinned = [torch.from_numpy(a).pin_memory() for _, _, a, _, _ in srcs]
 dev = [torch.empty_like(p, device="cuda") for p in pinned]
 total = sum(p.numel() for p in pinned)
 for S in (1, 2, 4, 8):

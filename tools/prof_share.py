@@ -14,9 +14,9 @@ from paper_2505_14864_b200 import dynmo as D  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 torch.cuda.set_device(0)
 ctx = D.Context(0)
-inp = bench.Inputs(0, n)
-dm = [torch.from_numpy(m).to("cuda") for _, m in inp.masks]
-plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, LB.SRC_MASK_U8, l) for t, (l, _) in zip(dm, inp.masks)], 0, n)
+srcs = list(bench.Cfg2().sources(0, n))
+dm = [torch.from_numpy(a).to("cuda") for _, _, a, _, _ in srcs]
+plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, LB.SRC_MASK_U8, l) for t, (_, l, _, _, _) in zip(dm, srcs)], 0, n)
 coef = D.coef_tensor(n, A=0, B=1, device="cuda")
 flush = bench.L2Flush("cuda")
 for _ in range(6):

@@ -29,10 +29,11 @@ def main():
     torch.cuda.set_device(0)
     ctx = D.Context(0)
     shape = synth.GPTShape()
-    L, n = shape.L, bench.N_STAGES
-    inp = bench.Inputs(0, L)
-    dmask = [torch.from_numpy(m).to(DEV) for _, m in inp.masks]
-    plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, LB.SRC_MASK_U8, l) for t, (l, _) in zip(dmask, inp.masks)], 0, L)
+    inp = bench.Cfg2()
+    L, n = shape.L, inp.n
+    srcs = list(inp.sources(0, L))
+    dmask = [torch.from_numpy(a).to(DEV) for _, _, a, _, _ in srcs]
+    plan = D.ProfilePlan(ctx, [D.SegmentSpec(t, LB.SRC_MASK_U8, l) for t, (_, l, _, _, _) in zip(dmask, srcs)], 0, L)
     coef = D.coef_tensor(L, A=0, B=1, device=DEV)
     mem_local = torch.from_numpy(inp.payload.astype(np.int64)).to(DEV)
     cost = torch.empty(L, dtype=torch.int64, device=DEV)
