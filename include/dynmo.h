@@ -431,6 +431,38 @@ dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan plan, int32_t n
  * setting, takes effect at the next call (and at graph capture).  INVALID if
  * max_ctas < 0. */
 dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
+/* Migration overlapped with the backward pass (NEXT-3; "by moving
+ * layers while the gradients calculation take place, from the last to the
+ * first layer"; P:L640, P:L672 per-iteration MoE / MoD rebalancing).  The
+ * payload tables are the plan's (params + gradients + optimizer state of a
+ * layer, any number of buffers per layer); the new split is a DEVICE array
+ * computed before the backward pass (profile -> partition after forward).
+ *   dynmo_migrate_bwd_begin: collective, once per iteration on every rank,
+ *     on the backward stream before its first layer_ready call: advances the
+ *     device-side epoch of this iteration's backward migration.
+ *   dynmo_migrate_layer_ready: on the stream that wrote layer `layer`'s
+ *     buffers (its gradients), after them: releases the layer's ready word
+ *     in this rank's peer window (a system-scope fence, then a release
+ *     store).  Ranks call it for the layers they own, last layer first as the
+ *     backward pass runs; it is a one-thread kernel, capturable.  INVALID if
+ *     layer is outside [0, n_layers).
+ *   dynmo_migrate_layers_bwd: on a side stream ordered after bwd_begin (an
+ *     event), every rank: receivers pull their incoming layers in DESCENDING
+ *     layer order, each as soon as its sender's ready word carries this
+ *     epoch (bounded wait, 10 s, over NVLink), then release done at their
+ *     senders; senders then wait for their receivers, so the stream may
+ *     reuse / free the sent buffers after this call.  Requires an SM budget
+ *     (dynmo_migrate_plan_set_ctas with 0 < max_ctas < SM count, else
+ *     INVALID): the pull spins on peers' flags and must leave SMs to this
+ *     rank's own backward pass.  Same device boundary / rank-map arguments
+ *     and error words as dynmo_migrate_layers_dev. */
+dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan plan, dynmo_stream stream);
+dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan plan, int32_t layer, dynmo_stream stream);
+dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
+                                      const int32_t *d_bnd_old, const int32_t *d_rank_old,
+                                      int32_t n_new, const int32_t *d_bnd_new,
+                                      const int32_t *d_rank_new, int64_t *d_bytes_sent,
+                                      int64_t *d_bytes_recv, dynmo_stream stream);
 /* Sticky device error of the peer-memory paths (0 = none); synchronous. */
 dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
 

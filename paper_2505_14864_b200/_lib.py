@@ -92,6 +92,9 @@ def lib():
         "dynmo_ctx_p2p_error": (i32, [p, p]),
         "dynmo_migrate_layers_dev": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
         "dynmo_migrate_plan_set_ctas": (i32, [p, i32]),
+        "dynmo_migrate_bwd_begin": (i32, [p, p, p]),
+        "dynmo_migrate_layer_ready": (i32, [p, p, i32, p]),
+        "dynmo_migrate_layers_bwd": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -111,4 +114,5 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_migrate_layers", "dynmo_migration_plan", "dynmo_migrate_plan_create",
             "dynmo_prune_plan_create", "dynmo_prune_plan_destroy", "dynmo_global_prune",
             "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",
-            "dynmo_migrate_layers_dev", "dynmo_migrate_plan_set_ctas"]
+            "dynmo_migrate_layers_dev", "dynmo_migrate_plan_set_ctas",
+            "dynmo_migrate_bwd_begin", "dynmo_migrate_layer_ready", "dynmo_migrate_layers_bwd"]

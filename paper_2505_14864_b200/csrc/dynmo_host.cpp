@@ -214,7 +214,8 @@ static dynmo_status setup_peer_window(dynmo_ctx c) {
     // peer window: flags every peer can write (CUDA IPC over NVLink)
     dynmo_status st = DYNMO_OK;
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
+        cudaMalloc((void **)&c->d_win, kPeerWindowBytes) != cudaSuccess ||
+        cudaMemset(c->d_win, 0, kPeerWindowBytes) != cudaSuccess)
         st = cuda_fail(cudaGetLastError(), "peer window");
     cudaIpcMemHandle_t h;
     if (!st && cudaIpcGetMemHandle(&h, c->d_win) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle");
@@ -241,7 +242,8 @@ static dynmo_status setup_peer_window(dynmo_ctx c) {
 // plan asks for the NCCL exchange (ensure_comm).
 static dynmo_status setup_single_window(dynmo_ctx c) {
     if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMalloc((void **)&c->d_win, 4096) != cudaSuccess || cudaMemset(c->d_win, 0, 4096) != cudaSuccess)
+        cudaMalloc((void **)&c->d_win, kPeerWindowBytes) != cudaSuccess ||
+        cudaMemset(c->d_win, 0, kPeerWindowBytes) != cudaSuccess)
         return cuda_fail(cudaGetLastError(), "peer window (single rank)");
     c->peer_win.assign(1, c->d_win);
     return DYNMO_OK;
@@ -1473,6 +1475,59 @@ dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
     const bool budget = mp->max_ctas > 0 && mp->max_ctas < ctx->num_sms;
     CUDA_TRY(launch_mig_dev(a, budget ? mp->max_ctas : ctx->num_sms, budget, s), "migration kernels launch");
+    phase_end(te, s);
+    return DYNMO_OK;
+}
+
+// ------------------------- NEXT-3: migration during the backward pass
+dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan mp, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_bwd_begin(ctx->d_win, (cudaStream_t)stream), "k_bwd_begin launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan mp, int32_t layer, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (layer < 0 || layer >= mp->n_layers || layer >= 1024) return invalid("layer outside [0, n_layers)");
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(launch_layer_ready(ctx->d_win, layer, (cudaStream_t)stream), "k_layer_ready launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_t *d_bnd_old,
+                                      const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                                      const int32_t *d_rank_new, int64_t *d_bytes_sent, int64_t *d_bytes_recv,
+                                      dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (!d_bnd_old || !d_rank_old || !d_bnd_new || !d_rank_new) return invalid("null boundary/rank array");
+    if (n_old < 1 || n_new < 1 || n_old > mp->n_layers || n_new > mp->n_layers) return invalid("bad stage count");
+    if (mp->n_layers > 1023) return invalid("n_layers > 1023");
+    DevMigArgs a{};
+    a.n_layers = mp->n_layers;
+    a.n_bufs = mp->n_bufs;
+    a.me = ctx->rank;
+    a.nranks = ctx->nranks;
+    a.n_old = n_old;
+    a.n_new = n_new;
+    a.bnd_old = d_bnd_old;
+    a.rank_old = d_rank_old;
+    a.bnd_new = d_bnd_new;
+    a.rank_new = d_rank_new;
+    a.src_tab = mp->d_src_tab;
+    a.recv_tab = mp->d_recv_tab;
+    a.win = ctx->d_win;
+    for (int r = 0; r < ctx->nranks; ++r) a.peer_win[r] = ctx->peer_win[r];
+    a.bytes_sent = d_bytes_sent;
+    a.bytes_recv = d_bytes_recv;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    // the pull waits for peers' backward passes: it must leave SMs to this
+    // rank's own backward pass (whose ready words peers wait for)
+    if (!(mp->max_ctas > 0 && mp->max_ctas < ctx->num_sms))
+        return invalid("backward migration needs an SM budget (dynmo_migrate_plan_set_ctas, < SM count)");
+    cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
+    CUDA_TRY(launch_mig_bwd(a, mp->max_ctas, true, s), "backward migration launch");
     phase_end(te, s);
     return DYNMO_OK;
 }

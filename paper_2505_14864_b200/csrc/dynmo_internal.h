@@ -127,7 +127,7 @@ struct ProfArgs {
 // prefetch per tile at kernel entry (all of a warp's range at once), so the
 // HBM queues fill at once instead of one register batch per warp at a time
 // (small per-GPU shares are latency / ramp bound).
-constexpr int64_t kL2PrefetchMaxBytes = 96ll << 20;
+constexpr int64_t kL2PrefetchMaxBytes = 0;  // off: measured slower (profiles/r02_ab_env.jsonl), knob kept for A/B
 
 struct PeerWindow;
 constexpr int kMaxRanksEpi = 16;
@@ -292,7 +292,16 @@ struct PeerWindow {
     uint64_t mig_dev_epoch;
     unsigned int dpull_ctr;
     int32_t barrier;            // dynmo_ctx_barrier's all-reduce word (local use only)
+    // migration overlapped with the backward pass (NEXT-3): this
+    // rank's per-layer "gradients written" words (read by receivers over
+    // NVLink), its backward-migration epoch, done words written by receivers
+    uint64_t bwd_epoch;
+    uint64_t bwd_done[kMaxRanksEpi];
+    unsigned int bwd_ctr;
+    uint64_t layer_ready[1024];
 };
+constexpr size_t kPeerWindowBytes = 16384;  // the window allocation
+static_assert(sizeof(PeerWindow) <= kPeerWindowBytes, "peer window page");
 
 struct DevBuf {
     void *ptr;
@@ -312,6 +321,11 @@ struct DevMigArgs {
     int64_t *bytes_sent, *bytes_recv;  // nullable
 };
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
+// NEXT-3 backward-ordered variant: epoch advance, per-layer ready release,
+// the descending-order pull (+ done) and the sender-side wait
+cudaError_t launch_bwd_begin(PeerWindow *win, cudaStream_t s);
+cudaError_t launch_layer_ready(PeerWindow *win, int32_t layer, cudaStream_t s);
+cudaError_t launch_mig_bwd(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
 
 struct P2PItem {
     const void *src;

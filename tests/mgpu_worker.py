@@ -338,6 +338,51 @@ def main():
         if rank != world - 1:
             assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "empty rank")
     pplan.close()
+    # NEXT-3: migration overlapped with the backward pass, last
+    # layer first.  Payload per layer = [gradients, params]; the "backward"
+    # on the main stream computes (a GEMM stand-in), writes each owned
+    # layer's gradient buffer with this iteration's value right before its
+    # ready flag; receivers pull on a side stream under an SM budget.  A pull
+    # that ran ahead of a flag would copy the previous iteration's gradients.
+    def grad_val(l, it):
+        return (l * 7 + it + 1) & 0xFF
+    sendb = {l: [torch.zeros(int(payload[l]), dtype=torch.uint8, device=dev), pattern(l, int(payload[l]) // 2 + 1).to(dev)]
+             for l in range(begin, begin + count)}
+    recvb = {int(l): [torch.zeros(int(payload[l]), dtype=torch.uint8, device=dev),
+                      torch.zeros(int(payload[l]) // 2 + 1, dtype=torch.uint8, device=dev)]
+             for l, s_, d_ in moves if d_ == rank}
+    pmb = D.PeerMigrator(ctx, shape.L, sendb, recvb, n_bufs=2)
+    pmb.set_ctas(8)
+    side_b = torch.cuda.Stream(device=dev)
+    Ab = torch.randn(1024, 1024, device=dev, dtype=torch.bfloat16)
+    for it in range(4):
+        main = torch.cuda.current_stream()
+        pmb.bwd_begin()
+        side_b.wait_stream(main)
+        with torch.cuda.stream(side_b):
+            pmb.backward(d_bo, d_ro, bnd, d_rn, bs, br)
+        for l in range(begin + count - 1, begin - 1, -1):  # backward: last layer first
+            for _ in range(2):
+                Ab = (Ab @ Ab).clamp_(-1, 1)
+            sendb[l][0].fill_(grad_val(l, it))
+            pmb.layer_ready(l)
+        main.wait_stream(side_b)
+        torch.cuda.synchronize()
+        assert pmb.error() == 0, (rank, it, pmb.error())
+        assert (int(bs.item()), int(br.item())) == (
+            sum(int(payload[l]) + int(payload[l]) // 2 + 1 for l, s_, _ in moves if s_ == rank),
+            sum(int(payload[l]) + int(payload[l]) // 2 + 1 for l, _, d_ in moves if d_ == rank)), (rank, it, "bwd bytes")
+        for l, bufs in recvb.items():
+            assert bool((bufs[0] == grad_val(l, it)).all()), (rank, it, l, "bwd grads")
+            assert torch.equal(bufs[1].cpu(), pattern(l, int(payload[l]) // 2 + 1)), (rank, it, l, "bwd params")
+    pmb.set_ctas(0)
+    try:
+        pmb.backward(d_bo, d_ro, bnd, d_rn, bs, br)  # no SM budget: refused on the host
+        raised = False
+    except RuntimeError:
+        raised = True
+    assert raised
+    pmb.close()
     # the host-driven pull with a CHANGING set of ranks
     # that move data between calls (some ranks sit calls out).  Epochs are
     # per directed rank pair, so every call is exact whatever the history.
