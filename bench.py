@@ -567,14 +567,15 @@ def step_stats(step_ms):
             "outliers": [[int(k), round(float(step_ms[k]), 4)] for k in np.flatnonzero(step_ms > 2 * med)[:8]]}
 
 
-def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G):
+def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G, cfg):
     peaks, peak_src = load_peaks()
     achieved = plan_bytes / (prof_avg_ms * 1e-3) / 1e9 if prof_avg_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_k_profile.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_launch_G%d" % G)
+            # one ncu --set full capture per workload (single process: G=1 only)
+            traffic = json.load(open(tp)).get("cfg%d_dram_bytes_per_launch_G%d" % (cfg, G))
         except Exception:
             traffic = None
     return {"kernel": "k_profile", "bound": "hbm", "achieved": round(achieved, 1),
@@ -882,7 +883,7 @@ def run_pipeline(args, wl):
                 "graph": bool(args.graph),
                 "stage_placement": ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
                                     else f"stage s on GPU floor(s*G/{n}) before and after")},
-            "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G),
+            "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G, args.config),
             "phases_ms_per_launch_diagnostic": diag_phases,
             "step_ms": step_stats(step_ms),
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
@@ -1052,7 +1053,7 @@ def run_batch(args, wl):
             "config": wl.config(G),
             "setup": {"graph": True, "exchange": "none (independent instances)", "migration": "none"},
             "instances_per_s": round(wl.N_INST / (ms * 1e-3), 1),
-            "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G),
+            "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G, args.config),
             "step_ms": step_stats(step_ms),
             "solution": {"workers_before": int(sum(n_cur_sum)), "workers_after_repack": int(sum(n_new_sum))},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(words.nbytes),

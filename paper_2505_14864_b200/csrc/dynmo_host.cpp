@@ -217,6 +217,7 @@ static dynmo_status setup_peer_window(dynmo_ctx c) {
         cudaMalloc((void **)&c->d_win, kPeerWindowBytes) != cudaSuccess ||
         cudaMemset(c->d_win, 0, kPeerWindowBytes) != cudaSuccess)
         st = cuda_fail(cudaGetLastError(), "peer window");
+    if (!st && preload_p2p_kernels() != cudaSuccess) st = cuda_fail(cudaGetLastError(), "peer kernels preload");
     cudaIpcMemHandle_t h;
     if (!st && cudaIpcGetMemHandle(&h, c->d_win) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "cudaIpcGetMemHandle");
     std::vector<char> all;
@@ -245,6 +246,7 @@ static dynmo_status setup_single_window(dynmo_ctx c) {
         cudaMalloc((void **)&c->d_win, kPeerWindowBytes) != cudaSuccess ||
         cudaMemset(c->d_win, 0, kPeerWindowBytes) != cudaSuccess)
         return cuda_fail(cudaGetLastError(), "peer window (single rank)");
+    if (preload_p2p_kernels() != cudaSuccess) return cuda_fail(cudaGetLastError(), "peer kernels preload");
     c->peer_win.assign(1, c->d_win);
     return DYNMO_OK;
 }

@@ -326,6 +326,8 @@ cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStrea
 cudaError_t launch_bwd_begin(PeerWindow *win, cudaStream_t s);
 cudaError_t launch_layer_ready(PeerWindow *win, int32_t layer, cudaStream_t s);
 cudaError_t launch_mig_bwd(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
+// force-load every peer-path kernel (CUDA lazy loading; see k_p2p.cu)
+cudaError_t preload_p2p_kernels();
 
 struct P2PItem {
     const void *src;

@@ -441,6 +441,27 @@ cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStrea
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// CUDA lazy loading (the default module loading mode) loads a kernel at its
+// first launch, and that load may synchronise the context.  A kernel that
+// spins on a flag released by a LATER launch in another stream (the
+// backward-ordered pull waits on k_layer_ready; the pulls wait on the
+// signals) would then deadlock until its bounded wait times out: load every
+// peer-path kernel once when the window is created.
+cudaError_t preload_p2p_kernels() {
+    cudaFuncAttributes fa;
+    const void *ks[] = {(const void *)k_signal,           (const void *)k_wait,
+                        (const void *)k_pull,             (const void *)k_mig_signal,
+                        (const void *)k_mig_pull<4>,      (const void *)k_mig_pull<16>,
+                        (const void *)k_mig_wait,         (const void *)k_bwd_begin,
+                        (const void *)k_layer_ready,      (const void *)k_mig_bwd_pull<4>,
+                        (const void *)k_mig_bwd_pull<16>, (const void *)k_mig_bwd_wait};
+    for (const void *k : ks) {
+        const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_signal(const P2PSignal &s, cudaStream_t st) {
     if (s.n == 0) return cudaSuccess;
     k_signal<<<1, 32, 0, st>>>(s);
