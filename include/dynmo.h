@@ -455,7 +455,13 @@ dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
  *     (dynmo_migrate_plan_set_ctas with 0 < max_ctas < SM count, else
  *     INVALID): the pull spins on peers' flags and must leave SMs to this
  *     rank's own backward pass.  Same device boundary / rank-map arguments
- *     and error words as dynmo_migrate_layers_dev. */
+ *     and error words as dynmo_migrate_layers_dev.
+ *   Lazy loading: while the pull spins, the first launch of a kernel whose
+ *     module is not loaded yet may synchronise the CUDA context (the default
+ *     CUDA_MODULE_LOADING=LAZY), and the pull then times out (E_NCCL).  The
+ *     library loads its own kernels when the ctx is created; the caller's
+ *     backward kernels must have run once before (a warm-up iteration) or
+ *     the process must use CUDA_MODULE_LOADING=EAGER. */
 dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan plan, dynmo_stream stream);
 dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan plan, int32_t layer, dynmo_stream stream);
 dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,

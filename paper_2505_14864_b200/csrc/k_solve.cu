@@ -8,10 +8,12 @@
 // from max_layers.
 //
 //  k_partition  contiguous min-max partition:
-//               exact integer 33-ary search over the bottleneck B: each lane
-//               tests one candidate with its own greedy (binary-search jumps
-//               in the prefix sums, memory cap folded in), a ballot picks the
-//               sub-interval.  Canonical lexmax boundaries (reading Q7),
+//               exact integer (T+1)-ary search over the bottleneck B: each of
+//               the T threads (256 per instance in the latency mode, 32 in
+//               the batched mode) tests its own candidate with its own greedy
+//               stage count (a broadcast scan of the prefix sums, or binary
+//               lifting for long models; memory cap folded in), ballots pick
+//               the sub-interval.  Canonical lexmax boundaries (reading Q7),
 //               fp64 Delta L (eq:imbalance).
 //  k_diffuse    blockIdx.y = 0: discrete diffusion (P:L497, P:L518-549,
 //               reading Q10), lane = stage pair; blockIdx.y = 1: the fluid
@@ -49,6 +51,7 @@ struct Inst {
     int16_t *nxt;    // [L+1] jump table
     int L;
     int64_t cap, maxc;
+    bool mfit;  // every m_i <= cap (MEM)
 };
 
 __host__ __device__ __forceinline__ size_t base_bytes(int Lmax, bool mem) {
@@ -82,6 +85,7 @@ __device__ Inst carve(char *sm, int Lmax, bool mem) {
     s.L = 0;
     s.cap = 0;
     s.maxc = 0;
+    s.mfit = true;
     return s;
 }
 
@@ -132,15 +136,21 @@ __device__ PrefixFlags load_prefix(Inst &s, const int64_t *cost, const int64_t *
     PrefixFlags f{false, false, false, false};
     int cneg = 0, mneg = 0;
     int64_t mx = 0;
+    int mbig = 0;
 #pragma unroll 1
     for (int i = lane; i < L; i += 32) {
         const int64_t c = cost[i];
         cneg |= c < 0;
         mx = c > mx ? c : mx;
-        if (mem) mneg |= mem[i] < 0;
+        if (mem) {
+            const int64_t m = mem[i];
+            mneg |= m < 0;
+            mbig |= m > s.cap;
+        }
     }
     f.cneg = __any_sync(FULL, cneg);
     f.mneg = __any_sync(FULL, mneg);
+    s.mfit = !__any_sync(FULL, mbig);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         const int64_t t = __shfl_xor_sync(FULL, mx, o);
@@ -191,183 +201,152 @@ __device__ __forceinline__ int warp_jump(const Inst &s, int j, int64_t t1, int64
     }
 }
 
-// Greedy maximal-prefix stage count under B (warp-uniform), stopping once it
-// exceeds `limit` (limit + 1 also for an unplaceable layer).
+// ------------------------------------------- one candidate per thread
+// The feasibility test of the search runs on every THREAD with its own
+// candidate B (instead of one warp per candidate), so a CTA of 256 threads
+// tests 256 candidates per round and a one-warp instance 32.  Two exact
+// greedy counts (maximal prefix stages, reading Q8/Q9), chosen per instance:
+//  scan_count   one pass over the layers: the shared loads of P[i] (and
+//               M[i]) are the same address for every lane (broadcast, no bank
+//               conflict) and independent of the data, so they pipeline; the
+//               dependent chain per layer is a compare and a select.
+//  jump_count   per stage, binary lifting over P (log2 L dependent loads):
+//               cheaper when n log2(L) << L (long models, few stages).
+// Both assume every layer fits a stage alone (B >= max c, every m <= cap),
+// which the search establishes before the first round.  A count above
+// `limit` may be reported as any value > limit.
 template <bool MEM>
-__device__ int warp_greedy(const Inst &s, int64_t B, int limit, int lane) {
+__device__ __forceinline__ int scan_count(const Inst &s, int64_t B) {
+    int64_t t1 = B;       // P[start] + B with start = 0
+    int64_t t2 = s.cap;   // M[start] + cap
+    int c = 1;
+#pragma unroll 4
+    for (int i = 1; i <= s.L; ++i) {
+        // layer i-1 joins the open stage iff P[i] <= t1 (and M[i] <= t2);
+        // else it opens the next stage (it fits alone)
+        bool cut = s.P[i] > t1;
+        if constexpr (MEM) cut |= s.M[i] > t2;
+        const int64_t n1 = satadd(s.P[i - 1], B);
+        t1 = cut ? n1 : t1;
+        if constexpr (MEM) {
+            const int64_t n2 = satadd(s.M[i - 1], s.cap);
+            t2 = cut ? n2 : t2;
+        }
+        c += cut;
+    }
+    return c;
+}
+
+template <bool MEM>
+__device__ __forceinline__ int jump_count(const Inst &s, int64_t B, int limit) {
+    const int L = s.L;
+    const int top = 1 << (31 - __clz(L));
     int j = 0, c = 0;
-    while (j < s.L) {
-        if (c == limit) return limit + 1;
+    while (j < L && c <= limit) {
         const int64_t t1 = satadd(s.P[j], B);
         int64_t t2 = 0;
         if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
-        const int K = warp_jump<MEM>(s, j, t1, t2, lane);
-        if (K == j) return limit + 1;
-        j = K;
-        ++c;
-    }
-    return c;
-}
-
-// Per-lane jump table (L <= 32 Q - 1): lane owns positions j = lane + 32 r
-// and finds nx[r] = the largest K in [j, L] with P[K] <= P[j] + B (and
-// M[K] <= M[j] + cap) by binary lifting: K += step whenever K + step still
-// satisfies both (monotone) predicates, steps = powers of two <= L in
-// decreasing order.  The Q searches are independent and interleaved (ILP);
-// every lane runs the same ceil(log2(L+1)) steps.  K == j: layer j does not
-// fit.  Replaces n dependent window jumps (~335 cycles each) by one parallel
-// search (~log2 L shared loads) plus n register shuffles.
-template <bool MEM, int Q>
-__device__ __forceinline__ void lane_table(const Inst &s, int64_t B, int lane, int (&nx)[Q]) {
-    const int L = s.L;
-    DYNMO_DCHECK(L >= 1 && L <= 32 * Q - 1);
-    int64_t t1[Q], t2[Q];
-#pragma unroll
-    for (int r = 0; r < Q; ++r) {
-        const int j = lane + 32 * r;
-        nx[r] = j;
-        const int jj = j <= L ? j : L;
-        t1[r] = satadd(s.P[jj], B);
-        t2[r] = MEM ? satadd(s.M[jj], s.cap) : 0;
-    }
-    // branch-free: indices clamped to L, loads unconditional, so the Q
-    // searches interleave (their latencies overlap)
-    for (int step = 1 << (31 - __clz(L)); step > 0; step >>= 1) {
-#pragma unroll
-        for (int r = 0; r < Q; ++r) {
-            const int c = nx[r] + step;
-            const int cc = c <= L ? c : L;
-            bool ok = (c <= L) & (s.P[cc] <= t1[r]);
-            if constexpr (MEM) ok &= s.M[cc] <= t2[r];
-            nx[r] = ok ? c : nx[r];
+        int K = j;
+        for (int step = top; step > 0; step >>= 1) {
+            const int k2 = K + step;
+            if (k2 <= L) {
+                bool ok = s.P[k2] <= t1;
+                if constexpr (MEM) ok = ok && s.M[k2] <= t2;
+                K = ok ? k2 : K;
+            }
         }
-    }
-}
-
-// nx of position j (warp-uniform j < 32 Q): register j >> 5 of lane j & 31.
-template <int Q>
-__device__ __forceinline__ int table_at(const int (&nx)[Q], int j) {
-    int v = nx[0];
-#pragma unroll
-    for (int r = 1; r < Q; ++r)
-        if ((j >> 5) == r) v = nx[r];
-    return __shfl_sync(FULL, v, j & 31);
-}
-
-template <bool MEM, int Q>
-__device__ int table_greedy(const Inst &s, int64_t B, int limit, int lane) {
-    int nx[Q];
-    lane_table<MEM, Q>(s, B, lane, nx);
-    int j = 0, c = 0;
-    while (j < s.L) {
-        if (c == limit) return limit + 1;
-        const int K = table_at<Q>(nx, j);
-        if (K == j) return limit + 1;
-        j = K;
+        j = K;  // K > j: layer j fits alone
         ++c;
     }
-    return c;
+    return j < L ? limit + 1 : c;
 }
 
-// Greedy stage count (same contract as warp_greedy): a jump table of Q
-// registers per lane (L <= 32 Q - 1), or warp windows (Q == 0, any L).  Q is
-// chosen on the host from the batch's max_layers, so a kernel holds one path.
-template <bool MEM, int Q>
-__device__ __forceinline__ int greedy_count(const Inst &s, int64_t B, int limit, int lane) {
-    if constexpr (Q == 0) return warp_greedy<MEM>(s, B, limit, lane);
-    else return table_greedy<MEM, Q>(s, B, limit, lane);
+__device__ __forceinline__ bool use_jumps(int L, int n) {
+    return n * (32 - __clz(L)) * 4 < L;
 }
 
-// Candidate w of NW per round: lo + floor(d (w+1) / (NW+1)) in 64-bit
-// arithmetic (d = a (NW+1) + r); NW+1 is a compile-time constant.
+template <bool MEM>
+__device__ __forceinline__ int thread_count(const Inst &s, int64_t B, int limit, bool jumps) {
+    return jumps ? jump_count<MEM>(s, B, limit) : scan_count<MEM>(s, B);
+}
+
+// Candidate t of NC per round: lo + floor(d (t+1) / (NC+1)) in 64-bit
+// arithmetic (d = a (NC+1) + r); NC+1 is a compile-time constant (the
+// division is a multiply-high).  Candidates are nondecreasing in t, < hi.
 template <int NC1>
 __device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
     const uint64_t qa = d / (uint64_t)NC1, qr = d % (uint64_t)NC1;
     return lo + (int64_t)(qa * (uint64_t)(c + 1) + (qr * (uint64_t)(c + 1)) / (uint64_t)NC1);
 }
 
-// Exact min-max search over B in [lo, hi] (hi feasible): each of the NW
-// warps tests one candidate per round with the warp-cooperative greedy, an
-// (NW+1)-ary search.  Feasibility is monotone in B, so the feasible
-// candidates form a suffix: the first feasible one is the new hi and its
-// predecessor + 1 the new lo.  Called by all NW warps after s is built and
-// visible.  Returns B* (uniform), or -1 if no split satisfies the memory cap.
-template <bool MEM, int NW, int Q>
-__device__ int64_t search_bottleneck(const Inst &s, int n) {
-    __shared__ int s_f[2][NW];
-    __shared__ int s_pre[2];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+// Bracket of the search: lo = max(max c, ceil(C/n)) is a lower bound of B*,
+// hi = min(ceil(C/n) + max c, C) is feasible on cost (Appendix A); under a
+// memory cap hi may not be, then it widens to C.  Returns false if no split
+// satisfies the cap.  s.mfit: every m_i <= cap (needed by both counts).
+template <bool MEM>
+__device__ __forceinline__ bool bracket(const Inst &s, int n, int64_t &lo, int64_t &hi, bool jumps) {
     const int64_t C = s.P[s.L];
     const int64_t ceil_cn = C / n + (C % n != 0);
-    int64_t lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
-    int64_t hi = satadd(ceil_cn, s.maxc);  // Appendix A: always feasible on cost
+    lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
+    hi = satadd(ceil_cn, s.maxc);
     if (hi > C) hi = C;
     if (lo > hi) lo = hi;
     if constexpr (MEM) {
-        // the memory cap may make the cost bracket infeasible: widen to C
-        int fh, fc;
-        if constexpr (NW > 1) {
-            if (w < 2) {
-                const int f = greedy_count<MEM, Q>(s, w == 0 ? hi : C, n, lane) <= n;
-                if (lane == 0) s_pre[w] = f;
-            }
-            __syncthreads();
-            fh = s_pre[0];
-            fc = s_pre[1];
-        } else {
-            fh = greedy_count<MEM, Q>(s, hi, n, lane) <= n;
-            fc = fh ? 1 : greedy_count<MEM, Q>(s, C, n, lane) <= n;
-        }
-        if (!fh) {
-            if (!fc) return -1;
+        if (!s.mfit) return false;
+        if (thread_count<MEM>(s, hi, n, jumps) > n) {
+            if (thread_count<MEM>(s, C, n, jumps) > n) return false;
             hi = C;
         }
     }
+    return true;
+}
+
+// Exact min-max search over B in [lo, hi] (hi feasible): every thread of the
+// NW warps tests one candidate per round, a (32 NW + 1)-ary search.
+// Feasibility is monotone in B, so the feasible candidates form a suffix:
+// the first feasible one is the new hi and its predecessor + 1 the new lo.
+// Called by all threads after s is built and visible.  Returns B* (uniform),
+// or -1 if no split satisfies the memory cap.
+template <bool MEM, int NW>
+__device__ int64_t search_bottleneck(const Inst &s, int n) {
+    constexpr int NT = 32 * NW;
+    __shared__ unsigned s_f[2][NW];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
+    const bool jumps = use_jumps(s.L, n);
+    int64_t lo, hi;
+    if (!bracket<MEM>(s, n, lo, hi, jumps)) return -1;
     int par = 0;
     while (lo < hi) {
         const uint64_t d = (uint64_t)(hi - lo);
-        const int64_t cand = candidate<NW + 1>(lo, d, w);
-        const int f = greedy_count<MEM, Q>(s, cand, n, lane) <= n;
+        const int64_t cand = candidate<NT + 1>(lo, d, t);
+        const unsigned m = __ballot_sync(FULL, thread_count<MEM>(s, cand, n, jumps) <= n);
         int first;
         if constexpr (NW == 1) {
-            first = f ? 0 : 1;
+            first = m ? __ffs(m) - 1 : NT;
         } else {
-            if (lane == 0) s_f[par][w] = f;
+            if (lane == 0) s_f[par][w] = m;
             __syncthreads();
-            first = NW;
+            first = NT;
 #pragma unroll
-            for (int k = NW - 1; k >= 0; --k)
-                if (s_f[par][k]) first = k;
+            for (int k = NW - 1; k >= 0; --k) {
+                const unsigned mk = s_f[par][k];
+                if (mk) first = 32 * k + __ffs(mk) - 1;
+            }
             par ^= 1;  // double buffer: the next round writes the other half
         }
-        const int64_t nhi = first < NW ? candidate<NW + 1>(lo, d, first) : hi;
-        const int64_t nlo = first > 0 ? candidate<NW + 1>(lo, d, first - 1) + 1 : lo;
+        const int64_t nhi = first < NT ? candidate<NT + 1>(lo, d, first) : hi;
+        const int64_t nlo = first > 0 ? candidate<NT + 1>(lo, d, first - 1) + 1 : lo;
         hi = nhi;
         lo = nlo;
     }
+    (void)w;
     return hi;
 }
 
 // Lexmax boundaries for B* (Appendix A): b_{s+1} = min(next(b_s), L - (n-1-s))
 // with warp-cooperative jumps.  One warp; writes s.b[0..n].
-template <bool MEM, int Q>
-__device__ void table_construct(Inst &s, int64_t Bs, int n, int lane) {
-    int nx[Q];
-    lane_table<MEM, Q>(s, Bs, lane, nx);
-    int j = 0;
-    if (lane == 0) s.b[0] = 0;
-    for (int st = 0; st < n; ++st) {
-        const int K = table_at<Q>(nx, j);  // j < L here (the reserve keeps it so)
-        const int reserve = s.L - (n - 1 - st);
-        j = K < reserve ? K : reserve;
-        if (lane == 0) s.b[st + 1] = j;
-    }
-    __syncwarp();
-}
-
-template <bool MEM, int Q>
+template <bool MEM>
 __device__ void construct(Inst &s, int64_t Bs, int n, int lane) {
-    if constexpr (Q > 0) return table_construct<MEM, Q>(s, Bs, n, lane);
     int j = 0;
     if (lane == 0) s.b[0] = 0;
     for (int st = 0; st < n; ++st) {
@@ -397,7 +376,7 @@ __device__ double imbalance_of(const int64_t *P, const int32_t *b, int n) {
 }
 
 // ------------------------------------------------------------ partition
-template <bool MEM, int NW, int Q>
+template <bool MEM, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -418,14 +397,16 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
         if (st == DYNMO_OK)
             st = prefix_status(load_prefix(s, a.cost + off, MEM ? a.mem + off : nullptr, L, lane), MEM);
         if (lane == 0) s_st = st;
-        if (lane == 0) s.x[0] = s.maxc;  // share maxc with the other warps
+        if (lane == 0) s.x[0] = s.maxc;  // share maxc and mfit with the other warps
+        if (lane == 0) s.x[1] = s.mfit;
     }
     __syncthreads();
     int st = s_st;
     s.maxc = s.x[0];
+    s.mfit = s.x[1] != 0;
     int64_t Bs = -1;
     if (st == DYNMO_OK) {
-        Bs = search_bottleneck<MEM, NW, Q>(s, n);
+        Bs = search_bottleneck<MEM, NW>(s, n);
         if (Bs < 0) st = DYNMO_E_INFEASIBLE;
     }
     if (w != 0) return;
@@ -438,7 +419,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
         }
         return;
     }
-    construct<MEM, Q>(s, Bs, n, lane);
+    construct<MEM>(s, Bs, n, lane);
 #pragma unroll 1
     for (int k = lane; k <= n; k += 32) bnd[k] = s.b[k];
     if (lane == 0) {
@@ -449,7 +430,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
 }
 
 // -------------------------------------------------------------- repack
-template <bool MEM, int NW, int Q>
+template <bool MEM, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -488,8 +469,9 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         }
         int k = n_cur, code = DYNMO_OK;
         if (st == DYNMO_OK && !alg2) {
-            // fewest workers: greedy count at B = bound (cost and mem), reading Q15
-            const int g = greedy_count<MEM, Q>(s, bound, n_cur, lane);
+            // fewest workers: greedy count at B = bound (cost and mem), reading Q15;
+            // a layer above the bound or the cap alone: no count meets it
+            const int g = (bound >= s.maxc && (!MEM || s.mfit)) ? scan_count<MEM>(s, bound) : n_cur + 1;
             if (g <= n_cur) {
                 k = g > fl ? g : fl;
             } else {
@@ -502,11 +484,13 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
             s_k = k;
             s_code = code;
             s.x[0] = s.maxc;
+            s.x[1] = s.mfit;
         }
     }
     __syncthreads();
     const int st0 = s_st;
     s.maxc = s.x[0];
+    s.mfit = s.x[1] != 0;
     if (st0 != DYNMO_OK) {
         if (w != 0) return;
         for (int k = lane; k <= n_cur && n_cur >= 1; k += 32) bnd[k] = -1;
@@ -557,7 +541,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         return;
     }
     const int k = s_k;
-    const int64_t Bs = search_bottleneck<MEM, NW, Q>(s, k);
+    const int64_t Bs = search_bottleneck<MEM, NW>(s, k);
     if (w != 0) return;
     if (Bs < 0) {
         for (int t = lane; t <= n_cur; t += 32) bnd[t] = -1;
@@ -568,7 +552,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         }
         return;
     }
-    construct<MEM, Q>(s, Bs, k, lane);
+    construct<MEM>(s, Bs, k, lane);
     for (int t = lane; t <= n_cur; t += 32) bnd[t] = t <= k ? s.b[t] : -1;
     if (lane == 0) {
         a.n_new[q] = k;
@@ -897,49 +881,29 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
 // search.  Large batches: 1 warp per instance (binary search, one wave).
 static bool latency_mode(const SolveArgs &a) { return a.n_inst <= 4 * 148; }
 
-// Jump-table width for the batch: registers per lane (L <= 32 Q - 1), or 0
-// = warp windows.  Tables shorten the dependent chain of ONE instance (the
-// latency mode); in the throughput mode (thousands of one-warp CTAs) total
-// work and occupancy decide, and a table of Q >= 4 costs 4-8x the shared
-// loads of n window jumps and ~150 registers (config 5: 38 -> 163 us), so
-// there only Q <= 2 is used.
-static int table_q(int max_layers, bool latency) {
-    if (!latency && max_layers >= 64) return 0;
-    return max_layers < 32 ? 1 : max_layers < 64 ? 2 : max_layers < 128 ? 4 : max_layers < 256 ? 8 : 0;
-}
-
-template <template <bool, int, int> class K>
+template <template <bool, int> class K>
 static cudaError_t launch_solver(const SolveArgs &a, cudaStream_t s) {
     const size_t sm = solve_smem_bytes(a.max_layers, a.mem != nullptr, false);
     const bool lm = latency_mode(a), mem = a.mem != nullptr;
     const dim3 grid(a.n_inst), block(lm ? 256 : 32);
-    cudaError_t e = cudaSuccess;
-#define DYNMO_SOLVER_Q(M, NW)                                                   \
-    switch (table_q(a.max_layers, lm)) {                                        \
-        case 1: e = K<M, NW, 1>::launch(grid, block, sm, s, a); break;        \
-        case 2: e = K<M, NW, 2>::launch(grid, block, sm, s, a); break;        \
-        case 4: e = K<M, NW, 4>::launch(grid, block, sm, s, a); break;        \
-        case 8: e = K<M, NW, 8>::launch(grid, block, sm, s, a); break;        \
-        default: e = K<M, NW, 0>::launch(grid, block, sm, s, a); break;       \
-    }
-    if (mem && lm) { DYNMO_SOLVER_Q(true, 8) }
-    else if (mem) { DYNMO_SOLVER_Q(true, 1) }
-    else if (lm) { DYNMO_SOLVER_Q(false, 8) }
-    else { DYNMO_SOLVER_Q(false, 1) }
-#undef DYNMO_SOLVER_Q
+    cudaError_t e;
+    if (mem && lm) e = K<true, 8>::launch(grid, block, sm, s, a);
+    else if (mem) e = K<true, 1>::launch(grid, block, sm, s, a);
+    else if (lm) e = K<false, 8>::launch(grid, block, sm, s, a);
+    else e = K<false, 1>::launch(grid, block, sm, s, a);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <bool M, int NW, int Q>
+template <bool M, int NW>
 struct PartitionK {
     static cudaError_t launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
-        return launch_pdl(k_partition<M, NW, Q>, g, b, sm, s, a);
+        return launch_pdl(k_partition<M, NW>, g, b, sm, s, a);
     }
 };
-template <bool M, int NW, int Q>
+template <bool M, int NW>
 struct RepackK {
     static cudaError_t launch(dim3 g, dim3 b, size_t sm, cudaStream_t s, const SolveArgs &a) {
-        return launch_pdl(k_repack<M, NW, Q>, g, b, sm, s, a);
+        return launch_pdl(k_repack<M, NW>, g, b, sm, s, a);
     }
 };
 

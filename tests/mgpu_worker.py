@@ -355,6 +355,13 @@ def main():
     pmb.set_ctas(8)
     side_b = torch.cuda.Stream(device=dev)
     Ab = torch.randn(1024, 1024, device=dev, dtype=torch.bfloat16)
+    # warm-up of the backward stand-in without migration: every kernel that
+    # runs while the pull spins must already be loaded (CUDA lazy loading may
+    # synchronise the context on a first launch; see dynmo.h)
+    for l in range(begin + count - 1, begin - 1, -1):
+        Ab = (Ab @ Ab).clamp_(-1, 1)
+        sendb[l][0].fill_(grad_val(l, -1))
+    torch.cuda.synchronize()
     for it in range(4):
         main = torch.cuda.current_stream()
         pmb.bwd_begin()
