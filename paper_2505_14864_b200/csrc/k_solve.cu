@@ -211,25 +211,38 @@ __device__ __forceinline__ int warp_jump(const Inst &s, int j, int64_t t1, int64
 //               conflict) and independent of the data, so they pipeline; the
 //               dependent chain per layer is a compare and a select.
 //  jump_count   per stage, binary lifting over P (log2 L dependent loads):
-//               cheaper when n log2(L) << L (long models, few stages).
+//               fewer instructions when n log2(L) << L.
 // Both assume every layer fits a stage alone (B >= max c, every m <= cap),
 // which the search establishes before the first round.  A count above
 // `limit` may be reported as any value > limit.
-template <bool MEM>
-__device__ __forceinline__ int scan_count(const Inst &s, int64_t B) {
-    int64_t t1 = B;       // P[start] + B with start = 0
-    int64_t t2 = s.cap;   // M[start] + cap
+// Arithmetic: unsigned, no saturation needed.  Every P, B <= C <= INT64_MAX
+// and M, cap' <= M[L] <= INT64_MAX (cap' = min(cap, M[L]) decides the same
+// splits), so P + B and M + cap' fit in uint64_t.  When C and M[L] are below
+// 2^31 the same sums fit in uint32_t: half the registers and compare
+// instructions (the 32-bit copies of P and M live in Inst::x, unused by the
+// partition and the repack).
+template <typename T>
+struct View {
+    const T *P, *M;
+    T cap;
+    int L;
+};
+
+template <typename T, bool MEM>
+__device__ __forceinline__ int scan_count(const View<T> &v, T B) {
+    T t1 = B;       // P[start] + B with start = 0
+    T t2 = v.cap;   // M[start] + cap
     int c = 1;
 #pragma unroll 4
-    for (int i = 1; i <= s.L; ++i) {
+    for (int i = 1; i <= v.L; ++i) {
         // layer i-1 joins the open stage iff P[i] <= t1 (and M[i] <= t2);
         // else it opens the next stage (it fits alone)
-        bool cut = s.P[i] > t1;
-        if constexpr (MEM) cut |= s.M[i] > t2;
-        const int64_t n1 = satadd(s.P[i - 1], B);
+        bool cut = v.P[i] > t1;
+        if constexpr (MEM) cut |= v.M[i] > t2;
+        const T n1 = v.P[i - 1] + B;
         t1 = cut ? n1 : t1;
         if constexpr (MEM) {
-            const int64_t n2 = satadd(s.M[i - 1], s.cap);
+            const T n2 = v.M[i - 1] + v.cap;
             t2 = cut ? n2 : t2;
         }
         c += cut;
@@ -237,23 +250,22 @@ __device__ __forceinline__ int scan_count(const Inst &s, int64_t B) {
     return c;
 }
 
-template <bool MEM>
-__device__ __forceinline__ int jump_count(const Inst &s, int64_t B, int limit) {
-    const int L = s.L;
+template <typename T, bool MEM>
+__device__ __forceinline__ int jump_count(const View<T> &v, T B, int limit) {
+    const int L = v.L;
     const int top = 1 << (31 - __clz(L));
     int j = 0, c = 0;
     while (j < L && c <= limit) {
-        const int64_t t1 = satadd(s.P[j], B);
-        int64_t t2 = 0;
-        if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
+        const T t1 = v.P[j] + B;
+        T t2 = 0;
+        if constexpr (MEM) t2 = v.M[j] + v.cap;
         int K = j;
         for (int step = top; step > 0; step >>= 1) {
             const int k2 = K + step;
-            if (k2 <= L) {
-                bool ok = s.P[k2] <= t1;
-                if constexpr (MEM) ok = ok && s.M[k2] <= t2;
-                K = ok ? k2 : K;
-            }
+            const int kc = k2 <= L ? k2 : L;  // branch-free: clamped load
+            bool ok = (k2 <= L) & (v.P[kc] <= t1);
+            if constexpr (MEM) ok &= v.M[kc] <= t2;
+            K = ok ? k2 : K;
         }
         j = K;  // K > j: layer j fits alone
         ++c;
@@ -261,65 +273,43 @@ __device__ __forceinline__ int jump_count(const Inst &s, int64_t B, int limit) {
     return j < L ? limit + 1 : c;
 }
 
-__device__ __forceinline__ bool use_jumps(int L, int n) {
-    return n * (32 - __clz(L)) * 4 < L;
-}
-
-template <bool MEM>
-__device__ __forceinline__ int thread_count(const Inst &s, int64_t B, int limit, bool jumps) {
-    return jumps ? jump_count<MEM>(s, B, limit) : scan_count<MEM>(s, B);
+template <typename T, bool MEM>
+__device__ __forceinline__ int thread_count(const View<T> &v, int64_t B, int limit, bool jumps) {
+    return jumps ? jump_count<T, MEM>(v, (T)B, limit) : scan_count<T, MEM>(v, (T)B);
 }
 
 // Candidate t of NC per round: lo + floor(d (t+1) / (NC+1)) in 64-bit
 // arithmetic (d = a (NC+1) + r); NC+1 is a compile-time constant (the
-// division is a multiply-high).  Candidates are nondecreasing in t, < hi.
+// division is a multiply-high).  Candidates are nondecreasing in t, < lo + d.
 template <int NC1>
 __device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
     const uint64_t qa = d / (uint64_t)NC1, qr = d % (uint64_t)NC1;
     return lo + (int64_t)(qa * (uint64_t)(c + 1) + (qr * (uint64_t)(c + 1)) / (uint64_t)NC1);
 }
 
-// Bracket of the search: lo = max(max c, ceil(C/n)) is a lower bound of B*,
-// hi = min(ceil(C/n) + max c, C) is feasible on cost (Appendix A); under a
-// memory cap hi may not be, then it widens to C.  Returns false if no split
-// satisfies the cap.  s.mfit: every m_i <= cap (needed by both counts).
-template <bool MEM>
-__device__ __forceinline__ bool bracket(const Inst &s, int n, int64_t &lo, int64_t &hi, bool jumps) {
-    const int64_t C = s.P[s.L];
-    const int64_t ceil_cn = C / n + (C % n != 0);
-    lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
-    hi = satadd(ceil_cn, s.maxc);
-    if (hi > C) hi = C;
-    if (lo > hi) lo = hi;
-    if constexpr (MEM) {
-        if (!s.mfit) return false;
-        if (thread_count<MEM>(s, hi, n, jumps) > n) {
-            if (thread_count<MEM>(s, C, n, jumps) > n) return false;
-            hi = C;
-        }
-    }
-    return true;
-}
-
-// Exact min-max search over B in [lo, hi] (hi feasible): every thread of the
-// NW warps tests one candidate per round, a (32 NW + 1)-ary search.
-// Feasibility is monotone in B, so the feasible candidates form a suffix:
-// the first feasible one is the new hi and its predecessor + 1 the new lo.
-// Called by all threads after s is built and visible.  Returns B* (uniform),
-// or -1 if no split satisfies the memory cap.
-template <bool MEM, int NW>
-__device__ int64_t search_bottleneck(const Inst &s, int n) {
+// Exact min-max search (all threads of the NW warps, after s is built and
+// visible).  Bracket: lo = max(max c, ceil(C/n)) is a lower bound of B*,
+// hi = min(ceil(C/n) + max c, C) is feasible on cost (Appendix A).  Every
+// round each thread tests one candidate; feasibility is monotone in B, so
+// the feasible candidates form a suffix: the first feasible one is the new
+// hi and its predecessor + 1 the new lo, a (32 NW + 1)-ary search.  Under a
+// memory cap hi may be infeasible: the first round then tests NT - 2
+// candidates in [lo, hi), hi itself and C (no feasible candidate: no split
+// satisfies the cap).  Returns B* (uniform), or -1.
+template <typename T, bool MEM, int NW>
+__device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, int64_t hi, bool jumps) {
     constexpr int NT = 32 * NW;
     __shared__ unsigned s_f[2][NW];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
-    const bool jumps = use_jumps(s.L, n);
-    int64_t lo, hi;
-    if (!bracket<MEM>(s, n, lo, hi, jumps)) return -1;
+    const int64_t C = s.P[s.L];
+    bool probe = MEM;  // first round also tests hi and C
     int par = 0;
-    while (lo < hi) {
+    while (probe || lo < hi) {
         const uint64_t d = (uint64_t)(hi - lo);
-        const int64_t cand = candidate<NT + 1>(lo, d, t);
-        const unsigned m = __ballot_sync(FULL, thread_count<MEM>(s, cand, n, jumps) <= n);
+        int64_t cand;
+        if (probe) cand = t < NT - 2 ? candidate<NT - 1>(lo, d, t) : (t == NT - 2 ? hi : C);
+        else cand = candidate<NT + 1>(lo, d, t);
+        const unsigned m = __ballot_sync(FULL, thread_count<T, MEM>(v, cand, n, jumps) <= n);
         int first;
         if constexpr (NW == 1) {
             first = m ? __ffs(m) - 1 : NT;
@@ -334,6 +324,21 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
             }
             par ^= 1;  // double buffer: the next round writes the other half
         }
+        if (probe) {
+            probe = false;
+            if (first == NT) return -1;        // C infeasible
+            if (first == NT - 1) {             // only C: B* in (hi, C]
+                lo = hi + 1;
+                hi = C;
+            } else if (first == NT - 2) {      // hi: B* in (last candidate, hi]
+                lo = NT > 2 ? candidate<NT - 1>(lo, d, NT - 3) + 1 : lo;
+            } else {
+                const int64_t nhi = candidate<NT - 1>(lo, d, first);
+                lo = first > 0 ? candidate<NT - 1>(lo, d, first - 1) + 1 : lo;
+                hi = nhi;
+            }
+            continue;
+        }
         const int64_t nhi = first < NT ? candidate<NT + 1>(lo, d, first) : hi;
         const int64_t nlo = first > 0 ? candidate<NT + 1>(lo, d, first - 1) + 1 : lo;
         hi = nhi;
@@ -341,6 +346,63 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
     }
     (void)w;
     return hi;
+}
+
+// Per-instance choice of the count: latency mode (NW > 1, one instance per
+// CTA) minimises the dependent chain (scan ~12 L cycles, jumps ~35 n log2 L);
+// the batched mode (NW == 1, issue bound) minimises instructions (scan ~10 L,
+// jumps ~5 n log2 L).
+template <int NW>
+__device__ __forceinline__ bool use_jumps(int L, int n) {
+    const int lg = 32 - __clz(L);
+    return NW > 1 ? L > 3 * n * lg : 2 * L > n * lg;
+}
+
+// 32-bit copies of P and M into s.x (2 (L+1) words <= its 8 (L+1) bytes),
+// then the search.  Called by all threads; the copy is made by all threads
+// and fenced with a CTA barrier (NW > 1) or warp sync.
+template <bool MEM, int NW>
+__device__ int64_t search_bottleneck(const Inst &s, int n) {
+    const int L = s.L;
+    const int64_t C = s.P[L];
+    const int64_t MC = MEM ? s.M[L] : 0;
+    const int64_t cap = MEM ? (s.cap < MC ? s.cap : MC) : 0;
+    if (MEM && !s.mfit) return -1;
+    const int64_t ceil_cn = C / n + (C % n != 0);
+    int64_t lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
+    int64_t hi = satadd(ceil_cn, s.maxc);
+    if (hi > C) hi = C;
+    if (lo > hi) lo = hi;
+    if (!MEM && lo == hi) return hi;
+    const bool jumps = use_jumps<NW>(L, n);
+    if (C < (1ll << 31) && MC < (1ll << 31)) {
+        uint32_t *p32 = reinterpret_cast<uint32_t *>(s.x);
+        uint32_t *m32 = p32 + (L + 1);
+        for (int i = threadIdx.x; i <= L; i += blockDim.x) {
+            p32[i] = (uint32_t)s.P[i];
+            if constexpr (MEM) m32[i] = (uint32_t)s.M[i];
+        }
+        if constexpr (NW > 1) __syncthreads();
+        else __syncwarp();
+        const View<uint32_t> v{p32, m32, (uint32_t)cap, L};
+        return search_t<uint32_t, MEM, NW>(s, v, n, lo, hi, jumps);
+    }
+    const View<uint64_t> v{reinterpret_cast<const uint64_t *>(s.P), reinterpret_cast<const uint64_t *>(s.M),
+                           (uint64_t)cap, L};
+    return search_t<uint64_t, MEM, NW>(s, v, n, lo, hi, jumps);
+}
+
+// Greedy stage count at one B (repack's fewest workers; one warp, every
+// lane the same B): 64-bit scan, cap clamped as above.
+template <bool MEM>
+__device__ int count_at(const Inst &s, int64_t B) {
+    const int64_t MC = MEM ? s.M[s.L] : 0;
+    const int64_t cap = MEM ? (s.cap < MC ? s.cap : MC) : 0;
+    const int64_t C = s.P[s.L];
+    const View<uint64_t> v{reinterpret_cast<const uint64_t *>(s.P), reinterpret_cast<const uint64_t *>(s.M),
+                           (uint64_t)cap, s.L};
+    // B > C behaves as B = C (one stage holds everything)
+    return scan_count<uint64_t, MEM>(v, (uint64_t)(B < C ? B : C));
 }
 
 // Lexmax boundaries for B* (Appendix A): b_{s+1} = min(next(b_s), L - (n-1-s))
@@ -381,7 +443,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) char smem[];
-    __shared__ int s_st;
+    __shared__ int s_st, s_mfit;
+    __shared__ int64_t s_maxc;
     const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     Inst s = carve(smem, a.max_layers, MEM);
     const int off = a.layer_off[q];
@@ -396,14 +459,16 @@ __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
         if (L < 1 || L > a.max_layers || n < 1 || n > L || (MEM && cap < 0)) st = DYNMO_E_INVALID;
         if (st == DYNMO_OK)
             st = prefix_status(load_prefix(s, a.cost + off, MEM ? a.mem + off : nullptr, L, lane), MEM);
-        if (lane == 0) s_st = st;
-        if (lane == 0) s.x[0] = s.maxc;  // share maxc and mfit with the other warps
-        if (lane == 0) s.x[1] = s.mfit;
+        if (lane == 0) {  // share status, maxc and mfit with the other warps
+            s_st = st;
+            s_maxc = s.maxc;
+            s_mfit = s.mfit;
+        }
     }
     __syncthreads();
     int st = s_st;
-    s.maxc = s.x[0];
-    s.mfit = s.x[1] != 0;
+    s.maxc = s_maxc;
+    s.mfit = s_mfit != 0;
     int64_t Bs = -1;
     if (st == DYNMO_OK) {
         Bs = search_bottleneck<MEM, NW>(s, n);
@@ -435,7 +500,8 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) char smem[];
-    __shared__ int s_st, s_k, s_code;
+    __shared__ int s_st, s_k, s_code, s_mfit;
+    __shared__ int64_t s_maxc;
     const int q = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     Inst s = carve(smem, a.max_layers, MEM);
     const int off = a.layer_off[q];
@@ -471,7 +537,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         if (st == DYNMO_OK && !alg2) {
             // fewest workers: greedy count at B = bound (cost and mem), reading Q15;
             // a layer above the bound or the cap alone: no count meets it
-            const int g = (bound >= s.maxc && (!MEM || s.mfit)) ? scan_count<MEM>(s, bound) : n_cur + 1;
+            const int g = (bound >= s.maxc && (!MEM || s.mfit)) ? count_at<MEM>(s, bound) : n_cur + 1;
             if (g <= n_cur) {
                 k = g > fl ? g : fl;
             } else {
@@ -483,14 +549,14 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
             s_st = st;
             s_k = k;
             s_code = code;
-            s.x[0] = s.maxc;
-            s.x[1] = s.mfit;
+            s_maxc = s.maxc;
+            s_mfit = s.mfit;
         }
     }
     __syncthreads();
     const int st0 = s_st;
-    s.maxc = s.x[0];
-    s.mfit = s.x[1] != 0;
+    s.maxc = s_maxc;
+    s.mfit = s_mfit != 0;
     if (st0 != DYNMO_OK) {
         if (w != 0) return;
         for (int k = lane; k <= n_cur && n_cur >= 1; k += 32) bnd[k] = -1;
