@@ -437,38 +437,49 @@ dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
  * payload tables are the plan's (params + gradients + optimizer state of a
  * layer, any number of buffers per layer); the new split is a DEVICE array
  * computed before the backward pass (profile -> partition after forward).
- *   dynmo_migrate_bwd_begin: collective, once per iteration on every rank,
- *     on the backward stream before its first layer_ready call: advances the
- *     device-side epoch of this iteration's backward migration.
+ * No kernel spins: waits are stream memory operations (cuStreamWaitValue64,
+ * polled by the GPU front end), so no SM is held while a layer's gradients
+ * are still being computed.  Per iteration, on every rank, in host order:
+ *   dynmo_migrate_bwd_begin: collective, once per iteration, before the
+ *     other three calls: advances the iteration epoch (host side; nothing is
+ *     launched).  DYNMO_E_CUDA if the device lacks 64-bit stream memory
+ *     operations.
  *   dynmo_migrate_layer_ready: on the stream that wrote layer `layer`'s
- *     buffers (its gradients), after them: releases the layer's ready word
- *     in this rank's peer window (a system-scope fence, then a release
- *     store).  Ranks call it for the layers they own, last layer first as the
- *     backward pass runs; it is a one-thread kernel, capturable.  INVALID if
- *     layer is outside [0, n_layers).
- *   dynmo_migrate_layers_bwd: on a side stream ordered after bwd_begin (an
- *     event), every rank: receivers pull their incoming layers in DESCENDING
- *     layer order, each as soon as its sender's ready word carries this
- *     epoch (bounded wait, 10 s, over NVLink), then release done at their
- *     senders; senders then wait for their receivers, so the stream may
- *     reuse / free the sent buffers after this call.  Requires an SM budget
+ *     buffers (its gradients), after them: a one-thread kernel fences at
+ *     system scope and releases the layer's word in EVERY rank's peer window.
+ *     Every layer must be released by its owner (old stage's rank) once per
+ *     iteration, last layer first as the backward pass runs.  INVALID if
+ *     layer is outside [0, n_layers) or before bwd_begin.
+ *   dynmo_migrate_layers_bwd: on a side stream: for each layer in
+ *     DESCENDING order, a stream wait for its ready word, then a pull kernel
+ *     of max_ctas CTAs that copies the layer over NVLink iff it moves to this
+ *     rank (device boundaries / rank maps, as dynmo_migrate_layers_dev);
+ *     then releases this rank's done word in every window.  *d_bytes_recv
+ *     (nullable) = bytes pulled.  Requires an SM budget
  *     (dynmo_migrate_plan_set_ctas with 0 < max_ctas < SM count, else
- *     INVALID): the pull spins on peers' flags and must leave SMs to this
- *     rank's own backward pass.  Same device boundary / rank-map arguments
- *     and error words as dynmo_migrate_layers_dev.
- *   Lazy loading: while the pull spins, the first launch of a kernel whose
- *     module is not loaded yet may synchronise the CUDA context (the default
- *     CUDA_MODULE_LOADING=LAZY), and the pull then times out (E_NCCL).  The
- *     library loads its own kernels when the ctx is created; the caller's
- *     backward kernels must have run once before (a warm-up iteration) or
- *     the process must use CUDA_MODULE_LOADING=EAGER. */
+ *     INVALID): the pulls share the GPU with this rank's backward pass.
+ *   dynmo_migrate_bwd_end: on the stream that reuses / frees the sent
+ *     buffers (e.g. the backward stream after its last layer): stream waits
+ *     for every rank's done word; *d_bytes_sent (nullable) = bytes of this
+ *     rank's layers the others pulled.
+ * Errors: a malformed split or rank map, or mismatched buffer sizes, set the
+ * ctx's sticky error word (DYNMO_E_INVALID, dynmo_ctx_p2p_error) and move
+ * nothing; the handshake still completes.  The waits are unbounded (like a
+ * NCCL collective): a rank that skips a call blocks its peers' streams.
+ * Host epochs are baked into the stream operations, so these calls are
+ * issued eagerly each iteration (not replayed from a captured graph). */
 dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan plan, dynmo_stream stream);
 dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan plan, int32_t layer, dynmo_stream stream);
 dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
                                       const int32_t *d_bnd_old, const int32_t *d_rank_old,
                                       int32_t n_new, const int32_t *d_bnd_new,
-                                      const int32_t *d_rank_new, int64_t *d_bytes_sent,
-                                      int64_t *d_bytes_recv, dynmo_stream stream);
+                                      const int32_t *d_rank_new, int64_t *d_bytes_recv,
+                                      dynmo_stream stream);
+dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
+                                   const int32_t *d_bnd_old, const int32_t *d_rank_old,
+                                   int32_t n_new, const int32_t *d_bnd_new,
+                                   const int32_t *d_rank_new, int64_t *d_bytes_sent,
+                                   dynmo_stream stream);
 /* Sticky device error of the peer-memory paths (0 = none); synchronous. */
 dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
 

@@ -94,7 +94,8 @@ def lib():
         "dynmo_migrate_plan_set_ctas": (i32, [p, i32]),
         "dynmo_migrate_bwd_begin": (i32, [p, p, p]),
         "dynmo_migrate_layer_ready": (i32, [p, p, i32, p]),
-        "dynmo_migrate_layers_bwd": (i32, [p, p, i32, p, p, i32, p, p, p, p, p]),
+        "dynmo_migrate_layers_bwd": (i32, [p, p, i32, p, p, i32, p, p, p, p]),
+        "dynmo_migrate_bwd_end": (i32, [p, p, i32, p, p, i32, p, p, p, p]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -115,4 +116,5 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_prune_plan_create", "dynmo_prune_plan_destroy", "dynmo_global_prune",
             "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",
             "dynmo_migrate_layers_dev", "dynmo_migrate_plan_set_ctas",
-            "dynmo_migrate_bwd_begin", "dynmo_migrate_layer_ready", "dynmo_migrate_layers_bwd"]
+            "dynmo_migrate_bwd_begin", "dynmo_migrate_layer_ready", "dynmo_migrate_layers_bwd",
+            "dynmo_migrate_bwd_end"]

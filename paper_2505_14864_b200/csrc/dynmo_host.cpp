@@ -69,6 +69,8 @@ struct dynmo_ctx_s {
     // host-driven peer migration: epochs per directed rank pair (P2PSignal)
     uint64_t send_epoch[kMaxRanks] = {}, recv_epoch[kMaxRanks] = {};
     long long *d_map_work = nullptr;  // [1 << kMaxMapRanks] DP table of dynmo_map_stages
+    uint64_t bwd_epoch = 0;  // backward-overlapped migration: iterations begun (host epochs)
+    bool memops = false;     // 64-bit stream memory operations available
 };
 
 namespace dynmo {
@@ -207,6 +209,23 @@ dynmo_status dynmo_get_unique_id(uint8_t h_id_out[128]) {
     return DYNMO_OK;
 }
 
+// 64-bit stream memory operations (CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS
+// = 122) and the cuStreamWaitValue64 entry point: the backward-ordered
+// migration's waits.
+static bool memops_supported(int device) {
+    typedef int (*AttrFn)(int *, int, int);
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuDeviceGetAttribute", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+        return false;
+    int v = 0;
+    if (((AttrFn)f)(&v, 122, device) != 0 || !v) return false;
+    void *w = nullptr;
+    return cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q) == cudaSuccess &&
+           q == cudaDriverEntryPointSuccess && w;
+}
+
 // Peer window of a multi-rank ctx: a page of flags every peer can write,
 // CUDA-IPC mapped by every rank (handles all-gathered over the ctx comm).
 static dynmo_status setup_peer_window(dynmo_ctx c) {
@@ -282,6 +301,7 @@ dynmo_status dynmo_ctx_create(int32_t device, int32_t nranks, int32_t rank,
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
         c->num_sms = sms;
+    c->memops = memops_supported(device);
     if (cudaMalloc((void **)&c->d_map_work, sizeof(long long) << kMaxMapRanks) != cudaSuccess) {
         delete c;
         return cuda_fail(cudaGetLastError(), "ctx workspace");
@@ -319,6 +339,7 @@ dynmo_status dynmo_ctx_split(dynmo_ctx ctx, int32_t color, int32_t key, dynmo_ct
     auto *c = new dynmo_ctx_s();
     c->device = ctx->device;
     c->num_sms = ctx->num_sms;
+    c->memops = ctx->memops;
     if (cudaMalloc((void **)&c->d_map_work, sizeof(long long) << kMaxMapRanks) != cudaSuccess) {
         delete c;
         return cuda_fail(cudaGetLastError(), "ctx workspace");
@@ -1482,30 +1503,47 @@ dynmo_status dynmo_migrate_layers_dev(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
 }
 
 // ------------------------- NEXT-3: migration during the backward pass
-dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan mp, dynmo_stream stream) {
-    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
-    DeviceGuard g(ctx->device);
-    CUDA_TRY(launch_bwd_begin(ctx->d_win, (cudaStream_t)stream), "k_bwd_begin launch");
+namespace {
+// cuStreamWaitValue64 through the runtime's driver entry point (no -lcuda).
+typedef int (*WaitValue64Fn)(cudaStream_t, unsigned long long, unsigned long long, unsigned int);
+WaitValue64Fn wait_value64() {
+    static WaitValue64Fn fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return (WaitValue64Fn)f;
+    }();
+    return fn;
+}
+
+// Stream waits until *addr - value >= 0 as int64 (CU_STREAM_WAIT_VALUE_GEQ):
+// the GPU front end polls; no kernel, no SM.
+dynmo_status stream_wait_geq(dynmo_ctx ctx, cudaStream_t s, const uint64_t *addr, uint64_t value) {
+    if (!ctx->memops) return DYNMO_E_CUDA;
+    const int r = wait_value64()(s, (unsigned long long)(uintptr_t)addr, (unsigned long long)value, 0x0);
+    if (r != 0) {
+        g_err = "cuStreamWaitValue64 failed (CUresult " + std::to_string(r) + ")";
+        return DYNMO_E_CUDA;
+    }
     return DYNMO_OK;
 }
 
-dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan mp, int32_t layer, dynmo_stream stream) {
-    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
-    if (layer < 0 || layer >= mp->n_layers || layer >= 1024) return invalid("layer outside [0, n_layers)");
-    DeviceGuard g(ctx->device);
-    CUDA_TRY(launch_layer_ready(ctx->d_win, layer, (cudaStream_t)stream), "k_layer_ready launch");
-    return DYNMO_OK;
+BwdPeers bwd_peers(dynmo_ctx ctx) {
+    BwdPeers p{};
+    p.nranks = ctx->nranks;
+    for (int r = 0; r < ctx->nranks; ++r) p.win[r] = ctx->peer_win[r];
+    return p;
 }
 
-dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_t *d_bnd_old,
-                                      const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
-                                      const int32_t *d_rank_new, int64_t *d_bytes_sent, int64_t *d_bytes_recv,
-                                      dynmo_stream stream) {
-    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+dynmo_status bwd_args(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_t *d_bnd_old,
+                      const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                      const int32_t *d_rank_new, DevMigArgs &a) {
     if (!d_bnd_old || !d_rank_old || !d_bnd_new || !d_rank_new) return invalid("null boundary/rank array");
     if (n_old < 1 || n_new < 1 || n_old > mp->n_layers || n_new > mp->n_layers) return invalid("bad stage count");
-    if (mp->n_layers > 1023) return invalid("n_layers > 1023");
-    DevMigArgs a{};
+    if (mp->n_layers > 1024) return invalid("n_layers > 1024");
+    a = DevMigArgs{};
     a.n_layers = mp->n_layers;
     a.n_bufs = mp->n_bufs;
     a.me = ctx->rank;
@@ -1520,17 +1558,68 @@ dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     a.recv_tab = mp->d_recv_tab;
     a.win = ctx->d_win;
     for (int r = 0; r < ctx->nranks; ++r) a.peer_win[r] = ctx->peer_win[r];
-    a.bytes_sent = d_bytes_sent;
-    a.bytes_recv = d_bytes_recv;
+    return DYNMO_OK;
+}
+}  // namespace
+
+dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan mp, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (!ctx->memops) {
+        g_err = "backward migration: 64-bit stream memory operations unsupported on this device/driver";
+        return DYNMO_E_CUDA;
+    }
+    (void)stream;
+    ++ctx->bwd_epoch;  // host-side iteration epoch (every rank calls this once per iteration)
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_layer_ready(dynmo_ctx ctx, dynmo_mplan mp, int32_t layer, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (layer < 0 || layer >= mp->n_layers || layer >= 1024) return invalid("layer outside [0, n_layers)");
+    if (ctx->bwd_epoch == 0) return invalid("dynmo_migrate_layer_ready before dynmo_migrate_bwd_begin");
     DeviceGuard g(ctx->device);
-    cudaStream_t s = (cudaStream_t)stream;
-    // the pull waits for peers' backward passes: it must leave SMs to this
-    // rank's own backward pass (whose ready words peers wait for)
+    CUDA_TRY(launch_layer_ready(bwd_peers(ctx), layer, ctx->bwd_epoch, (cudaStream_t)stream), "k_layer_ready launch");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_t *d_bnd_old,
+                                      const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                                      const int32_t *d_rank_new, int64_t *d_bytes_recv, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (ctx->bwd_epoch == 0) return invalid("dynmo_migrate_layers_bwd before dynmo_migrate_bwd_begin");
+    DevMigArgs a;
+    if (dynmo_status st = bwd_args(ctx, mp, n_old, d_bnd_old, d_rank_old, n_new, d_bnd_new, d_rank_new, a)) return st;
+    a.bytes_recv = d_bytes_recv;
+    // the pulls share the GPU with this rank's own backward pass
     if (!(mp->max_ctas > 0 && mp->max_ctas < ctx->num_sms))
         return invalid("backward migration needs an SM budget (dynmo_migrate_plan_set_ctas, < SM count)");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint64_t ep = ctx->bwd_epoch;
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
-    CUDA_TRY(launch_mig_bwd(a, mp->max_ctas, true, s), "backward migration launch");
+    if (d_bytes_recv) CUDA_TRY(cudaMemsetAsync(d_bytes_recv, 0, sizeof(int64_t), s), "bytes_recv reset");
+    for (int i = mp->n_layers - 1; i >= 0; --i) {  // the backward order: last layer first
+        if (dynmo_status st = stream_wait_geq(ctx, s, &ctx->d_win->layer_ready[i], ep)) return st;
+        CUDA_TRY(launch_bwd_pull_layer(a, i, mp->max_ctas, s), "k_bwd_pull_layer launch");
+    }
+    CUDA_TRY(launch_bwd_done(bwd_peers(ctx), ctx->rank, ep, s), "k_bwd_done launch");
     phase_end(te, s);
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_t *d_bnd_old,
+                                   const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
+                                   const int32_t *d_rank_new, int64_t *d_bytes_sent, dynmo_stream stream) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (ctx->bwd_epoch == 0) return invalid("dynmo_migrate_bwd_end before dynmo_migrate_bwd_begin");
+    DevMigArgs a;
+    if (dynmo_status st = bwd_args(ctx, mp, n_old, d_bnd_old, d_rank_old, n_new, d_bnd_new, d_rank_new, a)) return st;
+    a.bytes_sent = d_bytes_sent;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int r = 0; r < ctx->nranks; ++r)
+        if (dynmo_status st = stream_wait_geq(ctx, s, &ctx->d_win->bwd_done[r], ctx->bwd_epoch)) return st;
+    if (d_bytes_sent) CUDA_TRY(launch_bwd_sent(a, s), "k_bwd_sent launch");
     return DYNMO_OK;
 }
 

@@ -292,12 +292,11 @@ struct PeerWindow {
     uint64_t mig_dev_epoch;
     unsigned int dpull_ctr;
     int32_t barrier;            // dynmo_ctx_barrier's all-reduce word (local use only)
-    // migration overlapped with the backward pass (NEXT-3): this
-    // rank's per-layer "gradients written" words (read by receivers over
-    // NVLink), its backward-migration epoch, done words written by receivers
-    uint64_t bwd_epoch;
+    // migration overlapped with the backward pass (NEXT-3): per-layer
+    // "payload final" words and per-rank "pulls done" words, written by the
+    // owners / receivers into EVERY rank's window, polled locally by stream
+    // memory operations (epochs from the host)
     uint64_t bwd_done[kMaxRanksEpi];
-    unsigned int bwd_ctr;
     uint64_t layer_ready[1024];
 };
 constexpr size_t kPeerWindowBytes = 16384;  // the window allocation
@@ -321,11 +320,16 @@ struct DevMigArgs {
     int64_t *bytes_sent, *bytes_recv;  // nullable
 };
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
-// NEXT-3 backward-ordered variant: epoch advance, per-layer ready release,
-// the descending-order pull (+ done) and the sender-side wait
-cudaError_t launch_bwd_begin(PeerWindow *win, cudaStream_t s);
-cudaError_t launch_layer_ready(PeerWindow *win, int32_t layer, cudaStream_t s);
-cudaError_t launch_mig_bwd(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
+// NEXT-3 backward-ordered variant: per-layer ready release into every
+// window, one pull kernel per layer, the done release, the bytes sent
+struct BwdPeers {
+    PeerWindow *win[kMaxRanksEpi];
+    int32_t nranks;
+};
+cudaError_t launch_layer_ready(const BwdPeers &p, int32_t layer, uint64_t epoch, cudaStream_t s);
+cudaError_t launch_bwd_done(const BwdPeers &p, int32_t me, uint64_t epoch, cudaStream_t s);
+cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, int grid, cudaStream_t s);
+cudaError_t launch_bwd_sent(const DevMigArgs &a, cudaStream_t s);
 // force-load every peer-path kernel (CUDA lazy loading; see k_p2p.cu)
 cudaError_t preload_p2p_kernels();
 

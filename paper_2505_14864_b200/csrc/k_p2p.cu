@@ -294,103 +294,91 @@ __global__ void k_mig_wait(DevMigArgs a) {
 
 // ------------------- NEXT-3: migration during the backward pass
 // "moving layers while the gradients calculation take place, from the last
-// to the first layer": the backward pass releases layer i's ready word once
-// its gradients (and so its whole payload) are final; receivers pull their
-// incoming layers in DESCENDING layer order, each as soon as its sender has
-// released it, on a side stream under the plan's SM budget.
-__global__ void k_bwd_begin(PeerWindow *win) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) win->bwd_epoch = win->bwd_epoch + 1;
-}
-
-__global__ void k_layer_ready(PeerWindow *win, int32_t layer) {
+// to the first layer".  No kernel waits on the GPU: the backward stream
+// releases layer i (k_layer_ready: its payload is final) into EVERY rank's
+// window; each rank's side stream waits for the layers in descending order
+// with stream memory operations (the GPU front end polls, no SM is held) and
+// runs one short pull kernel per layer under the SM budget, which copies the
+// layer only if it is incoming here (device boundaries / rank maps).  Then
+// the side stream releases done[me] everywhere, and the senders' streams wait
+// for every rank's done before reusing the sent buffers (dynmo_migrate_bwd_end).
+__global__ void k_layer_ready(BwdPeers p, int32_t layer, uint64_t epoch) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         // the stream's earlier kernels wrote the layer's buffers: make them
-        // visible at system scope, then release the word peers poll
+        // visible at system scope, then release the layer on every rank
         __threadfence_system();
-        st_release_sys(&win->layer_ready[layer], win->bwd_epoch);
+        for (int r = 0; r < p.nranks; ++r) st_release_sys(&p.win[r]->layer_ready[layer], epoch);
     }
 }
 
+__global__ void k_bwd_done(BwdPeers p, int32_t me, uint64_t epoch) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        __threadfence_system();
+        for (int r = 0; r < p.nranks; ++r) st_release_sys(&p.win[r]->bwd_done[me], epoch);
+    }
+}
+
+// One layer (i) of the backward-ordered pull: every CTA checks the split and
+// the owners of layer i; if it moves to this rank, the grid copies its
+// buffers with U x 16-byte NVLink loads in flight per thread.
 template <int U>
-__global__ void __launch_bounds__(kP2PThreads) k_mig_bwd_pull(DevMigArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ MigView v;
-    __shared__ int16_t in_layers[1024];
-    __shared__ int8_t in_src[1024];
+__global__ void __launch_bounds__(kP2PThreads) k_bwd_pull_layer(DevMigArgs a, int32_t i) {
     __shared__ int s_ok;
-    mig_view(a, v, in_layers, in_src);
-    const uint64_t epoch = a.win->bwd_epoch;
-    if (threadIdx.x == 0 && !v.ok) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+    if (threadIdx.x == 0)
+        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
+               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
+    __syncthreads();
     const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (!s_ok) {
+        if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+        return;
+    }
+    const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
+    const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
+    if (dst != a.me || src == a.me) return;
     const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
     unsigned long long recvd = 0;
-    // incoming layers, last layer first (the order the backward pass frees them)
-    for (int i = a.n_layers - 1; v.ok && i >= 0; --i) {
-        const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
-        const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
-        if (dst != a.me || src == a.me) continue;
-        if (threadIdx.x == 0) {
-            s_ok = wait_flag(&a.peer_win[src]->layer_ready[i], epoch);
-            if (!s_ok) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+    for (int k = 0; k < a.n_bufs; ++k) {
+        const int64_t idx = (int64_t)i * a.n_bufs + k;
+        const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
+        const DevBuf rb = a.recv_tab[idx];
+        if (sb.bytes != rb.bytes || (sb.bytes > 0 && (!sb.ptr || !rb.ptr))) {
+            if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+            continue;
         }
-        __syncthreads();
-        const int ok = s_ok;
-        __syncthreads();
-        if (!ok) break;
-        for (int k = 0; k < a.n_bufs; ++k) {
-            const int64_t idx = (int64_t)i * a.n_bufs + k;
-            const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
-            const DevBuf rb = a.recv_tab[idx];
-            if (sb.bytes != rb.bytes || (sb.bytes > 0 && (!sb.ptr || !rb.ptr))) {
-                if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
-                continue;
-            }
-            const uint64_t bytes = (uint64_t)sb.bytes;
-            recvd += bytes;
-            const uint8_t *sp = (const uint8_t *)sb.ptr;
-            uint8_t *dp = (uint8_t *)rb.ptr;
-            const bool vec = (((uintptr_t)sp | (uintptr_t)dp) & 15) == 0;
-            const uint64_t nvec = vec ? bytes >> 4 : 0;
-            const uint4 *s4 = (const uint4 *)sp;
-            uint4 *d4 = (uint4 *)dp;
-            uint64_t x = gt;
-            for (; x + (U - 1) * gs < nvec; x += U * gs) {
-                uint4 q[U];
+        const uint64_t bytes = (uint64_t)sb.bytes;
+        recvd += bytes;
+        const uint8_t *sp = (const uint8_t *)sb.ptr;
+        uint8_t *dp = (uint8_t *)rb.ptr;
+        const bool vec = (((uintptr_t)sp | (uintptr_t)dp) & 15) == 0;
+        const uint64_t nvec = vec ? bytes >> 4 : 0;
+        const uint4 *s4 = (const uint4 *)sp;
+        uint4 *d4 = (uint4 *)dp;
+        uint64_t x = gt;
+        for (; x + (U - 1) * gs < nvec; x += U * gs) {
+            uint4 q[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
+            for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
 #pragma unroll
-                for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
-            }
-            for (; x < nvec; x += gs) d4[x] = s4[x];
-            for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
+            for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
         }
+        for (; x < nvec; x += gs) d4[x] = s4[x];
+        for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
     }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (blockIdx.x == 0 && a.bytes_recv) *a.bytes_recv = (int64_t)recvd;
-        const unsigned prev = atomicAdd(&a.win->bwd_ctr, 1u);
-        if (prev == gridDim.x - 1) {
-            a.win->bwd_ctr = 0u;
-            __threadfence_system();
-            for (int r = 0; r < a.nranks; ++r)
-                if (v.senders & (1u << r)) st_release_sys(&a.peer_win[r]->bwd_done[a.me], epoch);
-        }
-    }
+    if (gt == 0 && a.bytes_recv && recvd) atomicAdd((unsigned long long *)a.bytes_recv, recvd);
 }
 
-// Sender side: bytes sent, then wait until every receiver has pulled.
-__global__ void k_mig_bwd_wait(DevMigArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    __shared__ MigView v;
-    __shared__ int16_t in_layers[1024];
-    __shared__ int8_t in_src[1024];
+// Sender side (at dynmo_migrate_bwd_end, after the done waits): bytes sent.
+__global__ void k_bwd_sent(DevMigArgs a) {
     __shared__ unsigned long long s_sent;
-    if (threadIdx.x == 0) s_sent = 0ull;
-    mig_view(a, v, in_layers, in_src);
-    if (v.ok)
+    __shared__ int s_ok;
+    if (threadIdx.x == 0) {
+        s_sent = 0ull;
+        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
+               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
+    }
+    __syncthreads();
+    if (s_ok)
         for (int i = threadIdx.x; i < a.n_layers; i += blockDim.x) {
             const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
             const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
@@ -402,34 +390,29 @@ __global__ void k_mig_bwd_wait(DevMigArgs a) {
             }
         }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (a.bytes_sent) *a.bytes_sent = (int64_t)s_sent;
-        if (v.ok) {
-            const uint64_t epoch = a.win->bwd_epoch;
-            for (int r = 0; r < a.nranks; ++r)
-                if (v.receivers & (1u << r))
-                    if (!wait_flag(&a.win->bwd_done[r], epoch)) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
-        }
-    }
+    if (threadIdx.x == 0 && a.bytes_sent) *a.bytes_sent = s_ok ? (int64_t)s_sent : 0;
 }
 
 }  // namespace
 
-cudaError_t launch_bwd_begin(PeerWindow *win, cudaStream_t s) {
-    k_bwd_begin<<<1, 32, 0, s>>>(win);
+cudaError_t launch_layer_ready(const BwdPeers &p, int32_t layer, uint64_t epoch, cudaStream_t s) {
+    k_layer_ready<<<1, 32, 0, s>>>(p, layer, epoch);
     return cudaGetLastError();
 }
 
-cudaError_t launch_layer_ready(PeerWindow *win, int32_t layer, cudaStream_t s) {
-    k_layer_ready<<<1, 32, 0, s>>>(win, layer);
+cudaError_t launch_bwd_done(const BwdPeers &p, int32_t me, uint64_t epoch, cudaStream_t s) {
+    k_bwd_done<<<1, 32, 0, s>>>(p, me, epoch);
     return cudaGetLastError();
 }
 
-cudaError_t launch_mig_bwd(const DevMigArgs &a, int grid, bool budget, cudaStream_t s) {
-    cudaError_t e = budget ? launch_pdl(k_mig_bwd_pull<16>, grid, kP2PThreads, 0, s, a)
-                           : launch_pdl(k_mig_bwd_pull<4>, grid, kP2PThreads, 0, s, a);
-    if (e == cudaSuccess) e = launch_pdl(k_mig_bwd_wait, 1, 256, 0, s, a);
-    return e != cudaSuccess ? e : cudaGetLastError();
+cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, int grid, cudaStream_t s) {
+    k_bwd_pull_layer<16><<<grid, kP2PThreads, 0, s>>>(a, layer);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_sent(const DevMigArgs &a, cudaStream_t s) {
+    k_bwd_sent<<<1, 256, 0, s>>>(a);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s) {
@@ -452,9 +435,9 @@ cudaError_t preload_p2p_kernels() {
     const void *ks[] = {(const void *)k_signal,           (const void *)k_wait,
                         (const void *)k_pull,             (const void *)k_mig_signal,
                         (const void *)k_mig_pull<4>,      (const void *)k_mig_pull<16>,
-                        (const void *)k_mig_wait,         (const void *)k_bwd_begin,
-                        (const void *)k_layer_ready,      (const void *)k_mig_bwd_pull<4>,
-                        (const void *)k_mig_bwd_pull<16>, (const void *)k_mig_bwd_wait};
+                        (const void *)k_mig_wait,         (const void *)k_layer_ready,
+                        (const void *)k_bwd_done,         (const void *)k_bwd_pull_layer<16>,
+                        (const void *)k_bwd_sent};
     for (const void *k : ks) {
         const cudaError_t e = cudaFuncGetAttributes(&fa, k);
         if (e != cudaSuccess) return e;

@@ -813,11 +813,14 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
             const bool cRL = fabs(dr) > fabs(dl), cR0 = fabs(dr) > 0.0, cL0 = fabs(dl) > 0.0;
             const bool pR = hasR & ((hasL & cRL) | (!hasL & cR0));  // bitwise: no branches
             const bool pL = hasL & cL0;
-            const int pick = pR ? lane : (pL ? lane - 1 : -1);
-            const int pr = __shfl_down_sync(FULL, pick, 1);
-            const int pl = __shfl_up_sync(FULL, pick, 1);
-            const bool mR = hasR && pick == lane && pr == lane;
-            const bool mL = hasL && pick == lane - 1 && pl == lane - 1;
+            // the neighbours' picks from two ballots (a vote is cheaper
+            // than a shuffle): bit s of bR = stage s picks its right edge,
+            // of bL = stage s picks its left edge
+            const bool qL = !pR & pL;
+            const unsigned bR = __ballot_sync(FULL, pR);
+            const unsigned bL = __ballot_sync(FULL, qL);
+            const bool mR = pR & (((bL >> 1) >> lane) & 1u);       // stage s+1 picks left
+            const bool mL = qL & (((bR << 1) >> lane) & 1u);       // stage s-1 picks right
             x = mR ? avgR : (mL ? avgL : x);
         }
         __syncwarp();

@@ -437,24 +437,34 @@ class PeerMigrator:
 
     # NEXT-3: migration overlapped with the backward pass
     def bwd_begin(self, stream=None):
-        """dynmo_migrate_bwd_begin: once per iteration on every rank, on the
-        backward stream before its first layer_ready."""
+        """dynmo_migrate_bwd_begin: once per iteration on every rank, before
+        the other backward-migration calls (host-side epoch)."""
         _check(lib().dynmo_migrate_bwd_begin(self.ctx.handle, self._h, _stream(stream)), "dynmo_migrate_bwd_begin")
 
     def layer_ready(self, layer: int, stream=None):
         """dynmo_migrate_layer_ready: layer's buffers (its gradients) are
-        written on `stream`; peers may pull it."""
+        written on `stream`; released to every rank."""
         _check(lib().dynmo_migrate_layer_ready(self.ctx.handle, self._h, int(layer), _stream(stream)),
                "dynmo_migrate_layer_ready")
 
     def backward(self, bnd_old: torch.Tensor, rank_old: torch.Tensor, bnd_new: torch.Tensor,
-                 rank_new: torch.Tensor, bytes_sent=None, bytes_recv=None, stream=None):
-        """dynmo_migrate_layers_bwd: pull incoming layers last-to-first as
-        their senders release them (needs set_ctas(c), 0 < c < SMs)."""
+                 rank_new: torch.Tensor, bytes_recv=None, stream=None):
+        """dynmo_migrate_layers_bwd: per layer, last to first, a stream wait
+        for its release and a pull if it moves here (needs set_ctas(c),
+        0 < c < SMs)."""
         _check(lib().dynmo_migrate_layers_bwd(self.ctx.handle, self._h, rank_old.numel(), _ptr(bnd_old),
                                               _ptr(rank_old), rank_new.numel(), _ptr(bnd_new), _ptr(rank_new),
-                                              _ptr(bytes_sent), _ptr(bytes_recv), _stream(stream)),
+                                              _ptr(bytes_recv), _stream(stream)),
                "dynmo_migrate_layers_bwd")
+
+    def bwd_end(self, bnd_old: torch.Tensor, rank_old: torch.Tensor, bnd_new: torch.Tensor,
+                rank_new: torch.Tensor, bytes_sent=None, stream=None):
+        """dynmo_migrate_bwd_end: stream waits until every rank has pulled;
+        the sent buffers may be reused after it on `stream`."""
+        _check(lib().dynmo_migrate_bwd_end(self.ctx.handle, self._h, rank_old.numel(), _ptr(bnd_old),
+                                           _ptr(rank_old), rank_new.numel(), _ptr(bnd_new), _ptr(rank_new),
+                                           _ptr(bytes_sent), _stream(stream)),
+               "dynmo_migrate_bwd_end")
 
     def set_ctas(self, max_ctas: int):
         """dynmo_migrate_plan_set_ctas: SM budget of the device-driven pull

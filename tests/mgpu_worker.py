@@ -367,12 +367,13 @@ def main():
         pmb.bwd_begin()
         side_b.wait_stream(main)
         with torch.cuda.stream(side_b):
-            pmb.backward(d_bo, d_ro, bnd, d_rn, bs, br)
+            pmb.backward(d_bo, d_ro, bnd, d_rn, br)
         for l in range(begin + count - 1, begin - 1, -1):  # backward: last layer first
             for _ in range(2):
                 Ab = (Ab @ Ab).clamp_(-1, 1)
             sendb[l][0].fill_(grad_val(l, it))
             pmb.layer_ready(l)
+        pmb.bwd_end(d_bo, d_ro, bnd, d_rn, bs)
         main.wait_stream(side_b)
         torch.cuda.synchronize()
         assert pmb.error() == 0, (rank, it, pmb.error())
@@ -384,7 +385,7 @@ def main():
             assert torch.equal(bufs[1].cpu(), pattern(l, int(payload[l]) // 2 + 1)), (rank, it, l, "bwd params")
     pmb.set_ctas(0)
     try:
-        pmb.backward(d_bo, d_ro, bnd, d_rn, bs, br)  # no SM budget: refused on the host
+        pmb.backward(d_bo, d_ro, bnd, d_rn, br)  # no SM budget: refused on the host
         raised = False
     except RuntimeError:
         raised = True

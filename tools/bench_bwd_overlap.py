@@ -8,8 +8,10 @@ gradient buffer, then dynmo_migrate_layer_ready.  Modes (CUDA events, median
 of reps, max over ranks):
   bwd        the backward alone
   seq        the backward, then the device-driven pull of the moved layers
-  overlap    dynmo_migrate_layers_bwd on a high-priority side stream under an
-             SM budget, pulling each moved layer as soon as it is released
+  overlap    dynmo_migrate_layers_bwd on a high-priority side stream: per
+             layer a stream-memory wait for its release (no SM held), then a
+             pull under the SM budget if it moves here; dynmo_migrate_bwd_end
+             on the main stream after the backward
 Every overlapped iteration is checked byte-exact (this iteration's gradient
 value in every received layer).
 
@@ -80,8 +82,9 @@ def main():
                 pm.bwd_begin()
                 side.wait_stream(main)
                 with torch.cuda.stream(side):
-                    pm.backward(d_bo, d_r, d_bn, d_r, bs, br)
+                    pm.backward(d_bo, d_r, d_bn, d_r, br)
                 backward(it, True)
+                pm.bwd_end(d_bo, d_r, d_bn, d_r, bs)
                 main.wait_stream(side)
             elif mode == "seq":
                 backward(it, False)
