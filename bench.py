@@ -62,8 +62,6 @@ def parse(argv=None):
                     help="cost exchange over NVLink peer memory (default) or ncclAllGather")
     ap.add_argument("--migrate", choices=["p2p", "nccl"], default="p2p",
                     help="layer migration over NVLink peer memory (default) or NCCL send/recv")
-    ap.add_argument("--phase-timing", choices=["all", "profile", "none"], default="profile",
-                    help="which phases get CUDA-event nodes in the step graph")
     ap.add_argument("--map-stages", action="store_true",
                     help="NEXT-3: place the new stages on the GPU slots that keep the most payload in place "
                          "(dynmo_map_stages inside the step) instead of stage s on GPU floor(s*G/n)")
@@ -567,9 +565,10 @@ def step_stats(step_ms):
             "outliers": [[int(k), round(float(step_ms[k]), 4)] for k in np.flatnonzero(step_ms > 2 * med)[:8]]}
 
 
-def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G, cfg):
+def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G, cfg, span_ms=0.0):
     peaks, peak_src = load_peaks()
     achieved = plan_bytes / (prof_avg_ms * 1e-3) / 1e9 if prof_avg_ms > 0 else 0.0
+    span_gbs = plan_bytes / (span_ms * 1e-3) / 1e9 if span_ms > 0 else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_k_profile.json")
     if os.path.exists(tp):
@@ -582,7 +581,13 @@ def roofline(plan_bytes, prof_avg_ms, per_rank_frac, G, cfg):
             "peak": peaks.get("hbm_gbs"), "peak_source": peak_src, "unit": "GB/s",
             "frac": round(achieved / peaks.get("hbm_gbs", 1.0), 4), "traffic": traffic,
             "bytes_per_launch": int(plan_bytes), "avg_launch_ms": round(prof_avg_ms, 5),
-            "per_rank_frac": [round(x / peaks.get("hbm_gbs", 1.0), 4) for x in per_rank_frac]}
+            "per_rank_frac": [round(x / peaks.get("hbm_gbs", 1.0), 4) for x in per_rank_frac],
+            "timing": "CUDA event pair around every k_profile launch in a second pass of K timed steps "
+                      "(the headline steps carry no timing nodes)",
+            # the same launches on the device clock: first CTA start -> last CTA end
+            # (%globaltimer), i.e. without the event pair's launch + completion latency
+            "kernel_span_ms": round(span_ms, 5), "achieved_span": round(span_gbs, 1),
+            "frac_span": round(span_gbs / peaks.get("hbm_gbs", 1.0), 4)}
 
 
 def make_segments(D, srcs, dev):
@@ -733,18 +738,29 @@ def run_pipeline(args, wl):
         main.wait_stream(comm)
         return sr
 
+    rtimer, rgraph = None, None
     if args.graph:
-        # capture (phase events baked into the graph as external event-record nodes)
-        ctx.set_timing(True, phases=None if args.phase_timing == "all" else
-                       ([] if args.phase_timing == "none" else ["profile"]))
+        # headline graphs: no timing nodes (each event-record node costs ~3 us
+        # of the step); the roofline pass below replays copies captured with
+        # the k_profile event pair (+ the kernel's device-clock span)
+        ctx.set_timing(False)
         if dev_mig:
             timer.capture(solve_async)
         else:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=torch.cuda.Stream(device=dev)):
                 solve_async()
+        ctx.set_timing(True, phases=["profile"])
+        if dev_mig:
+            rtimer = StepTimer(ctx, dev, args.steps)
+            rtimer.capture(solve_async)
+        else:
+            rgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(rgraph, stream=torch.cuda.Stream(device=dev)):
+                solve_async()
         torch.cuda.synchronize()
         ctx.timing_read()  # discard
+        ctx.profile_span()
         ctx.set_timing(False)
     stream = torch.cuda.current_stream()
 
@@ -794,7 +810,43 @@ def run_pipeline(args, wl):
     step_ms = np.array(step_list)
     total_ms = float(step_ms.sum())
     prof_ms, prof_n = phases["profile"]
+    span_ms, span_n = 0.0, 0
+    if args.graph:
+        # ---- roofline pass: K more timed steps whose graphs carry the k_profile
+        # event pair (CUDA events on the launching stream) and the kernel's
+        # own device-clock span
+        ctx.set_timing(True)
+        for w in range(3):
+            flush()
+            if rtimer is not None:
+                rtimer.replay(w)
+            else:
+                rgraph.replay()
+                ev_res.synchronize()
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier()
+        ctx.timing_poll()
+        ctx.timing_read()
+        ctx.profile_span()
+        if rtimer is not None:
+            rtimer.run(args.steps, flush, ctx.timing_poll)
+        else:
+            for k in range(args.steps):
+                flush()
+                step_barrier()
+                rgraph.replay()
+                ev_res.synchronize()
+                torch.cuda.synchronize()
+                ctx.timing_poll()
+        torch.cuda.synchronize()
+        if G > 1:
+            dist.barrier()
+        ctx.set_timing(False)
+        prof_ms, prof_n = ctx.timing_read()["profile"]
+        span_ms, span_n = ctx.profile_span()
     prof_avg = prof_ms / max(prof_n, 1)
+    span_avg = span_ms / max(span_n, 1) if span_n else 0.0
     # our kernel nodes per step: k_profile, k_epilogue, [k_unpack(_p2p)], k_partition,
     # k_diffuse, k_repack, [k_mig_signal, k_mig_pull, k_mig_wait | k_signal, k_pull, k_wait]
     per_step = (5 + (1 if G > 1 else 0) + (3 if (G > 1 and args.migrate == "p2p" and moves_mine) else 0)
@@ -856,6 +908,7 @@ def run_pipeline(args, wl):
         [total_ms, prof_avg, e2e_ms, mig_ms, float(sent_recv[0]), float(sent_recv[1])], dev, G)
     per_rank_gbs = gather_list(achieved_local, dev, G)
     prof_at_min = gather_list(prof_avg, dev, G)
+    span_all = gather_list(span_avg, dev, G)
     bytes_all = gather_list(plan.bytes, dev, G)
     # per-step job time = max over ranks of each step's device interval
     st_t = torch.tensor(step_ms, dtype=torch.float64, device=dev)
@@ -883,7 +936,7 @@ def run_pipeline(args, wl):
                 "graph": bool(args.graph),
                 "stage_placement": ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
                                     else f"stage s on GPU floor(s*G/{n}) before and after")},
-            "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G, args.config),
+            "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G, args.config, span_all[worst]),
             "phases_ms_per_launch_diagnostic": diag_phases,
             "step_ms": step_stats(step_ms),
             "migrate": {"moved_layers": int(len(moves)), "max_bytes_sent_per_gpu": int(max_sent),
@@ -988,11 +1041,17 @@ def run_batch(args, wl):
     r0 = res_h.numpy().copy()
     if np.any(r0[:q] != 0) or np.any(r0[2 * q:3 * q] < 0) or r0[3 * q] != 0:
         raise SystemExit("config 5 rebalance failed")
+    # headline graphs without timing nodes; roofline graphs with the k_profile
+    # event pair and the kernel's device-clock span (a second timed pass)
     timer = StepTimer(ctx, dev, args.steps)
-    ctx.set_timing(True, phases=["profile"])
+    ctx.set_timing(False)
     timer.capture(solve_async)
+    rtimer = StepTimer(ctx, dev, args.steps)
+    ctx.set_timing(True, phases=["profile"])
+    rtimer.capture(solve_async)
     torch.cuda.synchronize()
     ctx.timing_read()
+    ctx.profile_span()
     ctx.set_timing(False)
     for w in range(max(args.warmup, 3, timer.C)):
         flush()
@@ -1000,18 +1059,32 @@ def run_batch(args, wl):
     torch.cuda.synchronize()
     if G > 1:
         dist.barrier()
-    ctx.set_timing(True)
-    ctx.timing_read()
     with ClockSampler(local) as clk:
         clk.start()
-        step_list = timer.run(args.steps, flush, ctx.timing_poll)
+        step_list = timer.run(args.steps, flush)
         torch.cuda.synchronize()
         clk.stop()
     if G > 1:
         dist.barrier()
+    ctx.set_timing(True)
+    for w in range(3):
+        flush()
+        rtimer.replay(w)
+    torch.cuda.synchronize()
+    ctx.timing_poll()
+    ctx.timing_read()
+    ctx.profile_span()
+    if G > 1:
+        dist.barrier()
+    rtimer.run(args.steps, flush, ctx.timing_poll)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
     ctx.set_timing(False)
     prof_ms, prof_n = ctx.timing_read()["profile"]
+    span_ms, span_n = ctx.profile_span()
     prof_avg = prof_ms / max(prof_n, 1)
+    span_avg = span_ms / max(span_n, 1) if span_n else 0.0
     step_ms = np.array(step_list)
     total_ms = float(step_ms.sum())
     # e2e: H2D of the rank's token masks from pinned memory + the result D2H
@@ -1036,6 +1109,7 @@ def run_batch(args, wl):
     total_ms, e2e_ms = reduce_max([total_ms, e2e_ms], dev, G)
     per_rank_gbs = gather_list(achieved_local, dev, G)
     prof_all = gather_list(prof_avg, dev, G)
+    span_all = gather_list(span_avg, dev, G)
     bytes_all = gather_list(plan.bytes, dev, G)
     n_new_sum = gather_list(float(r0[q:2 * q].sum()), dev, G)
     n_cur_sum = gather_list(float(sum(x.n for x in insts)), dev, G)
@@ -1053,7 +1127,7 @@ def run_batch(args, wl):
             "config": wl.config(G),
             "setup": {"graph": True, "exchange": "none (independent instances)", "migration": "none"},
             "instances_per_s": round(wl.N_INST / (ms * 1e-3), 1),
-            "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G, args.config),
+            "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G, args.config, span_all[worst]),
             "step_ms": step_stats(step_ms),
             "solution": {"workers_before": int(sum(n_cur_sum)), "workers_after_repack": int(sum(n_new_sum))},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(words.nbytes),

@@ -125,6 +125,13 @@ dynmo_status dynmo_ctx_barrier(dynmo_ctx ctx, dynmo_stream stream);
 dynmo_status dynmo_ctx_timing_detach(dynmo_ctx ctx);
 dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total_ms,
                                    int64_t *h_count);
+/* With the profile phase timed, k_profile also records its own span on the
+ * device clock (%globaltimer: first CTA start to last CTA end; the event
+ * pair around it adds the launch and completion latency, ~5 us on B200,
+ * tools/lat/ramp.cu); the epilogue folds each launch's span into an
+ * accumulator.  Returns (and resets) the accumulated milliseconds and
+ * launch count; synchronous. */
+dynmo_status dynmo_ctx_profile_span(dynmo_ctx ctx, double *h_total_ms, int64_t *h_count);
 
 /* ----------------------------------------------------------- profiling --
  * Sources of per-layer workload (P:L234-239 pruning p_i, P:L266-283 freezing

@@ -1021,11 +1021,15 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     }();
     ProfArgs pa{plan->d_tiles, plan->n_tiles, plan->d_acc, plan->d_hist, plan->d_exit,
                 std::max(1, plan->max_E), plan->d_ws_status, plan->warp_words, plan->n_local,
-                plan->bytes <= l2_max ? 1 : 0};
+                plan->bytes <= l2_max ? 1 : 0, nullptr};
+    // profile-phase timing also measures the kernel's own span on the device
+    unsigned long long *span = (ctx->timing & (1 << DYNMO_PHASE_PROFILE)) ? ctx->d_win->prof_span : nullptr;
+    pa.span = span;
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_PROFILE, s);
     CUDA_TRY(launch_profile(pa, plan->ops, plan->grid, s), "k_profile launch");
     phase_end(te, s);
     EpiArgs ea{};
+    ea.span = span;
     ea.layer_begin = plan->layer_begin;
     ea.n_local = plan->n_local;
     ea.n_total = plan->n_total;
@@ -1716,6 +1720,17 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     }
     CUDA_TRY(launch_wait(wt, s), "k_wait launch");
     phase_end(te, s);
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_profile_span(dynmo_ctx ctx, double *h_total_ms, int64_t *h_count) {
+    if (!ctx || !h_total_ms || !h_count) return invalid("null ctx/out");
+    DeviceGuard g(ctx->device);
+    unsigned long long h[4];
+    CUDA_TRY(cudaMemcpy(h, ctx->d_win->prof_span, sizeof(h), cudaMemcpyDeviceToHost), "read profile span");
+    *h_total_ms = (double)h[2] * 1e-6;
+    *h_count = (int64_t)h[3];
+    CUDA_TRY(cudaMemset(ctx->d_win->prof_span + 2, 0, 2 * sizeof(unsigned long long)), "reset profile span");
     return DYNMO_OK;
 }
 

@@ -122,6 +122,10 @@ struct ProfArgs {
     int32_t warp_words;  // per-warp histogram scratch (u32 words)
     int32_t n_local;     // layers of the plan (bounds of acc / hist rows)
     int32_t l2_prefetch; // 1: each warp bulk-prefetches its whole tile range into L2 at entry
+    // nullable: {~min CTA start, max CTA end} in %globaltimer ns (profile-phase
+    // timing: the kernel's own span, without the event-bracket launch and
+    // completion latencies); folded and reset by the epilogue's last block
+    unsigned long long *span;
 };
 // Plans whose bytes fit comfortably in the 126 MB L2 issue one L2 bulk
 // prefetch per tile at kernel entry (all of a warp's range at once), so the
@@ -158,6 +162,7 @@ struct EpiArgs {
     int32_t *ws_status;
     unsigned int *ws_done;
     int32_t *status_out;     // local mode final status
+    unsigned long long *span;  // nullable: [0] ~start, [1] end of k_profile, [2] sum of spans (ns), [3] launches
 };
 
 // ops: bit 0 count ops, bit 1 exit histogram, bit 2 expert histograms
@@ -298,6 +303,8 @@ struct PeerWindow {
     // memory operations (epochs from the host)
     uint64_t bwd_done[kMaxRanksEpi];
     uint64_t layer_ready[1024];
+    // profile-phase timing: k_profile's own span (ProfArgs::span), local use
+    unsigned long long prof_span[4];
 };
 constexpr size_t kPeerWindowBytes = 16384;  // the window allocation
 static_assert(sizeof(PeerWindow) <= kPeerWindowBytes, "peer window page");

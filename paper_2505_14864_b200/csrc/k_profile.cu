@@ -20,6 +20,12 @@
 namespace dynmo {
 namespace {
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -258,6 +264,7 @@ __device__ __forceinline__ void expert_small(const ProfTile &t, bool scalar, int
 template <int OPS>
 __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OPS & 8) ? 2 : 3) k_profile(ProfArgs a) {
     pdl_trigger();  // the epilogue may be scheduled now (it waits for this grid)
+    if (a.span && threadIdx.x == 0) atomicMax(&a.span[0], ~globaltimer_ns());  // ~start: zero-reset max
     constexpr bool HAS_CNT = OPS & 1, HAS_EXIT = (OPS & 2) != 0, HAS_EXP = (OPS & 4) != 0;
     constexpr bool HAS_BIGE = (OPS & 8) != 0;  // some expert layer has E > 16 (smem histograms)
     constexpr bool HAS_HIST = HAS_EXIT || HAS_EXP;
@@ -569,6 +576,10 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
     }
     // an expert id outside [0, E) or a time pair with end < begin
     if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
+    if (a.span) {  // the CTA's end: after all of its warps
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&a.span[1], globaltimer_ns());
+    }
 }
 
 // -------------------------------------------------------------- epilogue
@@ -719,6 +730,15 @@ __global__ void k_epilogue(EpiArgs a) {
     if (s_last) {
         __threadfence();
         for (int v = threadIdx.x; v < kExitBins; v += blockDim.x) a.exit_hist[v] = 0ull;
+        if (threadIdx.x == 0 && a.span) {  // k_profile has completed (pdl_wait)
+            const unsigned long long t0 = ~a.span[0], t1 = a.span[1];
+            if (a.span[0] && t1 > t0) {
+                a.span[2] += t1 - t0;
+                a.span[3] += 1ull;
+            }
+            a.span[0] = 0ull;
+            a.span[1] = 0ull;
+        }
         if (threadIdx.x == 0) {
             const int fin = atomicExch(a.ws_status, 0);
             *a.ws_done = 0u;

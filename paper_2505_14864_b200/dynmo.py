@@ -138,6 +138,13 @@ class Context:
             out[name] = (ms.value, cnt.value)
         return out
 
+    def profile_span(self):
+        """(total_ms, launches) of k_profile's own device-clock span since the
+        last call (profile-phase timing on); synchronous."""
+        ms, cnt = C.c_double(0.0), C.c_int64(0)
+        _check(lib().dynmo_ctx_profile_span(self._h, C.byref(ms), C.byref(cnt)), "dynmo_ctx_profile_span")
+        return ms.value, cnt.value
+
     def p2p_error(self) -> int:
         """Sticky device error word of the peer-memory paths (0 = none)."""
         e = C.c_int32(0)

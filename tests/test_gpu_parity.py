@@ -1020,6 +1020,42 @@ def test_ctx_barrier_timing_detach_and_split_single(D, L, ctx):
     del g
 
 
+def test_profile_span_clock(D, L, ctx):
+    """With the profile phase timed, every k_profile launch (eager and graph
+    replays) also records its device-clock span (dynmo_ctx_profile_span):
+    one span per launch, positive, no longer than the launch's event pair;
+    the counts stay exact; untimed launches record nothing."""
+    seg = D.SegmentSpec(_dev((np.arange(1 << 22) % 3).astype(np.uint8)), L.SRC_MASK_U8, 0)
+    plan = D.ProfilePlan(ctx, [seg], 0, 1)
+    coef = D.coef_tensor(1, B=1, device=DEV)
+    D.profile_layers(ctx, plan, coef)
+    torch.cuda.synchronize()
+    ctx.profile_span()
+    ctx.set_timing(True, phases=["profile"])
+    ctx.timing_read()
+    for _ in range(3):
+        cost, _, st = D.profile_layers(ctx, plan, coef)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        D.profile_layers(ctx, plan, coef)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        ctx.timing_poll()
+    torch.cuda.synchronize()
+    ev_ms, ev_n = ctx.timing_read()["profile"]
+    sp_ms, sp_n = ctx.profile_span()
+    ctx.timing_detach()
+    ctx.set_timing(False)
+    assert int(st.item()) == 0 and int(cost[0].item()) == (1 << 22) * 2 // 3
+    assert ev_n == 5 and sp_n == 5, (ev_n, sp_n)
+    assert 0.0 < sp_ms <= ev_ms, (sp_ms, ev_ms)
+    D.profile_layers(ctx, plan, coef)  # untimed: no span
+    torch.cuda.synchronize()
+    assert ctx.profile_span() == (0.0, 0)
+    plan.close()
+
+
 # ------------------------------- round 2: hand traces, large n, 1-rank exchange
 import json as _json
 import os as _os
