@@ -45,6 +45,13 @@ def test_host_argument_validation_without_gpu():
     assert L.dynmo_partition_stages(None, 1, 8, *([None] * 11)) == _lib.E_INVALID
     assert L.dynmo_migrate_plan_set_ctas(None, 16) == _lib.E_INVALID  # null plan
     assert L.dynmo_global_prune(None, None, 1, None, None, None) == _lib.E_INVALID  # null ctx / plan
+    # the backward-overlapped migration and the span read: null ctx / plan / outputs
+    assert L.dynmo_migrate_bwd_begin(None, None, None) == _lib.E_INVALID
+    assert L.dynmo_migrate_layer_ready(None, None, 0, None) == _lib.E_INVALID
+    assert L.dynmo_migrate_layers_bwd(None, None, 1, None, None, 1, None, None, None, None) == _lib.E_INVALID
+    assert L.dynmo_migrate_bwd_end(None, None, 1, None, None, 1, None, None, None, None) == _lib.E_INVALID
+    ms, n = ctypes.c_double(), ctypes.c_int64()
+    assert L.dynmo_ctx_profile_span(None, ctypes.byref(ms), ctypes.byref(n)) == _lib.E_INVALID
 
 
 def test_migration_plan_vs_oracle():
