@@ -839,69 +839,6 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
     }
 }
 
-// n <= 8: every lane holds all eight loads in registers and advances the
-// round redundantly -- no shuffle or vote on the per-round dependent chain
-// (gaps, picks, mutual matches and the averages are register arithmetic on
-// compile-time indices).  Same rule and rounding as fluid_chunks: a stage
-// picks its right edge iff its right gap beats its left one (no left edge:
-// the right gap > 0), else its left edge iff that gap > 0; matched pairs
-// become (x_e + x_{e+1}) * 0.5.  Lane 0 stores each round's row for the
-// chunked phi_f evaluation.
-__device__ void fluid_rep8(const Inst &s, int n, const int32_t *bi, double gf, int maxr, double *hist,
-                           double *xo, int &rr, double &ph, int &fst, int lane) {
-    double x[8];
-    bool ex[7];  // edge e present
-#pragma unroll
-    for (int k = 0; k < 8; ++k) x[k] = k < n ? (double)(s.P[bi[k + 1]] - s.P[bi[k]]) : 0.0;
-#pragma unroll
-    for (int e = 0; e < 7; ++e) ex[e] = e + 1 < n;
-    int size = 1;
-    for (int base = 0;; base += size, size = size < kChunk / 4 ? size * 4 : kChunk) {
-        for (int k = 0; k < size; ++k) {
-            if (lane == 0) {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) hist[k * kRow + u] = x[u];  // x(base + k)
-            }
-            double d[7], av[7];
-#pragma unroll
-            for (int e = 0; e < 7; ++e) {
-                d[e] = __dsub_rn(x[e], x[e + 1]);
-                av[e] = __dmul_rn(__dadd_rn(x[e], x[e + 1]), 0.5);
-            }
-            bool pr[8], pl[8];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const bool hasR = t < 7 && ex[t], hasL = t > 0 && ex[t - 1];
-                const bool cR = hasR && (hasL ? fabs(d[t]) > fabs(d[t - 1]) : d[t] != 0.0);
-                pr[t] = cR;
-                pl[t] = hasL && !cR && d[t - 1 < 0 ? 0 : t - 1] != 0.0;
-            }
-            bool m[7];
-#pragma unroll
-            for (int e = 0; e < 7; ++e) m[e] = pr[e] && pl[e + 1];
-#pragma unroll
-            for (int t = 0; t < 8; ++t) {
-                const bool mR = t < 7 && m[t < 7 ? t : 0];
-                const bool mL = t > 0 && m[t > 0 ? t - 1 : 0];
-                x[t] = mR ? av[t < 7 ? t : 0] : (mL ? av[t > 0 ? t - 1 : 0] : x[t]);
-            }
-        }
-        __syncwarp();
-        const double acc = lane < size ? phi_row(hist + lane * kRow, n) : 0.0;
-        const bool stop = lane < size && (acc <= gf || base + lane == maxr);
-        const unsigned msk = __ballot_sync(FULL, stop);
-        if (msk) {
-            const int k = __ffs(msk) - 1;
-            rr = base + k;
-            ph = __shfl_sync(FULL, acc, k);
-            if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
-            if (lane < n) xo[lane] = hist[k * kRow + lane];
-            return;
-        }
-        __syncwarp();
-    }
-}
-
 __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, const int32_t *bi,
                               int fst, double *hist, int lane) {
     const double gf = a.gamma_fluid ? a.gamma_fluid[q] : 0.0;
@@ -919,8 +856,7 @@ __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, c
     int rr = 0;
     double ph = 0.0;
     if (n <= 32) {
-        if (n <= 8 && a.fluid_rep8) fluid_rep8(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
-        else fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+        fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
     } else if (lane == 0) {
         // n > 32: serial on lane 0 over shared memory (s.x reused as fp64)
         double *sxf = reinterpret_cast<double *>(s.x);
