@@ -96,7 +96,7 @@ for cfg in (2, 4, 5):
         g2.replay()
         b.record()
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) * 1e-3)
+        ts.append(a.elapsed_time(b))
     out["graph_replay_events_us (profile + epilogue + graph launch)"] = med(ts)
     # (d) eager launch, bench-side event pair around profile_layers (k_profile + k_epilogue)
     ts = []
@@ -107,7 +107,7 @@ for cfg in (2, 4, 5):
         call()
         b.record()
         torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b) * 1e-3)
+        ts.append(a.elapsed_time(b))
     out["eager_call_events_us (profile + epilogue)"] = med(ts)
     print(json.dumps(out), flush=True)
     plan.close()
