@@ -206,44 +206,47 @@ __device__ __forceinline__ int warp_jump(const Inst &s, int j, int64_t t1, int64
 // candidate B (instead of one warp per candidate), so a CTA of 256 threads
 // tests 256 candidates per round and a one-warp instance 32.  Two exact
 // greedy counts (maximal prefix stages, reading Q8/Q9), chosen per instance:
-//  scan_count   one pass over the layers: the shared loads of P[i] (and
-//               M[i]) are the same address for every lane (broadcast, no bank
-//               conflict) and independent of the data, so they pipeline; the
+//  scan_count   one pass over the layers: the shared loads of P[i] are the
+//               same address for every lane (broadcast, no bank conflict)
+//               and independent of the data, so they pipeline; the
 //               dependent chain per layer is a compare and a select.
 //  jump_count   per stage, binary lifting over P (log2 L dependent loads):
 //               fewer instructions when n log2(L) << L.
-// Both assume every layer fits a stage alone (B >= max c, every m <= cap),
-// which the search establishes before the first round.  A count above
-// `limit` may be reported as any value > limit.
-// Arithmetic: unsigned, no saturation needed.  Every P, B <= C <= INT64_MAX
-// and M, cap' <= M[L] <= INT64_MAX (cap' = min(cap, M[L]) decides the same
-// splits), so P + B and M + cap' fit in uint64_t.  When C and M[L] are below
-// 2^31 the same sums fit in uint32_t: half the registers and compare
-// instructions (the 32-bit copies of P and M live in Inst::x, unused by the
-// partition and the repack).
+// The memory cap does not depend on B: reach[j] = the largest K with
+// M[K] - M[j] <= cap is computed once per instance (binary searches over M,
+// in the 16-bit table Inst::nxt), and a stage starting at j ends at
+// min(cost reach(j, B), reach[j]) -- one index compare instead of 64-bit
+// loads and compares of M in every step.  Both counts assume every layer
+// fits a stage alone (B >= max c, every m <= cap), which the search
+// establishes before the first round.  A count above `limit` may be reported
+// as any value > limit.
+// Arithmetic: unsigned, no saturation needed (every P, B <= C <= INT64_MAX,
+// so P + B fits in uint64_t); when C < 2^31 the same sums fit in uint32_t:
+// half the registers and compare instructions (the 32-bit copy of P lives in
+// Inst::x, unused by the partition and the repack).
 template <typename T>
 struct View {
-    const T *P, *M;
-    T cap;
+    const T *P;
+    const int16_t *reach;  // MEM only
     int L;
 };
 
 template <typename T, bool MEM>
 __device__ __forceinline__ int scan_count(const View<T> &v, T B) {
-    T t1 = B;       // P[start] + B with start = 0
-    T t2 = v.cap;   // M[start] + cap
+    T t1 = B;                            // P[start] + B with start = 0
+    int lim = MEM ? v.reach[0] : v.L;    // reach[start]
     int c = 1;
 #pragma unroll 4
     for (int i = 1; i <= v.L; ++i) {
-        // layer i-1 joins the open stage iff P[i] <= t1 (and M[i] <= t2);
+        // layer i-1 joins the open stage iff P[i] <= t1 and i <= reach[start];
         // else it opens the next stage (it fits alone)
         bool cut = v.P[i] > t1;
-        if constexpr (MEM) cut |= v.M[i] > t2;
+        if constexpr (MEM) cut |= i > lim;
         const T n1 = v.P[i - 1] + B;
         t1 = cut ? n1 : t1;
         if constexpr (MEM) {
-            const T n2 = v.M[i - 1] + v.cap;
-            t2 = cut ? n2 : t2;
+            const int nl = v.reach[i - 1];
+            lim = cut ? nl : lim;
         }
         c += cut;
     }
@@ -257,15 +260,15 @@ __device__ __forceinline__ int jump_count(const View<T> &v, T B, int limit) {
     int j = 0, c = 0;
     while (j < L && c <= limit) {
         const T t1 = v.P[j] + B;
-        T t2 = 0;
-        if constexpr (MEM) t2 = v.M[j] + v.cap;
         int K = j;
         for (int step = top; step > 0; step >>= 1) {
             const int k2 = K + step;
             const int kc = k2 <= L ? k2 : L;  // branch-free: clamped load
-            bool ok = (k2 <= L) & (v.P[kc] <= t1);
-            if constexpr (MEM) ok &= v.M[kc] <= t2;
-            K = ok ? k2 : K;
+            K = ((k2 <= L) & (v.P[kc] <= t1)) ? k2 : K;
+        }
+        if constexpr (MEM) {
+            const int r = v.reach[j];
+            K = K < r ? K : r;
         }
         j = K;  // K > j: layer j fits alone
         ++c;
@@ -276,6 +279,26 @@ __device__ __forceinline__ int jump_count(const View<T> &v, T B, int limit) {
 template <typename T, bool MEM>
 __device__ __forceinline__ int thread_count(const View<T> &v, int64_t B, int limit, bool jumps) {
     return jumps ? jump_count<T, MEM>(v, (T)B, limit) : scan_count<T, MEM>(v, (T)B);
+}
+
+// Memory reach of every start j (MEM): the largest K in [j, L] with
+// M[K] - M[j] <= cap (M is nondecreasing), by binary lifting; all threads,
+// then a barrier (CTA or warp).
+template <int NW>
+__device__ __forceinline__ void build_reach(Inst &s) {
+    const int L = s.L, top = 1 << (31 - __clz(L));
+    for (int j = threadIdx.x; j <= L; j += blockDim.x) {
+        const int64_t t = satadd(s.M[j], s.cap);
+        int K = j;
+        for (int step = top; step > 0; step >>= 1) {
+            const int k2 = K + step;
+            const int kc = k2 <= L ? k2 : L;
+            K = ((k2 <= L) & (s.M[kc] <= t)) ? k2 : K;
+        }
+        s.nxt[j] = (int16_t)K;
+    }
+    if constexpr (NW > 1) __syncthreads();
+    else __syncwarp();
 }
 
 // Candidate t of NC per round: lo + floor(d (t+1) / (NC+1)) in 64-bit
@@ -358,15 +381,12 @@ __device__ __forceinline__ bool use_jumps(int L, int n) {
     return NW > 1 ? L > 3 * n * lg : 2 * L > n * lg;
 }
 
-// 32-bit copies of P and M into s.x (2 (L+1) words <= its 8 (L+1) bytes),
-// then the search.  Called by all threads; the copy is made by all threads
-// and fenced with a CTA barrier (NW > 1) or warp sync.
+// The memory reach table (MEM), the 32-bit copy of P into s.x when C < 2^31,
+// then the search.  Called by all threads (barriers inside).
 template <bool MEM, int NW>
-__device__ int64_t search_bottleneck(const Inst &s, int n) {
+__device__ int64_t search_bottleneck(Inst &s, int n) {
     const int L = s.L;
     const int64_t C = s.P[L];
-    const int64_t MC = MEM ? s.M[L] : 0;
-    const int64_t cap = MEM ? (s.cap < MC ? s.cap : MC) : 0;
     if (MEM && !s.mfit) return -1;
     const int64_t ceil_cn = C / n + (C % n != 0);
     int64_t lo = s.maxc > ceil_cn ? s.maxc : ceil_cn;
@@ -375,34 +395,45 @@ __device__ int64_t search_bottleneck(const Inst &s, int n) {
     if (lo > hi) lo = hi;
     if (!MEM && lo == hi) return hi;
     const bool jumps = use_jumps<NW>(L, n);
-    if (C < (1ll << 31) && MC < (1ll << 31)) {
+    if (C < (1ll << 31)) {
         uint32_t *p32 = reinterpret_cast<uint32_t *>(s.x);
-        uint32_t *m32 = p32 + (L + 1);
-        for (int i = threadIdx.x; i <= L; i += blockDim.x) {
-            p32[i] = (uint32_t)s.P[i];
-            if constexpr (MEM) m32[i] = (uint32_t)s.M[i];
-        }
-        if constexpr (NW > 1) __syncthreads();
+        for (int i = threadIdx.x; i <= L; i += blockDim.x) p32[i] = (uint32_t)s.P[i];
+        if constexpr (MEM) build_reach<NW>(s);  // (its barrier also covers p32)
+        else if constexpr (NW > 1) __syncthreads();
         else __syncwarp();
-        const View<uint32_t> v{p32, m32, (uint32_t)cap, L};
+        const View<uint32_t> v{p32, s.nxt, L};
         return search_t<uint32_t, MEM, NW>(s, v, n, lo, hi, jumps);
     }
-    const View<uint64_t> v{reinterpret_cast<const uint64_t *>(s.P), reinterpret_cast<const uint64_t *>(s.M),
-                           (uint64_t)cap, L};
+    if constexpr (MEM) build_reach<NW>(s);
+    const View<uint64_t> v{reinterpret_cast<const uint64_t *>(s.P), s.nxt, L};
     return search_t<uint64_t, MEM, NW>(s, v, n, lo, hi, jumps);
 }
 
 // Greedy stage count at one B (repack's fewest workers; one warp, every
-// lane the same B): 64-bit scan, cap clamped as above.
+// lane the same B; B >= max c and every m <= cap): a 64-bit scan with the
+// memory test on M directly (no reach table yet).
 template <bool MEM>
 __device__ int count_at(const Inst &s, int64_t B) {
-    const int64_t MC = MEM ? s.M[s.L] : 0;
-    const int64_t cap = MEM ? (s.cap < MC ? s.cap : MC) : 0;
     const int64_t C = s.P[s.L];
-    const View<uint64_t> v{reinterpret_cast<const uint64_t *>(s.P), reinterpret_cast<const uint64_t *>(s.M),
-                           (uint64_t)cap, s.L};
-    // B > C behaves as B = C (one stage holds everything)
-    return scan_count<uint64_t, MEM>(v, (uint64_t)(B < C ? B : C));
+    const uint64_t b = (uint64_t)(B < C ? B : C);  // B > C behaves as C
+    const uint64_t *P = reinterpret_cast<const uint64_t *>(s.P);
+    const uint64_t *M = reinterpret_cast<const uint64_t *>(s.M);
+    const uint64_t cap = MEM ? (uint64_t)(s.cap < s.M[s.L] ? s.cap : s.M[s.L]) : 0;
+    uint64_t t1 = b, t2 = cap;
+    int c = 1;
+#pragma unroll 4
+    for (int i = 1; i <= s.L; ++i) {
+        bool cut = P[i] > t1;
+        if constexpr (MEM) cut |= M[i] > t2;
+        const uint64_t n1 = P[i - 1] + b;
+        t1 = cut ? n1 : t1;
+        if constexpr (MEM) {
+            const uint64_t n2 = M[i - 1] + cap;
+            t2 = cut ? n2 : t2;
+        }
+        c += cut;
+    }
+    return c;
 }
 
 // Lexmax boundaries for B* (Appendix A): b_{s+1} = min(next(b_s), L - (n-1-s))
