@@ -1601,12 +1601,11 @@ dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     cudaStream_t s = (cudaStream_t)stream;
     const uint64_t ep = ctx->bwd_epoch;
     cudaEvent_t te = phase_begin(ctx, DYNMO_PHASE_MIGRATE, s);
-    if (d_bytes_recv) CUDA_TRY(cudaMemsetAsync(d_bytes_recv, 0, sizeof(int64_t), s), "bytes_recv reset");
     for (int i = mp->n_layers - 1; i >= 0; --i) {  // the backward order: last layer first
         if (dynmo_status st = stream_wait_geq(ctx, s, &ctx->d_win->layer_ready[i], ep)) return st;
-        CUDA_TRY(launch_bwd_pull_layer(a, i, mp->max_ctas, s), "k_bwd_pull_layer launch");
+        CUDA_TRY(launch_bwd_pull_layer(a, i, ep, mp->max_ctas, s), "k_bwd_pull_layer launch");
     }
-    CUDA_TRY(launch_bwd_done(bwd_peers(ctx), ctx->rank, ep, s), "k_bwd_done launch");
+    CUDA_TRY(launch_bwd_done(a, bwd_peers(ctx), ep, s), "k_bwd_done launch");
     phase_end(te, s);
     return DYNMO_OK;
 }
@@ -1621,6 +1620,8 @@ dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,
     a.bytes_sent = d_bytes_sent;
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
+    // the caller's backward is done: pull what is left with every SM
+    CUDA_TRY(launch_bwd_drain(a, ctx->bwd_epoch, ctx->num_sms, s), "k_bwd_drain launch");
     for (int r = 0; r < ctx->nranks; ++r)
         if (dynmo_status st = stream_wait_geq(ctx, s, &ctx->d_win->bwd_done[r], ctx->bwd_epoch)) return st;
     if (d_bytes_sent) CUDA_TRY(launch_bwd_sent(a, s), "k_bwd_sent launch");

@@ -303,10 +303,12 @@ struct PeerWindow {
     // memory operations (epochs from the host)
     uint64_t bwd_done[kMaxRanksEpi];
     uint64_t layer_ready[1024];
+    unsigned long long bwd_claim[1024];  // per layer {epoch, chunks claimed} (local use)
+    unsigned int bwd_finished[2];        // chunks copied, per epoch parity (local use)
     // profile-phase timing: k_profile's own span (ProfArgs::span), local use
     unsigned long long prof_span[4];
 };
-constexpr size_t kPeerWindowBytes = 16384;  // the window allocation
+constexpr size_t kPeerWindowBytes = 32768;  // the window allocation
 static_assert(sizeof(PeerWindow) <= kPeerWindowBytes, "peer window page");
 
 struct DevBuf {
@@ -334,8 +336,9 @@ struct BwdPeers {
     int32_t nranks;
 };
 cudaError_t launch_layer_ready(const BwdPeers &p, int32_t layer, uint64_t epoch, cudaStream_t s);
-cudaError_t launch_bwd_done(const BwdPeers &p, int32_t me, uint64_t epoch, cudaStream_t s);
-cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, int grid, cudaStream_t s);
+cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, uint64_t epoch, int grid, cudaStream_t s);
+cudaError_t launch_bwd_drain(const DevMigArgs &a, uint64_t epoch, int grid, cudaStream_t s);
+cudaError_t launch_bwd_done(const DevMigArgs &a, const BwdPeers &p, uint64_t epoch, cudaStream_t s);
 cudaError_t launch_bwd_sent(const DevMigArgs &a, cudaStream_t s);
 // force-load every peer-path kernel (CUDA lazy loading; see k_p2p.cu)
 cudaError_t preload_p2p_kernels();

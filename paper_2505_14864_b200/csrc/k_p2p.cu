@@ -294,14 +294,20 @@ __global__ void k_mig_wait(DevMigArgs a) {
 
 // ------------------- NEXT-3: migration during the backward pass
 // "moving layers while the gradients calculation take place, from the last
-// to the first layer".  No kernel waits on the GPU: the backward stream
-// releases layer i (k_layer_ready: its payload is final) into EVERY rank's
-// window; each rank's side stream waits for the layers in descending order
-// with stream memory operations (the GPU front end polls, no SM is held) and
-// runs one short pull kernel per layer under the SM budget, which copies the
-// layer only if it is incoming here (device boundaries / rank maps).  Then
-// the side stream releases done[me] everywhere, and the senders' streams wait
-// for every rank's done before reusing the sent buffers (dynmo_migrate_bwd_end).
+// to the first layer".  While the backward runs, no kernel waits on the GPU:
+// the backward stream releases layer i (k_layer_ready: its payload is final)
+// into EVERY rank's window; each rank's side stream waits for the layers in
+// descending order with stream memory operations (the GPU front end polls,
+// no SM is held) and runs one pull kernel per layer under the SM budget.  A
+// layer's payload is cut into 256 KiB chunks claimed by CTAs through an
+// epoch-tagged counter, so a DRAIN kernel with every SM, launched by
+// dynmo_migrate_bwd_end once the caller's backward is done, can take over
+// the chunks not yet pulled (the last layers are released when there is no
+// compute left to hide them).  k_bwd_done waits until every incoming chunk
+// is copied, then releases done[me] everywhere; the senders' streams wait
+// for every rank's done before reusing the sent buffers.
+constexpr uint64_t kBwdChunk = 256u << 10;
+
 __global__ void k_layer_ready(BwdPeers p, int32_t layer, uint64_t epoch) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
         // the stream's earlier kernels wrote the layer's buffers: make them
@@ -311,50 +317,87 @@ __global__ void k_layer_ready(BwdPeers p, int32_t layer, uint64_t epoch) {
     }
 }
 
-__global__ void k_bwd_done(BwdPeers p, int32_t me, uint64_t epoch) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        __threadfence_system();
-        for (int r = 0; r < p.nranks; ++r) st_release_sys(&p.win[r]->bwd_done[me], epoch);
-    }
+__device__ __forceinline__ bool mig_args_ok(const DevMigArgs &a) {
+    return valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
+           ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
 }
 
-// One layer (i) of the backward-ordered pull: every CTA checks the split and
-// the owners of layer i; if it moves to this rank, the grid copies its
-// buffers with U x 16-byte NVLink loads in flight per thread.
-template <int U>
-__global__ void __launch_bounds__(kP2PThreads) k_bwd_pull_layer(DevMigArgs a, int32_t i) {
-    __shared__ int s_ok;
-    if (threadIdx.x == 0)
-        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
-               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
-    __syncthreads();
-    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (!s_ok) {
-        if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
-        return;
-    }
+// Sender of layer i if it moves to this rank, else -1.
+__device__ __forceinline__ int incoming_src(const DevMigArgs &a, int i) {
     const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
     const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
-    if (dst != a.me || src == a.me) return;
-    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
-    unsigned long long recvd = 0;
+    return (dst == a.me && src != a.me) ? src : -1;
+}
+
+// Chunks of layer i from src (every buffer cut at kBwdChunk); 0 and an error
+// if a receive buffer does not match its send buffer.
+__device__ uint32_t layer_chunks(const DevMigArgs &a, int i, int src, bool &bad) {
+    uint32_t nc = 0;
     for (int k = 0; k < a.n_bufs; ++k) {
         const int64_t idx = (int64_t)i * a.n_bufs + k;
         const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
         const DevBuf rb = a.recv_tab[idx];
         if (sb.bytes != rb.bytes || (sb.bytes > 0 && (!sb.ptr || !rb.ptr))) {
-            if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+            bad = true;
+            return 0;
+        }
+        nc += (uint32_t)(((uint64_t)sb.bytes + kBwdChunk - 1) / kBwdChunk);
+    }
+    return nc;
+}
+
+// Claim the next chunk of layer i in iteration `ep` (thread 0).  The word is
+// {epoch low 32 bits, claims}: a stale epoch restarts at 0, a newer one means
+// this launch's iteration is over (nothing to claim).  Returns the chunk
+// index, or UINT32_MAX.
+__device__ uint32_t claim_chunk(unsigned long long *w, uint64_t ep, uint32_t nc) {
+    const unsigned long long e = (unsigned long long)(uint32_t)ep;
+    unsigned long long cur = *(volatile unsigned long long *)w;
+    for (;;) {
+        const unsigned long long we = cur >> 32;
+        unsigned long long nxt;
+        uint32_t got;
+        if (we == e) {
+            got = (uint32_t)cur;
+            if (got >= nc) return UINT32_MAX;
+            nxt = cur + 1;
+        } else if ((uint32_t)(we - e) > 0x7FFFFFFFu) {  // stale (older) epoch
+            got = 0;
+            nxt = (e << 32) | 1ull;
+        } else {
+            return UINT32_MAX;  // a newer iteration owns the word
+        }
+        const unsigned long long prev = atomicCAS(w, cur, nxt);
+        if (prev == cur) return got;
+        cur = prev;
+    }
+}
+
+// Copy chunk c of layer i (whole CTA, 16 x 16-byte NVLink loads in flight
+// per thread), then count it finished (after a fence: the copy is visible
+// before the counter that k_bwd_done waits on).
+__device__ void copy_chunk(const DevMigArgs &a, int i, int src, uint32_t c, unsigned int *finished) {
+    constexpr int U = 16;
+    for (int k = 0; k < a.n_bufs; ++k) {
+        const int64_t idx = (int64_t)i * a.n_bufs + k;
+        const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
+        const DevBuf rb = a.recv_tab[idx];
+        const uint32_t nck = (uint32_t)(((uint64_t)sb.bytes + kBwdChunk - 1) / kBwdChunk);
+        if (c >= nck) {
+            c -= nck;
             continue;
         }
-        const uint64_t bytes = (uint64_t)sb.bytes;
-        recvd += bytes;
-        const uint8_t *sp = (const uint8_t *)sb.ptr;
-        uint8_t *dp = (uint8_t *)rb.ptr;
+        const uint64_t off = (uint64_t)c * kBwdChunk;
+        const uint64_t rem = (uint64_t)sb.bytes - off;
+        const uint64_t bytes = rem < kBwdChunk ? rem : kBwdChunk;
+        const uint8_t *sp = (const uint8_t *)sb.ptr + off;
+        uint8_t *dp = (uint8_t *)rb.ptr + off;
         const bool vec = (((uintptr_t)sp | (uintptr_t)dp) & 15) == 0;
         const uint64_t nvec = vec ? bytes >> 4 : 0;
         const uint4 *s4 = (const uint4 *)sp;
         uint4 *d4 = (uint4 *)dp;
-        uint64_t x = gt;
+        const uint64_t gs = blockDim.x;
+        uint64_t x = threadIdx.x;
         for (; x + (U - 1) * gs < nvec; x += U * gs) {
             uint4 q[U];
 #pragma unroll
@@ -363,9 +406,124 @@ __global__ void __launch_bounds__(kP2PThreads) k_bwd_pull_layer(DevMigArgs a, in
             for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
         }
         for (; x < nvec; x += gs) d4[x] = s4[x];
-        for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
+        for (uint64_t b = nvec * 16 + threadIdx.x; b < bytes; b += gs) dp[b] = sp[b];
+        break;
     }
-    if (gt == 0 && a.bytes_recv && recvd) atomicAdd((unsigned long long *)a.bytes_recv, recvd);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(finished, 1u);
+}
+
+// Claim-and-copy loop of one CTA over layer i.
+__device__ void pull_chunks(const DevMigArgs &a, int i, int src, uint32_t nc, uint64_t ep) {
+    __shared__ uint32_t s_c;
+    unsigned int *finished = &a.win->bwd_finished[ep & 1];
+    for (;;) {
+        if (threadIdx.x == 0) s_c = claim_chunk(&a.win->bwd_claim[i], ep, nc);
+        __syncthreads();
+        const uint32_t c = s_c;
+        __syncthreads();
+        if (c == UINT32_MAX) return;
+        copy_chunk(a, i, src, c, finished);
+    }
+}
+
+// One layer of the backward-ordered pull (side stream, SM budget).
+__global__ void __launch_bounds__(kP2PThreads) k_bwd_pull_layer(DevMigArgs a, int32_t i, uint64_t ep) {
+    __shared__ int s_ok;
+    __shared__ uint32_t s_nc;
+    if (threadIdx.x == 0) {
+        int ok = mig_args_ok(a);
+        s_nc = 0;
+        if (ok) {
+            const int src = incoming_src(a, i);
+            bool bad = false;
+            if (src >= 0) s_nc = layer_chunks(a, i, src, bad);
+            ok = !bad;
+        }
+        s_ok = ok;
+    }
+    __syncthreads();
+    if (!s_ok || s_nc == 0) return;  // errors are reported by k_bwd_done
+    pull_chunks(a, i, incoming_src(a, i), s_nc, ep);
+}
+
+// Drain (dynmo_migrate_bwd_end, every SM): the incoming layers in descending
+// order, each once its release has arrived (bounded wait), sharing the
+// chunk claims with the per-layer pulls still queued on the side stream.
+__global__ void __launch_bounds__(kP2PThreads) k_bwd_drain(DevMigArgs a, uint64_t ep) {
+    __shared__ int s_go;
+    __shared__ uint32_t s_nc;
+    __shared__ int s_src;
+    if (!mig_args_ok(a)) return;
+    for (int i = a.n_layers - 1; i >= 0; --i) {
+        if (threadIdx.x == 0) {
+            s_src = incoming_src(a, i);
+            bool bad = false;
+            s_nc = s_src >= 0 ? layer_chunks(a, i, s_src, bad) : 0u;
+            s_go = s_nc > 0 && !bad;
+            if (s_go && !wait_flag(&a.win->layer_ready[i], ep)) {
+                atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+                s_go = -1;
+            }
+        }
+        __syncthreads();
+        const int go = s_go;
+        const uint32_t nc = s_nc;
+        const int src = s_src;
+        __syncthreads();
+        if (go < 0) return;
+        if (go) pull_chunks(a, i, src, nc, ep);
+    }
+}
+
+// After the side stream's pulls: wait until every incoming chunk is copied
+// (by a pull or the drain; bounded), report the bytes and errors, reset the
+// finished counter of this epoch's parity, release done[me] everywhere.
+__global__ void k_bwd_done(DevMigArgs a, BwdPeers p, uint64_t ep) {
+    __shared__ unsigned long long s_bytes;
+    __shared__ unsigned s_total;
+    __shared__ int s_bad;
+    if (threadIdx.x == 0) {
+        s_bytes = 0ull;
+        s_total = 0u;
+        s_bad = !mig_args_ok(a);
+    }
+    __syncthreads();
+    if (!s_bad)
+        for (int i = threadIdx.x; i < a.n_layers; i += blockDim.x) {
+            const int src = incoming_src(a, i);
+            if (src < 0) continue;
+            bool bad = false;
+            const uint32_t nc = layer_chunks(a, i, src, bad);
+            if (bad) {
+                atomicExch(&s_bad, 1);
+                continue;
+            }
+            atomicAdd(&s_total, nc);
+            unsigned long long b = 0;
+            for (int k = 0; k < a.n_bufs; ++k)
+                b += (unsigned long long)a.recv_tab[(int64_t)i * a.n_bufs + k].bytes;
+            atomicAdd(&s_bytes, b);
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s_bad) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+        unsigned int *fin = &a.win->bwd_finished[ep & 1];
+        const uint64_t t0 = globaltimer();
+        while (*(volatile unsigned int *)fin < s_total) {
+            if (globaltimer() - t0 > 10ull * 1000 * 1000 * 1000) {
+                atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+                break;
+            }
+            __nanosleep(200);
+        }
+        __threadfence();
+        *fin = 0u;
+        if (a.bytes_recv) *a.bytes_recv = s_bad ? 0 : (int64_t)s_bytes;
+        __threadfence_system();
+        for (int r = 0; r < p.nranks; ++r) st_release_sys(&p.win[r]->bwd_done[a.me], ep);
+    }
 }
 
 // Sender side (at dynmo_migrate_bwd_end, after the done waits): bytes sent.
@@ -374,8 +532,7 @@ __global__ void k_bwd_sent(DevMigArgs a) {
     __shared__ int s_ok;
     if (threadIdx.x == 0) {
         s_sent = 0ull;
-        s_ok = valid_split(a.bnd_old, a.n_old, a.n_layers) && valid_split(a.bnd_new, a.n_new, a.n_layers) &&
-               ranks_ok(a.rank_old, a.n_old, a.nranks) && ranks_ok(a.rank_new, a.n_new, a.nranks);
+        s_ok = mig_args_ok(a);
     }
     __syncthreads();
     if (s_ok)
@@ -400,13 +557,18 @@ cudaError_t launch_layer_ready(const BwdPeers &p, int32_t layer, uint64_t epoch,
     return cudaGetLastError();
 }
 
-cudaError_t launch_bwd_done(const BwdPeers &p, int32_t me, uint64_t epoch, cudaStream_t s) {
-    k_bwd_done<<<1, 32, 0, s>>>(p, me, epoch);
+cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, uint64_t epoch, int grid, cudaStream_t s) {
+    k_bwd_pull_layer<<<grid, kP2PThreads, 0, s>>>(a, layer, epoch);
     return cudaGetLastError();
 }
 
-cudaError_t launch_bwd_pull_layer(const DevMigArgs &a, int32_t layer, int grid, cudaStream_t s) {
-    k_bwd_pull_layer<16><<<grid, kP2PThreads, 0, s>>>(a, layer);
+cudaError_t launch_bwd_drain(const DevMigArgs &a, uint64_t epoch, int grid, cudaStream_t s) {
+    k_bwd_drain<<<grid, kP2PThreads, 0, s>>>(a, epoch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bwd_done(const DevMigArgs &a, const BwdPeers &p, uint64_t epoch, cudaStream_t s) {
+    k_bwd_done<<<1, 256, 0, s>>>(a, p, epoch);
     return cudaGetLastError();
 }
 
@@ -436,8 +598,8 @@ cudaError_t preload_p2p_kernels() {
                         (const void *)k_pull,             (const void *)k_mig_signal,
                         (const void *)k_mig_pull<4>,      (const void *)k_mig_pull<16>,
                         (const void *)k_mig_wait,         (const void *)k_layer_ready,
-                        (const void *)k_bwd_done,         (const void *)k_bwd_pull_layer<16>,
-                        (const void *)k_bwd_sent};
+                        (const void *)k_bwd_done,         (const void *)k_bwd_pull_layer,
+                        (const void *)k_bwd_drain,        (const void *)k_bwd_sent};
     for (const void *k : ks) {
         const cudaError_t e = cudaFuncGetAttributes(&fa, k);
         if (e != cudaSuccess) return e;
