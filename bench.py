@@ -966,7 +966,9 @@ def run_pipeline(args, wl):
     # the communicator, then the peer-memory plans, then the ctx
     torch.cuda.synchronize()
     timer.copies.clear()
-    graph = None  # noqa: F841
+    if rtimer is not None:
+        rtimer.copies.clear()
+    graph = rgraph = None  # noqa: F841
     torch.cuda.synchronize()
     if pmig is not None:
         pmig.close()
@@ -1140,6 +1142,7 @@ def run_batch(args, wl):
         print(json.dumps(out), flush=True)
     torch.cuda.synchronize()
     timer.copies.clear()
+    rtimer.copies.clear()
     torch.cuda.synchronize()
     plan.close()
     ctx.close()
