@@ -1562,6 +1562,11 @@ dynmo_status bwd_args(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old, const int32_
     a.recv_tab = mp->d_recv_tab;
     a.win = ctx->d_win;
     for (int r = 0; r < ctx->nranks; ++r) a.peer_win[r] = ctx->peer_win[r];
+    static const int hint = [] {
+        const char *e = getenv("DYNMO_PULL_HINT");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    a.hint = hint;
     return DYNMO_OK;
 }
 }  // namespace
@@ -1621,7 +1626,11 @@ dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,
     DeviceGuard g(ctx->device);
     cudaStream_t s = (cudaStream_t)stream;
     // the caller's backward is done: pull what is left with every SM
-    CUDA_TRY(launch_bwd_drain(a, ctx->bwd_epoch, ctx->num_sms, s), "k_bwd_drain launch");
+    static const bool drain = [] {  // DYNMO_BWD_DRAIN=0: no drain (A/B knob)
+        const char *e = getenv("DYNMO_BWD_DRAIN");
+        return !(e && e[0] == '0');
+    }();
+    if (drain) CUDA_TRY(launch_bwd_drain(a, ctx->bwd_epoch, ctx->num_sms, s), "k_bwd_drain launch");
     for (int r = 0; r < ctx->nranks; ++r)
         if (dynmo_status st = stream_wait_geq(ctx, s, &ctx->d_win->bwd_done[r], ctx->bwd_epoch)) return st;
     if (d_bytes_sent) CUDA_TRY(launch_bwd_sent(a, s), "k_bwd_sent launch");

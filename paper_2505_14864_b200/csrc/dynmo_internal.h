@@ -327,6 +327,7 @@ struct DevMigArgs {
     PeerWindow *win;
     PeerWindow *peer_win[kMaxRanksEpi];
     int64_t *bytes_sent, *bytes_recv;  // nullable
+    int32_t hint;  // backward pulls: streaming cache hints (A/B knob DYNMO_PULL_HINT)
 };
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s);
 // NEXT-3 backward-ordered variant: per-layer ready release into every

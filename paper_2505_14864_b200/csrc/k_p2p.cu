@@ -373,6 +373,19 @@ __device__ uint32_t claim_chunk(unsigned long long *w, uint64_t ep, uint32_t nc)
     }
 }
 
+__device__ __forceinline__ uint4 ld_evict_first(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_evict_first(uint4 *p, const uint4 &v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // Copy chunk c of layer i (whole CTA, 16 x 16-byte NVLink loads in flight
 // per thread), then count it finished (after a fence: the copy is visible
 // before the counter that k_bwd_done waits on).
@@ -398,12 +411,22 @@ __device__ void copy_chunk(const DevMigArgs &a, int i, int src, uint32_t c, unsi
         uint4 *d4 = (uint4 *)dp;
         const uint64_t gs = blockDim.x;
         uint64_t x = threadIdx.x;
-        for (; x + (U - 1) * gs < nvec; x += U * gs) {
-            uint4 q[U];
+        if (a.hint) {  // streaming (.cs: evict-first) loads and stores
+            for (; x + (U - 1) * gs < nvec; x += U * gs) {
+                uint4 q[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
+                for (int u = 0; u < U; ++u) q[u] = ld_evict_first(s4 + x + u * gs);
 #pragma unroll
-            for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
+                for (int u = 0; u < U; ++u) st_evict_first(d4 + x + u * gs, q[u]);
+            }
+        } else {
+            for (; x + (U - 1) * gs < nvec; x += U * gs) {
+                uint4 q[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
+#pragma unroll
+                for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
+            }
         }
         for (; x < nvec; x += gs) d4[x] = s4[x];
         for (uint64_t b = nvec * 16 + threadIdx.x; b < bytes; b += gs) dp[b] = sp[b];
