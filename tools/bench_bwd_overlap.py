@@ -32,6 +32,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2505_14864_b200 import dynmo as D  # noqa: E402
+import bench  # noqa: E402
 
 L, LAYER_BYTES, M = 8, 128 << 20, 8192
 B_OLD, B_NEW, RANKS = [0, 6, 8], [0, 2, 8], [0, 1]
@@ -68,56 +69,76 @@ def main():
             if ready:
                 pm.layer_ready(l)
 
-    def timed(mode, reps=7, ctas=0):
-        ts = []
-        for it in range(reps + 2):
-            dist.all_reduce(bar)
-            torch.cuda.synchronize()
-            for bufs in recv.values():
-                bufs[0].zero_()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(main)
-            if mode == "overlap":
-                pm.bwd_begin()
-                side.wait_stream(main)
-                with torch.cuda.stream(side):
-                    pm.backward(d_bo, d_r, d_bn, d_r, br)
-                backward(it, True)
-                pm.bwd_end(d_bo, d_r, d_bn, d_r, bs)
-                main.wait_stream(side)
-            elif mode == "seq":
-                backward(it, False)
-                pm.device(d_bo, d_r, d_bn, d_r, bs, br)
-            else:
-                backward(it, False)
-            e1.record(main)
-            torch.cuda.synchronize()
-            if mode != "bwd":
-                for l, bufs in recv.items():
-                    v = (l * 7 + it) & 0xFF
-                    assert bool((bufs[0][:1 << 20] == v).all()) and bool((bufs[0][-(1 << 20):] == v).all()), (mode, l)
-            if it >= 2:
-                ts.append(e0.elapsed_time(e1))
-        v = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=dev)
-        dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        return round(float(v.item()), 4)
+    def one(mode, it, ctas):
+        """One iteration of `mode`; device time (CUDA events on main)."""
+        dist.all_reduce(bar)
+        torch.cuda.synchronize()
+        for bufs in recv.values():
+            bufs[0].zero_()
+        pm.set_ctas(ctas)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        if mode == "overlap":
+            pm.bwd_begin()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                pm.backward(d_bo, d_r, d_bn, d_r, br)
+            backward(it, True)
+            pm.bwd_end(d_bo, d_r, d_bn, d_r, bs)
+            main.wait_stream(side)
+        elif mode == "seq":
+            backward(it, False)
+            pm.device(d_bo, d_r, d_bn, d_r, bs, br)
+        else:
+            backward(it, False)
+        e1.record(main)
+        torch.cuda.synchronize()
+        if mode != "bwd":
+            for l, bufs in recv.items():
+                v = (l * 7 + it) & 0xFF
+                assert bool((bufs[0][:1 << 20] == v).all()) and bool((bufs[0][-(1 << 20):] == v).all()), (mode, l)
+        return e0.elapsed_time(e1)
 
+    # modes interleaved round-robin (clock / power drift hits every mode alike)
+    modes = [("bwd", "bwd", 0), ("seq", "seq", 0)] + [(f"overlap{c}", "overlap", c) for c in (32, 16, 8)]
+    REPS = 15
+    ts = {k: [] for k, _, _ in modes}
+    it = 0
+    with bench.ClockSampler(dev) as clk:
+        clk.start()
+        for rep in range(REPS + 2):
+            for key, mode, ctas in modes:
+                t = one(mode, it, ctas)
+                it += 1
+                if rep >= 2:
+                    ts[key].append(t)
+        clk.stop()
+    med = {}
+    for key in ts:
+        v = torch.tensor([float(np.median(ts[key])), float(np.percentile(ts[key], 25)),
+                          float(np.percentile(ts[key], 75))], dtype=torch.float64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        med[key] = [round(float(x), 4) for x in v.tolist()]
     out = {"workload": "2 GPUs: layers 2..5 of 8 (4 x 128 MiB = 512 MiB) GPU0 -> GPU1 during a backward stand-in "
                        f"(per layer, last first: one bf16 GEMM {M}^3, the gradient write, the ready flag); "
-                       "CUDA events, median of 7, max over ranks; every run byte-exact",
-           "bwd_alone_ms": timed("bwd")}
-    pm.set_ctas(0)
-    out["seq_ms"] = timed("seq")
+                       f"CUDA events, {REPS} reps per mode interleaved round-robin, median [p25, p75] per rank, "
+                       "max over ranks; every run byte-exact",
+           "bwd_alone_ms": med["bwd"][0], "seq_ms": med["seq"][0]}
     out["mig_alone_ms_est"] = round(out["seq_ms"] - out["bwd_alone_ms"], 4)
     rows = []
-    for ctas in (32, 16, 8):
-        pm.set_ctas(ctas)
-        t = timed("overlap", ctas=ctas)
-        rows.append({"ctas": ctas, "overlap_ms": t, "vs_bwd_alone": round(t / out["bwd_alone_ms"], 3),
+    for c in (32, 16, 8):
+        t = med[f"overlap{c}"][0]
+        rows.append({"ctas": c, "overlap_ms": t, "p25_p75": med[f"overlap{c}"][1:],
+                     "vs_bwd_alone": round(t / out["bwd_alone_ms"], 3),
                      "hidden_frac": round((out["seq_ms"] - t) / max(out["mig_alone_ms_est"], 1e-9), 3)})
     out["overlap"] = rows
+    out["bwd_p25_p75"] = med["bwd"][1:]
+    out["seq_p25_p75"] = med["seq"][1:]
     out["sms"] = sms
+    out["clocks_rank%d" % rank] = clk.summary()
+    out["drain"] = os.environ.get("DYNMO_BWD_DRAIN", "1") != "0"
+    out["pull_hint"] = os.environ.get("DYNMO_PULL_HINT", "0") == "1"
     assert pm.error() == 0
     if rank == 0:
         print(json.dumps(out), flush=True)
