@@ -46,7 +46,7 @@ for x in insts:
 p5 = D.ProfilePlan(ctx, segs5, 0, lay)
 c5, _, s5 = D.profile_layers(ctx, p5, D.coef_tensor(lay, A=1, device=dev))
 # solvers: small and large batches (1-warp and 8-warp variants), mem and no mem
-for n_inst in (3, 700):
+for n_inst in ((3, 40) if os.environ.get("DYNMO_SANITIZE_SMALL") == "1" else (3, 700)):
     Ls = g.integers(2, 130, n_inst); ns = [int(g.integers(1, min(8, l) + 1)) for l in Ls]
     b = D.Batch(Ls, ns, device=dev)
     cost_b = torch.from_numpy(g.integers(0, 1000, int(Ls.sum()))).to(dev)
