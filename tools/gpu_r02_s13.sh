@@ -1,7 +1,5 @@
 #!/bin/bash
 # 4 GPUs: bench configs 2-5 at N = 4.
-# (memcheck on the mixed-source + solver run; racecheck / synccheck on its
-# small variant), each bounded.
 mkdir -p gpurun_out
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29624"
 for c in 2 3 4 5; do
