@@ -383,6 +383,51 @@ def main():
         for l, bufs in recvb.items():
             assert bool((bufs[0] == grad_val(l, it)).all()), (rank, it, l, "bwd grads")
             assert torch.equal(bufs[1].cpu(), pattern(l, int(payload[l]) // 2 + 1)), (rank, it, l, "bwd params")
+    # multi-chunk payloads (the pulls claim 256 KiB chunks shared with the
+    # drain of dynmo_migrate_bwd_end): per layer an odd-sized 0.8 MB buffer,
+    # an unaligned view (byte copies) and an empty buffer; some iterations
+    # issue bwd_end only after a host delay so the budgeted per-layer pulls
+    # copy most chunks, others right away so the drain takes them over
+    def big(l, it):
+        g2 = np.random.default_rng(50_000 + 97 * l + it)
+        return torch.from_numpy(g2.integers(0, 256, 3 * (256 << 10) + 17 + 4099 * l, dtype=np.uint8))
+    sendc = {l: [torch.zeros(3 * (256 << 10) + 17 + 4099 * l, dtype=torch.uint8, device=dev),
+                 torch.zeros(70001 + l, dtype=torch.uint8, device=dev)[1:],
+                 torch.zeros(0, dtype=torch.uint8, device=dev)]
+             for l in range(begin, begin + count)}
+    recvc = {int(l): [torch.zeros(3 * (256 << 10) + 17 + 4099 * int(l), dtype=torch.uint8, device=dev),
+                      torch.zeros(70001 + int(l), dtype=torch.uint8, device=dev)[1:],
+                      torch.zeros(0, dtype=torch.uint8, device=dev)]
+             for l, s_, d_ in moves if d_ == rank}
+    pmc = D.PeerMigrator(ctx, shape.L, sendc, recvc, n_bufs=3)
+    pmc.set_ctas(4)
+    for it in range(6):
+        main = torch.cuda.current_stream()
+        for bufs in recvc.values():
+            bufs[0].zero_()
+            bufs[1].zero_()
+        pmc.bwd_begin()
+        side_b.wait_stream(main)
+        with torch.cuda.stream(side_b):
+            pmc.backward(d_bo, d_ro, bnd, d_rn, br)
+        for l in range(begin + count - 1, begin - 1, -1):
+            Ab = (Ab @ Ab).clamp_(-1, 1)
+            sendc[l][0].copy_(big(l, it).to(dev))
+            sendc[l][1].fill_(grad_val(l, it))
+            pmc.layer_ready(l)
+        if it % 2:
+            torch.cuda._sleep(2_000_000)  # ~1 ms: the budgeted pulls run first
+        pmc.bwd_end(d_bo, d_ro, bnd, d_rn, bs)
+        main.wait_stream(side_b)
+        torch.cuda.synchronize()
+        assert pmc.error() == 0, (rank, it, pmc.error())
+        nb = lambda l: 3 * (256 << 10) + 17 + 4099 * int(l) + 70000 + int(l)  # noqa: E731
+        assert (int(bs.item()), int(br.item())) == (sum(nb(l) for l, s_, _ in moves if s_ == rank),
+                                                    sum(nb(l) for l, _, d_ in moves if d_ == rank)), (rank, it, "chunks")
+        for l, bufs in recvc.items():
+            assert torch.equal(bufs[0].cpu(), big(l, it)), (rank, it, l, "chunked big")
+            assert bool((bufs[1] == grad_val(l, it)).all()), (rank, it, l, "chunked unaligned")
+    pmc.close()
     pmb.set_ctas(0)
     try:
         pmb.backward(d_bo, d_ro, bnd, d_rn, br)  # no SM budget: refused on the host
