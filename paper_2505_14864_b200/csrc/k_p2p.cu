@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "dynmo_internal.h"
 
@@ -289,6 +290,119 @@ __global__ void k_mig_wait(DevMigArgs a) {
         for (int r = 0; r < a.nranks; ++r)
             if (v.receivers & (1u << r))
                 if (!wait_flag(&a.win->ddone[r], epoch)) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+    }
+}
+
+// One-kernel device-driven migration (the three kernels above fused: one
+// launch on the step's critical path instead of three).  Every block derives
+// the moves from the device boundaries; block 0 releases dready[me] at this
+// rank's receivers (this call's epoch = the window's + 1, written back by the
+// last block); every block waits for its senders and copies its grid-stride
+// share; the last block to finish releases ddone[me] at the senders, then
+// waits (bounded) for every receiver's ddone -- releases always precede
+// waits in every rank's last block, so the ranks cannot wait on each other
+// in a cycle -- and only then lets the stream reuse the sent buffers.
+template <int U>
+__global__ void __launch_bounds__(kP2PThreads) k_mig_fused(DevMigArgs a) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ MigView v;
+    __shared__ int16_t in_layers[1024];
+    __shared__ int8_t in_src[1024];
+    __shared__ int s_ok;
+    __shared__ bool s_last;
+    mig_view(a, v, in_layers, in_src);
+    const uint64_t epoch = a.win->mig_dev_epoch + 1;
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            if (!v.ok) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+            else if (v.receivers) {
+                __threadfence_system();  // the payload written by earlier stream work
+                for (int r = 0; r < a.nranks; ++r)
+                    if (v.receivers & (1u << r)) st_release_sys(&a.peer_win[r]->dready[a.me], epoch);
+            }
+        }
+        int ok = v.ok;
+        for (int r = 0; ok && r < a.nranks; ++r)
+            if (v.senders & (1u << r)) ok &= wait_flag(&a.win->dready[r], epoch);
+        if (!ok && v.ok) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+        s_ok = ok;
+    }
+    __syncthreads();
+    const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t gs = (uint64_t)gridDim.x * blockDim.x;
+    unsigned long long recvd = 0;
+    if (s_ok) {
+        for (int it = 0; it < v.n_in; ++it) {
+            const int i = in_layers[it], src = in_src[it];
+            for (int k = 0; k < a.n_bufs; ++k) {
+                const int64_t idx = (int64_t)i * a.n_bufs + k;
+                const DevBuf sb = a.src_tab[((int64_t)src * a.n_layers) * a.n_bufs + idx];
+                const DevBuf rb = a.recv_tab[idx];
+                if (sb.bytes != rb.bytes || (sb.bytes > 0 && (!sb.ptr || !rb.ptr))) {
+                    if (gt == 0) atomicExch(&a.win->err, (int)DYNMO_E_INVALID);
+                    continue;
+                }
+                const uint64_t bytes = (uint64_t)sb.bytes;
+                recvd += bytes;
+                const uint8_t *sp = (const uint8_t *)sb.ptr;
+                uint8_t *dp = (uint8_t *)rb.ptr;
+                const bool vec = (((uintptr_t)sp | (uintptr_t)dp) & 15) == 0;
+                const uint64_t nvec = vec ? bytes >> 4 : 0;
+                const uint4 *s4 = (const uint4 *)sp;
+                uint4 *d4 = (uint4 *)dp;
+                uint64_t x = gt;
+                for (; x + (U - 1) * gs < nvec; x += U * gs) {
+                    uint4 q[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) q[u] = s4[x + u * gs];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) d4[x + u * gs] = q[u];
+                }
+                for (; x < nvec; x += gs) d4[x] = s4[x];
+                for (uint64_t b = nvec * 16 + gt; b < bytes; b += gs) dp[b] = sp[b];
+            }
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0 && a.bytes_recv) *a.bytes_recv = (int64_t)recvd;
+        const unsigned prev = atomicAdd(&a.win->dpull_ctr, 1u);
+        s_last = prev == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // the last block: done at the senders, then this rank's receivers, then
+    // the bytes this rank sent and the epoch for the next call
+    __shared__ unsigned long long s_sent;
+    if (threadIdx.x == 0) {
+        a.win->dpull_ctr = 0u;
+        s_sent = 0ull;
+        __threadfence_system();
+        for (int r = 0; r < a.nranks; ++r)
+            if (v.senders & (1u << r)) st_release_sys(&a.peer_win[r]->ddone[a.me], epoch);
+        if (v.ok)
+            for (int r = 0; r < a.nranks; ++r)
+                if (v.receivers & (1u << r))
+                    if (!wait_flag(&a.win->ddone[r], epoch)) atomicExch(&a.win->err, (int)DYNMO_E_NCCL);
+    }
+    __syncthreads();
+    if (v.ok)
+        for (int i = threadIdx.x; i < a.n_layers; i += blockDim.x) {
+            const int src = a.rank_old[stage_of(a.bnd_old, a.n_old, i)];
+            const int dst = a.rank_new[stage_of(a.bnd_new, a.n_new, i)];
+            if (src == a.me && dst != a.me) {
+                unsigned long long b = 0;
+                const DevBuf *row = a.src_tab + ((int64_t)a.me * a.n_layers + i) * a.n_bufs;
+                for (int k = 0; k < a.n_bufs; ++k) b += (unsigned long long)row[k].bytes;
+                atomicAdd(&s_sent, b);
+            }
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.bytes_sent) *a.bytes_sent = (int64_t)s_sent;
+        a.win->mig_dev_epoch = epoch;
     }
 }
 
@@ -601,6 +715,15 @@ cudaError_t launch_bwd_sent(const DevMigArgs &a, cudaStream_t s) {
 }
 
 cudaError_t launch_mig_dev(const DevMigArgs &a, int grid, bool budget, cudaStream_t s) {
+    static const bool fused = [] {  // DYNMO_MIG_FUSED=0: the three-kernel path (A/B knob)
+        const char *e = getenv("DYNMO_MIG_FUSED");
+        return !(e && e[0] == '0');
+    }();
+    if (fused) {
+        const cudaError_t f = budget ? launch_pdl(k_mig_fused<16>, grid, kP2PThreads, 0, s, a)
+                                     : launch_pdl(k_mig_fused<4>, grid, kP2PThreads, 0, s, a);
+        return f != cudaSuccess ? f : cudaGetLastError();
+    }
     cudaError_t e = launch_pdl(k_mig_signal, 1, 256, 0, s, a);
     if (e == cudaSuccess)
         e = budget ? launch_pdl(k_mig_pull<16>, grid, kP2PThreads, 0, s, a)
@@ -622,7 +745,8 @@ cudaError_t preload_p2p_kernels() {
                         (const void *)k_mig_pull<4>,      (const void *)k_mig_pull<16>,
                         (const void *)k_mig_wait,         (const void *)k_layer_ready,
                         (const void *)k_bwd_done,         (const void *)k_bwd_pull_layer,
-                        (const void *)k_bwd_drain,        (const void *)k_bwd_sent};
+                        (const void *)k_bwd_drain,        (const void *)k_bwd_sent,
+                        (const void *)k_mig_fused<4>,     (const void *)k_mig_fused<16>};
     for (const void *k : ks) {
         const cudaError_t e = cudaFuncGetAttributes(&fa, k);
         if (e != cudaSuccess) return e;
