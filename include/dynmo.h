@@ -472,7 +472,11 @@ dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
  * Errors: a malformed split or rank map, or mismatched buffer sizes, set the
  * ctx's sticky error word (DYNMO_E_INVALID, dynmo_ctx_p2p_error) and move
  * nothing; the handshake still completes.  The waits are unbounded (like a
- * NCCL collective): a rank that skips a call blocks its peers' streams.
+ * NCCL collective): a rank that skips a call blocks its peers' streams, and
+ * between bwd_begin and its last layer_ready a rank's host must not wait on
+ * the device (cudaDeviceSynchronize, synchronous copies, a first launch
+ * that lazily loads a module): its peers' streams may be waiting for the
+ * releases it has not issued yet while its own side stream waits for theirs.
  * Host epochs are baked into the stream operations, so these calls are
  * issued eagerly each iteration (not replayed from a captured graph). */
 dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan plan, dynmo_stream stream);

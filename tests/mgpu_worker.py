@@ -36,6 +36,9 @@ def pattern(layer: int, nbytes: int) -> torch.Tensor:
 
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+
+    def trace(msg):  # section markers (the test keeps the output even on a timeout)
+        print(f"TRACE {rank} {msg}", flush=True)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -86,6 +89,7 @@ def main():
     allb = [None] * world
     dist.all_gather_object(allb, b_new.tolist())
     assert all(x == allb[0] for x in allb)
+    trace('migration')
     # migration: senders hold the pattern, receivers get it
     send = {l: [pattern(l, int(payload[l])).to(dev)] for l in range(begin, begin + count)}
     moves = oracle.moves(shape.L, b_old, ranks, b_new, ranks)
@@ -106,6 +110,7 @@ def main():
     torch.cuda.synchronize()
     for l, bufs in recv.items():
         assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l])))
+    trace('the same moves over NVLink peer memory (')
     # the same moves over NVLink peer memory (IPC-mapped pull kernel)
     for bufs in recv.values():
         bufs[0].zero_()
@@ -118,6 +123,7 @@ def main():
         assert (s2, g2) == (want_sent, want_got), (rank, s2, g2)
         for l, bufs in recv.items():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, rep)
+    trace('device-driven variant')
     # device-driven variant: boundaries straight from the partition output,
     # captured in a CUDA graph together with the partition (several replays)
     d_bo, d_ro = torch.from_numpy(b_old.astype(np.int32)).to(dev), torch.from_numpy(ranks.astype(np.int32)).to(dev)
@@ -141,6 +147,7 @@ def main():
         torch.cuda.synchronize()
         for l, bufs in recv.items():
             assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "graph", rep)
+    trace('NEXT-3 overlap')
     # NEXT-3 overlap: the pull under a 2-CTA SM budget on a side stream while
     # the main stream runs a GEMM (the backward stand-in): byte-exact
     pm.set_ctas(2)
@@ -161,6 +168,7 @@ def main():
     pm.set_ctas(0)
     assert pm.error() == 0
     pm.close()
+    trace('NEXT-3 placement')
     # NEXT-3 placement: the new stages on capacity slots (slot j on GPU
     # ranks[j]) keeping the most payload in place; the device-driven pull
     # follows the mapped ranks (a non-identity stage -> rank map)
@@ -181,6 +189,7 @@ def main():
         assert torch.equal(bufs[0].cpu(), pattern(l, int(payload[l]))), (rank, l, "mapped")
     assert pm2.error() == 0
     pm2.close()
+    trace('ranks without layers (more GPUs than lay')
     # ranks without layers (more GPUs than layers): 2 layers over `world`
     # ranks, ranks >= 2 hold empty slices; the peer-memory and NCCL exchanges
     # still give every rank the full cost vector
@@ -198,6 +207,7 @@ def main():
             torch.cuda.synchronize()
             assert int(st0.item()) == 0 and c0.cpu().tolist() == [1000, 1017], (rank, mode0, c0.cpu().tolist())
         plan0.close()
+    trace('several buffers per layer (a CSR payload')
     # several buffers per layer (a CSR payload is values, indices and
     # optimizer state): 3 buffers of different sizes and dtypes per layer,
     # through NCCL send/recv, the host-driven and the device-driven pull
@@ -231,6 +241,7 @@ def main():
         for l, bufs in recv3.items():
             for t, w in zip(bufs, bufs_of(l)):
                 assert torch.equal(t.cpu(), w), (rank, mode, l)
+    trace('Alg. 1 global pruning across ranks (NCCL')
     # Alg. 1 global pruning across ranks (NCCL all-reduce of the histograms,
     # all-gather of the tie counts): every rank's masks == the oracle's on the
     # concatenation of all ranks' shards in rank order; quantised magnitudes
@@ -338,6 +349,7 @@ def main():
         if rank != world - 1:
             assert np.array_equal(mk.cpu().numpy(), om[rank]), (rank, kk, "empty rank")
     pplan.close()
+    trace('NEXT-3 (P')
     # NEXT-3: migration overlapped with the backward pass, last
     # layer first.  Payload per layer = [gradients, params]; the "backward"
     # on the main stream computes (a GEMM stand-in), writes each owned
@@ -383,6 +395,7 @@ def main():
         for l, bufs in recvb.items():
             assert bool((bufs[0] == grad_val(l, it)).all()), (rank, it, l, "bwd grads")
             assert torch.equal(bufs[1].cpu(), pattern(l, int(payload[l]) // 2 + 1)), (rank, it, l, "bwd params")
+    trace('multi-chunk payloads (the pulls claim 25')
     # multi-chunk payloads (the pulls claim 256 KiB chunks shared with the
     # drain of dynmo_migrate_bwd_end): per layer an odd-sized 0.8 MB buffer,
     # an unaligned view (byte copies) and an empty buffer; some iterations
@@ -401,6 +414,11 @@ def main():
              for l, s_, d_ in moves if d_ == rank}
     pmc = D.PeerMigrator(ctx, shape.L, sendc, recvc, n_bufs=3)
     pmc.set_ctas(4)
+    # this iteration's payloads staged on the device beforehand: between
+    # bwd_begin and the last layer_ready the host must not wait on the device
+    # (peers' streams wait for this rank's releases, as in a collective)
+    bigs = {(l, it): big(l, it).to(dev) for l in range(begin, begin + count) for it in range(6)}
+    torch.cuda.synchronize()
     for it in range(6):
         main = torch.cuda.current_stream()
         for bufs in recvc.values():
@@ -412,7 +430,7 @@ def main():
             pmc.backward(d_bo, d_ro, bnd, d_rn, br)
         for l in range(begin + count - 1, begin - 1, -1):
             Ab = (Ab @ Ab).clamp_(-1, 1)
-            sendc[l][0].copy_(big(l, it).to(dev))
+            sendc[l][0].copy_(bigs[(l, it)])
             sendc[l][1].fill_(grad_val(l, it))
             pmc.layer_ready(l)
         if it % 2:
@@ -436,6 +454,7 @@ def main():
         raised = True
     assert raised
     pmb.close()
+    trace('ADVICE r1 (high)')
     # the host-driven pull with a CHANGING set of ranks
     # that move data between calls (some ranks sit calls out).  Epochs are
     # per directed rank pair, so every call is exact whatever the history.
@@ -464,6 +483,7 @@ def main():
                 assert torch.equal(recv_all[int(l)][0].cpu(), pattern(int(l), int(payload[l]))), (rank, it, int(l))
     assert pmx.error() == 0
     pmx.close()
+    trace('ADVICE r1 (medium)')
     # a plan-creation failure on ONE rank fails the
     # collective plan creation on EVERY rank instead of leaving the others in
     # the setup all-gather
@@ -489,6 +509,7 @@ def main():
     torch.cuda.synchronize()
     assert int(st_ok.item()) == 0 and np.array_equal(c_ok.cpu().numpy(), want_cost)
     plan_ok.close()
+    trace('ADVICE r1 (medium)')
     # a stage -> rank entry outside [0, nranks) (the -1 a
     # failed map_stages writes) moves nothing and reports INVALID on every
     # rank -- no out-of-bounds table read, no hang.  Last: the error is sticky.
@@ -502,6 +523,7 @@ def main():
     assert pmb.error() == LB.E_INVALID, (rank, pmb.error())
     assert all(bool((t[0] == 7).all()) for t in recv_all.values()), rank
     pmb.close()
+    trace('Releasing GPUs after re-packing (P')
     # Releasing GPUs after re-packing: split the ctx -- even
     # ranks stay active, odd ranks are released (None) -- then the smaller
     # group profiles, partitions and maps its stages onto its own ranks
