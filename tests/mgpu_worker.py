@@ -413,12 +413,14 @@ def main():
                       torch.zeros(0, dtype=torch.uint8, device=dev)]
              for l, s_, d_ in moves if d_ == rank}
     pmc = D.PeerMigrator(ctx, shape.L, sendc, recvc, n_bufs=3)
+    trace("chunks: plan")
     pmc.set_ctas(4)
     # this iteration's payloads staged on the device beforehand: between
     # bwd_begin and the last layer_ready the host must not wait on the device
     # (peers' streams wait for this rank's releases, as in a collective)
     bigs = {(l, it): big(l, it).to(dev) for l in range(begin, begin + count) for it in range(6)}
     torch.cuda.synchronize()
+    trace("chunks: staged")
     for it in range(6):
         main = torch.cuda.current_stream()
         for bufs in recvc.values():
@@ -433,11 +435,14 @@ def main():
             sendc[l][0].copy_(bigs[(l, it)])
             sendc[l][1].fill_(grad_val(l, it))
             pmc.layer_ready(l)
+        trace(f"chunks: it {it} released")
         if it % 2:
             torch.cuda._sleep(2_000_000)  # ~1 ms: the budgeted pulls run first
         pmc.bwd_end(d_bo, d_ro, bnd, d_rn, bs)
+        trace(f"chunks: it {it} end issued")
         main.wait_stream(side_b)
         torch.cuda.synchronize()
+        trace(f"chunks: it {it} synced err={pmc.error()}")
         assert pmc.error() == 0, (rank, it, pmc.error())
         nb = lambda l: 3 * (256 << 10) + 17 + 4099 * int(l) + 70000 + int(l)  # noqa: E731
         assert (int(bs.item()), int(br.item())) == (sum(nb(l) for l, s_, _ in moves if s_ == rank),
