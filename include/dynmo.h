@@ -132,6 +132,13 @@ dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total
  * accumulator.  Returns (and resets) the accumulated milliseconds and
  * launch count; synchronous. */
 dynmo_status dynmo_ctx_profile_span(dynmo_ctx ctx, double *h_total_ms, int64_t *h_count);
+/* Hang analysis: a snapshot of this rank's peer window, copied on a private
+ * non-blocking stream (so it completes while the ctx's other streams wait):
+ * h_out[0] sticky error, [1] device-migration epoch, [2] exchange epoch,
+ * [3..19) backward done words, [19..21) chunks finished (epoch parities),
+ * [21..21+n) layer release words, [21+n..21+2n) chunk claim words
+ * (n = min(n_layers, 1024)).  INVALID if n_words < 21 + 2n. */
+dynmo_status dynmo_ctx_window_snapshot(dynmo_ctx ctx, int32_t n_layers, uint64_t *h_out, int64_t n_words);
 
 /* ----------------------------------------------------------- profiling --
  * Sources of per-layer workload (P:L234-239 pruning p_i, P:L266-283 freezing

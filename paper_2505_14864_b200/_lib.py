@@ -97,6 +97,7 @@ def lib():
         "dynmo_migrate_layers_bwd": (i32, [p, p, i32, p, p, i32, p, p, p, p]),
         "dynmo_migrate_bwd_end": (i32, [p, p, i32, p, p, i32, p, p, p, p]),
         "dynmo_ctx_profile_span": (i32, [p, p, p]),
+        "dynmo_ctx_window_snapshot": (i32, [p, i32, p, C.c_int64]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -118,4 +119,5 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_migrate_plan_destroy", "dynmo_migrate_layers_p2p", "dynmo_ctx_p2p_error",
             "dynmo_migrate_layers_dev", "dynmo_migrate_plan_set_ctas",
             "dynmo_migrate_bwd_begin", "dynmo_migrate_layer_ready", "dynmo_migrate_layers_bwd",
-            "dynmo_migrate_bwd_end", "dynmo_ctx_profile_span"]
+            "dynmo_migrate_bwd_end", "dynmo_ctx_profile_span",
+            "dynmo_ctx_window_snapshot"]

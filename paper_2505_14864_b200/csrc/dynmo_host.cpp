@@ -1733,6 +1733,35 @@ dynmo_status dynmo_migrate_layers_p2p(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_o
     return DYNMO_OK;
 }
 
+// Diagnostics: a snapshot of this rank's peer window (hang analysis).  Copies
+// on a private non-blocking stream, so it completes while other streams of
+// the ctx wait.  Words: [0] err, [1] mig_dev_epoch, [2] exch_epoch,
+// [3..3+16) bwd_done, [19..21) bwd_finished, [21..21+n) layer_ready,
+// then n claim words (n = min(n_layers, 1024)).
+dynmo_status dynmo_ctx_window_snapshot(dynmo_ctx ctx, int32_t n_layers, uint64_t *h_out, int64_t n_words) {
+    if (!ctx || !h_out || n_layers < 0) return invalid("null ctx/out");
+    const int n = std::min(n_layers, 1024);
+    if (n_words < 21 + 2 * (int64_t)n) return invalid("snapshot buffer too small");
+    DeviceGuard g(ctx->device);
+    std::vector<char> w(sizeof(PeerWindow));
+    cudaStream_t s;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "snapshot stream");
+    cudaError_t e = cudaMemcpyAsync(w.data(), ctx->d_win, sizeof(PeerWindow), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return cuda_fail(e, "window snapshot");
+    const PeerWindow *pw = (const PeerWindow *)w.data();
+    h_out[0] = (uint64_t)(int64_t)pw->err;
+    h_out[1] = pw->mig_dev_epoch;
+    h_out[2] = pw->exch_epoch;
+    for (int r = 0; r < 16; ++r) h_out[3 + r] = pw->bwd_done[r];
+    h_out[19] = pw->bwd_finished[0];
+    h_out[20] = pw->bwd_finished[1];
+    for (int i = 0; i < n; ++i) h_out[21 + i] = pw->layer_ready[i];
+    for (int i = 0; i < n; ++i) h_out[21 + n + i] = pw->bwd_claim[i];
+    return DYNMO_OK;
+}
+
 dynmo_status dynmo_ctx_profile_span(dynmo_ctx ctx, double *h_total_ms, int64_t *h_count) {
     if (!ctx || !h_total_ms || !h_count) return invalid("null ctx/out");
     DeviceGuard g(ctx->device);

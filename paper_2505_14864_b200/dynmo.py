@@ -138,6 +138,17 @@ class Context:
             out[name] = (ms.value, cnt.value)
         return out
 
+    def window_snapshot(self, n_layers: int) -> dict:
+        """dynmo_ctx_window_snapshot: this rank's peer-window words (hang
+        analysis; completes while the ctx's streams wait)."""
+        n = min(int(n_layers), 1024)
+        buf = (C.c_uint64 * (21 + 2 * n))()
+        _check(lib().dynmo_ctx_window_snapshot(self._h, n, buf, 21 + 2 * n), "dynmo_ctx_window_snapshot")
+        v = list(buf)
+        return {"err": C.c_int64(v[0]).value, "mig_dev_epoch": v[1], "exch_epoch": v[2], "bwd_done": v[3:19],
+                "bwd_finished": v[19:21], "layer_ready": v[21:21 + n],
+                "claim": [(x >> 32, x & 0xFFFFFFFF) for x in v[21 + n:21 + 2 * n]]}
+
     def profile_span(self):
         """(total_ms, launches) of k_profile's own device-clock span since the
         last call (profile-phase timing on); synchronous."""

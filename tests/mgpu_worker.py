@@ -39,6 +39,22 @@ def main():
 
     def trace(msg):  # section markers (the test keeps the output even on a timeout)
         print(f"TRACE {rank} {msg}", flush=True)
+
+    import threading
+
+    def watchdog(seconds, tag, streams=()):
+        """Prints this rank's peer-window snapshot and its streams' states if
+        the section has not finished within `seconds` (hang analysis)."""
+        def fire():
+            try:
+                print(f"WATCHDOG {rank} {tag} streams_idle={[s_.query() for s_ in streams]} "
+                      f"window={ctx.window_snapshot(shape.L)}", flush=True)
+            except Exception as e:  # pragma: no cover
+                print(f"WATCHDOG {rank} {tag} failed: {e!r}", flush=True)
+        t = threading.Timer(seconds, fire)
+        t.daemon = True
+        t.start()
+        return t
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -423,6 +439,7 @@ def main():
     trace("chunks: staged")
     for it in range(6):
         main = torch.cuda.current_stream()
+        wd = watchdog(30.0, f"chunks it {it}", (main, side_b))
         for bufs in recvc.values():
             bufs[0].zero_()
             bufs[1].zero_()
@@ -442,6 +459,7 @@ def main():
         trace(f"chunks: it {it} end issued")
         main.wait_stream(side_b)
         torch.cuda.synchronize()
+        wd.cancel()
         trace(f"chunks: it {it} synced err={pmc.error()}")
         assert pmc.error() == 0, (rank, it, pmc.error())
         nb = lambda l: 3 * (256 << 10) + 17 + 4099 * int(l) + 70000 + int(l)  # noqa: E731
