@@ -482,8 +482,15 @@ dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas);
  * NCCL collective): a rank that skips a call blocks its peers' streams, and
  * between bwd_begin and its last layer_ready a rank's host must not wait on
  * the device (cudaDeviceSynchronize, synchronous copies, a first launch
- * that lazily loads a module): its peers' streams may be waiting for the
- * releases it has not issued yet while its own side stream waits for theirs.
+ * that lazily loads a module): its side stream already waits for releases
+ * its own stream has not executed yet, and its peers' streams for its
+ * releases.  With the default CUDA_MODULE_LOADING=LAZY, every kernel the
+ * backward launches in that window must have run once before (a warm-up
+ * iteration; note that e.g. a fill of an unaligned view is a different
+ * kernel from the aligned one), or the process sets
+ * CUDA_MODULE_LOADING=EAGER.  The library loads its own kernels when the
+ * ctx is created.  dynmo_ctx_window_snapshot shows which release or done
+ * word a hung rank is waiting for.
  * Host epochs are baked into the stream operations, so these calls are
  * issued eagerly each iteration (not replayed from a captured graph). */
 dynmo_status dynmo_migrate_bwd_begin(dynmo_ctx ctx, dynmo_mplan plan, dynmo_stream stream);

@@ -435,6 +435,14 @@ def main():
     # bwd_begin and the last layer_ready the host must not wait on the device
     # (peers' streams wait for this rank's releases, as in a collective)
     bigs = {(l, it): big(l, it).to(dev) for l in range(begin, begin + count) for it in range(6)}
+    # warm-up of every kernel the loop launches between bwd_begin and the last
+    # layer_ready (the fill of an UNALIGNED view is its own kernel): a first
+    # launch there may lazily load a module, which waits for the context to
+    # go idle while the side stream waits for this rank's later releases
+    for l in range(begin, begin + count):
+        sendc[l][0].copy_(bigs[(l, 0)])
+        sendc[l][1].fill_(1)
+    torch.cuda._sleep(1000)
     torch.cuda.synchronize()
     trace("chunks: staged")
     for it in range(6):
