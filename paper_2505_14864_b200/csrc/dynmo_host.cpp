@@ -1050,6 +1050,10 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     ea.ws_status = plan->d_ws_status;
     ea.ws_done = plan->d_ws_done;
     ea.status_out = d_status;
+    static const bool fuse_exch = [] {  // DYNMO_EXCH_FUSED=0: separate k_unpack_p2p (A/B knob)
+        const char *e = getenv("DYNMO_EXCH_FUSED");
+        return !(e && e[0] == '0');
+    }();
     if (plan->exchange == 1) {
         ea.p2p = 1;
         ea.rank = ctx->rank;
@@ -1059,11 +1063,17 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
             ea.peer_slots[r] = plan->peer_slots[r];
             ea.peer_win[r] = ctx->peer_win[r];
         }
+        ea.fuse_unpack = fuse_exch;
+        ea.p2p_slots = plan->d_p2p_slots;
+        ea.decoded = plan->d_slot_recv;
+        ea.x_cost = d_cost;
+        ea.x_mem = d_mem;
+        ea.x_status = d_status;
     }
     te = phase_begin(ctx, DYNMO_PHASE_EPILOGUE, s);
     CUDA_TRY(launch_epilogue(ea, s), "k_epilogue launch");
     phase_end(te, s);
-    if (plan->exchange == 1) {
+    if (plan->exchange == 1 && !fuse_exch) {
         te = phase_begin(ctx, DYNMO_PHASE_EXCHANGE, s);
         CUDA_TRY(launch_unpack_p2p(plan->d_p2p_slots, ctx->d_win, ctx->nranks, plan->n_total, plan->d_slot_recv, d_cost, d_mem,
                                    d_status, s),

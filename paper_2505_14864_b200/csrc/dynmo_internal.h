@@ -163,6 +163,12 @@ struct EpiArgs {
     unsigned int *ws_done;
     int32_t *status_out;     // local mode final status
     unsigned long long *span;  // nullable: [0] ~start, [1] end of k_profile, [2] sum of spans (ns), [3] launches
+    // peer-memory exchange fused into the last block (p2p && fuse_unpack):
+    // this rank's receive area, the decode buffer, the global outputs
+    int32_t fuse_unpack;
+    const int64_t *p2p_slots;
+    int64_t *decoded, *x_cost, *x_mem;
+    int32_t *x_status;
 };
 
 // ops: bit 0 count ops, bit 1 exit histogram, bit 2 expert histograms

@@ -616,6 +616,9 @@ __device__ __forceinline__ bool ll_poll(const uint64_t *p, uint64_t epoch, uint6
     }
 }
 
+__device__ void unpack_p2p_dev(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
+                               int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out);
+
 __global__ void k_epilogue(EpiArgs a) {
     pdl_wait();
     pdl_trigger();
@@ -760,6 +763,10 @@ __global__ void k_epilogue(EpiArgs a) {
                 *a.status_out = fin;
             }
         }
+        if (a.p2p && a.fuse_unpack) {  // the exchange in this block: no extra launch
+            __syncthreads();  // exch_epoch written by thread 0
+            unpack_p2p_dev(a.p2p_slots, a.win, a.nranks, a.n_total, a.decoded, a.x_cost, a.x_mem, a.x_status);
+        }
     }
 }
 
@@ -826,6 +833,14 @@ __global__ void k_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nran
                              int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
     pdl_wait();
     pdl_trigger();
+    unpack_p2p_dev(slots, win, nranks, n_total, decoded, cost_out, mem_out, status_out);
+}
+
+// Polls every rank's LL slot words of this epoch (bounded), decodes them and
+// scatters the global vectors (one block; also the tail of the epilogue's
+// last block when the exchange is fused into it).
+__device__ void unpack_p2p_dev(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
+                               int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out) {
     __shared__ int s_ok;
     __shared__ int64_t s_hdr[3];
     const uint64_t epoch = win->exch_epoch;  // advanced by this rank's epilogue
