@@ -348,6 +348,40 @@ def test_partition_repack_threshold_sizes(D, ctx, count):
             assert np.array_equal(bnds[q][:x["n"] + 1], ob), (q, with_mem)
 
 
+@pytest.mark.parametrize("count", [60, 700])  # 8-warp latency mode / 1-warp batched mode (> 592)
+def test_search_paths_32_64_bit_and_counts(D, ctx, count):
+    """The round-2 search (one candidate per thread) switches on the data:
+    32-bit prefix sums when the total cost C < 2^31 (64-bit otherwise), the
+    broadcast scan or binary lifting per instance (long models / few stages
+    vs short models / many stages), and the 16-bit memory reach table.
+    Instances straddle C = 2^31 (totals just below and just above), span
+    both count choices, and carry tight and loose memory caps; partition and
+    BOUND repack vs the oracle."""
+    g = np.random.default_rng(31_2025 + count)
+    insts = []
+    for i in range(count):
+        kind = i % 4
+        Ly = int(g.integers(200, 1000)) if kind == 0 else int(g.integers(2, 40))
+        n = int(g.integers(1, 4)) if kind == 0 else int(g.integers(1, min(Ly, 32) + 1))
+        # total near 2^31: scale random weights so that C = 2^31 +- a few
+        target = (1 << 31) + int(g.integers(-3, 4)) if kind in (1, 2) else int(g.integers(1, 1 << 40))
+        w = g.random(Ly) + 0.05
+        cost = np.floor(w / w.sum() * target).astype(np.int64)
+        cost[-1] += target - int(cost.sum())  # exact total
+        mem = g.integers(1, 1 << 20, Ly)
+        cap = int(max(mem.max(), mem.sum() // n * g.uniform(0.9, 1.6))) if kind != 3 else int(mem.max())
+        insts.append(dict(cost=cost, n=n, mem=mem, cap=cap, bound=int(cost.sum() // n * g.uniform(1.0, 2.5)),
+                          floor=1))
+    for with_mem in (False, True):
+        _check_partition(insts, _run_partition(D, ctx, insts, with_mem), with_mem)
+        b, bnds, kn, bott, st = _run_repack(D, ctx, insts, 0, with_mem)
+        for q, x in enumerate(insts):
+            ost, ok, ob, oB = oracle.repack_bound(x["cost"], x["n"], x["bound"], 1,
+                                                  mem=x["mem"] if with_mem else None, cap=x["cap"] if with_mem else 0)
+            assert (st[q], kn[q], bott[q]) == (ost, ok, oB), (q, with_mem)
+            assert np.array_equal(bnds[q][:x["n"] + 1], ob), (q, with_mem)
+
+
 def test_partition_errors(D, ctx):
     """INVALID (n > L, n < 1, negative cost), OVERFLOW, INFEASIBLE."""
     insts = [dict(cost=np.array([1, 2]), n=3, mem=np.array([1, 1]), cap=5),
