@@ -114,7 +114,7 @@ constexpr int kMaxExperts = 1024;
 struct ProfArgs {
     const ProfTile *tiles;
     int64_t n_tiles;
-    unsigned long long *acc;    // [ACC_N][n_local] (slot-major)
+    unsigned long long *acc;    // [n_local][ACC_N]
     unsigned long long *hist;   // [n_local][max_E]
     unsigned long long *exit_hist;  // [kExitBins]
     int32_t max_E;

@@ -26,13 +26,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     return t;
 }
 
-// Counter slot `slot` of local layer `layer`: slot-major (acc[slot][layer]),
-// so one slot's counters of consecutive layers share sectors (config 5's
-// 360 k token-mask layers touch 2.9 MB of counters instead of 8.6 MB).
-__device__ __forceinline__ int64_t acc_key(int32_t layer, int32_t slot, int32_t n_local) {
-    return (int64_t)slot * n_local + layer;
-}
-
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -172,7 +165,7 @@ __device__ __forceinline__ bool small_count_tile(const ProfTile &t) {
 // S > 32, then one warp reduction per layer and lane u adds layer g0 + u's
 // count with one 64-bit atomic (distinct layers: no same-address contention,
 // and no per-layer descriptor to fetch).
-__device__ __forceinline__ void count_strided(const ProfTile &t, int lane, unsigned long long *acc, int32_t n_local) {
+__device__ __forceinline__ void count_strided(const ProfTile &t, int lane, unsigned long long *acc) {
     const uint32_t S = t.bits;
     const uint32_t k = t.nbytes / (S * 16u);
     const uint4 *p = (const uint4 *)t.ptr;
@@ -195,7 +188,7 @@ __device__ __forceinline__ void count_strided(const ProfTile &t, int lane, unsig
             mine = lane == u ? r : mine;
         }
         if (lane < 8 && g0 + lane < k && mine)
-            atomicAdd(&acc[acc_key(t.layer + (int32_t)(g0 + lane), t.aux, n_local)], (unsigned long long)mine);
+            atomicAdd(&acc[(int64_t)(t.layer + (int32_t)(g0 + lane)) * ACC_N + t.aux], (unsigned long long)mine);
     }
 }
 
@@ -379,7 +372,7 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
         if (HAS_CNT && (t.op & OP_STRIDED)) {
             if (ti + 1 < t_end) nxt = a.tiles[ti + 1];
             DYNMO_DCHECK(t.layer + (int64_t)(t.nbytes / (t.bits * 16u)) <= a.n_local);
-            count_strided(t, lane, a.acc, a.n_local);
+            count_strided(t, lane, a.acc);
             continue;
         }
         if (HAS_CNT && small_count_tile(t)) {
@@ -413,7 +406,7 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
             }
             c += __shfl_xor_sync(0xFFFFFFFFu, c, 1);
             c += __shfl_xor_sync(0xFFFFFFFFu, c, 2);
-            const int64_t key = acc_key(mine.layer, mine.aux, a.n_local);
+            const int64_t key = (int64_t)mine.layer * ACC_N + mine.aux;
             for (int u = 0; u < nb; ++u)
                 feed(__shfl_sync(0xFFFFFFFFu, key, 4 * u), __shfl_sync(0xFFFFFFFFu, c, 4 * u));
             ti += nb - 1;
@@ -434,7 +427,7 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, o);
-            feed(acc_key(t.layer, t.aux, a.n_local), s);
+            feed((int64_t)t.layer * ACC_N + t.aux, s);
             continue;
         }
         if (HAS_CNT && kind <= OP_NZ32) {
@@ -451,7 +444,7 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
                     default: c = count_tile<OP_NZ32>(p, nvec, lane); break;
                 }
             }
-            feed(acc_key(t.layer, t.aux, a.n_local), __reduce_add_sync(0xFFFFFFFFu, c));
+            feed((int64_t)t.layer * ACC_N + t.aux, __reduce_add_sync(0xFFFFFFFFu, c));
             continue;
         }
         if constexpr (HAS_HIST) {
@@ -634,12 +627,12 @@ __global__ void k_epilogue(EpiArgs a) {
     if (q < a.n_local) {
         const LayerInfo li = a.info[q];
         const int gi = a.layer_begin + q;
-        unsigned long long nnz_u = a.acc[acc_key(q, ACC_NNZ, a.n_local)];
-        unsigned long long tok_u = a.acc[acc_key(q, ACC_TOK, a.n_local)];
-        const unsigned long long time_u = a.acc[acc_key(q, ACC_TIME, a.n_local)];
-        a.acc[acc_key(q, ACC_NNZ, a.n_local)] = 0ull;
-        a.acc[acc_key(q, ACC_TOK, a.n_local)] = 0ull;
-        a.acc[acc_key(q, ACC_TIME, a.n_local)] = 0ull;
+        unsigned long long nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
+        unsigned long long tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
+        const unsigned long long time_u = a.acc[(int64_t)q * ACC_N + ACC_TIME];
+        a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
+        a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
+        a.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
         if (li.flags & SRC_HAS_EXIT)
             for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
         const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
