@@ -13,6 +13,7 @@
 //              every rank's slice into the global cost / mem vectors.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dynmo_internal.h"
@@ -584,6 +585,7 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
 
 // -------------------------------------------------------------- epilogue
 __device__ __forceinline__ int worse(int a, int b) { return a < b ? a : b; }
+constexpr int kEpiK = 4;  // layers per thread per epilogue iteration
 // LL ("flag in the data") words of the peer-memory exchange: an int64 as two
 // 8-byte words {32 data bits, low 32 bits of the call epoch}.  An aligned
 // 8-byte store is single-copy atomic, so a word read with the current epoch
@@ -619,99 +621,144 @@ __device__ __forceinline__ bool ll_poll(const uint64_t *p, uint64_t epoch, uint6
 __device__ void unpack_p2p_dev(const int64_t *slots, PeerWindow *win, int32_t nranks, int32_t n_total,
                                int64_t *decoded, int64_t *cost_out, int64_t *mem_out, int32_t *status_out);
 
+// Inputs of one layer, loaded before any of them is used so that a thread
+// has the loads of several layers in flight (the epilogue is a long list
+// of tiny independent layers for config 5: 360 k of them).
+struct EpiPre {
+    LayerInfo li;
+    dynmo_cost_coef cf;
+    unsigned long long nnz_u, tok_u, time_u;
+    int64_t m;
+    bool frozen;
+};
+
+__device__ __forceinline__ void epi_load(const EpiArgs &a, int q, EpiPre &p) {
+    p.li = a.info[q];
+    const uint4 *c4 = reinterpret_cast<const uint4 *>(a.coef + q);  // 48 B, 16-B aligned
+    uint4 *d4 = reinterpret_cast<uint4 *>(&p.cf);
+    d4[0] = c4[0];
+    d4[1] = c4[1];
+    d4[2] = c4[2];
+    p.nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
+    p.tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
+    p.time_u = a.acc[(int64_t)q * ACC_N + ACC_TIME];
+    p.frozen = a.frozen && a.frozen[q];
+    p.m = a.mem_local ? a.mem_local[q] : 0;
+}
+
+// Cost of local layer q from its prefetched inputs (a5, readings Q1-Q6);
+// consumes its counters; writes the outputs of the selected exchange mode.
+// Returns the layer's status.
+__device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p) {
+    int st = DYNMO_OK;
+    const LayerInfo li = p.li;
+    const int gi = a.layer_begin + q;
+    unsigned long long nnz_u = p.nnz_u;
+    unsigned long long tok_u = p.tok_u;
+    const unsigned long long time_u = p.time_u;
+    a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
+    a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
+    a.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
+    if (li.flags & SRC_HAS_EXIT)
+        for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
+    const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
+    const dynmo_cost_coef cf = p.cf;
+    const bool frozen = p.frozen;
+    // moe_i = EP * max over EP groups of group token counts (reading Q5)
+    __int128 moe = 0;
+    const bool bad_coef = cf.A < 0 || cf.B < 0 || cf.C < 0 || cf.F < 0 || cf.D < 0;
+    bool bad_ep = false;
+    if (li.flags & SRC_HAS_MOE) {
+        const int E = li.E;
+        const int EP = cf.ep_ranks <= 0 ? E : cf.ep_ranks;
+        unsigned long long *h = a.hist + (int64_t)q * a.max_E;
+        bad_ep = E < 1 || EP < 1 || E % EP != 0;
+        if (!bad_ep) {
+            const int g = E / EP;
+            __int128 best = 0;
+            for (int r = 0; r < EP; ++r) {
+                __int128 s = 0;
+                for (int e = r * g; e < (r + 1) * g; ++e) s += (__int128)h[e];
+                if (s > best) best = s;
+            }
+            moe = (__int128)EP * best;
+        }
+        for (int e = 0; e < E; ++e) {
+            if (a.hist_out) a.hist_out[(int64_t)q * a.max_E + e] = (int64_t)h[e];
+            h[e] = 0ull;
+        }
+    }
+    const __int128 LIM = (__int128)INT64_MAX;
+    const __int128 tok = has_tok ? (__int128)tok_u : (__int128)1;
+    const __int128 nnz = (__int128)nnz_u;
+    int64_t c = -1;
+    // order of the oracle: coefficients, then frozen, then the EP groups
+    if (bad_coef) {
+        st = DYNMO_E_INVALID;
+    } else if (frozen) {
+        c = cf.F;
+    } else if (bad_ep) {
+        st = DYNMO_E_INVALID;
+    } else {
+        const __int128 inner = (__int128)cf.A + (__int128)cf.B * nnz;
+        if (inner > LIM || tok > LIM || moe > LIM) {
+            st = DYNMO_E_OVERFLOW;
+        } else {
+            __int128 v = tok * inner;
+            const __int128 cm = (__int128)cf.C * moe;
+            const __int128 tm = (__int128)time_u;
+            const __int128 ct = tm > LIM ? LIM + 1 : (__int128)cf.D * tm;
+            if (tm > LIM || v > LIM || cm > LIM || v + cm > LIM || ct > LIM || v + cm + ct > LIM)
+                st = DYNMO_E_OVERFLOW;
+            else c = (int64_t)(v + cm + ct);
+        }
+    }
+    const int64_t m = p.m;
+    if (a.counters_out) {
+        int64_t *o = a.counters_out + (int64_t)q * 5;
+        o[0] = (int64_t)nnz_u;
+        o[1] = has_tok ? (int64_t)tok_u : 1;
+        o[2] = moe > LIM ? -1 : (int64_t)moe;
+        o[3] = c;
+        o[4] = time_u > (unsigned long long)INT64_MAX ? -1 : (int64_t)time_u;
+    }
+    if (a.p2p) {
+        // straight into every rank's receive slot as LL words (NVLink
+        // stores; each word carries the epoch, no fence or flag needed)
+        const uint64_t epoch = a.win->exch_epoch + 1;  // advanced by the last block
+        const int64_t S = 3 + 2 * (int64_t)a.n_total;
+        const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * 2 * S;
+        for (int r = 0; r < a.nranks; ++r) {
+            ll_store(a.peer_slots[r] + off + 2 * (3 + q), c, epoch);
+            ll_store(a.peer_slots[r] + off + 2 * (3 + a.n_total + q), m, epoch);
+        }
+    } else if (a.exchange) {
+        a.slot_send[3 + q] = c;
+        a.slot_send[3 + a.n_total + q] = m;
+    } else {
+        a.cost_out[q] = c;
+        if (a.mem_out) a.mem_out[q] = m;
+    }
+    return st;
+}
+
 __global__ void k_epilogue(EpiArgs a) {
     pdl_wait();
     pdl_trigger();
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    // grid-stride, kEpiK layers per thread with all their loads issued first
+    const int nthr = gridDim.x * blockDim.x;
     int st = DYNMO_OK;
-    if (q < a.n_local) {
-        const LayerInfo li = a.info[q];
-        const int gi = a.layer_begin + q;
-        unsigned long long nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
-        unsigned long long tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
-        const unsigned long long time_u = a.acc[(int64_t)q * ACC_N + ACC_TIME];
-        a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
-        a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
-        a.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
-        if (li.flags & SRC_HAS_EXIT)
-            for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
-        const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
-        const dynmo_cost_coef cf = a.coef[q];
-        const bool frozen = a.frozen && a.frozen[q];
-        // moe_i = EP * max over EP groups of group token counts (reading Q5)
-        __int128 moe = 0;
-        const bool bad_coef = cf.A < 0 || cf.B < 0 || cf.C < 0 || cf.F < 0 || cf.D < 0;
-        bool bad_ep = false;
-        if (li.flags & SRC_HAS_MOE) {
-            const int E = li.E;
-            const int EP = cf.ep_ranks <= 0 ? E : cf.ep_ranks;
-            unsigned long long *h = a.hist + (int64_t)q * a.max_E;
-            bad_ep = E < 1 || EP < 1 || E % EP != 0;
-            if (!bad_ep) {
-                const int g = E / EP;
-                __int128 best = 0;
-                for (int r = 0; r < EP; ++r) {
-                    __int128 s = 0;
-                    for (int e = r * g; e < (r + 1) * g; ++e) s += (__int128)h[e];
-                    if (s > best) best = s;
-                }
-                moe = (__int128)EP * best;
-            }
-            for (int e = 0; e < E; ++e) {
-                if (a.hist_out) a.hist_out[(int64_t)q * a.max_E + e] = (int64_t)h[e];
-                h[e] = 0ull;
-            }
+    for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < a.n_local; base += nthr * kEpiK) {
+        EpiPre p[kEpiK];
+#pragma unroll
+        for (int k = 0; k < kEpiK; ++k) {
+            const int q = base + k * nthr;
+            if (q < a.n_local) epi_load(a, q, p[k]);
         }
-        const __int128 LIM = (__int128)INT64_MAX;
-        const __int128 tok = has_tok ? (__int128)tok_u : (__int128)1;
-        const __int128 nnz = (__int128)nnz_u;
-        int64_t c = -1;
-        // order of the oracle: coefficients, then frozen, then the EP groups
-        if (bad_coef) {
-            st = DYNMO_E_INVALID;
-        } else if (frozen) {
-            c = cf.F;
-        } else if (bad_ep) {
-            st = DYNMO_E_INVALID;
-        } else {
-            const __int128 inner = (__int128)cf.A + (__int128)cf.B * nnz;
-            if (inner > LIM || tok > LIM || moe > LIM) {
-                st = DYNMO_E_OVERFLOW;
-            } else {
-                __int128 v = tok * inner;
-                const __int128 cm = (__int128)cf.C * moe;
-                const __int128 tm = (__int128)time_u;
-                const __int128 ct = tm > LIM ? LIM + 1 : (__int128)cf.D * tm;
-                if (tm > LIM || v > LIM || cm > LIM || v + cm > LIM || ct > LIM || v + cm + ct > LIM)
-                    st = DYNMO_E_OVERFLOW;
-                else c = (int64_t)(v + cm + ct);
-            }
-        }
-        const int64_t m = a.mem_local ? a.mem_local[q] : 0;
-        if (a.counters_out) {
-            int64_t *o = a.counters_out + (int64_t)q * 5;
-            o[0] = (int64_t)nnz_u;
-            o[1] = has_tok ? (int64_t)tok_u : 1;
-            o[2] = moe > LIM ? -1 : (int64_t)moe;
-            o[3] = c;
-            o[4] = time_u > (unsigned long long)INT64_MAX ? -1 : (int64_t)time_u;
-        }
-        if (a.p2p) {
-            // straight into every rank's receive slot as LL words (NVLink
-            // stores; each word carries the epoch, no fence or flag needed)
-            const uint64_t epoch = a.win->exch_epoch + 1;  // advanced by the last block
-            const int64_t S = 3 + 2 * (int64_t)a.n_total;
-            const int64_t off = ((int64_t)(epoch & 1) * a.nranks + a.rank) * 2 * S;
-            for (int r = 0; r < a.nranks; ++r) {
-                ll_store(a.peer_slots[r] + off + 2 * (3 + q), c, epoch);
-                ll_store(a.peer_slots[r] + off + 2 * (3 + a.n_total + q), m, epoch);
-            }
-        } else if (a.exchange) {
-            a.slot_send[3 + q] = c;
-            a.slot_send[3 + a.n_total + q] = m;
-        } else {
-            a.cost_out[q] = c;
-            if (a.mem_out) a.mem_out[q] = m;
+#pragma unroll
+        for (int k = 0; k < kEpiK; ++k) {
+            const int q = base + k * nthr;
+            if (q < a.n_local) st = worse(st, epi_one(a, q, p[k]));
         }
     }
     // block-reduce the status, then last-block finalisation
@@ -945,7 +992,16 @@ cudaError_t launch_profile(const ProfArgs &a, int ops, int grid, cudaStream_t s)
 
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s) {
     const int threads = 256;
-    const int grid = a.n_local > 0 ? (a.n_local + threads - 1) / threads : 1;
+    // one resident wave (grid-stride beyond it), kEpiK layers per thread
+    static const int wave = [] {
+        int dev = 0, sms = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_epilogue, 256, 0);
+        return std::max(1, sms * std::max(1, per));
+    }();
+    const int64_t need = ((int64_t)a.n_local + (int64_t)threads * kEpiK - 1) / ((int64_t)threads * kEpiK);
+    const int grid = a.n_local > 0 ? (int)std::min<int64_t>(need, wave) : 1;
     return launch_pdl(k_epilogue, grid, threads, 0, s, a);
 }
 
