@@ -409,29 +409,20 @@ __device__ int64_t search_bottleneck(Inst &s, int n) {
     return search_t<uint64_t, MEM, NW>(s, v, n, lo, hi, jumps);
 }
 
-// Greedy stage count at one B (repack's fewest workers; one warp, every
-// lane the same B; B >= max c and every m <= cap): a 64-bit scan with the
-// memory test on M directly (no reach table yet).
+// Greedy stage count at one B (repack's fewest workers; one warp; B >= max c
+// and every m <= cap): warp-cooperative window jumps (32 positions per
+// shared load, ballot = prefix of ones), stopping once the count exceeds
+// `limit` (then any value > limit is returned).
 template <bool MEM>
-__device__ int count_at(const Inst &s, int64_t B) {
-    const int64_t C = s.P[s.L];
-    const uint64_t b = (uint64_t)(B < C ? B : C);  // B > C behaves as C
-    const uint64_t *P = reinterpret_cast<const uint64_t *>(s.P);
-    const uint64_t *M = reinterpret_cast<const uint64_t *>(s.M);
-    const uint64_t cap = MEM ? (uint64_t)(s.cap < s.M[s.L] ? s.cap : s.M[s.L]) : 0;
-    uint64_t t1 = b, t2 = cap;
-    int c = 1;
-#pragma unroll 4
-    for (int i = 1; i <= s.L; ++i) {
-        bool cut = P[i] > t1;
-        if constexpr (MEM) cut |= M[i] > t2;
-        const uint64_t n1 = P[i - 1] + b;
-        t1 = cut ? n1 : t1;
-        if constexpr (MEM) {
-            const uint64_t n2 = M[i - 1] + cap;
-            t2 = cut ? n2 : t2;
-        }
-        c += cut;
+__device__ int count_at(const Inst &s, int64_t B, int limit, int lane) {
+    int j = 0, c = 0;
+    while (j < s.L) {
+        if (c > limit) return c;
+        const int64_t t1 = satadd(s.P[j], B);
+        int64_t t2 = 0;
+        if constexpr (MEM) t2 = satadd(s.M[j], s.cap);
+        j = warp_jump<MEM>(s, j, t1, t2, lane);  // > j: layer j fits alone
+        ++c;
     }
     return c;
 }
@@ -568,7 +559,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
         if (st == DYNMO_OK && !alg2) {
             // fewest workers: greedy count at B = bound (cost and mem), reading Q15;
             // a layer above the bound or the cap alone: no count meets it
-            const int g = (bound >= s.maxc && (!MEM || s.mfit)) ? count_at<MEM>(s, bound) : n_cur + 1;
+            const int g = (bound >= s.maxc && (!MEM || s.mfit)) ? count_at<MEM>(s, bound, n_cur, lane) : n_cur + 1;
             if (g <= n_cur) {
                 k = g > fl ? g : fl;
             } else {
