@@ -310,24 +310,134 @@ __device__ __forceinline__ int64_t candidate(int64_t lo, uint64_t d, int c) {
     return lo + (int64_t)(qa * (uint64_t)(c + 1) + (qr * (uint64_t)(c + 1)) / (uint64_t)NC1);
 }
 
+// Block-wide (NW warps) exclusive prefix sum of one int per thread; also the
+// total.  Two barriers; s_w is a per-call scratch of NW ints.
+template <int NW>
+__device__ __forceinline__ int block_excl_scan(int x, int &total, int *s_w) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if constexpr (NW == 1) {
+        total = __shfl_sync(FULL, incl, 31);
+        return incl - x;
+    } else {
+        if (lane == 31) s_w[w] = incl;
+        __syncthreads();
+        int before = 0, tot = 0;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const int v = s_w[k];
+            before += k < w ? v : 0;
+            tot += v;
+        }
+        __syncthreads();  // s_w may be reused
+        total = tot;
+        return before + incl - x;
+    }
+}
+
+// Block-wide min of one int64 per thread (one barrier pair for NW > 1).
+template <int NW>
+__device__ __forceinline__ int64_t block_min64(int64_t x, int64_t *s_w) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(FULL, x, o);
+        x = y < x ? y : x;
+    }
+    if constexpr (NW == 1) {
+        return x;
+    } else {
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        if (lane == 0) s_w[w] = x;
+        __syncthreads();
+        int64_t m = s_w[0];
+#pragma unroll
+        for (int k = 1; k < NW; ++k) m = s_w[k] < m ? s_w[k] : m;
+        __syncthreads();
+        return m;
+    }
+}
+
 // Exact min-max search (all threads of the NW warps, after s is built and
-// visible).  Bracket: lo = max(max c, ceil(C/n)) is a lower bound of B*,
-// hi = min(ceil(C/n) + max c, C) is feasible on cost (Appendix A).  Every
-// round each thread tests one candidate; feasibility is monotone in B, so
-// the feasible candidates form a suffix: the first feasible one is the new
-// hi and its predecessor + 1 the new lo, a (32 NW + 1)-ary search.  Under a
-// memory cap hi may be infeasible: the first round then tests NT - 2
-// candidates in [lo, hi), hi itself and C (no feasible candidate: no split
-// satisfies the cap).  Returns B* (uniform), or -1.
+// visible).  B* is the largest stage sum of an optimal split, so it is one
+// of the interval sums P[j] - P[i] (i < j); the search narrows [lo, hi]
+// until the interval sums inside it fit one per thread, then tests exactly
+// those candidates: the smallest feasible one is B*.  Narrowing rounds are
+// (NT+1)-ary over the integers (every thread tests one candidate;
+// feasibility is monotone in B, so the first feasible candidate is the new
+// hi and its predecessor + 1 the new lo).  Bracket: lo = max(max c,
+// ceil(C/n)) is a lower bound of B*, hi = min(ceil(C/n) + max c, C) is
+// feasible on cost (Appendix A); under a memory cap it may not be, so the
+// first narrowing round also tests hi itself and C, and if no interval sum
+// in [lo, hi] is feasible the search moves to (hi, C] (C infeasible: no
+// split satisfies the cap, -1).  Returns B* (uniform).
 template <typename T, bool MEM, int NW>
 __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, int64_t hi, bool jumps) {
     constexpr int NT = 32 * NW;
     __shared__ unsigned s_f[2][NW];
+    __shared__ int s_wi[NW];
+    __shared__ int64_t s_w64[NW];
+    __shared__ int64_t s_cand[NT];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
-    const int64_t C = s.P[s.L];
-    bool probe = MEM;  // first round also tests hi and C
+    const int L = s.L;
+    const int64_t C = s.P[L];
+    const int top = 1 << (31 - __clz(L));
+    bool probe = MEM;  // the first narrowing round also tests hi and C
     int par = 0;
-    while (probe || lo < hi) {
+    for (;;) {
+        // outside the first round under a cap, hi is known feasible: a
+        // one-point interval is the answer (its value may repeat as many
+        // interval sums -- zero-cost layers -- so it is not enumerated)
+        if (!probe && lo >= hi) return hi;
+        // interval sums in [lo, hi]: for each start i, the ends j in [ja, jb]
+        int cnt = 0;
+        for (int i = t; i < L; i += NT) {
+            const int64_t a1 = satadd(s.P[i], lo), a2 = satadd(s.P[i], hi);
+            int ja = i, jb = i;  // largest j with P[j] < P[i] + lo, and <= P[i] + hi
+            for (int step = top; step > 0; step >>= 1) {
+                const int j1 = ja + step, j2 = jb + step;
+                if (j1 <= L && s.P[j1] < a1) ja = j1;
+                if (j2 <= L && s.P[j2] <= a2) jb = j2;
+            }
+            cnt += jb - ja;  // ends ja+1 .. jb (ja >= i: the sums are > 0 or lo == 0 edge below)
+        }
+        int total;
+        const int off = block_excl_scan<NW>(cnt, total, s_wi);
+        if (total <= NT) {
+            int o = off;
+            for (int i = t; i < L; i += NT) {
+                const int64_t a1 = satadd(s.P[i], lo), a2 = satadd(s.P[i], hi);
+                int ja = i, jb = i;
+                for (int step = top; step > 0; step >>= 1) {
+                    const int j1 = ja + step, j2 = jb + step;
+                    if (j1 <= L && s.P[j1] < a1) ja = j1;
+                    if (j2 <= L && s.P[j2] <= a2) jb = j2;
+                }
+                for (int j = ja + 1; j <= jb; ++j) s_cand[o++] = s.P[j] - s.P[i];
+            }
+            if constexpr (NW > 1) __syncthreads();
+            else __syncwarp();
+            int64_t mine = I64MAX;
+            if (t < total) {
+                const int64_t c = s_cand[t];
+                if (thread_count<T, MEM>(v, c, n, jumps) <= n) mine = c;
+            }
+            const int64_t best = block_min64<NW>(mine, s_w64);
+            if constexpr (NW == 1) __syncwarp();  // s_cand is rewritten next pass
+            if (best != I64MAX) return best;
+            // no interval sum in [lo, hi] is feasible: only under a memory
+            // cap, and then B* lies in (hi, C] if C itself is feasible
+            if (!MEM || hi >= C) return -1;
+            if (thread_count<T, MEM>(v, C, n, jumps) > n) return -1;
+            lo = hi + 1;
+            hi = C;
+            probe = false;  // hi = C is known feasible now
+            continue;
+        }
         const uint64_t d = (uint64_t)(hi - lo);
         int64_t cand;
         if (probe) cand = t < NT - 2 ? candidate<NT - 1>(lo, d, t) : (t == NT - 2 ? hi : C);
@@ -367,8 +477,6 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
         hi = nhi;
         lo = nlo;
     }
-    (void)w;
-    return hi;
 }
 
 // Per-instance choice of the count: latency mode (NW > 1, one instance per
