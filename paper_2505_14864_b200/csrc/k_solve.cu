@@ -362,6 +362,22 @@ __device__ __forceinline__ int64_t block_min64(int64_t x, int64_t *s_w) {
     }
 }
 
+// Ends of the interval sums from start i inside [lo, hi]: j in (ja, jb],
+// where ja = the largest j >= i with P[j] - P[i] < lo and jb = the largest
+// j >= i with P[j] - P[i] <= hi (binary lifting; P is nondecreasing).  If
+// P[i] + lo overflows, no end qualifies.
+__device__ __forceinline__ void sum_range(const Inst &s, int i, int64_t lo, int64_t hi, int top, int &ja, int &jb) {
+    const int L = s.L;
+    ja = jb = i;
+    if (s.P[i] > I64MAX - lo) return;
+    const int64_t a1 = s.P[i] + lo, a2 = satadd(s.P[i], hi);
+    for (int step = top; step > 0; step >>= 1) {
+        const int j1 = ja + step, j2 = jb + step;
+        if (j1 <= L && s.P[j1] < a1) ja = j1;
+        if (j2 <= L && s.P[j2] <= a2) jb = j2;
+    }
+}
+
 // Exact min-max search (all threads of the NW warps, after s is built and
 // visible).  B* is the largest stage sum of an optimal split, so it is one
 // of the interval sums P[j] - P[i] (i < j); the search narrows [lo, hi]
@@ -394,29 +410,23 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
         // interval sums -- zero-cost layers -- so it is not enumerated)
         if (!probe && lo >= hi) return hi;
         // interval sums in [lo, hi]: for each start i, the ends j in [ja, jb]
-        int cnt = 0;
-        for (int i = t; i < L; i += NT) {
-            const int64_t a1 = satadd(s.P[i], lo), a2 = satadd(s.P[i], hi);
-            int ja = i, jb = i;  // largest j with P[j] < P[i] + lo, and <= P[i] + hi
-            for (int step = top; step > 0; step >>= 1) {
-                const int j1 = ja + step, j2 = jb + step;
-                if (j1 <= L && s.P[j1] < a1) ja = j1;
-                if (j2 <= L && s.P[j2] <= a2) jb = j2;
+        // (the one-candidate-per-thread latency mode only: with 32 threads
+        // the enumeration passes cost more than the rounds they save)
+        int cnt = 0, total = NT + 1;
+        if constexpr (NW > 1) {
+            for (int i = t; i < L; i += NT) {
+                int ja, jb;
+                sum_range(s, i, lo, hi, top, ja, jb);
+                cnt += jb - ja;
             }
-            cnt += jb - ja;  // ends ja+1 .. jb (ja >= i: the sums are > 0 or lo == 0 edge below)
         }
-        int total;
-        const int off = block_excl_scan<NW>(cnt, total, s_wi);
+        int off = 0;
+        if constexpr (NW > 1) off = block_excl_scan<NW>(cnt, total, s_wi);
         if (total <= NT) {
             int o = off;
             for (int i = t; i < L; i += NT) {
-                const int64_t a1 = satadd(s.P[i], lo), a2 = satadd(s.P[i], hi);
-                int ja = i, jb = i;
-                for (int step = top; step > 0; step >>= 1) {
-                    const int j1 = ja + step, j2 = jb + step;
-                    if (j1 <= L && s.P[j1] < a1) ja = j1;
-                    if (j2 <= L && s.P[j2] <= a2) jb = j2;
-                }
+                int ja, jb;
+                sum_range(s, i, lo, hi, top, ja, jb);
                 for (int j = ja + 1; j <= jb; ++j) s_cand[o++] = s.P[j] - s.P[i];
             }
             if constexpr (NW > 1) __syncthreads();
