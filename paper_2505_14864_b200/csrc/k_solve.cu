@@ -340,12 +340,12 @@ __device__ __forceinline__ int block_excl_scan(int x, int &total, int *s_w) {
     }
 }
 
-// Block-wide min of one int64 per thread (one barrier pair for NW > 1).
+// Block-wide min of one uint64 per thread (one barrier pair for NW > 1).
 template <int NW>
-__device__ __forceinline__ int64_t block_min64(int64_t x, int64_t *s_w) {
+__device__ __forceinline__ uint64_t block_min64(uint64_t x, uint64_t *s_w) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        const int64_t y = __shfl_xor_sync(FULL, x, o);
+        const uint64_t y = __shfl_xor_sync(FULL, x, o);
         x = y < x ? y : x;
     }
     if constexpr (NW == 1) {
@@ -354,7 +354,7 @@ __device__ __forceinline__ int64_t block_min64(int64_t x, int64_t *s_w) {
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         if (lane == 0) s_w[w] = x;
         __syncthreads();
-        int64_t m = s_w[0];
+        uint64_t m = s_w[0];
 #pragma unroll
         for (int k = 1; k < NW; ++k) m = s_w[k] < m ? s_w[k] : m;
         __syncthreads();
@@ -396,7 +396,7 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
     constexpr int NT = 32 * NW;
     __shared__ unsigned s_f[2][NW];
     __shared__ int s_wi[NW];
-    __shared__ int64_t s_w64[NW];
+    __shared__ uint64_t s_w64[NW];
     __shared__ int64_t s_cand[NT];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, t = threadIdx.x;
     const int L = s.L;
@@ -431,14 +431,16 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
             }
             if constexpr (NW > 1) __syncthreads();
             else __syncwarp();
-            int64_t mine = I64MAX;
+            // (a candidate may be INT64_MAX itself: the "none" sentinel is
+            // UINT64_MAX, outside the candidates' range)
+            uint64_t mine = ~0ull;
             if (t < total) {
                 const int64_t c = s_cand[t];
-                if (thread_count<T, MEM>(v, c, n, jumps) <= n) mine = c;
+                if (thread_count<T, MEM>(v, c, n, jumps) <= n) mine = (uint64_t)c;
             }
-            const int64_t best = block_min64<NW>(mine, s_w64);
+            const uint64_t best = block_min64<NW>(mine, s_w64);
             if constexpr (NW == 1) __syncwarp();  // s_cand is rewritten next pass
-            if (best != I64MAX) return best;
+            if (best != ~0ull) return (int64_t)best;
             // no interval sum in [lo, hi] is feasible: only under a memory
             // cap, and then B* lies in (hi, C] if C itself is feasible
             if (!MEM || hi >= C) return -1;
