@@ -412,8 +412,15 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
         // interval sums in [lo, hi]: for each start i, the ends j in [ja, jb]
         // (the one-candidate-per-thread latency mode only: with 32 threads
         // the enumeration passes cost more than the rounds they save)
+        // Enumerate only when it can pay: not when one integer round already
+        // covers [lo, hi) (d < NT), and not when the expected number of
+        // interval sums in the range (L(L+1)/2 spread over [0, C]) exceeds
+        // a thread's share
         int cnt = 0, total = NT + 1;
-        if constexpr (NW > 1) {
+        const double width = (double)(hi - lo) + 1.0;
+        const bool try_enum = NW > 1 && hi - lo >= NT &&
+                              0.5 * (double)L * (double)(L + 1) * width <= (double)NT * ((double)C + 1.0);
+        if (try_enum) {
             for (int i = t; i < L; i += NT) {
                 int ja, jb;
                 sum_range(s, i, lo, hi, top, ja, jb);
@@ -421,7 +428,7 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
             }
         }
         int off = 0;
-        if constexpr (NW > 1) off = block_excl_scan<NW>(cnt, total, s_wi);
+        if (try_enum) off = block_excl_scan<NW>(cnt, total, s_wi);
         if (total <= NT) {
             int o = off;
             for (int i = t; i < L; i += NT) {
