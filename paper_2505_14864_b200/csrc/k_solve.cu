@@ -412,7 +412,9 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
         // interval sums in [lo, hi]: for each start i, the ends j in [ja, jb]
         // (the one-candidate-per-thread latency mode only: with 32 threads
         // the enumeration passes cost more than the rounds they save)
-        // Enumerate only when it can pay: not when one integer round already
+        // Enumerate only when it can pay: in the 256-thread latency mode (the
+        // batched mode measured slower with it: config 5's 4096 partitions
+        // 32.8 vs 28.4 us), not when one integer round already
         // covers [lo, hi) (d < NT), and not when the expected number of
         // interval sums in the range (L(L+1)/2 spread over [0, C]) exceeds
         // a thread's share
