@@ -281,81 +281,6 @@ __device__ __forceinline__ int thread_count(const View<T> &v, int64_t B, int lim
     return jumps ? jump_count<T, MEM>(v, (T)B, limit) : scan_count<T, MEM>(v, (T)B);
 }
 
-// Two candidates per thread, their chains interleaved (the one-warp batched
-// mode: instruction-level parallelism for the dependent shared loads, and
-// twice the candidates per round).  Same counts as above.
-template <typename T, bool MEM>
-__device__ __forceinline__ void jump_count2(const View<T> &v, T B0, T B1, int limit, int &r0, int &r1) {
-    const int L = v.L;
-    const int top = 1 << (31 - __clz(L));
-    int j0 = 0, c0 = 0, j1 = 0, c1 = 0;
-    for (;;) {
-        const bool a0 = j0 < L && c0 <= limit, a1 = j1 < L && c1 <= limit;
-        if (!(a0 | a1)) break;
-        const T t0 = v.P[j0] + B0, t1 = v.P[j1] + B1;  // j <= L: valid
-        int K0 = j0, K1 = j1;
-        for (int step = top; step > 0; step >>= 1) {
-            const int k0 = K0 + step, k1 = K1 + step;
-            const int kc0 = k0 <= L ? k0 : L, kc1 = k1 <= L ? k1 : L;
-            const T p0 = v.P[kc0], p1 = v.P[kc1];
-            K0 = ((k0 <= L) & (p0 <= t0)) ? k0 : K0;
-            K1 = ((k1 <= L) & (p1 <= t1)) ? k1 : K1;
-        }
-        if constexpr (MEM) {
-            const int q0 = v.reach[j0], q1 = v.reach[j1];
-            K0 = K0 < q0 ? K0 : q0;
-            K1 = K1 < q1 ? K1 : q1;
-        }
-        if (a0) {
-            j0 = K0;
-            ++c0;
-        }
-        if (a1) {
-            j1 = K1;
-            ++c1;
-        }
-    }
-    r0 = j0 < L ? limit + 1 : c0;
-    r1 = j1 < L ? limit + 1 : c1;
-}
-
-template <typename T, bool MEM>
-__device__ __forceinline__ void scan_count2(const View<T> &v, T B0, T B1, int &r0, int &r1) {
-    T u0 = B0, u1 = B1;
-    int l0 = MEM ? v.reach[0] : v.L, l1 = l0;
-    int c0 = 1, c1 = 1;
-#pragma unroll 4
-    for (int i = 1; i <= v.L; ++i) {
-        const T p = v.P[i], pm = v.P[i - 1];
-        bool x0 = p > u0, x1 = p > u1;
-        if constexpr (MEM) {
-            x0 |= i > l0;
-            x1 |= i > l1;
-        }
-        u0 = x0 ? pm + B0 : u0;
-        u1 = x1 ? pm + B1 : u1;
-        if constexpr (MEM) {
-            const int nl = v.reach[i - 1];
-            l0 = x0 ? nl : l0;
-            l1 = x1 ? nl : l1;
-        }
-        c0 += x0;
-        c1 += x1;
-    }
-    r0 = c0;
-    r1 = c1;
-}
-
-template <typename T, bool MEM>
-__device__ __forceinline__ void thread_count2(const View<T> &v, int64_t B0, int64_t B1, int limit, bool jumps,
-                                              bool &f0, bool &f1) {
-    int r0, r1;
-    if (jumps) jump_count2<T, MEM>(v, (T)B0, (T)B1, limit, r0, r1);
-    else scan_count2<T, MEM>(v, (T)B0, (T)B1, r0, r1);
-    f0 = r0 <= limit;
-    f1 = r1 <= limit;
-}
-
 // Memory reach of every start j (MEM): the largest K in [j, L] with
 // M[K] - M[j] <= cap (M is nondecreasing), by binary lifting; all threads,
 // then a barrier (CTA or warp).
@@ -534,58 +459,42 @@ __device__ int64_t search_t(const Inst &s, const View<T> &v, int n, int64_t lo, 
             probe = false;  // hi = C is known feasible now
             continue;
         }
-        // integer round: NC candidates, CPT per thread (two in the one-warp
-        // mode, their count chains interleaved)
-        constexpr int CPT = NW == 1 ? 2 : 1;
-        constexpr int NC = NT * CPT;
         const uint64_t d = (uint64_t)(hi - lo);
-        int64_t cand[CPT];
-#pragma unroll
-        for (int u = 0; u < CPT; ++u) {
-            const int k = CPT * t + u;
-            if (probe) cand[u] = k < NC - 2 ? candidate<NC - 1>(lo, d, k) : (k == NC - 2 ? hi : C);
-            else cand[u] = candidate<NC + 1>(lo, d, k);
-        }
+        int64_t cand;
+        if (probe) cand = t < NT - 2 ? candidate<NT - 1>(lo, d, t) : (t == NT - 2 ? hi : C);
+        else cand = candidate<NT + 1>(lo, d, t);
+        const unsigned m = __ballot_sync(FULL, thread_count<T, MEM>(v, cand, n, jumps) <= n);
         int first;
-        if constexpr (CPT == 2) {
-            bool f0, f1;
-            thread_count2<T, MEM>(v, cand[0], cand[1], n, jumps, f0, f1);
-            const unsigned m0 = __ballot_sync(FULL, f0), m1 = __ballot_sync(FULL, f1);
-            const int a0 = m0 ? 2 * (__ffs(m0) - 1) : NC, a1 = m1 ? 2 * (__ffs(m1) - 1) + 1 : NC;
-            first = a0 < a1 ? a0 : a1;
+        if constexpr (NW == 1) {
+            first = m ? __ffs(m) - 1 : NT;
         } else {
-            const unsigned m = __ballot_sync(FULL, thread_count<T, MEM>(v, cand[0], n, jumps) <= n);
-            if constexpr (NW == 1) {
-                first = m ? __ffs(m) - 1 : NC;
-            } else {
-                if (lane == 0) s_f[par][w] = m;
-                __syncthreads();
-                first = NC;
+            if (lane == 0) s_f[par][w] = m;
+            __syncthreads();
+            first = NT;
 #pragma unroll
-                for (int k = NW - 1; k >= 0; --k) {
-                    const unsigned mk = s_f[par][k];
-                    if (mk) first = 32 * k + __ffs(mk) - 1;
-                }
-                par ^= 1;  // double buffer: the next round writes the other half
+            for (int k = NW - 1; k >= 0; --k) {
+                const unsigned mk = s_f[par][k];
+                if (mk) first = 32 * k + __ffs(mk) - 1;
             }
+            par ^= 1;  // double buffer: the next round writes the other half
         }
         if (probe) {
             probe = false;
-            if (first == NC) return -1;        // C infeasible
-            if (first == NC - 1) {             // only C: B* in (hi, C]
+            if (first == NT) return -1;        // C infeasible
+            if (first == NT - 1) {             // only C: B* in (hi, C]
                 lo = hi + 1;
                 hi = C;
-            } else if (first == NC - 2) {      // hi: B* in (last candidate, hi]
-                lo = NC > 2 ? candidate<NC - 1>(lo, d, NC - 3) + 1 : lo;
+            } else if (first == NT - 2) {      // hi: B* in (last candidate, hi]
+                lo = NT > 2 ? candidate<NT - 1>(lo, d, NT - 3) + 1 : lo;
             } else {
-                const int64_t nhi = candidate<NC - 1>(lo, d, first);
-                lo = first > 0 ? candidate<NC - 1>(lo, d, first - 1) + 1 : lo;
+                const int64_t nhi = candidate<NT - 1>(lo, d, first);
+                lo = first > 0 ? candidate<NT - 1>(lo, d, first - 1) + 1 : lo;
                 hi = nhi;
             }
             continue;
         }
-        const int64_t nhi = first < NC ? candidate<NC + 1>(lo, d, first) : hi;
-        const int64_t nlo = first > 0 ? candidate<NC + 1>(lo, d, first - 1) + 1 : lo;
+        const int64_t nhi = first < NT ? candidate<NT + 1>(lo, d, first) : hi;
+        const int64_t nlo = first > 0 ? candidate<NT + 1>(lo, d, first - 1) + 1 : lo;
         hi = nhi;
         lo = nlo;
     }
