@@ -500,6 +500,13 @@ dynmo_status dynmo_migrate_layers_bwd(dynmo_ctx ctx, dynmo_mplan plan, int32_t n
                                       int32_t n_new, const int32_t *d_bnd_new,
                                       const int32_t *d_rank_new, int64_t *d_bytes_recv,
                                       dynmo_stream stream);
+/* Escape hatch (the waits above are unbounded): releases every layer and
+ * done word of the current epoch in this rank's own window and sets the
+ * sticky error to DYNMO_E_NCCL, so this rank's streams stop waiting.  For a
+ * host watchdog that sees an iteration overrun (a peer that skipped a call
+ * or died); copies on a private stream.  The iteration's received payload is
+ * undefined; the next iteration (dynmo_migrate_bwd_begin) starts clean. */
+dynmo_status dynmo_migrate_bwd_abort(dynmo_ctx ctx, dynmo_mplan plan);
 dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_old,
                                    const int32_t *d_bnd_old, const int32_t *d_rank_old,
                                    int32_t n_new, const int32_t *d_bnd_new,
@@ -507,6 +514,9 @@ dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan plan, int32_t n_ol
                                    dynmo_stream stream);
 /* Sticky device error of the peer-memory paths (0 = none); synchronous. */
 dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err);
+/* Resets the sticky error word to 0 after the device is idle (e.g. after a
+ * handled dynmo_migrate_bwd_abort); synchronous. */
+dynmo_status dynmo_ctx_p2p_error_clear(dynmo_ctx ctx);
 
 /* Host-only helper (no GPU, no ctx): the migration plan call 5 executes.
  * Writes moves (layer, src_rank, dst_rank), layer ascending, for every layer

@@ -98,6 +98,8 @@ def lib():
         "dynmo_migrate_bwd_end": (i32, [p, p, i32, p, p, i32, p, p, p, p]),
         "dynmo_ctx_profile_span": (i32, [p, p, p]),
         "dynmo_ctx_window_snapshot": (i32, [p, i32, p, C.c_int64]),
+        "dynmo_migrate_bwd_abort": (i32, [p, p]),
+        "dynmo_ctx_p2p_error_clear": (i32, [p]),
     }
     for name, (res, args) in sigs.items():
         f = getattr(L, name)
@@ -120,4 +122,5 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_migrate_layers_dev", "dynmo_migrate_plan_set_ctas",
             "dynmo_migrate_bwd_begin", "dynmo_migrate_layer_ready", "dynmo_migrate_layers_bwd",
             "dynmo_migrate_bwd_end", "dynmo_ctx_profile_span",
-            "dynmo_ctx_window_snapshot"]
+            "dynmo_ctx_window_snapshot", "dynmo_migrate_bwd_abort",
+            "dynmo_ctx_p2p_error_clear"]

@@ -1647,6 +1647,33 @@ dynmo_status dynmo_migrate_bwd_end(dynmo_ctx ctx, dynmo_mplan mp, int32_t n_old,
     return DYNMO_OK;
 }
 
+// Escape hatch of the unbounded stream waits: releases, in this rank's OWN
+// window, every layer word and every done word at the current epoch and sets
+// the sticky error to E_NCCL, so this rank's streams waiting in
+// dynmo_migrate_layers_bwd / dynmo_migrate_bwd_end complete.  Copies on a
+// private non-blocking stream (no kernel, no SM).  The iteration's received
+// payload is undefined afterwards; the next iteration starts clean.
+dynmo_status dynmo_migrate_bwd_abort(dynmo_ctx ctx, dynmo_mplan mp) {
+    if (!ctx || !mp || mp->ctx != ctx) return invalid("bad ctx/mplan");
+    if (ctx->bwd_epoch == 0) return invalid("dynmo_migrate_bwd_abort before dynmo_migrate_bwd_begin");
+    DeviceGuard g(ctx->device);
+    const int n = std::min<int>(mp->n_layers, 1024);
+    std::vector<uint64_t> ready(n, ctx->bwd_epoch), done(ctx->nranks, ctx->bwd_epoch);
+    const int32_t err = DYNMO_E_NCCL;
+    cudaStream_t s;
+    CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "abort stream");
+    cudaError_t e = cudaMemcpyAsync(&ctx->d_win->err, &err, sizeof(err), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->d_win->layer_ready, ready.data(), sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(ctx->d_win->bwd_done, done.data(), sizeof(uint64_t) * done.size(),
+                            cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e != cudaSuccess) return cuda_fail(e, "backward migration abort");
+    return DYNMO_OK;
+}
+
 dynmo_status dynmo_migrate_plan_set_ctas(dynmo_mplan plan, int32_t max_ctas) {
     if (!plan) return invalid("null plan");
     if (max_ctas < 0) return invalid("max_ctas < 0");
@@ -1789,6 +1816,15 @@ dynmo_status dynmo_ctx_p2p_error(dynmo_ctx ctx, int32_t *h_err) {
     if (!ctx->d_win) return DYNMO_OK;
     DeviceGuard g(ctx->device);
     CUDA_TRY(cudaMemcpy(h_err, &ctx->d_win->err, sizeof(int32_t), cudaMemcpyDeviceToHost), "read p2p error");
+    return DYNMO_OK;
+}
+
+dynmo_status dynmo_ctx_p2p_error_clear(dynmo_ctx ctx) {
+    if (!ctx) return invalid("null ctx");
+    if (!ctx->d_win) return DYNMO_OK;
+    DeviceGuard g(ctx->device);
+    CUDA_TRY(cudaDeviceSynchronize(), "p2p error clear (drain)");
+    CUDA_TRY(cudaMemset(&ctx->d_win->err, 0, sizeof(int32_t)), "p2p error clear");
     return DYNMO_OK;
 }
 

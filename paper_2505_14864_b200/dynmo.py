@@ -484,6 +484,15 @@ class PeerMigrator:
                                            _ptr(bytes_sent), _stream(stream)),
                "dynmo_migrate_bwd_end")
 
+    def clear_error(self):
+        """dynmo_ctx_p2p_error_clear: reset the sticky error word (synchronous)."""
+        _check(lib().dynmo_ctx_p2p_error_clear(self.ctx.handle), "dynmo_ctx_p2p_error_clear")
+
+    def bwd_abort(self):
+        """dynmo_migrate_bwd_abort: release this rank's waits of the current
+        iteration and set the sticky error (host watchdog escape hatch)."""
+        _check(lib().dynmo_migrate_bwd_abort(self.ctx.handle, self._h), "dynmo_migrate_bwd_abort")
+
     def set_ctas(self, max_ctas: int):
         """dynmo_migrate_plan_set_ctas: SM budget of the device-driven pull
         (0 = every SM), for a migration overlapped with compute."""

@@ -476,6 +476,51 @@ def main():
         for l, bufs in recvc.items():
             assert torch.equal(bufs[0].cpu(), big(l, it)), (rank, it, l, "chunked big")
             assert bool((bufs[1] == grad_val(l, it)).all()), (rank, it, l, "chunked unaligned")
+    # failure path: the last rank skips the release of its first layer (a
+    # peer that died or skipped a call).  Every rank's side stream waits for
+    # that release without bound; a host watchdog sees the iteration overrun
+    # and calls dynmo_migrate_bwd_abort, which releases this rank's own waits
+    # and sets the sticky error.  The next iteration is exact again.
+    trace("chunks: abort")
+    import time as _time
+    for it, skip in ((100, True), (101, False)):
+        main = torch.cuda.current_stream()
+        for bufs in recvc.values():
+            bufs[0].zero_()
+            bufs[1].zero_()
+        pmc.bwd_begin()
+        side_b.wait_stream(main)
+        with torch.cuda.stream(side_b):
+            pmc.backward(d_bo, d_ro, bnd, d_rn, br)
+        for l in range(begin + count - 1, begin - 1, -1):
+            Ab = (Ab @ Ab).clamp_(-1, 1)
+            sendc[l][0].copy_(bigs[(l, it % 6)])
+            sendc[l][1].fill_(grad_val(l, it))
+            if not (skip and rank == world - 1 and l == begin):
+                pmc.layer_ready(l)
+        pmc.bwd_end(d_bo, d_ro, bnd, d_rn, bs)
+        main.wait_stream(side_b)
+        ev = torch.cuda.Event()
+        ev.record(main)
+        t0 = _time.time()
+        while not ev.query() and _time.time() - t0 < 3.0:
+            _time.sleep(0.01)
+        aborted = not ev.query()
+        if aborted:
+            pmc.bwd_abort()
+        torch.cuda.synchronize()
+        flags = torch.tensor([1 if aborted else 0], device=dev)
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        if skip:
+            assert int(flags.item()) == 1, (rank, "every rank waits for the skipped release")
+            assert pmc.error() == -5, (rank, pmc.error())
+            pmc.clear_error()
+        else:
+            assert not aborted, (rank, "clean iteration after an abort")
+            for l, bufs in recvc.items():
+                assert torch.equal(bufs[0].cpu(), big(l, it % 6)), (rank, it, l, "after abort")
+                assert bool((bufs[1] == grad_val(l, it)).all()), (rank, it, l, "after abort")
+    trace("chunks: abort done")
     pmc.close()
     pmb.set_ctas(0)
     try:

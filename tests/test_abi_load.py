@@ -50,6 +50,8 @@ def test_host_argument_validation_without_gpu():
     assert L.dynmo_migrate_layer_ready(None, None, 0, None) == _lib.E_INVALID
     assert L.dynmo_migrate_layers_bwd(None, None, 1, None, None, 1, None, None, None, None) == _lib.E_INVALID
     assert L.dynmo_migrate_bwd_end(None, None, 1, None, None, 1, None, None, None, None) == _lib.E_INVALID
+    assert L.dynmo_migrate_bwd_abort(None, None) == _lib.E_INVALID
+    assert L.dynmo_ctx_p2p_error_clear(None) == _lib.E_INVALID
     ms, n = ctypes.c_double(), ctypes.c_int64()
     assert L.dynmo_ctx_profile_span(None, ctypes.byref(ms), ctypes.byref(n)) == _lib.E_INVALID
 
