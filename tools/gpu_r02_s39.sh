@@ -1,5 +1,5 @@
 #!/bin/bash
-# 2 GPUs: the worker with the abort scenario (traced, watchdog).
+# 4 GPUs: the 4-rank worker with the abort scenario (traced, watchdog).
 mkdir -p gpurun_out
 export DYNMO_MGPU_LOG_DIR=gpurun_out DYNMO_MGPU_TIMEOUT=300
 timeout 400 python -m pytest "tests/test_multigpu.py::test_exchange_and_migration[4]" -q -p no:cacheprovider > gpurun_out/s39_pytest_w4.log 2>&1; echo "w4 rc=$?"
