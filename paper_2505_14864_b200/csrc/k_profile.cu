@@ -564,34 +564,9 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
         }
     }
     DYNMO_DCHECK(run_key < 0 || run_key < (int64_t)a.n_local * ACC_N);
-    // Final flush, combined per CTA: the warps of a CTA hold consecutive tile
-    // ranges, so their last (layer, slot) run and their last E <= 16 expert
-    // histogram mostly belong to the same layer; one global atomic per
-    // distinct key instead of one per warp (all warps finish together, and
-    // ~100 same-address atomics per counter serialise in L2 at the tail).
-    constexpr int NWB = kProfThreads / 32;
-    __shared__ long long s_rkey[NWB];
-    __shared__ unsigned long long s_rsum[NWB];
-    __shared__ int s_hl[NWB], s_hE[NWB];
-    __shared__ uint32_t s_hc[NWB][16];
-    if (lane == 0) {
-        s_rkey[wib] = run_sum ? (long long)run_key : -1ll;
-        s_rsum[wib] = run_sum;
-    }
+    if (lane == 0 && run_sum) atomicAdd(&a.acc[run_key], run_sum);
     if constexpr (HAS_HIST) {
-        if (hist_layer >= 0 && hist_E <= 16) {
-            spill_regs();
-            if (lane < 16) s_hc[wib][lane] = mycnt;
-            if (lane == 0) {
-                s_hl[wib] = hist_layer;
-                s_hE[wib] = hist_E;
-            }
-            mycnt = 0;
-            hist_layer = -1;
-        } else {
-            flush_experts();
-            if (lane == 0) s_hl[wib] = -1;
-        }
+        flush_experts();
         if (exit_dirty) {
             __syncwarp();
             for (int vb = lane; vb < kExitBins; vb += 32) {
@@ -602,38 +577,10 @@ __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OP
     }
     // an expert id outside [0, E) or a time pair with end < begin
     if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicMin(a.ws_status, (int)DYNMO_E_INVALID);
-    __syncthreads();  // the CTA's warps are done: combine their final flushes
-    if (wib == 0) {
-        if (lane < NWB) {
-            const long long k = s_rkey[lane];
-            bool lead = k >= 0;
-            unsigned long long sum = 0;
-            for (int w2 = 0; w2 < NWB; ++w2) {
-                const long long k2 = s_rkey[w2];
-                if (k2 == k) {
-                    sum += s_rsum[w2];
-                    lead = lead && w2 >= lane;  // the first warp with this key adds
-                }
-            }
-            if (lead && sum) atomicAdd(&a.acc[k], sum);
-        }
-        if constexpr (HAS_HIST) {
-            for (int x = lane; x < NWB * 16; x += 32) {
-                const int w1 = x >> 4, e = x & 15;
-                const int layer = s_hl[w1];
-                if (layer < 0 || e >= s_hE[w1]) continue;
-                bool lead = true;
-                unsigned long long sum = 0;
-                for (int w2 = 0; w2 < NWB; ++w2)
-                    if (s_hl[w2] == layer) {
-                        sum += s_hc[w2][e];
-                        lead = lead && w2 >= w1;
-                    }
-                if (lead && sum) atomicAdd(&a.hist[(int64_t)layer * a.max_E + e], sum);
-            }
-        }
+    if (a.span) {  // the CTA's end: after all of its warps
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&a.span[1], globaltimer_ns());
     }
-    if (a.span && threadIdx.x == 0) atomicMax(&a.span[1], globaltimer_ns());  // the CTA's end
 }
 
 // -------------------------------------------------------------- epilogue
