@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_fused(DevMigArgs a) {
             }
         }
     }
-    __threadfence_system();
+    if (v.n_in > 0) __threadfence_system();  // (a step that moves nothing skips the system fences)
     __syncthreads();
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0 && a.bytes_recv) *a.bytes_recv = (int64_t)recvd;
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kP2PThreads) k_mig_fused(DevMigArgs a) {
     if (threadIdx.x == 0) {
         a.win->dpull_ctr = 0u;
         s_sent = 0ull;
-        __threadfence_system();
+        if (v.senders) __threadfence_system();
         for (int r = 0; r < a.nranks; ++r)
             if (v.senders & (1u << r)) st_release_sys(&a.peer_win[r]->ddone[a.me], epoch);
         if (v.ok)
