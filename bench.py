@@ -847,10 +847,19 @@ def run_pipeline(args, wl):
         span_ms, span_n = ctx.profile_span()
     prof_avg = prof_ms / max(prof_n, 1)
     span_avg = span_ms / max(span_n, 1) if span_n else 0.0
-    # our kernel nodes per step: k_profile, k_epilogue, [k_unpack(_p2p)], k_partition,
-    # k_diffuse, k_repack, [k_mig_signal, k_mig_pull, k_mig_wait | k_signal, k_pull, k_wait]
-    per_step = (5 + (1 if G > 1 else 0) + (3 if (G > 1 and args.migrate == "p2p" and moves_mine) else 0)
-                + (1 if use_map else 0))  # + k_map_stages
+    # our kernel nodes per step: k_profile, k_epilogue (the peer-memory
+    # exchange's unpack runs in its last block; the NCCL exchange adds
+    # k_unpack), k_partition, k_diffuse, k_repack, [k_map_stages], and at G > 1
+    # the migration: one k_mig_fused in the graph (device-driven), or
+    # k_signal / k_pull / k_wait per host-driven call, or none (NCCL)
+    exch_kernels = 1 if (G > 1 and args.exchange == "nccl") else 0
+    if G == 1:
+        mig_kernels = 0
+    elif dev_mig:
+        mig_kernels = 1
+    else:
+        mig_kernels = 3 if (args.migrate == "p2p" and moves_mine) else 0
+    per_step = 5 + exch_kernels + mig_kernels + (1 if use_map else 0)
     launches = per_step * args.steps
     mig_ms = phases["migrate"][0] / max(phases["migrate"][1], 1) if phases["migrate"][1] else 0.0
     if dev_mig:
