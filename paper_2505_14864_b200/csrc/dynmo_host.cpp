@@ -1195,6 +1195,11 @@ dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_la
     a.phi = d_phi;
     a.phi0 = d_phi0;
     a.fluid_x = d_fluid_x;
+    static const int spec = [] {  // DYNMO_FLUID_SPEC=0: the per-round chain (A/B knob)
+        const char *e = getenv("DYNMO_FLUID_SPEC");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.fluid_spec = spec;
     a.fluid_rounds = d_fluid_rounds;
     a.fluid_phi = d_fluid_phi;
     a.fluid_status = d_fluid_status;

@@ -257,6 +257,7 @@ cudaError_t launch_unpack_p2p(const int64_t *slots, PeerWindow *win, int32_t nra
 // ------------------------------------------------------------------ solvers
 struct SolveArgs {
     int32_t n_inst, max_layers;
+    int32_t fluid_spec;  // fluid process: speculative rounds (1) or the exact per-round chain (0)
     const int64_t *cost, *mem;
     const int32_t *layer_off, *n_stages;   // n_stages: n (partition/diffuse) or n_cur (repack)
     const int64_t *cap;

@@ -903,6 +903,7 @@ __device__ void diffuse_discrete(const SolveArgs &a, Inst &s, int q, int n, cons
 }
 
 // Fluid process of Lemma 2's proof, exact per round, one warp
+// (the A/B path, DYNMO_FLUID_SPEC=0; fluid_spec below is the default)
 // with lane s holding x_s (n <= 32).  A round: each stage picks its incident
 // edge with the largest gap > 0 (ties: lower edge index); mutually picked
 // pairs set both ends to (x_e + x_{e+1}) * 0.5 (neighbours via shuffles).
@@ -990,6 +991,164 @@ __device__ void fluid_chunks(const Inst &s, int n, const int32_t *bi, double gf,
     }
 }
 
+// Speculative fluid rounds (n <= 32, lane = stage).  The matching of the
+// fluid process settles into a period-2 pattern (even edges, odd edges:
+// config 2 repeats the matching of two rounds earlier in 254 of 256
+// rounds), so most rows of a chunk are advanced with the PREDICTED matching
+// (that of two rounds earlier): per round one shuffle of the partner and
+// one fma on the dependent chain.  A chunk opens with `e` exact rounds after
+// a misprediction (the transient before the pattern settles) and stores
+// every row; then lane j recomputes row j's TRUE matching and phi_f in
+// parallel.  A row whose true matching equals the one applied produced the
+// next row exactly as the per-round process does; at the first mispredicted
+// row the true next state is computed from it and a new chunk starts there.
+// The stop rule (phi_f <= gamma_f or max_rounds) sees the valid rows only.
+//
+// Arithmetic identity used: for doubles x, y >= 0 (no overflow, no
+// subnormal halves) fma(y, 0.5, x * 0.5) == (x + y) * 0.5 == (y + x) * 0.5
+// bit for bit (halving is exact and commutes with rounding; + commutes), and
+// an unmatched stage (partner = itself) gets fma(x, 0.5, x * 0.5) == x.
+__device__ __forceinline__ unsigned match_bits(const double *x, int n) {
+    unsigned pr = 0u, pl = 0u;  // bit t: stage t picks its right / left edge
+    double dprev = 0.0;
+    for (int t = 0; t < n; ++t) {
+        const bool hasR = t + 1 < n, hasL = t > 0;
+        const double d = hasR ? __dsub_rn(x[t], x[t + 1]) : 0.0;
+        const bool cR = hasR && (hasL ? fabs(d) > fabs(dprev) : fabs(d) > 0.0);
+        const bool cL = hasL && !cR && fabs(dprev) > 0.0;
+        pr |= (unsigned)cR << t;
+        pl |= (unsigned)cL << t;
+        dprev = d;
+    }
+    return pr & (pl >> 1);  // edge e matched: stage e picks right, stage e+1 left
+}
+
+// True matching and phi_f of one history row.  n <= 8: the row in registers,
+// every loop unrolled (as phi_row).
+__device__ __forceinline__ void verify_row(const double *row, int n, unsigned &tm, double &acc) {
+    if (n <= 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = u < n ? row[u] : 0.0;
+        unsigned pr = 0u, pl = 0u;
+        double dprev = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+            const bool hasR = t + 1 < n, hasL = t > 0 && t < n;
+            const double d = (t + 1 < 8 && hasR) ? __dsub_rn(x[t], x[t < 7 ? t + 1 : t]) : 0.0;
+            const bool cR = hasR && (hasL ? fabs(d) > fabs(dprev) : fabs(d) > 0.0);
+            const bool cL = hasL && !cR && fabs(dprev) > 0.0;
+            pr |= (unsigned)cR << t;
+            pl |= (unsigned)cL << t;
+            dprev = d;
+        }
+        tm = pr & (pl >> 1);
+        double a = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int v = u + 1; v < 8; ++v)
+                if (v < n) a = __dadd_rn(a, fabs(__dsub_rn(x[u], x[v])));
+        acc = a;
+        return;
+    }
+    tm = match_bits(row, n);
+    acc = phi_row(row, n);
+}
+
+// One exact round (fluid_chunks' body); returns the new x, m = edge mask.
+__device__ __forceinline__ double exact_round(double x, bool hasL, bool hasR, int lane, unsigned &m) {
+    const double xl = __shfl_up_sync(FULL, x, 1);
+    const double xr = __shfl_down_sync(FULL, x, 1);
+    const double dl = __dsub_rn(xl, x), dr = __dsub_rn(x, xr);
+    const double avgL = __dmul_rn(__dadd_rn(xl, x), 0.5);
+    const double avgR = __dmul_rn(__dadd_rn(x, xr), 0.5);
+    const bool cRL = fabs(dr) > fabs(dl), cR0 = fabs(dr) > 0.0, cL0 = fabs(dl) > 0.0;
+    const bool pR = hasR & ((hasL & cRL) | (!hasL & cR0));
+    const bool pL = hasL & cL0;
+    const bool qL = !pR & pL;
+    const unsigned bR = __ballot_sync(FULL, pR);
+    const unsigned bL = __ballot_sync(FULL, qL);
+    const bool mR = pR & (((bL >> 1) >> lane) & 1u);
+    const bool mL = qL & (((bR << 1) >> lane) & 1u);
+    m = bR & (bL >> 1);
+    return mR ? avgR : (mL ? avgL : x);
+}
+
+__device__ __forceinline__ int partner_of(unsigned m, int lane) {
+    return ((m >> lane) & 1u) ? lane + 1 : ((lane > 0 && ((m >> (lane - 1)) & 1u)) ? lane - 1 : lane);
+}
+
+// A round under a known matching: partner's x by one shuffle, then one fma.
+__device__ __forceinline__ double step_pair(double x, int partner) {
+    const double y = __shfl_sync(FULL, x, partner);
+    return fma(y, 0.5, __dmul_rn(x, 0.5));
+}
+
+__device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, int maxr, double *hist,
+                           double *xo, int &rr, double &ph, int &fst, int lane) {
+    double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
+    const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
+    unsigned h0 = 0u, h1 = 0u;  // true matchings of the two rounds before the next row
+    int e = 4, size = 8;        // exact rows, rows of the chunk
+    for (int base = 0;;) {
+        const unsigned s1 = h1;  // matching of round base - 1
+        unsigned used = 0u;      // lane k: the matching applied to row k
+        for (int k = 0; k < e; ++k) {
+            if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
+            unsigned m;
+            x = exact_round(x, hasL, hasR, lane, m);
+            used = lane == k ? m : used;
+            h0 = h1;
+            h1 = m;
+        }
+        {
+            const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
+            for (int k = e; k < size; ++k) {
+                if (lane < n) hist[k * kRow + lane] = x;
+                const bool odd = (k - e) & 1;
+                used = lane == k ? (odd ? h1 : h0) : used;
+                x = step_pair(x, odd ? pb : pa);
+            }
+        }
+        __syncwarp();
+        unsigned tm = 0u;
+        double acc = 0.0;
+        if (lane < size) verify_row(hist + lane * kRow, n, tm, acc);
+        const unsigned mbad = __ballot_sync(FULL, lane < size && tm != used);
+        const int fb = mbad ? __ffs(mbad) - 1 : size;  // rows 0 .. fb are exact
+        const bool stop = lane < size && lane <= fb && (acc <= gf || base + lane == maxr);
+        const unsigned mstop = __ballot_sync(FULL, stop);
+        if (mstop) {
+            const int k = __ffs(mstop) - 1;
+            rr = base + k;
+            ph = __shfl_sync(FULL, acc, k);
+            if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
+            if (lane < n) xo[lane] = hist[k * kRow + lane];
+            return;
+        }
+        if (fb < size) {
+            // the true next state from the first mispredicted row
+            const unsigned tb = __shfl_sync(FULL, tm, fb);
+            const unsigned tp = __shfl_sync(FULL, tm, fb > 0 ? fb - 1 : 0);
+            const double xv = lane < n ? hist[fb * kRow + lane] : 0.0;
+            h0 = fb > 0 ? tp : s1;
+            h1 = tb;
+            x = step_pair(xv, partner_of(tb, lane));
+            base += fb + 1;
+            e = 4;
+            size = min(kChunk, max(8, 2 * (fb + 1)));
+        } else {
+            h0 = __shfl_sync(FULL, used, size - 2);
+            h1 = __shfl_sync(FULL, used, size - 1);
+            base += size;
+            e = 0;
+            size = min(kChunk, size * 4);
+        }
+        __syncwarp();
+    }
+}
+
 __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, const int32_t *bi,
                               int fst, double *hist, int lane) {
     const double gf = a.gamma_fluid ? a.gamma_fluid[q] : 0.0;
@@ -1007,7 +1166,8 @@ __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, c
     int rr = 0;
     double ph = 0.0;
     if (n <= 32) {
-        fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+        if (a.fluid_spec) fluid_spec(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+        else fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
     } else if (lane == 0) {
         // n > 32: serial on lane 0 over shared memory (s.x reused as fp64)
         double *sxf = reinterpret_cast<double *>(s.x);

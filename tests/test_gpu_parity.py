@@ -542,6 +542,34 @@ def test_diffuse_random(D, ctx, with_mem, Lmax, maxr):
     _check_diffuse(D, ctx, insts, with_mem, maxr)
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_diffuse_fluid_long(D, ctx, seed):
+    """The speculative fluid rounds of k_diffuse (n <= 32: chunks advanced
+    with the matching of two rounds earlier, verified row by row, rolled back
+    at the first mispredicted row): long fluid runs (max_rounds 4096, tiny
+    gamma_f) from skewed, random and near-periodic starts, n = 2 .. 32, fluid
+    loads bit-equal to the oracle's per-round process."""
+    g = np.random.default_rng(1000 + seed)
+    insts = []
+    for q in range(24):
+        n = int(g.integers(2, 33))
+        Ly = int(g.integers(n, 4 * n + 40))
+        kind = q % 3
+        cost = g.integers(0, 1000, Ly)
+        if kind == 1:
+            cost = (g.pareto(1.2, Ly) * 100).astype(np.int64)  # skewed: many rollbacks
+        elif kind == 2:
+            cost = np.full(Ly, 7, np.int64)
+            cost[int(g.integers(0, Ly))] = 5000  # one hot layer: period-2 after the start
+        inner = np.sort(g.choice(np.arange(1, Ly), n - 1, replace=False))
+        bnd = np.concatenate([[0], inner, [Ly]]).astype(np.int32)
+        x0 = oracle.stage_loads(cost, bnd).astype(float)
+        x = dict(cost=cost, n=n, bnd_in=bnd, gamma=0, mem=None, cap=0,
+                 gamma_f=float(g.choice([0.0, 1e-12, 1e-6])) * oracle.phi_f64(x0))
+        insts.append(x)
+    _check_diffuse(D, ctx, insts, False, 4096)
+
+
 def test_diffuse_invalid(D, ctx):
     insts = [dict(cost=np.array([1, 2, 3]), n=2, bnd_in=np.array([0, 3, 3], np.int32), mem=None, cap=0),
              dict(cost=np.array([1, -2, 3]), n=2, bnd_in=np.array([0, 1, 3], np.int32), mem=None, cap=0),
