@@ -68,6 +68,9 @@ def parse(argv=None):
     ap.add_argument("--host-migrate", action="store_true",
                     help="host-driven migration (D2H of the boundaries, then the migrate call) "
                          "instead of the device-driven call inside the step's graph")
+    ap.add_argument("--result-read", choices=["publish", "copy"], default="publish",
+                    help="the step's result (new boundaries + statuses) to the host: stored by a kernel "
+                         "into mapped pinned memory (dynmo_publish, default) or a D2H copy node")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch every call eagerly instead of replaying a CUDA graph")
     ap.add_argument("--ref-budget", type=float, default=120.0,
@@ -688,7 +691,10 @@ def run_pipeline(args, wl):
         if dev_mig and pmig is not None:
             with torch.cuda.nvtx.range("dynmo.migrate"):
                 pmig.device(d_bold, d_ranks, part["bnd"], d_rmap, d_bytes[0:1], d_bytes[1:2])
-        res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
+        if args.result_read == "publish":
+            D.publish(ctx, res_d[:n_host], res_h[:n_host])
+        else:
+            res_h[:n_host].copy_(res_d[:n_host], non_blocking=True)
         ev_res.record(main)
         for sd in side:
             main.wait_stream(sd)
@@ -849,7 +855,7 @@ def run_pipeline(args, wl):
     span_avg = span_ms / max(span_n, 1) if span_n else 0.0
     # our kernel nodes per step: k_profile, k_epilogue (the peer-memory
     # exchange's unpack runs in its last block; the NCCL exchange adds
-    # k_unpack), k_partition, k_diffuse, k_repack, [k_map_stages], and at G > 1
+    # k_unpack), k_partition, k_diffuse, k_repack, [k_map_stages], [k_publish], and at G > 1
     # the migration: one k_mig_fused in the graph (device-driven), or
     # k_signal / k_pull / k_wait per host-driven call, or none (NCCL)
     exch_kernels = 1 if (G > 1 and args.exchange == "nccl") else 0
@@ -859,7 +865,8 @@ def run_pipeline(args, wl):
         mig_kernels = 1
     else:
         mig_kernels = 3 if (args.migrate == "p2p" and moves_mine) else 0
-    per_step = 5 + exch_kernels + mig_kernels + (1 if use_map else 0)
+    per_step = 5 + exch_kernels + mig_kernels + (1 if use_map else 0) + (
+        args.result_read == "publish" and n_host * 4 <= D.PUBLISH_KERNEL_MAX)
     launches = per_step * args.steps
     mig_ms = phases["migrate"][0] / max(phases["migrate"][1], 1) if phases["migrate"][1] else 0.0
     if dev_mig:
@@ -943,6 +950,8 @@ def run_pipeline(args, wl):
                               if dev_mig else "host-driven peer-memory pull" if args.migrate == "p2p"
                               else "host-driven NCCL send/recv"),
                 "graph": bool(args.graph),
+                "result_read": ("kernel store into mapped pinned memory (dynmo_publish)"
+                                if args.result_read == "publish" else "D2H copy node"),
                 "stage_placement": ("migration-minimising (dynmo_map_stages, NEXT-3)" if use_map
                                     else f"stage s on GPU floor(s*G/{n}) before and after")},
             "roofline": roofline(bytes_all[worst], prof_at_min[worst], per_rank_gbs, G, args.config, span_all[worst]),
@@ -1044,7 +1053,10 @@ def run_batch(args, wl):
             D.partition_stages(ctx, batch, cost, mem=mem, cap=cap, bnd=part["bnd"], bottleneck=part["bott"],
                                status=part["st"])
         main.wait_stream(side)
-        res_h.copy_(res_d, non_blocking=True)
+        if args.result_read == "publish":
+            D.publish(ctx, res_d, res_h)
+        else:
+            res_h.copy_(res_d, non_blocking=True)
         ev_res.record(main)
 
     solve_async()
@@ -1136,14 +1148,18 @@ def run_batch(args, wl):
             "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": wl.config(G),
-            "setup": {"graph": True, "exchange": "none (independent instances)", "migration": "none"},
+            "setup": {"graph": True, "exchange": "none (independent instances)", "migration": "none",
+                      "result_read": ("kernel store into mapped pinned memory (dynmo_publish)"
+                                      if args.result_read == "publish" else "D2H copy node")},
             "instances_per_s": round(wl.N_INST / (ms * 1e-3), 1),
             "roofline": roofline(bytes_all[worst], prof_all[worst], per_rank_gbs, G, args.config, span_all[worst]),
             "step_ms": step_stats(step_ms),
             "solution": {"workers_before": int(sum(n_cur_sum)), "workers_after_repack": int(sum(n_new_sum))},
             "e2e": {"value": round(e2e_ms, 4), "unit": "ms", "h2d_bytes_per_step": int(words.nbytes),
                     "d2h_bytes_per_step": int(res_h.numel() * 4), "steps": args.e2e_steps},
-            "gpu_launches": 4 * args.steps,  # k_profile, k_epilogue, k_partition, k_repack
+            # k_profile, k_epilogue, k_partition, k_repack, [k_publish]
+            "gpu_launches": (4 + (args.result_read == "publish"
+                                  and res_h.numel() * 4 <= D.PUBLISH_KERNEL_MAX)) * args.steps,
             "clocks": clk.summary(),
         }
         if G == 1 and not args.no_cpu_baseline:

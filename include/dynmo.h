@@ -266,6 +266,23 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
  * in a CUDA graph.  d_slot: int64 device pointer, caller-owned. */
 dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream);
 
+/* Publish a step result to the host without a copy-engine transfer: enqueues
+ * on `stream` a kernel that stores `bytes` bytes of device memory d_src into
+ * h_dst, page-locked host memory mapped into the device address space
+ * (cudaHostAlloc / cudaMallocHost / torch pin_memory, unified addressing),
+ * then fences system-wide.  The bytes are visible to the host once work
+ * recorded after it on the stream (an event) has completed.  The kernel
+ * starts programmatically (PDL) and waits for the preceding kernel.  In the
+ * bench's step it replaces the D2H copy node of the new boundaries + status
+ * (the "result read" of the per-step path, "the new partition is
+ * broadcast"): ~6 us of copy-engine latency per step for tens of bytes.
+ * Results above 4 KiB go through cudaMemcpyAsync instead (GPU stores to host
+ * memory run at a few GB/s: the copy engine is faster there).
+ * Capturable.  Errors: INVALID for null pointers, bytes < 0, d_src not device
+ * memory, or h_dst (first or last byte) not mapped page-locked host memory --
+ * nothing is enqueued then.  bytes = 0 is a no-op. */
+dynmo_status dynmo_publish(dynmo_ctx ctx, const void *d_src, void *h_dst, int64_t bytes, dynmo_stream stream);
+
 /* -------------------------------------------------------------- solvers --
  * Batched instance layout shared by calls 2-4 (one CTA per instance):
  *   instance q owns layers [d_layer_off[q], d_layer_off[q+1]) of d_cost /

@@ -1113,6 +1113,45 @@ dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream
     return DYNMO_OK;
 }
 
+constexpr int64_t kPublishKernelMax = 4096;  // larger results: the copy engine
+
+dynmo_status dynmo_publish(dynmo_ctx ctx, const void *d_src, void *h_dst, int64_t bytes, dynmo_stream stream) {
+    if (!ctx || !d_src || !h_dst) return invalid("null ctx/src/dst");
+    if (bytes < 0) return invalid("bytes < 0");
+    if (bytes == 0) return DYNMO_OK;
+    DeviceGuard g(ctx->device);
+    // h_dst: page-locked host memory mapped into the device address space
+    // (cudaHostAlloc / cudaMallocHost / torch pin_memory under UVA); both
+    // ends of the range must be, or nothing is enqueued
+    void *d_dst = nullptr;
+    for (int end = 0; end < 2; ++end) {
+        cudaPointerAttributes at{};
+        const char *q = (const char *)h_dst + (end ? bytes - 1 : 0);
+        if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+            cudaGetLastError();
+            return invalid("h_dst is not CUDA-registered host memory");
+        }
+        if (at.type != cudaMemoryTypeHost || !at.devicePointer)
+            return invalid("h_dst is not page-locked, device-mapped host memory");
+        if (!end) d_dst = at.devicePointer;
+    }
+    cudaPointerAttributes sa{};
+    if (cudaPointerGetAttributes(&sa, d_src) != cudaSuccess || sa.type != cudaMemoryTypeDevice) {
+        cudaGetLastError();
+        return invalid("d_src is not device memory");
+    }
+    // GPU stores to host memory run at a few GB/s (tools/publish_bench.py:
+    // 49 KB 15.4 us vs 11.4 us by the copy engine); the kernel wins only
+    // for small results, where it saves the copy node's fixed latency
+    if (bytes > kPublishKernelMax) {
+        CUDA_TRY(cudaMemcpyAsync(h_dst, d_src, (size_t)bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+                 "publish copy");
+        return DYNMO_OK;
+    }
+    CUDA_TRY(launch_publish(d_src, d_dst, bytes, (cudaStream_t)stream), "k_publish launch");
+    return DYNMO_OK;
+}
+
 dynmo_status dynmo_map_stages(dynmo_ctx ctx, int32_t n_layers, int32_t n_old, const int32_t *d_bnd_old,
                               const int32_t *d_rank_old, int32_t n_new, const int32_t *d_bnd_new,
                               const int64_t *d_bytes, int32_t G, uint32_t allowed, const int32_t *d_slot_rank,

@@ -245,6 +245,7 @@ cudaError_t launch_map_stages(const MapArgs &a, cudaStream_t s);
 
 cudaError_t launch_epilogue(const EpiArgs &a, cudaStream_t s);
 cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s);
+cudaError_t launch_publish(const void *d_src, void *d_dst, int64_t bytes, cudaStream_t s);
 cudaError_t launch_unpack(const int64_t *slot_recv, int32_t nranks, int32_t n_total,
                           int64_t *cost_out, int64_t *mem_out, int32_t *status_out,
                           cudaStream_t s);

@@ -252,6 +252,24 @@ def timestamp(ctx: Context, slot: torch.Tensor, stream=None):
     _check(lib().dynmo_timestamp(ctx.handle, _ptr(slot), _stream(stream)), "dynmo_timestamp")
 
 
+PUBLISH_KERNEL_MAX = 4096  # dynmo_publish: larger results go through the copy engine (no kernel)
+
+
+def publish(ctx: Context, src: torch.Tensor, dst: torch.Tensor, stream=None):
+    """dynmo_publish: the device tensor `src` stored by a kernel into the
+    pinned host tensor `dst` (same byte size, contiguous): the step's result
+    read without a copy-engine D2H node.  Visible on the host once an event
+    recorded after it has completed."""
+    if not src.is_cuda or dst.is_cuda or not dst.is_pinned():
+        raise ValueError("src must be a device tensor and dst a pinned host tensor")
+    if not (src.is_contiguous() and dst.is_contiguous()):
+        raise ValueError("src and dst must be contiguous")
+    nb = src.numel() * src.element_size()
+    if nb != dst.numel() * dst.element_size():
+        raise ValueError("src and dst differ in size")
+    _check(lib().dynmo_publish(ctx.handle, _ptr(src), dst.data_ptr(), nb, _stream(stream)), "dynmo_publish")
+
+
 def profile_layers(ctx: Context, plan: ProfilePlan, coef: torch.Tensor, *, frozen=None,
                    mem_local=None, counters=None, hist=None, cost=None, mem=None, status=None,
                    stream=None):

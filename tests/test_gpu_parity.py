@@ -1082,6 +1082,50 @@ def test_ctx_barrier_timing_detach_and_split_single(D, L, ctx):
     del g
 
 
+def test_publish_to_pinned_host(D, L, ctx):
+    """dynmo_publish: device bytes stored by a kernel into mapped pinned host
+    memory -- every size class (0, bytes, one vector, a partial CTA, several
+    CTAs), aligned and unaligned ends, eager and inside a replayed CUDA graph;
+    non-pinned / device destinations and host sources are INVALID."""
+    import ctypes
+    g = torch.Generator().manual_seed(5)
+    for nb in (0, 1, 7, 16, 48, 4096, 49_156, 1 << 20):
+        for off in (0, 3, 16):
+            src_full = torch.randint(0, 256, (nb + off + 1,), dtype=torch.uint8, generator=g).cuda()
+            dst_full = torch.zeros(nb + off + 5, dtype=torch.uint8).pin_memory()
+            src, dst = src_full[off:off + nb], dst_full[off:off + nb]
+            if nb == 0:
+                assert L.lib().dynmo_publish(ctx.handle, src_full.data_ptr(), dst_full.data_ptr(), 0, None) == 0
+                continue
+            D.publish(ctx, src, dst)
+            torch.cuda.synchronize()
+            assert torch.equal(dst, src.cpu()), (nb, off)
+            assert not dst_full[off + nb:].any() and not dst_full[:off].any(), (nb, off)
+    # inside a graph: the replay publishes the current device contents
+    src = torch.arange(40, dtype=torch.int32, device="cuda")
+    dst = torch.zeros(40, dtype=torch.int32).pin_memory()
+    side = torch.cuda.Stream()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=side):
+        src.add_(1)
+        D.publish(ctx, src, dst)
+    for k in range(3):
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(dst, torch.arange(40, dtype=torch.int32) + k + 1), k
+    del gr
+    # errors: pageable host destination, device destination, host source
+    pageable = torch.zeros(64, dtype=torch.uint8)
+    dsrc = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    assert L.lib().dynmo_publish(ctx.handle, dsrc.data_ptr(), pageable.data_ptr(), 64, None) == L.E_INVALID
+    assert L.lib().dynmo_publish(ctx.handle, dsrc.data_ptr(), dsrc.data_ptr(), 64, None) == L.E_INVALID
+    pin = torch.zeros(64, dtype=torch.uint8).pin_memory()
+    assert L.lib().dynmo_publish(ctx.handle, pin.data_ptr(), pin.data_ptr(), 64, None) == L.E_INVALID
+    with pytest.raises(ValueError):
+        D.publish(ctx, dsrc, pageable)
+    torch.cuda.synchronize()
+
+
 def test_profile_span_clock(D, L, ctx):
     """With the profile phase timed, every k_profile launch (eager and graph
     replays) also records its device-clock span (dynmo_ctx_profile_span):

@@ -1,7 +1,8 @@
 #!/bin/bash
-# 2 GPUs: the worker with the abort scenario (traced, watchdog).
+# 1 GPU: config-2 step timeline (branch completion offsets) with the
+# speculative fluid rounds and with the per-round chain.
 mkdir -p gpurun_out
-export DYNMO_MGPU_LOG_DIR=gpurun_out DYNMO_MGPU_TIMEOUT=300
-timeout 400 python -m pytest "tests/test_multigpu.py::test_exchange_and_migration[2]" -q -p no:cacheprovider > gpurun_out/s38_pytest_w2.log 2>&1; echo "w2 rc=$?"
-grep -h "TRACE 0 chunks\|TIMEOUT\|Error\|WATCHDOG\|assert" gpurun_out/mgpu_worker_w2.log | tail -12
-cp gpurun_out/mgpu_worker_w2.log gpurun_out/s38_worker_w2.log
+for sp in 1 0; do
+  DYNMO_FLUID_SPEC=$sp timeout 300 python tools/step_timeline.py > gpurun_out/s38_timeline_spec$sp.json 2> gpurun_out/s38_timeline_spec$sp.err; echo "spec$sp rc=$?"
+  cat gpurun_out/s38_timeline_spec$sp.json; tail -3 gpurun_out/s38_timeline_spec$sp.err
+done

@@ -1,7 +1,7 @@
 #!/bin/bash
-# 4 GPUs: the 4-rank worker with the abort scenario (traced, watchdog).
+# 1 GPU: config-2 step graph -- three solver branches vs one stream, PDL on/off.
 mkdir -p gpurun_out
-export DYNMO_MGPU_LOG_DIR=gpurun_out DYNMO_MGPU_TIMEOUT=300
-timeout 400 python -m pytest "tests/test_multigpu.py::test_exchange_and_migration[4]" -q -p no:cacheprovider > gpurun_out/s39_pytest_w4.log 2>&1; echo "w4 rc=$?"
-grep -h "TRACE 0 chunks\|TIMEOUT\|Error\|WATCHDOG\|assert" gpurun_out/mgpu_worker_w4.log | tail -12
-cp gpurun_out/mgpu_worker_w4.log gpurun_out/s39_worker_w4.log
+for pdl in 1 0; do
+  DYNMO_PDL=$pdl timeout 300 python tools/step_timeline.py > gpurun_out/s39_timeline_pdl$pdl.json 2> gpurun_out/s39_timeline_pdl$pdl.err; echo "pdl$pdl rc=$?"
+  cat gpurun_out/s39_timeline_pdl$pdl.json; tail -3 gpurun_out/s39_timeline_pdl$pdl.err
+done

@@ -1,7 +1,7 @@
 #!/bin/bash
-# 1 GPU: regression of the final code: GPU tier, smoke, bench config 2.
+# 1 GPU: publish test; result-read microbench over bytes per CTA.
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/s41_pytest_gpu.log 2>&1; echo "tier rc=$?"; tail -2 gpurun_out/s41_pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
-timeout 600 python bench.py > gpurun_out/s41_bench.json 2>/dev/null; echo "bench rc=$?"
-python -c "import json;d=json.loads(open('gpurun_out/s41_bench.json').read().strip().splitlines()[-1]);r=d['roofline'];print(d['value'],r['frac'],r['frac_span'],d['clocks'])"
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "publish" > gpurun_out/s41_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/s41_pytest.log
+for cb in 16384 4096 1024 256; do
+  DYNMO_PUBLISH_CTA_BYTES=$cb timeout 300 python tools/publish_bench.py
+done

@@ -1,11 +1,10 @@
 #!/bin/bash
-# 2 GPUs: fence-skip in the fused migration: worker (2 ranks), bench configs 3
-# and 2 at N = 2 (two runs each).
+# 1 GPU: publish test (kernel <= 4 KiB, copy engine above), full GPU tier,
+# bench configs 2..5 (default = publish) and the publish microbench.
 mkdir -p gpurun_out
-export DYNMO_MGPU_LOG_DIR=gpurun_out DYNMO_MGPU_TIMEOUT=300
-timeout 400 python -m pytest "tests/test_multigpu.py::test_exchange_and_migration[2]" -q -p no:cacheprovider > gpurun_out/s42_pytest_w2.log 2>&1; echo "w2 rc=$?"
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29642"
-for rep in 1 2; do for c in 3 2; do
-  timeout 300 $TR bench.py --config $c --gpus 2 --steps 300 > gpurun_out/s42.json 2>/dev/null
-  python -c "import json;d=json.loads(open('gpurun_out/s42.json').read().strip().splitlines()[-1]);print('cfg$c', d['value'], d['phases_ms_per_launch_diagnostic'].get('migrate'))"
-done; done
+timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/s42_pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/s42_pytest_gpu.log
+timeout 300 python tools/publish_bench.py > gpurun_out/s42_publish_bench.jsonl 2>&1; cat gpurun_out/s42_publish_bench.jsonl
+for c in 2 3 4 5; do
+  timeout 300 python bench.py --config $c > gpurun_out/s42_bench_cfg${c}_n1.json 2>gpurun_out/s42_bench_cfg${c}_n1.err
+  echo "cfg$c rc=$? $(python -c "import json;d=json.load(open('gpurun_out/s42_bench_cfg${c}_n1.json'));print(d['value'],d['e2e']['value'],d['gpu_launches'],d['roofline']['frac'],d['clocks'])" 2>&1 | tail -1)"
+done

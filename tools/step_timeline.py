@@ -55,8 +55,9 @@ def main():
     def mk():
         return torch.cuda.Event(enable_timing=True, external=True)
 
-    def step(ev=None, parts=("diffuse", "repack", "partition", "d2h")):
+    def step(ev=None, parts=("diffuse", "repack", "partition", "d2h"), serial=False):
         main = torch.cuda.current_stream()
+        br = [main, main] if serial else side
         if ev is not None:
             ev["start"].record(main)
         D.profile_layers(ctx, plan, coef, mem_local=mem_local, cost=cost, mem=mem, status=pst)
@@ -65,21 +66,25 @@ def main():
         for sd in side:
             sd.wait_stream(main)
         if "diffuse" in parts:
-            with torch.cuda.stream(side[0]):
+            with torch.cuda.stream(br[0]):
                 D.diffuse_balance(ctx, batch, cost, bnd_in, mem=mem, cap=cap, gamma=gamma, gamma_fluid=gamma_f,
                                   max_rounds=256, out=dif)
                 if ev is not None:
-                    ev["diffuse"].record(side[0])
+                    ev["diffuse"].record(br[0])
         if "repack" in parts:
-            with torch.cuda.stream(side[1]):
+            with torch.cuda.stream(br[1]):
                 D.repack_workers(ctx, batch, cost, floor=floor, bound=bound, mem=mem, cap=cap, out=rep)
                 if ev is not None:
-                    ev["repack"].record(side[1])
+                    ev["repack"].record(br[1])
         if "partition" in parts:
             bnd, _, _, st = D.partition_stages(ctx, batch, cost, mem=mem, cap=cap)
             part["bnd"] = bnd
             if ev is not None:
                 ev["partition"].record(main)
+            if "pub" in parts:
+                D.publish(ctx, bnd, res_h[:n + 1])
+                if ev is not None:
+                    ev["d2h"].record(main)
             if "d2h" in parts:
                 res_h[:n + 1].copy_(bnd, non_blocking=True)
                 if ev is not None:
@@ -112,8 +117,8 @@ def main():
                 offs[k].append(ev["start"].elapsed_time(ev[k]) * 1e3)
     out["timeline_us_from_start"] = {k: round(float(np.median(v)), 2) for k, v in offs.items()}
 
-    def timed(parts, reps=40):
-        gg = capture(lambda: step(None, parts))
+    def timed(parts, reps=40, serial=False):
+        gg = capture(lambda: step(None, parts, serial))
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ts = []
         for i in range(reps + 5):
@@ -128,6 +133,10 @@ def main():
 
     out["graph_us"] = {
         "full": timed(("diffuse", "repack", "partition", "d2h")),
+        "full_one_stream": timed(("diffuse", "repack", "partition", "d2h"), serial=True),
+        "full_publish": timed(("diffuse", "repack", "partition", "pub")),
+        "profile+partition+publish": timed(("partition", "pub")),
+        "profile+3_solvers_no_d2h": timed(("diffuse", "repack", "partition")),
         "profile_only": timed(()),
         "profile+partition": timed(("partition",)),
         "profile+partition+d2h": timed(("partition", "d2h")),
