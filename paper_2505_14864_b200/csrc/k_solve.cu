@@ -825,30 +825,68 @@ __device__ void diffuse_discrete(const SolveArgs &a, Inst &s, int q, int n, cons
                 break;
             }
             // best re-split of edge e: min of (pair max, |j - b|, j) over
-            // mem-feasible j in (b_e, b_{e+2}); lane = edge
+            // mem-feasible j in (b_e, b_{e+2}).  G lanes per edge (G the
+            // largest power of two with (n - 1) G <= 32), lane sub of the
+            // group scans j = lo + 1 + sub, + G, ...; the group's minimum by
+            // shuffles (ties on (max, dist): the lower j, as the serial scan)
             int any = 0;
-            for (int e = lane; e + 1 < n; e += 32) {
-                const int lo = s.b[e], hi = s.b[e + 2], cur = s.b[e + 1];
-                const int64_t Plo = s.P[lo], Phi = s.P[hi];
-                int64_t km = I64MAX;
-                int kd = 0, kj = -1;
-                for (int j = lo + 1; j < hi; ++j) {
-                    if constexpr (MEM)
-                        if (s.M[j] - s.M[lo] > cap || s.M[hi] - s.M[j] > cap) continue;
-                    const int64_t l = s.P[j] - Plo, r = Phi - s.P[j];
-                    const int64_t m = l > r ? l : r;
-                    const int d = j > cur ? j - cur : cur - j;
-                    // j ascending, so equal (max, dist) keeps the lower j
-                    if (kj < 0 || m < km || (m == km && d < kd)) {
-                        km = m;
-                        kd = d;
-                        kj = j;
+            {
+                // target >= 2 candidates per lane under a memory cap (its
+                // test lengthens an iteration), >= 8 without: below that the
+                // group reduction costs more than the shorter scan saves
+                // (config 2, 48 layers / 8 stages: 10.6 -> 9.0 us with the
+                // cap at G = 4; 7.2 -> 7.8 us without it at G = 4)
+                const int ne = n - 1;
+                const int per_lane = MEM ? 2 : 8;
+                int G = 32;
+                while (G > 1 && (ne * G > 32 || G * per_lane > (2 * s.L) / n)) G >>= 1;
+                const int sub = lane & (G - 1);
+                for (int e0 = 0; e0 < ne; e0 += 32 / G) {
+                    const int e = e0 + lane / G;
+                    int64_t km = I64MAX;
+                    int kd = 0, kj = -1;
+                    if (e < ne) {
+                        const int lo = s.b[e], hi = s.b[e + 2], cur = s.b[e + 1];
+                        const int64_t Plo = s.P[lo], Phi = s.P[hi];
+                        int64_t Mlo = 0, Mhi = 0;
+                        if constexpr (MEM) {
+                            Mlo = s.M[lo];
+                            Mhi = s.M[hi];
+                        }
+                        for (int j = lo + 1 + sub; j < hi; j += G) {
+                            if constexpr (MEM)
+                                if (s.M[j] - Mlo > cap || Mhi - s.M[j] > cap) continue;
+                            const int64_t Pj = s.P[j];
+                            const int64_t l = Pj - Plo, r = Phi - Pj;
+                            const int64_t m = l > r ? l : r;
+                            const int d = j > cur ? j - cur : cur - j;
+                            // j ascending, so equal (max, dist) keeps the lower j
+                            if (kj < 0 || m < km || (m == km && d < kd)) {
+                                km = m;
+                                kd = d;
+                                kj = j;
+                            }
+                        }
+                    }
+                    for (int o = 1; o < G; o <<= 1) {
+                        const int64_t om = __shfl_xor_sync(FULL, km, o);
+                        const int od = __shfl_xor_sync(FULL, kd, o);
+                        const int oj = __shfl_xor_sync(FULL, kj, o);
+                        const bool take = oj >= 0 && (kj < 0 || om < km ||
+                                                      (om == km && (od < kd || (od == kd && oj < kj))));
+                        if (take) {
+                            km = om;
+                            kd = od;
+                            kj = oj;
+                        }
+                    }
+                    if (e < ne && sub == 0) {
+                        const int64_t pm = s.x[e] > s.x[e + 1] ? s.x[e] : s.x[e + 1];
+                        const int t = (kj >= 0 && km < pm) ? kj : -1;
+                        s.tgt[e] = t;
+                        any |= t >= 0;
                     }
                 }
-                const int64_t pm = s.x[e] > s.x[e + 1] ? s.x[e] : s.x[e + 1];
-                const int t = (kj >= 0 && km < pm) ? kj : -1;
-                s.tgt[e] = t;
-                any |= t >= 0;
             }
             any = __any_sync(FULL, any);
             if (!any) {
@@ -1024,7 +1062,9 @@ __device__ __forceinline__ unsigned match_bits(const double *x, int n) {
 }
 
 // True matching and phi_f of one history row.  n <= 8: the row in registers,
-// every loop unrolled (as phi_row).
+// every loop unrolled (as phi_row).  (A variant that skipped phi_f wherever
+// the bound phi_f >= (n - 1)(max - min) exceeded gamma_f measured no faster
+// on config 2 and slower at L = 127: the range chain costs what it saves.)
 __device__ __forceinline__ void verify_row(const double *row, int n, unsigned &tm, double &acc) {
     if (n <= 8) {
         double x[8];

@@ -24,12 +24,14 @@ d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
 cubin = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
 sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cubin)], capture_output=True, text=True).stdout
-line_of = {}
+# several instantiations may match the name: take the one whose instruction
+# count equals the profiled kernel's (else the first match)
+cands = []
 for sec in re.split(r"\n\s*\.section\s+", sass):
     h = sec.split("\n")[0]
     if not sec.startswith(".text.") or kname not in h:
         continue
-    cur = None
+    lo, cur = {}, None
     for ln in sec.split("\n"):
         m = re.search(r'//## File "([^"]+)", line (\d+)', ln)
         if m:
@@ -37,8 +39,11 @@ for sec in re.split(r"\n\s*\.section\s+", sass):
             continue
         mm = re.match(r"\s+/\*([0-9a-f]+)\*/", ln)
         if mm:
-            line_of[int(mm.group(1), 16)] = cur
-    break
+            lo[int(mm.group(1), 16)] = cur
+    cands.append((h, lo))
+pick = [c for c in cands if len(c[1]) == len(data)] or cands
+print("section", pick[0][0][:100], "of", len(cands))
+line_of = pick[0][1]
 agg = collections.Counter()
 ex = collections.Counter()
 for r in data:

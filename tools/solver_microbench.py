@@ -1,5 +1,6 @@
 """Isolated timing of the solver kernels (CUDA events over many launches)."""
 import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
@@ -12,24 +13,7 @@ cost2 = np.load(os.path.join(os.path.dirname(__file__), "cfg2_cost.npy")) if os.
     os.path.join(os.path.dirname(__file__), "cfg2_cost.npy")) else np.random.default_rng(0).integers(0, 2_400_000, 48)
 
 
-def t(fn, iters=20, reps=20):
-    """Device time per call: capture `iters` back-to-back calls in a CUDA graph
-    and time graph replays (no host launch overhead inside)."""
-    fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
-        for _ in range(iters):
-            fn()
-    g.replay()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        g.replay()
-    b.record()
-    torch.cuda.synchronize()
-    return round(a.elapsed_time(b) / (iters * reps) * 1e3, 2)
+from solver_microbench_t import t  # noqa: E402
 
 
 res = {}
