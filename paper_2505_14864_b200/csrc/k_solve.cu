@@ -1125,8 +1125,19 @@ __device__ __forceinline__ double step_pair(double x, int partner) {
     return fma(y, 0.5, __dmul_rn(x, 0.5));
 }
 
+#ifdef DYNMO_FLUID_PROF  // diagnostic build only: phase cycles into fluid_x (tools/fluid_prof.py)
+__shared__ long long g_fprof_t0;
+#define FPROF(v) const long long v = clock64()
+#else
+#define FPROF(v)
+#endif
+
 __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, int maxr, double *hist,
                            double *xo, int &rr, double &ph, int &fst, int lane) {
+#ifdef DYNMO_FLUID_PROF
+    long long c_ex = 0, c_sp = 0, c_ve = 0, chunks = 0;
+    const long long c_in = clock64();
+#endif
     double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
     const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
     unsigned h0 = 0u, h1 = 0u;  // true matchings of the two rounds before the next row
@@ -1134,6 +1145,7 @@ __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, i
     for (int base = 0;;) {
         const unsigned s1 = h1;  // matching of round base - 1
         unsigned used = 0u;      // lane k: the matching applied to row k
+        FPROF(ta);
         for (int k = 0; k < e; ++k) {
             if (lane < n) hist[k * kRow + lane] = x;  // x(base + k)
             unsigned m;
@@ -1142,6 +1154,7 @@ __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, i
             h0 = h1;
             h1 = m;
         }
+        FPROF(tb);
         {
             const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
             for (int k = e; k < size; ++k) {
@@ -1152,6 +1165,7 @@ __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, i
             }
         }
         __syncwarp();
+        FPROF(tc);
         unsigned tm = 0u;
         double acc = 0.0;
         if (lane < size) verify_row(hist + lane * kRow, n, tm, acc);
@@ -1159,12 +1173,32 @@ __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, i
         const int fb = mbad ? __ffs(mbad) - 1 : size;  // rows 0 .. fb are exact
         const bool stop = lane < size && lane <= fb && (acc <= gf || base + lane == maxr);
         const unsigned mstop = __ballot_sync(FULL, stop);
+        FPROF(td);
+#ifdef DYNMO_FLUID_PROF
+        c_ex += tb - ta;
+        c_sp += tc - tb;
+        c_ve += td - tc;
+        ++chunks;
+#endif
         if (mstop) {
             const int k = __ffs(mstop) - 1;
             rr = base + k;
             ph = __shfl_sync(FULL, acc, k);
             if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
             if (lane < n) xo[lane] = hist[k * kRow + lane];
+#ifdef DYNMO_FLUID_PROF
+            __syncwarp();
+            const long long te = clock64();
+            if (lane == 0) {
+                xo[0] = (double)(c_in - g_fprof_t0);  // kernel start -> fluid entry
+                xo[1] = (double)c_ex;
+                xo[2] = (double)c_sp;
+                xo[3] = (double)c_ve;
+                xo[4] = (double)(te - c_in - c_ex - c_sp - c_ve);  // bookkeeping
+                xo[5] = (double)chunks;
+                xo[6] = (double)(te - g_fprof_t0);
+            }
+#endif
             return;
         }
         if (fb < size) {
@@ -1257,6 +1291,9 @@ __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
     extern __shared__ __align__(16) char smem[];
+#ifdef DYNMO_FLUID_PROF
+    if (threadIdx.x == 0) g_fprof_t0 = clock64();
+#endif
     const int q = blockIdx.x, lane = threadIdx.x;
     const bool fluid = blockIdx.y == 1;
     Inst s = carve(smem, a.max_layers, MEM && !fluid);
