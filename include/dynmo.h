@@ -269,9 +269,9 @@ dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream
 /* Publish a step result to the host without a copy-engine transfer: enqueues
  * on `stream` a kernel that stores `bytes` bytes of device memory d_src into
  * h_dst, page-locked host memory mapped into the device address space
- * (cudaHostAlloc / cudaMallocHost / torch pin_memory, unified addressing),
- * then fences system-wide.  The bytes are visible to the host once work
- * recorded after it on the stream (an event) has completed.  The kernel
+ * (cudaHostAlloc / cudaMallocHost / torch pin_memory, unified addressing).
+ * The bytes are visible to the host once work recorded after it on the
+ * stream (an event) has completed.  The kernel
  * starts programmatically (PDL) and waits for the preceding kernel.  In the
  * bench's step it replaces the D2H copy node of the new boundaries + status
  * (the "result read" of the per-step path, "the new partition is

@@ -769,7 +769,11 @@ __global__ void k_epilogue(EpiArgs a) {
     __syncthreads();
     if (st != DYNMO_OK) atomicMin(&s_st, st);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // one block (a few thousand layers or fewer): it is the last block, and
+    // its status needs no global atomics or fences (k_profile's errors are
+    // read from the status word with a plain load: k_profile has completed)
+    const bool single = gridDim.x == 1;
+    if (threadIdx.x == 0 && !single) {
         if (s_st != DYNMO_OK) atomicMin(a.ws_status, s_st);
         // this block's (remote) slot stores before the counter; the last
         // block's system-scope fence + release below is cumulative over them
@@ -778,8 +782,8 @@ __global__ void k_epilogue(EpiArgs a) {
         s_last = prev == gridDim.x - 1;
     }
     __syncthreads();
-    if (s_last) {
-        __threadfence();
+    if (single || s_last) {
+        if (!single || a.p2p) __threadfence();
         for (int v = threadIdx.x; v < kExitBins; v += blockDim.x) a.exit_hist[v] = 0ull;
         if (threadIdx.x == 0 && a.span) {  // k_profile has completed (pdl_wait)
             const unsigned long long t0 = ~a.span[0], t1 = a.span[1];
@@ -791,8 +795,15 @@ __global__ void k_epilogue(EpiArgs a) {
             a.span[1] = 0ull;
         }
         if (threadIdx.x == 0) {
-            const int fin = atomicExch(a.ws_status, 0);
-            *a.ws_done = 0u;
+            int fin;
+            if (single) {  // k_profile's own errors (bad ids, time pairs) are in ws_status
+                const int w = *a.ws_status;
+                fin = w < s_st ? w : s_st;
+                if (w) *a.ws_status = 0;
+            } else {
+                fin = atomicExch(a.ws_status, 0);
+                *a.ws_done = 0u;
+            }
             if (a.p2p) {
                 const uint64_t epoch = a.win->exch_epoch + 1;
                 const int64_t S = 3 + 2 * (int64_t)a.n_total;
@@ -1036,7 +1047,9 @@ __global__ void k_publish(const uint8_t *__restrict__ src, uint8_t *dst, int64_t
     } else {
         for (int64_t i = t; i < bytes; i += nt) dst[i] = src[i];
     }
-    __threadfence_system();
+    // no __threadfence_system(): the host reads after an event recorded
+    // behind this kernel completes, and completion makes the stores visible
+    // (the fence only held the kernel ~3 us longer for the PCIe acks)
 }
 
 cudaError_t launch_publish(const void *d_src, void *d_dst, int64_t bytes, cudaStream_t s) {
