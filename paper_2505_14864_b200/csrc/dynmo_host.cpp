@@ -1234,9 +1234,9 @@ dynmo_status dynmo_diffuse_balance(dynmo_ctx ctx, int32_t n_inst, int32_t max_la
     a.phi = d_phi;
     a.phi0 = d_phi0;
     a.fluid_x = d_fluid_x;
-    static const int spec = [] {  // DYNMO_FLUID_SPEC=0: the per-round chain (A/B knob)
+    static const int spec = [] {  // DYNMO_FLUID_SPEC: 0 per-round chain, 1 speculative, 2 (default) + overlap for n <= 8
         const char *e = getenv("DYNMO_FLUID_SPEC");
-        return e && e[0] == '0' ? 0 : 1;
+        return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : 2;
     }();
     a.fluid_spec = spec;
     a.fluid_rounds = d_fluid_rounds;
