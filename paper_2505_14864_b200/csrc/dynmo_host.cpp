@@ -1115,6 +1115,21 @@ dynmo_status dynmo_timestamp(dynmo_ctx ctx, int64_t *d_slot, dynmo_stream stream
 
 constexpr int64_t kPublishKernelMax = 4096;  // larger results: the copy engine
 
+// Diagnostic build only (-DDYNMO_STEP_STAMPS; not in dynmo.h): per step
+// kernel [first warp start, last warp end] in %globaltimer ns, 2 x STAMP_N
+// pairs (k_profile.cu's table, then k_solve.cu's); reset re-arms them.
+extern "C" int dynmo_diag_step_stamps(unsigned long long *h_out, int reset) {
+#ifdef DYNMO_STEP_STAMPS
+    diag_stamps_profile(h_out, reset != 0);
+    diag_stamps_solve(h_out + 2 * STAMP_N, reset != 0);
+    return STAMP_N;
+#else
+    (void)h_out;
+    (void)reset;
+    return 0;
+#endif
+}
+
 dynmo_status dynmo_publish(dynmo_ctx ctx, const void *d_src, void *h_dst, int64_t bytes, dynmo_stream stream) {
     if (!ctx || !d_src || !h_dst) return invalid("null ctx/src/dst");
     if (bytes < 0) return invalid("bytes < 0");

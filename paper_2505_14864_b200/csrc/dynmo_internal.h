@@ -85,6 +85,34 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 bool pdl_enabled();
 
+// Diagnostic build only (-DDYNMO_STEP_STAMPS, tools/step_stamps.py): every
+// step kernel records the first warp start (after its griddepcontrol.wait)
+// and the last warp end in %globaltimer ns, per kernel id, in a per-file
+// device table read by dynmo_diag_step_stamps.
+enum { STAMP_PROFILE = 0, STAMP_EPILOGUE, STAMP_PUBLISH, STAMP_PARTITION, STAMP_DIFFUSE_D, STAMP_DIFFUSE_F,
+       STAMP_REPACK, STAMP_N };
+#ifdef DYNMO_STEP_STAMPS
+__device__ __forceinline__ unsigned long long stamp_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct StampScope {
+    unsigned long long *row;
+    __device__ explicit StampScope(unsigned long long *r) : row(r) {
+        if ((threadIdx.x & 31) == 0) atomicMin(&row[0], stamp_now());
+    }
+    __device__ ~StampScope() {
+        if ((threadIdx.x & 31) == 0) atomicMax(&row[1], stamp_now());
+    }
+};
+#define STEP_STAMP(id) StampScope step_stamp_scope_(g_step_stamp[id])
+#else
+#define STEP_STAMP(id)
+#endif
+void diag_stamps_profile(unsigned long long *h, bool reset);  // k_profile.cu's kernels
+void diag_stamps_solve(unsigned long long *h, bool reset);    // k_solve.cu's kernels
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args... args) {

@@ -20,6 +20,27 @@
 #include "dynmo_internal.h"
 
 namespace dynmo {
+
+#ifdef DYNMO_STEP_STAMPS
+__device__ unsigned long long g_step_stamp[STAMP_N][2];
+#endif
+void diag_stamps_profile(unsigned long long *h, bool reset) {
+#ifdef DYNMO_STEP_STAMPS
+    cudaMemcpyFromSymbol(h, g_step_stamp, sizeof(unsigned long long) * STAMP_N * 2);
+    if (reset) {
+        unsigned long long z[STAMP_N][2];
+        for (int i = 0; i < STAMP_N; ++i) {
+            z[i][0] = ~0ull;
+            z[i][1] = 0ull;
+        }
+        cudaMemcpyToSymbol(g_step_stamp, z, sizeof(z));
+    }
+#else
+    (void)h;
+    (void)reset;
+#endif
+}
+
 namespace {
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
@@ -266,6 +287,7 @@ __device__ __forceinline__ void expert_small(const ProfTile &t, bool scalar, int
 template <int OPS>
 __global__ void __launch_bounds__(kProfThreads, (OPS == 1 || OPS == 4) ? 4 : (OPS & 8) ? 2 : 3) k_profile(ProfArgs a) {
     pdl_trigger();  // the epilogue may be scheduled now (it waits for this grid)
+    STEP_STAMP(STAMP_PROFILE);
     if (a.span && threadIdx.x == 0) atomicMax(&a.span[0], ~globaltimer_ns());  // ~start: zero-reset max
     constexpr bool HAS_CNT = OPS & 1, HAS_EXIT = (OPS & 2) != 0, HAS_EXP = (OPS & 4) != 0;
     constexpr bool HAS_BIGE = (OPS & 8) != 0;  // some expert layer has E > 16 (smem histograms)
@@ -746,6 +768,7 @@ __device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p)
 __global__ void k_epilogue(EpiArgs a) {
     pdl_wait();
     pdl_trigger();
+    STEP_STAMP(STAMP_EPILOGUE);
     // grid-stride, kEpiK layers per thread with all their loads issued first
     const int nthr = gridDim.x * blockDim.x;
     int st = DYNMO_OK;
@@ -1038,6 +1061,7 @@ cudaError_t launch_stamp(int64_t *d_slot, cudaStream_t s) {
 // kernel's completion (griddepcontrol.wait) before reading.
 __global__ void k_publish(const uint8_t *__restrict__ src, uint8_t *dst, int64_t bytes) {
     pdl_wait();
+    STEP_STAMP(STAMP_PUBLISH);
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)bytes) & 15) == 0) {

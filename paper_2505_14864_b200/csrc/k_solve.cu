@@ -29,6 +29,27 @@
 #include "dynmo_internal.h"
 
 namespace dynmo {
+
+#ifdef DYNMO_STEP_STAMPS
+__device__ unsigned long long g_step_stamp[STAMP_N][2];
+#endif
+void diag_stamps_solve(unsigned long long *h, bool reset) {
+#ifdef DYNMO_STEP_STAMPS
+    cudaMemcpyFromSymbol(h, g_step_stamp, sizeof(unsigned long long) * STAMP_N * 2);
+    if (reset) {
+        unsigned long long z[STAMP_N][2];
+        for (int i = 0; i < STAMP_N; ++i) {
+            z[i][0] = ~0ull;
+            z[i][1] = 0ull;
+        }
+        cudaMemcpyToSymbol(g_step_stamp, z, sizeof(z));
+    }
+#else
+    (void)h;
+    (void)reset;
+#endif
+}
+
 namespace {
 
 constexpr unsigned FULL = 0xFFFFFFFFu;
@@ -595,6 +616,7 @@ template <bool MEM, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) k_partition(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
+    STEP_STAMP(STAMP_PARTITION);
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st, s_mfit;
     __shared__ int64_t s_maxc;
@@ -652,6 +674,7 @@ template <bool MEM, int NW>
 __global__ void __launch_bounds__(32 * NW, 1) k_repack(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
+    STEP_STAMP(STAMP_REPACK);
     extern __shared__ __align__(16) char smem[];
     __shared__ int s_st, s_k, s_code, s_mfit;
     __shared__ int64_t s_maxc;
@@ -1459,6 +1482,7 @@ template <bool MEM>
 __global__ void __launch_bounds__(32) k_diffuse(SolveArgs a) {
     pdl_wait();
     pdl_trigger();
+    STEP_STAMP(blockIdx.y == 1 ? STAMP_DIFFUSE_F : STAMP_DIFFUSE_D);
     extern __shared__ __align__(16) char smem[];
 #ifdef DYNMO_FLUID_PROF
     if (threadIdx.x == 0) g_fprof_t0 = clock64();
