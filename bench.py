@@ -39,10 +39,10 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# rank 0 prints exactly one JSON line on stdout: keep NCCL's version banner
-# (NCCL_DEBUG=VERSION) off it; an explicit INFO/WARN/TRACE setting is kept
-if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-    os.environ["NCCL_DEBUG"] = "WARN"
+# rank 0 prints exactly one JSON line on stdout: NCCL's log (its version
+# banner included, printed at NCCL_DEBUG >= WARN) goes to stderr unless the
+# caller chose a log file
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import synth  # noqa: E402
 
