@@ -39,9 +39,11 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# rank 0 prints exactly one JSON line on stdout: NCCL's log (its version
-# banner included, printed at NCCL_DEBUG >= WARN) goes to stderr unless the
-# caller chose a log file
+# rank 0 prints exactly one JSON line on stdout: NCCL_DEBUG=VERSION (set in
+# this image) prints NCCL's version banner there with printf, so it is
+# dropped; an explicit INFO/WARN/TRACE level is kept, its log sent to stderr
+if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+    del os.environ["NCCL_DEBUG"]
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import synth  # noqa: E402
