@@ -82,7 +82,7 @@ __host__ __device__ __forceinline__ size_t base_bytes(int Lmax, bool mem) {
 }
 
 __host__ __device__ __forceinline__ size_t solve_smem_bytes(int Lmax, bool mem, bool fluid) {
-    // fluid history: two buffers of kChunk rows (fluid_spec8 verifies one
+    // fluid history: two buffers of kChunk rows (fluid_overlap verifies one
     // while it fills the other)
     return base_bytes(Lmax, mem) + (fluid ? sizeof(double) * (2 * kChunk * kRow + kChunk) : 0);
 }
@@ -1150,6 +1150,110 @@ __device__ __forceinline__ double step_pair(double x, int partner) {
     return fma(y, 0.5, __dmul_rn(x, 0.5));
 }
 
+// n <= 8: fluid_spec's speculative rounds, and once a full 32-row chunk
+// has verified (the matching has settled), the verification of each chunk
+// overlapped with the production of the next: one straight-line block
+// verifies chunk A (lane j: row j's true matching and phi_f, independent of
+// the production chain) while it produces the 32 rows of chunk B (one
+// shuffle + one fma per row on the chain, fully unrolled), so the
+// verification fills the chain's idle issue slots.  B continues A's
+// predictions (32 is even: the period-2 roles of h0 / h1 carry over).  A
+// stop row in A ends the process; a misprediction in A drops B and returns
+// to fluid_spec's small chunks (4 exact rounds, then predictions) at the
+// true successor.  Rows, arithmetic and stop rule are fluid_spec's.
+//
+// verify_row for n <= 8 without branches (every row entry loaded, absent
+// ones replaced by 0; absent phi_f terms add +0.0, which leaves the running
+// sum bit-identical), so it shares a basic block with the production.
+__device__ __forceinline__ void verify_row8(const double *row, int n, unsigned &tm, double &acc) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const double v = row[u];
+        x[u] = u < n ? v : 0.0;
+    }
+    unsigned pr = 0u, pl = 0u;
+    double dprev = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const bool hasR = t + 1 < n, hasL = t > 0 && t < n;
+        const double d = hasR ? __dsub_rn(x[t], x[t < 7 ? t + 1 : t]) : 0.0;
+        const bool cR = hasR && (hasL ? fabs(d) > fabs(dprev) : fabs(d) > 0.0);
+        const bool cL = hasL && !cR && fabs(dprev) > 0.0;
+        pr |= (unsigned)cR << t;
+        pl |= (unsigned)cL << t;
+        dprev = d;
+    }
+    tm = pr & (pl >> 1);
+    double a = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int v = u + 1; v < 8; ++v) a = __dadd_rn(a, v < n ? fabs(__dsub_rn(x[u], x[v])) : 0.0);
+    acc = a;
+}
+
+// The overlapped mode, entered after a verified full chunk with x the next
+// row and h0 / h1 the true matchings of the two rows before it.  Returns
+// true once it has written the stop row; false at a misprediction, with
+// (x, h0, h1, base, fb) describing the restart at the true successor.
+__device__ bool fluid_overlap(int n, double gf, int maxr, double *hist, double *xo, int &rr, double &ph,
+                              int &fst, int lane, double &x, unsigned &h0, unsigned &h1, int &base, int &fb) {
+    int bufA = 0, baseA = base;
+    unsigned usedA = 0u, s1A = h1;
+    {
+        const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            hist[k * kRow + lane] = x;  // lanes >= n store into the row's padding
+            usedA = lane == k ? ((k & 1) ? h1 : h0) : usedA;
+            x = step_pair(x, (k & 1) ? pb : pa);
+        }
+    }
+    for (;;) {
+        double *hA = hist + bufA * kChunk * kRow, *hB = hist + (bufA ^ 1) * kChunk * kRow;
+        __syncwarp();
+        unsigned tm, usedB = 0u;
+        double acc;
+        {
+            const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k) {
+                if (k == 1) verify_row8(hA + lane * kRow, n, tm, acc);  // chunk A, lane = row
+                hB[k * kRow + lane] = x;
+                usedB = lane == k ? ((k & 1) ? h1 : h0) : usedB;
+                x = step_pair(x, (k & 1) ? pb : pa);
+            }
+        }
+        const unsigned mbad = __ballot_sync(FULL, tm != usedA);
+        fb = mbad ? __ffs(mbad) - 1 : kChunk;
+        const unsigned mstop = __ballot_sync(FULL, lane <= fb && (acc <= gf || baseA + lane == maxr));
+        if (mstop) {
+            const int k = __ffs(mstop) - 1;
+            rr = baseA + k;
+            ph = __shfl_sync(FULL, acc, k);
+            if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
+            if (lane < n) xo[lane] = hA[k * kRow + lane];
+            return true;
+        }
+        if (fb < kChunk) {  // drop B; restart at the true successor of row fb
+            const unsigned tb = __shfl_sync(FULL, tm, fb);
+            const unsigned tp = __shfl_sync(FULL, tm, fb > 0 ? fb - 1 : 0);
+            const double xv = lane < n ? hA[fb * kRow + lane] : 0.0;
+            h0 = fb > 0 ? tp : s1A;
+            h1 = tb;
+            x = step_pair(xv, partner_of(tb, lane));
+            base = baseA + fb + 1;
+            __syncwarp();
+            return false;
+        }
+        s1A = __shfl_sync(FULL, usedA, kChunk - 1);
+        baseA += kChunk;
+        usedA = usedB;
+        bufA ^= 1;
+    }
+}
+
 #ifdef DYNMO_FLUID_PROF  // diagnostic build only: phase cycles into fluid_x (tools/fluid_prof.py)
 __shared__ long long g_fprof_t0;
 #define FPROF(v) const long long v = clock64()
@@ -1157,6 +1261,7 @@ __shared__ long long g_fprof_t0;
 #define FPROF(v)
 #endif
 
+template <bool OVL>  // OVL (n <= 8): the overlapped mode once a full chunk has verified
 __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, int maxr, double *hist,
                            double *xo, int &rr, double &ph, int &fst, int lane) {
 #ifdef DYNMO_FLUID_PROF
@@ -1241,176 +1346,18 @@ __device__ void fluid_spec(const Inst &s, int n, const int32_t *bi, double gf, i
             h0 = __shfl_sync(FULL, used, size - 2);
             h1 = __shfl_sync(FULL, used, size - 1);
             base += size;
-            e = 0;
-            size = min(kChunk, size * 4);
-        }
-        __syncwarp();
-    }
-}
-
-// n <= 8: fluid_spec's speculative rounds, and once a full 32-row chunk
-// has verified (the matching has settled), the verification of each chunk
-// overlapped with the production of the next: one straight-line block
-// verifies chunk A (lane j: row j's true matching and phi_f, independent of
-// the production chain) while it produces the 32 rows of chunk B (one
-// shuffle + one fma per row on the chain, fully unrolled), so the
-// verification fills the chain's idle issue slots.  B continues A's
-// predictions (32 is even: the period-2 roles of h0 / h1 carry over).  A
-// stop row in A ends the process; a misprediction in A drops B and returns
-// to fluid_spec's small chunks (4 exact rounds, then predictions) at the
-// true successor.  Rows, arithmetic and stop rule are fluid_spec's.
-//
-// verify_row for n <= 8 without branches (every row entry loaded, absent
-// ones replaced by 0; absent phi_f terms add +0.0, which leaves the running
-// sum bit-identical), so it shares a basic block with the production.
-__device__ __forceinline__ void verify_row8(const double *row, int n, unsigned &tm, double &acc) {
-    double x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-        const double v = row[u];
-        x[u] = u < n ? v : 0.0;
-    }
-    unsigned pr = 0u, pl = 0u;
-    double dprev = 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-        const bool hasR = t + 1 < n, hasL = t > 0 && t < n;
-        const double d = hasR ? __dsub_rn(x[t], x[t < 7 ? t + 1 : t]) : 0.0;
-        const bool cR = hasR && (hasL ? fabs(d) > fabs(dprev) : fabs(d) > 0.0);
-        const bool cL = hasL && !cR && fabs(dprev) > 0.0;
-        pr |= (unsigned)cR << t;
-        pl |= (unsigned)cL << t;
-        dprev = d;
-    }
-    tm = pr & (pl >> 1);
-    double a = 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-#pragma unroll
-        for (int v = u + 1; v < 8; ++v) a = __dadd_rn(a, v < n ? fabs(__dsub_rn(x[u], x[v])) : 0.0);
-    acc = a;
-}
-
-__device__ void fluid_spec8(const Inst &s, int n, const int32_t *bi, double gf, int maxr, double *hist,
-                            double *xo, int &rr, double &ph, int &fst, int lane) {
-    double x = lane < n ? (double)(s.P[bi[lane + 1]] - s.P[bi[lane]]) : 0.0;
-    const bool hasL = lane >= 1 && lane < n, hasR = lane + 1 < n;
-    unsigned h0 = 0u, h1 = 0u;  // true matchings of the two rounds before the next row
-    int e = 4, size = 8;        // small chunks: exact rows, rows of the chunk
-    for (int base = 0;;) {
-        // ---- a small chunk (fluid_spec) in buffer 0
-        const unsigned s1 = h1;
-        unsigned used = 0u;
-        for (int k = 0; k < e; ++k) {
-            if (lane < n) hist[k * kRow + lane] = x;
-            unsigned m;
-            x = exact_round(x, hasL, hasR, lane, m);
-            used = lane == k ? m : used;
-            h0 = h1;
-            h1 = m;
-        }
-        {
-            const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
-            for (int k = e; k < size; ++k) {
-                if (lane < n) hist[k * kRow + lane] = x;
-                const bool odd = (k - e) & 1;
-                used = lane == k ? (odd ? h1 : h0) : used;
-                x = step_pair(x, odd ? pb : pa);
-            }
-        }
-        __syncwarp();
-        unsigned tm = 0u;
-        double acc = 0.0;
-        if (lane < size) verify_row(hist + lane * kRow, n, tm, acc);
-        unsigned mbad = __ballot_sync(FULL, lane < size && tm != used);
-        int fb = mbad ? __ffs(mbad) - 1 : size;
-        unsigned mstop = __ballot_sync(FULL, lane < size && lane <= fb && (acc <= gf || base + lane == maxr));
-        if (mstop) {
-            const int k = __ffs(mstop) - 1;
-            rr = base + k;
-            ph = __shfl_sync(FULL, acc, k);
-            if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
-            if (lane < n) xo[lane] = hist[k * kRow + lane];
-            return;
-        }
-        if (fb < size) {
-            const unsigned tb = __shfl_sync(FULL, tm, fb);
-            const unsigned tp = __shfl_sync(FULL, tm, fb > 0 ? fb - 1 : 0);
-            const double xv = lane < n ? hist[fb * kRow + lane] : 0.0;
-            h0 = fb > 0 ? tp : s1;
-            h1 = tb;
-            x = step_pair(xv, partner_of(tb, lane));
-            base += fb + 1;
-            e = 4;
-            size = min(kChunk, max(8, 2 * (fb + 1)));
-            __syncwarp();
-            continue;
-        }
-        h0 = __shfl_sync(FULL, used, size - 2);
-        h1 = __shfl_sync(FULL, used, size - 1);
-        base += size;
-        if (size < kChunk) {
-            e = 0;
-            size = min(kChunk, size * 4);
-            __syncwarp();
-            continue;
-        }
-        // ---- overlapped mode: chunk A (buffer bufA) verified while B is produced
-        __syncwarp();
-        int bufA = 0, baseA = base;
-        unsigned usedA = 0u, s1A = h1;
-        {
-            const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k) {
-                hist[k * kRow + lane] = x;  // lanes >= n store into the row's padding
-                usedA = lane == k ? ((k & 1) ? h1 : h0) : usedA;
-                x = step_pair(x, (k & 1) ? pb : pa);
-            }
-        }
-        for (;;) {
-            double *hA = hist + bufA * kChunk * kRow, *hB = hist + (bufA ^ 1) * kChunk * kRow;
-            __syncwarp();
-            unsigned usedB = 0u;
-            {
-                const int pa = partner_of(h0, lane), pb = partner_of(h1, lane);
-#pragma unroll
-                for (int k = 0; k < kChunk; ++k) {
-                    if (k == 1) verify_row8(hA + lane * kRow, n, tm, acc);  // chunk A, lane = row
-                    hB[k * kRow + lane] = x;
-                    usedB = lane == k ? ((k & 1) ? h1 : h0) : usedB;
-                    x = step_pair(x, (k & 1) ? pb : pa);
-                }
-            }
-            mbad = __ballot_sync(FULL, tm != usedA);
-            fb = mbad ? __ffs(mbad) - 1 : kChunk;
-            mstop = __ballot_sync(FULL, lane <= fb && (acc <= gf || baseA + lane == maxr));
-            if (mstop) {
-                const int k = __ffs(mstop) - 1;
-                rr = baseA + k;
-                ph = __shfl_sync(FULL, acc, k);
-                if (!(ph <= gf)) fst = DYNMO_W_NOT_CONVERGED;
-                if (lane < n) xo[lane] = hA[k * kRow + lane];
-                return;
-            }
-            if (fb < kChunk) {  // drop B; back to small chunks at the true successor of row fb
-                const unsigned tb = __shfl_sync(FULL, tm, fb);
-                const unsigned tp = __shfl_sync(FULL, tm, fb > 0 ? fb - 1 : 0);
-                const double xv = lane < n ? hA[fb * kRow + lane] : 0.0;
-                h0 = fb > 0 ? tp : s1A;
-                h1 = tb;
-                x = step_pair(xv, partner_of(tb, lane));
-                base = baseA + fb + 1;
-                e = 4;
-                size = min(kChunk, max(8, 2 * (fb + 1)));
+            if (OVL && size == kChunk) {
                 __syncwarp();
-                break;
+                int fbo;
+                if (fluid_overlap(n, gf, maxr, hist, xo, rr, ph, fst, lane, x, h0, h1, base, fbo)) return;
+                e = 4;
+                size = min(kChunk, max(8, 2 * (fbo + 1)));
+                continue;
             }
-            s1A = __shfl_sync(FULL, usedA, kChunk - 1);
-            baseA += kChunk;
-            usedA = usedB;
-            bufA ^= 1;
+            e = 0;
+            size = min(kChunk, size * 4);
         }
+        __syncwarp();
     }
 }
 
@@ -1431,8 +1378,8 @@ __device__ void diffuse_fluid(const SolveArgs &a, const Inst &s, int q, int n, c
     int rr = 0;
     double ph = 0.0;
     if (n <= 32) {
-        if (a.fluid_spec == 2 && n <= 8) fluid_spec8(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
-        else if (a.fluid_spec) fluid_spec(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+        if (a.fluid_spec == 2 && n <= 8) fluid_spec<true>(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
+        else if (a.fluid_spec) fluid_spec<false>(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
         else fluid_chunks(s, n, bi, gf, maxr, hist, xo, rr, ph, fst, lane);
     } else if (lane == 0) {
         // n > 32: serial on lane 0 over shared memory (s.x reused as fp64)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# 1 GPU: fluid_spec8 (n <= 8: chunk verification overlapped with the next
+# 1 GPU: fluid_spec<true> (n <= 8: chunk verification overlapped with the next
 # chunk's production) -- diffusion parity, fluid slope, microbench, steps.
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "diffuse" > gpurun_out/s51_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/s51_pytest.log
