@@ -132,6 +132,16 @@ dynmo_status dynmo_ctx_timing_read(dynmo_ctx ctx, int32_t phase, double *h_total
  * accumulator.  Returns (and resets) the accumulated milliseconds and
  * launch count; synchronous. */
 dynmo_status dynmo_ctx_profile_span(dynmo_ctx ctx, double *h_total_ms, int64_t *h_count);
+
+/* Device step timeline, diagnostic builds only (compiled with
+ * -DDYNMO_STEP_STAMPS, tools/build_stamps.sh): copies to h_out (host,
+ * 4 * 7 uint64) each step kernel's {first-warp start, last-warp end} in
+ * %globaltimer ns -- k_profile, k_epilogue, k_publish, then k_partition,
+ * k_diffuse (discrete block), k_diffuse (fluid block), k_repack, in two
+ * tables of 7 pairs (unused rows {~0, 0}) -- and, if reset != 0, re-arms
+ * them.  Synchronous (device-wide copies); not for use inside a capture.
+ * Returns 7, or 0 in a normal build (no stamps recorded, h_out untouched). */
+int dynmo_diag_step_stamps(unsigned long long *h_out, int reset);
 /* Hang analysis: a snapshot of this rank's peer window, copied on a private
  * non-blocking stream (so it completes while the ctx's other streams wait):
  * h_out[0] sticky error, [1] device-migration epoch, [2] exchange epoch,

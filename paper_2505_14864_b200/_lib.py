@@ -73,6 +73,7 @@ def lib():
         "dynmo_profile_layers": (i32, [p, p, p, p, p, p, p, p, p, p, p]),
         "dynmo_timestamp": (i32, [p, p, p]),
         "dynmo_publish": (i32, [p, p, p, i64, p]),
+        "dynmo_diag_step_stamps": (i32, [p, i32]),
         "dynmo_ctx_split": (i32, [p, i32, i32, p]),
         "dynmo_ctx_timing_detach": (i32, [p]),
         "dynmo_ctx_barrier": (i32, [p, p]),
@@ -114,7 +115,7 @@ EXPORTED = ["dynmo_strerror", "dynmo_last_error", "dynmo_version", "dynmo_get_un
             "dynmo_ctx_create", "dynmo_ctx_destroy", "dynmo_ctx_nranks", "dynmo_ctx_rank",
             "dynmo_ctx_set_timing", "dynmo_ctx_timing_read", "dynmo_ctx_timing_poll",
             "dynmo_profile_plan_create", "dynmo_profile_plan_destroy", "dynmo_plan_num_tiles",
-            "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers", "dynmo_timestamp", "dynmo_publish", "dynmo_ctx_split", "dynmo_map_stages", "dynmo_ctx_timing_detach",
+            "dynmo_plan_bytes", "dynmo_plan_max_experts", "dynmo_profile_layers", "dynmo_timestamp", "dynmo_publish", "dynmo_diag_step_stamps", "dynmo_ctx_split", "dynmo_map_stages", "dynmo_ctx_timing_detach",
             "dynmo_ctx_barrier",
             "dynmo_partition_stages", "dynmo_diffuse_balance", "dynmo_repack_workers",
             "dynmo_migrate_layers", "dynmo_migration_plan", "dynmo_migrate_plan_create",

@@ -1118,7 +1118,7 @@ constexpr int64_t kPublishKernelMax = 4096;  // larger results: the copy engine
 // Diagnostic build only (-DDYNMO_STEP_STAMPS; not in dynmo.h): per step
 // kernel [first warp start, last warp end] in %globaltimer ns, 2 x STAMP_N
 // pairs (k_profile.cu's table, then k_solve.cu's); reset re-arms them.
-extern "C" int dynmo_diag_step_stamps(unsigned long long *h_out, int reset) {
+int dynmo_diag_step_stamps(unsigned long long *h_out, int reset) {
 #ifdef DYNMO_STEP_STAMPS
     diag_stamps_profile(h_out, reset != 0);
     diag_stamps_solve(h_out + 2 * STAMP_N, reset != 0);

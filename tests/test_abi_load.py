@@ -55,6 +55,7 @@ def test_host_argument_validation_without_gpu():
     ms, n = ctypes.c_double(), ctypes.c_int64()
     assert L.dynmo_ctx_profile_span(None, ctypes.byref(ms), ctypes.byref(n)) == _lib.E_INVALID
     assert L.dynmo_publish(None, None, None, 4, None) == _lib.E_INVALID
+    assert L.dynmo_diag_step_stamps(None, 0) == 0  # a normal build records no stamps
 
 
 def test_migration_plan_vs_oracle():

@@ -25,9 +25,7 @@ NAMES = ["profile", "epilogue", "publish", "partition", "diffuse_discrete", "dif
 torch.cuda.set_device(0)
 ctx = D.Context(0)
 L_ = LB.lib()
-fn = L_.dynmo_diag_step_stamps
-fn.restype = ctypes.c_int
-fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+fn = L_.dynmo_diag_step_stamps  # signature bound in _lib
 buf = (ctypes.c_ulonglong * (4 * len(NAMES)))()
 if fn(buf, 1) == 0:
     raise SystemExit("not a -DDYNMO_STEP_STAMPS build (set DYNMO_LIB)")
