@@ -167,6 +167,7 @@ struct dynmo_plan_s {
     unsigned long long *d_acc = nullptr, *d_hist = nullptr, *d_exit = nullptr;
     int32_t *d_ws_status = nullptr;
     unsigned int *d_ws_done = nullptr;
+    unsigned long long *d_warm = nullptr;  // epilogue code warm-up scratch (EpiArgs::warm)
     int64_t *d_slot_send = nullptr, *d_slot_recv = nullptr;
     int64_t slot_elems = 0;
     // exchange over peer memory (exchange == 1): [2][nranks][slot_elems] here,
@@ -692,10 +693,11 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
     const size_t sz_hist = up(sizeof(unsigned long long) * (size_t)std::max(1, n_local) * std::max(1, max_E));
     const size_t sz_exit = up(sizeof(unsigned long long) * kExitBins);
     const size_t sz_ws = up(16);
+    const size_t sz_warm = up(sizeof(unsigned long long) * (3 + 3 * (size_t)std::max(1, max_E) + kExitBins + 8));
     pl->slot_elems = 3 + 2 * (int64_t)n_total;
     const size_t sz_send = exchange ? up(sizeof(int64_t) * pl->slot_elems) : 0;
     const size_t sz_recv = exchange ? up(sizeof(int64_t) * pl->slot_elems * ctx->nranks) : 0;
-    const size_t total = sz_tiles + sz_info + sz_acc + sz_hist + sz_exit + sz_ws + sz_send + sz_recv;
+    const size_t total = sz_tiles + sz_info + sz_acc + sz_hist + sz_exit + sz_ws + sz_warm + sz_send + sz_recv;
     DeviceGuard g(ctx->device);
     cudaError_t e = cudaMalloc(&pl->dmem, total);
     if (e != cudaSuccess) {
@@ -711,6 +713,7 @@ static dynmo_status profile_plan_local(dynmo_ctx ctx, const dynmo_segment *h_seg
     pl->d_exit = (unsigned long long *)b; b += sz_exit;
     pl->d_ws_status = (int32_t *)b;
     pl->d_ws_done = (unsigned int *)(b + 4); b += sz_ws;
+    pl->d_warm = (unsigned long long *)b; b += sz_warm;
     if (exchange) {
         pl->d_slot_send = (int64_t *)b; b += sz_send;
         pl->d_slot_recv = (int64_t *)b;
@@ -1050,6 +1053,11 @@ dynmo_status dynmo_profile_layers(dynmo_ctx ctx, dynmo_plan plan, const uint8_t 
     ea.ws_status = plan->d_ws_status;
     ea.ws_done = plan->d_ws_done;
     ea.status_out = d_status;
+    static const bool epi_warm = [] {  // DYNMO_EPI_WARM=0: no code warm-up pass (A/B knob)
+        const char *e = getenv("DYNMO_EPI_WARM");
+        return !(e && e[0] == '0');
+    }();
+    ea.warm = epi_warm ? plan->d_warm : nullptr;
     static const bool fuse_exch = [] {  // DYNMO_EXCH_FUSED=0: separate k_unpack_p2p (A/B knob)
         const char *e = getenv("DYNMO_EXCH_FUSED");
         return !(e && e[0] == '0');

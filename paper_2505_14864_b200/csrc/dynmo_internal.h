@@ -191,6 +191,9 @@ struct EpiArgs {
     unsigned int *ws_done;
     int32_t *status_out;     // local mode final status
     unsigned long long *span;  // nullable: [0] ~start, [1] end of k_profile, [2] sum of spans (ns), [3] launches
+    // nullable: plan scratch (3 + 2 max_E + 256 + 8 + max_E u64, zero) for the
+    // epilogue's code warm-up pass before griddepcontrol.wait
+    unsigned long long *warm;
     // peer-memory exchange fused into the last block (p2p && fuse_unpack):
     // this rank's receive area, the decode buffer, the global outputs
     int32_t fuse_unpack;

@@ -655,16 +655,24 @@ struct EpiPre {
     bool frozen;
 };
 
-__device__ __forceinline__ void epi_load(const EpiArgs &a, int q, EpiPre &p) {
+// The per-layer data the epilogue consumes and produces: the real buffers,
+// or (code warm-up before griddepcontrol.wait) scratch of the plan.
+struct EpiIO {
+    unsigned long long *acc, *hist, *exit_hist;
+    int64_t *counters_out, *hist_out, *cost_out, *mem_out;
+    int32_t p2p, exchange;
+};
+
+__device__ __forceinline__ void epi_load(const EpiArgs &a, const EpiIO &io, int q, EpiPre &p) {
     p.li = a.info[q];
     const uint4 *c4 = reinterpret_cast<const uint4 *>(a.coef + q);  // 48 B, 16-B aligned
     uint4 *d4 = reinterpret_cast<uint4 *>(&p.cf);
     d4[0] = c4[0];
     d4[1] = c4[1];
     d4[2] = c4[2];
-    p.nnz_u = a.acc[(int64_t)q * ACC_N + ACC_NNZ];
-    p.tok_u = a.acc[(int64_t)q * ACC_N + ACC_TOK];
-    p.time_u = a.acc[(int64_t)q * ACC_N + ACC_TIME];
+    p.nnz_u = io.acc[(int64_t)q * ACC_N + ACC_NNZ];
+    p.tok_u = io.acc[(int64_t)q * ACC_N + ACC_TOK];
+    p.time_u = io.acc[(int64_t)q * ACC_N + ACC_TIME];
     p.frozen = a.frozen && a.frozen[q];
     p.m = a.mem_local ? a.mem_local[q] : 0;
 }
@@ -672,18 +680,18 @@ __device__ __forceinline__ void epi_load(const EpiArgs &a, int q, EpiPre &p) {
 // Cost of local layer q from its prefetched inputs (a5, readings Q1-Q6);
 // consumes its counters; writes the outputs of the selected exchange mode.
 // Returns the layer's status.
-__device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p) {
+__device__ __forceinline__ int epi_one(const EpiArgs &a, const EpiIO &io, int q, const EpiPre &p) {
     int st = DYNMO_OK;
     const LayerInfo li = p.li;
     const int gi = a.layer_begin + q;
     unsigned long long nnz_u = p.nnz_u;
     unsigned long long tok_u = p.tok_u;
     const unsigned long long time_u = p.time_u;
-    a.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
-    a.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
-    a.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
+    io.acc[(int64_t)q * ACC_N + ACC_NNZ] = 0ull;
+    io.acc[(int64_t)q * ACC_N + ACC_TOK] = 0ull;
+    io.acc[(int64_t)q * ACC_N + ACC_TIME] = 0ull;
     if (li.flags & SRC_HAS_EXIT)
-        for (int v = gi + 1; v < kExitBins; ++v) tok_u += a.exit_hist[v];
+        for (int v = gi + 1; v < kExitBins; ++v) tok_u += io.exit_hist[v];
     const bool has_tok = (li.flags & SRC_HAS_TOK) != 0;
     const dynmo_cost_coef cf = p.cf;
     const bool frozen = p.frozen;
@@ -694,7 +702,7 @@ __device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p)
     if (li.flags & SRC_HAS_MOE) {
         const int E = li.E;
         const int EP = cf.ep_ranks <= 0 ? E : cf.ep_ranks;
-        unsigned long long *h = a.hist + (int64_t)q * a.max_E;
+        unsigned long long *h = io.hist + (int64_t)q * a.max_E;
         bad_ep = E < 1 || EP < 1 || E % EP != 0;
         if (!bad_ep) {
             const int g = E / EP;
@@ -707,7 +715,7 @@ __device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p)
             moe = (__int128)EP * best;
         }
         for (int e = 0; e < E; ++e) {
-            if (a.hist_out) a.hist_out[(int64_t)q * a.max_E + e] = (int64_t)h[e];
+            if (io.hist_out) io.hist_out[(int64_t)q * a.max_E + e] = (int64_t)h[e];
             h[e] = 0ull;
         }
     }
@@ -737,15 +745,15 @@ __device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p)
         }
     }
     const int64_t m = p.m;
-    if (a.counters_out) {
-        int64_t *o = a.counters_out + (int64_t)q * 5;
+    if (io.counters_out) {
+        int64_t *o = io.counters_out + (int64_t)q * 5;
         o[0] = (int64_t)nnz_u;
         o[1] = has_tok ? (int64_t)tok_u : 1;
         o[2] = moe > LIM ? -1 : (int64_t)moe;
         o[3] = c;
         o[4] = time_u > (unsigned long long)INT64_MAX ? -1 : (int64_t)time_u;
     }
-    if (a.p2p) {
+    if (io.p2p) {
         // straight into every rank's receive slot as LL words (NVLink
         // stores; each word carries the epoch, no fence or flag needed)
         const uint64_t epoch = a.win->exch_epoch + 1;  // advanced by the last block
@@ -755,35 +763,57 @@ __device__ __forceinline__ int epi_one(const EpiArgs &a, int q, const EpiPre &p)
             ll_store(a.peer_slots[r] + off + 2 * (3 + q), c, epoch);
             ll_store(a.peer_slots[r] + off + 2 * (3 + a.n_total + q), m, epoch);
         }
-    } else if (a.exchange) {
+    } else if (io.exchange) {
         a.slot_send[3 + q] = c;
         a.slot_send[3 + a.n_total + q] = m;
     } else {
-        a.cost_out[q] = c;
-        if (a.mem_out) a.mem_out[q] = m;
+        io.cost_out[q] = c;
+        if (io.mem_out) io.mem_out[q] = m;
     }
     return st;
 }
 
-__global__ void k_epilogue(EpiArgs a) {
-    pdl_wait();
-    pdl_trigger();
-    STEP_STAMP(STAMP_EPILOGUE);
-    // grid-stride, kEpiK layers per thread with all their loads issued first
+__global__ void __launch_bounds__(256, 2) k_epilogue(EpiArgs a) {
+    // grid-stride, kEpiK layers per thread with all their loads issued first.
+    // Pass 0 (a.warm: plan scratch), before griddepcontrol.wait: thread 0 of
+    // block 0 runs the same loop code on layer 0's step-invariant inputs
+    // and scratch counters / outputs, so the instructions are fetched while
+    // k_profile still runs (after an L2 flush the epilogue's cold start is
+    // its code, `profiles/r02_ab_epi_prefetch/`).  Pass 1 is the real one.
+    STEP_STAMP(STAMP_EPILOGUE);  // (diagnostic build: the start is the CTA's, before the wait)
     const int nthr = gridDim.x * blockDim.x;
     int st = DYNMO_OK;
-    for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < a.n_local; base += nthr * kEpiK) {
-        EpiPre p[kEpiK];
-#pragma unroll
-        for (int k = 0; k < kEpiK; ++k) {
-            const int q = base + k * nthr;
-            if (q < a.n_local) epi_load(a, q, p[k]);
+#pragma unroll 1
+    for (int pass = a.warm ? 0 : 1; pass < 2; ++pass) {
+        EpiIO io;
+        int nl;
+        if (pass == 0) {
+            unsigned long long *w = a.warm;
+            int64_t *o = reinterpret_cast<int64_t *>(w + ACC_N + 2 * a.max_E + kExitBins);
+            io = EpiIO{w, w + ACC_N, w + ACC_N + a.max_E, o, a.hist_out ? o + 8 : nullptr, o + 5, a.mem_out ? o + 6 : nullptr,
+                       0, 0};
+            nl = a.n_local > 0 && blockIdx.x == 0 ? 1 : 0;
+        } else {
+            pdl_wait();
+            pdl_trigger();
+            io = EpiIO{a.acc, a.hist, a.exit_hist, a.counters_out, a.hist_out, a.cost_out, a.mem_out, a.p2p,
+                       a.exchange};
+            nl = a.n_local;
         }
+        for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < nl; base += nthr * kEpiK) {
+            EpiPre p[kEpiK];
 #pragma unroll
-        for (int k = 0; k < kEpiK; ++k) {
-            const int q = base + k * nthr;
-            if (q < a.n_local) st = worse(st, epi_one(a, q, p[k]));
+            for (int k = 0; k < kEpiK; ++k) {
+                const int q = base + k * nthr;
+                if (q < nl) epi_load(a, io, q, p[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < kEpiK; ++k) {
+                const int q = base + k * nthr;
+                if (q < nl) st = worse(st, epi_one(a, io, q, p[k]));
+            }
         }
+        if (pass == 0) st = DYNMO_OK;
     }
     // block-reduce the status, then last-block finalisation
     __shared__ int s_st;
